@@ -1,0 +1,365 @@
+/*
+ * pstf_keys.cuh — spatio-directional key quantisation for the B200 field cache.
+ *
+ * Bit-exact restatement (host+device) of the reference key math:
+ *   selectLevel    proj/core/src/field.cpp:68-76
+ *   cellSize       field.cpp:78-80,  dirResolution field.cpp:82-84
+ *   keyFor         field.cpp:86-101, packKeyFields field.cpp:38-44, mixBits rng.h:61-68
+ *   sphereToSquare proj/core/include/pstf/mappings.h:33-51
+ * Exactness strategy:
+ *   - compiled with -fmad=false (device) / -ffp-contract=off (host): no FMA contraction;
+ *     explicit fma() appears only inside error-free transformations (two_prod).
+ *   - floor(log2(s)) comes from the exponent bits plus an exact test of whether the correctly
+ *     rounded log2(s) rounds up to the next integer (s a few ulps below a power of two).
+ *   - atan2 is evaluated with the fast libm/libdevice routine; only when the resulting
+ *     octahedral coordinate lies within 1e-11 of a directional-cell boundary is it recomputed
+ *     with a double-double atan2 that returns the correctly rounded result (what glibc returns
+ *     on >99.8% of inputs, SURVEY.md Appendix B libm probe).
+ *   - int32 conversions reproduce x86-64 cvttsd2si: NaN / out of range -> INT32_MIN.
+ */
+#pragma once
+#include <stdint.h>
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define PSTF_HD __host__ __device__ __forceinline__
+#define PSTF_HD_NOINLINE __host__ __device__ __noinline__
+#else
+#define PSTF_HD static inline
+#define PSTF_HD_NOINLINE static
+#endif
+
+namespace pstf_b200 {
+
+struct Key {
+    int32_t level;
+    int32_t cell[3];
+    int32_t dir[2];
+    uint32_t checksum;
+};
+
+struct KeyParams {
+    double base_cell_size;
+    double level_select_k;
+    int32_t max_level;
+};
+
+PSTF_HD uint64_t mix_bits(uint64_t v) {
+    v ^= v >> 30;
+    v *= 0xbf58476d1ce4e5b9ULL;
+    v ^= v >> 27;
+    v *= 0x94d049bb133111ebULL;
+    v ^= v >> 31;
+    return v;
+}
+
+PSTF_HD uint64_t pack_key_fields(int32_t level, int32_t c0, int32_t c1, int32_t c2, int32_t d0,
+                                 int32_t d1) {
+    uint64_t h = (uint64_t)(uint32_t)level;
+    h = mix_bits(h ^ (((uint64_t)(uint32_t)c0 << 32) | (uint32_t)c1));
+    h = mix_bits(h ^ (((uint64_t)(uint32_t)c2 << 32) | (uint32_t)d0));
+    h = mix_bits(h ^ (uint64_t)(uint32_t)d1);
+    return h;
+}
+
+PSTF_HD uint32_t checksum_of(uint64_t packed) {
+    uint32_t s = (uint32_t)mix_bits(packed ^ 0x5bf03635ULL);
+    return s == 0 ? 1u : s;
+}
+
+/* x86-64 cvttsd2si: the reference's int32_t(double) on the reference platform */
+PSTF_HD int32_t i32_x86(double x) {
+    if (!(x >= -2147483648.0 && x < 2147483648.0)) return INT32_MIN;
+    return (int32_t)x;
+}
+
+PSTF_HD uint64_t dbits(double x) {
+#if defined(__CUDA_ARCH__)
+    return (uint64_t)__double_as_longlong(x);
+#else
+    union { double d; uint64_t u; } c;
+    c.d = x;
+    return c.u;
+#endif
+}
+
+PSTF_HD double bitsd(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)u);
+#else
+    union { double d; uint64_t u; } c;
+    c.u = u;
+    return c.d;
+#endif
+}
+
+PSTF_HD double pow2d(int k) { /* 2^k, k in [-1022, 1023] */
+    return bitsd((uint64_t)(k + 1023) << 52);
+}
+
+#define PSTF_INV_LN2 1.4426950408889634
+
+/* field.cpp:68-76: clamp(floor(log2(footprint*K/base)), 0, maxLevel), with the rounding of a
+ * correctly rounded log2 reproduced exactly. */
+PSTF_HD int select_level(const KeyParams &p, double footprint) {
+    if (!(footprint > 0.0)) return 0;
+    double s = footprint * p.level_select_k / p.base_cell_size;
+    if (s <= 1.0) return 0;
+    int level;
+    if (!(s <= 1.7976931348623157e308)) {
+        level = INT32_MIN; /* log2(inf)=inf / log2(NaN)=NaN -> int32 on x86 -> INT32_MIN */
+    } else {
+        uint64_t b = dbits(s);
+        int e = (int)((b >> 52) & 0x7ff) - 1023; /* s > 1 is a normal number */
+        /* m = s / 2^(e+1) in [0.5, 1) exactly; delta = 1 - m exact (Sterbenz) */
+        double m = bitsd((b & 0x000fffffffffffffULL) | (0x3feULL << 52));
+        double delta = 1.0 - m;
+        /* log2(s) = L + log2(1 - delta), L = e + 1; rounds to L iff the deficit
+         * -log2(1-delta) ~= delta/ln2 (1 + delta/2) is <= half the gap below L */
+        int L = e + 1;
+        uint64_t lb = dbits((double)L);
+        int pexp = (int)((lb >> 52) & 0x7ff) - 1023;
+        int pow2 = (lb & 0x000fffffffffffffULL) == 0;
+        double half_gap = pow2d(pexp - (pow2 ? 54 : 53));
+        double deficit = delta * PSTF_INV_LN2 * (1.0 + 0.5 * delta);
+        level = (deficit <= half_gap) ? L : e;
+    }
+    if (level < 0) level = 0;
+    return level < p.max_level ? level : p.max_level;
+}
+
+PSTF_HD double cell_size(const KeyParams &p, int level) {
+    return p.base_cell_size * (double)((uint64_t)1 << level); /* field.cpp:78-80 */
+}
+
+PSTF_HD int dir_resolution(int level) { return 8 >> (level < 2 ? level : 2); } /* field.cpp:82-84 */
+
+/* ---------------- double-double atan2 (slow path, correctly rounded) ---------------- */
+struct DD { double hi, lo; };
+
+PSTF_HD DD dd_two_sum(double a, double b) {
+    double s = a + b;
+    double bb = s - a;
+    double e = (a - (s - bb)) + (b - bb);
+    DD r; r.hi = s; r.lo = e; return r;
+}
+PSTF_HD DD dd_quick(double a, double b) {
+    double s = a + b;
+    DD r; r.hi = s; r.lo = b - (s - a); return r;
+}
+PSTF_HD DD dd_two_prod(double a, double b) {
+    double p = a * b;
+    DD r; r.hi = p; r.lo = fma(a, b, -p); return r;
+}
+PSTF_HD DD dd_add(DD x, DD y) {
+    DD s = dd_two_sum(x.hi, y.hi);
+    DD t = dd_two_sum(x.lo, y.lo);
+    s.lo += t.hi;
+    s = dd_quick(s.hi, s.lo);
+    s.lo += t.lo;
+    return dd_quick(s.hi, s.lo);
+}
+PSTF_HD DD dd_neg(DD x) { x.hi = -x.hi; x.lo = -x.lo; return x; }
+PSTF_HD DD dd_mul(DD x, DD y) {
+    DD p = dd_two_prod(x.hi, y.hi);
+    p.lo += x.hi * y.lo + x.lo * y.hi;
+    return dd_quick(p.hi, p.lo);
+}
+PSTF_HD DD dd_div(DD x, DD y) {
+    double q1 = x.hi / y.hi;
+    DD r = dd_add(x, dd_neg(dd_mul(y, DD{q1, 0.0})));
+    double q2 = r.hi / y.hi;
+    r = dd_add(r, dd_neg(dd_mul(y, DD{q2, 0.0})));
+    double q3 = r.hi / y.hi;
+    DD q = dd_quick(q1, q2);
+    return dd_add(q, DD{q3, 0.0});
+}
+
+#define PSTF_ATAN_TABLE \
+    {0.0, 0.0}, \
+    {0.015623728620476831, -4.913600136566304e-19}, \
+    {0.031239833430268277, -1.188442711587748e-18}, \
+    {0.046840712915969654, -1.655677442254952e-19}, \
+    {0.06241880999595735, -1.5490756308295046e-18}, \
+    {0.0779666338315423, 5.804551873143357e-18}, \
+    {0.09347678115858947, -6.2844725995420954e-18}, \
+    {0.10894195698986579, 6.8267122072409585e-18}, \
+    {0.12435499454676144, -3.1253241424539383e-18}, \
+    {0.13970887428916365, -2.9579864247315813e-18}, \
+    {0.15499674192394097, 9.585415594114324e-18}, \
+    {0.1702119252854744, -3.541164079802125e-18}, \
+    {0.18534794999569476, 4.180692268843079e-18}, \
+    {0.2003985538258785, 3.1399542871844493e-18}, \
+    {0.21535769969773805, 4.738160130078733e-19}, \
+    {0.23021958727684372, 1.2313404529142703e-17}, \
+    {0.24497866312686414, 1.0698755618734451e-17}, \
+    {0.2596296294082575, 1.9238754924615304e-17}, \
+    {0.2741674511196588, 8.261353575163773e-18}, \
+    {0.2885873618940774, -1.428369957377257e-17}, \
+    {0.3028848683749714, -1.1010827903001369e-17}, \
+    {0.31705575320914703, -1.893928924292642e-17}, \
+    {0.3310960767041321, -7.952610375793799e-18}, \
+    {0.34500217720710513, -2.2938804755578304e-17}, \
+    {0.35877067027057225, -2.4623815582638635e-17}, \
+    {0.3723984466767542, 1.9612311504845653e-17}, \
+    {0.38588266939807375, 2.378822732491941e-17}, \
+    {0.39922076957525254, 2.246598105617042e-17}, \
+    {0.4124104415973873, -1.587652227770689e-17}, \
+    {0.42544963737004227, 2.3315530741892885e-17}, \
+    {0.43833655985795783, -2.494277030626541e-17}, \
+    {0.4510696559885235, -2.2703795229420475e-17}, \
+    {0.4636476090008061, 2.2698777452961687e-17}, \
+    {0.4760693303227612, 1.4654487332256713e-17}, \
+    {0.48833395105640554, -1.1373236189329585e-17}, \
+    {0.5004408131472942, -4.7181675085518756e-17}, \
+    {0.5123894603107377, -2.5462781472855804e-17}, \
+    {0.5241796287829132, 5.520094119641666e-18}, \
+    {0.5358112379604637, -4.0637956834825575e-18}, \
+    {0.5472843809874369, 4.923709671396255e-17}, \
+    {0.5585993153435624, -5.4556305485916264e-18}, \
+    {0.5697564534829784, 1.2255062085054184e-17}, \
+    {0.5807563535676704, -1.441464378193067e-17}, \
+    {0.5915997103351114, 4.920495453686772e-17}, \
+    {0.6022873461349642, 2.950430737228402e-17}, \
+    {0.6128202021652414, -3.1552061848586226e-17}, \
+    {0.6231993299340659, 2.672403885140095e-17}, \
+    {0.6334258829691446, -2.7290767436015276e-17}, \
+    {0.6435011087932844, 1.5834785051444286e-17}, \
+    {0.6534263411807619, 3.5800634857340095e-17}, \
+    {0.6632029927060933, -3.076054864429649e-17}, \
+    {0.6728325475937632, -1.899315009714705e-17}, \
+    {0.6823165548747481, 6.943223671560008e-18}, \
+    {0.6916566218531999, -8.117151192285796e-18}, \
+    {0.7008544078844502, -1.987626234335816e-17}, \
+    {0.7099116184635249, -4.597166450584887e-17}, \
+    {0.7188299996216245, -2.1478388444456983e-17}, \
+    {0.7276113326265107, 2.569325697391839e-18}, \
+    {0.7362574289814281, 3.473937648299457e-17}, \
+    {0.7447701257160751, 3.708315849135547e-17}, \
+    {0.7531512809621944, -2.4256934659182068e-17}, \
+    {0.7614027698055784, 9.850030332752822e-18}, \
+    {0.7695264804056583, -3.704991905602721e-17}, \
+    {0.7775243103733478, -2.6676490951944502e-17}, \
+    {0.7853981633974483, 3.061616997868383e-17}, \
+
+#if defined(__CUDACC__)
+__device__ __constant__ double pstf_atan_tab_dev[65][2] = {PSTF_ATAN_TABLE};
+#endif
+static const double pstf_atan_tab_host[65][2] = {PSTF_ATAN_TABLE};
+
+PSTF_HD DD atan_tab(int i) {
+#if defined(__CUDA_ARCH__)
+    return DD{pstf_atan_tab_dev[i][0], pstf_atan_tab_dev[i][1]};
+#else
+    return DD{pstf_atan_tab_host[i][0], pstf_atan_tab_host[i][1]};
+#endif
+}
+
+/* atan(t) for t = th + tl in [0, 1], double-double, ~2^-104 relative */
+PSTF_HD_NOINLINE DD dd_atan01(DD t) {
+    int i = (int)(t.hi * 64.0 + 0.5);
+    if (i > 64) i = 64;
+    double c = (double)i * 0.015625;
+    DD num = dd_add(t, DD{-c, 0.0});
+    DD tc = dd_mul(t, DD{c, 0.0});
+    DD den = dd_add(DD{1.0, 0.0}, tc);
+    DD r = dd_div(num, den);
+    DD s = dd_mul(r, r);
+    /* P(s) = sum_k (-1)^k s^k / (2k+1), k = 0..8 (|r| <= 2^-7) */
+    const double ch[9] = {1.0, -0.3333333333333333, 0.2, -0.14285714285714285, 0.1111111111111111,
+                          -0.09090909090909091, 0.07692307692307693, -0.06666666666666667,
+                          0.058823529411764705};
+    const double cl[9] = {0.0, -1.850371707708594e-17, -1.1102230246251566e-17,
+                          -7.93016446160826e-18, 6.1679056923619804e-18, 2.523234146875356e-18,
+                          -4.270088556250602e-18, -9.251858538542971e-19, 8.163404592832033e-19};
+    DD acc = DD{ch[8], cl[8]};
+    for (int k = 7; k >= 0; --k) acc = dd_add(dd_mul(acc, s), DD{ch[k], cl[k]});
+    DD at = dd_mul(r, acc);
+    return dd_add(atan_tab(i), at);
+}
+
+/* correctly rounded atan2(y, x) for x, y >= 0 (not both zero), incl. infinities */
+PSTF_HD_NOINLINE double atan2_cr_pos(double y, double x) {
+    const DD pio2 = DD{1.5707963267948966, 6.123233995736766e-17};
+    if (x != x || y != y) return x + y;
+    const double inf = HUGE_VAL;
+    if (x == inf && y == inf) return 0.7853981633974483;
+    if (x == inf) return 0.0;
+    if (y == inf) return 1.5707963267948966;
+    if (y == x) return 0.7853981633974483;
+    int swap = y > x;
+    double a = swap ? x : y, b = swap ? y : x; /* a < b */
+    double th = a / b;
+    double tl = fma(-th, b, a) / b;
+    DD t = dd_quick(th, tl);
+    DD r = dd_atan01(t);
+    if (swap) r = dd_add(pio2, dd_neg(r));
+    return r.hi + r.lo;
+}
+
+PSTF_HD double atan2_fast(double y, double x) { return atan2(y, x); }
+
+/* mappings.h:33-51 with the reference's operation order; exact_atan selects the slow path */
+PSTF_HD void sphere_to_square_impl(double dx, double dy, double dz, int exact_atan, double *uo,
+                                   double *vo) {
+    double x = fabs(dx), y = fabs(dy), z = fabs(dz);
+    double omz = 1.0 - z;
+    double r = sqrt((0.0 < omz) ? omz : 0.0); /* safeSqrt: std::max(0.0, x) vecmath.h:22 */
+    double phi;
+    if (x == 0.0 && y == 0.0) phi = 0.0;
+    else phi = (exact_atan ? atan2_cr_pos(y, x) : atan2_fast(y, x)) * (2.0 / 3.14159265358979323846);
+    double v = phi * r;
+    double u = r - v;
+    if (dz < 0.0) {
+        double t = u;
+        u = v;
+        v = t;
+        u = 1.0 - u;
+        v = 1.0 - v;
+    }
+    u = copysign(u, dx);
+    v = copysign(v, dy);
+    *uo = 0.5 * (u + 1.0);
+    *vo = 0.5 * (v + 1.0);
+}
+
+PSTF_HD int near_cell_boundary(double q) {
+    if (!(q == q)) return 0;
+    double f = floor(q);
+    return (q - f) < 1e-11 || (f + 1.0 - q) < 1e-11;
+}
+
+/* dirCell (field.cpp:93-95) for resolution d */
+PSTF_HD void dir_cells(double dx, double dy, double dz, int d, int32_t *d0, int32_t *d1) {
+    double u, v;
+    sphere_to_square_impl(dx, dy, dz, 0, &u, &v);
+    double qu = u * (double)d, qv = v * (double)d;
+    if (near_cell_boundary(qu) || near_cell_boundary(qv)) {
+        sphere_to_square_impl(dx, dy, dz, 1, &u, &v);
+        qu = u * (double)d;
+        qv = v * (double)d;
+    }
+    int32_t a = i32_x86(qu), b = i32_x86(qv);
+    *d0 = a < d - 1 ? a : d - 1;
+    *d1 = b < d - 1 ? b : d - 1;
+}
+
+/* field.cpp:86-101 */
+PSTF_HD Key key_for(const KeyParams &p, double px, double py, double pz, double dx, double dy,
+                    double dz, int level) {
+    Key k;
+    k.level = level;
+    double cs = cell_size(p, level);
+    k.cell[0] = i32_x86(floor(px / cs));
+    k.cell[1] = i32_x86(floor(py / cs));
+    k.cell[2] = i32_x86(floor(pz / cs));
+    dir_cells(dx, dy, dz, dir_resolution(level), &k.dir[0], &k.dir[1]);
+    k.checksum = checksum_of(pack_key_fields(level, k.cell[0], k.cell[1], k.cell[2], k.dir[0], k.dir[1]));
+    return k;
+}
+
+PSTF_HD uint64_t key_pack(const Key &k) {
+    return pack_key_fields(k.level, k.cell[0], k.cell[1], k.cell[2], k.dir[0], k.dir[1]);
+}
+
+} // namespace pstf_b200

@@ -87,3 +87,22 @@ def level_footprints(base, k=4.0, max_exp=8):
 
 def random_footprints(rng, n, base):
     return base * np.exp(rng.uniform(-4, 8, size=n))
+
+
+def boundary_dirs(rng, n):
+    """Directions whose octahedral coordinates sit within a few ulps of directional-cell
+    boundaries (phi = k/8 rays, perturbed by 0..4 ulps per component)."""
+    k = rng.integers(0, 9, size=n)
+    z = rng.choice([0.0, 0.0, 0.5, 0.25, 0.75, 1.0 / 3.0], size=n) * rng.choice([-1, 1], size=n)
+    s = np.sqrt(1 - z * z)
+    ang = k / 8.0 * (np.pi / 2)
+    x = np.cos(ang) * s
+    y = np.sin(ang) * s
+    for _ in range(4):
+        step = rng.integers(-1, 2, size=n)
+        x = np.where(step > 0, np.nextafter(x, np.inf), np.where(step < 0, np.nextafter(x, -np.inf), x))
+        step = rng.integers(-1, 2, size=n)
+        y = np.where(step > 0, np.nextafter(y, np.inf), np.where(step < 0, np.nextafter(y, -np.inf), y))
+    sx = rng.choice([-1.0, 1.0], size=n)
+    sy = rng.choice([-1.0, 1.0], size=n)
+    return np.stack([x * sx, y * sy, z], axis=1)
