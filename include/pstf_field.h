@@ -1,0 +1,222 @@
+/*
+ * pstf_field.h — C ABI of the B200-native PSTF field cache (libpstf_b200.so).
+ *
+ * Drop-in boundary for the reference's field engine, pstf::FieldStore / FieldUpdateQueue
+ * (/root/reference/proj/core/include/pstf/field.h:19-167).  Each entry point below names the
+ * reference interface it replaces.  Batch entry points take DEVICE pointers (SoA) and a CUDA
+ * stream handle passed as void*; functions that return data to the caller say so.  Every
+ * function returns 0 on success and a negative PSTF_E* code on failure; pstf_last_error()
+ * gives a thread-local message.  No C++ exception crosses this boundary.
+ *
+ * There is no CPU implementation behind this ABI: every computing entry point launches
+ * sm_100a kernels and fails with PSTF_E_CUDA when no device is usable.
+ */
+#ifndef PSTF_FIELD_H
+#define PSTF_FIELD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSTF_ABI_VERSION 1
+
+enum {
+    PSTF_OK = 0,
+    PSTF_E_INVALID = -1, /* bad argument */
+    PSTF_E_CUDA = -2,    /* CUDA runtime / launch failure (incl. no device) */
+    PSTF_E_NOMEM = -3,   /* device or host allocation failed */
+    PSTF_E_IO = -4,      /* snapshot file I/O (field.cpp:340-341, 361-384) */
+    PSTF_E_FORMAT = -5   /* not a snapshot / bad version / truncated */
+};
+
+/* FieldKind (field.h:19) */
+enum { PSTF_KIND_LO = 0, PSTF_KIND_LO_MINUS_E = 1, PSTF_KIND_LI = 2, PSTF_KIND_FLI = 3 };
+/* Technique (field.h:22-27) */
+enum { PSTF_TECH_CAMERA = 1, PSTF_TECH_CONTINUATION = 2, PSTF_TECH_NEE = 4, PSTF_TECH_ALL = 7 };
+/* FieldStoreConfig::Blend (field.h:51) */
+enum { PSTF_BLEND_SQRT = 0, PSTF_BLEND_LINEAR = 1 };
+
+/* Update application modes.
+ * Slot placement is the same in every mode: new keys take slots exactly as sequential
+ * insertion in priority order would (field.cpp:116-146).
+ *  ATOMIC     : priority = key order (FieldUpdateQueue order, field.cpp:402-406); values are
+ *               summed with fp64 atomics (order-free; within 1e-12 relative in practice).
+ *  ORDERED    : bit-exact FieldUpdateQueue::apply (field.cpp:396-420): per slot, updates are
+ *               folded sequentially in the queue's canonical sort order.
+ *  SEQUENTIAL : bit-exact sequence of scalar incrementCounter/accumulate calls in submission
+ *               order (priority = first submission of a key; folds in submission order). */
+enum { PSTF_MODE_ATOMIC = 0, PSTF_MODE_ORDERED = 1, PSTF_MODE_SEQUENTIAL = 2 };
+
+/* FieldStoreConfig (field.h:44-55), same field order and meaning */
+typedef struct pstf_field_config {
+    uint32_t kind;
+    uint32_t capacity_log2;  /* hash-table entries = 2^capacity_log2 (1..30) */
+    int32_t max_level;       /* levels 0..max_level (0..62) */
+    double base_cell_size;   /* level-0 spatial cell edge */
+    double level_select_k;   /* footprint multiplier for level selection */
+    double t_max;            /* temporal window cap; <= 0 or non-finite = unlimited */
+    uint32_t blend;          /* PSTF_BLEND_* */
+    uint32_t technique_mask; /* carried, not read by the store (as in the reference) */
+    uint32_t probe_window;   /* linear-probe window (>= 1) */
+    uint32_t evict_age_frames;
+} pstf_field_config;
+
+/* SpatioDirectionalKey (field.h:32-42); 28 bytes */
+typedef struct pstf_key {
+    int32_t level;
+    int32_t cell[3];
+    int32_t dir_cell[2];
+    uint32_t checksum;
+} pstf_key;
+
+/* FieldStore::SnapshotRecord (field.h:113-120); 64 bytes in memory */
+typedef struct pstf_snapshot_record {
+    int32_t level;
+    int32_t cell[3];
+    int32_t dir_cell[2];
+    uint32_t checksum;
+    double value[3];
+    double c_old;
+} pstf_snapshot_record;
+
+/* One table slot (FieldStore::Slot, field.cpp:48-58) for occupancy/parity dumps; 104 bytes */
+typedef struct pstf_slot_record {
+    uint32_t checksum; /* 0 = empty */
+    int32_t level;
+    int32_t cell[3];
+    int32_t dir_cell[2];
+    double value_old[3];
+    double c_old;
+    double accum[3];
+    double c_new;
+    uint32_t last_touched;
+} pstf_slot_record;
+
+typedef struct pstf_field_stats {
+    uint64_t frame;           /* frameIndex()      field.h:105 */
+    uint64_t rejected;        /* rejectedUpdates() field.h:106 */
+    uint64_t dropped;         /* droppedInserts()  field.h:107 */
+    uint64_t internal_errors; /* internalErrors()  field.h:108 */
+    uint64_t live;            /* liveCellCount()   field.h:109 */
+    uint64_t touched_last;    /* slots touched in the last committed frame */
+    uint64_t new_keys_last;   /* keys placed by the last update pass */
+    uint64_t evicted_last;    /* slots evicted by the last endFrame */
+    uint64_t placement_rounds_last; /* deterministic-placement rounds of the last pass */
+} pstf_field_stats;
+
+/* Three coordinate arrays of one fp64 vector field (device pointers) */
+typedef struct pstf_vec3_soa {
+    const double *x, *y, *z;
+} pstf_vec3_soa;
+
+/* The canonical per-vertex record FieldRecorder::onVertex reads (estimators.cpp:194-262,
+ * VertexRecord pathtracer.h:59-90), SoA.  nee_loe = nee.value() (pathtracer.h:42-46),
+ * nee_fli = nee.f * nee.radiance * nee.misWeight (estimators.cpp:251),
+ * ratio = transportRatio() (pathtracer.h:86-89), flags bit0 contExtended, bit1 nextIsSurface,
+ * bit2 nee.sampled.  276 bytes per vertex. */
+typedef struct pstf_vertex_soa {
+    pstf_vec3_soa position, wo, wi, next_position, nee_dir;
+    const double *footprint, *next_footprint, *ratio, *next_emis_mis_weight;
+    pstf_vec3_soa emission_here, f, next_emission, nee_loe, nee_fli;
+    const uint32_t *flags;
+} pstf_vertex_soa;
+
+#define PSTF_VERTEX_CONT_EXTENDED 1u
+#define PSTF_VERTEX_NEXT_IS_SURFACE 2u
+#define PSTF_VERTEX_NEE_SAMPLED 4u
+
+typedef struct pstf_field pstf_field;
+
+int pstf_abi_version(void);
+const char *pstf_last_error(void);
+
+/* FieldStore(const FieldStoreConfig&) field.h:78 / ~FieldStore() field.h:79 */
+int pstf_field_create(const pstf_field_config *config, int device, pstf_field **out);
+int pstf_field_destroy(pstf_field *f);
+/* config() field.h:81 */
+int pstf_field_get_config(const pstf_field *f, pstf_field_config *out);
+
+/* selectLevel(double) field.h:83, batched: level[i] = selectLevel(footprint[i]) */
+int pstf_select_level(const pstf_field *f, const double *footprint, int32_t *level, uint64_t n,
+                      void *stream);
+/* keyFor(pos, dir, level) field.h:86, batched */
+int pstf_key_for(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
+                 const int32_t *level, uint64_t n, pstf_key *keys, void *stream);
+
+/* incrementCounter / accumulate (field.h:89-91) and FieldUpdateQueue::apply (field.h:157),
+ * batched.  value = 3 device arrays (r, g, b; ignored where is_counter[i] != 0, may be NULL if
+ * all are counters), w[n], is_counter[n] (NULL = all accumulates).  mode = PSTF_MODE_*. */
+int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *value,
+                     const double *w, const uint8_t *is_counter, uint64_t n, int mode,
+                     void *stream);
+
+/* query(pos, dir, footprint) / queryFromLevel(pos, dir, level) field.h:93-94, batched.
+ * Exactly one of footprint / level is non-NULL.  Outputs: value (3 arrays), valid, fallback,
+ * out_level (any may be NULL). */
+int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
+                     const double *footprint, const int32_t *level, uint64_t n, double *value_r,
+                     double *value_g, double *value_b, uint8_t *valid, uint8_t *fallback,
+                     int32_t *out_level, void *stream);
+
+/* endFrame() field.h:100 */
+int pstf_field_end_frame(pstf_field *f, void *stream);
+/* invalidate() / invalidate(const Aabb&) field.h:102-103; aabb = host double[6] {lo, hi} or NULL */
+int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream);
+
+/* frameIndex / rejectedUpdates / droppedInserts / internalErrors / liveCellCount
+ * (field.h:105-109); synchronises the store's work. */
+int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out);
+/* weightedMeanValue() field.h:111 (host out[3]); synchronises. */
+int pstf_field_weighted_mean(pstf_field *f, double out[3]);
+
+/* Snapshot records sorted by key, as dumpSnapshot writes them (field.cpp:311-337), into a host
+ * buffer.  *count = number of live records; at most cap are written. */
+int pstf_field_snapshot(pstf_field *f, pstf_snapshot_record *records, uint64_t cap,
+                        uint64_t *count);
+/* dumpSnapshot(path) field.h:123: PSTFSNAP v1 file, byte-identical to the reference writer */
+int pstf_field_dump_snapshot(pstf_field *f, const char *path);
+/* readSnapshot(path) field.h:124; kind may be NULL */
+int pstf_read_snapshot(const char *path, pstf_snapshot_record *records, uint64_t cap,
+                       uint64_t *count, uint32_t *kind);
+
+/* Slot-array dump (host) of slots [begin, begin+count) for occupancy parity. */
+int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_record *out);
+
+/* Fused per-vertex pass: FieldRecorder::onVertex (estimators.cpp:194-262) for n vertices, i.e.
+ * next-vertex Lo/LoE lookups on committed state, key generation, update values, and the
+ * counter/accumulate updates into Lo, LoE, FLi (and Li when li != NULL).  Device pointers.
+ * mode = PSTF_MODE_ATOMIC (fast) or PSTF_MODE_ORDERED (== EstimatorRun deterministic mode). */
+int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                     const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask, uint32_t fli_mask,
+                     int mode, void *stream);
+
+/* Same with HOST vertex arrays (pinned for overlap): staged to the device in chunks on the
+ * stream, overlapping copies with the pass.  Returns after the work is enqueued when the host
+ * arrays are pinned, otherwise after the copies complete. */
+int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                          const pstf_vertex_soa *host_v, uint64_t n, uint32_t loe_mask,
+                          uint32_t fli_mask, int mode, void *stream);
+
+/* CV / guiding lookup at the current vertex (estimators.cpp:438-462): out = Lo\E query at
+ * (position, wo, footprint) for every vertex of the record (config 3 "CV lookup"). */
+int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, double *value_r,
+                   double *value_g, double *value_b, uint8_t *valid, void *stream);
+
+/* Synthetic Cornell-box vertex stream written on the device into a
+ * contiguous buffer of 34*n fp64 followed by n uint32 flags (n = width*height*bounces).
+ * Test/bench input, not part of the reference API. */
+int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iteration,
+                        double cam_shift_x, double *buffer, void *stream);
+/* Fills a pstf_vertex_soa view of such a contiguous buffer (host or device memory). */
+void pstf_vertex_soa_from_buffer(const double *buffer, uint64_t n, pstf_vertex_soa *out);
+
+/* Number of kernels this library launched since load (bench evidence). */
+uint64_t pstf_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSTF_FIELD_H */

@@ -1,0 +1,2041 @@
+/*
+ * field.cu — B200-native PSTF field cache: sm_100a kernels + host orchestration + C ABI.
+ *
+ * Reference semantics: /root/reference/proj/core/src/field.cpp (FieldStore, FieldUpdateQueue)
+ * and estimators.cpp:194-262 (FieldRecorder::onVertex).  Design: DESIGN.md.
+ *
+ * Per frame the update path is
+ *   phase 1  one fused pass over the vertex (or update) stream: keys, committed-state lookups,
+ *            update values; updates whose key already owns a slot reachable before any empty
+ *            slot are added straight into the slot with warp-aggregated fp64 RED; updates of
+ *            keys that would insert go to a pending buffer.
+ *   phase 2  pending keys are sorted (priority order), de-duplicated and placed by a parallel
+ *            deterministic deferred-acceptance loop whose fixpoint is exactly the slot layout of
+ *            sequential insertion in priority order (field.cpp:116-146 applied in the order of
+ *            FieldUpdateQueue::apply, field.cpp:396-420); then their sums are committed.
+ *   endFrame two passes over the touched-slot list (mean c_new, then blend + cap) and an
+ *            age-eviction sweep when the table is more than 3/4 full (field.cpp:197-263).
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/pstf_field.h"
+#include "kernels.cuh"
+#include "pstf_keys.cuh"
+#include "pstf_synth.h"
+#include "store.cuh"
+
+using namespace pstf_b200;
+
+/* ------------------------------------------------------------------------------------------ */
+/* errors, launch accounting                                                                   */
+
+static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+static int set_err(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(PSTF_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                                      \
+    do {                                                                                    \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                         \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                 \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(PSTF_E_CUDA, std::string(#kernel) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+static unsigned grid_for(uint64_t n, unsigned block) {
+    uint64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 0x7fffffffULL) g = 0x7fffffffULL;
+    return (unsigned)g;
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* device buffers                                                                              */
+
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t nb = std::max(need, (size_t)256);
+        nb = nb + nb / 4;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e == cudaSuccess) bytes = nb;
+        return e;
+    }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+#define ENSURE(buf, nbytes) CK((buf).ensure(nbytes))
+
+struct Scratch {
+    DBuf pend, pend_seq, pend_count;
+    DBuf valid, scan;                       // apply(): order-preserving compaction
+    DBuf ranges;                            // int32 min/max of 7 key fields
+    DBuf words;                             // packed sort words [nw][N]
+    DBuf ktmp0, ktmp1, perm0, perm1, cub;   // radix sort
+    DBuf head, uid, ufirst, ukey, ucs, usid, uhome, ucalls, usum, ures0, ures1, rank, csr, useq;
+    DBuf changed;
+    DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
+    DBuf snap;                              // snapshot gather
+    unsigned long long *h_small = nullptr;  // pinned readback
+    ~Scratch() {
+        if (h_small) cudaFreeHost(h_small);
+    }
+};
+
+struct pstf_field {
+    pstf_field_config cfg;
+    int device = 0;
+    uint64_t frame = 0;
+    DevStore d;
+    uint32_t *hold[2] = {nullptr, nullptr};
+    void *arena = nullptr;
+    Scratch sc;
+    uint64_t new_keys_last = 0, rounds_last = 0;
+};
+
+static DevStore dev_view(const pstf_field *f) {
+    DevStore s = f->d;
+    s.frame = (uint32_t)f->frame;
+    return s;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K1: select_level / key_for batch                                                            */
+
+__global__ void k_select_level(KeyParams kp, const double *fp, int32_t *out, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = select_level(kp, fp[i]);
+}
+
+__global__ void k_key_for(KeyParams kp, pstf_vec3_soa pos, pstf_vec3_soa dir, const int32_t *level,
+                          uint64_t n, pstf_key *out) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Key k = key_for(kp, pos.x[i], pos.y[i], pos.z[i], dir.x[i], dir.y[i], dir.z[i], level[i]);
+    pstf_key o;
+    o.level = k.level;
+    o.cell[0] = k.cell[0];
+    o.cell[1] = k.cell[1];
+    o.cell[2] = k.cell[2];
+    o.dir_cell[0] = k.dir[0];
+    o.dir_cell[1] = k.dir[1];
+    o.checksum = k.checksum;
+    out[i] = o;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K4: hierarchical lookup (queryFromLevel, field.cpp:179-195)                                 */
+
+__device__ __forceinline__ bool lookup_level_chain(const DevStore &s, double px, double py,
+                                                   double pz, double dx, double dy, double dz,
+                                                   int level, double3 *val, int *lev_out) {
+    for (int l = level; l <= s.kp.max_level; ++l) {
+        Key k = key_for(s.kp, px, py, pz, dx, dy, dz, l);
+        int idx = probe_find(s, (uint32_t)key_pack(k) & s.mask, k.checksum);
+        if (idx >= 0) {
+            double4 c = s.com[idx];
+            if (c.w > 0.0) {
+                *val = make_double3(c.x, c.y, c.z);
+                *lev_out = l;
+                return true;
+            }
+        }
+    }
+    *lev_out = level;
+    return false;
+}
+
+__global__ void k_query(DevStore s, pstf_vec3_soa pos, pstf_vec3_soa dir, const double *fp,
+                        const int32_t *level, uint64_t n, double *vr, double *vg, double *vb,
+                        uint8_t *valid, uint8_t *fallback, int32_t *olevel) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int l0 = fp ? select_level(s.kp, fp[i]) : level[i];
+    double3 v = make_double3(0.0, 0.0, 0.0);
+    int lo;
+    bool ok = lookup_level_chain(s, pos.x[i], pos.y[i], pos.z[i], dir.x[i], dir.y[i], dir.z[i], l0,
+                                 &v, &lo);
+    if (!ok) v = make_double3(0.0, 0.0, 0.0);
+    if (vr) vr[i] = v.x;
+    if (vg) vg[i] = v.y;
+    if (vb) vb[i] = v.z;
+    if (valid) valid[i] = ok;
+    if (fallback) fallback[i] = ok && lo != l0;
+    if (olevel) olevel[i] = lo;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K5: fused vertex pass (phase 1)                                                             */
+
+struct VPArgs {
+    Stores4 st;
+    int has_li;
+    int same_lo_loe, same_fli_lo, same_li_fli;
+    uint32_t loe_mask, fli_mask;
+    pstf_vertex_soa v;
+    uint64_t n;
+    PendRec *pend;
+    unsigned long long *pend_count;
+    uint64_t pend_cap;
+};
+
+#define VP_BLOCK 256
+#define WARPS_PER_BLOCK (VP_BLOCK / 32)
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ bool finite3(double a, double b, double c) {
+    return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+/* Appends records with one atomic per warp; all 32 lanes must call it. */
+__device__ __forceinline__ void warp_append(const VPArgs &a, bool want, const PendRec &r) {
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    unsigned lane = lane_id();
+    int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if ((int)lane == leader) base = atomicAdd(a.pend_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (want) {
+        unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+        if (pos < a.pend_cap) a.pend[pos] = r;
+    }
+}
+
+/* One update slot of the vertex (ATOMIC mode), executed by all 32 lanes in lock-step:
+ * probe the frame-start table; existing slot -> warp-aggregated RED; empty-first -> pending;
+ * exhausted -> dropped. */
+__device__ __forceinline__ void contribute_atomic(const VPArgs &a, double4 *sm, int sid, bool has,
+                                                  const Key &k, double4 v, uint32_t ncalls) {
+    const DevStore &s = a.st.s[sid & 3];
+    int res = -3;
+    uint64_t packed = 0;
+    if (has) {
+        packed = key_pack(k);
+        res = probe_existing(s, (uint32_t)packed & s.mask, k.checksum);
+    }
+    unsigned lane = lane_id();
+    unsigned long long gk = res >= 0 ? (((unsigned long long)sid << 32) | (unsigned)res)
+                                     : (0xffffffff00000000ull | lane);
+    unsigned peers = __match_any_sync(0xffffffffu, gk);
+    sm[lane] = v;
+    __syncwarp();
+    if (res >= 0 && (int)lane == __ffs(peers) - 1) {
+        double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+        unsigned m = peers;
+        while (m) {
+            int j = __ffs(m) - 1;
+            m &= m - 1;
+            double4 x = sm[j];
+            t.x += x.x;
+            t.y += x.y;
+            t.z += x.z;
+            t.w += x.w;
+        }
+        double4 *dst = &s.acc[res];
+        if (t.x != 0.0) atomicAdd(&dst->x, t.x);
+        if (t.y != 0.0) atomicAdd(&dst->y, t.y);
+        if (t.z != 0.0) atomicAdd(&dst->z, t.z);
+        if (t.w != 0.0) atomicAdd(&dst->w, t.w);
+        touch_slot(s, (uint32_t)res);
+    }
+    __syncwarp();
+    PendRec r;
+    bool want = res == -1;
+    if (want) {
+        r.k[0] = k.level;
+        r.k[1] = k.cell[0];
+        r.k[2] = k.cell[1];
+        r.k[3] = k.cell[2];
+        r.k[4] = k.dir[0];
+        r.k[5] = k.dir[1];
+        r.cs = k.checksum;
+        r.meta = PSTF_META(sid, 0, ncalls);
+        r.v[0] = v.x;
+        r.v[1] = v.y;
+        r.v[2] = v.z;
+        r.v[3] = v.w;
+    }
+    warp_append(a, want, r);
+    if (res == -2) atomicAdd(&s.ctr[C_DROPPED], (unsigned long long)ncalls);
+}
+
+/* ORDERED mode: every call becomes a record. */
+__device__ __forceinline__ void emit_call(const VPArgs &a, bool want, int sid, const Key &k,
+                                          bool is_counter, double r_, double g_, double b_,
+                                          double w) {
+    PendRec r;
+    if (want) {
+        r.k[0] = k.level;
+        r.k[1] = k.cell[0];
+        r.k[2] = k.cell[1];
+        r.k[3] = k.cell[2];
+        r.k[4] = k.dir[0];
+        r.k[5] = k.dir[1];
+        r.cs = k.checksum;
+        r.meta = PSTF_META(sid, is_counter ? 1 : 0, 1);
+        r.v[0] = r_;
+        r.v[1] = g_;
+        r.v[2] = b_;
+        r.v[3] = w;
+    }
+    warp_append(a, want, r);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
+    __shared__ double4 smem[WARPS_PER_BLOCK][32];
+    double4 *sm = smem[threadIdx.x >> 5];
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool live = i < a.n;
+    const uint64_t ii = live ? i : 0;
+    const pstf_vertex_soa &V = a.v;
+    const DevStore &sLo = a.st.s[0];
+    const DevStore &sLoe = a.st.s[1];
+    const DevStore &sFli = a.st.s[2];
+    const DevStore &sLi = a.st.s[3];
+
+    uint32_t fl = live ? __ldg(&V.flags[ii]) : 0u;
+    const bool cont = (fl & PSTF_VERTEX_CONT_EXTENDED) != 0;
+    const bool nsurf = (fl & PSTF_VERTEX_NEXT_IS_SURFACE) != 0;
+    const bool nee = (fl & PSTF_VERTEX_NEE_SAMPLED) != 0;
+
+    const double px = __ldg(&V.position.x[ii]), py = __ldg(&V.position.y[ii]),
+                 pz = __ldg(&V.position.z[ii]);
+    const double wox = __ldg(&V.wo.x[ii]), woy = __ldg(&V.wo.y[ii]), woz = __ldg(&V.wo.z[ii]);
+    const double wix = __ldg(&V.wi.x[ii]), wiy = __ldg(&V.wi.y[ii]), wiz = __ldg(&V.wi.z[ii]);
+    const double fp = __ldg(&V.footprint[ii]);
+    const int level = select_level(sLo.kp, fp); /* estimators.cpp:195 */
+
+    /* next-vertex lookups on committed state (estimators.cpp:197-211) */
+    double3 loNext = make_double3(0.0, 0.0, 0.0), loeNext = make_double3(0.0, 0.0, 0.0);
+    const double nex = __ldg(&V.next_emission.x[ii]), ney = __ldg(&V.next_emission.y[ii]),
+                 nez = __ldg(&V.next_emission.z[ii]);
+    if (live && cont) {
+        if (nsurf) {
+            const double qx = __ldg(&V.next_position.x[ii]), qy = __ldg(&V.next_position.y[ii]),
+                         qz = __ldg(&V.next_position.z[ii]);
+            const double nfp = __ldg(&V.next_footprint[ii]);
+            const double dx = -wix, dy = -wiy, dz = -wiz;
+            int lq;
+            double3 r;
+            if (a.same_lo_loe) {
+                /* Lo and LoE share the quantisation: one key per level, two probes */
+                int l0 = select_level(sLo.kp, nfp);
+                bool doneLo = false, doneLoe = false;
+                for (int l = l0; l <= sLo.kp.max_level && !(doneLo && doneLoe); ++l) {
+                    Key k = key_for(sLo.kp, qx, qy, qz, dx, dy, dz, l);
+                    uint64_t pk = key_pack(k);
+                    if (!doneLo) {
+                        int idx = probe_find(sLo, (uint32_t)pk & sLo.mask, k.checksum);
+                        if (idx >= 0) {
+                            double4 c = sLo.com[idx];
+                            if (c.w > 0.0) {
+                                loNext = make_double3(c.x, c.y, c.z);
+                                doneLo = true;
+                            }
+                        }
+                    }
+                    if (!doneLoe) {
+                        int idx = probe_find(sLoe, (uint32_t)pk & sLoe.mask, k.checksum);
+                        if (idx >= 0) {
+                            double4 c = sLoe.com[idx];
+                            if (c.w > 0.0) {
+                                loeNext = make_double3(c.x, c.y, c.z);
+                                doneLoe = true;
+                            }
+                        }
+                    }
+                }
+            } else {
+                if (lookup_level_chain(sLo, qx, qy, qz, dx, dy, dz, select_level(sLo.kp, nfp), &r, &lq))
+                    loNext = r;
+                if (lookup_level_chain(sLoe, qx, qy, qz, dx, dy, dz, select_level(sLoe.kp, nfp), &r, &lq))
+                    loeNext = r;
+            }
+        } else {
+            loNext = make_double3(nex, ney, nez);
+        }
+    }
+    const double ratio = __ldg(&V.ratio[ii]);
+    const double fr = __ldg(&V.f.x[ii]), fg = __ldg(&V.f.y[ii]), fb = __ldg(&V.f.z[ii]);
+    const double nmis = __ldg(&V.next_emis_mis_weight[ii]);
+    const double ehx = __ldg(&V.emission_here.x[ii]), ehy = __ldg(&V.emission_here.y[ii]),
+                 ehz = __ldg(&V.emission_here.z[ii]);
+
+    /* ---- Lo (estimators.cpp:215-221) ---- */
+    Key kLo = key_for(sLo.kp, px, py, pz, wox, woy, woz, level);
+    const bool transp = cont && ratio > 0.0;
+    double ulx = ((0.0 + loNext.x) * fr) * ratio, uly = ((0.0 + loNext.y) * fg) * ratio,
+           ulz = ((0.0 + loNext.z) * fb) * ratio; /* computeUpdateValue(Lo) field.cpp:17-18 */
+    /* ---- LoE (226-234) ---- */
+    Key kLoe = a.same_lo_loe ? kLo : key_for(sLoe.kp, px, py, pz, wox, woy, woz, level);
+    const double lex = nex * nmis, ley = ney * nmis, lez = nez * nmis;
+    double uex = ((lex + loeNext.x) * fr) * ratio, uey = ((ley + loeNext.y) * fg) * ratio,
+           uez = ((lez + loeNext.z) * fb) * ratio;
+    const bool loeCont = transp && (a.loe_mask & PSTF_TECH_CONTINUATION);
+    const bool loeNee = nee && (a.loe_mask & PSTF_TECH_NEE);
+    double nlx = 0, nly = 0, nlz = 0;
+    if (loeNee) {
+        nlx = __ldg(&V.nee_loe.x[ii]);
+        nly = __ldg(&V.nee_loe.y[ii]);
+        nlz = __ldg(&V.nee_loe.z[ii]);
+    }
+    /* lIncoming (237) */
+    const double lix = lex + loeNext.x, liy = ley + loeNext.y, liz = lez + loeNext.z;
+    /* ---- FLi continuation (241-246) ---- */
+    Key kFc = key_for(sFli.kp, px, py, pz, wix, wiy, wiz, level);
+    const bool fliCont = cont && (a.fli_mask & PSTF_TECH_CONTINUATION);
+    const double fcx = fr * lix, fcy = fg * liy, fcz = fb * liz;
+    /* ---- FLi NEE (247-254) ---- */
+    Key kFn;
+    double nfx = 0, nfy = 0, nfz = 0;
+    const bool fliNee = nee && (a.fli_mask & PSTF_TECH_NEE);
+    if (nee) {
+        kFn = key_for(sFli.kp, px, py, pz, __ldg(&V.nee_dir.x[ii]), __ldg(&V.nee_dir.y[ii]),
+                      __ldg(&V.nee_dir.z[ii]), level);
+        if (fliNee) {
+            nfx = __ldg(&V.nee_fli.x[ii]);
+            nfy = __ldg(&V.nee_fli.y[ii]);
+            nfz = __ldg(&V.nee_fli.z[ii]);
+        }
+    } else {
+        kFn = kFc;
+    }
+    /* ---- Li (256-261) ---- */
+    Key kLi = kFc;
+    if (a.has_li && !a.same_li_fli) kLi = key_for(sLi.kp, px, py, pz, wix, wiy, wiz, level);
+    const double lvx = lix * 1.0, lvy = liy * 1.0, lvz = liz * 1.0;
+
+    if (MODE == PSTF_MODE_ATOMIC) {
+        /* per-(vertex, store, key) aggregation of the reference's separate calls; non-finite
+         * accumulates are rejected and counted like field.cpp:161-163 */
+        unsigned rej = 0;
+        double4 vlo = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nlo = 1;
+        if (finite3(ehx, ehy, ehz)) { vlo.x += ehx; vlo.y += ehy; vlo.z += ehz; ++nlo; } else ++rej;
+        if (transp) {
+            if (finite3(ulx, uly, ulz)) { vlo.x += ulx; vlo.y += uly; vlo.z += ulz; ++nlo; } else ++rej;
+        }
+        double4 vle = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nle = 1;
+        unsigned rejLoe = 0;
+        if (loeCont) {
+            if (finite3(uex, uey, uez)) { vle.x += uex; vle.y += uey; vle.z += uez; ++nle; } else ++rejLoe;
+        }
+        if (loeNee) {
+            if (finite3(nlx, nly, nlz)) { vle.x += nlx; vle.y += nly; vle.z += nlz; ++nle; } else ++rejLoe;
+        }
+        double4 vfc = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nfc = 1;
+        unsigned rejFli = 0;
+        if (fliCont) {
+            if (finite3(fcx, fcy, fcz)) { vfc.x += fcx; vfc.y += fcy; vfc.z += fcz; ++nfc; } else ++rejFli;
+        }
+        double4 vfn = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nfn = 1;
+        if (fliNee) {
+            if (finite3(nfx, nfy, nfz)) { vfn.x += nfx; vfn.y += nfy; vfn.z += nfz; ++nfn; } else ++rejFli;
+        }
+        double4 vli = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nli = 1;
+        unsigned rejLi = 0;
+        if (finite3(lvx, lvy, lvz)) { vli.x += lvx; vli.y += lvy; vli.z += lvz; ++nli; } else ++rejLi;
+
+        if (live) {
+            if (rej) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rej);
+            if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
+            if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
+            if (a.has_li && cont && rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
+        }
+        contribute_atomic(a, sm, 0, live, kLo, vlo, nlo);
+        contribute_atomic(a, sm, 1, live, kLoe, vle, nle);
+        contribute_atomic(a, sm, 2, live && cont, kFc, vfc, nfc);
+        contribute_atomic(a, sm, 2, live && nee, kFn, vfn, nfn);
+        if (a.has_li) contribute_atomic(a, sm, 3, live && cont, kLi, vli, nli);
+    } else {
+        /* ORDERED: the reference's individual calls, in any order (the sort canonicalises) */
+        unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
+        emit_call(a, live, 0, kLo, true, 0.0, 0.0, 0.0, 1.0);
+        bool ok = finite3(ehx, ehy, ehz);
+        rejLo += live && !ok;
+        emit_call(a, live && ok, 0, kLo, false, ehx, ehy, ehz, 1.0);
+        ok = finite3(ulx, uly, ulz);
+        rejLo += live && transp && !ok;
+        emit_call(a, live && transp && ok, 0, kLo, false, ulx, uly, ulz, 1.0);
+        emit_call(a, live, 1, kLoe, true, 0.0, 0.0, 0.0, 1.0);
+        ok = finite3(uex, uey, uez);
+        rejLoe += live && loeCont && !ok;
+        emit_call(a, live && loeCont && ok, 1, kLoe, false, uex, uey, uez, 1.0);
+        ok = finite3(nlx, nly, nlz);
+        rejLoe += live && loeNee && !ok;
+        emit_call(a, live && loeNee && ok, 1, kLoe, false, nlx, nly, nlz, 1.0);
+        emit_call(a, live && cont, 2, kFc, true, 0.0, 0.0, 0.0, 1.0);
+        ok = finite3(fcx, fcy, fcz);
+        rejFli += live && fliCont && !ok;
+        emit_call(a, live && fliCont && ok, 2, kFc, false, fcx, fcy, fcz, 1.0);
+        emit_call(a, live && nee, 2, kFn, true, 0.0, 0.0, 0.0, 1.0);
+        ok = finite3(nfx, nfy, nfz);
+        rejFli += live && fliNee && !ok;
+        emit_call(a, live && fliNee && ok, 2, kFn, false, nfx, nfy, nfz, 1.0);
+        if (a.has_li) {
+            emit_call(a, live && cont, 3, kLi, true, 0.0, 0.0, 0.0, 1.0);
+            ok = finite3(lvx, lvy, lvz);
+            rejLi += live && cont && !ok;
+            emit_call(a, live && cont && ok, 3, kLi, false, lvx, lvy, lvz, 1.0);
+        }
+        if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
+        if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
+        if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
+        if (rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
+    }
+}
+
+/* CV lookup at the current vertex (estimators.cpp:453-462) */
+__global__ void k_cv_lookup(DevStore s, pstf_vertex_soa V, uint64_t n, double *vr, double *vg,
+                            double *vb, uint8_t *valid) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double3 v = make_double3(0.0, 0.0, 0.0);
+    int lo;
+    bool ok = lookup_level_chain(s, V.position.x[i], V.position.y[i], V.position.z[i], V.wo.x[i],
+                                 V.wo.y[i], V.wo.z[i], select_level(s.kp, V.footprint[i]), &v, &lo);
+    if (!ok) v = make_double3(0.0, 0.0, 0.0);
+    if (vr) vr[i] = v.x;
+    if (vg) vg[i] = v.y;
+    if (vb) vb[i] = v.z;
+    if (valid) valid[i] = ok;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* apply(): batched incrementCounter / accumulate / FieldUpdateQueue::apply                    */
+
+__device__ __forceinline__ bool update_valid(bool is_counter, double r, double g, double b,
+                                             double w) {
+    if (is_counter) return (w >= 0.0) && isfinite(w); /* field.cpp:149 */
+    return finite3(r, g, b) && isfinite(w) && !(w < 0.0); /* field.cpp:161 */
+}
+
+struct ApplyArgs {
+    DevStore s;
+    const pstf_key *keys;
+    const double *vr, *vg, *vb;
+    const double *w;
+    const uint8_t *isc;
+    uint64_t n;
+};
+
+/* ATOMIC: existing slot -> RED, new key -> pending, exhausted -> dropped */
+__global__ void k_apply_atomic(ApplyArgs a, PendRec *pend, unsigned long long *pend_count,
+                               uint64_t cap) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const bool isc = a.isc ? a.isc[i] != 0 : false;
+    const double w = a.w[i];
+    const double r = (isc || !a.vr) ? 0.0 : a.vr[i], g = (isc || !a.vg) ? 0.0 : a.vg[i],
+                 b = (isc || !a.vb) ? 0.0 : a.vb[i];
+    if (!update_valid(isc, r, g, b, w)) {
+        atomicAdd(&a.s.ctr[C_REJECTED], 1ull);
+        return;
+    }
+    pstf_key k = a.keys[i];
+    uint64_t pk = pack_key_fields(k.level, k.cell[0], k.cell[1], k.cell[2], k.dir_cell[0],
+                                  k.dir_cell[1]);
+    double4 v = isc ? make_double4(0.0, 0.0, 0.0, w > 0.0 ? w : 0.0)
+                    : make_double4(r * w, g * w, b * w, 0.0);
+    int res = probe_existing(a.s, (uint32_t)pk & a.s.mask, k.checksum);
+    if (res >= 0) {
+        double4 *dst = &a.s.acc[res];
+        if (v.x != 0.0) atomicAdd(&dst->x, v.x);
+        if (v.y != 0.0) atomicAdd(&dst->y, v.y);
+        if (v.z != 0.0) atomicAdd(&dst->z, v.z);
+        if (v.w != 0.0) atomicAdd(&dst->w, v.w);
+        touch_slot(a.s, (uint32_t)res);
+    } else if (res == -2) {
+        atomicAdd(&a.s.ctr[C_DROPPED], 1ull);
+    } else {
+        unsigned long long pos = atomicAdd(pend_count, 1ull);
+        if (pos < cap) {
+            PendRec rr;
+            rr.k[0] = k.level;
+            rr.k[1] = k.cell[0];
+            rr.k[2] = k.cell[1];
+            rr.k[3] = k.cell[2];
+            rr.k[4] = k.dir_cell[0];
+            rr.k[5] = k.dir_cell[1];
+            rr.cs = k.checksum;
+            rr.meta = PSTF_META(0, 0, 1);
+            rr.v[0] = v.x;
+            rr.v[1] = v.y;
+            rr.v[2] = v.z;
+            rr.v[3] = v.w;
+            pend[pos] = rr;
+        }
+    }
+}
+
+/* ORDERED / SEQUENTIAL: validity flags, then an order-preserving compaction */
+__global__ void k_apply_flags(ApplyArgs a, uint32_t *valid) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const bool isc = a.isc ? a.isc[i] != 0 : false;
+    const double w = a.w[i];
+    const double r = (isc || !a.vr) ? 0.0 : a.vr[i], g = (isc || !a.vg) ? 0.0 : a.vg[i],
+                 b = (isc || !a.vb) ? 0.0 : a.vb[i];
+    bool ok = update_valid(isc, r, g, b, w);
+    valid[i] = ok ? 1u : 0u;
+    if (!ok) atomicAdd(&a.s.ctr[C_REJECTED], 1ull);
+}
+
+__global__ void k_apply_records(ApplyArgs a, const uint32_t *valid, const uint32_t *scan,
+                                PendRec *pend, uint64_t *seq) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n || !valid[i]) return;
+    const bool isc = a.isc ? a.isc[i] != 0 : false;
+    pstf_key k = a.keys[i];
+    PendRec rr;
+    rr.k[0] = k.level;
+    rr.k[1] = k.cell[0];
+    rr.k[2] = k.cell[1];
+    rr.k[3] = k.cell[2];
+    rr.k[4] = k.dir_cell[0];
+    rr.k[5] = k.dir_cell[1];
+    rr.cs = k.checksum;
+    rr.meta = PSTF_META(0, isc ? 1 : 0, 1);
+    rr.v[0] = (isc || !a.vr) ? 0.0 : a.vr[i];
+    rr.v[1] = (isc || !a.vg) ? 0.0 : a.vg[i];
+    rr.v[2] = (isc || !a.vb) ? 0.0 : a.vb[i];
+    rr.v[3] = a.w[i];
+    uint32_t pos = scan[i];
+    pend[pos] = rr;
+    if (seq) seq[pos] = i;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* phase 2: sort pending records into priority order                                           */
+
+#define NF_KEY 7 /* store, level, c0, c1, c2, d0, d1 */
+enum { F_STORE = 0, F_LEVEL, F_C0, F_C1, F_C2, F_D0, F_D1, F_ISC, F_R, F_G, F_B, F_W, F_SEQ, F_MAX };
+
+struct Layout {
+    int nfields;
+    int fid[F_MAX];
+    int word[F_MAX];
+    int shift[F_MAX];
+    int bits[F_MAX];
+    long long minv[F_MAX];
+    int nwords;
+    int begin_bit[F_MAX];
+};
+
+__device__ __forceinline__ int rec_field_i(const PendRec &r, int f) {
+    return f == F_STORE ? (int)PSTF_META_SID(r.meta) : r.k[f - 1];
+}
+
+/* min/max of the 7 key fields over the pending records; out[2f] = min, out[2f+1] = max */
+__global__ void k_ranges(const PendRec *pend, const unsigned long long *count, uint64_t cap,
+                         int *out) {
+    uint64_t n = *count;
+    if (n > cap) n = cap;
+    int mn[NF_KEY], mx[NF_KEY];
+    for (int f = 0; f < NF_KEY; ++f) {
+        mn[f] = INT32_MAX;
+        mx[f] = INT32_MIN;
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        PendRec r = pend[i];
+        for (int f = 0; f < NF_KEY; ++f) {
+            int v = rec_field_i(r, f);
+            mn[f] = min(mn[f], v);
+            mx[f] = max(mx[f], v);
+        }
+    }
+    for (int f = 0; f < NF_KEY; ++f) {
+        int a = __reduce_min_sync(0xffffffffu, mn[f]);
+        int b = __reduce_max_sync(0xffffffffu, mx[f]);
+        if (lane_id() == 0) {
+            atomicMin(&out[2 * f], a);
+            atomicMax(&out[2 * f + 1], b);
+        }
+    }
+}
+
+__global__ void k_encode(const PendRec *pend, const uint64_t *seq, uint64_t n, Layout L,
+                         uint64_t *words) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    PendRec r = pend[i];
+    uint64_t w[F_MAX];
+    for (int k = 0; k < L.nwords; ++k) w[k] = 0;
+    for (int q = 0; q < L.nfields; ++q) {
+        int f = L.fid[q];
+        uint64_t v;
+        if (f < NF_KEY) v = (uint64_t)((long long)rec_field_i(r, f) - L.minv[q]);
+        else if (f == F_ISC) v = PSTF_META_ISC(r.meta);
+        else if (f == F_SEQ) v = seq[i];
+        else v = dbits(r.v[f - F_R]);
+        w[L.word[q]] |= L.bits[q] == 64 ? v : (v << L.shift[q]);
+    }
+    for (int k = 0; k < L.nwords; ++k) words[(uint64_t)k * n + i] = w[k];
+}
+
+__global__ void k_iota(uint32_t *p, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_u64(const uint64_t *src, const uint32_t *perm, uint64_t n, uint64_t *dst) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+/* head[j] = 1 where the (store, key) of sorted position j differs from j-1 */
+__global__ void k_heads(const PendRec *pend, const uint32_t *perm, uint64_t n, uint32_t *head) {
+    uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    if (j == 0) {
+        head[0] = 1;
+        return;
+    }
+    PendRec a = pend[perm[j - 1]], b = pend[perm[j]];
+    bool same = PSTF_META_SID(a.meta) == PSTF_META_SID(b.meta);
+    for (int f = 0; f < 6; ++f) same = same && a.k[f] == b.k[f];
+    head[j] = same ? 0u : 1u;
+}
+
+struct UniqArgs {
+    uint32_t *ufirst;
+    KeyFields *ukey;
+    uint32_t *ucs, *usid, *uhome;
+    uint32_t *ucalls;
+    double4 *usum;
+    uint64_t *useq; // first submission seq (SEQUENTIAL)
+};
+
+__global__ void k_unique_build(const PendRec *pend, const uint32_t *perm, const uint32_t *head,
+                               const uint32_t *uid, const uint64_t *seq, uint64_t n, Stores4 st,
+                               UniqArgs u) {
+    uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n || !head[j]) return;
+    uint32_t q = uid[j] - 1u;
+    uint32_t r = perm[j];
+    PendRec p = pend[r];
+    u.ufirst[q] = (uint32_t)j;
+    KeyFields kf = {p.k[0], p.k[1], p.k[2], p.k[3], p.k[4], p.k[5]};
+    u.ukey[q] = kf;
+    u.ucs[q] = p.cs;
+    uint32_t sid = PSTF_META_SID(p.meta);
+    u.usid[q] = sid;
+    uint64_t pk = pack_key_fields(p.k[0], p.k[1], p.k[2], p.k[3], p.k[4], p.k[5]);
+    u.uhome[q] = (uint32_t)pk & st.s[sid].mask;
+    if (u.useq) u.useq[q] = seq[r];
+}
+
+/* per-unique sums (ATOMIC) and call counts (all modes), warp-aggregated over sorted runs */
+__global__ void k_unique_sums(const PendRec *pend, const uint32_t *perm, const uint32_t *uid,
+                              uint64_t n, int atomic_mode, UniqArgs u) {
+    __shared__ double4 smem[8][32];
+    double4 *sm = smem[threadIdx.x >> 5];
+    uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    bool live = j < n;
+    uint32_t q = live ? uid[j] - 1u : 0xffffffffu;
+    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+    uint32_t calls = 0;
+    if (live) {
+        PendRec p = pend[perm[j]];
+        v = make_double4(p.v[0], p.v[1], p.v[2], p.v[3]);
+        calls = PSTF_META_CALLS(p.meta);
+    }
+    unsigned peers = __match_any_sync(0xffffffffu, q);
+    sm[lane_id()] = v;
+    unsigned tot = 0;
+    __syncwarp();
+    if (live && (int)lane_id() == __ffs(peers) - 1) {
+        double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+        unsigned m = peers;
+        while (m) {
+            int l = __ffs(m) - 1;
+            m &= m - 1;
+            double4 x = sm[l];
+            t.x += x.x;
+            t.y += x.y;
+            t.z += x.z;
+            t.w += x.w;
+        }
+        (void)tot;
+        if (atomic_mode) {
+            if (t.x != 0.0) atomicAdd(&u.usum[q].x, t.x);
+            if (t.y != 0.0) atomicAdd(&u.usum[q].y, t.y);
+            if (t.z != 0.0) atomicAdd(&u.usum[q].z, t.z);
+            if (t.w != 0.0) atomicAdd(&u.usum[q].w, t.w);
+        }
+    }
+    /* call counts: integer, any order */
+    unsigned c = __reduce_add_sync(peers, calls);
+    if (live && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&u.ucalls[q], c);
+}
+
+__global__ void k_rank_scatter(const uint32_t *sorted_uid, uint64_t nu, uint32_t *rank,
+                               const uint32_t *ucs, uint32_t *cs_by_rank) {
+    uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= nu) return;
+    uint32_t u = sorted_uid[r];
+    rank[u] = (uint32_t)r;
+    cs_by_rank[r] = ucs[u];
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* phase 2: deterministic placement (deferred acceptance, Jacobi rounds)                       */
+
+struct PlaceArgs {
+    Stores4 st;
+    uint64_t nu;
+    const uint32_t *usid, *uhome, *ucs;
+    const uint32_t *rank;       // NULL -> rank = u
+    const uint32_t *cs_by_rank; // checksum of the key holding rank r
+    int parity;                 // which hold array is "prev"
+};
+
+__global__ void k_place_round(PlaceArgs a, const unsigned long long *res_prev,
+                              unsigned long long *res_next, int *changed) {
+    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= a.nu) return;
+    const DevStore &s = a.st.s[a.usid[u]];
+    const uint32_t *hold_prev = a.parity ? s.hold1 : s.hold0;
+    uint32_t *hold_next = a.parity ? s.hold0 : s.hold1;
+    const uint32_t r = a.rank ? a.rank[u] : (uint32_t)u;
+    const uint32_t cs = a.ucs[u];
+    const uint32_t home = a.uhome[u];
+    unsigned long long res = PSTF_RES(R_DROP, 0);
+    for (uint32_t i = 0; i < s.window; ++i) {
+        uint32_t idx = (home + i) & s.mask;
+        uint32_t c = s.chk[idx];
+        if (c != 0) {
+            if (c == cs) { /* an older resident with this checksum (field.cpp:122) */
+                res = PSTF_RES(R_FIXED, idx);
+                break;
+            }
+            continue;
+        }
+        uint32_t h = hold_prev[idx];
+        if (h < r) {
+            if (a.cs_by_rank[h] == cs) { /* a higher-priority new key with equal checksum */
+                res = PSTF_RES(R_MERGE, idx);
+                break;
+            }
+            continue;
+        }
+        res = PSTF_RES(R_PROPOSE, idx);
+        break;
+    }
+    if (PSTF_RES_T(res) == R_PROPOSE) atomicMin(&hold_next[PSTF_RES_SLOT(res)], r);
+    res_next[u] = res;
+    if (res != res_prev[u]) *changed = 1;
+}
+
+/* reset the previous round's proposals in hold_prev (so it is all-empty for reuse) */
+__global__ void k_place_clear(PlaceArgs a, const unsigned long long *res_prev) {
+    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= a.nu) return;
+    unsigned long long r = res_prev[u];
+    if (PSTF_RES_T(r) != R_PROPOSE) return;
+    const DevStore &s = a.st.s[a.usid[u]];
+    uint32_t *hold_prev = a.parity ? s.hold1 : s.hold0;
+    hold_prev[PSTF_RES_SLOT(r)] = PSTF_HOLD_NONE;
+}
+
+/* commit placement: owners write the slot; everyone adds its sums (ATOMIC) and touches */
+__global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFields *ukey,
+                         const uint32_t *ucalls, const double4 *usum, int atomic_mode) {
+    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= a.nu) return;
+    const DevStore &s = a.st.s[a.usid[u]];
+    unsigned long long r = res[u];
+    uint32_t t = PSTF_RES_T(r), slot = PSTF_RES_SLOT(r);
+    if (t == R_DROP) {
+        atomicAdd(&s.ctr[C_DROPPED], (unsigned long long)ucalls[u]);
+        return;
+    }
+    if (t == R_PROPOSE) {
+        uint32_t *hold_cur = a.parity ? s.hold0 : s.hold1; /* the array the last round wrote */
+        hold_cur[slot] = PSTF_HOLD_NONE;
+        s.chk[slot] = a.ucs[u];
+        s.keyf[slot] = ukey[u];
+        atomicAdd(&s.ctr[C_LIVE], 1ull);
+        atomicAdd(&s.ctr[C_NEW_KEYS], 1ull);
+    }
+    if (atomic_mode) {
+        double4 v = usum[u];
+        double4 *dst = &s.acc[slot];
+        if (v.x != 0.0) atomicAdd(&dst->x, v.x);
+        if (v.y != 0.0) atomicAdd(&dst->y, v.y);
+        if (v.z != 0.0) atomicAdd(&dst->z, v.z);
+        if (v.w != 0.0) atomicAdd(&dst->w, v.w);
+    }
+    touch_slot(s, slot);
+}
+
+/* ORDERED / SEQUENTIAL: per-record fold target (store << 32 | slot), dropped -> ~0 */
+__global__ void k_fold_targets(const uint32_t *perm, const uint32_t *uid, uint64_t n,
+                               const unsigned long long *res, const uint32_t *usid,
+                               int by_record, uint64_t *tgt, uint32_t *order) {
+    uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    uint32_t u = uid[j] - 1u;
+    unsigned long long r = res[u];
+    uint64_t t = PSTF_RES_T(r) == R_DROP
+                     ? ~0ull
+                     : (((uint64_t)usid[u] << 32) | (uint64_t)PSTF_RES_SLOT(r));
+    uint32_t rec = perm[j];
+    if (by_record) { /* SEQUENTIAL: position = record index = submission order */
+        tgt[rec] = t;
+        order[rec] = rec;
+    } else { /* ORDERED: position = canonical sorted position */
+        tgt[j] = t;
+        order[j] = rec;
+    }
+}
+
+/* one thread per run of equal targets: sequential fold in the sorted order (field.cpp:413-418) */
+__global__ void k_fold(const PendRec *pend, const uint64_t *tgt, const uint32_t *recs, uint64_t n,
+                       Stores4 st) {
+    uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    uint64_t t = tgt[p];
+    if (t == ~0ull) return;
+    if (p > 0 && tgt[p - 1] == t) return;
+    const DevStore &s = st.s[t >> 32];
+    uint32_t slot = (uint32_t)t;
+    double4 acc = s.acc[slot];
+    for (uint64_t q = p; q < n && tgt[q] == t; ++q) {
+        PendRec r = pend[recs[q]];
+        double w = r.v[3];
+        if (PSTF_META_ISC(r.meta)) {
+            if (w > 0.0) acc.w += w; /* field.cpp:157 */
+        } else {
+            acc.x += r.v[0] * w; /* field.cpp:168-170 */
+            acc.y += r.v[1] * w;
+            acc.z += r.v[2] * w;
+        }
+    }
+    s.acc[slot] = acc;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K3: endFrame (field.cpp:197-263) on the touched list                                        */
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+#define EF_BLOCK 256
+
+__global__ void k_ef_reduce(DevStore s) {
+    __shared__ double ssum[EF_BLOCK / 32];
+    __shared__ unsigned long long scnt[EF_BLOCK / 32];
+    uint64_t n = s.ctr[C_TOUCHED_N];
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+    double sum = 0.0;
+    unsigned long long cnt = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double cn = s.acc[s.touched[i]].w;
+        if (cn > 0.0) {
+            sum += cn;
+            ++cnt;
+        }
+    }
+    sum = warp_sum_d(sum);
+    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    if (lane_id() == 0) {
+        ssum[threadIdx.x >> 5] = sum;
+        scnt[threadIdx.x >> 5] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        unsigned long long c = 0;
+        for (int w = 0; w < EF_BLOCK / 32; ++w) {
+            t += ssum[w];
+            c += scnt[w];
+        }
+        if (c) {
+            atomicAdd(s.cn_sum, t);
+            atomicAdd(&s.ctr[C_CN_COUNT], c);
+        }
+    }
+}
+
+__global__ void k_ef_blend(DevStore s) {
+    uint64_t n = s.ctr[C_TOUCHED_N];
+    const unsigned long long cnt = s.ctr[C_CN_COUNT];
+    const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
+    const double tMax = s.t_max;
+    const bool limited = tMax > 0.0 && isfinite(tMax);
+    const double cap = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
+    unsigned long long internal = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t slot = s.touched[i];
+        double4 a = s.acc[slot];
+        double cn = a.w;
+        if (cn > 0.0) {
+            double4 c = s.com[slot];
+            double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+            double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+            if (limited) {
+                double fl = 1.0 / tMax;
+                alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+            }
+            double oma = 1.0 - alpha;
+            c.x = c.x * oma + cx * alpha;
+            c.y = c.y * oma + cy * alpha;
+            c.z = c.z * oma + cz * alpha;
+            c.w = c.w + cn;
+            if (limited) c.w = (cap < c.w) ? cap : c.w; /* std::min(cOld, cap) */
+            s.com[slot] = c;
+        } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+            ++internal;
+        }
+        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+    if (internal) atomicAdd(&s.ctr[C_INTERNAL], internal);
+}
+
+/* age eviction once live*4 > capacity*3 (field.cpp:247-260); live_snap taken before */
+__global__ void k_evict(DevStore s) {
+    unsigned long long cap = (unsigned long long)s.mask + 1ull;
+    const unsigned long long live_snap = s.ctr[C_LIVE_SNAP];
+    if (!(live_snap * 4ull > cap * 3ull)) return;
+    unsigned long long ev = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = s.chk[i];
+        if (c == 0) continue;
+        uint32_t age = s.frame - s.last[i];
+        if (age >= s.evict_age) {
+            s.chk[i] = 0;
+            s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+            ++ev;
+        }
+    }
+    ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);
+    if (lane_id() == 0 && ev) {
+        atomicAdd(&s.ctr[C_EVICTED], ev);
+        atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* invalidate / weighted mean / snapshot / slots                                               */
+
+__global__ void k_invalidate(DevStore s, int use_box, double lx, double ly, double lz, double hx,
+                             double hy, double hz) {
+    uint64_t cap = (uint64_t)s.mask + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (s.chk[i] == 0) continue;
+        if (use_box) {
+            KeyFields k = s.keyf[i];
+            double cs = cell_size(s.kp, k.level); /* field.cpp:278-283 */
+            double cx = ((double)k.c0 + 0.5) * cs, cy = ((double)k.c1 + 0.5) * cs,
+                   cz = ((double)k.c2 + 0.5) * cs;
+            if (!(cx >= lx && cx <= hx && cy >= ly && cy <= hy && cz >= lz && cz <= hz)) continue;
+        }
+        s.com[i].w = 0.0;
+    }
+}
+
+__global__ void k_weighted_mean(DevStore s, double *out4) {
+    uint64_t cap = (uint64_t)s.mask + 1;
+    double r = 0, g = 0, b = 0, w = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (s.chk[i] == 0) continue;
+        double4 c = s.com[i];
+        if (c.w <= 0.0) continue; /* field.cpp:299 */
+        r += c.x * c.w;
+        g += c.y * c.w;
+        b += c.z * c.w;
+        w += c.w;
+    }
+    r = warp_sum_d(r);
+    g = warp_sum_d(g);
+    b = warp_sum_d(b);
+    w = warp_sum_d(w);
+    if (lane_id() == 0 && w != 0.0) {
+        atomicAdd(&out4[0], r);
+        atomicAdd(&out4[1], g);
+        atomicAdd(&out4[2], b);
+        atomicAdd(&out4[3], w);
+    }
+}
+
+__global__ void k_snap_gather(DevStore s, pstf_snapshot_record *out, unsigned long long *count) {
+    uint64_t cap = (uint64_t)s.mask + 1;
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    bool live = i < cap && s.chk[i] != 0;
+    unsigned m = __ballot_sync(0xffffffffu, live);
+    if (!m) return;
+    unsigned long long base = 0;
+    int leader = __ffs(m) - 1;
+    if ((int)lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!live) return;
+    /* slot order is kept by sorting on (key, slot) afterwards */
+    unsigned long long pos = base + __popc(m & ((1u << lane_id()) - 1u));
+    KeyFields k = s.keyf[i];
+    double4 c = s.com[i];
+    pstf_snapshot_record r;
+    r.level = k.level;
+    r.cell[0] = k.c0;
+    r.cell[1] = k.c1;
+    r.cell[2] = k.c2;
+    r.dir_cell[0] = k.d0;
+    r.dir_cell[1] = k.d1;
+    r.checksum = s.chk[i];
+    r.value[0] = c.x;
+    r.value[1] = c.y;
+    r.value[2] = c.z;
+    r.c_old = c.w;
+    out[pos] = r;
+}
+
+/* snapshot sort words: 3 x u64 = (level,c0) (c1,c2) (d0,d1), signed -> biased */
+__global__ void k_snap_words(const pstf_snapshot_record *r, uint64_t n, uint64_t *words) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto b = [](int32_t v) { return (uint64_t)((uint32_t)v ^ 0x80000000u); };
+    pstf_snapshot_record x = r[i];
+    words[i] = (b(x.level) << 32) | b(x.cell[0]);
+    words[n + i] = (b(x.cell[1]) << 32) | b(x.cell[2]);
+    words[2 * n + i] = (b(x.dir_cell[0]) << 32) | b(x.dir_cell[1]);
+}
+
+__global__ void k_snap_permute(const pstf_snapshot_record *src, const uint32_t *perm, uint64_t n,
+                               pstf_snapshot_record *dst) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* synthetic stream                                                                            */
+
+__global__ void k_synth(ps_params P, double *buf, uint64_t n_total) {
+    uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t n_paths = (uint64_t)P.width * (uint64_t)P.height;
+    if (p >= n_paths) return;
+    ps_gen_path(&P, p, buf, (uint32_t *)(buf + 34 * n_total), n_total);
+}
+
+/* ========================================================================================== */
+/* host orchestration                                                                          */
+
+static int sort_multiword(Scratch &sc, const uint64_t *words, const int *begin_bits, int nw,
+                          uint64_t n, uint32_t **perm_out, cudaStream_t st) {
+    ENSURE(sc.perm0, n * 4);
+    ENSURE(sc.perm1, n * 4);
+    ENSURE(sc.ktmp0, n * 8);
+    ENSURE(sc.ktmp1, n * 8);
+    uint32_t *pa = sc.perm0.as<uint32_t>(), *pb = sc.perm1.as<uint32_t>();
+    LAUNCH(k_iota, grid_for(n, 256), 256, 0, st, pa, n);
+    for (int k = nw - 1; k >= 0; --k) {
+        const uint64_t *src = words + (uint64_t)k * n;
+        uint64_t *kin = sc.ktmp0.as<uint64_t>();
+        if (k == nw - 1) {
+            CK(cudaMemcpyAsync(kin, src, n * 8, cudaMemcpyDeviceToDevice, st));
+        } else {
+            LAUNCH(k_gather_u64, grid_for(n, 256), 256, 0, st, src, pa, n, kin);
+        }
+        size_t bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, sc.ktmp1.as<uint64_t>(), pa, pb,
+                                           (int64_t)n, begin_bits[k], 64, st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, kin, sc.ktmp1.as<uint64_t>(), pa, pb,
+                                           (int64_t)n, begin_bits[k], 64, st));
+        g_launches.fetch_add(4, std::memory_order_relaxed);
+        std::swap(pa, pb);
+    }
+    *perm_out = pa;
+    return PSTF_OK;
+}
+
+static int bits_for(unsigned long long range) {
+    return range == 0 ? 0 : 64 - __builtin_clzll(range);
+}
+
+static void add_field(Layout &L, int fid, int bits, long long minv, int &word, int &free_bits) {
+    if (bits <= 0) return;
+    if (bits > free_bits) {
+        L.begin_bit[word] = free_bits;
+        ++word;
+        free_bits = 64;
+    }
+    int q = L.nfields++;
+    L.fid[q] = fid;
+    L.bits[q] = bits;
+    L.word[q] = word;
+    L.shift[q] = free_bits - bits;
+    L.minv[q] = minv;
+    free_bits -= bits;
+}
+
+static Stores4 stores4(pstf_field *const *fs, int nf) {
+    Stores4 s;
+    memset(&s, 0, sizeof(s));
+    for (int i = 0; i < nf && i < 4; ++i)
+        if (fs[i]) s.s[i] = dev_view(fs[i]);
+    return s;
+}
+
+static int read_small(Scratch &sc, const void *dev, size_t bytes, cudaStream_t st) {
+    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+    CK(cudaMemcpyAsync(sc.h_small, dev, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PSTF_OK;
+}
+
+/* Phase 2 for the records sitting in sc.pend (count on device in sc.pend_count).
+ * fs[0..nf) are the stores addressed by record store ids. */
+static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode, uint64_t n_known,
+                           cudaStream_t st) {
+    uint64_t n = n_known;
+    if (n == (uint64_t)-1) {
+        int rc = read_small(sc, sc.pend_count.p, 8, st);
+        if (rc) return rc;
+        n = sc.h_small[0];
+    }
+    for (int i = 0; i < nf; ++i)
+        if (fs[i]) {
+            fs[i]->new_keys_last = 0;
+            fs[i]->rounds_last = 0;
+            CK(cudaMemsetAsync(&fs[i]->d.ctr[C_NEW_KEYS], 0, 8, st));
+        }
+    if (n == 0) return PSTF_OK;
+    if (n > sc.pend.bytes / sizeof(PendRec))
+        return set_err(PSTF_E_NOMEM, "pending-update buffer overflow");
+    if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "too many pending updates");
+    const PendRec *pend = sc.pend.as<PendRec>();
+    const uint64_t *seq = mode == PSTF_MODE_SEQUENTIAL ? sc.pend_seq.as<uint64_t>() : nullptr;
+    Stores4 S = stores4(fs, nf);
+
+    /* 1. key-field ranges -> compact sort layout */
+    ENSURE(sc.ranges, 2 * NF_KEY * 4);
+    {
+        int init[2 * NF_KEY];
+        for (int f = 0; f < NF_KEY; ++f) {
+            init[2 * f] = INT32_MAX;
+            init[2 * f + 1] = INT32_MIN;
+        }
+        if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+        memcpy(sc.h_small, init, sizeof(init));
+        CK(cudaMemcpyAsync(sc.ranges.p, sc.h_small, sizeof(init), cudaMemcpyHostToDevice, st));
+        unsigned g = std::min<uint64_t>(grid_for(n, 256), (uint64_t)sm_count() * 8);
+        LAUNCH(k_ranges, g, 256, 0, st, pend, sc.pend_count.as<unsigned long long>(), n,
+               sc.ranges.as<int>());
+    }
+    int rng[2 * NF_KEY];
+    {
+        int rc = read_small(sc, sc.ranges.p, sizeof(rng), st);
+        if (rc) return rc;
+        memcpy(rng, sc.h_small, sizeof(rng));
+    }
+    Layout L;
+    memset(&L, 0, sizeof(L));
+    int word = 0, free_bits = 64;
+    for (int f = 0; f < NF_KEY; ++f) {
+        long long mn = rng[2 * f], mx = rng[2 * f + 1];
+        add_field(L, f, bits_for((unsigned long long)(mx - mn)), mn, word, free_bits);
+    }
+    if (mode == PSTF_MODE_ORDERED) { /* field.cpp:407-410 tie-break: (isCounter, r, g, b, w) */
+        add_field(L, F_ISC, 1, 0, word, free_bits);
+        for (int c = 0; c < 4; ++c) add_field(L, F_R + c, 64, 0, word, free_bits);
+    } else if (mode == PSTF_MODE_SEQUENTIAL) {
+        add_field(L, F_SEQ, std::max(1, bits_for(n)), 0, word, free_bits);
+    }
+    if (L.nfields == 0) add_field(L, F_STORE, 1, 0, word, free_bits);
+    L.begin_bit[word] = free_bits;
+    L.nwords = word + 1;
+
+    ENSURE(sc.words, (size_t)L.nwords * n * 8);
+    LAUNCH(k_encode, grid_for(n, 256), 256, 0, st, pend, seq, n, L, sc.words.as<uint64_t>());
+    uint32_t *perm = nullptr;
+    {
+        int rc = sort_multiword(sc, sc.words.as<uint64_t>(), L.begin_bit, L.nwords, n, &perm, st);
+        if (rc) return rc;
+    }
+
+    /* 2. unique keys (segments of equal (store, key)) */
+    ENSURE(sc.head, n * 4);
+    ENSURE(sc.uid, n * 4);
+    LAUNCH(k_heads, grid_for(n, 256), 256, 0, st, pend, perm, n, sc.head.as<uint32_t>());
+    {
+        size_t bytes = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, sc.head.as<uint32_t>(),
+                                         sc.uid.as<uint32_t>(), (int64_t)n, st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceScan::InclusiveSum(sc.cub.p, bytes, sc.head.as<uint32_t>(),
+                                         sc.uid.as<uint32_t>(), (int64_t)n, st));
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+    }
+    uint64_t nu;
+    {
+        int rc = read_small(sc, sc.uid.as<uint32_t>() + (n - 1), 4, st);
+        if (rc) return rc;
+        nu = ((uint32_t *)sc.h_small)[0];
+    }
+    ENSURE(sc.ufirst, nu * 4);
+    ENSURE(sc.ukey, nu * sizeof(KeyFields));
+    ENSURE(sc.ucs, nu * 4);
+    ENSURE(sc.usid, nu * 4);
+    ENSURE(sc.uhome, nu * 4);
+    ENSURE(sc.ucalls, nu * 4);
+    ENSURE(sc.usum, nu * sizeof(double4));
+    ENSURE(sc.ures0, nu * 8);
+    ENSURE(sc.ures1, nu * 8);
+    ENSURE(sc.changed, 4);
+    UniqArgs U;
+    U.ufirst = sc.ufirst.as<uint32_t>();
+    U.ukey = sc.ukey.as<KeyFields>();
+    U.ucs = sc.ucs.as<uint32_t>();
+    U.usid = sc.usid.as<uint32_t>();
+    U.uhome = sc.uhome.as<uint32_t>();
+    U.ucalls = sc.ucalls.as<uint32_t>();
+    U.usum = sc.usum.as<double4>();
+    U.useq = nullptr;
+    if (mode == PSTF_MODE_SEQUENTIAL) {
+        ENSURE(sc.useq, nu * 8);
+        U.useq = sc.useq.as<uint64_t>();
+    }
+    CK(cudaMemsetAsync(U.ucalls, 0, nu * 4, st));
+    CK(cudaMemsetAsync(U.usum, 0, nu * sizeof(double4), st));
+    LAUNCH(k_unique_build, grid_for(n, 256), 256, 0, st, pend, perm, sc.head.as<uint32_t>(),
+           sc.uid.as<uint32_t>(), seq, n, S, U);
+    LAUNCH(k_unique_sums, grid_for(n, 256), 256, 0, st, pend, perm, sc.uid.as<uint32_t>(), n,
+           mode == PSTF_MODE_ATOMIC ? 1 : 0, U);
+
+    /* 3. priority ranks */
+    PlaceArgs P;
+    P.st = S;
+    P.nu = nu;
+    P.usid = U.usid;
+    P.uhome = U.uhome;
+    P.ucs = U.ucs;
+    P.rank = nullptr;
+    P.cs_by_rank = U.ucs;
+    if (mode == PSTF_MODE_SEQUENTIAL) { /* priority = first submission (scalar-call order) */
+        ENSURE(sc.rank, nu * 4);
+        ENSURE(sc.csr, nu * 4);
+        uint32_t *ids_in = nullptr, *ids = nullptr;
+        ENSURE(sc.fperm, nu * 4);
+        ENSURE(sc.fperm_out, nu * 4);
+        ENSURE(sc.fkey_out, nu * 8);
+        ids_in = sc.fperm.as<uint32_t>();
+        ids = sc.fperm_out.as<uint32_t>();
+        LAUNCH(k_iota, grid_for(nu, 256), 256, 0, st, ids_in, nu);
+        size_t bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, U.useq, sc.fkey_out.as<uint64_t>(),
+                                           ids_in, ids, (int64_t)nu, 0, 64, st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, U.useq, sc.fkey_out.as<uint64_t>(),
+                                           ids_in, ids, (int64_t)nu, 0, 64, st));
+        g_launches.fetch_add(4, std::memory_order_relaxed);
+        LAUNCH(k_rank_scatter, grid_for(nu, 256), 256, 0, st, ids, nu, sc.rank.as<uint32_t>(),
+               U.ucs, sc.csr.as<uint32_t>());
+        P.rank = sc.rank.as<uint32_t>();
+        P.cs_by_rank = sc.csr.as<uint32_t>();
+    }
+
+    /* 4. deterministic placement: Jacobi rounds to the unique fixpoint */
+    unsigned long long *rprev = sc.ures0.as<unsigned long long>(),
+                       *rnext = sc.ures1.as<unsigned long long>();
+    CK(cudaMemsetAsync(rprev, 0, nu * 8, st));
+    int parity = 0;
+    uint64_t rounds = 0;
+    const uint64_t max_rounds = nu + 2;
+    for (;;) {
+        P.parity = parity;
+        CK(cudaMemsetAsync(sc.changed.p, 0, 4, st));
+        LAUNCH(k_place_round, grid_for(nu, 256), 256, 0, st, P, rprev, rnext,
+               sc.changed.as<int>());
+        LAUNCH(k_place_clear, grid_for(nu, 256), 256, 0, st, P, rprev);
+        ++rounds;
+        std::swap(rprev, rnext);
+        parity ^= 1;
+        int rc = read_small(sc, sc.changed.p, 4, st);
+        if (rc) return rc;
+        if (((int *)sc.h_small)[0] == 0) break;
+        if (rounds > max_rounds) return set_err(PSTF_E_CUDA, "placement did not converge");
+    }
+    /* rprev now holds the fixpoint; the last round wrote hold[parity ^ 1]... after the swap the
+     * array written last is "prev" for parity, i.e. hold[parity] (cleared in k_commit) */
+    P.parity = parity ^ 1;
+    LAUNCH(k_commit, grid_for(nu, 256), 256, 0, st, P, rprev, U.ukey, U.ucalls, U.usum,
+           mode == PSTF_MODE_ATOMIC ? 1 : 0);
+    for (int i = 0; i < nf; ++i)
+        if (fs[i]) fs[i]->rounds_last = rounds;
+
+    /* 5. ORDERED / SEQUENTIAL: sequential fold per slot */
+    if (mode != PSTF_MODE_ATOMIC) {
+        ENSURE(sc.ftgt, n * 8);
+        ENSURE(sc.fperm, n * 4);
+        ENSURE(sc.fkey_out, n * 8);
+        ENSURE(sc.fperm_out, n * 4);
+        LAUNCH(k_fold_targets, grid_for(n, 256), 256, 0, st, perm, sc.uid.as<uint32_t>(), n, rprev,
+               U.usid, mode == PSTF_MODE_SEQUENTIAL ? 1 : 0, sc.ftgt.as<uint64_t>(),
+               sc.fperm.as<uint32_t>());
+        size_t bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, sc.ftgt.as<uint64_t>(),
+                                           sc.fkey_out.as<uint64_t>(), sc.fperm.as<uint32_t>(),
+                                           sc.fperm_out.as<uint32_t>(), (int64_t)n, 0, 64, st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, sc.ftgt.as<uint64_t>(),
+                                           sc.fkey_out.as<uint64_t>(), sc.fperm.as<uint32_t>(),
+                                           sc.fperm_out.as<uint32_t>(), (int64_t)n, 0, 64, st));
+        g_launches.fetch_add(4, std::memory_order_relaxed);
+        LAUNCH(k_fold, grid_for(n, 256), 256, 0, st, pend, sc.fkey_out.as<uint64_t>(),
+               sc.fperm_out.as<uint32_t>(), n, S);
+    }
+    return PSTF_OK;
+}
+
+static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t st) {
+    ENSURE(sc.pend, cap * sizeof(PendRec));
+    ENSURE(sc.pend_count, 8);
+    if (with_seq) ENSURE(sc.pend_seq, cap * 8);
+    CK(cudaMemsetAsync(sc.pend_count.p, 0, 8, st));
+    return PSTF_OK;
+}
+
+static bool same_quant(const pstf_field_config &a, const pstf_field_config &b) {
+    return a.base_cell_size == b.base_cell_size && a.level_select_k == b.level_select_k &&
+           a.max_level == b.max_level;
+}
+
+static int check_config(const pstf_field_config *c) {
+    if (!c) return set_err(PSTF_E_INVALID, "config is NULL");
+    if (c->capacity_log2 < 1 || c->capacity_log2 > 30)
+        return set_err(PSTF_E_INVALID, "capacity_log2 must be in [1, 30]");
+    if (c->max_level < 0 || c->max_level > 62)
+        return set_err(PSTF_E_INVALID, "max_level must be in [0, 62]");
+    if (c->probe_window < 1) return set_err(PSTF_E_INVALID, "probe_window must be >= 1");
+    if (c->kind > 3) return set_err(PSTF_E_INVALID, "unknown field kind");
+    return PSTF_OK;
+}
+
+/* ========================================================================================== */
+/* C ABI                                                                                       */
+
+extern "C" {
+
+int pstf_abi_version(void) { return PSTF_ABI_VERSION; }
+const char *pstf_last_error(void) { return g_last_error.c_str(); }
+uint64_t pstf_kernel_launch_count(void) { return g_launches.load(); }
+
+int pstf_field_create(const pstf_field_config *config, int device, pstf_field **out) {
+    if (!out) return set_err(PSTF_E_INVALID, "out is NULL");
+    *out = nullptr;
+    int rc = check_config(config);
+    if (rc) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+        return set_err(PSTF_E_CUDA, "no CUDA device available (the field cache has no CPU path)");
+    if (device < 0 || device >= ndev) return set_err(PSTF_E_INVALID, "bad device ordinal");
+    CK(cudaSetDevice(device));
+    pstf_field *f = new (std::nothrow) pstf_field();
+    if (!f) return set_err(PSTF_E_NOMEM, "host allocation failed");
+    f->cfg = *config;
+    f->device = device;
+    const uint64_t cap = 1ull << config->capacity_log2;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    size_t o_chk = take(cap * 4), o_com = take(cap * 32), o_acc = take(cap * 32),
+           o_keyf = take(cap * sizeof(KeyFields)), o_last = take(cap * 4), o_tmark = take(cap * 4),
+           o_touched = take(cap * 4), o_h0 = take(cap * 4), o_h1 = take(cap * 4),
+           o_ctr = take(C_NUM * 8), o_sum = take(8);
+    cudaError_t e = cudaMalloc(&f->arena, off);
+    if (e != cudaSuccess) {
+        delete f;
+        return set_err(PSTF_E_NOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+    }
+    char *base = (char *)f->arena;
+    DevStore &d = f->d;
+    memset(&d, 0, sizeof(d));
+    d.chk = (uint32_t *)(base + o_chk);
+    d.com = (double4 *)(base + o_com);
+    d.acc = (double4 *)(base + o_acc);
+    d.keyf = (KeyFields *)(base + o_keyf);
+    d.last = (uint32_t *)(base + o_last);
+    d.tmark = (uint32_t *)(base + o_tmark);
+    d.touched = (uint32_t *)(base + o_touched);
+    d.hold0 = (uint32_t *)(base + o_h0);
+    d.hold1 = (uint32_t *)(base + o_h1);
+    d.ctr = (unsigned long long *)(base + o_ctr);
+    d.cn_sum = (double *)(base + o_sum);
+    d.mask = (uint32_t)(cap - 1);
+    d.window = config->probe_window;
+    d.kp.base_cell_size = config->base_cell_size;
+    d.kp.level_select_k = config->level_select_k;
+    d.kp.max_level = config->max_level;
+    d.t_max = config->t_max;
+    d.blend = config->blend;
+    d.evict_age = config->evict_age_frames;
+    /* value-initialised slots (field.cpp:232: make_unique<Slot[]>) */
+    e = cudaMemset(f->arena, 0, off);
+    if (e == cudaSuccess) e = cudaMemset(d.hold0, 0xff, cap * 4);
+    if (e == cudaSuccess) e = cudaMemset(d.hold1, 0xff, cap * 4);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(f->arena);
+        delete f;
+        return set_err(PSTF_E_CUDA, cudaGetErrorString(e));
+    }
+    *out = f;
+    return PSTF_OK;
+}
+
+int pstf_field_destroy(pstf_field *f) {
+    if (!f) return PSTF_OK;
+    cudaSetDevice(f->device);
+    cudaDeviceSynchronize();
+    if (f->arena) cudaFree(f->arena);
+    delete f;
+    return PSTF_OK;
+}
+
+int pstf_field_get_config(const pstf_field *f, pstf_field_config *out) {
+    if (!f || !out) return set_err(PSTF_E_INVALID, "NULL argument");
+    *out = f->cfg;
+    return PSTF_OK;
+}
+
+int pstf_select_level(const pstf_field *f, const double *footprint, int32_t *level, uint64_t n,
+                      void *stream) {
+    if (!f || (!footprint && n) || (!level && n)) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    LAUNCH(k_select_level, grid_for(n, 256), 256, 0, (cudaStream_t)stream, f->d.kp, footprint,
+           level, n);
+    return PSTF_OK;
+}
+
+int pstf_key_for(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
+                 const int32_t *level, uint64_t n, pstf_key *keys, void *stream) {
+    if (!f || !pos || !dir || (n && (!level || !keys))) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    LAUNCH(k_key_for, grid_for(n, 256), 256, 0, (cudaStream_t)stream, f->d.kp, *pos, *dir, level,
+           n, keys);
+    return PSTF_OK;
+}
+
+int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *value,
+                     const double *w, const uint8_t *is_counter, uint64_t n, int mode,
+                     void *stream) {
+    if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (mode < 0 || mode > 2) return set_err(PSTF_E_INVALID, "bad mode");
+    if (!n) return PSTF_OK;
+    if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "batch too large");
+    CK(cudaSetDevice(f->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch &sc = f->sc;
+    ApplyArgs a;
+    a.s = dev_view(f);
+    a.keys = keys;
+    a.vr = value ? value->x : nullptr;
+    a.vg = value ? value->y : nullptr;
+    a.vb = value ? value->z : nullptr;
+    a.w = w;
+    a.isc = is_counter;
+    a.n = n;
+    int rc = ensure_pending(sc, n, mode == PSTF_MODE_SEQUENTIAL, st);
+    if (rc) return rc;
+    uint64_t known = (uint64_t)-1;
+    if (mode == PSTF_MODE_ATOMIC) {
+        LAUNCH(k_apply_atomic, grid_for(n, 256), 256, 0, st, a, sc.pend.as<PendRec>(),
+               sc.pend_count.as<unsigned long long>(), n);
+    } else {
+        ENSURE(sc.valid, n * 4);
+        ENSURE(sc.scan, n * 4);
+        LAUNCH(k_apply_flags, grid_for(n, 256), 256, 0, st, a, sc.valid.as<uint32_t>());
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sc.valid.as<uint32_t>(),
+                                         sc.scan.as<uint32_t>(), (int64_t)n, st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, sc.valid.as<uint32_t>(),
+                                         sc.scan.as<uint32_t>(), (int64_t)n, st));
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+        LAUNCH(k_apply_records, grid_for(n, 256), 256, 0, st, a, sc.valid.as<uint32_t>(),
+               sc.scan.as<uint32_t>(), sc.pend.as<PendRec>(),
+               mode == PSTF_MODE_SEQUENTIAL ? sc.pend_seq.as<uint64_t>() : nullptr);
+        uint32_t last[2];
+        rc = read_small(sc, sc.scan.as<uint32_t>() + (n - 1), 4, st);
+        if (rc) return rc;
+        last[0] = ((uint32_t *)sc.h_small)[0];
+        rc = read_small(sc, sc.valid.as<uint32_t>() + (n - 1), 4, st);
+        if (rc) return rc;
+        last[1] = ((uint32_t *)sc.h_small)[0];
+        known = (uint64_t)last[0] + last[1];
+    }
+    pstf_field *fs[1] = {f};
+    return resolve_pending(sc, fs, 1, mode, known, st);
+}
+
+int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
+                     const double *footprint, const int32_t *level, uint64_t n, double *value_r,
+                     double *value_g, double *value_b, uint8_t *valid, uint8_t *fallback,
+                     int32_t *out_level, void *stream) {
+    if (!f || !pos || !dir) return set_err(PSTF_E_INVALID, "NULL argument");
+    if ((footprint == nullptr) == (level == nullptr))
+        return set_err(PSTF_E_INVALID, "exactly one of footprint / level must be given");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    LAUNCH(k_query, grid_for(n, 256), 256, 0, (cudaStream_t)stream, dev_view(f), *pos, *dir,
+           footprint, level, n, value_r, value_g, value_b, valid, fallback, out_level);
+    return PSTF_OK;
+}
+
+int pstf_field_end_frame(pstf_field *f, void *stream) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    DevStore s = dev_view(f);
+    const unsigned g = (unsigned)sm_count() * 4;
+    CK(cudaMemsetAsync(&s.ctr[C_EVICTED], 0, 8, st));
+    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, s);
+    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, s);
+    const unsigned long long cap = (unsigned long long)s.mask + 1ull;
+    const unsigned ge = std::min<unsigned>(grid_for(cap, 256), g);
+    LAUNCH(k_evict, ge, 256, 0, st, s);
+    /* roll the frame: keep the touched count for stats, clear per-frame scratch */
+    CK(cudaMemcpyAsync(&s.ctr[C_TOUCHED_LAST], &s.ctr[C_TOUCHED_N], 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(s.cn_sum, 0, 8, st));
+    CK(cudaMemsetAsync(&s.ctr[C_CN_COUNT], 0, 8, st));
+    CK(cudaMemsetAsync(&s.ctr[C_TOUCHED_N], 0, 8, st));
+    f->frame += 1;
+    return PSTF_OK;
+}
+
+int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    unsigned g = std::min<unsigned>(grid_for(cap, 256), (unsigned)sm_count() * 8);
+    if (aabb)
+        LAUNCH(k_invalidate, g, 256, 0, (cudaStream_t)stream, f->d, 1, aabb[0], aabb[1], aabb[2],
+               aabb[3], aabb[4], aabb[5]);
+    else
+        LAUNCH(k_invalidate, g, 256, 0, (cudaStream_t)stream, f->d, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0);
+    return PSTF_OK;
+}
+
+int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out) {
+    if (!f || !out) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    unsigned long long c[C_NUM];
+    CK(cudaMemcpy(c, f->d.ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    out->frame = f->frame;
+    out->rejected = c[C_REJECTED];
+    out->dropped = c[C_DROPPED];
+    out->internal_errors = c[C_INTERNAL];
+    out->live = c[C_LIVE];
+    out->touched_last = c[C_TOUCHED_LAST];
+    out->new_keys_last = c[C_NEW_KEYS];
+    out->evicted_last = c[C_EVICTED];
+    out->placement_rounds_last = f->rounds_last;
+    return PSTF_OK;
+}
+
+int pstf_field_weighted_mean(pstf_field *f, double out[3]) {
+    if (!f || !out) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    Scratch &sc = f->sc;
+    ENSURE(sc.ranges, 64);
+    CK(cudaMemset(sc.ranges.p, 0, 32));
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    unsigned g = std::min<unsigned>(grid_for(cap, 256), (unsigned)sm_count() * 8);
+    LAUNCH(k_weighted_mean, g, 256, 0, (cudaStream_t)0, f->d, sc.ranges.as<double>());
+    double h[4];
+    CK(cudaMemcpy(h, sc.ranges.p, 32, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < 3; ++c) out[c] = h[3] > 0.0 ? h[c] / h[3] : 0.0;
+    return PSTF_OK;
+}
+
+static int snapshot_device(pstf_field *f, uint64_t *count, pstf_snapshot_record **dev_sorted) {
+    Scratch &sc = f->sc;
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    CK(cudaDeviceSynchronize());
+    unsigned long long live = 0;
+    CK(cudaMemcpy(&live, &f->d.ctr[C_LIVE], 8, cudaMemcpyDeviceToHost));
+    ENSURE(sc.snap, (live + 1) * 2 * sizeof(pstf_snapshot_record));
+    ENSURE(sc.pend_count, 8);
+    CK(cudaMemset(sc.pend_count.p, 0, 8));
+    pstf_snapshot_record *tmp = sc.snap.as<pstf_snapshot_record>();
+    pstf_snapshot_record *sorted = tmp + (live + 1);
+    LAUNCH(k_snap_gather, grid_for(cap, 256), 256, 0, (cudaStream_t)0, f->d, tmp,
+           sc.pend_count.as<unsigned long long>());
+    unsigned long long n = 0;
+    CK(cudaMemcpy(&n, sc.pend_count.p, 8, cudaMemcpyDeviceToHost));
+    if (n != live) return set_err(PSTF_E_CUDA, "live counter disagrees with the table");
+    if (n) {
+        ENSURE(sc.words, n * 3 * 8);
+        LAUNCH(k_snap_words, grid_for(n, 256), 256, 0, (cudaStream_t)0, tmp, n,
+               sc.words.as<uint64_t>());
+        int bb[3] = {0, 0, 0};
+        uint32_t *perm = nullptr;
+        int rc = sort_multiword(sc, sc.words.as<uint64_t>(), bb, 3, n, &perm, 0);
+        if (rc) return rc;
+        LAUNCH(k_snap_permute, grid_for(n, 256), 256, 0, (cudaStream_t)0, tmp, perm, n, sorted);
+    }
+    *count = n;
+    *dev_sorted = sorted;
+    return PSTF_OK;
+}
+
+int pstf_field_snapshot(pstf_field *f, pstf_snapshot_record *records, uint64_t cap,
+                        uint64_t *count) {
+    if (!f || !count || (cap && !records)) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    uint64_t n = 0;
+    pstf_snapshot_record *d = nullptr;
+    int rc = snapshot_device(f, &n, &d);
+    if (rc) return rc;
+    *count = n;
+    uint64_t m = std::min(n, cap);
+    if (m) CK(cudaMemcpy(records, d, m * sizeof(pstf_snapshot_record), cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
+int pstf_field_dump_snapshot(pstf_field *f, const char *path) {
+    if (!f || !path) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    uint64_t n = 0;
+    pstf_snapshot_record *d = nullptr;
+    int rc = snapshot_device(f, &n, &d);
+    if (rc) return rc;
+    std::vector<pstf_snapshot_record> h(n);
+    if (n) CK(cudaMemcpy(h.data(), d, n * sizeof(pstf_snapshot_record), cudaMemcpyDeviceToHost));
+    FILE *fp = fopen(path, "wb");
+    if (!fp) /* field.cpp:340-341 */
+        return set_err(PSTF_E_IO, std::string("cannot open snapshot file '") + path + "' for writing");
+    const char magic[8] = {'P', 'S', 'T', 'F', 'S', 'N', 'A', 'P'};
+    uint32_t version = 1, kind = f->cfg.kind;
+    uint64_t cnt = n;
+    bool ok = fwrite(magic, 1, 8, fp) == 8 && fwrite(&version, 4, 1, fp) == 1 &&
+              fwrite(&kind, 4, 1, fp) == 1 && fwrite(&cnt, 8, 1, fp) == 1;
+    for (uint64_t i = 0; ok && i < n; ++i) { /* 60-byte packed records, field.cpp:348-355 */
+        const pstf_snapshot_record &r = h[i];
+        ok = fwrite(&r.level, 4, 1, fp) == 1 && fwrite(r.cell, 4, 3, fp) == 3 &&
+             fwrite(r.dir_cell, 4, 2, fp) == 2 && fwrite(&r.checksum, 4, 1, fp) == 1 &&
+             fwrite(r.value, 8, 3, fp) == 3 && fwrite(&r.c_old, 8, 1, fp) == 1;
+    }
+    if (fclose(fp) != 0) ok = false;
+    if (!ok) return set_err(PSTF_E_IO, std::string("write failed: ") + path);
+    return PSTF_OK;
+}
+
+int pstf_read_snapshot(const char *path, pstf_snapshot_record *records, uint64_t cap,
+                       uint64_t *count, uint32_t *kind_out) {
+    if (!path || !count) return set_err(PSTF_E_INVALID, "NULL argument");
+    FILE *fp = fopen(path, "rb");
+    if (!fp) return set_err(PSTF_E_IO, std::string("cannot open snapshot file '") + path + "'");
+    char magic[8];
+    uint32_t version = 0, kind = 0;
+    uint64_t n = 0;
+    if (fread(magic, 1, 8, fp) != 8 || memcmp(magic, "PSTFSNAP", 8) != 0) {
+        fclose(fp);
+        return set_err(PSTF_E_FORMAT, std::string("'") + path + "': not a field snapshot");
+    }
+    if (fread(&version, 4, 1, fp) != 1 || fread(&kind, 4, 1, fp) != 1 || fread(&n, 8, 1, fp) != 1) {
+        fclose(fp);
+        return set_err(PSTF_E_FORMAT, std::string("'") + path + "': truncated snapshot");
+    }
+    if (version != 1) {
+        fclose(fp);
+        return set_err(PSTF_E_FORMAT, std::string("'") + path + "': unsupported snapshot version");
+    }
+    bool ok = true;
+    for (uint64_t i = 0; i < n; ++i) {
+        pstf_snapshot_record r;
+        memset(&r, 0, sizeof(r));
+        ok = fread(&r.level, 4, 1, fp) == 1 && fread(r.cell, 4, 3, fp) == 3 &&
+             fread(r.dir_cell, 4, 2, fp) == 2 && fread(&r.checksum, 4, 1, fp) == 1 &&
+             fread(r.value, 8, 3, fp) == 3 && fread(&r.c_old, 8, 1, fp) == 1;
+        if (!ok) break;
+        if (i < cap && records) records[i] = r;
+    }
+    fclose(fp);
+    if (!ok) return set_err(PSTF_E_FORMAT, std::string("'") + path + "': truncated snapshot");
+    *count = n;
+    if (kind_out) *kind_out = kind;
+    return PSTF_OK;
+}
+
+int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_record *out) {
+    if (!f || (count && !out)) return set_err(PSTF_E_INVALID, "NULL argument");
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    if (begin > cap || count > cap - begin) return set_err(PSTF_E_INVALID, "slot range out of bounds");
+    if (!count) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<uint32_t> chk(count), last(count);
+    std::vector<double4> com(count), acc(count);
+    std::vector<KeyFields> kf(count);
+    CK(cudaMemcpy(chk.data(), f->d.chk + begin, count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(last.data(), f->d.last + begin, count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(com.data(), f->d.com + begin, count * 32, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(acc.data(), f->d.acc + begin, count * 32, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(kf.data(), f->d.keyf + begin, count * sizeof(KeyFields), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < count; ++i) {
+        pstf_slot_record &r = out[i];
+        memset(&r, 0, sizeof(r));
+        r.checksum = chk[i];
+        r.level = kf[i].level;
+        r.cell[0] = kf[i].c0;
+        r.cell[1] = kf[i].c1;
+        r.cell[2] = kf[i].c2;
+        r.dir_cell[0] = kf[i].d0;
+        r.dir_cell[1] = kf[i].d1;
+        r.value_old[0] = com[i].x;
+        r.value_old[1] = com[i].y;
+        r.value_old[2] = com[i].z;
+        r.c_old = com[i].w;
+        r.accum[0] = acc[i].x;
+        r.accum[1] = acc[i].y;
+        r.accum[2] = acc[i].z;
+        r.c_new = acc[i].w;
+        r.last_touched = last[i];
+    }
+    return PSTF_OK;
+}
+
+static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                         const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
+                         uint32_t fli_mask, int mode, cudaStream_t st) {
+    VPArgs a;
+    memset(&a, 0, sizeof(a));
+    pstf_field *fs[4] = {lo, loe, fli, li};
+    a.st = stores4(fs, 4);
+    a.has_li = li != nullptr;
+    a.same_lo_loe = same_quant(lo->cfg, loe->cfg);
+    a.same_fli_lo = same_quant(fli->cfg, lo->cfg);
+    a.same_li_fli = li ? same_quant(li->cfg, fli->cfg) : 1;
+    a.loe_mask = loe_mask;
+    a.fli_mask = fli_mask;
+    a.v = *v;
+    a.n = n;
+    a.pend = lo->sc.pend.as<PendRec>();
+    a.pend_count = lo->sc.pend_count.as<unsigned long long>();
+    a.pend_cap = lo->sc.pend.bytes / sizeof(PendRec);
+    if (mode == PSTF_MODE_ATOMIC)
+        LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
+    else
+        LAUNCH(k_vertex_pass<PSTF_MODE_ORDERED>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
+    return PSTF_OK;
+}
+
+static int vertex_checks(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li, int mode) {
+    if (!lo || !loe || !fli) return set_err(PSTF_E_INVALID, "lo, loe and fli stores are required");
+    if (mode != PSTF_MODE_ATOMIC && mode != PSTF_MODE_ORDERED)
+        return set_err(PSTF_E_INVALID, "vertex pass supports ATOMIC and ORDERED modes");
+    if (loe->device != lo->device || fli->device != lo->device || (li && li->device != lo->device))
+        return set_err(PSTF_E_INVALID, "all stores must live on one device");
+    return PSTF_OK;
+}
+
+static uint64_t records_per_vertex(int mode, bool li) {
+    return mode == PSTF_MODE_ATOMIC ? (li ? 5 : 4) : (li ? 12 : 10);
+}
+
+int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                     const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask, uint32_t fli_mask,
+                     int mode, void *stream) {
+    int rc = vertex_checks(lo, loe, fli, li, mode);
+    if (rc) return rc;
+    if (!v) return set_err(PSTF_E_INVALID, "NULL vertex record");
+    CK(cudaSetDevice(lo->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
+    if (rc) return rc;
+    if (n) {
+        rc = vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, mode, st);
+        if (rc) return rc;
+    }
+    pstf_field *fs[4] = {lo, loe, fli, li};
+    return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
+}
+
+void pstf_vertex_soa_from_buffer(const double *b, uint64_t n, pstf_vertex_soa *o) {
+    auto v3 = [&](int k) {
+        pstf_vec3_soa s;
+        s.x = b + (uint64_t)k * n;
+        s.y = b + (uint64_t)(k + 1) * n;
+        s.z = b + (uint64_t)(k + 2) * n;
+        return s;
+    };
+    o->position = v3(PS_POS);
+    o->wo = v3(PS_WO);
+    o->wi = v3(PS_WI);
+    o->next_position = v3(PS_NPOS);
+    o->nee_dir = v3(PS_NDIR);
+    o->footprint = b + (uint64_t)PS_FP * n;
+    o->next_footprint = b + (uint64_t)PS_NFP * n;
+    o->ratio = b + (uint64_t)PS_RATIO * n;
+    o->next_emis_mis_weight = b + (uint64_t)PS_NMIS * n;
+    o->emission_here = v3(PS_EMIS);
+    o->f = v3(PS_F);
+    o->next_emission = v3(PS_NEMIS);
+    o->nee_loe = v3(PS_NEELOE);
+    o->nee_fli = v3(PS_NEEFLI);
+    o->flags = (const uint32_t *)(b + (uint64_t)PS_NUM_F64 * n);
+}
+
+/* Host-resident vertex arrays: chunked H2D on a copy stream (double-buffered staging) overlapped
+ * with phase 1 of the previous chunk on the compute stream; phase 2 runs once at the end so
+ * every lookup sees the frame-start table (Jacobi). */
+int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                          const pstf_vertex_soa *hv, uint64_t n, uint32_t loe_mask,
+                          uint32_t fli_mask, int mode, void *stream) {
+    int rc = vertex_checks(lo, loe, fli, li, mode);
+    if (rc) return rc;
+    if (!hv) return set_err(PSTF_E_INVALID, "NULL vertex record");
+    CK(cudaSetDevice(lo->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
+    if (rc) return rc;
+    const uint64_t chunk = std::min<uint64_t>(n, 1ull << 21);
+    static thread_local cudaStream_t cs = nullptr;
+    static thread_local cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+    static thread_local DBuf stage[2];
+    if (!cs) {
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&ev_copy[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
+        }
+    }
+    const size_t per = PS_BYTES_PER_VERTEX;
+    for (int b = 0; b < 2; ++b) ENSURE(stage[b], chunk * per + 64);
+    /* the copy stream must not run ahead of earlier work on the compute stream */
+    CK(cudaEventRecord(ev_done[0], st));
+    CK(cudaStreamWaitEvent(cs, ev_done[0], 0));
+    CK(cudaEventRecord(ev_done[1], st));
+    for (uint64_t off = 0, k = 0; off < n; off += chunk, ++k) {
+        const int b = (int)(k & 1);
+        const uint64_t m = std::min(chunk, n - off);
+        CK(cudaStreamWaitEvent(cs, ev_done[b], 0));
+        double *d = stage[b].as<double>();
+        const double *src3[15][3] = {};
+        (void)src3;
+        const pstf_vec3_soa *v3s[10] = {&hv->position, &hv->wo, &hv->wi, &hv->next_position,
+                                        &hv->nee_dir, &hv->emission_here, &hv->f,
+                                        &hv->next_emission, &hv->nee_loe, &hv->nee_fli};
+        const int v3f[10] = {PS_POS, PS_WO, PS_WI, PS_NPOS, PS_NDIR, PS_EMIS, PS_F, PS_NEMIS,
+                             PS_NEELOE, PS_NEEFLI};
+        for (int q = 0; q < 10; ++q) {
+            const double *c[3] = {v3s[q]->x, v3s[q]->y, v3s[q]->z};
+            for (int j = 0; j < 3; ++j)
+                CK(cudaMemcpyAsync(d + (uint64_t)(v3f[q] + j) * m, c[j] + off, m * 8,
+                                   cudaMemcpyHostToDevice, cs));
+        }
+        const double *sc1[4] = {hv->footprint, hv->next_footprint, hv->ratio, hv->next_emis_mis_weight};
+        const int sf[4] = {PS_FP, PS_NFP, PS_RATIO, PS_NMIS};
+        for (int q = 0; q < 4; ++q)
+            CK(cudaMemcpyAsync(d + (uint64_t)sf[q] * m, sc1[q] + off, m * 8, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(d + (uint64_t)PS_NUM_F64 * m, hv->flags + off, m * 4,
+                           cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(ev_copy[b], cs));
+        CK(cudaStreamWaitEvent(st, ev_copy[b], 0));
+        pstf_vertex_soa dv;
+        pstf_vertex_soa_from_buffer(d, m, &dv);
+        rc = vertex_phase1(lo, loe, fli, li, &dv, m, loe_mask, fli_mask, mode, st);
+        if (rc) return rc;
+        CK(cudaEventRecord(ev_done[b], st));
+    }
+    pstf_field *fs[4] = {lo, loe, fli, li};
+    return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
+}
+
+int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, double *value_r,
+                   double *value_g, double *value_b, uint8_t *valid, void *stream) {
+    if (!loe || !v) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(loe->device));
+    LAUNCH(k_cv_lookup, grid_for(n, 256), 256, 0, (cudaStream_t)stream, dev_view(loe), *v, n,
+           value_r, value_g, value_b, valid);
+    return PSTF_OK;
+}
+
+int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iteration,
+                        double cam_shift_x, double *buffer, void *stream) {
+    if (width <= 0 || height <= 0 || bounces <= 0 || !buffer)
+        return set_err(PSTF_E_INVALID, "bad synthetic stream arguments");
+    ps_params P;
+    P.width = width;
+    P.height = height;
+    P.bounces = bounces;
+    P.seed = seed;
+    P.iter = iteration;
+    P.cam_shift_x = cam_shift_x;
+    uint64_t n_paths = (uint64_t)width * height;
+    LAUNCH(k_synth, grid_for(n_paths, 128), 128, 0, (cudaStream_t)stream, P, buffer,
+           n_paths * (uint64_t)bounces);
+    return PSTF_OK;
+}
+
+} // extern "C"
