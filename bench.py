@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — PSTF field cache (keygen + insert + blend + lookup) on B200.
+
+Workload (BASELINE.json configs[1]): a 1920x1080 1 spp x 4-bounce
+synthetic Cornell vertex stream (8,294,400 vertices/iteration, 276 B/vertex canonical fp64 SoA
+record), spatio-directional keys, three field stores (Lo, Lo\\E, FLi) of 2^22 slots each,
+base cell = diameter/256.  One step = one progressive iteration: the fused onVertex pass
+(lookups on committed state + key generation + counter/accumulate updates incl. deterministic
+placement of new keys) followed by endFrame on the three stores (blend + cap + eviction).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+`value` is device-timed with CUDA events (inputs resident in HBM, 8 distinct iteration streams
+of 2.29 GB each cycled, i.e. inputs larger than L2); `e2e` is the same metric through the C ABI
+with pinned HOST vertex arrays copied in every step; `roofline` covers the dominant kernel
+(k_vertex_pass) and `step_roofline` the whole iteration against SURVEY.md §8d's algorithmic
+bytes (276 B/vertex + 172 B/touched cell).  `--impl reference` times the reference's own
+FieldStore (oracle/_ref, compiled from /root/reference) driven by the onVertex replay on all
+host cores.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filtered path vertices/sec (insert+blend+lookup) 1080p×4 bounces; % HBM roofline"
+UNIT = "vertices/s"
+BYTES_PER_VERTEX = 276
+BYTES_PER_TOUCHED = 172
+DIAMETER = math.sqrt(12.0)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--bounces", type=int, default=4)
+    p.add_argument("--capacity-log2", type=int, default=22)
+    p.add_argument("--streams", type=int, default=8)
+    p.add_argument("--mode", default="atomic", choices=["atomic", "ordered"])
+    p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--cpu-seconds", type=float, default=20.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [s for s in self.samples if s[6].isdigit() and int(s[6]) > 0] or self.samples
+        sm = sorted(float(s[0]) for s in load if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()),
+                 default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in load for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(load)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ---------------------------------------------------------------- CPU reference leg
+def cpu_reference_run(args, steps, warmup, budget_s):
+    """The reference FieldStore (oracle/_ref) + onVertex replay, non-deterministic mode on all host
+    threads (EstimatorRun::renderFrame threading, estimators.cpp:566-608).  Each step replays a
+    path sample (all bounces of a random subset of the frame's paths) and runs endFrame on the
+    three stores; the sample is sized so warmup+steps fit the time budget."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    kind = "reference" if po.ref_available() else "port"
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    base = DIAMETER / 256.0
+    W, H, B = args.width, args.height, args.bounces
+    n_paths = W * H
+    n_full = n_paths * B
+    gen_threads = max(1, threads)
+    bufs = [po.synth_generate(W, H, B, iteration=i, threads=gen_threads)[0] for i in range(2)]
+
+    def sample(buf, frac, seed):
+        k = max(1, int(n_paths * frac))
+        rng = np.random.default_rng(seed)
+        paths = np.sort(rng.choice(n_paths, size=k, replace=False))
+        idx = (np.arange(B)[:, None] * n_paths + paths[None, :]).reshape(-1)
+        f64, flags = po.soa_views(buf, n_full)
+        m = len(idx)
+        out = np.zeros(34 * m + (m + 1) // 2, np.float64)
+        out[:34 * m] = f64[:, idx].reshape(-1)
+        out[34 * m:].view(np.uint32)[:m] = flags[idx]
+        return out, m
+
+    if kind == "reference":
+        mk = lambda k: po.RefStore(po.Config.make(kind=k, capacity_log2=args.capacity_log2,
+                                                  base_cell_size=base))
+    else:
+        mk = lambda k: po.OracleStore(po.Config.make(kind=k, capacity_log2=args.capacity_log2,
+                                                     base_cell_size=base))
+    stores = [mk(k) for k in (po.KIND_LO, po.KIND_LOE, po.KIND_FLI)] + [None]
+
+    def step(sbuf, m):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            po.vertex_pass_ref(*stores, sbuf, m, deterministic=False, threads=threads,
+                               chunk=W)
+        else:
+            po.vertex_pass_oracle(*stores, sbuf, m, deterministic=False)
+        t1 = time.perf_counter()
+        for s in stores[:3]:
+            s.end_frame()
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1
+
+    # calibrate on a small sample, then size the sample to the budget
+    cal, cm = sample(bufs[0], 1.0 / 64, 1)
+    tp, te = step(cal, cm)
+    rate = cm / max(tp, 1e-9)
+    per_step = budget_s / max(1, steps + warmup)
+    frac = max(1.0 / 64, min(1.0, (per_step - te) * rate / n_full)) if per_step > te else 1.0 / 64
+    samples = [sample(bufs[i % 2], frac, 100 + i) for i in range(2)]
+    for i in range(warmup):
+        step(*samples[i % 2])
+    tot_v, tot_t, t_pass, t_ef = 0, 0.0, 0.0, 0.0
+    for i in range(steps):
+        sbuf, m = samples[i % 2]
+        a, b = step(sbuf, m)
+        tot_v += m
+        tot_t += a + b
+        t_pass += a
+        t_ef += b
+    value = tot_v / tot_t
+    return {
+        "value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
+        "kind": kind,
+        "sample": (f"{frac:.4f} of the {n_full}-vertex config-2 iteration per step "
+                   f"({samples[0][1]} vertices = all {B} bounces of a random path subset), "
+                   f"{steps} steps after {warmup} warm-up; each step = onVertex replay "
+                   f"({'non-deterministic, ' + str(threads) + ' std::threads' if kind == 'reference' else '1 thread'}) "
+                   f"+ endFrame x3 at 2^{args.capacity_log2}; pass {t_pass / steps * 1e3:.1f} ms, "
+                   f"endFrame {t_ef / steps * 1e3:.1f} ms per step; full-iteration extrapolation "
+                   f"{n_full / (t_pass / steps * n_full / samples[0][1] + t_ef / steps):.4g} v/s"),
+        "ms_per_step": tot_t / steps * 1e3,
+    }
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    r = cpu_reference_run(args, args.steps, args.warmup, budget_s=150.0)
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex "
+                               "stream, Lo/LoE/FLi stores x 2^22 slots (reference FieldStore on "
+                               "host cores)", "vertices_per_iter": args.width * args.height * args.bounces},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- B200 leg
+def run_b200(args):
+    import numpy as np
+    import torch
+    import paper_2005_07547_b200 as pb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, H, B = args.width, args.height, args.bounces
+    base = DIAMETER / 256.0
+    mode = pb.MODE_ATOMIC if args.mode == "atomic" else pb.MODE_ORDERED
+    stores = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=args.capacity_log2,
+                                                base_cell_size=base), device=local)
+              for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
+    n = W * H * B
+    S = max(1, args.streams)
+    bufs = []
+    for i in range(S):
+        b, _ = pb.synth_generate(W, H, B, iteration=i + 1000 * rank)
+        bufs.append(b)
+    torch.cuda.synchronize()
+
+    touched = []
+
+    def step(i, record=False):
+        pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
+        for s in stores:
+            s.end_frame()
+        if record:
+            touched.append(sum(s.stats()["touched_last"] for s in stores))
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = pb.kernel_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pb.profile_collect()
+    with ClockSampler(local) as clk:
+        pb.profile_enable(True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for i in range(args.steps):
+            step(args.warmup + i, record=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        pb.profile_enable(False)
+    launches = pb.kernel_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    prof = pb.profile_collect()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_vertices = n * args.steps * world
+    value = total_vertices / (ms / 1e3)
+    ms_step = ms / args.steps
+    st = [s.stats() for s in stores]
+
+    # roofline: dominant kernel = the fused vertex pass (k_vertex_pass)
+    peak, peak_src = peaks()
+    vp = [(k, v) for k, v in prof.items() if k.startswith("k_vertex_pass")]
+    vp_ms, vp_n = (vp[0][1] if vp else (float("nan"), 1))
+    vp_avg = vp_ms / max(vp_n, 1)
+    vp_bytes = BYTES_PER_VERTEX * n
+    ach = vp_bytes / (vp_avg / 1e3) / 1e9
+    mean_touched = float(np.mean(touched)) if touched else 0.0
+    step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched
+    step_ach = step_bytes / (ms_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_vertex_pass_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (pstf_synth.h Cornell-box generator, IEEE-exact, seed 0x5EED)",
+        "config": {
+            "workload": "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, "
+                        "spatio-directional keys, Lo/LoE/FLi stores x 2^22 slots, base=diam/256",
+            "vertices_per_iter": n, "capacity_log2": args.capacity_log2, "stores": 3,
+            "mode": args.mode, "iteration_streams": S,
+            "l2": "inputs larger than L2 (2.29 GB per iteration stream, %d streams cycled)" % S,
+            "parallelism": "single GPU" if world == 1 else
+                           f"{world} ranks x independent image replicas (no cache exchange yet)",
+        },
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": traffic,
+                     "kernel": vp[0][0] if vp else None,
+                     "bytes_per_launch": vp_bytes, "avg_launch_ms": vp_avg,
+                     "peak_source": peak_src},
+        "step_roofline": {"achieved": step_ach, "peak": peak, "unit": "GB/s",
+                          "frac": step_ach / peak,
+                          "bytes_per_step": step_bytes, "touched_cells_per_step": mean_touched},
+        "kernels": kernels,
+        "field_stats": {k: [s[k] for s in st] for k in ("live", "dropped", "rejected",
+                                                         "new_keys_last", "touched_last",
+                                                         "placement_rounds_last")},
+        "clocks": clk.summary(),
+    }
+
+    # e2e: same metric through the C ABI with pinned HOST vertex arrays (H2D every step)
+    if not args.no_e2e:
+        hosts = [bufs[i].cpu().pin_memory() for i in range(min(2, S))]
+        E = max(1, args.e2e_steps)
+
+        def estep(i):
+            pb.vertex_pass_host(stores[0], stores[1], stores[2], None, hosts[i % len(hosts)], n,
+                                mode=mode)
+            for s in stores:
+                s.end_frame()
+            return [s.stats()["live"] for s in stores]  # D2H read of the step's result
+
+        estep(0)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(E):
+            estep(i + 1)
+        torch.cuda.synchronize()
+        et = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([et], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        line["e2e"] = {"value": n * E * world / et, "unit": UNIT,
+                       "h2d_bytes_per_step": BYTES_PER_VERTEX * n,
+                       "d2h_bytes_per_step": 3 * 8 * 11, "steps": E,
+                       "path": "pstf_vertex_pass_host (pinned host SoA, chunked H2D overlapped "
+                               "with phase 1) + pstf_field_end_frame x3 + stats readback"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_run(args, 2, 1, budget_s=args.cpu_seconds)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # report, never fail the GPU line
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                                    "sample": f"error: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

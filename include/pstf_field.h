@@ -216,6 +216,12 @@ void pstf_vertex_soa_from_buffer(const double *buffer, uint64_t n, pstf_vertex_s
 /* Number of kernels this library launched since load (bench evidence). */
 uint64_t pstf_kernel_launch_count(void);
 
+/* Per-kernel CUDA-event timing (events recorded on each launch's stream while enabled).
+ * pstf_profile_collect synchronises, aggregates by kernel name (names: n_max x 64 chars),
+ * total milliseconds and launch counts, then clears the record. */
+int pstf_profile_enable(int on);
+int pstf_profile_collect(char *names, double *ms, uint64_t *counts, int n_max, int *n_out);
+
 #ifdef __cplusplus
 }
 #endif

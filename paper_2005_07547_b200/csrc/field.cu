@@ -56,8 +56,51 @@ static int set_err(int code, const std::string &msg) {
             return set_err(PSTF_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+/* Optional per-kernel CUDA-event timing on the launching stream (bench.py roofline). */
+static std::atomic<int> g_prof{0};
+static std::mutex g_prof_mu;
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static cudaEvent_t prof_event() {
+    cudaEvent_t e = nullptr;
+    if (!g_prof_pool.empty()) {
+        e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+
+struct ProfScope {
+    const char *name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(const char *n, cudaStream_t s) : name(n), st(s) {
+        if (g_prof.load(std::memory_order_relaxed)) {
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            a = prof_event();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            cudaEvent_t b = prof_event();
+            cudaEventRecord(b, st);
+            g_prof_recs.push_back({name, a, b});
+        }
+    }
+};
+
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                                      \
     do {                                                                                    \
+        ProfScope ps_(#kernel, (stream));                                                   \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                         \
         g_launches.fetch_add(1, std::memory_order_relaxed);                                 \
         cudaError_t e_ = cudaGetLastError();                                                \
@@ -1197,9 +1240,10 @@ static int sort_multiword(Scratch &sc, const uint64_t *words, const int *begin_b
                                            (int64_t)n, begin_bits[k], 64, st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
+        { ProfScope ps_("cub::DeviceRadixSort", st);
         CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, kin, sc.ktmp1.as<uint64_t>(), pa, pb,
                                            (int64_t)n, begin_bits[k], 64, st));
-        g_launches.fetch_add(4, std::memory_order_relaxed);
+        g_launches.fetch_add(4, std::memory_order_relaxed); }
         std::swap(pa, pb);
     }
     *perm_out = pa;
@@ -1321,9 +1365,10 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
                                          sc.uid.as<uint32_t>(), (int64_t)n, st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
+        { ProfScope ps_("cub::DeviceScan", st);
         CK(cub::DeviceScan::InclusiveSum(sc.cub.p, bytes, sc.head.as<uint32_t>(),
                                          sc.uid.as<uint32_t>(), (int64_t)n, st));
-        g_launches.fetch_add(2, std::memory_order_relaxed);
+        g_launches.fetch_add(2, std::memory_order_relaxed); }
     }
     uint64_t nu;
     {
@@ -1385,9 +1430,10 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
                                            ids_in, ids, (int64_t)nu, 0, 64, st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
+        { ProfScope ps_("cub::DeviceRadixSort", st);
         CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, U.useq, sc.fkey_out.as<uint64_t>(),
                                            ids_in, ids, (int64_t)nu, 0, 64, st));
-        g_launches.fetch_add(4, std::memory_order_relaxed);
+        g_launches.fetch_add(4, std::memory_order_relaxed); }
         LAUNCH(k_rank_scatter, grid_for(nu, 256), 256, 0, st, ids, nu, sc.rank.as<uint32_t>(),
                U.ucs, sc.csr.as<uint32_t>());
         P.rank = sc.rank.as<uint32_t>();
@@ -1438,10 +1484,11 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
                                            sc.fperm_out.as<uint32_t>(), (int64_t)n, 0, 64, st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
+        { ProfScope ps_("cub::DeviceRadixSort", st);
         CK(cub::DeviceRadixSort::SortPairs(sc.cub.p, bytes, sc.ftgt.as<uint64_t>(),
                                            sc.fkey_out.as<uint64_t>(), sc.fperm.as<uint32_t>(),
                                            sc.fperm_out.as<uint32_t>(), (int64_t)n, 0, 64, st));
-        g_launches.fetch_add(4, std::memory_order_relaxed);
+        g_launches.fetch_add(4, std::memory_order_relaxed); }
         LAUNCH(k_fold, grid_for(n, 256), 256, 0, st, pend, sc.fkey_out.as<uint64_t>(),
                sc.fperm_out.as<uint32_t>(), n, S);
     }
@@ -1480,6 +1527,48 @@ extern "C" {
 int pstf_abi_version(void) { return PSTF_ABI_VERSION; }
 const char *pstf_last_error(void) { return g_last_error.c_str(); }
 uint64_t pstf_kernel_launch_count(void) { return g_launches.load(); }
+
+int pstf_profile_enable(int on) {
+    g_prof.store(on ? 1 : 0);
+    return PSTF_OK;
+}
+
+/* Synchronises on the recorded events, aggregates per kernel name, clears the record.
+ * names: n_max entries of 64 chars; ms / counts: n_max entries. */
+int pstf_profile_collect(char *names, double *ms, uint64_t *counts, int n_max, int *n_out) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<std::string> nm;
+    std::vector<double> tot;
+    std::vector<uint64_t> cnt;
+    for (auto &r : g_prof_recs) {
+        float t = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        while (k < nm.size() && nm[k] != r.name) ++k;
+        if (k == nm.size()) {
+            nm.push_back(r.name);
+            tot.push_back(0.0);
+            cnt.push_back(0);
+        }
+        tot[k] += t;
+        cnt[k] += 1;
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    int n = (int)std::min<size_t>(nm.size(), (size_t)std::max(n_max, 0));
+    for (int i = 0; i < n; ++i) {
+        if (names) {
+            strncpy(names + 64 * i, nm[i].c_str(), 63);
+            names[64 * i + 63] = 0;
+        }
+        if (ms) ms[i] = tot[i];
+        if (counts) counts[i] = cnt[i];
+    }
+    if (n_out) *n_out = n;
+    return PSTF_OK;
+}
 
 int pstf_field_create(const pstf_field_config *config, int device, pstf_field **out) {
     if (!out) return set_err(PSTF_E_INVALID, "out is NULL");
@@ -1616,9 +1705,10 @@ int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *v
                                          sc.scan.as<uint32_t>(), (int64_t)n, st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
+        { ProfScope ps_("cub::DeviceScan", st);
         CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, sc.valid.as<uint32_t>(),
                                          sc.scan.as<uint32_t>(), (int64_t)n, st));
-        g_launches.fetch_add(2, std::memory_order_relaxed);
+        g_launches.fetch_add(2, std::memory_order_relaxed); }
         LAUNCH(k_apply_records, grid_for(n, 256), 256, 0, st, a, sc.valid.as<uint32_t>(),
                sc.scan.as<uint32_t>(), sc.pend.as<PendRec>(),
                mode == PSTF_MODE_SEQUENTIAL ? sc.pend_seq.as<uint64_t>() : nullptr);

@@ -106,6 +106,8 @@ def lib():
         "pstf_cv_lookup": ([vp, vp, u64, vp, vp, vp, vp, vp], i32),
         "pstf_synth_generate": ([i32, i32, i32, u64, u64, d, vp, vp], i32),
         "pstf_vertex_soa_from_buffer": ([vp, u64, vp], None),
+        "pstf_profile_enable": ([i32], i32),
+        "pstf_profile_collect": ([vp, vp, vp, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -122,6 +124,26 @@ def _check(rc):
 
 def kernel_launch_count() -> int:
     return int(lib().pstf_kernel_launch_count())
+
+
+def profile_enable(on: bool = True):
+    """Records CUDA events around every library launch on its stream (bench instrumentation)."""
+    _check(lib().pstf_profile_enable(1 if on else 0))
+
+
+def profile_collect() -> dict:
+    """{kernel name: (total ms, launches)} since the last collect; synchronises."""
+    n_max = 128
+    names = C.create_string_buffer(64 * n_max)
+    ms = (C.c_double * n_max)()
+    cnt = (C.c_uint64 * n_max)()
+    n = C.c_int()
+    _check(lib().pstf_profile_collect(names, ms, cnt, n_max, C.byref(n)))
+    out = {}
+    for i in range(n.value):
+        nm = names.raw[64 * i:64 * (i + 1)].split(b"\0")[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def _torch():
