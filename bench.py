@@ -255,8 +255,7 @@ def run_b200(args):
 
     def step(i, record=False):
         pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
-        for s in stores:
-            s.end_frame()
+        pb.end_frame_all(stores)
         if record:
             touched.append(sum(s.stats()["touched_last"] for s in stores))
 
@@ -348,8 +347,7 @@ def run_b200(args):
         def estep(i):
             pb.vertex_pass_host(stores[0], stores[1], stores[2], None, hosts[i % len(hosts)], n,
                                 mode=mode)
-            for s in stores:
-                s.end_frame()
+            pb.end_frame_all(stores)
             return [s.stats()["live"] for s in stores]  # D2H read of the step's result
 
         estep(0)

@@ -163,6 +163,9 @@ int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_v
 
 /* endFrame() field.h:100 */
 int pstf_field_end_frame(pstf_field *f, void *stream);
+/* endFrame() on n (1..4) stores of one device in a single pair of sweeps (e.g. Lo, LoE, FLi, Li
+ * at the frame barrier, estimators.cpp:647-651); same result as n separate calls. */
+int pstf_fields_end_frame(pstf_field *const *fields, int n, void *stream);
 /* invalidate() / invalidate(const Aabb&) field.h:102-103; aabb = host double[6] {lo, hi} or NULL */
 int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream);
 

@@ -12,5 +12,5 @@ from .field import (  # noqa: F401
     FieldStore, FieldStoreConfig, FieldUpdateQueue, PstfError, SpatioDirectionalKey,
     SNAPSHOT_DTYPE, SLOT_DTYPE, KEY_DTYPE, lib, library_path, read_snapshot, synth_generate,
     vertex_pass, vertex_pass_host, cv_lookup, vertex_soa, kernel_launch_count,
-    VERTEX_BYTES, VERTEX_F64_FIELDS, profile_enable, profile_collect,
+    VERTEX_BYTES, VERTEX_F64_FIELDS, profile_enable, profile_collect, end_frame_all,
 )

@@ -13,8 +13,9 @@
  *            deterministic deferred-acceptance loop whose fixpoint is exactly the slot layout of
  *            sequential insertion in priority order (field.cpp:116-146 applied in the order of
  *            FieldUpdateQueue::apply, field.cpp:396-420); then their sums are committed.
- *   endFrame two passes over the touched-slot list (mean c_new, then blend + cap) and an
- *            age-eviction sweep when the table is more than 3/4 full (field.cpp:197-263).
+ *   endFrame two sweeps over the 8 B slot words of all stores of the batch: mean c_new of the
+ *            slots touched this frame, then blend + cap + zero accumulators, fused with the
+ *            age-eviction rule when the table is more than 3/4 full (field.cpp:197-263).
  */
 #include <cuda_runtime.h>
 
@@ -267,6 +268,12 @@ struct VPArgs {
 #define VP_BLOCK 256
 #define WARPS_PER_BLOCK (VP_BLOCK / 32)
 
+struct PendSink {
+    PendRec *pend;
+    unsigned long long *count;
+    uint64_t cap;
+};
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ bool finite3(double a, double b, double c) {
@@ -274,58 +281,65 @@ __device__ __forceinline__ bool finite3(double a, double b, double c) {
 }
 
 /* Appends records with one atomic per warp; all 32 lanes must call it. */
-__device__ __forceinline__ void warp_append(const VPArgs &a, bool want, const PendRec &r) {
+__device__ __forceinline__ void warp_append(const PendSink &a, bool want, const PendRec &r) {
     unsigned m = __ballot_sync(0xffffffffu, want);
     if (!m) return;
     unsigned lane = lane_id();
     int leader = __ffs(m) - 1;
     unsigned long long base = 0;
-    if ((int)lane == leader) base = atomicAdd(a.pend_count, (unsigned long long)__popc(m));
+    if ((int)lane == leader) base = atomicAdd(a.count, (unsigned long long)__popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (want) {
         unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
-        if (pos < a.pend_cap) a.pend[pos] = r;
+        if (pos < a.cap) a.pend[pos] = r;
     }
 }
 
 /* One update slot of the vertex (ATOMIC mode), executed by all 32 lanes in lock-step:
  * probe the frame-start table; existing slot -> warp-aggregated RED; empty-first -> pending;
  * exhausted -> dropped. */
-__device__ __forceinline__ void contribute_atomic(const VPArgs &a, double4 *sm, int sid, bool has,
-                                                  const Key &k, double4 v, uint32_t ncalls) {
-    const DevStore &s = a.st.s[sid & 3];
-    int res = -3;
-    uint64_t packed = 0;
-    if (has) {
-        packed = key_pack(k);
-        res = probe_existing(s, (uint32_t)packed & s.mask, k.checksum);
-    }
+__device__ __forceinline__ void red_add4(double4 *dst, double4 t) {
+    if (t.x != 0.0) atomicAdd(&dst->x, t.x);
+    if (t.y != 0.0) atomicAdd(&dst->y, t.y);
+    if (t.z != 0.0) atomicAdd(&dst->z, t.z);
+    if (t.w != 0.0) atomicAdd(&dst->w, t.w);
+}
+
+/* res: >= 0 existing slot, -1 new key, -2 dropped, -3 no update; mark = slot's meta.y */
+__device__ __forceinline__ void apply_contribution(const DevStore &s, const PendSink &a,
+                                                   double4 *sm, int sid, const Key &k, double4 v,
+                                                   uint32_t ncalls, int res, uint32_t mark,
+                                                   bool do_red = true, bool aggregate = true) {
     unsigned lane = lane_id();
     unsigned long long gk = res >= 0 ? (((unsigned long long)sid << 32) | (unsigned)res)
                                      : (0xffffffff00000000ull | lane);
-    unsigned peers = __match_any_sync(0xffffffffu, gk);
-    sm[lane] = v;
-    __syncwarp();
-    if (res >= 0 && (int)lane == __ffs(peers) - 1) {
-        double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
-        unsigned m = peers;
-        while (m) {
-            int j = __ffs(m) - 1;
-            m &= m - 1;
-            double4 x = sm[j];
-            t.x += x.x;
-            t.y += x.y;
-            t.z += x.z;
-            t.w += x.w;
+    unsigned peers = aggregate ? __match_any_sync(0xffffffffu, gk) : (1u << lane);
+    if (!aggregate || __all_sync(0xffffffffu, peers == (1u << lane))) {
+        /* no two lanes share a slot: one RED per component, no shared-memory round trip */
+        if (res >= 0) {
+            if (do_red) red_add4(&s.acc[res], v);
+            touch_slot(s, (uint32_t)res, mark);
         }
-        double4 *dst = &s.acc[res];
-        if (t.x != 0.0) atomicAdd(&dst->x, t.x);
-        if (t.y != 0.0) atomicAdd(&dst->y, t.y);
-        if (t.z != 0.0) atomicAdd(&dst->z, t.z);
-        if (t.w != 0.0) atomicAdd(&dst->w, t.w);
-        touch_slot(s, (uint32_t)res);
+    } else {
+        sm[lane] = v;
+        __syncwarp();
+        if (res >= 0 && (int)lane == __ffs(peers) - 1) {
+            double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+            unsigned m = peers;
+            while (m) {
+                int j = __ffs(m) - 1;
+                m &= m - 1;
+                double4 x = sm[j];
+                t.x += x.x;
+                t.y += x.y;
+                t.z += x.z;
+                t.w += x.w;
+            }
+            if (do_red) red_add4(&s.acc[res], t);
+            touch_slot(s, (uint32_t)res, mark);
+        }
+        __syncwarp();
     }
-    __syncwarp();
     PendRec r;
     bool want = res == -1;
     if (want) {
@@ -346,8 +360,17 @@ __device__ __forceinline__ void contribute_atomic(const VPArgs &a, double4 *sm, 
     if (res == -2) atomicAdd(&s.ctr[C_DROPPED], (unsigned long long)ncalls);
 }
 
+__device__ __forceinline__ void contribute_atomic(const DevStore &s, const PendSink &a, double4 *sm,
+                                                  int sid, bool has, const Key &k, double4 v,
+                                                  uint32_t ncalls, bool do_red = true) {
+    int res = -3;
+    uint32_t mark = 0;
+    if (has) res = probe_existing(s, k.pack_lo & s.mask, k.checksum, &mark);
+    apply_contribution(s, a, sm, sid, k, v, ncalls, res, mark, do_red);
+}
+
 /* ORDERED mode: every call becomes a record. */
-__device__ __forceinline__ void emit_call(const VPArgs &a, bool want, int sid, const Key &k,
+__device__ __forceinline__ void emit_call(const PendSink &a, bool want, int sid, const Key &k,
                                           bool is_counter, double r_, double g_, double b_,
                                           double w) {
     PendRec r;
@@ -478,8 +501,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
     double nfx = 0, nfy = 0, nfz = 0;
     const bool fliNee = nee && (a.fli_mask & PSTF_TECH_NEE);
     if (nee) {
-        kFn = key_for(sFli.kp, px, py, pz, __ldg(&V.nee_dir.x[ii]), __ldg(&V.nee_dir.y[ii]),
-                      __ldg(&V.nee_dir.z[ii]), level);
+        kFn = key_for(sFli.kp, px, py, pz, nee ? __ldg(&V.nee_dir.x[ii]) : 0.36,
+                      nee ? __ldg(&V.nee_dir.y[ii]) : 0.48, nee ? __ldg(&V.nee_dir.z[ii]) : 0.8,
+                      level);
         if (fliNee) {
             nfx = __ldg(&V.nee_fli.x[ii]);
             nfy = __ldg(&V.nee_fli.y[ii]);
@@ -534,46 +558,399 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
             if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
             if (a.has_li && cont && rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
         }
-        contribute_atomic(a, sm, 0, live, kLo, vlo, nlo);
-        contribute_atomic(a, sm, 1, live, kLoe, vle, nle);
-        contribute_atomic(a, sm, 2, live && cont, kFc, vfc, nfc);
-        contribute_atomic(a, sm, 2, live && nee, kFn, vfn, nfn);
-        if (a.has_li) contribute_atomic(a, sm, 3, live && cont, kLi, vli, nli);
+        const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+        contribute_atomic(sLo, ps, sm, 0, live, kLo, vlo, nlo);
+        contribute_atomic(sLoe, ps, sm, 1, live, kLoe, vle, nle);
+        contribute_atomic(sFli, ps, sm, 2, live && cont, kFc, vfc, nfc);
+        contribute_atomic(sFli, ps, sm, 2, live && nee, kFn, vfn, nfn);
+        if (a.has_li) contribute_atomic(sLi, ps, sm, 3, live && cont, kLi, vli, nli);
     } else {
         /* ORDERED: the reference's individual calls, in any order (the sort canonicalises) */
+        const PendSink ps{a.pend, a.pend_count, a.pend_cap};
         unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
-        emit_call(a, live, 0, kLo, true, 0.0, 0.0, 0.0, 1.0);
+        emit_call(ps, live, 0, kLo, true, 0.0, 0.0, 0.0, 1.0);
         bool ok = finite3(ehx, ehy, ehz);
         rejLo += live && !ok;
-        emit_call(a, live && ok, 0, kLo, false, ehx, ehy, ehz, 1.0);
+        emit_call(ps, live && ok, 0, kLo, false, ehx, ehy, ehz, 1.0);
         ok = finite3(ulx, uly, ulz);
         rejLo += live && transp && !ok;
-        emit_call(a, live && transp && ok, 0, kLo, false, ulx, uly, ulz, 1.0);
-        emit_call(a, live, 1, kLoe, true, 0.0, 0.0, 0.0, 1.0);
+        emit_call(ps, live && transp && ok, 0, kLo, false, ulx, uly, ulz, 1.0);
+        emit_call(ps, live, 1, kLoe, true, 0.0, 0.0, 0.0, 1.0);
         ok = finite3(uex, uey, uez);
         rejLoe += live && loeCont && !ok;
-        emit_call(a, live && loeCont && ok, 1, kLoe, false, uex, uey, uez, 1.0);
+        emit_call(ps, live && loeCont && ok, 1, kLoe, false, uex, uey, uez, 1.0);
         ok = finite3(nlx, nly, nlz);
         rejLoe += live && loeNee && !ok;
-        emit_call(a, live && loeNee && ok, 1, kLoe, false, nlx, nly, nlz, 1.0);
-        emit_call(a, live && cont, 2, kFc, true, 0.0, 0.0, 0.0, 1.0);
+        emit_call(ps, live && loeNee && ok, 1, kLoe, false, nlx, nly, nlz, 1.0);
+        emit_call(ps, live && cont, 2, kFc, true, 0.0, 0.0, 0.0, 1.0);
         ok = finite3(fcx, fcy, fcz);
         rejFli += live && fliCont && !ok;
-        emit_call(a, live && fliCont && ok, 2, kFc, false, fcx, fcy, fcz, 1.0);
-        emit_call(a, live && nee, 2, kFn, true, 0.0, 0.0, 0.0, 1.0);
+        emit_call(ps, live && fliCont && ok, 2, kFc, false, fcx, fcy, fcz, 1.0);
+        emit_call(ps, live && nee, 2, kFn, true, 0.0, 0.0, 0.0, 1.0);
         ok = finite3(nfx, nfy, nfz);
         rejFli += live && fliNee && !ok;
-        emit_call(a, live && fliNee && ok, 2, kFn, false, nfx, nfy, nfz, 1.0);
+        emit_call(ps, live && fliNee && ok, 2, kFn, false, nfx, nfy, nfz, 1.0);
         if (a.has_li) {
-            emit_call(a, live && cont, 3, kLi, true, 0.0, 0.0, 0.0, 1.0);
+            emit_call(ps, live && cont, 3, kLi, true, 0.0, 0.0, 0.0, 1.0);
             ok = finite3(lvx, lvy, lvz);
             rejLi += live && cont && !ok;
-            emit_call(a, live && cont && ok, 3, kLi, false, lvx, lvy, lvz, 1.0);
+            emit_call(ps, live && cont && ok, 3, kLi, false, lvx, lvy, lvz, 1.0);
         }
         if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
         if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
         if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
         if (rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K5 (fast path): persistent, TMA-staged fused vertex pass (ATOMIC mode, shared quantisation) */
+/*
+ * Each CTA (VT threads, one vertex per thread per tile) loops over tiles of VT vertices.  The 35
+ * SoA field segments of the next tiles are fetched by one elected thread with 1-D bulk async
+ * copies (cp.async.bulk, L2 evict-first: the stream is read once) into a 2-stage shared-memory
+ * ring guarded by mbarriers, so the 276 B/vertex input stream never stalls the warps; lanes read
+ * their fields from shared memory just in time.  Per vertex the position is divided by the base
+ * cell once and each direction goes through atan2 once (pos_q / octa_pair), shared by the Lo,
+ * Lo\E, FLi and Li keys and by every level of the next-vertex lookup chain.
+ */
+#define VT 128
+#define VT_STAGES 2
+#define VT_BLOCKS_PER_SM 3
+
+struct TileStage {
+    double f[PS_NUM_F64][VT];
+    uint32_t flags[VT];
+};
+
+struct VPArgs2 {
+    Stores4 st;
+    FastParams fp;
+    int dbg; /* experiment switches (PSTF_VP_DBG): 1 no lookups, 2 no RED, 4 keys only */
+    int has_li;
+    uint32_t loe_mask, fli_mask;
+    const double *fld[PS_NUM_F64];
+    const uint32_t *flags;
+    uint64_t n;
+    PendRec *pend;
+    unsigned long long *pend_count;
+    uint64_t pend_cap;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(64); /* back off: leave issue slots to the other CTAs on the SM */
+    }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void issue_tile(const VPArgs2 &a, TileStage *st, uint64_t *bar,
+                                           uint64_t tile, uint64_t policy) {
+    mbar_expect_tx(bar, (uint32_t)(PS_NUM_F64 * VT * 8 + VT * 4));
+    const uint64_t v0 = tile * VT;
+    for (int k = 0; k < PS_NUM_F64; ++k) bulk_g2s(&st->f[k][0], a.fld[k] + v0, VT * 8, bar, policy);
+    bulk_g2s(&st->flags[0], a.flags + v0, VT * 4, bar, policy);
+}
+
+/* pull a later tile's segments into L2 so its shared-memory copy completes at L2 latency */
+__device__ __forceinline__ void prefetch_tile(const VPArgs2 &a, uint64_t tile) {
+    const uint64_t v0 = tile * VT;
+    for (int k = 0; k < PS_NUM_F64; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
+    prefetch_l2(a.flags + v0, VT * 4);
+}
+
+struct SmemSrc {
+    const TileStage *t;
+    int j;
+    __device__ __forceinline__ double f(int k) const { return t->f[k][j]; }
+    __device__ __forceinline__ uint32_t flags() const { return t->flags[j]; }
+};
+
+struct GmemSrc {
+    const VPArgs2 &a;
+    uint64_t i;
+    __device__ __forceinline__ double f(int k) const { return __ldg(a.fld[k] + i); }
+    __device__ __forceinline__ uint32_t flags() const { return __ldg(a.flags + i); }
+};
+
+__device__ __forceinline__ Key make_key(uint64_t h1, int level, int32_t c0, int32_t c1, int32_t c2,
+                                        int32_t d0, int32_t d1) {
+    Key k;
+    k.level = level;
+    k.cell[0] = c0;
+    k.cell[1] = c1;
+    k.cell[2] = c2;
+    k.dir[0] = d0;
+    k.dir[1] = d1;
+    const uint64_t pk = pack_from_h1(h1, c2, d0, d1);
+    k.checksum = checksum_of(pk);
+    k.pack_lo = (uint32_t)pk;
+    return k;
+}
+
+template <class Src>
+__device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
+                                            double4 *sm) {
+    const DevStore &sLo = a.st.s[0];
+    const DevStore &sLoe = a.st.s[1];
+    const DevStore &sFli = a.st.s[2];
+    const DevStore &sLi = a.st.s[3];
+    const KeyParams &kp = sLo.kp;
+    const FastParams &fq = a.fp;
+    const uint32_t fl = live ? S.flags() : 0u;
+    const bool cont = (fl & PSTF_VERTEX_CONT_EXTENDED) != 0;
+    const bool nsurf = (fl & PSTF_VERTEX_NEXT_IS_SURFACE) != 0;
+    const bool nee = (fl & PSTF_VERTEX_NEE_SAMPLED) != 0;
+    const bool look = cont && nsurf && !(a.dbg & 1);
+
+    /* ---- keys (estimators.cpp:195, 215, 226, 242, 248, 257): one level, one cell triple and
+     * one packKeyFields prefix for all update keys of the vertex ---- */
+    const int level = select_level_fast(fq, S.f(PS_FP));
+    const double px = S.f(PS_POS), py = S.f(PS_POS + 1), pz = S.f(PS_POS + 2);
+    const PosQ q = pos_q(fq, px, py, pz);
+    const int32_t c0 = cell_at(fq, q.q[0], px, level), c1 = cell_at(fq, q.q[1], py, level),
+                  c2 = cell_at(fq, q.q[2], pz, level);
+    const uint64_t h1 = pack_h1(level, c0, c1);
+    DirF8 fo, fi, fin, fn, ftmp;
+    octa_f8(S.f(PS_WO), S.f(PS_WO + 1), S.f(PS_WO + 2), 0, &fo, &ftmp);
+    octa_f8(S.f(PS_WI), S.f(PS_WI + 1), S.f(PS_WI + 2), look, &fi, &fin);
+    /* lanes without NEE use a fixed generic direction so a speculated evaluation never takes
+     * the exact-atan2 path for their zero nee.dir */
+    octa_f8(nee ? S.f(PS_NDIR) : 0.36, nee ? S.f(PS_NDIR + 1) : 0.48,
+            nee ? S.f(PS_NDIR + 2) : 0.8, 0, &fn, &ftmp);
+    const Key kLo = make_key(h1, level, c0, c1, c2, dir_cell_f8(fo.u, level), dir_cell_f8(fo.v, level));
+    const Key kFc = make_key(h1, level, c0, c1, c2, dir_cell_f8(fi.u, level), dir_cell_f8(fi.v, level));
+    const Key kFn = make_key(h1, level, c0, c1, c2, dir_cell_f8(fn.u, level), dir_cell_f8(fn.v, level));
+
+    /* ---- first lookup key at the next vertex (estimators.cpp:198-206) ---- */
+    const double qx = S.f(PS_NPOS), qy = S.f(PS_NPOS + 1), qz = S.f(PS_NPOS + 2);
+    const PosQ nq = pos_q(fq, qx, qy, qz);
+    const int l0 = select_level_fast(fq, S.f(PS_NFP));
+    uint64_t qpk = pack_key_fields(l0, cell_at(fq, nq.q[0], qx, l0), cell_at(fq, nq.q[1], qy, l0),
+                                   cell_at(fq, nq.q[2], qz, l0), dir_cell_f8(fin.u, l0),
+                                   dir_cell_f8(fin.v, l0));
+
+    /* ---- one round trip: the five update home words, the two lookup home words and (on
+     * speculation that the lookup key sits at its home slot) the two committed records ---- */
+    const bool has2 = live && cont, has3 = live && nee, has4 = a.has_li && live && cont;
+    const uint32_t h0 = kLo.pack_lo & sLo.mask, h1s = kLo.pack_lo & sLoe.mask,
+                   h2 = kFc.pack_lo & sFli.mask, h3 = kFn.pack_lo & sFli.mask,
+                   h4 = kFc.pack_lo & sLi.mask;
+    const uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
+    const uint2 z = make_uint2(0u, 0u);
+    const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
+    const uint2 m0 = live ? sLo.meta[h0] : z, m1 = live ? sLoe.meta[h1s] : z,
+                m2 = has2 ? sFli.meta[h2] : z, m3 = has3 ? sFli.meta[h3] : z,
+                m4 = has4 ? sLi.meta[h4] : z;
+    const uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
+    const double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
+
+    double3 loNext = make_double3(0.0, 0.0, 0.0), loeNext = make_double3(0.0, 0.0, 0.0);
+    const double nex = S.f(PS_NEMIS), ney = S.f(PS_NEMIS + 1), nez = S.f(PS_NEMIS + 2);
+    if (look) {
+        const uint32_t cs = checksum_of(qpk);
+        bool doneLo = false, doneLoe = false;
+        if (wl == cs) { /* speculation hit: sl is the committed record of the slot */
+            if (sl.w > 0.0) loNext = make_double3(sl.x, sl.y, sl.z);
+            doneLo = sl.w > 0.0;
+        }
+        if (we == cs) {
+            if (se.w > 0.0) loeNext = make_double3(se.x, se.y, se.z);
+            doneLoe = se.w > 0.0;
+        }
+        /* general path: rest of the probe window at l0 (unless the home word settled it), then
+         * the coarser levels (queryFromLevel, field.cpp:179-195) */
+        const bool homeLo = wl == cs || wl == 0u, homeLoe = we == cs || we == 0u;
+        if (!(doneLo && doneLoe)) {
+            for (int l = l0; l <= kp.max_level && !(doneLo && doneLoe); ++l) {
+                uint64_t pk = qpk;
+                if (l != l0)
+                    pk = pack_key_fields(l, cell_at(fq, nq.q[0], qx, l), cell_at(fq, nq.q[1], qy, l),
+                                         cell_at(fq, nq.q[2], qz, l), dir_cell_f8(fin.u, l),
+                                         dir_cell_f8(fin.v, l));
+                const uint32_t ccs = checksum_of(pk);
+                const uint32_t hl = (uint32_t)pk & sLo.mask, he = (uint32_t)pk & sLoe.mask;
+                int il = -1, ie = -1;
+                if (!doneLo) {
+                    if (l == l0 && homeLo) il = -1; /* home word: empty, or match not > 0 */
+                    else il = resolve_find(sLo, hl, ccs, l == l0 ? wl : sLo.meta[hl].x);
+                }
+                if (!doneLoe) {
+                    if (l == l0 && homeLoe) ie = -1;
+                    else ie = resolve_find(sLoe, he, ccs, l == l0 ? we : sLoe.meta[he].x);
+                }
+                const double4 cl = il >= 0 ? sLo.com[il] : z4;
+                const double4 ce = ie >= 0 ? sLoe.com[ie] : z4;
+                if (il >= 0 && cl.w > 0.0) {
+                    loNext = make_double3(cl.x, cl.y, cl.z);
+                    doneLo = true;
+                }
+                if (ie >= 0 && ce.w > 0.0) {
+                    loeNext = make_double3(ce.x, ce.y, ce.z);
+                    doneLoe = true;
+                }
+            }
+        }
+    } else if (cont && !nsurf) {
+        loNext = make_double3(nex, ney, nez); /* environment: exactly known (209) */
+    }
+
+    /* ---- update values (field.cpp:13-25 evaluation order) ---- */
+    const double ratio = S.f(PS_RATIO);
+    const double fr = S.f(PS_F), fg = S.f(PS_F + 1), fb = S.f(PS_F + 2);
+    const double nmis = S.f(PS_NMIS);
+    const bool transp = cont && ratio > 0.0;
+    const double lex = nex * nmis, ley = ney * nmis, lez = nez * nmis;
+    const double lix = lex + loeNext.x, liy = ley + loeNext.y, liz = lez + loeNext.z;
+
+    unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
+    double4 vlo = make_double4(0.0, 0.0, 0.0, 1.0); /* Lo: counter, emission, transport */
+    uint32_t nlo = 1;
+    {
+        const double ex = S.f(PS_EMIS), ey = S.f(PS_EMIS + 1), ez = S.f(PS_EMIS + 2);
+        if (finite3(ex, ey, ez)) { vlo.x += ex; vlo.y += ey; vlo.z += ez; ++nlo; } else ++rejLo;
+        if (transp) {
+            const double ux = ((0.0 + loNext.x) * fr) * ratio, uy = ((0.0 + loNext.y) * fg) * ratio,
+                         uz = ((0.0 + loNext.z) * fb) * ratio;
+            if (finite3(ux, uy, uz)) { vlo.x += ux; vlo.y += uy; vlo.z += uz; ++nlo; } else ++rejLo;
+        }
+    }
+    double4 vle = make_double4(0.0, 0.0, 0.0, 1.0); /* Lo\E (226-234) */
+    uint32_t nle = 1;
+    if (transp && (a.loe_mask & PSTF_TECH_CONTINUATION)) {
+        const double ux = ((lex + loeNext.x) * fr) * ratio, uy = ((ley + loeNext.y) * fg) * ratio,
+                     uz = ((lez + loeNext.z) * fb) * ratio;
+        if (finite3(ux, uy, uz)) { vle.x += ux; vle.y += uy; vle.z += uz; ++nle; } else ++rejLoe;
+    }
+    if (nee && (a.loe_mask & PSTF_TECH_NEE)) {
+        const double x = S.f(PS_NEELOE), y = S.f(PS_NEELOE + 1), z2 = S.f(PS_NEELOE + 2);
+        if (finite3(x, y, z2)) { vle.x += x; vle.y += y; vle.z += z2; ++nle; } else ++rejLoe;
+    }
+    double4 vfc = make_double4(0.0, 0.0, 0.0, 1.0); /* FLi continuation (241-246) */
+    uint32_t nfc = 1;
+    if (cont && (a.fli_mask & PSTF_TECH_CONTINUATION)) {
+        const double x = fr * lix, y = fg * liy, z2 = fb * liz;
+        if (finite3(x, y, z2)) { vfc.x += x; vfc.y += y; vfc.z += z2; ++nfc; } else ++rejFli;
+    }
+    double4 vfn = make_double4(0.0, 0.0, 0.0, 1.0); /* FLi NEE (247-254) */
+    uint32_t nfn = 1;
+    if (nee && (a.fli_mask & PSTF_TECH_NEE)) {
+        const double x = S.f(PS_NEEFLI), y = S.f(PS_NEEFLI + 1), z2 = S.f(PS_NEEFLI + 2);
+        if (finite3(x, y, z2)) { vfn.x += x; vfn.y += y; vfn.z += z2; ++nfn; } else ++rejFli;
+    }
+    double4 vli = make_double4(0.0, 0.0, 0.0, 1.0); /* Li (256-261) */
+    uint32_t nli = 1;
+    if (a.has_li && cont) {
+        const double x = lix * 1.0, y = liy * 1.0, z2 = liz * 1.0;
+        if (finite3(x, y, z2)) { vli.x += x; vli.y += y; vli.z += z2; ++nli; } else ++rejLi;
+    }
+    if (live) {
+        if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
+        if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
+        if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
+        if (rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
+    }
+    const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+    if (a.dbg & 4) {
+        const double t = vlo.x + vle.y + vfc.z + vfn.x + vli.y;
+        if ((m0.x ^ m1.x ^ m2.x ^ m3.x ^ m4.x ^ kLo.checksum ^ kFc.checksum ^ kFn.checksum) ==
+                0x12345u && t == 1.2345)
+            atomicAdd(&sLo.ctr[C_INTERNAL], 1ull);
+        return;
+    }
+    uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
+    const int r0 = live ? resolve_probe(sLo, h0, kLo.checksum, m0, &k0) : -3;
+    const int r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
+    const int r2 = has2 ? resolve_probe(sFli, h2, kFc.checksum, m2, &k2) : -3;
+    const int r3 = has3 ? resolve_probe(sFli, h3, kFn.checksum, m3, &k3) : -3;
+    const int r4 = has4 ? resolve_probe(sLi, h4, kFc.checksum, m4, &k4) : -3;
+    const bool red = !(a.dbg & 2);
+    const bool agg = (a.dbg & 16) != 0; /* warp aggregation measured slower on config 2 */
+    apply_contribution(sLo, ps, sm, 0, kLo, vlo, nlo, r0, k0, red, agg);
+    apply_contribution(sLoe, ps, sm, 1, kLo, vle, nle, r1, k1, red, agg); /* Lo\E key == Lo key */
+    apply_contribution(sFli, ps, sm, 2, kFc, vfc, nfc, r2, k2, red, agg);
+    apply_contribution(sFli, ps, sm, 2, kFn, vfn, nfn, r3, k3, red, agg);
+    if (a.has_li) apply_contribution(sLi, ps, sm, 3, kFc, vli, nli, r4, k4, red, agg);
+}
+
+template <int STAGES, int MINB>
+__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TileStage *stages = reinterpret_cast<TileStage *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + STAGES * sizeof(TileStage));
+    __shared__ double4 wsm[VT / 32][32];
+    const int tid = threadIdx.x;
+    double4 *sm = wsm[tid >> 5];
+    const uint64_t nfull = a.n / VT;
+    uint64_t policy = 0;
+    if (tid == 0) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < STAGES; ++s) {
+            uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+            if (t < nfull) issue_tile(a, &stages[s], &bars[s], t, policy);
+            if (t + gridDim.x < nfull) prefetch_tile(a, t + gridDim.x);
+        }
+    uint32_t it = 0;
+    for (uint64_t tile = blockIdx.x; tile < nfull; tile += gridDim.x, ++it) {
+        const int s = (int)(it % STAGES);
+        mbar_wait(&bars[s], (it / STAGES) & 1u);
+        SmemSrc src{&stages[s], tid};
+        vertex_body(a, src, true, sm);
+        __syncthreads(); /* every lane is done with stage s */
+        const uint64_t nt = tile + (uint64_t)STAGES * gridDim.x;
+        if (tid == 0 && nt < nfull) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_tile(a, &stages[s], &bars[s], nt, policy);
+            if (nt + gridDim.x < nfull) prefetch_tile(a, nt + gridDim.x);
+        }
+    }
+    /* partial last tile straight from global memory */
+    if ((a.n % VT) && blockIdx.x == (unsigned)(nfull % gridDim.x)) {
+        const uint64_t v = nfull * VT + tid;
+        const bool live = v < a.n;
+        GmemSrc src{a, live ? v : nfull * VT};
+        vertex_body(a, src, live, sm);
     }
 }
 
@@ -629,14 +1006,11 @@ __global__ void k_apply_atomic(ApplyArgs a, PendRec *pend, unsigned long long *p
                                   k.dir_cell[1]);
     double4 v = isc ? make_double4(0.0, 0.0, 0.0, w > 0.0 ? w : 0.0)
                     : make_double4(r * w, g * w, b * w, 0.0);
-    int res = probe_existing(a.s, (uint32_t)pk & a.s.mask, k.checksum);
+    uint32_t mark = 0;
+    int res = probe_existing(a.s, (uint32_t)pk & a.s.mask, k.checksum, &mark);
     if (res >= 0) {
-        double4 *dst = &a.s.acc[res];
-        if (v.x != 0.0) atomicAdd(&dst->x, v.x);
-        if (v.y != 0.0) atomicAdd(&dst->y, v.y);
-        if (v.z != 0.0) atomicAdd(&dst->z, v.z);
-        if (v.w != 0.0) atomicAdd(&dst->w, v.w);
-        touch_slot(a.s, (uint32_t)res);
+        red_add4(&a.s.acc[res], v);
+        touch_slot(a.s, (uint32_t)res, mark);
     } else if (res == -2) {
         atomicAdd(&a.s.ctr[C_DROPPED], 1ull);
     } else {
@@ -896,7 +1270,7 @@ __global__ void k_place_round(PlaceArgs a, const unsigned long long *res_prev,
     unsigned long long res = PSTF_RES(R_DROP, 0);
     for (uint32_t i = 0; i < s.window; ++i) {
         uint32_t idx = (home + i) & s.mask;
-        uint32_t c = s.chk[idx];
+        uint32_t c = s.meta[idx].x;
         if (c != 0) {
             if (c == cs) { /* an older resident with this checksum (field.cpp:122) */
                 res = PSTF_RES(R_FIXED, idx);
@@ -946,7 +1320,7 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
     if (t == R_PROPOSE) {
         uint32_t *hold_cur = a.parity ? s.hold0 : s.hold1; /* the array the last round wrote */
         hold_cur[slot] = PSTF_HOLD_NONE;
-        s.chk[slot] = a.ucs[u];
+        s.meta[slot].x = a.ucs[u];
         s.keyf[slot] = ukey[u];
         atomicAdd(&s.ctr[C_LIVE], 1ull);
         atomicAdd(&s.ctr[C_NEW_KEYS], 1ull);
@@ -1009,7 +1383,7 @@ __global__ void k_fold(const PendRec *pend, const uint64_t *tgt, const uint32_t 
 }
 
 /* ------------------------------------------------------------------------------------------ */
-/* K3: endFrame (field.cpp:197-263) on the touched list                                        */
+/* K3: endFrame (field.cpp:197-263), all stores of a batch in one launch per pass            */
 
 __device__ __forceinline__ double warp_sum_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1018,100 +1392,154 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 #define EF_BLOCK 256
 
-__global__ void k_ef_reduce(DevStore s) {
+/* Pass 1 (field.cpp:205-216) for every store of the batch: sweep meta (8 B/slot, coalesced),
+ * sum c_new over live slots touched this frame (meta.y == frame+1; untouched slots have zero
+ * accumulators by construction), count them, and snapshot `live` for the eviction rule. */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
     __shared__ double ssum[EF_BLOCK / 32];
-    __shared__ unsigned long long scnt[EF_BLOCK / 32];
-    uint64_t n = s.ctr[C_TOUCHED_N];
-    if (blockIdx.x == 0 && threadIdx.x == 0) s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
-    double sum = 0.0;
-    unsigned long long cnt = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        double cn = s.acc[s.touched[i]].w;
-        if (cn > 0.0) {
-            sum += cn;
-            ++cnt;
-        }
-    }
-    sum = warp_sum_d(sum);
-    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-    if (lane_id() == 0) {
-        ssum[threadIdx.x >> 5] = sum;
-        scnt[threadIdx.x >> 5] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        unsigned long long c = 0;
-        for (int w = 0; w < EF_BLOCK / 32; ++w) {
-            t += ssum[w];
-            c += scnt[w];
-        }
-        if (c) {
-            atomicAdd(s.cn_sum, t);
-            atomicAdd(&s.ctr[C_CN_COUNT], c);
-        }
-    }
-}
-
-__global__ void k_ef_blend(DevStore s) {
-    uint64_t n = s.ctr[C_TOUCHED_N];
-    const unsigned long long cnt = s.ctr[C_CN_COUNT];
-    const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
-    const double tMax = s.t_max;
-    const bool limited = tMax > 0.0 && isfinite(tMax);
-    const double cap = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
-    unsigned long long internal = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t slot = s.touched[i];
-        double4 a = s.acc[slot];
-        double cn = a.w;
-        if (cn > 0.0) {
-            double4 c = s.com[slot];
-            double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
-            double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
-            if (limited) {
-                double fl = 1.0 / tMax;
-                alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+    __shared__ unsigned long long scnt[EF_BLOCK / 32], stch[EF_BLOCK / 32];
+    for (int j = 0; j < nst; ++j) {
+        const DevStore &s = st.s[j];
+        if (blockIdx.x == 0 && threadIdx.x == 0) s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+        const uint64_t cap = (uint64_t)s.mask + 1;
+        const uint32_t m1 = s.frame + 1u;
+        double sum = 0.0;
+        unsigned cnt = 0, tch = 0;
+        /* 16 B loads cover two slot words; two of them in flight per iteration */
+        const uint4 *m4 = reinterpret_cast<const uint4 *>(s.meta);
+        const uint64_t npairs = cap / 2, stride = (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npairs;
+             p += 2 * stride) {
+            const uint4 a4 = m4[p];
+            const uint4 b4 = p + stride < npairs ? m4[p + stride] : make_uint4(0, 0, 0, 0);
+            const uint32_t xs[4] = {a4.x, a4.z, b4.x, b4.z}, ys[4] = {a4.y, a4.w, b4.y, b4.w};
+            const uint64_t idx[4] = {2 * p, 2 * p + 1, 2 * (p + stride), 2 * (p + stride) + 1};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (xs[k] != 0 && ys[k] == m1) {
+                    ++tch;
+                    const double cn = s.acc[idx[k]].w;
+                    if (cn > 0.0) {
+                        sum += cn;
+                        ++cnt;
+                    }
+                }
             }
-            double oma = 1.0 - alpha;
-            c.x = c.x * oma + cx * alpha;
-            c.y = c.y * oma + cy * alpha;
-            c.z = c.z * oma + cz * alpha;
-            c.w = c.w + cn;
-            if (limited) c.w = (cap < c.w) ? cap : c.w; /* std::min(cOld, cap) */
-            s.com[slot] = c;
-        } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
-            ++internal;
         }
-        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+        sum = warp_sum_d(sum);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        tch = __reduce_add_sync(0xffffffffu, tch);
+        if (lane_id() == 0) {
+            ssum[threadIdx.x >> 5] = sum;
+            scnt[threadIdx.x >> 5] = cnt;
+            stch[threadIdx.x >> 5] = tch;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            unsigned long long c = 0, h = 0;
+            for (int w = 0; w < EF_BLOCK / 32; ++w) {
+                t += ssum[w];
+                c += scnt[w];
+                h += stch[w];
+            }
+            if (c) {
+                atomicAdd(s.cn_sum, t);
+                atomicAdd(&s.ctr[C_CN_COUNT], c);
+            }
+            if (h) atomicAdd(&s.ctr[C_TOUCHED_N], h);
+        }
+        __syncthreads();
     }
-    if (internal) atomicAdd(&s.ctr[C_INTERNAL], internal);
 }
 
-/* age eviction once live*4 > capacity*3 (field.cpp:247-260); live_snap taken before */
-__global__ void k_evict(DevStore s) {
-    unsigned long long cap = (unsigned long long)s.mask + 1ull;
-    const unsigned long long live_snap = s.ctr[C_LIVE_SNAP];
-    if (!(live_snap * 4ull > cap * 3ull)) return;
-    unsigned long long ev = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t c = s.chk[i];
-        if (c == 0) continue;
-        uint32_t age = s.frame - s.last[i];
-        if (age >= s.evict_age) {
-            s.chk[i] = 0;
-            s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
-            ++ev;
+/* Passes 2+3 (field.cpp:218-260) fused per slot: blend + cap the touched slots, zero their
+ * accumulators, then age-evict when live*4 > capacity*3 (live taken before any eviction). */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
+    for (int j = 0; j < nst; ++j) {
+        const DevStore &s = st.s[j];
+        const uint64_t cap = (uint64_t)s.mask + 1;
+        const uint32_t m1 = s.frame + 1u;
+        const unsigned long long cnt = s.ctr[C_CN_COUNT];
+        const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
+        const double tMax = s.t_max;
+        const bool limited = tMax > 0.0 && isfinite(tMax);
+        const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
+        const bool evict = s.ctr[C_LIVE_SNAP] * 4ull > (unsigned long long)cap * 3ull;
+        unsigned internal = 0, ev = 0;
+        const uint4 *m4 = reinterpret_cast<const uint4 *>(s.meta);
+        const uint64_t npairs = cap / 2, stride = (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npairs;
+             p += 2 * stride) {
+            const uint4 a4 = m4[p];
+            const uint4 b4 = p + stride < npairs ? m4[p + stride] : make_uint4(0, 0, 0, 0);
+            const uint32_t xs[4] = {a4.x, a4.z, b4.x, b4.z}, ys[4] = {a4.y, a4.w, b4.y, b4.w};
+            const uint64_t idx[4] = {2 * p, 2 * p + 1, 2 * (p + stride), 2 * (p + stride) + 1};
+            bool tk[4];
+            double4 av[4], cv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { /* issue all loads first */
+                tk[k] = xs[k] != 0 && ys[k] == m1;
+                av[k] = tk[k] ? s.acc[idx[k]] : make_double4(0.0, 0.0, 0.0, 0.0);
+                cv[k] = tk[k] ? s.com[idx[k]] : make_double4(0.0, 0.0, 0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (xs[k] == 0) continue;
+                const uint64_t i = idx[k];
+                if (tk[k]) {
+                    const double4 a = av[k];
+                    const double cn = a.w;
+                    if (cn > 0.0) {
+                        double4 c = cv[k];
+                        const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+                        double alpha =
+                            s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+                        if (limited) {
+                            const double fl = 1.0 / tMax;
+                            alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+                        }
+                        const double oma = 1.0 - alpha;
+                        c.x = c.x * oma + cx * alpha;
+                        c.y = c.y * oma + cy * alpha;
+                        c.z = c.z * oma + cz * alpha;
+                        c.w = c.w + cn;
+                        if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+                        s.com[i] = c;
+                    } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+                        ++internal;
+                    }
+                    if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
+                        s.acc[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+                }
+                if (evict && (uint32_t)(s.frame - (ys[k] - 1u)) >= s.evict_age) {
+                    s.meta[i].x = 0;
+                    s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+                    ++ev;
+                }
+            }
+        }
+        internal = __reduce_add_sync(0xffffffffu, internal);
+        ev = __reduce_add_sync(0xffffffffu, ev);
+        if (lane_id() == 0) {
+            if (internal) atomicAdd(&s.ctr[C_INTERNAL], (unsigned long long)internal);
+            if (ev) {
+                atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
+                atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
+            }
         }
     }
-    ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);
-    if (lane_id() == 0 && ev) {
-        atomicAdd(&s.ctr[C_EVICTED], ev);
-        atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
-    }
+}
+
+/* roll the per-frame scratch of every store of the batch */
+__global__ void k_ef_finish(Stores4 st, int nst) {
+    const int j = threadIdx.x;
+    if (j >= nst) return;
+    const DevStore &s = st.s[j];
+    s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
+    s.ctr[C_TOUCHED_N] = 0;
+    s.ctr[C_CN_COUNT] = 0;
+    *s.cn_sum = 0.0;
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -1122,7 +1550,7 @@ __global__ void k_invalidate(DevStore s, int use_box, double lx, double ly, doub
     uint64_t cap = (uint64_t)s.mask + 1;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        if (s.chk[i] == 0) continue;
+        if (s.meta[i].x == 0) continue;
         if (use_box) {
             KeyFields k = s.keyf[i];
             double cs = cell_size(s.kp, k.level); /* field.cpp:278-283 */
@@ -1139,7 +1567,7 @@ __global__ void k_weighted_mean(DevStore s, double *out4) {
     double r = 0, g = 0, b = 0, w = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        if (s.chk[i] == 0) continue;
+        if (s.meta[i].x == 0) continue;
         double4 c = s.com[i];
         if (c.w <= 0.0) continue; /* field.cpp:299 */
         r += c.x * c.w;
@@ -1162,7 +1590,7 @@ __global__ void k_weighted_mean(DevStore s, double *out4) {
 __global__ void k_snap_gather(DevStore s, pstf_snapshot_record *out, unsigned long long *count) {
     uint64_t cap = (uint64_t)s.mask + 1;
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    bool live = i < cap && s.chk[i] != 0;
+    bool live = i < cap && s.meta[i].x != 0;
     unsigned m = __ballot_sync(0xffffffffu, live);
     if (!m) return;
     unsigned long long base = 0;
@@ -1181,7 +1609,7 @@ __global__ void k_snap_gather(DevStore s, pstf_snapshot_record *out, unsigned lo
     r.cell[2] = k.c2;
     r.dir_cell[0] = k.d0;
     r.dir_cell[1] = k.d1;
-    r.checksum = s.chk[i];
+    r.checksum = s.meta[i].x;
     r.value[0] = c.x;
     r.value[1] = c.y;
     r.value[2] = c.z;
@@ -1591,10 +2019,8 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
         off += (bytes + 255) & ~(size_t)255;
         return o;
     };
-    size_t o_chk = take(cap * 4), o_com = take(cap * 32), o_acc = take(cap * 32),
-           o_keyf = take(cap * sizeof(KeyFields)), o_last = take(cap * 4), o_tmark = take(cap * 4),
-           o_touched = take(cap * 4), o_h0 = take(cap * 4), o_h1 = take(cap * 4),
-           o_ctr = take(C_NUM * 8), o_sum = take(8);
+    size_t o_meta = take(cap * 8), o_com = take(cap * 32), o_acc = take(cap * 32),
+           o_keyf = take(cap * sizeof(KeyFields)), o_h0 = take(cap * 4), o_h1 = take(cap * 4), o_ctr = take(C_NUM * 8), o_sum = take(8);
     cudaError_t e = cudaMalloc(&f->arena, off);
     if (e != cudaSuccess) {
         delete f;
@@ -1603,13 +2029,10 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     char *base = (char *)f->arena;
     DevStore &d = f->d;
     memset(&d, 0, sizeof(d));
-    d.chk = (uint32_t *)(base + o_chk);
+    d.meta = (uint2 *)(base + o_meta);
     d.com = (double4 *)(base + o_com);
     d.acc = (double4 *)(base + o_acc);
     d.keyf = (KeyFields *)(base + o_keyf);
-    d.last = (uint32_t *)(base + o_last);
-    d.tmark = (uint32_t *)(base + o_tmark);
-    d.touched = (uint32_t *)(base + o_touched);
     d.hold0 = (uint32_t *)(base + o_h0);
     d.hold1 = (uint32_t *)(base + o_h1);
     d.ctr = (unsigned long long *)(base + o_ctr);
@@ -1739,25 +2162,34 @@ int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_v
     return PSTF_OK;
 }
 
+int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
+    if (!fs || n < 1 || n > 4) return set_err(PSTF_E_INVALID, "1..4 stores per batch");
+    for (int i = 0; i < n; ++i) {
+        if (!fs[i]) return set_err(PSTF_E_INVALID, "NULL store");
+        if (fs[i]->device != fs[0]->device)
+            return set_err(PSTF_E_INVALID, "all stores must live on one device");
+        for (int j = 0; j < i; ++j)
+            if (fs[j] == fs[i]) return set_err(PSTF_E_INVALID, "store listed twice");
+    }
+    CK(cudaSetDevice(fs[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Stores4 S = stores4(fs, n);
+    uint64_t maxcap = 0;
+    for (int i = 0; i < n; ++i) {
+        maxcap = std::max<uint64_t>(maxcap, (uint64_t)fs[i]->d.mask + 1);
+        CK(cudaMemsetAsync(&fs[i]->d.ctr[C_EVICTED], 0, 8, st));
+    }
+    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
+    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n);
+    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n);
+    LAUNCH(k_ef_finish, 1, 32, 0, st, S, n);
+    for (int i = 0; i < n; ++i) fs[i]->frame += 1;
+    return PSTF_OK;
+}
+
 int pstf_field_end_frame(pstf_field *f, void *stream) {
     if (!f) return set_err(PSTF_E_INVALID, "NULL argument");
-    CK(cudaSetDevice(f->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    DevStore s = dev_view(f);
-    const unsigned g = (unsigned)sm_count() * 4;
-    CK(cudaMemsetAsync(&s.ctr[C_EVICTED], 0, 8, st));
-    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, s);
-    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, s);
-    const unsigned long long cap = (unsigned long long)s.mask + 1ull;
-    const unsigned ge = std::min<unsigned>(grid_for(cap, 256), g);
-    LAUNCH(k_evict, ge, 256, 0, st, s);
-    /* roll the frame: keep the touched count for stats, clear per-frame scratch */
-    CK(cudaMemcpyAsync(&s.ctr[C_TOUCHED_LAST], &s.ctr[C_TOUCHED_N], 8, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(s.cn_sum, 0, 8, st));
-    CK(cudaMemsetAsync(&s.ctr[C_CN_COUNT], 0, 8, st));
-    CK(cudaMemsetAsync(&s.ctr[C_TOUCHED_N], 0, 8, st));
-    f->frame += 1;
-    return PSTF_OK;
+    return pstf_fields_end_frame(&f, 1, stream);
 }
 
 int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream) {
@@ -1923,18 +2355,17 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
     if (!count) return PSTF_OK;
     CK(cudaSetDevice(f->device));
     CK(cudaDeviceSynchronize());
-    std::vector<uint32_t> chk(count), last(count);
+    std::vector<uint2> meta(count);
     std::vector<double4> com(count), acc(count);
     std::vector<KeyFields> kf(count);
-    CK(cudaMemcpy(chk.data(), f->d.chk + begin, count * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(last.data(), f->d.last + begin, count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(meta.data(), f->d.meta + begin, count * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(com.data(), f->d.com + begin, count * 32, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(acc.data(), f->d.acc + begin, count * 32, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(kf.data(), f->d.keyf + begin, count * sizeof(KeyFields), cudaMemcpyDeviceToHost));
     for (uint64_t i = 0; i < count; ++i) {
         pstf_slot_record &r = out[i];
         memset(&r, 0, sizeof(r));
-        r.checksum = chk[i];
+        r.checksum = meta[i].x;
         r.level = kf[i].level;
         r.cell[0] = kf[i].c0;
         r.cell[1] = kf[i].c1;
@@ -1949,7 +2380,7 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
         r.accum[1] = acc[i].y;
         r.accum[2] = acc[i].z;
         r.c_new = acc[i].w;
-        r.last_touched = last[i];
+        r.last_touched = meta[i].y == 0 ? 0u : meta[i].y - 1u; /* stored biased by +1 */
     }
     return PSTF_OK;
 }
@@ -1972,7 +2403,54 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
     a.pend = lo->sc.pend.as<PendRec>();
     a.pend_count = lo->sc.pend_count.as<unsigned long long>();
     a.pend_cap = lo->sc.pend.bytes / sizeof(PendRec);
-    if (mode == PSTF_MODE_ATOMIC)
+    const bool shared_quant = a.same_lo_loe && a.same_fli_lo && a.same_li_fli;
+    /* TMA path: every SoA segment must be 16 B aligned for cp.async.bulk */
+    const void *ptrs[35] = {v->position.x, v->position.y, v->position.z, v->wo.x, v->wo.y,
+                            v->wo.z, v->wi.x, v->wi.y, v->wi.z, v->next_position.x,
+                            v->next_position.y, v->next_position.z, v->nee_dir.x, v->nee_dir.y,
+                            v->nee_dir.z, v->footprint, v->next_footprint, v->ratio,
+                            v->next_emis_mis_weight, v->emission_here.x, v->emission_here.y,
+                            v->emission_here.z, v->f.x, v->f.y, v->f.z, v->next_emission.x,
+                            v->next_emission.y, v->next_emission.z, v->nee_loe.x, v->nee_loe.y,
+                            v->nee_loe.z, v->nee_fli.x, v->nee_fli.y, v->nee_fli.z, v->flags};
+    bool aligned = true;
+    for (int k = 0; k < 35; ++k) aligned = aligned && ((uintptr_t)ptrs[k] % 16 == 0);
+    if (mode == PSTF_MODE_ATOMIC && shared_quant && aligned && !getenv("PSTF_NO_TMA")) {
+        VPArgs2 b;
+        memset(&b, 0, sizeof(b));
+        b.st = a.st;
+        b.fp = make_fast_params(lo->d.kp);
+        b.dbg = getenv("PSTF_VP_DBG") ? atoi(getenv("PSTF_VP_DBG")) : 0;
+        b.has_li = a.has_li;
+        b.loe_mask = loe_mask;
+        b.fli_mask = fli_mask;
+        for (int k = 0; k < PS_NUM_F64; ++k) b.fld[k] = (const double *)ptrs[k];
+        b.flags = v->flags;
+        b.n = n;
+        b.pend = a.pend;
+        b.pend_count = a.pend_count;
+        b.pend_cap = a.pend_cap;
+        /* (stages, CTAs/SM): 2x3 = TMA double buffering at 168 regs; 1x4 / 1x5 trade the
+         * prefetch depth for more resident warps (PSTF_TILED_CFG selects, default 2x3) */
+        const char *cfgs = getenv("PSTF_TILED_CFG");
+        const int cfg = cfgs ? atoi(cfgs) : 0;
+        const int stages = cfg == 0 ? 2 : 1;
+        const int minb = cfg == 0 ? 3 : (cfg == 1 ? 4 : 5);
+        const size_t smem = stages * sizeof(TileStage) + 64;
+        static bool attr[3] = {false, false, false};
+        if (!attr[cfg]) {
+            cudaError_t e = cfg == 0 ? cudaFuncSetAttribute(k_vertex_pass_tiled<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                          : cfg == 1 ? cudaFuncSetAttribute(k_vertex_pass_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                     : cudaFuncSetAttribute(k_vertex_pass_tiled<1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            CK(e);
+            attr[cfg] = true;
+        }
+        const uint64_t tiles = (n + VT - 1) / VT;
+        const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
+        if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
+        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
+        else LAUNCH((k_vertex_pass_tiled<1, 5>), grid, VT, smem, st, b);
+    } else if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
     else
         LAUNCH(k_vertex_pass<PSTF_MODE_ORDERED>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);

@@ -11,10 +11,12 @@
  *     explicit fma() appears only inside error-free transformations (two_prod).
  *   - floor(log2(s)) comes from the exponent bits plus an exact test of whether the correctly
  *     rounded log2(s) rounds up to the next integer (s a few ulps below a power of two).
- *   - atan2 is evaluated with the fast libm/libdevice routine; only when the resulting
- *     octahedral coordinate lies within 1e-11 of a directional-cell boundary is it recomputed
- *     with a double-double atan2 that returns the correctly rounded result (what glibc returns
- *     on >99.8% of inputs, SURVEY.md Appendix B libm probe).
+ *   - atan2 is evaluated with a fast polynomial; only when the resulting octahedral
+ *     coordinate lies within 1e-11 of a directional-cell boundary is it recomputed with a
+ *     double-double atan2 that returns the correctly rounded result (what glibc returns on
+ *     >99.8% of inputs, SURVEY.md Appendix B libm probe).  The fused vertex kernel also uses
+ *     approximate divisions / square roots with exact re-evaluation near cell boundaries
+ *     (see "fast shared per-vertex quantisation" below).
  *   - int32 conversions reproduce x86-64 cvttsd2si: NaN / out of range -> INT32_MIN.
  */
 #pragma once
@@ -36,6 +38,7 @@ struct Key {
     int32_t cell[3];
     int32_t dir[2];
     uint32_t checksum;
+    uint32_t pack_lo; /* low 32 bits of packKeyFields: home slot = pack_lo & mask */
 };
 
 struct KeyParams {
@@ -60,6 +63,16 @@ PSTF_HD uint64_t pack_key_fields(int32_t level, int32_t c0, int32_t c1, int32_t 
     h = mix_bits(h ^ (((uint64_t)(uint32_t)c2 << 32) | (uint32_t)d0));
     h = mix_bits(h ^ (uint64_t)(uint32_t)d1);
     return h;
+}
+
+/* packKeyFields split after its first round: keys sharing (level, cell0, cell1) share h1 */
+PSTF_HD uint64_t pack_h1(int32_t level, int32_t c0, int32_t c1) {
+    return mix_bits((uint64_t)(uint32_t)level ^ (((uint64_t)(uint32_t)c0 << 32) | (uint32_t)c1));
+}
+
+PSTF_HD uint64_t pack_from_h1(uint64_t h1, int32_t c2, int32_t d0, int32_t d1) {
+    uint64_t h = mix_bits(h1 ^ (((uint64_t)(uint32_t)c2 << 32) | (uint32_t)d0));
+    return mix_bits(h ^ (uint64_t)(uint32_t)d1);
 }
 
 PSTF_HD uint32_t checksum_of(uint64_t packed) {
@@ -297,7 +310,59 @@ PSTF_HD_NOINLINE double atan2_cr_pos(double y, double x) {
     return r.hi + r.lo;
 }
 
-PSTF_HD double atan2_fast(double y, double x) { return atan2(y, x); }
+/* Approximate reciprocal / square root for the fast (non-deciding) path: single-precision
+ * hardware estimate + Newton steps in fp64, relative error ~1e-16 for den in [1e-30, 1e30]. */
+PSTF_HD double fast_rcp(double den) {
+#if defined(__CUDA_ARCH__)
+    double r = (double)__frcp_rn((float)den);
+#else
+    double r = (double)(1.0f / (float)den);
+#endif
+    r = r * fma(-den, r, 2.0);
+    r = r * fma(-den, r, 2.0);
+    return r;
+}
+
+PSTF_HD double fast_sqrt01(double w) { /* w in [0, 1]; |error| < 1e-15 */
+    if (!(w >= 1e-30)) return 0.0;
+#if defined(__CUDA_ARCH__)
+    double y = (double)rsqrtf((float)w);
+#else
+    double y = (double)(1.0f / sqrtf((float)w));
+#endif
+    y = y * fma(-0.5 * w, y * y, 1.5);
+    y = y * fma(-0.5 * w, y * y, 1.5);
+    return w * y;
+}
+
+/* Fast atan2 for x, y >= 0 (|error| < 1e-15 rad): octant reduction to |t| <= tan(pi/8) with one
+ * approximate reciprocal, then a degree-9 polynomial in t^2 (Chebyshev-node fit).  Only used to
+ * pick the directional cell; results within 1e-11 of a cell boundary are recomputed with the
+ * correctly rounded atan2_cr_pos, so it never decides a key on its own near a boundary. */
+PSTF_HD double atan2_fast(double y, double x) {
+    if (!(x <= 1.7976931348623157e308 && y <= 1.7976931348623157e308)) return atan2_cr_pos(y, x);
+    const int swap = y > x;
+    const double a = swap ? x : y, b = swap ? y : x; /* 0 <= a <= b, b > 0 */
+    double t, base;
+    const bool small = a <= b * 0.41421356237309503;
+    const double num = small ? a : a - b, den = small ? b : a + b;
+    base = small ? 0.0 : 0.7853981633974483;
+    if (den >= 1e-30 && den <= 1e30) t = num * fast_rcp(den);
+    else t = num / den;
+    const double z = t * t;
+    double p = -0.025316479573776477;
+    p = fma(p, z, 0.05024762118940128);
+    p = fma(p, z, -0.0650598296717084);
+    p = fma(p, z, 0.07673535428183285);
+    p = fma(p, z, -0.09089529956562307);
+    p = fma(p, z, 0.11111048853751296);
+    p = fma(p, z, -0.14285712661684793);
+    p = fma(p, z, 0.19999999978392663);
+    p = fma(p, z, -0.3333333333322143);
+    p = fma(p, z, 0.999999999999999);
+    const double th = base + t * p;
+    return swap ? 1.5707963267948966 - th : th;
+}
 
 /* mappings.h:33-51 with the reference's operation order; exact_atan selects the slow path */
 PSTF_HD void sphere_to_square_impl(double dx, double dy, double dz, int exact_atan, double *uo,
@@ -354,12 +419,160 @@ PSTF_HD Key key_for(const KeyParams &p, double px, double py, double pz, double 
     k.cell[1] = i32_x86(floor(py / cs));
     k.cell[2] = i32_x86(floor(pz / cs));
     dir_cells(dx, dy, dz, dir_resolution(level), &k.dir[0], &k.dir[1]);
-    k.checksum = checksum_of(pack_key_fields(level, k.cell[0], k.cell[1], k.cell[2], k.dir[0], k.dir[1]));
+    uint64_t pk = pack_key_fields(level, k.cell[0], k.cell[1], k.cell[2], k.dir[0], k.dir[1]);
+    k.checksum = checksum_of(pk);
+    k.pack_lo = (uint32_t)pk;
     return k;
 }
 
 PSTF_HD uint64_t key_pack(const Key &k) {
     return pack_key_fields(k.level, k.cell[0], k.cell[1], k.cell[2], k.dir[0], k.dir[1]);
+}
+
+/* ---------------- fast shared per-vertex quantisation (same results as key_for) -------------
+ * Used by the fused vertex kernel.  Every key of a vertex uses the same position at the same
+ * level, every level of a lookup uses the same position and direction, and d / -d share their
+ * octahedral magnitudes.  Each quantity is first computed approximately (reciprocal multiply,
+ * polynomial atan2, Newton sqrt) and the exact reference operation is re-run only when the
+ * approximation lies within its error bound of a cell boundary:
+ *  cells     x' = p * (1/base) * 2^-l is within 2^-51 |x| of fl(p / (base 2^l)); if x' is further
+ *            than 2^-50 |x'| from every integer, floor(x') == floor(fl(p / cs)).
+ *  level     s' = footprint * (K / base) is within a few ulps of fl(fl(fp K) / base); away from
+ *            powers of two its exponent is floor(log2(s)); near them select_level runs exactly.
+ *  dirCell   u, v to ~1e-15 absolute; within 1e-11 of k/8 the correctly rounded path re-runs.
+ *            floor(U d) == floor(U 8) >> log2(8/d), so one floor per direction serves all
+ *            levels (U is in [0, 1] or NaN). */
+struct FastParams {
+    KeyParams kp;
+    double inv_base;   /* fl(1 / base) */
+    double k_inv_base; /* fl(K / base) */
+};
+
+PSTF_HD FastParams make_fast_params(const KeyParams &kp) {
+    FastParams f;
+    f.kp = kp;
+    f.inv_base = 1.0 / kp.base_cell_size;
+    f.k_inv_base = kp.level_select_k / kp.base_cell_size;
+    return f;
+}
+
+PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
+    if (!(footprint > 0.0)) return 0;
+    const double s = footprint * f.k_inv_base;
+    if (s > 1.0000000001 && s < 1e300) {
+        const uint64_t b = dbits(s);
+        const uint64_t mant = b & 0x000fffffffffffffULL;
+        /* mantissa not within 2^-40 of either end of [1, 2): exponent == floor(log2(s)) */
+        if (mant > (1ULL << 12) && mant < 0x000fffffffffffffULL - (1ULL << 12)) {
+            int level = (int)((b >> 52) & 0x7ff) - 1023;
+            return level < f.kp.max_level ? level : f.kp.max_level;
+        }
+    }
+    return select_level(f.kp, footprint);
+}
+
+struct PosQ {
+    double q[3];
+};
+
+PSTF_HD PosQ pos_q(const FastParams &f, double px, double py, double pz) {
+    PosQ r;
+    r.q[0] = px * f.inv_base;
+    r.q[1] = py * f.inv_base;
+    r.q[2] = pz * f.inv_base;
+    return r;
+}
+
+PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level) {
+    const double x = q * pow2d(-level);
+    const double ax = fabs(x);
+    if (ax >= 0x1p-900 && ax < 4294967296.0) {
+        const double fl = floor(x);
+        const double e = ax * 0x1p-50;
+        if (x - fl >= e && (fl + 1.0) - x >= e) return i32_x86(fl);
+    } else if (ax >= 4294967296.0 && ax <= 1.7976931348623157e308) {
+        return INT32_MIN; /* far outside int32: the reference's conversion gives INT32_MIN */
+    }
+    if (pcoord == 0.0) return 0;
+    return i32_x86(floor(pcoord / cell_size(f.kp, level))); /* exact reference operation */
+}
+
+/* pre-swap octahedral coordinates from |x|, |y|, |z| (mappings.h:34-42) */
+PSTF_HD void octa_base(double dx, double dy, double dz, int exact, double *u0, double *v0) {
+    double x = fabs(dx), y = fabs(dy), z = fabs(dz);
+    double omz = 1.0 - z;
+    double w = (0.0 < omz) ? omz : 0.0; /* safeSqrt: std::max(0.0, x) vecmath.h:22 */
+    double r = exact ? sqrt(w) : fast_sqrt01(w);
+    double phi;
+    if (x == 0.0 && y == 0.0) phi = 0.0;
+    else phi = (exact ? atan2_cr_pos(y, x) : atan2_fast(y, x)) * (2.0 / 3.14159265358979323846);
+    *v0 = phi * r;
+    *u0 = r - *v0;
+}
+
+/* hemisphere swap + sign restoration + [0,1]^2 (mappings.h:43-50) */
+PSTF_HD void octa_uv(double u0, double v0, double dx, double dy, double dz, double *U, double *V) {
+    double u = u0, v = v0;
+    if (dz < 0.0) {
+        double t = u;
+        u = v;
+        v = t;
+        u = 1.0 - u;
+        v = 1.0 - v;
+    }
+    u = copysign(u, dx);
+    v = copysign(v, dy);
+    *U = 0.5 * (u + 1.0);
+    *V = 0.5 * (v + 1.0);
+}
+
+/* floor(U * 8) with the reference's int32 conversion (NaN -> INT32_MIN); near = within 1e-11 */
+PSTF_HD int32_t f8_of(double U, int *near) {
+    const double q = U * 8.0;
+    const double fl = floor(q);
+    *near |= (q - fl) < 1e-11 || (fl + 1.0 - q) < 1e-11;
+    return i32_x86(fl);
+}
+
+struct DirF8 {
+    int32_t u, v;
+};
+
+/* octahedral cell coordinates (at resolution 8) of d and optionally -d, bit-identical to
+ * min(int32(sphereToSquare(d) * 8), ...) before the per-level clamp */
+PSTF_HD void octa_f8(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg) {
+    double u0, v0, U, V;
+    int near = 0;
+    octa_base(dx, dy, dz, 0, &u0, &v0);
+    octa_uv(u0, v0, dx, dy, dz, &U, &V);
+    pos->u = f8_of(U, &near);
+    pos->v = f8_of(V, &near);
+    if (want_neg) {
+        octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
+        neg->u = f8_of(U, &near);
+        neg->v = f8_of(V, &near);
+    }
+    if (near) {
+        int dummy = 0;
+        octa_base(dx, dy, dz, 1, &u0, &v0);
+        octa_uv(u0, v0, dx, dy, dz, &U, &V);
+        pos->u = f8_of(U, &dummy);
+        pos->v = f8_of(V, &dummy);
+        if (want_neg) {
+            octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
+            neg->u = f8_of(U, &dummy);
+            neg->v = f8_of(V, &dummy);
+        }
+    }
+}
+
+/* dirCell at a level from floor(U*8): min(floor(U*d), d-1) (field.cpp:93-95) */
+PSTF_HD int32_t dir_cell_f8(int32_t f8, int level) {
+    if (f8 == INT32_MIN) return INT32_MIN;
+    const int sh = level < 2 ? level : 2;
+    const int32_t d = 8 >> sh;
+    const int32_t c = f8 >> sh;
+    return c < d - 1 ? c : d - 1;
 }
 
 } // namespace pstf_b200

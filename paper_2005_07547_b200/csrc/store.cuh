@@ -2,15 +2,15 @@
  * store.cuh — HBM layout of one B200 field store and the device-side probe/touch helpers.
  *
  * One pstf::FieldStore (reference: proj/core/src/field.cpp:48-58, an AoS of 104 B slots) becomes
- * a set of slot-indexed SoA arrays so each kernel streams only what it needs:
+ * slot-indexed arrays so each kernel streams only what it needs:
  *
- *   chk   u32[cap]      checksum, 0 = empty                 (probe path, L2-resident: 4 B/slot)
+ *   meta  uint2[cap]    {checksum (0 = empty), lastTouched + 1 (0 = never touched)}
+ *                       one 8 B probe load gives identity and "already touched this frame"
  *   com   double4[cap]  {valueOld.rgb, cOld}  committed     (lookup reads one 32 B sector)
  *   acc   double4[cap]  {accum.rgb, cNew}     this frame    (fp64 RED target, one sector)
  *   keyf  KeyFields[cap] level, cell[3], dirCell[2]         (written on insert; snapshot/invalidate)
- *   last  u32[cap]      lastTouched                          (eviction age, field.cpp:123-137)
- *   tmark u32[cap]      frame+1 when the slot was first touched this frame (touched-list dedupe)
- *   touched u32[cap]    list of slots touched this frame -> endFrame works on touched cells only
+ *   (a slot was touched this frame iff meta.y == frame + 1; endFrame sweeps meta and works only
+ *    on those slots, so the hot kernels mark a touch with one plain store)
  *   hold  u32[2][cap]   deterministic-placement scratch (rank of the proposing key, ~0 = none)
  */
 #pragma once
@@ -30,23 +30,20 @@ enum Ctr : int {
     C_DROPPED,
     C_INTERNAL,
     C_LIVE,
-    C_TOUCHED_N,   // entries in the touched list
-    C_NEW_KEYS,    // keys placed by the last pass
-    C_EVICTED,     // evicted by the last endFrame
-    C_CN_COUNT,    // endFrame: live slots with cNew > 0
-    C_LIVE_SNAP,   // endFrame: live count before eviction (field.cpp:205-212)
+    C_TOUCHED_N,    // unused (kept for counter layout stability)
+    C_NEW_KEYS,     // keys placed by the last pass
+    C_EVICTED,      // evicted by the last endFrame
+    C_CN_COUNT,     // endFrame: live slots with cNew > 0
+    C_LIVE_SNAP,    // endFrame: live count before eviction (field.cpp:205-212)
     C_TOUCHED_LAST, // touched slots of the last committed frame
     C_NUM
 };
 
 struct DevStore {
-    uint32_t *chk;
+    uint2 *meta;
     double4 *com;
     double4 *acc;
     KeyFields *keyf;
-    uint32_t *last;
-    uint32_t *tmark;
-    uint32_t *touched;
     uint32_t *hold0, *hold1;
     unsigned long long *ctr; // C_NUM counters
     double *cn_sum;          // endFrame scratch
@@ -61,11 +58,15 @@ struct DevStore {
 
 #define PSTF_HOLD_NONE 0xffffffffu
 
+__device__ __forceinline__ uint32_t ld_chk(const DevStore &s, uint32_t idx) {
+    return s.meta[idx].x;
+}
+
 /* findSlot (field.cpp:103-114): slot index, or -1 */
 __device__ __forceinline__ int probe_find(const DevStore &s, uint32_t home, uint32_t cs) {
     for (uint32_t i = 0; i < s.window; ++i) {
         uint32_t idx = (home + i) & s.mask;
-        uint32_t c = __ldg(&s.chk[idx]);
+        uint32_t c = ld_chk(s, idx);
         if (c == cs) return (int)idx;
         if (c == 0) return -1;
     }
@@ -74,25 +75,65 @@ __device__ __forceinline__ int probe_find(const DevStore &s, uint32_t home, uint
 
 /* findOrInsertSlot's search over the frame-start table (field.cpp:116-146):
  * >= 0 existing slot, -1 an empty slot comes first (new key -> deterministic placement),
- * -2 window exhausted with no empty slot and no match (dropped; new keys cannot change that). */
-__device__ __forceinline__ int probe_existing(const DevStore &s, uint32_t home, uint32_t cs) {
+ * -2 window exhausted with no empty slot and no match (dropped; new keys cannot change that).
+ * *touched_mark receives the slot's lastTouched+1 word. */
+__device__ __forceinline__ int probe_existing(const DevStore &s, uint32_t home, uint32_t cs,
+                                              uint32_t *touched_mark) {
     for (uint32_t i = 0; i < s.window; ++i) {
         uint32_t idx = (home + i) & s.mask;
-        uint32_t c = s.chk[idx];
-        if (c == cs) return (int)idx;
-        if (c == 0) return -1;
+        uint2 m = s.meta[idx];
+        if (m.x == cs) {
+            *touched_mark = m.y;
+            return (int)idx;
+        }
+        if (m.x == 0) return -1;
     }
     return -2;
 }
 
-/* lastTouched = frame (field.cpp:123,133,137) + append to the touched list once per frame */
+/* lastTouched = frame (field.cpp:123,133,137); mark = the meta.y word seen by the probe, so an
+ * already-touched slot costs no store */
+__device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot, uint32_t mark) {
+    const uint32_t m = s.frame + 1u;
+    if (mark != m) s.meta[slot].y = m;
+}
+
 __device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot) {
-    if (s.last[slot] != s.frame) s.last[slot] = s.frame;
-    uint32_t m = s.frame + 1u;
-    if (s.tmark[slot] != m && atomicExch(&s.tmark[slot], m) != m) {
-        unsigned long long pos = atomicAdd(&s.ctr[C_TOUCHED_N], 1ull);
-        s.touched[pos] = slot;
+    s.meta[slot].y = s.frame + 1u;
+}
+
+/* finish a probe whose home-slot word m0 was already loaded (findOrInsertSlot's search) */
+__device__ __forceinline__ int resolve_probe(const DevStore &s, uint32_t home, uint32_t cs,
+                                             uint2 m0, uint32_t *mark) {
+    if (m0.x == cs) {
+        *mark = m0.y;
+        return (int)home;
     }
+    if (m0.x == 0) return -1;
+    for (uint32_t i = 1; i < s.window; ++i) {
+        uint32_t idx = (home + i) & s.mask;
+        uint2 m = s.meta[idx];
+        if (m.x == cs) {
+            *mark = m.y;
+            return (int)idx;
+        }
+        if (m.x == 0) return -1;
+    }
+    return -2;
+}
+
+/* finish a findSlot (lookup) whose home word was already loaded: slot or -1 */
+__device__ __forceinline__ int resolve_find(const DevStore &s, uint32_t home, uint32_t cs,
+                                            uint32_t c0) {
+    if (c0 == cs) return (int)home;
+    if (c0 == 0) return -1;
+    for (uint32_t i = 1; i < s.window; ++i) {
+        uint32_t idx = (home + i) & s.mask;
+        uint32_t c = s.meta[idx].x;
+        if (c == cs) return (int)idx;
+        if (c == 0) return -1;
+    }
+    return -1;
 }
 
 } // namespace pstf_b200

@@ -94,6 +94,7 @@ def lib():
         "pstf_field_apply": ([vp, vp, vp, vp, vp, u64, i32, vp], i32),
         "pstf_field_query": ([vp, vp, vp, vp, vp, u64, vp, vp, vp, vp, vp, vp, vp], i32),
         "pstf_field_end_frame": ([vp, vp], i32),
+        "pstf_fields_end_frame": ([vp, i32, vp], i32),
         "pstf_field_invalidate": ([vp, vp, vp], i32),
         "pstf_field_get_stats": ([vp, vp], i32),
         "pstf_field_weighted_mean": ([vp, vp], i32),
@@ -497,6 +498,16 @@ def _soa3(x, device):
     if x.dim() == 2 and x.shape[1] == 3:
         x = x.t()
     return x.to(device).contiguous()
+
+
+def end_frame_all(stores):
+    """endFrame on up to 4 stores of one device with one pair of sweeps (frame barrier,
+    estimators.cpp:647-651); identical to calling end_frame on each."""
+    stores = [s for s in stores if s is not None]
+    for s in stores:
+        s.flush()
+    arr = (C.c_void_p * len(stores))(*[s._h.value for s in stores])
+    _check(lib().pstf_fields_end_frame(arr, len(stores), _stream()))
 
 
 def read_snapshot(path: str):

@@ -228,6 +228,24 @@ def test_vertex_pass_vs_oracle(mode, cap, mult, li, evict):
                 assert st[k] == so[k], (it, k, st[k], so[k])
 
 
+@pytest.mark.parametrize("w,h,b", [(97, 53, 4), (33, 21, 3), (128, 1, 4), (5, 3, 2)])
+def test_vertex_pass_shapes(w, h, b):
+    """Tail tiles (n % 128 != 0), unaligned SoA segments (odd n -> non-TMA kernel) and tiny
+    streams all give the oracle's occupancy/counters and values (ATOMIC)."""
+    o, g = _vertex_stores(14, inputs.BASE_CORNELL * 6.0, li=True, evict=2)
+    for it in range(3):
+        buf, n = pb.synth_generate(w, h, b, iteration=it)
+        pb.vertex_pass(*g, buf, n, mode=pb.MODE_ATOMIC)
+        po.vertex_pass_oracle(*o, buf.cpu().numpy(), n, deterministic=True)
+        for a, c in zip(g, o):
+            a.end_frame()
+            c.end_frame()
+            gu.assert_slots_close(a.slots(), c.slots(), rtol=1e-9)
+            st, so = a.stats(), c.stats()
+            for k in ("frame", "rejected", "dropped", "internal_errors", "live"):
+                assert st[k] == so[k], (it, k, st[k], so[k])
+
+
 def test_vertex_pass_matches_reference_replay():
     """Against the reference FieldStore itself (EstimatorRun deterministic-mode replay)."""
     if not po.ref_available():

@@ -91,3 +91,45 @@ def test_atan2_slow_path_is_correctly_rounded(kh):
     kh.kh_atan2_cr_batch(_p(y), _p(x), C.c_int64(len(y)), _p(out))
     exact = np.array([float(mp.atan2(mp.mpf(a), mp.mpf(b))) for a, b in zip(y, x)])
     np.testing.assert_array_equal(out, exact)
+
+
+@pytest.mark.parametrize("negate", [0, 1])
+@pytest.mark.parametrize("base", [0.5, inputs.BASE_CORNELL, 1e-300, 1e300])
+def test_shared_quantisation_identities(kh, negate, base):
+    """The fast kernel's shared per-vertex quantisation (one division per coordinate for all
+    levels; one atan2 for d and -d) gives exactly the reference keyFor keys."""
+    cfg = po.Config.make(capacity_log2=10, base_cell_size=base, max_level=6)
+    ref = _checker(cfg)
+    rng = np.random.default_rng(77 + negate)
+    d = np.concatenate([inputs.random_dirs(rng, 40000), inputs.boundary_dirs(rng, 40000),
+                        inputs.structured_dirs(), inputs.special_dirs()])
+    n = len(d)
+    pos = np.concatenate([inputs.random_positions(rng, n - 8), inputs.special_positions()])
+    pos[:200] *= 1e-310  # subnormal positions exercise the direct-division fallback
+    # positions on (or an ulp off) cell boundaries at every level exercise the exact re-check
+    k = rng.integers(-300, 300, size=(3000, 3)).astype(np.float64)
+    on = k * base * np.exp2(rng.integers(0, 7, size=(3000, 1)))
+    pos[200:3200] = np.where(rng.random((3000, 3)) < 0.3, np.nextafter(on, np.inf), on)
+    for level in range(cfg.max_level + 1):
+        lv = np.full(n, level, np.int32)
+        out = np.zeros(n, po.KEY_DTYPE)
+        pT, dT = np.ascontiguousarray(pos.T), np.ascontiguousarray(d.T)
+        kh.kh_key_for_shared_batch(C.c_double(base), C.c_double(4.0), C.c_int(6), _p(pT), _p(dT),
+                                   _p(lv), C.c_int64(n), C.c_int(negate), _p(out))
+        want = ref.keys_for(pos, -d if negate else d, lv)
+        bad = _mismatch(out, want)
+        assert bad.sum() == 0, (level, np.nonzero(bad)[0][:10])
+
+
+@pytest.mark.parametrize("max_level", [4, 60])
+def test_select_level_fast_matches_reference(kh, max_level):
+    """select_level_fast (reciprocal multiply + exponent, exact path near powers of two)."""
+    cfg = po.Config.make(capacity_log2=10, base_cell_size=inputs.BASE_CORNELL, max_level=max_level)
+    ref = _checker(cfg)
+    rng = np.random.default_rng(max_level + 5)
+    fp = np.concatenate([inputs.level_footprints(cfg.base_cell_size, max_exp=max_level + 2),
+                         inputs.random_footprints(rng, 300000, cfg.base_cell_size)])
+    out = np.zeros(len(fp), np.int32)
+    kh.kh_select_level_fast_batch(C.c_double(cfg.base_cell_size), C.c_double(4.0),
+                                  C.c_int(max_level), _p(fp), C.c_int64(len(fp)), _p(out))
+    np.testing.assert_array_equal(out, ref.select_levels(fp))
