@@ -1392,141 +1392,135 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 #define EF_BLOCK 256
 
-/* Pass 1 (field.cpp:205-216) for every store of the batch: sweep meta (8 B/slot, coalesced),
- * sum c_new over live slots touched this frame (meta.y == frame+1; untouched slots have zero
- * accumulators by construction), count them, and snapshot `live` for the eviction rule. */
+/* Pass 1 (field.cpp:205-216) for every store of the batch: compact the touched-slot bitmap into
+ * tlist (clearing it), sum c_new over those slots (untouched slots have zero accumulators by
+ * construction) and snapshot `live` for the eviction rule. */
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
     __shared__ double ssum[EF_BLOCK / 32];
-    __shared__ unsigned long long scnt[EF_BLOCK / 32], stch[EF_BLOCK / 32];
+    __shared__ unsigned long long scnt[EF_BLOCK / 32];
     for (int j = 0; j < nst; ++j) {
         const DevStore &s = st.s[j];
         if (blockIdx.x == 0 && threadIdx.x == 0) s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
-        const uint64_t cap = (uint64_t)s.mask + 1;
-        const uint32_t m1 = s.frame + 1u;
+        const uint64_t nwords = ((uint64_t)s.mask + 32) / 32;
         double sum = 0.0;
-        unsigned cnt = 0, tch = 0;
-        /* 16 B loads cover two slot words; two of them in flight per iteration */
-        const uint4 *m4 = reinterpret_cast<const uint4 *>(s.meta);
-        const uint64_t npairs = cap / 2, stride = (uint64_t)gridDim.x * blockDim.x;
-        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npairs;
-             p += 2 * stride) {
-            const uint4 a4 = m4[p];
-            const uint4 b4 = p + stride < npairs ? m4[p + stride] : make_uint4(0, 0, 0, 0);
-            const uint32_t xs[4] = {a4.x, a4.z, b4.x, b4.z}, ys[4] = {a4.y, a4.w, b4.y, b4.w};
-            const uint64_t idx[4] = {2 * p, 2 * p + 1, 2 * (p + stride), 2 * (p + stride) + 1};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (xs[k] != 0 && ys[k] == m1) {
-                    ++tch;
-                    const double cn = s.acc[idx[k]].w;
-                    if (cn > 0.0) {
-                        sum += cn;
-                        ++cnt;
-                    }
+        unsigned cnt = 0;
+        const unsigned lane = lane_id();
+        /* every lane of a warp runs the same number of iterations (shuffles below) */
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        const uint64_t iters = (nwords + stride - 1) / stride;
+        for (uint64_t it = 0; it < iters; ++it) {
+            const uint64_t wi = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+            uint32_t w = wi < nwords ? s.tbits[wi] : 0u;
+            if (w) s.tbits[wi] = 0u;
+            const unsigned c = __popc(w);
+            unsigned incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += t;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+            if (!total) continue;
+            unsigned long long base = 0;
+            if (lane == 31) base = atomicAdd(&s.ctr[C_TOUCHED_N], (unsigned long long)total);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            unsigned long long pos = base + (incl - c);
+            while (w) {
+                const uint32_t slot = (uint32_t)(wi * 32 + (uint64_t)(__ffs(w) - 1));
+                w &= w - 1;
+                s.tlist[pos++] = slot;
+                const double cn = s.acc[slot].w;
+                if (cn > 0.0) {
+                    sum += cn;
+                    ++cnt;
                 }
             }
         }
         sum = warp_sum_d(sum);
         cnt = __reduce_add_sync(0xffffffffu, cnt);
-        tch = __reduce_add_sync(0xffffffffu, tch);
-        if (lane_id() == 0) {
+        if (lane == 0) {
             ssum[threadIdx.x >> 5] = sum;
             scnt[threadIdx.x >> 5] = cnt;
-            stch[threadIdx.x >> 5] = tch;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
-            unsigned long long c = 0, h = 0;
+            unsigned long long c = 0;
             for (int w = 0; w < EF_BLOCK / 32; ++w) {
                 t += ssum[w];
                 c += scnt[w];
-                h += stch[w];
             }
             if (c) {
                 atomicAdd(s.cn_sum, t);
                 atomicAdd(&s.ctr[C_CN_COUNT], c);
             }
-            if (h) atomicAdd(&s.ctr[C_TOUCHED_N], h);
         }
         __syncthreads();
     }
 }
 
-/* Passes 2+3 (field.cpp:218-260) fused per slot: blend + cap the touched slots, zero their
- * accumulators, then age-evict when live*4 > capacity*3 (live taken before any eviction). */
+/* Pass 2 (field.cpp:218-245) over the touched list: blend + cap, zero the accumulators. */
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
     for (int j = 0; j < nst; ++j) {
         const DevStore &s = st.s[j];
-        const uint64_t cap = (uint64_t)s.mask + 1;
-        const uint32_t m1 = s.frame + 1u;
+        const uint64_t n = s.ctr[C_TOUCHED_N];
         const unsigned long long cnt = s.ctr[C_CN_COUNT];
         const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
         const double tMax = s.t_max;
         const bool limited = tMax > 0.0 && isfinite(tMax);
         const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
-        const bool evict = s.ctr[C_LIVE_SNAP] * 4ull > (unsigned long long)cap * 3ull;
-        unsigned internal = 0, ev = 0;
-        const uint4 *m4 = reinterpret_cast<const uint4 *>(s.meta);
-        const uint64_t npairs = cap / 2, stride = (uint64_t)gridDim.x * blockDim.x;
-        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npairs;
-             p += 2 * stride) {
-            const uint4 a4 = m4[p];
-            const uint4 b4 = p + stride < npairs ? m4[p + stride] : make_uint4(0, 0, 0, 0);
-            const uint32_t xs[4] = {a4.x, a4.z, b4.x, b4.z}, ys[4] = {a4.y, a4.w, b4.y, b4.w};
-            const uint64_t idx[4] = {2 * p, 2 * p + 1, 2 * (p + stride), 2 * (p + stride) + 1};
-            bool tk[4];
-            double4 av[4], cv[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) { /* issue all loads first */
-                tk[k] = xs[k] != 0 && ys[k] == m1;
-                av[k] = tk[k] ? s.acc[idx[k]] : make_double4(0.0, 0.0, 0.0, 0.0);
-                cv[k] = tk[k] ? s.com[idx[k]] : make_double4(0.0, 0.0, 0.0, 0.0);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (xs[k] == 0) continue;
-                const uint64_t i = idx[k];
-                if (tk[k]) {
-                    const double4 a = av[k];
-                    const double cn = a.w;
-                    if (cn > 0.0) {
-                        double4 c = cv[k];
-                        const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
-                        double alpha =
-                            s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
-                        if (limited) {
-                            const double fl = 1.0 / tMax;
-                            alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
-                        }
-                        const double oma = 1.0 - alpha;
-                        c.x = c.x * oma + cx * alpha;
-                        c.y = c.y * oma + cy * alpha;
-                        c.z = c.z * oma + cz * alpha;
-                        c.w = c.w + cn;
-                        if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
-                        s.com[i] = c;
-                    } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
-                        ++internal;
-                    }
-                    if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
-                        s.acc[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+        unsigned internal = 0;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const uint32_t slot = s.tlist[i];
+            const double4 a = s.acc[slot];
+            const double cn = a.w;
+            if (cn > 0.0) {
+                double4 c = s.com[slot];
+                const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+                double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+                if (limited) {
+                    const double fl = 1.0 / tMax;
+                    alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
                 }
-                if (evict && (uint32_t)(s.frame - (ys[k] - 1u)) >= s.evict_age) {
-                    s.meta[i].x = 0;
-                    s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
-                    ++ev;
-                }
+                const double oma = 1.0 - alpha;
+                c.x = c.x * oma + cx * alpha;
+                c.y = c.y * oma + cy * alpha;
+                c.z = c.z * oma + cz * alpha;
+                c.w = c.w + cn;
+                if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+                s.com[slot] = c;
+            } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+                ++internal;
             }
+            if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
+                s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
         }
         internal = __reduce_add_sync(0xffffffffu, internal);
-        ev = __reduce_add_sync(0xffffffffu, ev);
-        if (lane_id() == 0) {
-            if (internal) atomicAdd(&s.ctr[C_INTERNAL], (unsigned long long)internal);
-            if (ev) {
-                atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
-                atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
+        if (lane_id() == 0 && internal) atomicAdd(&s.ctr[C_INTERNAL], (unsigned long long)internal);
+    }
+}
+
+/* Pass 3 (field.cpp:247-260): age eviction, only when live*4 > capacity*3 (live before
+ * eviction); the kernel exits at once otherwise. */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst) {
+    for (int j = 0; j < nst; ++j) {
+        const DevStore &s = st.s[j];
+        const uint64_t cap = (uint64_t)s.mask + 1;
+        if (!(s.ctr[C_LIVE_SNAP] * 4ull > (unsigned long long)cap * 3ull)) continue;
+        unsigned ev = 0;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const uint2 m = s.meta[i];
+            if (m.x != 0 && (uint32_t)(s.frame - (m.y - 1u)) >= s.evict_age) {
+                s.meta[i].x = 0;
+                s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+                ++ev;
             }
+        }
+        ev = __reduce_add_sync(0xffffffffu, ev);
+        if (lane_id() == 0 && ev) {
+            atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
+            atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
         }
     }
 }
@@ -2020,7 +2014,9 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
         return o;
     };
     size_t o_meta = take(cap * 8), o_com = take(cap * 32), o_acc = take(cap * 32),
-           o_keyf = take(cap * sizeof(KeyFields)), o_h0 = take(cap * 4), o_h1 = take(cap * 4), o_ctr = take(C_NUM * 8), o_sum = take(8);
+           o_keyf = take(cap * sizeof(KeyFields)), o_h0 = take(cap * 4), o_h1 = take(cap * 4),
+           o_tbits = take(((cap + 31) / 32) * 4), o_tlist = take(cap * 4), o_ctr = take(C_NUM * 8),
+           o_sum = take(8);
     cudaError_t e = cudaMalloc(&f->arena, off);
     if (e != cudaSuccess) {
         delete f;
@@ -2033,6 +2029,8 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     d.com = (double4 *)(base + o_com);
     d.acc = (double4 *)(base + o_acc);
     d.keyf = (KeyFields *)(base + o_keyf);
+    d.tbits = (uint32_t *)(base + o_tbits);
+    d.tlist = (uint32_t *)(base + o_tlist);
     d.hold0 = (uint32_t *)(base + o_h0);
     d.hold1 = (uint32_t *)(base + o_h1);
     d.ctr = (unsigned long long *)(base + o_ctr);
@@ -2182,6 +2180,7 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
     LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n);
     LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n);
+    LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n);
     LAUNCH(k_ef_finish, 1, 32, 0, st, S, n);
     for (int i = 0; i < n; ++i) fs[i]->frame += 1;
     return PSTF_OK;
@@ -2431,9 +2430,10 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         b.pend_count = a.pend_count;
         b.pend_cap = a.pend_cap;
         /* (stages, CTAs/SM): 2x3 = TMA double buffering at 168 regs; 1x4 / 1x5 trade the
-         * prefetch depth for more resident warps (PSTF_TILED_CFG selects, default 2x3) */
+         * prefetch depth (the next tile is prefetched into L2) for more resident warps;
+         * 1x4 measured fastest on config 2 (PSTF_TILED_CFG selects, default 1) */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? atoi(cfgs) : 0;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : (cfg == 1 ? 4 : 5);
         const size_t smem = stages * sizeof(TileStage) + 64;

@@ -442,6 +442,16 @@ PSTF_HD uint64_t key_pack(const Key &k) {
  *  dirCell   u, v to ~1e-15 absolute; within 1e-11 of k/8 the correctly rounded path re-runs.
  *            floor(U d) == floor(U 8) >> log2(8/d), so one floor per direction serves all
  *            levels (U is in [0, 1] or NaN). */
+/* rare exact re-evaluations kept out of line (instruction-cache footprint of the hot kernel) */
+PSTF_HD int select_level_exact(const KeyParams &p, double footprint) {
+    return select_level(p, footprint);
+}
+
+PSTF_HD int32_t cell_exact(const KeyParams &p, double pcoord, int level) {
+    if (pcoord == 0.0) return 0;
+    return i32_x86(floor(pcoord / cell_size(p, level)));
+}
+
 struct FastParams {
     KeyParams kp;
     double inv_base;   /* fl(1 / base) */
@@ -468,7 +478,7 @@ PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
             return level < f.kp.max_level ? level : f.kp.max_level;
         }
     }
-    return select_level(f.kp, footprint);
+    return select_level_exact(f.kp, footprint);
 }
 
 struct PosQ {
@@ -493,8 +503,7 @@ PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level)
     } else if (ax >= 4294967296.0 && ax <= 1.7976931348623157e308) {
         return INT32_MIN; /* far outside int32: the reference's conversion gives INT32_MIN */
     }
-    if (pcoord == 0.0) return 0;
-    return i32_x86(floor(pcoord / cell_size(f.kp, level))); /* exact reference operation */
+    return cell_exact(f.kp, pcoord, level); /* exact reference operation */
 }
 
 /* pre-swap octahedral coordinates from |x|, |y|, |z| (mappings.h:34-42) */
@@ -538,6 +547,21 @@ struct DirF8 {
     int32_t u, v;
 };
 
+PSTF_HD void octa_f8_exact(double dx, double dy, double dz, int want_neg, DirF8 *pos,
+                                    DirF8 *neg) {
+    double u0, v0, U, V;
+    int dummy = 0;
+    octa_base(dx, dy, dz, 1, &u0, &v0);
+    octa_uv(u0, v0, dx, dy, dz, &U, &V);
+    pos->u = f8_of(U, &dummy);
+    pos->v = f8_of(V, &dummy);
+    if (want_neg) {
+        octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
+        neg->u = f8_of(U, &dummy);
+        neg->v = f8_of(V, &dummy);
+    }
+}
+
 /* octahedral cell coordinates (at resolution 8) of d and optionally -d, bit-identical to
  * min(int32(sphereToSquare(d) * 8), ...) before the per-level clamp */
 PSTF_HD void octa_f8(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg) {
@@ -552,18 +576,7 @@ PSTF_HD void octa_f8(double dx, double dy, double dz, int want_neg, DirF8 *pos, 
         neg->u = f8_of(U, &near);
         neg->v = f8_of(V, &near);
     }
-    if (near) {
-        int dummy = 0;
-        octa_base(dx, dy, dz, 1, &u0, &v0);
-        octa_uv(u0, v0, dx, dy, dz, &U, &V);
-        pos->u = f8_of(U, &dummy);
-        pos->v = f8_of(V, &dummy);
-        if (want_neg) {
-            octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
-            neg->u = f8_of(U, &dummy);
-            neg->v = f8_of(V, &dummy);
-        }
-    }
+    if (near) octa_f8_exact(dx, dy, dz, want_neg, pos, neg);
 }
 
 /* dirCell at a level from floor(U*8): min(floor(U*d), d-1) (field.cpp:93-95) */

@@ -9,8 +9,9 @@
  *   com   double4[cap]  {valueOld.rgb, cOld}  committed     (lookup reads one 32 B sector)
  *   acc   double4[cap]  {accum.rgb, cNew}     this frame    (fp64 RED target, one sector)
  *   keyf  KeyFields[cap] level, cell[3], dirCell[2]         (written on insert; snapshot/invalidate)
- *   (a slot was touched this frame iff meta.y == frame + 1; endFrame sweeps meta and works only
- *    on those slots, so the hot kernels mark a touch with one plain store)
+ *   tbits u32[cap/32]    touched-this-frame bitmap: a slot's first touch in a frame (seen via
+ *                       meta.y != frame + 1) sets its bit with a fire-and-forget RED.OR
+ *   tlist u32[cap]       endFrame compacts the bitmap into this list and blends only those slots
  *   hold  u32[2][cap]   deterministic-placement scratch (rank of the proposing key, ~0 = none)
  */
 #pragma once
@@ -30,7 +31,7 @@ enum Ctr : int {
     C_DROPPED,
     C_INTERNAL,
     C_LIVE,
-    C_TOUCHED_N,    // unused (kept for counter layout stability)
+    C_TOUCHED_N,    // entries in tlist (endFrame of the current frame)
     C_NEW_KEYS,     // keys placed by the last pass
     C_EVICTED,      // evicted by the last endFrame
     C_CN_COUNT,     // endFrame: live slots with cNew > 0
@@ -44,6 +45,8 @@ struct DevStore {
     double4 *com;
     double4 *acc;
     KeyFields *keyf;
+    uint32_t *tbits;
+    uint32_t *tlist;
     uint32_t *hold0, *hold1;
     unsigned long long *ctr; // C_NUM counters
     double *cn_sum;          // endFrame scratch
@@ -95,11 +98,15 @@ __device__ __forceinline__ int probe_existing(const DevStore &s, uint32_t home, 
  * already-touched slot costs no store */
 __device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot, uint32_t mark) {
     const uint32_t m = s.frame + 1u;
-    if (mark != m) s.meta[slot].y = m;
+    if (mark != m) {
+        s.meta[slot].y = m;
+        atomicOr(&s.tbits[slot >> 5], 1u << (slot & 31u)); /* RED.OR, idempotent */
+    }
 }
 
 __device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot) {
     s.meta[slot].y = s.frame + 1u;
+    atomicOr(&s.tbits[slot >> 5], 1u << (slot & 31u));
 }
 
 /* finish a probe whose home-slot word m0 was already loaded (findOrInsertSlot's search) */
