@@ -105,6 +105,7 @@ typedef struct pstf_field_stats {
     uint64_t new_keys_last;   /* keys placed by the last update pass */
     uint64_t evicted_last;    /* slots evicted by the last endFrame */
     uint64_t placement_rounds_last; /* deterministic-placement rounds of the last pass */
+    uint64_t touched_total;   /* touched slots summed over all committed frames */
 } pstf_field_stats;
 
 /* Three coordinate arrays of one fp64 vector field (device pointers) */
@@ -152,6 +153,21 @@ int pstf_key_for(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_
 int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *value,
                      const double *w, const uint8_t *is_counter, uint64_t n, int mode,
                      void *stream);
+
+/* Host-pointer variants of the small-batch calls (scalar facade use: the C++ drop-in header
+ * paper_2005_07547_b200/cxx/include/pstf/field.h).  Inputs/outputs are host arrays, staged
+ * through the store's device scratch; the call returns when the result is on the host.
+ * pos/dir are AoS xyz triples here (Vec3 layout). */
+int pstf_key_for_host(const pstf_field *f, const double *pos_xyz, const double *dir_xyz,
+                      const int32_t *level, uint64_t n, pstf_key *keys);
+int pstf_select_level_host(const pstf_field *f, const double *footprint, int32_t *level,
+                           uint64_t n);
+int pstf_field_apply_host(pstf_field *f, const pstf_key *keys, const double *rgb_xyz,
+                          const double *w, const uint8_t *is_counter, uint64_t n, int mode);
+int pstf_field_query_host(const pstf_field *f, const double *pos_xyz, const double *dir_xyz,
+                          const double *footprint, const int32_t *level, uint64_t n,
+                          double *value_rgb, uint8_t *valid, uint8_t *fallback,
+                          int32_t *out_level);
 
 /* query(pos, dir, footprint) / queryFromLevel(pos, dir, level) field.h:93-94, batched.
  * Exactly one of footprint / level is non-NULL.  Outputs: value (3 arrays), valid, fallback,

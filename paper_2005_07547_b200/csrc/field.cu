@@ -162,6 +162,7 @@ struct Scratch {
     DBuf changed;
     DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
     DBuf snap;                              // snapshot gather
+    DBuf hio;                               // host-pointer API staging
     unsigned long long *h_small = nullptr;  // pinned readback
     ~Scratch() {
         if (h_small) cudaFreeHost(h_small);
@@ -177,6 +178,7 @@ struct pstf_field {
     void *arena = nullptr;
     Scratch sc;
     uint64_t new_keys_last = 0, rounds_last = 0;
+    std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
 };
 
 static DevStore dev_view(const pstf_field *f) {
@@ -1531,6 +1533,7 @@ __global__ void k_ef_finish(Stores4 st, int nst) {
     if (j >= nst) return;
     const DevStore &s = st.s[j];
     s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
+    s.ctr[C_TOUCHED_TOTAL] += s.ctr[C_TOUCHED_N];
     s.ctr[C_TOUCHED_N] = 0;
     s.ctr[C_CN_COUNT] = 0;
     *s.cn_sum = 0.0;
@@ -2146,6 +2149,146 @@ int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *v
     return resolve_pending(sc, fs, 1, mode, known, st);
 }
 
+/* ---- host-pointer variants (scalar facade): stage through device scratch, synchronise ---- */
+static int stage_h2d(Scratch &sc, const std::vector<const void *> &src,
+                     const std::vector<size_t> &bytes, std::vector<char *> &dst) {
+    size_t tot = 0;
+    for (size_t b : bytes) tot += (b + 255) & ~(size_t)255;
+    ENSURE(sc.hio, tot + 256);
+    char *p = sc.hio.as<char>();
+    dst.clear();
+    for (size_t k = 0; k < src.size(); ++k) {
+        dst.push_back(p);
+        if (src[k] && bytes[k]) CK(cudaMemcpy(p, src[k], bytes[k], cudaMemcpyHostToDevice));
+        p += (bytes[k] + 255) & ~(size_t)255;
+    }
+    return PSTF_OK;
+}
+
+static void aos_to_soa(const double *aos, uint64_t n, std::vector<double> &soa) {
+    soa.resize(3 * n);
+    for (uint64_t i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) soa[c * n + i] = aos[3 * i + c];
+}
+
+int pstf_key_for_host(const pstf_field *f, const double *pos_xyz, const double *dir_xyz,
+                      const int32_t *level, uint64_t n, pstf_key *keys) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    std::lock_guard<std::mutex> lk(const_cast<pstf_field *>(f)->host_mu);
+    if (!f || (n && (!pos_xyz || !dir_xyz || !level || !keys)))
+        return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<double> p, d;
+    aos_to_soa(pos_xyz, n, p);
+    aos_to_soa(dir_xyz, n, d);
+    std::vector<char *> dv;
+    Scratch &sc = const_cast<pstf_field *>(f)->sc;
+    int rc = stage_h2d(sc, {p.data(), d.data(), level, nullptr},
+                       {p.size() * 8, d.size() * 8, n * 4, n * sizeof(pstf_key)}, dv);
+    if (rc) return rc;
+    const double *dp = (const double *)dv[0], *dd = (const double *)dv[1];
+    pstf_vec3_soa ps{dp, dp + n, dp + 2 * n}, ds{dd, dd + n, dd + 2 * n};
+    rc = pstf_key_for(f, &ps, &ds, (const int32_t *)dv[2], n, (pstf_key *)dv[3], nullptr);
+    if (rc) return rc;
+    CK(cudaMemcpy(keys, dv[3], n * sizeof(pstf_key), cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
+int pstf_select_level_host(const pstf_field *f, const double *footprint, int32_t *level,
+                           uint64_t n) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    std::lock_guard<std::mutex> lk(const_cast<pstf_field *>(f)->host_mu);
+    if (!f || (n && (!footprint || !level))) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<char *> dv;
+    Scratch &sc = const_cast<pstf_field *>(f)->sc;
+    int rc = stage_h2d(sc, {footprint, nullptr}, {n * 8, n * 4}, dv);
+    if (rc) return rc;
+    rc = pstf_select_level(f, (const double *)dv[0], (int32_t *)dv[1], n, nullptr);
+    if (rc) return rc;
+    CK(cudaMemcpy(level, dv[1], n * 4, cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
+int pstf_field_apply_host(pstf_field *f, const pstf_key *keys, const double *rgb_xyz,
+                          const double *w, const uint8_t *is_counter, uint64_t n, int mode) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    std::lock_guard<std::mutex> lk(const_cast<pstf_field *>(f)->host_mu);
+    if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<double> v;
+    if (rgb_xyz) aos_to_soa(rgb_xyz, n, v);
+    std::vector<char *> dv;
+    /* staging lives in its own buffer: pstf_field_apply reuses the store scratch */
+    static thread_local DBuf io;
+    size_t sz[4] = {n * sizeof(pstf_key), rgb_xyz ? 3 * n * 8 : 0, n * 8, is_counter ? n : 0};
+    size_t tot = 0;
+    for (size_t b : sz) tot += (b + 255) & ~(size_t)255;
+    ENSURE(io, tot + 256);
+    char *p = io.as<char>();
+    const void *src[4] = {keys, rgb_xyz ? (const void *)v.data() : nullptr, w, is_counter};
+    for (int k = 0; k < 4; ++k) {
+        dv.push_back(p);
+        if (src[k] && sz[k]) CK(cudaMemcpy(p, src[k], sz[k], cudaMemcpyHostToDevice));
+        p += (sz[k] + 255) & ~(size_t)255;
+    }
+    const double *dvv = (const double *)dv[1];
+    pstf_vec3_soa vs{dvv, dvv + n, dvv + 2 * n};
+    int rc = pstf_field_apply(f, (const pstf_key *)dv[0], rgb_xyz ? &vs : nullptr,
+                              (const double *)dv[2], is_counter ? (const uint8_t *)dv[3] : nullptr,
+                              n, mode, nullptr);
+    if (rc) return rc;
+    CK(cudaDeviceSynchronize());
+    return PSTF_OK;
+}
+
+int pstf_field_query_host(const pstf_field *f, const double *pos_xyz, const double *dir_xyz,
+                          const double *footprint, const int32_t *level, uint64_t n,
+                          double *value_rgb, uint8_t *valid, uint8_t *fallback,
+                          int32_t *out_level) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    std::lock_guard<std::mutex> lk(const_cast<pstf_field *>(f)->host_mu);
+    if (!f || (n && (!pos_xyz || !dir_xyz))) return set_err(PSTF_E_INVALID, "NULL argument");
+    if ((footprint == nullptr) == (level == nullptr))
+        return set_err(PSTF_E_INVALID, "exactly one of footprint / level must be given");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(f->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<double> p, d;
+    aos_to_soa(pos_xyz, n, p);
+    aos_to_soa(dir_xyz, n, d);
+    std::vector<char *> dv;
+    Scratch &sc = const_cast<pstf_field *>(f)->sc;
+    int rc = stage_h2d(sc, {p.data(), d.data(), footprint ? (const void *)footprint : level,
+                            nullptr, nullptr, nullptr, nullptr},
+                       {3 * n * 8, 3 * n * 8, footprint ? n * 8 : n * 4, 3 * n * 8, n, n, n * 4},
+                       dv);
+    if (rc) return rc;
+    const double *dp = (const double *)dv[0], *dd = (const double *)dv[1];
+    pstf_vec3_soa ps{dp, dp + n, dp + 2 * n}, ds{dd, dd + n, dd + 2 * n};
+    double *val = (double *)dv[3];
+    rc = pstf_field_query(f, &ps, &ds, footprint ? (const double *)dv[2] : nullptr,
+                          footprint ? nullptr : (const int32_t *)dv[2], n, val, val + n,
+                          val + 2 * n, (uint8_t *)dv[4], (uint8_t *)dv[5], (int32_t *)dv[6],
+                          nullptr);
+    if (rc) return rc;
+    std::vector<double> hv(3 * n);
+    CK(cudaMemcpy(hv.data(), val, 3 * n * 8, cudaMemcpyDeviceToHost));
+    if (value_rgb)
+        for (uint64_t i = 0; i < n; ++i)
+            for (int c = 0; c < 3; ++c) value_rgb[3 * i + c] = hv[c * n + i];
+    if (valid) CK(cudaMemcpy(valid, dv[4], n, cudaMemcpyDeviceToHost));
+    if (fallback) CK(cudaMemcpy(fallback, dv[5], n, cudaMemcpyDeviceToHost));
+    if (out_level) CK(cudaMemcpy(out_level, dv[6], n * 4, cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
 int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
                      const double *footprint, const int32_t *level, uint64_t n, double *value_r,
                      double *value_g, double *value_b, uint8_t *valid, uint8_t *fallback,
@@ -2219,6 +2362,7 @@ int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out) {
     out->new_keys_last = c[C_NEW_KEYS];
     out->evicted_last = c[C_EVICTED];
     out->placement_rounds_last = f->rounds_last;
+    out->touched_total = c[C_TOUCHED_TOTAL];
     return PSTF_OK;
 }
 

@@ -37,6 +37,7 @@ enum Ctr : int {
     C_CN_COUNT,     // endFrame: live slots with cNew > 0
     C_LIVE_SNAP,    // endFrame: live count before eviction (field.cpp:205-212)
     C_TOUCHED_LAST, // touched slots of the last committed frame
+    C_TOUCHED_TOTAL, // touched slots summed over all committed frames
     C_NUM
 };
 

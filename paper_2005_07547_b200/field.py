@@ -50,7 +50,8 @@ class _Config(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("frame", "rejected", "dropped", "internal_errors",
                                           "live", "touched_last", "new_keys_last",
-                                          "evicted_last", "placement_rounds_last")]
+                                          "evicted_last", "placement_rounds_last",
+                                          "touched_total")]
 
 
 class _Vec3(C.Structure):
