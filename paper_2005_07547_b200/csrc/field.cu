@@ -956,6 +956,31 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
     }
 }
 
+/* Variant without shared-memory staging: persistent grid, each lane reads its fields straight
+ * from global memory (coalesced) while the tile PREFETCH_AHEAD tiles ahead is pulled into L2
+ * with cp.async.bulk.prefetch.L2, so the loads hit L2; occupancy is bounded by registers only. */
+template <int MINB, int PREFETCH_AHEAD>
+__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_l2(VPArgs2 a) {
+    __shared__ double4 wsm[VT / 32][32];
+    const int tid = threadIdx.x;
+    double4 *sm = wsm[tid >> 5];
+    const uint64_t ntiles = (a.n + VT - 1) / VT;
+    const uint64_t nfull = a.n / VT;
+    if (tid == 0)
+        for (int k = 0; k < PREFETCH_AHEAD; ++k) {
+            const uint64_t t = blockIdx.x + (uint64_t)k * gridDim.x;
+            if (t < nfull) prefetch_tile(a, t);
+        }
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t pt = tile + (uint64_t)PREFETCH_AHEAD * gridDim.x;
+        if (tid == 0 && pt < nfull) prefetch_tile(a, pt);
+        const uint64_t v = tile * VT + tid;
+        const bool live = v < a.n;
+        GmemSrc src{a, live ? v : tile * VT};
+        vertex_body(a, src, live, sm);
+    }
+}
+
 /* CV lookup at the current vertex (estimators.cpp:453-462) */
 __global__ void k_cv_lookup(DevStore s, pstf_vertex_soa V, uint64_t n, double *vr, double *vg,
                             double *vb, uint8_t *valid) {
@@ -2577,7 +2602,16 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
          * prefetch depth (the next tile is prefetched into L2) for more resident warps;
          * 1x4 measured fastest on config 2 (PSTF_TILED_CFG selects, default 1) */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 5) : 1;
+        const uint64_t tiles = (n + VT - 1) / VT;
+        if (cfg >= 3) { /* L2-prefetch variants: 3 = 4 CTAs/SM, 4 = 5 CTAs/SM, 5 = 4 CTAs/SM x2 ahead */
+            const int minb = cfg == 4 ? 5 : 4;
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
+            if (cfg == 3) LAUNCH((k_vertex_pass_l2<4, 1>), grid, VT, 0, st, b);
+            else if (cfg == 4) LAUNCH((k_vertex_pass_l2<5, 1>), grid, VT, 0, st, b);
+            else LAUNCH((k_vertex_pass_l2<4, 2>), grid, VT, 0, st, b);
+            return PSTF_OK;
+        }
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : (cfg == 1 ? 4 : 5);
         const size_t smem = stages * sizeof(TileStage) + 64;
@@ -2589,7 +2623,6 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             CK(e);
             attr[cfg] = true;
         }
-        const uint64_t tiles = (n + VT - 1) / VT;
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
         if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
         else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);

@@ -496,6 +496,7 @@ PSTF_HD PosQ pos_q(const FastParams &f, double px, double py, double pz) {
 PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level) {
     const double x = q * pow2d(-level);
     const double ax = fabs(x);
+    if (pcoord == 0.0) return 0; /* floor(+-0 / cs) == 0 (points on the coordinate planes) */
     if (ax >= 0x1p-900 && ax < 4294967296.0) {
         const double fl = floor(x);
         const double e = ax * 0x1p-50;
