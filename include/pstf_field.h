@@ -229,8 +229,48 @@ int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, 
  * Test/bench input, not part of the reference API. */
 int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iteration,
                         double cam_shift_x, double *buffer, void *stream);
+/* Same for the image stripe of paths [path0, path0 + npaths) (n = npaths*bounces vertices). */
+int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed,
+                               uint64_t iteration, double cam_shift_x, uint64_t path0,
+                               uint64_t npaths, double *buffer, void *stream);
 /* Fills a pstf_vertex_soa view of such a contiguous buffer (host or device memory). */
 void pstf_vertex_soa_from_buffer(const double *buffer, uint64_t n, pstf_vertex_soa *out);
+
+/* ---- key-owner sharding across ranks (one process per GPU) ----
+ * Every rank holds a full replica of each store's occupancy and committed state; rank r owns
+ * the contiguous slot range [r*cap/world, (r+1)*cap/world) and alone blends / evicts it.
+ * Per frame (collectives are the caller's, e.g. NCCL via torch.distributed):
+ *   1. pstf_vertex_pass_local on the rank's image stripe (lookups on the replica, REDs into a
+ *      local partial accumulator; new keys stay pending)
+ *   2. all-gather the pending records (pstf_pending_count/_copy) and pstf_resolve_records on
+ *      every rank: identical deterministic placement everywhere, own records' sums applied
+ *   3. pstf_partials_export (touched non-owned slots, destination-major) -> all-to-all ->
+ *      pstf_partials_import on the owners
+ *   4. pstf_end_frame_reduce -> all-reduce the (sum c_new, count) pairs ->
+ *      pstf_end_frame_commit (blend + evict the owned range, emit deltas)
+ *   5. all-gather deltas -> pstf_deltas_import (replicas converge)
+ * Slot placement equals the single-GPU layout; values differ only in summation order.
+ * Only the ATOMIC mode is sharded. */
+int pstf_shard_set(pstf_field *f, int rank, int world);
+int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                           const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
+                           uint32_t fli_mask, void *stream);
+int pstf_pending_count(pstf_field *lo, uint64_t *n);
+int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream);
+int pstf_resolve_records(pstf_field *const *stores, int nst, const void *records, uint64_t n,
+                         void *stream);
+int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
+                         uint64_t *counts_per_rank, void *stream);
+int pstf_partials_import(pstf_field *const *stores, int nst, const void *records, uint64_t n,
+                         void *stream);
+int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_count, void *stream);
+int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_count,
+                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
+int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,
+                       void *stream);
+uint64_t pstf_pending_record_bytes(void); /* 64 */
+uint64_t pstf_partial_record_bytes(void); /* 40: {u32 store, u32 slot, f64 acc[4]} */
+uint64_t pstf_delta_record_bytes(void);   /* 48: {u32 store, slot, checksum, last+1; f64 com[4]} */
 
 /* Number of kernels this library launched since load (bench evidence). */
 uint64_t pstf_kernel_launch_count(void);

@@ -560,6 +560,8 @@ void po_synth_generate(int width, int height, int bounces, uint64_t seed, uint64
     P.seed = seed;
     P.iter = iter;
     P.cam_shift_x = cam_shift_x;
+    P.path0 = 0;
+    P.n_local = 0;
     uint64_t n_paths = (uint64_t)width * (uint64_t)height;
     uint64_t n_total = n_paths * (uint64_t)bounces;
     if (threads < 1) threads = 1;

@@ -179,6 +179,8 @@ struct pstf_field {
     Scratch sc;
     uint64_t new_keys_last = 0, rounds_last = 0;
     std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
+    int world = 1;      /* key-owner sharding */
+    std::vector<uint32_t> sc_px_scan_copy;
 };
 
 static DevStore dev_view(const pstf_field *f) {
@@ -352,7 +354,7 @@ __device__ __forceinline__ void apply_contribution(const DevStore &s, const Pend
         r.k[4] = k.dir[0];
         r.k[5] = k.dir[1];
         r.cs = k.checksum;
-        r.meta = PSTF_META(sid, 0, ncalls);
+        r.meta = PSTF_META(sid, 0, ncalls) | ((uint32_t)s.rank << 3);
         r.v[0] = v.x;
         r.v[1] = v.y;
         r.v[2] = v.z;
@@ -1221,7 +1223,7 @@ __global__ void k_unique_build(const PendRec *pend, const uint32_t *perm, const 
 
 /* per-unique sums (ATOMIC) and call counts (all modes), warp-aggregated over sorted runs */
 __global__ void k_unique_sums(const PendRec *pend, const uint32_t *perm, const uint32_t *uid,
-                              uint64_t n, int atomic_mode, UniqArgs u) {
+                              uint64_t n, int atomic_mode, UniqArgs u, int own_origin) {
     __shared__ double4 smem[8][32];
     double4 *sm = smem[threadIdx.x >> 5];
     uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -1231,8 +1233,12 @@ __global__ void k_unique_sums(const PendRec *pend, const uint32_t *perm, const u
     uint32_t calls = 0;
     if (live) {
         PendRec p = pend[perm[j]];
-        v = make_double4(p.v[0], p.v[1], p.v[2], p.v[3]);
-        calls = PSTF_META_CALLS(p.meta);
+        /* sharded: only this rank's records add values / count drops here (the other ranks'
+         * records are present so that every replica places every new key identically) */
+        if (own_origin < 0 || (int)PSTF_META_ORIGIN(p.meta) == own_origin) {
+            v = make_double4(p.v[0], p.v[1], p.v[2], p.v[3]);
+            calls = PSTF_META_CALLS(p.meta);
+        }
     }
     unsigned peers = __match_any_sync(0xffffffffu, q);
     sm[lane_id()] = v;
@@ -1360,7 +1366,8 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
         if (v.z != 0.0) atomicAdd(&dst->z, v.z);
         if (v.w != 0.0) atomicAdd(&dst->w, v.w);
     }
-    touch_slot(s, slot);
+    /* sharded: a replica touches a slot only for its own records or as the slot's owner */
+    if (ucalls[u] != 0 || owned(s, slot)) touch_slot(s, slot);
 }
 
 /* ORDERED / SEQUENTIAL: per-record fold target (store << 32 | slot), dropped -> ~0 */
@@ -1552,6 +1559,126 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst) {
     }
 }
 
+/* ---------------- key-owner sharding (multi-GPU) ---------------- */
+struct PartialRec { /* 40 B: one touched non-owned slot's partial accumulators */
+    uint32_t store, slot;
+    double acc[4];
+};
+struct DeltaRec { /* 48 B: one committed slot of the owner's range */
+    uint32_t store, slot, checksum, last_biased;
+    double com[4];
+};
+
+/* words of the touched bitmap owned by another rank: popcounts */
+__global__ void k_px_count(DevStore s, uint32_t *cnt, uint64_t nwords) {
+    uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (w > nwords) return;
+    if (w == nwords) {
+        cnt[w] = 0;
+        return;
+    }
+    cnt[w] = owned(s, (uint32_t)(w * 32)) ? 0u : (uint32_t)__popc(s.tbits[w]);
+}
+
+/* export touched non-owned slots (slot order == owner order), zero them, clear their bits */
+__global__ void k_px_write(DevStore s, uint32_t sid, const uint32_t *scan, uint64_t nwords,
+                           uint64_t words_per_rank, const unsigned long long *dest_base,
+                           PartialRec *out) {
+    uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (w >= nwords || owned(s, (uint32_t)(w * 32))) return;
+    uint32_t bits = s.tbits[w];
+    if (!bits) return;
+    s.tbits[w] = 0;
+    const uint64_t r = w / words_per_rank;
+    unsigned long long pos = dest_base[r] + (scan[w] - scan[r * words_per_rank]);
+    while (bits) {
+        const uint32_t slot = (uint32_t)(w * 32 + (uint64_t)(__ffs(bits) - 1));
+        bits &= bits - 1;
+        const double4 a = s.acc[slot];
+        PartialRec rec;
+        rec.store = sid;
+        rec.slot = slot;
+        rec.acc[0] = a.x;
+        rec.acc[1] = a.y;
+        rec.acc[2] = a.z;
+        rec.acc[3] = a.w;
+        out[pos++] = rec;
+        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+}
+
+__global__ void k_px_import(Stores4 st, const PartialRec *recs, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const PartialRec r = recs[i];
+    const DevStore &s = st.s[r.store & 3];
+    red_add4(&s.acc[r.slot], make_double4(r.acc[0], r.acc[1], r.acc[2], r.acc[3]));
+    touch_slot(s, r.slot);
+}
+
+/* after the blend: every slot of the touched list (all owned) becomes a delta */
+__global__ void k_dx_touched(DevStore s, uint32_t sid, DeltaRec *out, unsigned long long *count) {
+    const uint64_t n = s.ctr[C_TOUCHED_N];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t slot = s.tlist[i];
+        const uint2 m = s.meta[slot];
+        const double4 c = s.com[slot];
+        DeltaRec d;
+        d.store = sid;
+        d.slot = slot;
+        d.checksum = m.x;
+        d.last_biased = m.y;
+        d.com[0] = c.x;
+        d.com[1] = c.y;
+        d.com[2] = c.z;
+        d.com[3] = c.w;
+        out[atomicAdd(count, 1ull)] = d;
+    }
+}
+
+/* age eviction of the owned slot range only; evicted slots become deltas */
+__global__ void k_ef_evict_range(DevStore s, uint32_t sid, uint64_t lo, uint64_t hi, DeltaRec *out,
+                                 unsigned long long *count) {
+    const uint64_t cap = (uint64_t)s.mask + 1;
+    if (!(s.ctr[C_LIVE_SNAP] * 4ull > (unsigned long long)cap * 3ull)) return;
+    unsigned ev = 0;
+    for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 m = s.meta[i];
+        if (m.x != 0 && (uint32_t)(s.frame - (m.y - 1u)) >= s.evict_age) {
+            s.meta[i].x = 0;
+            s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+            ++ev;
+            DeltaRec d;
+            d.store = sid;
+            d.slot = (uint32_t)i;
+            d.checksum = 0;
+            d.last_biased = m.y;
+            d.com[0] = d.com[1] = d.com[2] = d.com[3] = 0.0;
+            out[atomicAdd(count, 1ull)] = d;
+        }
+    }
+    ev = __reduce_add_sync(0xffffffffu, ev);
+    if (lane_id() == 0 && ev) {
+        atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
+        atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
+    }
+}
+
+/* replicas apply the other owners' committed slots (own deltas are already in place) */
+__global__ void k_dx_import(Stores4 st, const DeltaRec *recs, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const DeltaRec d = recs[i];
+    const DevStore &s = st.s[d.store & 3];
+    if (owned(s, d.slot)) return;
+    const uint32_t old = s.meta[d.slot].x;
+    s.meta[d.slot] = make_uint2(d.checksum, d.last_biased);
+    s.com[d.slot] = make_double4(d.com[0], d.com[1], d.com[2], d.com[3]);
+    if (old != 0 && d.checksum == 0) atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-1ll));
+}
+
 /* roll the per-frame scratch of every store of the batch */
 __global__ void k_ef_finish(Stores4 st, int nst) {
     const int j = threadIdx.x;
@@ -1661,9 +1788,9 @@ __global__ void k_snap_permute(const pstf_snapshot_record *src, const uint32_t *
 
 __global__ void k_synth(ps_params P, double *buf, uint64_t n_total) {
     uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    uint64_t n_paths = (uint64_t)P.width * (uint64_t)P.height;
+    uint64_t n_paths = P.n_local ? P.n_local : (uint64_t)P.width * (uint64_t)P.height;
     if (p >= n_paths) return;
-    ps_gen_path(&P, p, buf, (uint32_t *)(buf + 34 * n_total), n_total);
+    ps_gen_path(&P, p + P.path0, buf, (uint32_t *)(buf + 34 * n_total), n_total);
 }
 
 /* ========================================================================================== */
@@ -1738,7 +1865,7 @@ static int read_small(Scratch &sc, const void *dev, size_t bytes, cudaStream_t s
 /* Phase 2 for the records sitting in sc.pend (count on device in sc.pend_count).
  * fs[0..nf) are the stores addressed by record store ids. */
 static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode, uint64_t n_known,
-                           cudaStream_t st) {
+                           cudaStream_t st, int own_origin = -1) {
     uint64_t n = n_known;
     if (n == (uint64_t)-1) {
         int rc = read_small(sc, sc.pend_count.p, 8, st);
@@ -1854,7 +1981,7 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     LAUNCH(k_unique_build, grid_for(n, 256), 256, 0, st, pend, perm, sc.head.as<uint32_t>(),
            sc.uid.as<uint32_t>(), seq, n, S, U);
     LAUNCH(k_unique_sums, grid_for(n, 256), 256, 0, st, pend, perm, sc.uid.as<uint32_t>(), n,
-           mode == PSTF_MODE_ATOMIC ? 1 : 0, U);
+           mode == PSTF_MODE_ATOMIC ? 1 : 0, U, own_origin);
 
     /* 3. priority ranks */
     PlaceArgs P;
@@ -2071,6 +2198,8 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     d.t_max = config->t_max;
     d.blend = config->blend;
     d.evict_age = config->evict_age_frames;
+    d.rank = 0;
+    d.owner_shift = config->capacity_log2; /* unsharded: every slot is owned by rank 0 */
     /* value-initialised slots (field.cpp:232: make_unique<Slot[]>) */
     e = cudaMemset(f->arena, 0, off);
     if (e == cudaSuccess) e = cudaMemset(d.hold0, 0xff, cap * 4);
@@ -2766,9 +2895,11 @@ int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, 
     return PSTF_OK;
 }
 
-int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iteration,
-                        double cam_shift_x, double *buffer, void *stream) {
-    if (width <= 0 || height <= 0 || bounces <= 0 || !buffer)
+int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed,
+                               uint64_t iteration, double cam_shift_x, uint64_t path0,
+                               uint64_t npaths, double *buffer, void *stream) {
+    const uint64_t total = (uint64_t)width * (uint64_t)height;
+    if (width <= 0 || height <= 0 || bounces <= 0 || !buffer || path0 + npaths > total)
         return set_err(PSTF_E_INVALID, "bad synthetic stream arguments");
     ps_params P;
     P.width = width;
@@ -2777,10 +2908,249 @@ int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint6
     P.seed = seed;
     P.iter = iteration;
     P.cam_shift_x = cam_shift_x;
-    uint64_t n_paths = (uint64_t)width * height;
-    LAUNCH(k_synth, grid_for(n_paths, 128), 128, 0, (cudaStream_t)stream, P, buffer,
-           n_paths * (uint64_t)bounces);
+    P.path0 = path0;
+    P.n_local = npaths == total && path0 == 0 ? 0 : npaths;
+    LAUNCH(k_synth, grid_for(npaths, 128), 128, 0, (cudaStream_t)stream, P, buffer,
+           npaths * (uint64_t)bounces);
     return PSTF_OK;
 }
 
+int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iteration,
+                        double cam_shift_x, double *buffer, void *stream) {
+    return pstf_synth_generate_stripe(width, height, bounces, seed, iteration, cam_shift_x, 0,
+                                      (uint64_t)width * (uint64_t)height, buffer, stream);
+}
+
+/* ---------------- key-owner sharding (multi-GPU) ---------------- */
+static int shard_checks(pstf_field *const *fs, int n) {
+    if (!fs || n < 1 || n > 4) return set_err(PSTF_E_INVALID, "1..4 stores per batch");
+    for (int i = 0; i < n; ++i) {
+        if (!fs[i]) return set_err(PSTF_E_INVALID, "NULL store");
+        if (fs[i]->device != fs[0]->device || fs[i]->world != fs[0]->world ||
+            fs[i]->d.rank != fs[0]->d.rank)
+            return set_err(PSTF_E_INVALID, "stores must share device and shard layout");
+    }
+    return PSTF_OK;
+}
+
+int pstf_shard_set(pstf_field *f, int rank, int world) {
+    if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    if (world < 1 || world > 32 || (world & (world - 1)))
+        return set_err(PSTF_E_INVALID, "world must be a power of two in [1, 32]");
+    if (rank < 0 || rank >= world) return set_err(PSTF_E_INVALID, "bad rank");
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    if (cap / (uint64_t)world < 32) return set_err(PSTF_E_INVALID, "capacity/world must be >= 32");
+    int lw = 0;
+    while ((1 << lw) < world) ++lw;
+    f->d.rank = rank;
+    f->d.owner_shift = f->cfg.capacity_log2 - (uint32_t)lw;
+    f->world = world;
+    return PSTF_OK;
+}
+
+int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                           const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
+                           uint32_t fli_mask, void *stream) {
+    int rc = vertex_checks(lo, loe, fli, li, PSTF_MODE_ATOMIC);
+    if (rc) return rc;
+    if (!v) return set_err(PSTF_E_INVALID, "NULL vertex record");
+    CK(cudaSetDevice(lo->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(PSTF_MODE_ATOMIC, li)),
+                        false, st);
+    if (rc) return rc;
+    if (n) return vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, PSTF_MODE_ATOMIC, st);
+    return PSTF_OK;
+}
+
+int pstf_pending_count(pstf_field *lo, uint64_t *n) {
+    if (!lo || !n) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(lo->device));
+    CK(cudaDeviceSynchronize());
+    unsigned long long c = 0;
+    if (lo->sc.pend_count.p) CK(cudaMemcpy(&c, lo->sc.pend_count.p, 8, cudaMemcpyDeviceToHost));
+    *n = std::min<uint64_t>(c, lo->sc.pend.bytes / sizeof(PendRec));
+    return PSTF_OK;
+}
+
+int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream) {
+    if (!lo || (n && !dst)) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(lo->device));
+    CK(cudaMemcpyAsync(dst, lo->sc.pend.p, n * sizeof(PendRec), cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream));
+    return PSTF_OK;
+}
+
+int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, uint64_t n,
+                         void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    CK(cudaSetDevice(stores[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch &sc = stores[0]->sc;
+    rc = ensure_pending(sc, std::max<uint64_t>(n, 1), false, st);
+    if (rc) return rc;
+    if (n) CK(cudaMemcpyAsync(sc.pend.p, recs, n * sizeof(PendRec), cudaMemcpyDeviceToDevice, st));
+    return resolve_pending(sc, stores, nst, PSTF_MODE_ATOMIC, n, st, stores[0]->d.rank);
+}
+
+int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
+                         uint64_t *counts, void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!counts) return set_err(PSTF_E_INVALID, "NULL counts");
+    CK(cudaSetDevice(stores[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int world = stores[0]->world;
+    Scratch &sc = stores[0]->sc;
+    /* per store: word popcounts -> scan -> per-destination counts */
+    std::vector<std::vector<uint64_t>> cnt(nst, std::vector<uint64_t>(world, 0));
+    for (int j = 0; j < nst; ++j) {
+        DevStore s = dev_view(stores[j]);
+        const uint64_t nwords = ((uint64_t)s.mask + 1) / 32;
+        ENSURE(sc.head, (nwords + 1) * 4);
+        ENSURE(sc.uid, (nwords + 1) * 4);
+        LAUNCH(k_px_count, grid_for(nwords + 1, 256), 256, 0, st, s, sc.head.as<uint32_t>(), nwords);
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sc.head.as<uint32_t>(),
+                                         sc.uid.as<uint32_t>(), (int64_t)(nwords + 1), st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, sc.head.as<uint32_t>(),
+                                         sc.uid.as<uint32_t>(), (int64_t)(nwords + 1), st));
+        std::vector<uint32_t> hs(nwords + 1);
+        CK(cudaMemcpyAsync(hs.data(), sc.uid.p, (nwords + 1) * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint64_t wpr = nwords / (uint64_t)world;
+        for (int r = 0; r < world; ++r) cnt[j][r] = hs[(r + 1) * wpr] - hs[r * wpr];
+        stores[j]->sc_px_scan_copy = hs; /* kept for the write pass (scratch is reused) */
+    }
+    uint64_t total = 0;
+    for (int r = 0; r < world; ++r) {
+        counts[r] = 0;
+        for (int j = 0; j < nst; ++j) counts[r] += cnt[j][r];
+        total += counts[r];
+    }
+    if (total > cap) return set_err(PSTF_E_NOMEM, "partials buffer too small");
+    std::vector<uint64_t> rbase(world, 0);
+    for (int r = 1; r < world; ++r) rbase[r] = rbase[r - 1] + counts[r - 1];
+    ENSURE(sc.ranges, (size_t)world * 8 + 64);
+    for (int j = 0; j < nst; ++j) {
+        DevStore s = dev_view(stores[j]);
+        const uint64_t nwords = ((uint64_t)s.mask + 1) / 32;
+        std::vector<unsigned long long> db(world);
+        for (int r = 0; r < world; ++r) {
+            uint64_t b = rbase[r];
+            for (int jj = 0; jj < j; ++jj) b += cnt[jj][r];
+            db[r] = b;
+        }
+        /* rescan this store (the scratch was reused by the next store) */
+        ENSURE(sc.head, (nwords + 1) * 4);
+        ENSURE(sc.uid, (nwords + 1) * 4);
+        CK(cudaMemcpyAsync(sc.uid.p, stores[j]->sc_px_scan_copy.data(), (nwords + 1) * 4,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(sc.ranges.p, db.data(), world * 8, cudaMemcpyHostToDevice, st));
+        LAUNCH(k_px_write, grid_for(nwords, 256), 256, 0, st, s, (uint32_t)j, sc.uid.as<uint32_t>(),
+               nwords, nwords / (uint64_t)world, sc.ranges.as<unsigned long long>(),
+               (PartialRec *)out);
+        CK(cudaStreamSynchronize(st));
+        stores[j]->sc_px_scan_copy.clear();
+    }
+    return PSTF_OK;
+}
+
+int pstf_partials_import(pstf_field *const *stores, int nst, const void *recs, uint64_t n,
+                         void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(stores[0]->device));
+    LAUNCH(k_px_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
+           (const PartialRec *)recs, n);
+    return PSTF_OK;
+}
+
+int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!sum_cnt) return set_err(PSTF_E_INVALID, "NULL sum_cnt");
+    CK(cudaSetDevice(stores[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t maxcap = 0;
+    for (int i = 0; i < nst; ++i) {
+        maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
+        CK(cudaMemsetAsync(&stores[i]->d.ctr[C_EVICTED], 0, 8, st));
+    }
+    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
+    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, stores4(stores, nst), nst);
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < nst; ++i) {
+        unsigned long long c = 0;
+        CK(cudaMemcpy(&sum_cnt[2 * i], stores[i]->d.cn_sum, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&c, &stores[i]->d.ctr[C_CN_COUNT], 8, cudaMemcpyDeviceToHost));
+        sum_cnt[2 * i + 1] = (double)c;
+    }
+    return PSTF_OK;
+}
+
+int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_cnt,
+                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!global_sum_cnt || !ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(stores[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch &sc = stores[0]->sc;
+    for (int i = 0; i < nst; ++i) { /* the batch-wide mean c_new of pass 1 */
+        unsigned long long c = (unsigned long long)global_sum_cnt[2 * i + 1];
+        CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &global_sum_cnt[2 * i], 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &c, 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    uint64_t maxcap = 0;
+    for (int i = 0; i < nst; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
+    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
+    Stores4 S = stores4(stores, nst);
+    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, nst);
+    ENSURE(sc.changed, 16);
+    CK(cudaMemsetAsync(sc.changed.p, 0, 8, st));
+    unsigned long long *dcount = (unsigned long long *)sc.changed.p;
+    const bool out = deltas != nullptr && cap > 0;
+    for (int i = 0; i < nst; ++i) {
+        DevStore s = dev_view(stores[i]);
+        if (out) LAUNCH(k_dx_touched, g, EF_BLOCK, 0, st, s, (uint32_t)i, (DeltaRec *)deltas, dcount);
+        const uint64_t per = ((uint64_t)s.mask + 1) / (uint64_t)stores[i]->world; /* owned range */
+        const uint64_t lo = (uint64_t)s.rank * per, hi = lo + per;
+        if (out)
+            LAUNCH(k_ef_evict_range, g, EF_BLOCK, 0, st, s, (uint32_t)i, lo, hi, (DeltaRec *)deltas,
+                   dcount);
+    }
+    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst);
+    LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
+    for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
+    unsigned long long nd = 0;
+    CK(cudaMemcpyAsync(&nd, dcount, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (out && nd > cap) return set_err(PSTF_E_NOMEM, "deltas buffer overflow");
+    *ndeltas = nd;
+    return PSTF_OK;
+}
+
+int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,
+                       void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!n) return PSTF_OK;
+    CK(cudaSetDevice(stores[0]->device));
+    LAUNCH(k_dx_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
+           (const DeltaRec *)deltas, n);
+    return PSTF_OK;
+}
+
+uint64_t pstf_pending_record_bytes(void) { return sizeof(PendRec); }
+uint64_t pstf_partial_record_bytes(void) { return sizeof(PartialRec); }
+uint64_t pstf_delta_record_bytes(void) { return sizeof(DeltaRec); }
+
 } // extern "C"
+

@@ -20,7 +20,7 @@ namespace pstf_b200 {
 struct PendRec {
     int32_t k[6];  // level, cell[3], dirCell[2]
     uint32_t cs;   // checksum
-    uint32_t meta; // bits 0-1 store id, bit 2 is_counter, bits 8-31 number of calls
+    uint32_t meta; // bits 0-1 store id, bit 2 is_counter, bits 3-7 origin rank, 8-31 calls
     double v[4];   // ATOMIC: {r,g,b,c} aggregated; ORDERED/SEQUENTIAL: {r,g,b,w} of one call
 };
 static_assert(sizeof(PendRec) == 64, "PendRec must be 64 B");
@@ -30,6 +30,7 @@ static_assert(sizeof(PendRec) == 64, "PendRec must be 64 B");
 #define PSTF_META_SID(m) ((m)&3u)
 #define PSTF_META_ISC(m) (((m) >> 2) & 1u)
 #define PSTF_META_CALLS(m) ((m) >> 8)
+#define PSTF_META_ORIGIN(m) (((m) >> 3) & 31u) /* producing rank (key-owner sharding) */
 
 struct Stores4 {
     DevStore s[4];

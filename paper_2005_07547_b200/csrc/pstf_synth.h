@@ -49,6 +49,8 @@ typedef struct {
     uint64_t seed;
     uint64_t iter;
     double cam_shift_x; /* config 5: camera translated along x */
+    uint64_t path0;     /* image stripe: paths [path0, path0 + n_local) ... */
+    uint64_t n_local;   /* ... stored at b * n_local + (p - path0); 0 = whole image */
 } ps_params;
 
 typedef struct { double x, y, z; } ps_v3;
@@ -140,7 +142,8 @@ PS_HD ps_v3 ps_to_world(int w, double a, double b, double c) {
 /* Writes the B vertices of one path into a contiguous SoA buffer of n_total vertices. */
 PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t *flags,
                        uint64_t n_total) {
-    const uint64_t n_paths = (uint64_t)P->width * (uint64_t)P->height;
+    const uint64_t n_paths = P->n_local ? P->n_local : (uint64_t)P->width * (uint64_t)P->height;
+    const uint64_t lpath = P->n_local ? path - P->path0 : path;
     const uint64_t base = ps_mix(ps_mix(P->seed ^ (P->iter * 0xd1b54a32d192ed03ULL)) ^ path);
     const int px = (int)(path % (uint64_t)P->width);
     const int py = (int)(path / (uint64_t)P->width);
@@ -165,7 +168,7 @@ PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t 
     double emis = ps_is_lamp(wall, pos) ? PS_LAMP_EMISSION : 0.0;
 
     for (int b = 0; b < P->bounces; ++b) {
-        const uint64_t vi = (uint64_t)b * n_paths + path;
+        const uint64_t vi = (uint64_t)b * n_paths + lpath;
         ps_v3 n = ps_wall_normal(wall);
         ps_v3 alb = ps_albedo(wall);
         ps_v3 wo = ps_v(-d.x, -d.y, -d.z);

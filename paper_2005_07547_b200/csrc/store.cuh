@@ -57,8 +57,14 @@ struct DevStore {
     double t_max;
     uint32_t blend;
     uint32_t evict_age;
-    uint32_t frame; // uint32_t(m_frame) for this launch
+    uint32_t frame;       // uint32_t(m_frame) for this launch
+    int32_t rank;         // key-owner sharding: this rank (0 when not sharded)
+    uint32_t owner_shift; // owner(slot) = slot >> owner_shift (capacity_log2 - log2 world)
 };
+
+__device__ __forceinline__ bool owned(const DevStore &s, uint32_t slot) {
+    return (int32_t)(slot >> s.owner_shift) == s.rank;
+}
 
 #define PSTF_HOLD_NONE 0xffffffffu
 
