@@ -249,12 +249,21 @@ def run_b200(args):
     n = W * H * B
     S = max(1, args.streams)
     bufs = []
-    for i in range(S):
-        b, _ = pb.synth_generate(W, H, B, iteration=i + 1000 * rank)
+    for i in range(S):  # rank r traces its own 1 spp of the frame (seed offset): weak scaling
+        b, _ = pb.synth_generate(W, H, B, seed=0x5EED + 7919 * rank, iteration=i)
         bufs.append(b)
     torch.cuda.synchronize()
+    sharded = None
+    if dist is not None:
+        # one global field cache, hash space sharded by key owner across the ranks
+        from paper_2005_07547_b200.shard import Collectives, CudaBackend, ShardedFieldCache
+        sharded = ShardedFieldCache(CudaBackend(stores, rank, world),
+                                    Collectives(dist, torch.device("cuda", local)))
 
     def step(i):
+        if sharded is not None:
+            sharded.iteration((bufs[i % S], n))
+            return
         pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
         pb.end_frame_all(stores)
 
@@ -321,7 +330,8 @@ def run_b200(args):
             "mode": args.mode, "iteration_streams": S,
             "l2": "inputs larger than L2 (2.29 GB per iteration stream, %d streams cycled)" % S,
             "parallelism": "single GPU" if world == 1 else
-                           f"{world} ranks x independent image replicas (no cache exchange yet)",
+                           f"{world} ranks, 1 spp of the 1080p frame each (weak scaling), one "
+                           f"field cache sharded by key owner (NCCL all-gather / all-to-all)",
         },
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
@@ -345,9 +355,13 @@ def run_b200(args):
         E = max(1, args.e2e_steps)
 
         def estep(i):
-            pb.vertex_pass_host(stores[0], stores[1], stores[2], None, hosts[i % len(hosts)], n,
-                                mode=mode)
-            pb.end_frame_all(stores)
+            if sharded is not None:  # H2D of this rank's stream, then the sharded iteration
+                bufs[0].copy_(hosts[i % len(hosts)], non_blocking=True)
+                sharded.iteration((bufs[0], n))
+            else:
+                pb.vertex_pass_host(stores[0], stores[1], stores[2], None, hosts[i % len(hosts)],
+                                    n, mode=mode)
+                pb.end_frame_all(stores)
             return [s.stats()["live"] for s in stores]  # D2H read of the step's result
 
         estep(0)
@@ -366,8 +380,10 @@ def run_b200(args):
         line["e2e"] = {"value": n * E * world / et, "unit": UNIT,
                        "h2d_bytes_per_step": BYTES_PER_VERTEX * n,
                        "d2h_bytes_per_step": 3 * 8 * 11, "steps": E,
-                       "path": "pstf_vertex_pass_host (pinned host SoA, chunked H2D overlapped "
-                               "with phase 1) + pstf_field_end_frame x3 + stats readback"}
+                       "path": ("pstf_vertex_pass_host (pinned host SoA, chunked H2D overlapped "
+                                "with phase 1) + pstf_fields_end_frame + stats readback")
+                       if sharded is None else
+                       "pinned host SoA -> HBM copy + sharded iteration + stats readback"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

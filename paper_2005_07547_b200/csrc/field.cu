@@ -940,7 +940,11 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         const int s = (int)(it % STAGES);
         mbar_wait(&bars[s], (it / STAGES) & 1u);
         SmemSrc src{&stages[s], tid};
-        vertex_body(a, src, true, sm);
+        if (a.dbg & 32) { /* experiment: stream only */
+            if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
+        } else {
+            vertex_body(a, src, true, sm);
+        }
         __syncthreads(); /* every lane is done with stage s */
         const uint64_t nt = tile + (uint64_t)STAGES * gridDim.x;
         if (tid == 0 && nt < nfull) {
