@@ -318,7 +318,26 @@ __device__ __forceinline__ void apply_contribution(const DevStore &s, const Pend
     unsigned long long gk = res >= 0 ? (((unsigned long long)sid << 32) | (unsigned)res)
                                      : (0xffffffff00000000ull | lane);
     unsigned peers = aggregate ? __match_any_sync(0xffffffffu, gk) : (1u << lane);
-    if (!aggregate || __all_sync(0xffffffffu, peers == (1u << lane))) {
+    if (!aggregate) {
+        /* Sector-coalesced REDs: the warp's 32 cells x 4 components are transposed through
+         * shared memory so each RED instruction covers 8 cells x {r,g,b,c}; the 4 lanes of a
+         * cell hit one 32 B sector, so L1 sends 8 sector requests per instruction, not 32. */
+        int *rsm = reinterpret_cast<int *>(sm + 32);
+        sm[lane] = v;
+        rsm[lane] = do_red ? res : -3;
+        __syncwarp();
+        const double *flat = reinterpret_cast<const double *>(sm);
+        const int comp = lane & 3;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int cell = 8 * k + (lane >> 2);
+            const int rs = rsm[cell];
+            const double val = flat[4 * cell + comp];
+            if (rs >= 0 && val != 0.0) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+        }
+        __syncwarp();
+        if (res >= 0) touch_slot(s, (uint32_t)res, mark);
+    } else if (__all_sync(0xffffffffu, peers == (1u << lane))) {
         /* no two lanes share a slot: one RED per component, no shared-memory round trip */
         if (res >= 0) {
             if (do_red) red_add4(&s.acc[res], v);
@@ -397,7 +416,7 @@ __device__ __forceinline__ void emit_call(const PendSink &a, bool want, int sid,
 
 template <int MODE>
 __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
-    __shared__ double4 smem[WARPS_PER_BLOCK][32];
+    __shared__ double4 smem[WARPS_PER_BLOCK][36];
     double4 *sm = smem[threadIdx.x >> 5];
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const bool live = i < a.n;
@@ -918,7 +937,7 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileStage *stages = reinterpret_cast<TileStage *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + STAGES * sizeof(TileStage));
-    __shared__ double4 wsm[VT / 32][32];
+    __shared__ double4 wsm[VT / 32][36]; /* 32 cells + 32 ints of probe results */
     const int tid = threadIdx.x;
     double4 *sm = wsm[tid >> 5];
     const uint64_t nfull = a.n / VT;
@@ -967,7 +986,7 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
  * with cp.async.bulk.prefetch.L2, so the loads hit L2; occupancy is bounded by registers only. */
 template <int MINB, int PREFETCH_AHEAD>
 __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_l2(VPArgs2 a) {
-    __shared__ double4 wsm[VT / 32][32];
+    __shared__ double4 wsm[VT / 32][36]; /* 32 cells + 32 ints of probe results */
     const int tid = threadIdx.x;
     double4 *sm = wsm[tid >> 5];
     const uint64_t ntiles = (a.n + VT - 1) / VT;
