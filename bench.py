@@ -53,7 +53,16 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                   help="BASELINE.json config: 2 = 1080p x4 (default, the metric's workload); "
+                        "3 = + CV lookup at every vertex; 4 = 4K x6 at 2^24 slots; 5 = drifting "
+                        "camera (+0.02/iter), 2^20 slots so eviction engages")
+    a = p.parse_args()
+    if a.config == 4:
+        a.width, a.height, a.bounces, a.capacity_log2, a.streams = 3840, 2160, 6, 24, 2
+    if a.config == 5:
+        a.capacity_log2 = 20
+    return a
 
 
 def peaks():
@@ -248,11 +257,24 @@ def run_b200(args):
               for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
     n = W * H * B
     S = max(1, args.streams)
+    drift = args.config == 5
     bufs = []
-    for i in range(S):  # rank r traces its own 1 spp of the frame (seed offset): weak scaling
+    for i in range(1 if drift else S):  # rank r traces its own 1 spp of the frame: weak scaling
         b, _ = pb.synth_generate(W, H, B, seed=0x5EED + 7919 * rank, iteration=i)
         bufs.append(b)
+    if drift:
+        S = 1
+    cv_out = None
+    if args.config == 3:  # CV lookup at every vertex (estimators.cpp:453-462): RGB f64 + valid
+        cv_out = (torch.empty((3, n), dtype=torch.float64, device="cuda"),
+                  torch.empty(n, dtype=torch.uint8, device="cuda"))
     torch.cuda.synchronize()
+
+    def regenerate(i):
+        """config 5: the camera drifts +0.02 per iteration (untimed input production)"""
+        shift = ((0.02 * i + 0.9) % 1.8) - 0.9
+        pb.synth_generate(W, H, B, seed=0x5EED + 7919 * rank, iteration=i, cam_shift_x=shift,
+                          out=bufs[0])
     sharded = None
     if dist is not None:
         # one global field cache, hash space sharded by key owner across the ranks
@@ -264,10 +286,17 @@ def run_b200(args):
         if sharded is not None:
             sharded.iteration((bufs[i % S], n))
             return
+        if cv_out is not None:
+            pb.field._check(pb.lib().pstf_cv_lookup(
+                stores[1].handle, pb.field.C.byref(pb.vertex_soa(bufs[i % S], n)), n,
+                pb.field._ptr(cv_out[0][0]), pb.field._ptr(cv_out[0][1]),
+                pb.field._ptr(cv_out[0][2]), pb.field._ptr(cv_out[1]), pb.field._stream()))
         pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
         pb.end_frame_all(stores)
 
     for i in range(args.warmup):
+        if drift:
+            regenerate(i)
         step(i)
     torch.cuda.synchronize()
     if dist:
@@ -279,14 +308,28 @@ def run_b200(args):
     with ClockSampler(local) as clk:
         pb.profile_enable(True)
         torch.cuda.synchronize()
-        ev0.record()
-        for i in range(args.steps):
-            step(args.warmup + i)
-        ev1.record()
-        torch.cuda.synchronize()
+        if drift:  # per-step events: the input regeneration stays outside the timed region
+            evs = []
+            for i in range(args.steps):
+                pb.profile_enable(False)
+                regenerate(args.warmup + i)
+                pb.profile_enable(True)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                step(args.warmup + i)
+                e1.record()
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            ev0.record()
+            for i in range(args.steps):
+                step(args.warmup + i)
+            ev1.record()
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
         pb.profile_enable(False)
     launches = pb.kernel_launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
     prof = pb.profile_collect()
     if dist:
         t = torch.tensor([ms], device="cuda")
@@ -305,7 +348,8 @@ def run_b200(args):
     vp_bytes = BYTES_PER_VERTEX * n
     ach = vp_bytes / (vp_avg / 1e3) / 1e9
     mean_touched = (sum(s["touched_total"] for s in st) - touched0) / args.steps
-    step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched
+    step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched + \
+        (25 * n if cv_out is not None else 0)  # +25 B per CV lookup (config 3)
     step_ach = step_bytes / (ms_step / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_vertex_pass_traffic.json")
@@ -324,8 +368,14 @@ def run_b200(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (pstf_synth.h Cornell-box generator, IEEE-exact, seed 0x5EED)",
         "config": {
-            "workload": "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, "
-                        "spatio-directional keys, Lo/LoE/FLi stores x 2^22 slots, base=diam/256",
+            "workload": {2: "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, "
+                            "spatio-directional keys, Lo/LoE/FLi stores x 2^22 slots, "
+                            "base=diam/256",
+                         3: "config3: config 2 + CV lookup (Lo\\E query) at every vertex "
+                            "(Lambertian synthetic scene, not glossy)",
+                         4: "config4: 3840x2160 1spp x6 bounces, Lo/LoE/FLi x 2^24 slots",
+                         5: "config5: config 2 with the camera drifting +0.02/iteration, "
+                            "2^20 slots (eviction engages), inputs regenerated untimed"}[args.config],
             "vertices_per_iter": n, "capacity_log2": args.capacity_log2, "stores": 3,
             "mode": args.mode, "iteration_streams": S,
             "l2": "inputs larger than L2 (2.29 GB per iteration stream, %d streams cycled)" % S,

@@ -650,6 +650,7 @@ struct VPArgs2 {
     Stores4 st;
     FastParams fp;
     int dbg; /* experiment switches (PSTF_VP_DBG): 1 no lookups, 2 no RED, 4 keys only */
+    int pf;  /* L2 prefetch distance in tiles of this CTA (PSTF_VP_PF, default 1) */
     int has_li;
     uint32_t loe_mask, fli_mask;
     const double *fld[PS_NUM_F64];
@@ -747,9 +748,15 @@ __device__ __forceinline__ Key make_key(uint64_t h1, int level, int32_t c0, int3
     return k;
 }
 
-template <class Src>
+struct NoPhase {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+/* Phase: called once every lane has read its last "A" field (position, directions, footprints,
+ * flags) and before the first "B" field (values), so a split-staged caller can refill A. */
+template <class Src, class Phase = NoPhase>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
-                                            double4 *sm) {
+                                            double4 *sm, const Phase &phase = Phase()) {
     const DevStore &sLo = a.st.s[0];
     const DevStore &sLoe = a.st.s[1];
     const DevStore &sFli = a.st.s[2];
@@ -805,7 +812,6 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
 
     double3 loNext = make_double3(0.0, 0.0, 0.0), loeNext = make_double3(0.0, 0.0, 0.0);
-    const double nex = S.f(PS_NEMIS), ney = S.f(PS_NEMIS + 1), nez = S.f(PS_NEMIS + 2);
     if (look) {
         const uint32_t cs = checksum_of(qpk);
         bool doneLo = false, doneLoe = false;
@@ -850,11 +856,12 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 }
             }
         }
-    } else if (cont && !nsurf) {
-        loNext = make_double3(nex, ney, nez); /* environment: exactly known (209) */
     }
+    phase(); /* every "A" field has been read */
 
     /* ---- update values (field.cpp:13-25 evaluation order) ---- */
+    const double nex = S.f(PS_NEMIS), ney = S.f(PS_NEMIS + 1), nez = S.f(PS_NEMIS + 2);
+    if (cont && !nsurf) loNext = make_double3(nex, ney, nez); /* environment (209) */
     const double ratio = S.f(PS_RATIO);
     const double fr = S.f(PS_F), fg = S.f(PS_F + 1), fb = S.f(PS_F + 2);
     const double nmis = S.f(PS_NMIS);
@@ -952,7 +959,8 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         for (int s = 0; s < STAGES; ++s) {
             uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
             if (t < nfull) issue_tile(a, &stages[s], &bars[s], t, policy);
-            if (t + gridDim.x < nfull) prefetch_tile(a, t + gridDim.x);
+            for (int d = 1; d <= a.pf; ++d)
+                if (t + (uint64_t)d * gridDim.x < nfull) prefetch_tile(a, t + (uint64_t)d * gridDim.x);
         }
     uint32_t it = 0;
     for (uint64_t tile = blockIdx.x; tile < nfull; tile += gridDim.x, ++it) {
@@ -969,7 +977,7 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         if (tid == 0 && nt < nfull) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_tile(a, &stages[s], &bars[s], nt, policy);
-            if (nt + gridDim.x < nfull) prefetch_tile(a, nt + gridDim.x);
+            if (nt + (uint64_t)a.pf * gridDim.x < nfull) prefetch_tile(a, nt + (uint64_t)a.pf * gridDim.x);
         }
     }
     /* partial last tile straight from global memory */
@@ -977,31 +985,6 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         const uint64_t v = nfull * VT + tid;
         const bool live = v < a.n;
         GmemSrc src{a, live ? v : nfull * VT};
-        vertex_body(a, src, live, sm);
-    }
-}
-
-/* Variant without shared-memory staging: persistent grid, each lane reads its fields straight
- * from global memory (coalesced) while the tile PREFETCH_AHEAD tiles ahead is pulled into L2
- * with cp.async.bulk.prefetch.L2, so the loads hit L2; occupancy is bounded by registers only. */
-template <int MINB, int PREFETCH_AHEAD>
-__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_l2(VPArgs2 a) {
-    __shared__ double4 wsm[VT / 32][36]; /* 32 cells + 32 ints of probe results */
-    const int tid = threadIdx.x;
-    double4 *sm = wsm[tid >> 5];
-    const uint64_t ntiles = (a.n + VT - 1) / VT;
-    const uint64_t nfull = a.n / VT;
-    if (tid == 0)
-        for (int k = 0; k < PREFETCH_AHEAD; ++k) {
-            const uint64_t t = blockIdx.x + (uint64_t)k * gridDim.x;
-            if (t < nfull) prefetch_tile(a, t);
-        }
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t pt = tile + (uint64_t)PREFETCH_AHEAD * gridDim.x;
-        if (tid == 0 && pt < nfull) prefetch_tile(a, pt);
-        const uint64_t v = tile * VT + tid;
-        const bool live = v < a.n;
-        GmemSrc src{a, live ? v : tile * VT};
         vertex_body(a, src, live, sm);
     }
 }
@@ -1457,7 +1440,10 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
     __shared__ unsigned long long scnt[EF_BLOCK / 32];
     for (int j = 0; j < nst; ++j) {
         const DevStore &s = st.s[j];
-        if (blockIdx.x == 0 && threadIdx.x == 0) s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+            s.ctr[C_EVICTED] = 0;
+        }
         const uint64_t nwords = ((uint64_t)s.mask + 32) / 32;
         double sum = 0.0;
         unsigned cnt = 0;
@@ -1526,31 +1512,41 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
         const bool limited = tMax > 0.0 && isfinite(tMax);
         const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
         unsigned internal = 0;
-        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-             i += (uint64_t)gridDim.x * blockDim.x) {
-            const uint32_t slot = s.tlist[i];
-            const double4 a = s.acc[slot];
-            const double cn = a.w;
-            if (cn > 0.0) {
-                double4 c = s.com[slot];
-                const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
-                double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
-                if (limited) {
-                    const double fl = 1.0 / tMax;
-                    alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        /* two list entries per iteration, acc and com loads of both in flight together */
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+            const bool two = i + stride < n;
+            const uint32_t sl[2] = {s.tlist[i], two ? s.tlist[i + stride] : s.tlist[i]};
+            const double4 av[2] = {s.acc[sl[0]], s.acc[sl[1]]};
+            const double4 cv[2] = {s.com[sl[0]], s.com[sl[1]]};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (k == 1 && !two) break;
+                const uint32_t slot = sl[k];
+                const double4 a = av[k];
+                const double cn = a.w;
+                if (cn > 0.0) {
+                    double4 c = cv[k];
+                    const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+                    double alpha =
+                        s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+                    if (limited) {
+                        const double fl = 1.0 / tMax;
+                        alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+                    }
+                    const double oma = 1.0 - alpha;
+                    c.x = c.x * oma + cx * alpha;
+                    c.y = c.y * oma + cy * alpha;
+                    c.z = c.z * oma + cz * alpha;
+                    c.w = c.w + cn;
+                    if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+                    s.com[slot] = c;
+                } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+                    ++internal;
                 }
-                const double oma = 1.0 - alpha;
-                c.x = c.x * oma + cx * alpha;
-                c.y = c.y * oma + cy * alpha;
-                c.z = c.z * oma + cz * alpha;
-                c.w = c.w + cn;
-                if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
-                s.com[slot] = c;
-            } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
-                ++internal;
+                if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
+                    s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
             }
-            if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
-                s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
         }
         internal = __reduce_add_sync(0xffffffffu, internal);
         if (lane_id() == 0 && internal) atomicAdd(&s.ctr[C_INTERNAL], (unsigned long long)internal);
@@ -1559,7 +1555,15 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
 
 /* Pass 3 (field.cpp:247-260): age eviction, only when live*4 > capacity*3 (live before
  * eviction); the kernel exits at once otherwise. */
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst) {
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish) {
+    if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
+        const DevStore &s = st.s[threadIdx.x];
+        s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
+        s.ctr[C_TOUCHED_TOTAL] += s.ctr[C_TOUCHED_N];
+        s.ctr[C_TOUCHED_N] = 0;
+        s.ctr[C_CN_COUNT] = 0;
+        *s.cn_sum = 0.0;
+    }
     for (int j = 0; j < nst; ++j) {
         const DevStore &s = st.s[j];
         const uint64_t cap = (uint64_t)s.mask + 1;
@@ -2493,15 +2497,11 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     Stores4 S = stores4(fs, n);
     uint64_t maxcap = 0;
-    for (int i = 0; i < n; ++i) {
-        maxcap = std::max<uint64_t>(maxcap, (uint64_t)fs[i]->d.mask + 1);
-        CK(cudaMemsetAsync(&fs[i]->d.ctr[C_EVICTED], 0, 8, st));
-    }
+    for (int i = 0; i < n; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)fs[i]->d.mask + 1);
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
     LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n);
     LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n);
-    LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n);
-    LAUNCH(k_ef_finish, 1, 32, 0, st, S, n);
+    LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n, 1); /* + the per-frame scratch roll */
     for (int i = 0; i < n; ++i) fs[i]->frame += 1;
     return PSTF_OK;
 }
@@ -2741,6 +2741,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         b.st = a.st;
         b.fp = make_fast_params(lo->d.kp);
         b.dbg = getenv("PSTF_VP_DBG") ? atoi(getenv("PSTF_VP_DBG")) : 0;
+        b.pf = getenv("PSTF_VP_PF") ? std::max(0, atoi(getenv("PSTF_VP_PF"))) : 1;
         b.has_li = a.has_li;
         b.loe_mask = loe_mask;
         b.fli_mask = fli_mask;
@@ -2750,35 +2751,27 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         b.pend = a.pend;
         b.pend_count = a.pend_count;
         b.pend_cap = a.pend_cap;
-        /* (stages, CTAs/SM): 2x3 = TMA double buffering at 168 regs; 1x4 / 1x5 trade the
-         * prefetch depth (the next tile is prefetched into L2) for more resident warps;
-         * 1x4 measured fastest on config 2 (PSTF_TILED_CFG selects, default 1) */
+        /* (stages, CTAs/SM): 2x3 = TMA double buffering at 168 regs; 1x4 trades the prefetch
+         * depth (the next tile is prefetched into L2) for more resident warps and measured
+         * fastest on config 2 (PSTF_TILED_CFG=0 selects 2x3).  Also measured slower: 1x5
+         * (96 regs, spills), L2-prefetch-only loads without staging, and a split A/B
+         * two-group staging with an extra barrier per tile. */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 5) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 1) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
-        if (cfg >= 3) { /* L2-prefetch variants: 3 = 4 CTAs/SM, 4 = 5 CTAs/SM, 5 = 4 CTAs/SM x2 ahead */
-            const int minb = cfg == 4 ? 5 : 4;
-            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
-            if (cfg == 3) LAUNCH((k_vertex_pass_l2<4, 1>), grid, VT, 0, st, b);
-            else if (cfg == 4) LAUNCH((k_vertex_pass_l2<5, 1>), grid, VT, 0, st, b);
-            else LAUNCH((k_vertex_pass_l2<4, 2>), grid, VT, 0, st, b);
-            return PSTF_OK;
-        }
         const int stages = cfg == 0 ? 2 : 1;
-        const int minb = cfg == 0 ? 3 : (cfg == 1 ? 4 : 5);
+        const int minb = cfg == 0 ? 3 : 4;
         const size_t smem = stages * sizeof(TileStage) + 64;
-        static bool attr[3] = {false, false, false};
+        static bool attr[2] = {false, false};
         if (!attr[cfg]) {
             cudaError_t e = cfg == 0 ? cudaFuncSetAttribute(k_vertex_pass_tiled<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                          : cfg == 1 ? cudaFuncSetAttribute(k_vertex_pass_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                     : cudaFuncSetAttribute(k_vertex_pass_tiled<1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                     : cudaFuncSetAttribute(k_vertex_pass_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             CK(e);
             attr[cfg] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
         if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
-        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
-        else LAUNCH((k_vertex_pass_tiled<1, 5>), grid, VT, smem, st, b);
+        else LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
     } else if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
     else
@@ -3149,7 +3142,7 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
             LAUNCH(k_ef_evict_range, g, EF_BLOCK, 0, st, s, (uint32_t)i, lo, hi, (DeltaRec *)deltas,
                    dcount);
     }
-    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst);
+    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0);
     LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
     for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
     unsigned long long nd = 0;
