@@ -280,8 +280,11 @@ struct PendSink {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+/* isfinite(a) && isfinite(b) && isfinite(c) on the exponent fields (integer pipe) */
 __device__ __forceinline__ bool finite3(double a, double b, double c) {
-    return isfinite(a) && isfinite(b) && isfinite(c);
+    const int ea = __double2hiint(a) & 0x7ff00000, eb = __double2hiint(b) & 0x7ff00000,
+              ec = __double2hiint(c) & 0x7ff00000;
+    return max(ea, max(eb, ec)) != 0x7ff00000;
 }
 
 /* Appends records with one atomic per warp; all 32 lanes must call it. */
@@ -686,8 +689,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-        if (done) break;
-        __nanosleep(64); /* back off: leave issue slots to the other CTAs on the SM */
+        if (done) break; /* try_wait suspends the warp in hardware until the phase flips */
     }
 }
 
@@ -708,6 +710,9 @@ __device__ __forceinline__ void issue_tile(const VPArgs2 &a, TileStage *st, uint
                                            uint64_t tile, uint64_t policy) {
     mbar_expect_tx(bar, (uint32_t)(PS_NUM_F64 * VT * 8 + VT * 4));
     const uint64_t v0 = tile * VT;
+#if PSTF_ISSUE_ROLLED
+#pragma unroll 1
+#endif
     for (int k = 0; k < PS_NUM_F64; ++k) bulk_g2s(&st->f[k][0], a.fld[k] + v0, VT * 8, bar, policy);
     bulk_g2s(&st->flags[0], a.flags + v0, VT * 4, bar, policy);
 }
@@ -715,6 +720,9 @@ __device__ __forceinline__ void issue_tile(const VPArgs2 &a, TileStage *st, uint
 /* pull a later tile's segments into L2 so its shared-memory copy completes at L2 latency */
 __device__ __forceinline__ void prefetch_tile(const VPArgs2 &a, uint64_t tile) {
     const uint64_t v0 = tile * VT;
+#if PSTF_ISSUE_ROLLED
+#pragma unroll 1
+#endif
     for (int k = 0; k < PS_NUM_F64; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
     prefetch_l2(a.flags + v0, VT * 4);
 }
@@ -726,12 +734,6 @@ struct SmemSrc {
     __device__ __forceinline__ uint32_t flags() const { return t->flags[j]; }
 };
 
-struct GmemSrc {
-    const VPArgs2 &a;
-    uint64_t i;
-    __device__ __forceinline__ double f(int k) const { return __ldg(a.fld[k] + i); }
-    __device__ __forceinline__ uint32_t flags() const { return __ldg(a.flags + i); }
-};
 
 __device__ __forceinline__ Key make_key(uint64_t h1, int level, int32_t c0, int32_t c1, int32_t c2,
                                         int32_t d0, int32_t d1) {
@@ -752,8 +754,9 @@ struct NoPhase {
     __device__ __forceinline__ void operator()() const {}
 };
 
-/* Phase: called once every lane has read its last "A" field (position, directions, footprints,
- * flags) and before the first "B" field (values), so a split-staged caller can refill A. */
+/* Phase: called by every lane once it has read its last input field and before the probes and
+ * contributions, so the tiled caller can start the next tile's bulk copy into the stage while
+ * this tile's REDs are still in flight. */
 template <class Src, class Phase = NoPhase>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
                                             double4 *sm, const Phase &phase = Phase()) {
@@ -771,30 +774,48 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
 
     /* ---- keys (estimators.cpp:195, 215, 226, 242, 248, 257): one level, one cell triple and
      * one packKeyFields prefix for all update keys of the vertex ---- */
-    const int level = select_level_fast(fq, S.f(PS_FP));
+    int nx = 0; /* set when any quantity lies too close to a cell boundary for the fast path */
+    int level = select_level_try(fq, S.f(PS_FP), &nx);
     const double px = S.f(PS_POS), py = S.f(PS_POS + 1), pz = S.f(PS_POS + 2);
     const PosQ q = pos_q(fq, px, py, pz);
-    const int32_t c0 = cell_at(fq, q.q[0], px, level), c1 = cell_at(fq, q.q[1], py, level),
-                  c2 = cell_at(fq, q.q[2], pz, level);
-    const uint64_t h1 = pack_h1(level, c0, c1);
+    int32_t c0 = cell_try(q.q[0], px, level, &nx), c1 = cell_try(q.q[1], py, level, &nx),
+            c2 = cell_try(q.q[2], pz, level, &nx);
     DirF8 fo, fi, fin, fn, ftmp;
-    octa_f8(S.f(PS_WO), S.f(PS_WO + 1), S.f(PS_WO + 2), 0, &fo, &ftmp);
-    octa_f8(S.f(PS_WI), S.f(PS_WI + 1), S.f(PS_WI + 2), look, &fi, &fin);
-    /* lanes without NEE use a fixed generic direction so a speculated evaluation never takes
-     * the exact-atan2 path for their zero nee.dir */
-    octa_f8(nee ? S.f(PS_NDIR) : 0.36, nee ? S.f(PS_NDIR + 1) : 0.48,
-            nee ? S.f(PS_NDIR + 2) : 0.8, 0, &fn, &ftmp);
+    const double wox = S.f(PS_WO), woy = S.f(PS_WO + 1), woz = S.f(PS_WO + 2);
+    const double wix = S.f(PS_WI), wiy = S.f(PS_WI + 1), wiz = S.f(PS_WI + 2);
+    /* lanes without NEE use a fixed generic direction so a speculated evaluation never lands
+     * near a boundary for their zero nee.dir */
+    const double ndx = nee ? S.f(PS_NDIR) : 0.36, ndy = nee ? S.f(PS_NDIR + 1) : 0.48,
+                 ndz = nee ? S.f(PS_NDIR + 2) : 0.8;
+    octa_f8_try(wox, woy, woz, 0, &fo, &ftmp, &nx);
+    octa_f8_try(wix, wiy, wiz, look, &fi, &fin, &nx);
+    octa_f8_try(ndx, ndy, ndz, 0, &fn, &ftmp, &nx);
+    const double qx = S.f(PS_NPOS), qy = S.f(PS_NPOS + 1), qz = S.f(PS_NPOS + 2);
+    const PosQ nq = pos_q(fq, qx, qy, qz);
+    int l0 = select_level_try(fq, S.f(PS_NFP), &nx);
+    int32_t n0 = cell_try(nq.q[0], qx, l0, &nx), n1 = cell_try(nq.q[1], qy, l0, &nx),
+            n2 = cell_try(nq.q[2], qz, l0, &nx);
+    if (nx) { /* rare: the vertex's quantities through the exact reference operations (one
+               * out-of-the-way block instead of a fallback at every use) */
+        level = select_level(kp, S.f(PS_FP));
+        c0 = cell_exact(kp, px, level);
+        c1 = cell_exact(kp, py, level);
+        c2 = cell_exact(kp, pz, level);
+        octa_f8_exact(wox, woy, woz, 0, &fo, &ftmp);
+        octa_f8_exact(wix, wiy, wiz, look, &fi, &fin);
+        octa_f8_exact(ndx, ndy, ndz, 0, &fn, &ftmp);
+        l0 = select_level(kp, S.f(PS_NFP));
+        n0 = cell_exact(kp, qx, l0);
+        n1 = cell_exact(kp, qy, l0);
+        n2 = cell_exact(kp, qz, l0);
+    }
+    const uint64_t h1 = pack_h1(level, c0, c1);
     const Key kLo = make_key(h1, level, c0, c1, c2, dir_cell_f8(fo.u, level), dir_cell_f8(fo.v, level));
     const Key kFc = make_key(h1, level, c0, c1, c2, dir_cell_f8(fi.u, level), dir_cell_f8(fi.v, level));
     const Key kFn = make_key(h1, level, c0, c1, c2, dir_cell_f8(fn.u, level), dir_cell_f8(fn.v, level));
 
     /* ---- first lookup key at the next vertex (estimators.cpp:198-206) ---- */
-    const double qx = S.f(PS_NPOS), qy = S.f(PS_NPOS + 1), qz = S.f(PS_NPOS + 2);
-    const PosQ nq = pos_q(fq, qx, qy, qz);
-    const int l0 = select_level_fast(fq, S.f(PS_NFP));
-    uint64_t qpk = pack_key_fields(l0, cell_at(fq, nq.q[0], qx, l0), cell_at(fq, nq.q[1], qy, l0),
-                                   cell_at(fq, nq.q[2], qz, l0), dir_cell_f8(fin.u, l0),
-                                   dir_cell_f8(fin.v, l0));
+    uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
 
     /* ---- one round trip: the five update home words, the two lookup home words and (on
      * speculation that the lookup key sits at its home slot) the two committed records ---- */
@@ -829,10 +850,17 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         if (!(doneLo && doneLoe)) {
             for (int l = l0; l <= kp.max_level && !(doneLo && doneLoe); ++l) {
                 uint64_t pk = qpk;
-                if (l != l0)
-                    pk = pack_key_fields(l, cell_at(fq, nq.q[0], qx, l), cell_at(fq, nq.q[1], qy, l),
-                                         cell_at(fq, nq.q[2], qz, l), dir_cell_f8(fin.u, l),
-                                         dir_cell_f8(fin.v, l));
+                if (l != l0) {
+                    int lx = 0;
+                    int32_t a0 = cell_try(nq.q[0], qx, l, &lx), a1 = cell_try(nq.q[1], qy, l, &lx),
+                            a2 = cell_try(nq.q[2], qz, l, &lx);
+                    if (lx) {
+                        a0 = cell_exact(kp, qx, l);
+                        a1 = cell_exact(kp, qy, l);
+                        a2 = cell_exact(kp, qz, l);
+                    }
+                    pk = pack_key_fields(l, a0, a1, a2, dir_cell_f8(fin.u, l), dir_cell_f8(fin.v, l));
+                }
                 const uint32_t ccs = checksum_of(pk);
                 const uint32_t hl = (uint32_t)pk & sLo.mask, he = (uint32_t)pk & sLoe.mask;
                 int il = -1, ie = -1;
@@ -857,7 +885,6 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             }
         }
     }
-    phase(); /* every "A" field has been read */
 
     /* ---- update values (field.cpp:13-25 evaluation order) ---- */
     const double nex = S.f(PS_NEMIS), ney = S.f(PS_NEMIS + 1), nez = S.f(PS_NEMIS + 2);
@@ -910,6 +937,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         const double x = lix * 1.0, y = liy * 1.0, z2 = liz * 1.0;
         if (finite3(x, y, z2)) { vli.x += x; vli.y += y; vli.z += z2; ++nli; } else ++rejLi;
     }
+    phase(); /* every input field of the vertex has been read: the stage may be refilled */
     if (live) {
         if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
         if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
@@ -949,8 +977,13 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
     double4 *sm = wsm[tid >> 5];
     const uint64_t nfull = a.n / VT;
     uint64_t policy = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+#if PSTF_REFILL_EARLY
+    __shared__ unsigned empty_cnt_s;
+    unsigned *empty_cnt = &empty_cnt_s;
+    if (tid == 0) empty_cnt_s = 0u;
+#endif
     if (tid == 0) {
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
         for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -963,29 +996,61 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
                 if (t + (uint64_t)d * gridDim.x < nfull) prefetch_tile(a, t + (uint64_t)d * gridDim.x);
         }
     uint32_t it = 0;
-    for (uint64_t tile = blockIdx.x; tile < nfull; tile += gridDim.x, ++it) {
+    const uint64_t ntiles = (a.n + VT - 1) / VT;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = (int)(it % STAGES);
-        mbar_wait(&bars[s], (it / STAGES) & 1u);
+        bool live = true;
+        if (tile < nfull) {
+            mbar_wait(&bars[s], (it / STAGES) & 1u);
+        } else {
+            /* the partial last tile: plain loads into this lane's own column of the stage (no
+             * bulk copy is in flight any more), so the one inlined body serves every tile */
+            const uint64_t v = tile * VT + tid;
+            live = v < a.n;
+            for (int k = 0; k < PS_NUM_F64; ++k) stages[s].f[k][tid] = live ? a.fld[k][v] : 0.0;
+            stages[s].flags[tid] = live ? a.flags[v] : 0u;
+        }
         SmemSrc src{&stages[s], tid};
+        const uint64_t nt = tile + (uint64_t)STAGES * gridDim.x;
+        const auto issue_next = [&]() {
+            if (nt < nfull) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_tile(a, &stages[s], &bars[s], nt, policy);
+                if (nt + (uint64_t)a.pf * gridDim.x < nfull)
+                    prefetch_tile(a, nt + (uint64_t)a.pf * gridDim.x);
+            }
+        };
+#if PSTF_REFILL_EARLY
+        /* The last warp to finish reading its inputs refills stage s with tile nt; no warp waits
+         * for the others (the stage is only read column-per-lane, so only the bulk copy needs
+         * every read to be done). */
+        const auto release = [&]() {
+            __syncwarp();
+            if ((tid & 31) == 0) {
+                __threadfence_block();
+                if (atomicAdd(empty_cnt, 1u) == VT / 32 - 1) {
+                    *empty_cnt = 0u;
+                    __threadfence_block();
+                    issue_next();
+                }
+            }
+            __syncwarp();
+        };
+        if (a.dbg & 32) { /* experiment: stream only */
+            if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
+            release();
+        } else {
+            vertex_body(a, src, live, sm, release);
+        }
+#else
         if (a.dbg & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body(a, src, true, sm);
+            vertex_body(a, src, live, sm);
         }
         __syncthreads(); /* every lane is done with stage s */
-        const uint64_t nt = tile + (uint64_t)STAGES * gridDim.x;
-        if (tid == 0 && nt < nfull) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile(a, &stages[s], &bars[s], nt, policy);
-            if (nt + (uint64_t)a.pf * gridDim.x < nfull) prefetch_tile(a, nt + (uint64_t)a.pf * gridDim.x);
-        }
-    }
-    /* partial last tile straight from global memory */
-    if ((a.n % VT) && blockIdx.x == (unsigned)(nfull % gridDim.x)) {
-        const uint64_t v = nfull * VT + tid;
-        const bool live = v < a.n;
-        GmemSrc src{a, live ? v : nfull * VT};
-        vertex_body(a, src, live, sm);
+        if (tid == 0) issue_next();
+#endif
     }
 }
 

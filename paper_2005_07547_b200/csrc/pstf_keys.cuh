@@ -311,26 +311,26 @@ PSTF_HD_NOINLINE double atan2_cr_pos(double y, double x) {
 }
 
 /* Approximate reciprocal / square root for the fast (non-deciding) path: single-precision
- * hardware estimate + Newton steps in fp64, relative error ~1e-16 for den in [1e-30, 1e30]. */
+ * hardware estimate (relative error < 2^-22 incl. the rounding of the argument to float) + one
+ * Newton step in fp64, relative error < 2^-43 (~1.2e-13) for den in [1e-30, 1e30].  The octahedral
+ * coordinates built from them stay within ~1e-12 of the exact ones, well inside the 1e-11 margin
+ * that sends a coordinate to the exact path. */
 PSTF_HD double fast_rcp(double den) {
 #if defined(__CUDA_ARCH__)
     double r = (double)__frcp_rn((float)den);
 #else
     double r = (double)(1.0f / (float)den);
 #endif
-    r = r * fma(-den, r, 2.0);
-    r = r * fma(-den, r, 2.0);
-    return r;
+    return r * fma(-den, r, 2.0);
 }
 
-PSTF_HD double fast_sqrt01(double w) { /* w in [0, 1]; |error| < 1e-15 */
+PSTF_HD double fast_sqrt01(double w) { /* w in [0, 1]; relative error < 2^-42 */
     if (!(w >= 1e-30)) return 0.0;
 #if defined(__CUDA_ARCH__)
     double y = (double)rsqrtf((float)w);
 #else
     double y = (double)(1.0f / sqrtf((float)w));
 #endif
-    y = y * fma(-0.5 * w, y * y, 1.5);
     y = y * fma(-0.5 * w, y * y, 1.5);
     return w * y;
 }
@@ -466,9 +466,13 @@ PSTF_HD FastParams make_fast_params(const KeyParams &kp) {
     return f;
 }
 
-PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
+/* Fast level: decided from the exponent of s' = footprint * fl(K / base), which lies within a few
+ * ulps of the reference's fl(fl(footprint K) / base); sets *nx when s' is too close to a power of
+ * two (or out of range) for that to be certain.  (*nx = "needs the exact reference operation") */
+PSTF_HD int select_level_try(const FastParams &f, double footprint, int *nx) {
     if (!(footprint > 0.0)) return 0;
     const double s = footprint * f.k_inv_base;
+    if (s < 0.9999999999) return 0; /* exact s <= 1: level 0 (field.cpp:71) */
     if (s > 1.0000000001 && s < 1e300) {
         const uint64_t b = dbits(s);
         const uint64_t mant = b & 0x000fffffffffffffULL;
@@ -478,7 +482,14 @@ PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
             return level < f.kp.max_level ? level : f.kp.max_level;
         }
     }
-    return select_level_exact(f.kp, footprint);
+    *nx = 1;
+    return 0;
+}
+
+PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
+    int nx = 0;
+    const int l = select_level_try(f, footprint, &nx);
+    return nx ? select_level_exact(f.kp, footprint) : l;
 }
 
 struct PosQ {
@@ -493,18 +504,27 @@ PSTF_HD PosQ pos_q(const FastParams &f, double px, double py, double pz) {
     return r;
 }
 
-PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level) {
+/* Fast cell coordinate floor(pcoord / (base 2^level)) from q = pcoord * fl(1 / base); sets *nx
+ * when x' is within 2^-50 |x'| of an integer (or out of the plain range). */
+PSTF_HD int32_t cell_try(double q, double pcoord, int level, int *nx) {
     const double x = q * pow2d(-level);
     const double ax = fabs(x);
     if (pcoord == 0.0) return 0; /* floor(+-0 / cs) == 0 (points on the coordinate planes) */
-    if (ax >= 0x1p-900 && ax < 4294967296.0) {
-        const double fl = floor(x);
+    if (ax >= 0x1p-900 && ax < 2147483647.0) {
+        const double fl = floor(x); /* in [-2^31 + 1, 2^31 - 2]: a plain conversion is exact */
         const double e = ax * 0x1p-50;
-        if (x - fl >= e && (fl + 1.0) - x >= e) return i32_x86(fl);
+        if (x - fl >= e && (fl + 1.0) - x >= e) return (int32_t)fl;
     } else if (ax >= 4294967296.0 && ax <= 1.7976931348623157e308) {
         return INT32_MIN; /* far outside int32: the reference's conversion gives INT32_MIN */
     }
-    return cell_exact(f.kp, pcoord, level); /* exact reference operation */
+    *nx = 1;
+    return 0;
+}
+
+PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level) {
+    int nx = 0;
+    const int32_t c = cell_try(q, pcoord, level, &nx);
+    return nx ? cell_exact(f.kp, pcoord, level) : c; /* exact reference operation */
 }
 
 /* pre-swap octahedral coordinates from |x|, |y|, |z| (mappings.h:34-42) */
@@ -536,12 +556,14 @@ PSTF_HD void octa_uv(double u0, double v0, double dx, double dy, double dz, doub
     *V = 0.5 * (v + 1.0);
 }
 
-/* floor(U * 8) with the reference's int32 conversion (NaN -> INT32_MIN); near = within 1e-11 */
+/* floor(U * 8) with the reference's int32 conversion (NaN -> INT32_MIN); near = within 1e-11 of
+ * an integer.  U lies in [-1e-12, 1 + 1e-12] or is NaN, so floor(U * 8) is in [-1, 8] or NaN;
+ * f = q - fl is exact and 1 - f == fl + 1 - q wherever it is small. */
 PSTF_HD int32_t f8_of(double U, int *near) {
     const double q = U * 8.0;
     const double fl = floor(q);
-    *near |= (q - fl) < 1e-11 || (fl + 1.0 - q) < 1e-11;
-    return i32_x86(fl);
+    *near |= fabs((q - fl) - 0.5) > 0.5 - 1e-11;
+    return fl == fl ? (int32_t)fl : INT32_MIN;
 }
 
 struct DirF8 {
@@ -563,21 +585,59 @@ PSTF_HD void octa_f8_exact(double dx, double dy, double dz, int want_neg, DirF8 
     }
 }
 
+/* atan2 for x, y >= 0 not both zero, no internal fallback: *nx set when the reduction's
+ * denominator leaves [1e-30, 1e30] (infinities, NaN, denormal-scale directions) */
+PSTF_HD double atan2_try(double y, double x, int *nx) {
+    const int swap = y > x;
+    const double a = swap ? x : y, b = swap ? y : x; /* 0 <= a <= b, b > 0 */
+    const bool small = a <= b * 0.41421356237309503;
+    const double num = small ? a : a - b, den = small ? b : a + b;
+    *nx |= !(den >= 1e-30 && den <= 1e30);
+    const double t = num * fast_rcp(den);
+    const double z = t * t;
+    double p = -0.025316479573776477;
+    p = fma(p, z, 0.05024762118940128);
+    p = fma(p, z, -0.0650598296717084);
+    p = fma(p, z, 0.07673535428183285);
+    p = fma(p, z, -0.09089529956562307);
+    p = fma(p, z, 0.11111048853751296);
+    p = fma(p, z, -0.14285712661684793);
+    p = fma(p, z, 0.19999999978392663);
+    p = fma(p, z, -0.3333333333322143);
+    p = fma(p, z, 0.999999999999999);
+    const double th = (small ? 0.0 : 0.7853981633974483) + t * p;
+    return swap ? 1.5707963267948966 - th : th;
+}
+
+/* octahedral cell coordinates (at resolution 8) of d and optionally -d from the fast path; *nx
+ * set when any coordinate lies within 1e-11 of a cell boundary or the inputs are out of the fast
+ * path's domain (the caller then recomputes with octa_f8_exact) */
+PSTF_HD void octa_f8_try(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg,
+                         int *nx) {
+    const double x = fabs(dx), y = fabs(dy), z = fabs(dz);
+    const double omz = 1.0 - z;
+    const double w = (0.0 < omz) ? omz : 0.0; /* safeSqrt: std::max(0.0, x) vecmath.h:22 */
+    const double r = fast_sqrt01(w);
+    const double phi =
+        (x == 0.0 && y == 0.0) ? 0.0 : atan2_try(y, x, nx) * (2.0 / 3.14159265358979323846);
+    const double v0 = phi * r, u0 = r - v0;
+    double U, V;
+    octa_uv(u0, v0, dx, dy, dz, &U, &V);
+    pos->u = f8_of(U, nx);
+    pos->v = f8_of(V, nx);
+    if (want_neg) {
+        octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
+        neg->u = f8_of(U, nx);
+        neg->v = f8_of(V, nx);
+    }
+}
+
 /* octahedral cell coordinates (at resolution 8) of d and optionally -d, bit-identical to
  * min(int32(sphereToSquare(d) * 8), ...) before the per-level clamp */
 PSTF_HD void octa_f8(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg) {
-    double u0, v0, U, V;
-    int near = 0;
-    octa_base(dx, dy, dz, 0, &u0, &v0);
-    octa_uv(u0, v0, dx, dy, dz, &U, &V);
-    pos->u = f8_of(U, &near);
-    pos->v = f8_of(V, &near);
-    if (want_neg) {
-        octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
-        neg->u = f8_of(U, &near);
-        neg->v = f8_of(V, &near);
-    }
-    if (near) octa_f8_exact(dx, dy, dz, want_neg, pos, neg);
+    int nx = 0;
+    octa_f8_try(dx, dy, dz, want_neg, pos, neg, &nx);
+    if (nx) octa_f8_exact(dx, dy, dz, want_neg, pos, neg);
 }
 
 /* dirCell at a level from floor(U*8): min(floor(U*d), d-1) (field.cpp:93-95) */

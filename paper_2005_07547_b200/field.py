@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libpstf_b200.so")
+_LIB_PATH = os.environ.get("PSTF_LIB_PATH") or os.path.join(_HERE, "lib", "libpstf_b200.so")
 
 KIND_LO, KIND_LO_MINUS_E, KIND_LI, KIND_FLI = 0, 1, 2, 3
 TECH_CAMERA, TECH_CONTINUATION, TECH_NEE, TECH_ALL = 1, 2, 4, 7
