@@ -287,19 +287,28 @@ __device__ __forceinline__ bool finite3(double a, double b, double c) {
     return max(ea, max(eb, ec)) != 0x7ff00000;
 }
 
-/* Appends records with one atomic per warp; all 32 lanes must call it. */
-__device__ __forceinline__ void warp_append(const PendSink &a, bool want, const PendRec &r) {
+/* Reserves pending-record positions with one atomic per warp; all 32 lanes must call it.
+ * Returns this lane's record, or nullptr (not wanted / buffer full: the host sees the count). */
+__device__ __forceinline__ PendRec *warp_reserve(const PendSink &a, bool want) {
     unsigned m = __ballot_sync(0xffffffffu, want);
-    if (!m) return;
+    if (!m) return nullptr;
     unsigned lane = lane_id();
     int leader = __ffs(m) - 1;
     unsigned long long base = 0;
     if ((int)lane == leader) base = atomicAdd(a.count, (unsigned long long)__popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (want) {
-        unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
-        if (pos < a.cap) a.pend[pos] = r;
-    }
+    const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+    return want && pos < a.cap ? a.pend + pos : nullptr;
+}
+
+/* one 64 B record written as four 16 B stores straight from registers (no local-memory copy) */
+__device__ __forceinline__ void put_record(PendRec *p, const Key &k, uint32_t meta, double v0,
+                                           double v1, double v2, double v3) {
+    int4 *q = reinterpret_cast<int4 *>(p);
+    q[0] = make_int4(k.level, k.cell[0], k.cell[1], k.cell[2]);
+    q[1] = make_int4(k.dir[0], k.dir[1], (int)k.checksum, (int)meta);
+    reinterpret_cast<double2 *>(p)[2] = make_double2(v0, v1);
+    reinterpret_cast<double2 *>(p)[3] = make_double2(v2, v3);
 }
 
 /* One update slot of the vertex (ATOMIC mode), executed by all 32 lanes in lock-step:
@@ -366,23 +375,8 @@ __device__ __forceinline__ void apply_contribution(const DevStore &s, const Pend
         }
         __syncwarp();
     }
-    PendRec r;
-    bool want = res == -1;
-    if (want) {
-        r.k[0] = k.level;
-        r.k[1] = k.cell[0];
-        r.k[2] = k.cell[1];
-        r.k[3] = k.cell[2];
-        r.k[4] = k.dir[0];
-        r.k[5] = k.dir[1];
-        r.cs = k.checksum;
-        r.meta = PSTF_META(sid, 0, ncalls) | ((uint32_t)s.rank << 3);
-        r.v[0] = v.x;
-        r.v[1] = v.y;
-        r.v[2] = v.z;
-        r.v[3] = v.w;
-    }
-    warp_append(a, want, r);
+    if (PendRec *p = warp_reserve(a, res == -1))
+        put_record(p, k, PSTF_META(sid, 0, ncalls) | ((uint32_t)s.rank << 3), v.x, v.y, v.z, v.w);
     if (res == -2) atomicAdd(&s.ctr[C_DROPPED], (unsigned long long)ncalls);
 }
 
@@ -399,22 +393,8 @@ __device__ __forceinline__ void contribute_atomic(const DevStore &s, const PendS
 __device__ __forceinline__ void emit_call(const PendSink &a, bool want, int sid, const Key &k,
                                           bool is_counter, double r_, double g_, double b_,
                                           double w) {
-    PendRec r;
-    if (want) {
-        r.k[0] = k.level;
-        r.k[1] = k.cell[0];
-        r.k[2] = k.cell[1];
-        r.k[3] = k.cell[2];
-        r.k[4] = k.dir[0];
-        r.k[5] = k.dir[1];
-        r.cs = k.checksum;
-        r.meta = PSTF_META(sid, is_counter ? 1 : 0, 1);
-        r.v[0] = r_;
-        r.v[1] = g_;
-        r.v[2] = b_;
-        r.v[3] = w;
-    }
-    warp_append(a, want, r);
+    if (PendRec *p = warp_reserve(a, want))
+        put_record(p, k, PSTF_META(sid, is_counter ? 1 : 0, 1), r_, g_, b_, w);
 }
 
 template <int MODE>
@@ -886,72 +866,16 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         }
     }
 
-    /* ---- update values (field.cpp:13-25 evaluation order) ---- */
-    const double nex = S.f(PS_NEMIS), ney = S.f(PS_NEMIS + 1), nez = S.f(PS_NEMIS + 2);
-    if (cont && !nsurf) loNext = make_double3(nex, ney, nez); /* environment (209) */
-    const double ratio = S.f(PS_RATIO);
-    const double fr = S.f(PS_F), fg = S.f(PS_F + 1), fb = S.f(PS_F + 2);
-    const double nmis = S.f(PS_NMIS);
-    const bool transp = cont && ratio > 0.0;
-    const double lex = nex * nmis, ley = ney * nmis, lez = nez * nmis;
-    const double lix = lex + loeNext.x, liy = ley + loeNext.y, liz = lez + loeNext.z;
-
-    unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
-    double4 vlo = make_double4(0.0, 0.0, 0.0, 1.0); /* Lo: counter, emission, transport */
-    uint32_t nlo = 1;
-    {
-        const double ex = S.f(PS_EMIS), ey = S.f(PS_EMIS + 1), ez = S.f(PS_EMIS + 2);
-        if (finite3(ex, ey, ez)) { vlo.x += ex; vlo.y += ey; vlo.z += ez; ++nlo; } else ++rejLo;
-        if (transp) {
-            const double ux = ((0.0 + loNext.x) * fr) * ratio, uy = ((0.0 + loNext.y) * fg) * ratio,
-                         uz = ((0.0 + loNext.z) * fb) * ratio;
-            if (finite3(ux, uy, uz)) { vlo.x += ux; vlo.y += uy; vlo.z += uz; ++nlo; } else ++rejLo;
-        }
-    }
-    double4 vle = make_double4(0.0, 0.0, 0.0, 1.0); /* Lo\E (226-234) */
-    uint32_t nle = 1;
-    if (transp && (a.loe_mask & PSTF_TECH_CONTINUATION)) {
-        const double ux = ((lex + loeNext.x) * fr) * ratio, uy = ((ley + loeNext.y) * fg) * ratio,
-                     uz = ((lez + loeNext.z) * fb) * ratio;
-        if (finite3(ux, uy, uz)) { vle.x += ux; vle.y += uy; vle.z += uz; ++nle; } else ++rejLoe;
-    }
-    if (nee && (a.loe_mask & PSTF_TECH_NEE)) {
-        const double x = S.f(PS_NEELOE), y = S.f(PS_NEELOE + 1), z2 = S.f(PS_NEELOE + 2);
-        if (finite3(x, y, z2)) { vle.x += x; vle.y += y; vle.z += z2; ++nle; } else ++rejLoe;
-    }
-    double4 vfc = make_double4(0.0, 0.0, 0.0, 1.0); /* FLi continuation (241-246) */
-    uint32_t nfc = 1;
-    if (cont && (a.fli_mask & PSTF_TECH_CONTINUATION)) {
-        const double x = fr * lix, y = fg * liy, z2 = fb * liz;
-        if (finite3(x, y, z2)) { vfc.x += x; vfc.y += y; vfc.z += z2; ++nfc; } else ++rejFli;
-    }
-    double4 vfn = make_double4(0.0, 0.0, 0.0, 1.0); /* FLi NEE (247-254) */
-    uint32_t nfn = 1;
-    if (nee && (a.fli_mask & PSTF_TECH_NEE)) {
-        const double x = S.f(PS_NEEFLI), y = S.f(PS_NEEFLI + 1), z2 = S.f(PS_NEEFLI + 2);
-        if (finite3(x, y, z2)) { vfn.x += x; vfn.y += y; vfn.z += z2; ++nfn; } else ++rejFli;
-    }
-    double4 vli = make_double4(0.0, 0.0, 0.0, 1.0); /* Li (256-261) */
-    uint32_t nli = 1;
-    if (a.has_li && cont) {
-        const double x = lix * 1.0, y = liy * 1.0, z2 = liz * 1.0;
-        if (finite3(x, y, z2)) { vli.x += x; vli.y += y; vli.z += z2; ++nli; } else ++rejLi;
-    }
-    phase(); /* every input field of the vertex has been read: the stage may be refilled */
-    if (live) {
-        if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
-        if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
-        if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
-        if (rejLi) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rejLi);
-    }
-    const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+    phase(); /* hook between the lookups and the contributions (NoPhase in the tiled kernel) */
     if (a.dbg & 4) {
-        const double t = vlo.x + vle.y + vfc.z + vfn.x + vli.y;
         if ((m0.x ^ m1.x ^ m2.x ^ m3.x ^ m4.x ^ kLo.checksum ^ kFc.checksum ^ kFn.checksum) ==
-                0x12345u && t == 1.2345)
+                0x12345u && loNext.x + loeNext.y == 1.2345)
             atomicAdd(&sLo.ctr[C_INTERNAL], 1ull);
         return;
     }
+
+    /* ---- probes of the five update keys: settle the frame-start table first, so the home
+     * words die before the values are built ---- */
     uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
     const int r0 = live ? resolve_probe(sLo, h0, kLo.checksum, m0, &k0) : -3;
     const int r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
@@ -960,11 +884,84 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const int r4 = has4 ? resolve_probe(sLi, h4, kFc.checksum, m4, &k4) : -3;
     const bool red = !(a.dbg & 2);
     const bool agg = (a.dbg & 16) != 0; /* warp aggregation measured slower on config 2 */
-    apply_contribution(sLo, ps, sm, 0, kLo, vlo, nlo, r0, k0, red, agg);
-    apply_contribution(sLoe, ps, sm, 1, kLo, vle, nle, r1, k1, red, agg); /* Lo\E key == Lo key */
-    apply_contribution(sFli, ps, sm, 2, kFc, vfc, nfc, r2, k2, red, agg);
-    apply_contribution(sFli, ps, sm, 2, kFn, vfn, nfn, r3, k3, red, agg);
-    if (a.has_li) apply_contribution(sLi, ps, sm, 3, kFc, vli, nli, r4, k4, red, agg);
+    const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+
+    /* ---- update values (field.cpp:13-25 evaluation order), each built from the staged inputs
+     * just before its contribution so at most one value is live at a time ---- */
+    if (cont && !nsurf) /* environment (estimators.cpp:209) */
+        loNext = make_double3(S.f(PS_NEMIS), S.f(PS_NEMIS + 1), S.f(PS_NEMIS + 2));
+    const bool transp = cont && S.f(PS_RATIO) > 0.0;
+    unsigned rej = 0;
+    {   /* Lo: counter, emission, transport (estimators.cpp:210-224) */
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nc = 1;
+        const double ex = S.f(PS_EMIS), ey = S.f(PS_EMIS + 1), ez = S.f(PS_EMIS + 2);
+        if (finite3(ex, ey, ez)) { v.x += ex; v.y += ey; v.z += ez; ++nc; } else ++rej;
+        if (transp) {
+            const double ratio = S.f(PS_RATIO);
+            const double ux = ((0.0 + loNext.x) * S.f(PS_F)) * ratio,
+                         uy = ((0.0 + loNext.y) * S.f(PS_F + 1)) * ratio,
+                         uz = ((0.0 + loNext.z) * S.f(PS_F + 2)) * ratio;
+            if (finite3(ux, uy, uz)) { v.x += ux; v.y += uy; v.z += uz; ++nc; } else ++rej;
+        }
+        if (live && rej) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rej);
+        apply_contribution(sLo, ps, sm, 0, kLo, v, nc, r0, k0, red, agg);
+    }
+    {   /* Lo\E (226-234); its key is the Lo key */
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nc = 1;
+        rej = 0;
+        if (transp && (a.loe_mask & PSTF_TECH_CONTINUATION)) {
+            const double nmis = S.f(PS_NMIS), ratio = S.f(PS_RATIO);
+            const double ux = ((S.f(PS_NEMIS) * nmis + loeNext.x) * S.f(PS_F)) * ratio,
+                         uy = ((S.f(PS_NEMIS + 1) * nmis + loeNext.y) * S.f(PS_F + 1)) * ratio,
+                         uz = ((S.f(PS_NEMIS + 2) * nmis + loeNext.z) * S.f(PS_F + 2)) * ratio;
+            if (finite3(ux, uy, uz)) { v.x += ux; v.y += uy; v.z += uz; ++nc; } else ++rej;
+        }
+        if (nee && (a.loe_mask & PSTF_TECH_NEE)) {
+            const double x = S.f(PS_NEELOE), y = S.f(PS_NEELOE + 1), z2 = S.f(PS_NEELOE + 2);
+            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        }
+        if (live && rej) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rej);
+        apply_contribution(sLoe, ps, sm, 1, kLo, v, nc, r1, k1, red, agg);
+    }
+    /* Li = Le + Lo\E(next) (estimators.cpp:239) */
+    const auto li = [&](int c, double lo_e) {
+        return S.f(PS_NEMIS + c) * S.f(PS_NMIS) + lo_e;
+    };
+    rej = 0;
+    {   /* FLi continuation (241-246) */
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nc = 1;
+        if (cont && (a.fli_mask & PSTF_TECH_CONTINUATION)) {
+            const double x = S.f(PS_F) * li(0, loeNext.x), y = S.f(PS_F + 1) * li(1, loeNext.y),
+                         z2 = S.f(PS_F + 2) * li(2, loeNext.z);
+            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        }
+        apply_contribution(sFli, ps, sm, 2, kFc, v, nc, r2, k2, red, agg);
+    }
+    {   /* FLi NEE (247-254) */
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nc = 1;
+        if (nee && (a.fli_mask & PSTF_TECH_NEE)) {
+            const double x = S.f(PS_NEEFLI), y = S.f(PS_NEEFLI + 1), z2 = S.f(PS_NEEFLI + 2);
+            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        }
+        if (live && rej) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rej);
+        apply_contribution(sFli, ps, sm, 2, kFn, v, nc, r3, k3, red, agg);
+    }
+    if (a.has_li) { /* Li (256-261) */
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+        uint32_t nc = 1;
+        rej = 0;
+        if (cont) {
+            const double x = li(0, loeNext.x) * 1.0, y = li(1, loeNext.y) * 1.0,
+                         z2 = li(2, loeNext.z) * 1.0;
+            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        }
+        if (live && rej) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rej);
+        apply_contribution(sLi, ps, sm, 3, kFc, v, nc, r4, k4, red, agg);
+    }
 }
 
 template <int STAGES, int MINB>
@@ -2822,21 +2819,23 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
          * (96 regs, spills), L2-prefetch-only loads without staging, and a split A/B
          * two-group staging with an extra barrier per tile. */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 1) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
         const int stages = cfg == 0 ? 2 : 1;
-        const int minb = cfg == 0 ? 3 : 4;
+        const int minb = cfg == 0 ? 3 : cfg == 1 ? 4 : 5;
         const size_t smem = stages * sizeof(TileStage) + 64;
-        static bool attr[2] = {false, false};
+        static bool attr[3] = {false, false, false};
         if (!attr[cfg]) {
-            cudaError_t e = cfg == 0 ? cudaFuncSetAttribute(k_vertex_pass_tiled<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                     : cudaFuncSetAttribute(k_vertex_pass_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            CK(e);
+            const void *fn = cfg == 0 ? (const void *)k_vertex_pass_tiled<2, 3>
+                           : cfg == 1 ? (const void *)k_vertex_pass_tiled<1, 4>
+                                      : (const void *)k_vertex_pass_tiled<1, 5>;
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr[cfg] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
         if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
-        else LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
+        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
+        else LAUNCH((k_vertex_pass_tiled<1, 5>), grid, VT, smem, st, b);
     } else if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
     else

@@ -609,26 +609,67 @@ PSTF_HD double atan2_try(double y, double x, int *nx) {
     return swap ? 1.5707963267948966 - th : th;
 }
 
-/* octahedral cell coordinates (at resolution 8) of d and optionally -d from the fast path; *nx
- * set when any coordinate lies within 1e-11 of a cell boundary or the inputs are out of the fast
- * path's domain (the caller then recomputes with octa_f8_exact) */
+/* floor(q) of q = 8 U in single precision; near when q is within 2e-5 of an integer (the
+ * single-precision U below is within 1e-6 of the exact one, see octa_f8_try) */
+PSTF_HD int32_t f8_of32(float U, int *near) {
+    const float q = U * 8.0f;
+    const float fl = floorf(q);
+    *near |= fabsf((q - fl) - 0.5f) > 0.5f - 2e-5f;
+    return (int32_t)fl;
+}
+
+/* octahedral cell coordinates (at resolution 8) of d and optionally -d from a single-precision
+ * fast path; *nx set when any coordinate may lie within its error of a cell boundary or the
+ * inputs are outside the fast path's domain (the caller then recomputes with octa_f8_exact).
+ * Error budget (|.| in U units): w = 1 - |z| is formed in double precision and rounded once
+ * (6e-8 relative), r = sqrtf(w) correctly rounded, phi from a degree-4 minimax polynomial in t^2
+ * after an octant reduction with a correctly rounded reciprocal (|error| < 3e-7), then four
+ * rounded products/sums: |U' - U| < 1e-6, so q' = 8 U' is within 8e-6 of q, well inside the
+ * 2e-5 margin.  NaN, infinite and denormal-scale x, y always take the exact path. */
 PSTF_HD void octa_f8_try(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg,
                          int *nx) {
     const double x = fabs(dx), y = fabs(dy), z = fabs(dz);
     const double omz = 1.0 - z;
-    const double w = (0.0 < omz) ? omz : 0.0; /* safeSqrt: std::max(0.0, x) vecmath.h:22 */
-    const double r = fast_sqrt01(w);
-    const double phi =
-        (x == 0.0 && y == 0.0) ? 0.0 : atan2_try(y, x, nx) * (2.0 / 3.14159265358979323846);
-    const double v0 = phi * r, u0 = r - v0;
-    double U, V;
-    octa_uv(u0, v0, dx, dy, dz, &U, &V);
-    pos->u = f8_of(U, nx);
-    pos->v = f8_of(V, nx);
+    const float r = sqrtf((float)((0.0 < omz) ? omz : 0.0)); /* safeSqrt (vecmath.h:22) */
+    float phi = 0.0f;
+    if (!(x == 0.0 && y == 0.0)) {
+        const double mx = x > y ? x : y;
+        *nx |= !(mx >= 1e-30 && mx <= 1e30); /* also NaN */
+        const float xf = (float)x, yf = (float)y;
+        const bool swap = yf > xf;
+        const float a = swap ? xf : yf, b = swap ? yf : xf; /* 0 <= a <= b */
+        const bool small = a <= b * 0.41421356f;
+        const float num = small ? a : a - b, den = small ? b : a + b;
+#if defined(__CUDA_ARCH__)
+        const float t = num * __frcp_rn(den);
+#else
+        const float t = num * (1.0f / den);
+#endif
+        const float zz = t * t;
+        float p = 0.07726402580738068f;
+        p = fmaf(p, zz, -0.13751664757728577f);
+        p = fmaf(p, zz, 0.19961561262607574f);
+        p = fmaf(p, zz, -0.33332183957099915f);
+        p = fmaf(p, zz, 0.9999998807907104f);
+        const float th = (small ? 0.0f : 0.78539816f) + t * p;
+        phi = (swap ? 1.57079633f - th : th) * 0.63661977f; /* * 2/pi */
+    }
+    const float v0 = phi * r, u0 = r - v0;
+    float u = u0, v = v0;
+    if (dz < 0.0) { /* hemisphere swap (mappings.h:43-48) */
+        u = 1.0f - v0;
+        v = 1.0f - u0;
+    }
+    pos->u = f8_of32(0.5f * (copysignf(u, (float)dx) + 1.0f), nx);
+    pos->v = f8_of32(0.5f * (copysignf(v, (float)dy) + 1.0f), nx);
     if (want_neg) {
-        octa_uv(u0, v0, -dx, -dy, -dz, &U, &V);
-        neg->u = f8_of(U, nx);
-        neg->v = f8_of(V, nx);
+        float un = u0, vn = v0;
+        if (-dz < 0.0) {
+            un = 1.0f - v0;
+            vn = 1.0f - u0;
+        }
+        neg->u = f8_of32(0.5f * (copysignf(un, (float)-dx) + 1.0f), nx);
+        neg->v = f8_of32(0.5f * (copysignf(vn, (float)-dy) + 1.0f), nx);
     }
 }
 
