@@ -322,7 +322,8 @@ __device__ __forceinline__ void red_add4(double4 *dst, double4 t) {
 }
 
 /* res: >= 0 existing slot, -1 new key, -2 dropped, -3 no update; mark = slot's meta.y */
-__device__ __forceinline__ void apply_contribution(const DevStore &s, const PendSink &a,
+template <class Store>
+__device__ __forceinline__ void apply_contribution(const Store &s, const PendSink &a,
                                                    double4 *sm, int sid, const Key &k, double4 v,
                                                    uint32_t ncalls, int res, uint32_t mark,
                                                    bool do_red = true, bool aggregate = true) {
@@ -620,9 +621,11 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
  * cell once and each direction goes through atan2 once (pos_q / octa_pair), shared by the Lo,
  * Lo\E, FLi and Li keys and by every level of the next-vertex lookup chain.
  */
-#define VT 128
-#define VT_STAGES 2
-#define VT_BLOCKS_PER_SM 3
+#ifndef VT_THREADS
+#define VT_THREADS 128 /* vertices (= threads) per tile and CTA */
+#endif
+#define VT VT_THREADS
+#define VT_MINB (512 / VT) /* resident CTAs per SM of the default single-stage config */
 
 struct TileStage {
     double f[PS_NUM_F64][VT];
@@ -730,16 +733,21 @@ __device__ __forceinline__ Key make_key(uint64_t h1, int level, int32_t c0, int3
     return k;
 }
 
-struct NoPhase {
-    __device__ __forceinline__ void operator()() const {}
+/* Pipe hooks of vertex_body, called by all 32 lanes of every warp:
+ *   key_inputs_done()  every key input (fields 0..PS_NA-1 and the flags) has been read
+ *   wait_values()      before the first value input (fields PS_NA..) is read
+ *   values_done()      every value input has been read
+ * The single-stage tiled kernel needs none of them (NoPipe); the split-stage kernel refills its
+ * key-input stage early and its value-input stage late through them. */
+struct NoPipe {
+    __device__ __forceinline__ void key_inputs_done() const {}
+    __device__ __forceinline__ void wait_values() const {}
+    __device__ __forceinline__ void values_done() const {}
 };
 
-/* Phase: called by every lane once it has read its last input field and before the probes and
- * contributions, so the tiled caller can start the next tile's bulk copy into the stage while
- * this tile's REDs are still in flight. */
-template <class Src, class Phase = NoPhase>
+template <class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
-                                            double4 *sm, const Phase &phase = Phase()) {
+                                            double4 *sm, const Pipe &pipe = Pipe()) {
     const DevStore &sLo = a.st.s[0];
     const DevStore &sLoe = a.st.s[1];
     const DevStore &sFli = a.st.s[2];
@@ -789,6 +797,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         n1 = cell_exact(kp, qy, l0);
         n2 = cell_exact(kp, qz, l0);
     }
+    pipe.key_inputs_done();
     const uint64_t h1 = pack_h1(level, c0, c1);
     const Key kLo = make_key(h1, level, c0, c1, c2, dir_cell_f8(fo.u, level), dir_cell_f8(fo.v, level));
     const Key kFc = make_key(h1, level, c0, c1, c2, dir_cell_f8(fi.u, level), dir_cell_f8(fi.v, level));
@@ -866,11 +875,12 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         }
     }
 
-    phase(); /* hook between the lookups and the contributions (NoPhase in the tiled kernel) */
     if (a.dbg & 4) {
         if ((m0.x ^ m1.x ^ m2.x ^ m3.x ^ m4.x ^ kLo.checksum ^ kFc.checksum ^ kFn.checksum) ==
                 0x12345u && loNext.x + loeNext.y == 1.2345)
             atomicAdd(&sLo.ctr[C_INTERNAL], 1ull);
+        pipe.wait_values();
+        pipe.values_done();
         return;
     }
 
@@ -887,81 +897,73 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const PendSink ps{a.pend, a.pend_count, a.pend_cap};
 
     /* ---- update values (field.cpp:13-25 evaluation order), each built from the staged inputs
-     * just before its contribution so at most one value is live at a time ---- */
+     * just before its contribution; one rolled loop over the five contributions keeps a single
+     * copy of the probe/RED/pending code in the instruction stream ---- */
+    pipe.wait_values();
     if (cont && !nsurf) /* environment (estimators.cpp:209) */
         loNext = make_double3(S.f(PS_NEMIS), S.f(PS_NEMIS + 1), S.f(PS_NEMIS + 2));
     const bool transp = cont && S.f(PS_RATIO) > 0.0;
-    unsigned rej = 0;
-    {   /* Lo: counter, emission, transport (estimators.cpp:210-224) */
-        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
-        uint32_t nc = 1;
-        const double ex = S.f(PS_EMIS), ey = S.f(PS_EMIS + 1), ez = S.f(PS_EMIS + 2);
-        if (finite3(ex, ey, ez)) { v.x += ex; v.y += ey; v.z += ez; ++nc; } else ++rej;
-        if (transp) {
-            const double ratio = S.f(PS_RATIO);
-            const double ux = ((0.0 + loNext.x) * S.f(PS_F)) * ratio,
-                         uy = ((0.0 + loNext.y) * S.f(PS_F + 1)) * ratio,
-                         uz = ((0.0 + loNext.z) * S.f(PS_F + 2)) * ratio;
-            if (finite3(ux, uy, uz)) { v.x += ux; v.y += uy; v.z += uz; ++nc; } else ++rej;
-        }
-        if (live && rej) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rej);
-        apply_contribution(sLo, ps, sm, 0, kLo, v, nc, r0, k0, red, agg);
-    }
-    {   /* Lo\E (226-234); its key is the Lo key */
-        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
-        uint32_t nc = 1;
-        rej = 0;
-        if (transp && (a.loe_mask & PSTF_TECH_CONTINUATION)) {
-            const double nmis = S.f(PS_NMIS), ratio = S.f(PS_RATIO);
-            const double ux = ((S.f(PS_NEMIS) * nmis + loeNext.x) * S.f(PS_F)) * ratio,
-                         uy = ((S.f(PS_NEMIS + 1) * nmis + loeNext.y) * S.f(PS_F + 1)) * ratio,
-                         uz = ((S.f(PS_NEMIS + 2) * nmis + loeNext.z) * S.f(PS_F + 2)) * ratio;
-            if (finite3(ux, uy, uz)) { v.x += ux; v.y += uy; v.z += uz; ++nc; } else ++rej;
-        }
-        if (nee && (a.loe_mask & PSTF_TECH_NEE)) {
-            const double x = S.f(PS_NEELOE), y = S.f(PS_NEELOE + 1), z2 = S.f(PS_NEELOE + 2);
-            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
-        }
-        if (live && rej) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rej);
-        apply_contribution(sLoe, ps, sm, 1, kLo, v, nc, r1, k1, red, agg);
-    }
     /* Li = Le + Lo\E(next) (estimators.cpp:239) */
     const auto li = [&](int c, double lo_e) {
         return S.f(PS_NEMIS + c) * S.f(PS_NMIS) + lo_e;
     };
-    rej = 0;
-    {   /* FLi continuation (241-246) */
-        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
-        uint32_t nc = 1;
-        if (cont && (a.fli_mask & PSTF_TECH_CONTINUATION)) {
-            const double x = S.f(PS_F) * li(0, loeNext.x), y = S.f(PS_F + 1) * li(1, loeNext.y),
-                         z2 = S.f(PS_F + 2) * li(2, loeNext.z);
-            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+    const auto add3 = [](double4 &v, uint32_t &nc, unsigned &rej, double x, double y, double z2) {
+        if (finite3(x, y, z2)) {
+            v.x += x;
+            v.y += y;
+            v.z += z2;
+            ++nc;
+        } else {
+            ++rej;
         }
-        apply_contribution(sFli, ps, sm, 2, kFc, v, nc, r2, k2, red, agg);
-    }
-    {   /* FLi NEE (247-254) */
-        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
+    };
+    unsigned rej = 0;
+    const int ncontrib = a.has_li ? 5 : 4;
+#pragma unroll 1
+    for (int c = 0; c < ncontrib; ++c) {
+        double4 v = make_double4(0.0, 0.0, 0.0, 1.0); /* the counter call */
         uint32_t nc = 1;
-        if (nee && (a.fli_mask & PSTF_TECH_NEE)) {
-            const double x = S.f(PS_NEEFLI), y = S.f(PS_NEEFLI + 1), z2 = S.f(PS_NEEFLI + 2);
-            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        if (c == 0) { /* Lo: emission, transport (estimators.cpp:210-224) */
+            add3(v, nc, rej, S.f(PS_EMIS), S.f(PS_EMIS + 1), S.f(PS_EMIS + 2));
+            if (transp) {
+                const double ratio = S.f(PS_RATIO);
+                add3(v, nc, rej, ((0.0 + loNext.x) * S.f(PS_F)) * ratio,
+                     ((0.0 + loNext.y) * S.f(PS_F + 1)) * ratio,
+                     ((0.0 + loNext.z) * S.f(PS_F + 2)) * ratio);
+            }
+        } else if (c == 1) { /* Lo\E (226-234); its key is the Lo key */
+            if (transp && (a.loe_mask & PSTF_TECH_CONTINUATION)) {
+                const double nmis = S.f(PS_NMIS), ratio = S.f(PS_RATIO);
+                add3(v, nc, rej, ((S.f(PS_NEMIS) * nmis + loeNext.x) * S.f(PS_F)) * ratio,
+                     ((S.f(PS_NEMIS + 1) * nmis + loeNext.y) * S.f(PS_F + 1)) * ratio,
+                     ((S.f(PS_NEMIS + 2) * nmis + loeNext.z) * S.f(PS_F + 2)) * ratio);
+            }
+            if (nee && (a.loe_mask & PSTF_TECH_NEE))
+                add3(v, nc, rej, S.f(PS_NEELOE), S.f(PS_NEELOE + 1), S.f(PS_NEELOE + 2));
+        } else if (c == 2) { /* FLi continuation (241-246) */
+            if (cont && (a.fli_mask & PSTF_TECH_CONTINUATION))
+                add3(v, nc, rej, S.f(PS_F) * li(0, loeNext.x), S.f(PS_F + 1) * li(1, loeNext.y),
+                     S.f(PS_F + 2) * li(2, loeNext.z));
+        } else if (c == 3) { /* FLi NEE (247-254) */
+            if (nee && (a.fli_mask & PSTF_TECH_NEE))
+                add3(v, nc, rej, S.f(PS_NEEFLI), S.f(PS_NEEFLI + 1), S.f(PS_NEEFLI + 2));
+        } else { /* Li (256-261) */
+            if (cont)
+                add3(v, nc, rej, li(0, loeNext.x) * 1.0, li(1, loeNext.y) * 1.0,
+                     li(2, loeNext.z) * 1.0);
         }
-        if (live && rej) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rej);
-        apply_contribution(sFli, ps, sm, 2, kFn, v, nc, r3, k3, red, agg);
-    }
-    if (a.has_li) { /* Li (256-261) */
-        double4 v = make_double4(0.0, 0.0, 0.0, 1.0);
-        uint32_t nc = 1;
-        rej = 0;
-        if (cont) {
-            const double x = li(0, loeNext.x) * 1.0, y = li(1, loeNext.y) * 1.0,
-                         z2 = li(2, loeNext.z) * 1.0;
-            if (finite3(x, y, z2)) { v.x += x; v.y += y; v.z += z2; ++nc; } else ++rej;
+        const int sid = c < 2 ? c : (c < 4 ? 2 : 3);
+        const StoreRef s = store_ref(sid == 0 ? sLo : sid == 1 ? sLoe : sid == 2 ? sFli : sLi);
+        if (c != 2) { /* the two FLi contributions share one rejected-counter update */
+            if (live && rej) atomicAdd(&s.ctr[C_REJECTED], (unsigned long long)rej);
+            rej = 0;
         }
-        if (live && rej) atomicAdd(&sLi.ctr[C_REJECTED], (unsigned long long)rej);
-        apply_contribution(sLi, ps, sm, 3, kFc, v, nc, r4, k4, red, agg);
+        const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
+        const int res = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : c == 3 ? r3 : r4;
+        const uint32_t mark = c == 0 ? k0 : c == 1 ? k1 : c == 2 ? k2 : c == 3 ? k3 : k4;
+        apply_contribution(s, ps, sm, sid, k, v, nc, res, mark, red, agg);
     }
+    pipe.values_done();
 }
 
 template <int STAGES, int MINB>
@@ -975,11 +977,6 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
     const uint64_t nfull = a.n / VT;
     uint64_t policy = 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-#if PSTF_REFILL_EARLY
-    __shared__ unsigned empty_cnt_s;
-    unsigned *empty_cnt = &empty_cnt_s;
-    if (tid == 0) empty_cnt_s = 0u;
-#endif
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1017,29 +1014,6 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
                     prefetch_tile(a, nt + (uint64_t)a.pf * gridDim.x);
             }
         };
-#if PSTF_REFILL_EARLY
-        /* The last warp to finish reading its inputs refills stage s with tile nt; no warp waits
-         * for the others (the stage is only read column-per-lane, so only the bulk copy needs
-         * every read to be done). */
-        const auto release = [&]() {
-            __syncwarp();
-            if ((tid & 31) == 0) {
-                __threadfence_block();
-                if (atomicAdd(empty_cnt, 1u) == VT / 32 - 1) {
-                    *empty_cnt = 0u;
-                    __threadfence_block();
-                    issue_next();
-                }
-            }
-            __syncwarp();
-        };
-        if (a.dbg & 32) { /* experiment: stream only */
-            if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
-            release();
-        } else {
-            vertex_body(a, src, live, sm, release);
-        }
-#else
         if (a.dbg & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
@@ -1047,7 +1021,141 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
-#endif
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* K5 (split stages): the key inputs (fields 0..16 + flags, 140 B/vertex, read at the start of a
+ * vertex) and the value inputs (fields 17..33, 136 B/vertex, read at the end) live in two
+ * single-buffered stages with their own mbarriers.  The last warp of the CTA to finish reading
+ * a stage refills it with the CTA's next tile, with no CTA-wide barrier: the key stage is
+ * refilled while this tile's probes and REDs are still running, the value stage while the next
+ * tile's keys are being computed, so neither copy's latency is exposed and shared memory stays
+ * at one tile (35 KB) per CTA. */
+#define PS_NA 17 /* key-input fields: position, wo, wi, next position, nee dir, footprints */
+#define PS_NB (PS_NUM_F64 - PS_NA)
+
+struct StageA {
+    double f[PS_NA][VT];
+    uint32_t flags[VT];
+};
+struct StageB {
+    double f[PS_NB][VT];
+};
+
+struct SplitSrc {
+    const StageA *A;
+    const StageB *B;
+    int j;
+    __device__ __forceinline__ double f(int k) const {
+        return k < PS_NA ? A->f[k][j] : B->f[k - PS_NA][j];
+    }
+    __device__ __forceinline__ uint32_t flags() const { return A->flags[j]; }
+};
+
+__device__ __forceinline__ void issue_group(const VPArgs2 &a, void *dst, uint64_t *bar, int g,
+                                            uint64_t tile, uint64_t policy) {
+    const uint64_t v0 = tile * VT;
+    if (g == 0) {
+        StageA *st = reinterpret_cast<StageA *>(dst);
+        mbar_expect_tx(bar, (uint32_t)(PS_NA * VT * 8 + VT * 4));
+        for (int k = 0; k < PS_NA; ++k) bulk_g2s(&st->f[k][0], a.fld[k] + v0, VT * 8, bar, policy);
+        bulk_g2s(&st->flags[0], a.flags + v0, VT * 4, bar, policy);
+    } else {
+        StageB *st = reinterpret_cast<StageB *>(dst);
+        mbar_expect_tx(bar, (uint32_t)(PS_NB * VT * 8));
+        for (int k = 0; k < PS_NB; ++k)
+            bulk_g2s(&st->f[k][0], a.fld[PS_NA + k] + v0, VT * 8, bar, policy);
+    }
+}
+
+__device__ __forceinline__ void prefetch_group(const VPArgs2 &a, int g, uint64_t tile) {
+    const uint64_t v0 = tile * VT;
+    if (g == 0) {
+        for (int k = 0; k < PS_NA; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
+        prefetch_l2(a.flags + v0, VT * 4);
+    } else {
+        for (int k = PS_NA; k < PS_NUM_F64; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
+    }
+}
+
+struct SplitPipe {
+    const VPArgs2 &a;
+    StageA *A;
+    StageB *B;
+    uint64_t *bars;   /* [0] key stage full, [1] value stage full */
+    unsigned *done;   /* per stage: warps done reading (monotonic; every VT/32-th is the last) */
+    uint64_t nt;      /* this CTA's next tile */
+    uint64_t nfull;
+    uint64_t policy;
+    uint32_t parity;
+    bool partial;     /* the partial last tile: filled by plain loads, no barrier wait */
+
+    __device__ __forceinline__ void release(int g) const {
+        __syncwarp();
+        if ((threadIdx.x & 31u) == 0u && (atomicAdd(&done[g], 1u) % (VT / 32)) == VT / 32 - 1 &&
+            nt < nfull) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_group(a, g == 0 ? (void *)A : (void *)B, &bars[g], g, nt, policy);
+            if (nt + (uint64_t)a.pf * gridDim.x < nfull)
+                prefetch_group(a, g, nt + (uint64_t)a.pf * gridDim.x);
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ void key_inputs_done() const { release(0); }
+    __device__ __forceinline__ void wait_values() const {
+        if (!partial) mbar_wait(&bars[1], parity);
+    }
+    __device__ __forceinline__ void values_done() const { release(1); }
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_split(VPArgs2 a) {
+    __shared__ __align__(128) StageA sA;
+    __shared__ __align__(128) StageB sB;
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ unsigned done[2];
+    __shared__ double4 wsm[VT / 32][36]; /* 32 cells + 32 ints of probe results */
+    const int tid = threadIdx.x;
+    double4 *sm = wsm[tid >> 5];
+    const uint64_t nfull = a.n / VT;
+    uint64_t policy = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        done[0] = done[1] = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < nfull) {
+        issue_group(a, &sA, &bars[0], 0, blockIdx.x, policy);
+        issue_group(a, &sB, &bars[1], 1, blockIdx.x, policy);
+        if (blockIdx.x + (uint64_t)a.pf * gridDim.x < nfull) {
+            prefetch_group(a, 0, blockIdx.x + (uint64_t)a.pf * gridDim.x);
+            prefetch_group(a, 1, blockIdx.x + (uint64_t)a.pf * gridDim.x);
+        }
+    }
+    uint32_t it = 0;
+    const uint64_t ntiles = (a.n + VT - 1) / VT;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const bool partial = tile >= nfull;
+        bool live = true;
+        if (!partial) {
+            mbar_wait(&bars[0], it & 1u);
+        } else {
+            /* the partial last tile: plain loads into this lane's own columns (no bulk copy is
+             * in flight any more and every lane only ever touches its own columns) */
+            const uint64_t v = tile * VT + tid;
+            live = v < a.n;
+            for (int k = 0; k < PS_NA; ++k) sA.f[k][tid] = live ? a.fld[k][v] : 0.0;
+            for (int k = 0; k < PS_NB; ++k) sB.f[k][tid] = live ? a.fld[PS_NA + k][v] : 0.0;
+            sA.flags[tid] = live ? a.flags[v] : 0u;
+        }
+        const SplitSrc src{&sA, &sB, tid};
+        const SplitPipe pipe{a, &sA, &sB, bars, done, tile + gridDim.x, nfull, policy, it & 1u,
+                             partial};
+        vertex_body(a, src, live, sm, pipe);
     }
 }
 
@@ -2819,22 +2927,27 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
          * (96 regs, spills), L2-prefetch-only loads without staging, and a split A/B
          * two-group staging with an extra barrier per tile. */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 3) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
+        if (cfg == 3) {
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
+            LAUNCH((k_vertex_pass_split<VT_MINB>), grid, VT, 0, st, b);
+            return PSTF_OK;
+        }
         const int stages = cfg == 0 ? 2 : 1;
-        const int minb = cfg == 0 ? 3 : cfg == 1 ? 4 : 5;
+        const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
         const size_t smem = stages * sizeof(TileStage) + 64;
         static bool attr[3] = {false, false, false};
         if (!attr[cfg]) {
             const void *fn = cfg == 0 ? (const void *)k_vertex_pass_tiled<2, 3>
-                           : cfg == 1 ? (const void *)k_vertex_pass_tiled<1, 4>
+                           : cfg == 1 ? (const void *)k_vertex_pass_tiled<1, VT_MINB>
                                       : (const void *)k_vertex_pass_tiled<1, 5>;
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr[cfg] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
         if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
-        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, 4>), grid, VT, smem, st, b);
+        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, VT_MINB>), grid, VT, smem, st, b);
         else LAUNCH((k_vertex_pass_tiled<1, 5>), grid, VT, smem, st, b);
     } else if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);

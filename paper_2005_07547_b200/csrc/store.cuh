@@ -62,6 +62,20 @@ struct DevStore {
     uint32_t owner_shift; // owner(slot) = slot >> owner_shift (capacity_log2 - log2 world)
 };
 
+/* the members of a store that a contribution touches, selectable per loop iteration */
+struct StoreRef {
+    uint2 *meta;
+    double4 *acc;
+    uint32_t *tbits;
+    unsigned long long *ctr;
+    uint32_t frame;
+    int32_t rank;
+};
+
+__device__ __forceinline__ StoreRef store_ref(const DevStore &s) {
+    return StoreRef{s.meta, s.acc, s.tbits, s.ctr, s.frame, s.rank};
+}
+
 __device__ __forceinline__ bool owned(const DevStore &s, uint32_t slot) {
     return (int32_t)(slot >> s.owner_shift) == s.rank;
 }
@@ -103,7 +117,8 @@ __device__ __forceinline__ int probe_existing(const DevStore &s, uint32_t home, 
 
 /* lastTouched = frame (field.cpp:123,133,137); mark = the meta.y word seen by the probe, so an
  * already-touched slot costs no store */
-__device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot, uint32_t mark) {
+template <class Store>
+__device__ __forceinline__ void touch_slot(const Store &s, uint32_t slot, uint32_t mark) {
     const uint32_t m = s.frame + 1u;
     if (mark != m) {
         s.meta[slot].y = m;
@@ -111,7 +126,8 @@ __device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot, uin
     }
 }
 
-__device__ __forceinline__ void touch_slot(const DevStore &s, uint32_t slot) {
+template <class Store>
+__device__ __forceinline__ void touch_slot(const Store &s, uint32_t slot) {
     s.meta[slot].y = s.frame + 1u;
     atomicOr(&s.tbits[slot >> 5], 1u << (slot & 31u));
 }
