@@ -17,6 +17,8 @@
  *            slots touched this frame, then blend + cap + zero accumulators, fused with the
  *            age-eviction rule when the table is more than 3/4 full (field.cpp:197-263).
  */
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -700,6 +702,29 @@ __device__ __forceinline__ void issue_tile(const VPArgs2 &a, TileStage *st, uint
     bulk_g2s(&st->flags[0], a.flags + v0, VT * 4, bar, policy);
 }
 
+/* Uniformly strided inputs (all 34 f64 fields of one buffer at a fixed field stride, the layout
+ * of pstf_synth_generate and pstf_vertex_soa_from_buffer): one 2-D tensor copy moves a tile's
+ * [34][VT] block, one 1-D bulk copy its flags, instead of 35 per-field copies. */
+__device__ __forceinline__ void issue_tile_tmap(const VPArgs2 &a, const CUtensorMap *tm,
+                                                TileStage *st, uint64_t *bar, uint64_t tile,
+                                                uint64_t policy) {
+    mbar_expect_tx(bar, (uint32_t)(PS_NUM_F64 * VT * 8 + VT * 4));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(&st->f[0][0])),
+        "l"(tm), "r"((int)(tile * VT)), "r"(0), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+    bulk_g2s(&st->flags[0], a.flags + tile * VT, VT * 4, bar, policy);
+}
+
+__device__ __forceinline__ void prefetch_tile_tmap(const VPArgs2 &a, const CUtensorMap *tm,
+                                                   uint64_t tile) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tm),
+                 "r"((int)(tile * VT)), "r"(0)
+                 : "memory");
+    prefetch_l2(a.flags + tile * VT, VT * 4);
+}
+
 /* pull a later tile's segments into L2 so its shared-memory copy completes at L2 latency */
 __device__ __forceinline__ void prefetch_tile(const VPArgs2 &a, uint64_t tile) {
     const uint64_t v0 = tile * VT;
@@ -966,8 +991,9 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     pipe.values_done();
 }
 
-template <int STAGES, int MINB>
-__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
+template <int STAGES, int MINB, bool TMAP>
+__global__ void __launch_bounds__(VT, MINB)
+    k_vertex_pass_tiled(VPArgs2 a, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileStage *stages = reinterpret_cast<TileStage *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + STAGES * sizeof(TileStage));
@@ -985,9 +1011,15 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
     if (tid == 0)
         for (int s = 0; s < STAGES; ++s) {
             uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
-            if (t < nfull) issue_tile(a, &stages[s], &bars[s], t, policy);
+            if (t < nfull) {
+                if (TMAP) issue_tile_tmap(a, &tm, &stages[s], &bars[s], t, policy);
+                else issue_tile(a, &stages[s], &bars[s], t, policy);
+            }
             for (int d = 1; d <= a.pf; ++d)
-                if (t + (uint64_t)d * gridDim.x < nfull) prefetch_tile(a, t + (uint64_t)d * gridDim.x);
+                if (t + (uint64_t)d * gridDim.x < nfull) {
+                    if (TMAP) prefetch_tile_tmap(a, &tm, t + (uint64_t)d * gridDim.x);
+                    else prefetch_tile(a, t + (uint64_t)d * gridDim.x);
+                }
         }
     uint32_t it = 0;
     const uint64_t ntiles = (a.n + VT - 1) / VT;
@@ -1009,9 +1041,14 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_tiled(VPArgs2 a) {
         const auto issue_next = [&]() {
             if (nt < nfull) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_tile(a, &stages[s], &bars[s], nt, policy);
-                if (nt + (uint64_t)a.pf * gridDim.x < nfull)
-                    prefetch_tile(a, nt + (uint64_t)a.pf * gridDim.x);
+                const uint64_t pt = nt + (uint64_t)a.pf * gridDim.x;
+                if (TMAP) {
+                    issue_tile_tmap(a, &tm, &stages[s], &bars[s], nt, policy);
+                    if (pt < nfull) prefetch_tile_tmap(a, &tm, pt);
+                } else {
+                    issue_tile(a, &stages[s], &bars[s], nt, policy);
+                    if (pt < nfull) prefetch_tile(a, pt);
+                }
             }
         };
         if (a.dbg & 32) { /* experiment: stream only */
@@ -2052,6 +2089,20 @@ static Stores4 stores4(pstf_field *const *fs, int nf) {
     return s;
 }
 
+/* cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link) */
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
 static int read_small(Scratch &sc, const void *dev, size_t bytes, cudaStream_t st) {
     if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
     CK(cudaMemcpyAsync(sc.h_small, dev, bytes, cudaMemcpyDeviceToHost, st));
@@ -2937,18 +2988,43 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
         const size_t smem = stages * sizeof(TileStage) + 64;
-        static bool attr[3] = {false, false, false};
-        if (!attr[cfg]) {
-            const void *fn = cfg == 0 ? (const void *)k_vertex_pass_tiled<2, 3>
-                           : cfg == 1 ? (const void *)k_vertex_pass_tiled<1, VT_MINB>
-                                      : (const void *)k_vertex_pass_tiled<1, 5>;
+        /* one 2-D tensor map over the 34 f64 fields when they sit at a uniform stride */
+        CUtensorMap tm;
+        memset(&tm, 0, sizeof(tm));
+        bool tmap = false;
+        if (cfg == 1 && !getenv("PSTF_NO_TMAP")) {
+            const long long stride = (const char *)ptrs[1] - (const char *)ptrs[0];
+            bool uniform = stride > 0 && stride % 16 == 0 && (uint64_t)stride >= n * 8 &&
+                           n < (1ull << 31);
+            for (int k = 2; k < PS_NUM_F64 && uniform; ++k)
+                uniform = (const char *)ptrs[k] - (const char *)ptrs[0] == k * stride;
+            PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+            if (uniform && enc) {
+                const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)PS_NUM_F64};
+                const cuuint64_t gstride[1] = {(cuuint64_t)stride};
+                const cuuint32_t box[2] = {VT, PS_NUM_F64};
+                const cuuint32_t es[2] = {1, 1};
+                tmap = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptrs[0]),
+                           gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+        }
+        const int fi = cfg == 0 ? 0 : cfg == 2 ? 1 : tmap ? 3 : 2;
+        static bool attr[4] = {false, false, false, false};
+        if (!attr[fi]) {
+            const void *fn = fi == 0 ? (const void *)k_vertex_pass_tiled<2, 3, false>
+                           : fi == 1 ? (const void *)k_vertex_pass_tiled<1, 5, false>
+                           : fi == 2 ? (const void *)k_vertex_pass_tiled<1, VT_MINB, false>
+                                     : (const void *)k_vertex_pass_tiled<1, VT_MINB, true>;
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr[cfg] = true;
+            attr[fi] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
-        if (cfg == 0) LAUNCH((k_vertex_pass_tiled<2, 3>), grid, VT, smem, st, b);
-        else if (cfg == 1) LAUNCH((k_vertex_pass_tiled<1, VT_MINB>), grid, VT, smem, st, b);
-        else LAUNCH((k_vertex_pass_tiled<1, 5>), grid, VT, smem, st, b);
+        if (fi == 0) LAUNCH((k_vertex_pass_tiled<2, 3, false>), grid, VT, smem, st, b, tm);
+        else if (fi == 1) LAUNCH((k_vertex_pass_tiled<1, 5, false>), grid, VT, smem, st, b, tm);
+        else if (fi == 2) LAUNCH((k_vertex_pass_tiled<1, VT_MINB, false>), grid, VT, smem, st, b, tm);
+        else LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true>), grid, VT, smem, st, b, tm);
     } else if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
     else
