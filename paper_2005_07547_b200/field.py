@@ -546,13 +546,33 @@ def synth_generate(width, height, bounces, seed=0x5EED, iteration=0, cam_shift_x
     return out, n
 
 
+def vertex_soa_from_fields(fields, flags) -> _VertexSoa:
+    """pstf_vertex_soa from 34 separate fp64 device arrays (PS_* order: position xyz, wo, wi,
+    next position, nee dir, footprint, next footprint, ratio, next MIS weight, emission, f,
+    next emission, nee Lo\\E, nee FLi) and a u32 flags array (tensors or raw pointers)."""
+    ptr = lambda t: t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+    v = _VertexSoa()
+    k = 0
+    for name, typ in _VertexSoa._fields_:
+        if name == "flags":
+            v.flags = ptr(flags)
+        elif typ is _Vec3:
+            setattr(v, name, _Vec3(ptr(fields[k]), ptr(fields[k + 1]), ptr(fields[k + 2])))
+            k += 3
+        else:
+            setattr(v, name, ptr(fields[k]))
+            k += 1
+    return v
+
+
 def vertex_pass(lo, loe, fli, li, buf, n, loe_mask=TECH_ALL, fli_mask=TECH_ALL,
-                mode=MODE_ATOMIC):
-    """FieldRecorder::onVertex for n vertices in a device buffer (estimators.cpp:194-262)."""
+                mode=MODE_ATOMIC, soa=None):
+    """FieldRecorder::onVertex for n vertices in a device buffer (estimators.cpp:194-262);
+    soa: a prebuilt pstf_vertex_soa (vertex_soa_from_fields) instead of buf."""
     for s in (lo, loe, fli, li):
         if s is not None:
             s.flush()
-    v = vertex_soa(buf, n)
+    v = soa if soa is not None else vertex_soa(buf, n)
     _check(lib().pstf_vertex_pass(lo._h, loe._h, fli._h, li._h if li is not None else None,
                                   C.byref(v), n, loe_mask, fli_mask, mode, _stream()))
 
