@@ -1090,9 +1090,21 @@ struct SplitSrc {
     __device__ __forceinline__ uint32_t flags() const { return A->flags[j]; }
 };
 
-__device__ __forceinline__ void issue_group(const VPArgs2 &a, void *dst, uint64_t *bar, int g,
-                                            uint64_t tile, uint64_t policy) {
+__device__ __forceinline__ void issue_group(const VPArgs2 &a, const CUtensorMap *tm, void *dst,
+                                            uint64_t *bar, int g, uint64_t tile,
+                                            uint64_t policy) {
     const uint64_t v0 = tile * VT;
+    if (tm) { /* one [17][VT] tensor copy per group (+ the flags with the key group) */
+        mbar_expect_tx(bar, (uint32_t)(PS_NA * VT * 8 + (g == 0 ? VT * 4 : 0)));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+            "l"(tm), "r"((int)v0), "r"(g == 0 ? 0 : PS_NA), "r"(smem_u32(bar)), "l"(policy)
+            : "memory");
+        if (g == 0)
+            bulk_g2s(&reinterpret_cast<StageA *>(dst)->flags[0], a.flags + v0, VT * 4, bar, policy);
+        return;
+    }
     if (g == 0) {
         StageA *st = reinterpret_cast<StageA *>(dst);
         mbar_expect_tx(bar, (uint32_t)(PS_NA * VT * 8 + VT * 4));
@@ -1116,8 +1128,11 @@ __device__ __forceinline__ void prefetch_group(const VPArgs2 &a, int g, uint64_t
     }
 }
 
+static_assert(PS_NA == PS_NB, "one tensor-map box serves both stage groups");
+
 struct SplitPipe {
     const VPArgs2 &a;
+    const CUtensorMap *tm; /* nullptr: per-field copies */
     StageA *A;
     StageB *B;
     uint64_t *bars;   /* [0] key stage full, [1] value stage full */
@@ -1133,7 +1148,7 @@ struct SplitPipe {
         if ((threadIdx.x & 31u) == 0u && (atomicAdd(&done[g], 1u) % (VT / 32)) == VT / 32 - 1 &&
             nt < nfull) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_group(a, g == 0 ? (void *)A : (void *)B, &bars[g], g, nt, policy);
+            issue_group(a, tm, g == 0 ? (void *)A : (void *)B, &bars[g], g, nt, policy);
             if (nt + (uint64_t)a.pf * gridDim.x < nfull)
                 prefetch_group(a, g, nt + (uint64_t)a.pf * gridDim.x);
         }
@@ -1146,8 +1161,10 @@ struct SplitPipe {
     __device__ __forceinline__ void values_done() const { release(1); }
 };
 
-template <int MINB>
-__global__ void __launch_bounds__(VT, MINB) k_vertex_pass_split(VPArgs2 a) {
+template <int MINB, bool TMAP>
+__global__ void __launch_bounds__(VT, MINB)
+    k_vertex_pass_split(VPArgs2 a, const __grid_constant__ CUtensorMap tmap) {
+    const CUtensorMap *tm = TMAP ? &tmap : nullptr;
     __shared__ __align__(128) StageA sA;
     __shared__ __align__(128) StageB sB;
     __shared__ __align__(8) uint64_t bars[2];
@@ -1166,8 +1183,8 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_split(VPArgs2 a) {
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x < nfull) {
-        issue_group(a, &sA, &bars[0], 0, blockIdx.x, policy);
-        issue_group(a, &sB, &bars[1], 1, blockIdx.x, policy);
+        issue_group(a, tm, &sA, &bars[0], 0, blockIdx.x, policy);
+        issue_group(a, tm, &sB, &bars[1], 1, blockIdx.x, policy);
         if (blockIdx.x + (uint64_t)a.pf * gridDim.x < nfull) {
             prefetch_group(a, 0, blockIdx.x + (uint64_t)a.pf * gridDim.x);
             prefetch_group(a, 1, blockIdx.x + (uint64_t)a.pf * gridDim.x);
@@ -1190,8 +1207,8 @@ __global__ void __launch_bounds__(VT, MINB) k_vertex_pass_split(VPArgs2 a) {
             sA.flags[tid] = live ? a.flags[v] : 0u;
         }
         const SplitSrc src{&sA, &sB, tid};
-        const SplitPipe pipe{a, &sA, &sB, bars, done, tile + gridDim.x, nfull, policy, it & 1u,
-                             partial};
+        const SplitPipe pipe{a, tm, &sA, &sB, bars, done, tile + gridDim.x, nfull, policy,
+                             it & 1u, partial};
         vertex_body(a, src, live, sm, pipe);
     }
 }
@@ -2980,19 +2997,11 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         const char *cfgs = getenv("PSTF_TILED_CFG");
         const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 3) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
-        if (cfg == 3) {
-            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
-            LAUNCH((k_vertex_pass_split<VT_MINB>), grid, VT, 0, st, b);
-            return PSTF_OK;
-        }
-        const int stages = cfg == 0 ? 2 : 1;
-        const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
-        const size_t smem = stages * sizeof(TileStage) + 64;
         /* one 2-D tensor map over the 34 f64 fields when they sit at a uniform stride */
         CUtensorMap tm;
         memset(&tm, 0, sizeof(tm));
         bool tmap = false;
-        if (cfg == 1 && !getenv("PSTF_NO_TMAP")) {
+        if ((cfg == 1 || cfg == 3) && !getenv("PSTF_NO_TMAP")) {
             const long long stride = (const char *)ptrs[1] - (const char *)ptrs[0];
             bool uniform = stride > 0 && stride % 16 == 0 && (uint64_t)stride >= n * 8 &&
                            n < (1ull << 31);
@@ -3002,7 +3011,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             if (uniform && enc) {
                 const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)PS_NUM_F64};
                 const cuuint64_t gstride[1] = {(cuuint64_t)stride};
-                const cuuint32_t box[2] = {VT, PS_NUM_F64};
+                const cuuint32_t box[2] = {VT, cfg == 3 ? (cuuint32_t)PS_NA : PS_NUM_F64};
                 const cuuint32_t es[2] = {1, 1};
                 tmap = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptrs[0]),
                            gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -3010,6 +3019,15 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             }
         }
+        if (cfg == 3) {
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
+            if (tmap) LAUNCH((k_vertex_pass_split<VT_MINB, true>), grid, VT, 0, st, b, tm);
+            else LAUNCH((k_vertex_pass_split<VT_MINB, false>), grid, VT, 0, st, b, tm);
+            return PSTF_OK;
+        }
+        const int stages = cfg == 0 ? 2 : 1;
+        const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
+        const size_t smem = stages * sizeof(TileStage) + 64;
         const int fi = cfg == 0 ? 0 : cfg == 2 ? 1 : tmap ? 3 : 2;
         static bool attr[4] = {false, false, false, false};
         if (!attr[fi]) {
