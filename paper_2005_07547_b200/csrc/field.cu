@@ -762,8 +762,9 @@ __device__ __forceinline__ Key make_key(uint64_t h1, int level, int32_t c0, int3
  *   key_inputs_done()  every key input (fields 0..PS_NA-1 and the flags) has been read
  *   wait_values()      before the first value input (fields PS_NA..) is read
  *   values_done()      every value input has been read
- * The single-stage tiled kernel needs none of them (NoPipe); the split-stage kernel refills its
- * key-input stage early and its value-input stage late through them. */
+ * The single-stage tiled kernel needs none of them (NoPipe).  A split-stage kernel that refilled
+ * its key-input stage early and its value-input stage late through them (no CTA barrier per
+ * tile) measured 0.99 ms against 0.91 ms for the synchronized single stage on config 2. */
 struct NoPipe {
     __device__ __forceinline__ void key_inputs_done() const {}
     __device__ __forceinline__ void wait_values() const {}
@@ -1058,158 +1059,6 @@ __global__ void __launch_bounds__(VT, MINB)
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
-    }
-}
-
-/* ------------------------------------------------------------------------------------------ */
-/* K5 (split stages): the key inputs (fields 0..16 + flags, 140 B/vertex, read at the start of a
- * vertex) and the value inputs (fields 17..33, 136 B/vertex, read at the end) live in two
- * single-buffered stages with their own mbarriers.  The last warp of the CTA to finish reading
- * a stage refills it with the CTA's next tile, with no CTA-wide barrier: the key stage is
- * refilled while this tile's probes and REDs are still running, the value stage while the next
- * tile's keys are being computed, so neither copy's latency is exposed and shared memory stays
- * at one tile (35 KB) per CTA. */
-#define PS_NA 17 /* key-input fields: position, wo, wi, next position, nee dir, footprints */
-#define PS_NB (PS_NUM_F64 - PS_NA)
-
-struct StageA {
-    double f[PS_NA][VT];
-    uint32_t flags[VT];
-};
-struct StageB {
-    double f[PS_NB][VT];
-};
-
-struct SplitSrc {
-    const StageA *A;
-    const StageB *B;
-    int j;
-    __device__ __forceinline__ double f(int k) const {
-        return k < PS_NA ? A->f[k][j] : B->f[k - PS_NA][j];
-    }
-    __device__ __forceinline__ uint32_t flags() const { return A->flags[j]; }
-};
-
-__device__ __forceinline__ void issue_group(const VPArgs2 &a, const CUtensorMap *tm, void *dst,
-                                            uint64_t *bar, int g, uint64_t tile,
-                                            uint64_t policy) {
-    const uint64_t v0 = tile * VT;
-    if (tm) { /* one [17][VT] tensor copy per group (+ the flags with the key group) */
-        mbar_expect_tx(bar, (uint32_t)(PS_NA * VT * 8 + (g == 0 ? VT * 4 : 0)));
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-            "l"(tm), "r"((int)v0), "r"(g == 0 ? 0 : PS_NA), "r"(smem_u32(bar)), "l"(policy)
-            : "memory");
-        if (g == 0)
-            bulk_g2s(&reinterpret_cast<StageA *>(dst)->flags[0], a.flags + v0, VT * 4, bar, policy);
-        return;
-    }
-    if (g == 0) {
-        StageA *st = reinterpret_cast<StageA *>(dst);
-        mbar_expect_tx(bar, (uint32_t)(PS_NA * VT * 8 + VT * 4));
-        for (int k = 0; k < PS_NA; ++k) bulk_g2s(&st->f[k][0], a.fld[k] + v0, VT * 8, bar, policy);
-        bulk_g2s(&st->flags[0], a.flags + v0, VT * 4, bar, policy);
-    } else {
-        StageB *st = reinterpret_cast<StageB *>(dst);
-        mbar_expect_tx(bar, (uint32_t)(PS_NB * VT * 8));
-        for (int k = 0; k < PS_NB; ++k)
-            bulk_g2s(&st->f[k][0], a.fld[PS_NA + k] + v0, VT * 8, bar, policy);
-    }
-}
-
-__device__ __forceinline__ void prefetch_group(const VPArgs2 &a, int g, uint64_t tile) {
-    const uint64_t v0 = tile * VT;
-    if (g == 0) {
-        for (int k = 0; k < PS_NA; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
-        prefetch_l2(a.flags + v0, VT * 4);
-    } else {
-        for (int k = PS_NA; k < PS_NUM_F64; ++k) prefetch_l2(a.fld[k] + v0, VT * 8);
-    }
-}
-
-static_assert(PS_NA == PS_NB, "one tensor-map box serves both stage groups");
-
-struct SplitPipe {
-    const VPArgs2 &a;
-    const CUtensorMap *tm; /* nullptr: per-field copies */
-    StageA *A;
-    StageB *B;
-    uint64_t *bars;   /* [0] key stage full, [1] value stage full */
-    unsigned *done;   /* per stage: warps done reading (monotonic; every VT/32-th is the last) */
-    uint64_t nt;      /* this CTA's next tile */
-    uint64_t nfull;
-    uint64_t policy;
-    uint32_t parity;
-    bool partial;     /* the partial last tile: filled by plain loads, no barrier wait */
-
-    __device__ __forceinline__ void release(int g) const {
-        __syncwarp();
-        if ((threadIdx.x & 31u) == 0u && (atomicAdd(&done[g], 1u) % (VT / 32)) == VT / 32 - 1 &&
-            nt < nfull) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_group(a, tm, g == 0 ? (void *)A : (void *)B, &bars[g], g, nt, policy);
-            if (nt + (uint64_t)a.pf * gridDim.x < nfull)
-                prefetch_group(a, g, nt + (uint64_t)a.pf * gridDim.x);
-        }
-        __syncwarp();
-    }
-    __device__ __forceinline__ void key_inputs_done() const { release(0); }
-    __device__ __forceinline__ void wait_values() const {
-        if (!partial) mbar_wait(&bars[1], parity);
-    }
-    __device__ __forceinline__ void values_done() const { release(1); }
-};
-
-template <int MINB, bool TMAP>
-__global__ void __launch_bounds__(VT, MINB)
-    k_vertex_pass_split(VPArgs2 a, const __grid_constant__ CUtensorMap tmap) {
-    const CUtensorMap *tm = TMAP ? &tmap : nullptr;
-    __shared__ __align__(128) StageA sA;
-    __shared__ __align__(128) StageB sB;
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ unsigned done[2];
-    __shared__ double4 wsm[VT / 32][36]; /* 32 cells + 32 ints of probe results */
-    const int tid = threadIdx.x;
-    double4 *sm = wsm[tid >> 5];
-    const uint64_t nfull = a.n / VT;
-    uint64_t policy = 0;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        done[0] = done[1] = 0u;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0 && blockIdx.x < nfull) {
-        issue_group(a, tm, &sA, &bars[0], 0, blockIdx.x, policy);
-        issue_group(a, tm, &sB, &bars[1], 1, blockIdx.x, policy);
-        if (blockIdx.x + (uint64_t)a.pf * gridDim.x < nfull) {
-            prefetch_group(a, 0, blockIdx.x + (uint64_t)a.pf * gridDim.x);
-            prefetch_group(a, 1, blockIdx.x + (uint64_t)a.pf * gridDim.x);
-        }
-    }
-    uint32_t it = 0;
-    const uint64_t ntiles = (a.n + VT - 1) / VT;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const bool partial = tile >= nfull;
-        bool live = true;
-        if (!partial) {
-            mbar_wait(&bars[0], it & 1u);
-        } else {
-            /* the partial last tile: plain loads into this lane's own columns (no bulk copy is
-             * in flight any more and every lane only ever touches its own columns) */
-            const uint64_t v = tile * VT + tid;
-            live = v < a.n;
-            for (int k = 0; k < PS_NA; ++k) sA.f[k][tid] = live ? a.fld[k][v] : 0.0;
-            for (int k = 0; k < PS_NB; ++k) sB.f[k][tid] = live ? a.fld[PS_NA + k][v] : 0.0;
-            sA.flags[tid] = live ? a.flags[v] : 0u;
-        }
-        const SplitSrc src{&sA, &sB, tid};
-        const SplitPipe pipe{a, tm, &sA, &sB, bars, done, tile + gridDim.x, nfull, policy,
-                             it & 1u, partial};
-        vertex_body(a, src, live, sm, pipe);
     }
 }
 
@@ -2989,19 +2838,19 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         b.pend = a.pend;
         b.pend_count = a.pend_count;
         b.pend_cap = a.pend_cap;
-        /* (stages, CTAs/SM): 2x3 = TMA double buffering at 168 regs; 1x4 trades the prefetch
-         * depth (the next tile is prefetched into L2) for more resident warps and measured
-         * fastest on config 2 (PSTF_TILED_CFG=0 selects 2x3).  Also measured slower: 1x5
-         * (96 regs, spills), L2-prefetch-only loads without staging, and a split A/B
-         * two-group staging with an extra barrier per tile. */
+        /* (stages, CTAs/SM): 1x4 (cfg 1, default) measured fastest on config 2; 2x3 (cfg 0,
+         * double buffering) and 1x5 (cfg 2, 96 registers) are slower, as were VT = 64 / 96,
+         * L2-prefetch-only loads without staging, refilling the stage before the
+         * contributions (mid-tile barrier, or last-warp refill without one), and two stage
+         * groups refilled at different points of the tile. */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 3) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
         /* one 2-D tensor map over the 34 f64 fields when they sit at a uniform stride */
         CUtensorMap tm;
         memset(&tm, 0, sizeof(tm));
         bool tmap = false;
-        if ((cfg == 1 || cfg == 3) && !getenv("PSTF_NO_TMAP")) {
+        if (cfg == 1 && !getenv("PSTF_NO_TMAP")) {
             const long long stride = (const char *)ptrs[1] - (const char *)ptrs[0];
             bool uniform = stride > 0 && stride % 16 == 0 && (uint64_t)stride >= n * 8 &&
                            n < (1ull << 31);
@@ -3011,19 +2860,13 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             if (uniform && enc) {
                 const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)PS_NUM_F64};
                 const cuuint64_t gstride[1] = {(cuuint64_t)stride};
-                const cuuint32_t box[2] = {VT, cfg == 3 ? (cuuint32_t)PS_NA : PS_NUM_F64};
+                const cuuint32_t box[2] = {VT, PS_NUM_F64};
                 const cuuint32_t es[2] = {1, 1};
                 tmap = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptrs[0]),
                            gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             }
-        }
-        if (cfg == 3) {
-            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
-            if (tmap) LAUNCH((k_vertex_pass_split<VT_MINB, true>), grid, VT, 0, st, b, tm);
-            else LAUNCH((k_vertex_pass_split<VT_MINB, false>), grid, VT, 0, st, b, tm);
-            return PSTF_OK;
         }
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
