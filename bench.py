@@ -286,12 +286,11 @@ def run_b200(args):
         if sharded is not None:
             sharded.iteration((bufs[i % S], n))
             return
-        if cv_out is not None:
-            pb.field._check(pb.lib().pstf_cv_lookup(
-                stores[1].handle, pb.field.C.byref(pb.vertex_soa(bufs[i % S], n)), n,
-                pb.field._ptr(cv_out[0][0]), pb.field._ptr(cv_out[0][1]),
-                pb.field._ptr(cv_out[0][2]), pb.field._ptr(cv_out[1]), pb.field._stream()))
-        pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
+        if cv_out is not None:  # config 3: the CV lookup of every vertex fused into the pass
+            pb.vertex_pass_cv(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode,
+                              out=cv_out)
+        else:
+            pb.vertex_pass(stores[0], stores[1], stores[2], None, bufs[i % S], n, mode=mode)
         pb.end_frame_all(stores)
 
     for i in range(args.warmup):
@@ -345,11 +344,11 @@ def run_b200(args):
     vp = [(k.strip("()"), v) for k, v in prof.items() if "k_vertex_pass" in k]
     vp_ms, vp_n = (vp[0][1] if vp else (float("nan"), 1))
     vp_avg = vp_ms / max(vp_n, 1)
-    vp_bytes = BYTES_PER_VERTEX * n
+    cv_bytes = 25 * n if cv_out is not None else 0  # +25 B per CV lookup (config 3)
+    vp_bytes = BYTES_PER_VERTEX * n + cv_bytes  # the CV outputs are written by the fused kernel
     ach = vp_bytes / (vp_avg / 1e3) / 1e9
     mean_touched = (sum(s["touched_total"] for s in st) - touched0) / args.steps
-    step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched + \
-        (25 * n if cv_out is not None else 0)  # +25 B per CV lookup (config 3)
+    step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched + cv_bytes
     step_ach = step_bytes / (ms_step / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_vertex_pass_traffic.json")

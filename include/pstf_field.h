@@ -219,6 +219,15 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
                           const pstf_vertex_soa *host_v, uint64_t n, uint32_t loe_mask,
                           uint32_t fli_mask, int mode, void *stream);
 
+/* pstf_vertex_pass plus the CV lookup of every vertex (the Lo\E query at its position, wo and
+ * footprint on the frame-start table, exactly pstf_cv_lookup run before the pass), fused into
+ * the vertex kernel: the query's first key is the vertex's Lo key, already probed for the
+ * update (config 3 "CV lookup at every vertex", estimators.cpp:453-462 + 194-262). */
+int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                        const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
+                        uint32_t fli_mask, int mode, double *cv_r, double *cv_g, double *cv_b,
+                        uint8_t *cv_valid, void *stream);
+
 /* CV / guiding lookup at the current vertex (estimators.cpp:438-462): out = Lo\E query at
  * (position, wo, footprint) for every vertex of the record (config 3 "CV lookup"). */
 int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, double *value_r,

@@ -11,7 +11,7 @@ from .field import (  # noqa: F401
     MODE_ORDERED, MODE_SEQUENTIAL, TECH_ALL, TECH_CAMERA, TECH_CONTINUATION, TECH_NEE,
     FieldStore, FieldStoreConfig, FieldUpdateQueue, PstfError, SpatioDirectionalKey,
     SNAPSHOT_DTYPE, SLOT_DTYPE, KEY_DTYPE, lib, library_path, read_snapshot, synth_generate,
-    vertex_pass, vertex_pass_host, cv_lookup, vertex_soa, vertex_soa_from_fields,
+    vertex_pass, vertex_pass_host, vertex_pass_cv, cv_lookup, vertex_soa, vertex_soa_from_fields,
     kernel_launch_count,
     VERTEX_BYTES, VERTEX_F64_FIELDS, profile_enable, profile_collect, end_frame_all,
 )

@@ -628,6 +628,7 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #endif
 #define VT VT_THREADS
 #define VT_MINB (512 / VT) /* resident CTAs per SM of the default single-stage config */
+static_assert(VT_MINB == 4, "the vertex-pass launch table instantiates 4 CTAs/SM");
 
 struct TileStage {
     double f[PS_NUM_F64][VT];
@@ -647,6 +648,8 @@ struct VPArgs2 {
     PendRec *pend;
     unsigned long long *pend_count;
     uint64_t pend_cap;
+    double *cv[3];     /* fused CV lookup outputs (estimators.cpp:453-462), CV instantiation only */
+    uint8_t *cv_valid;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -738,8 +741,10 @@ __device__ __forceinline__ void prefetch_tile(const VPArgs2 &a, uint64_t tile) {
 struct SmemSrc {
     const TileStage *t;
     int j;
+    uint64_t v; /* global vertex index */
     __device__ __forceinline__ double f(int k) const { return t->f[k][j]; }
     __device__ __forceinline__ uint32_t flags() const { return t->flags[j]; }
+    __device__ __forceinline__ uint64_t index() const { return v; }
 };
 
 
@@ -771,7 +776,7 @@ struct NoPipe {
     __device__ __forceinline__ void values_done() const {}
 };
 
-template <class Src, class Pipe = NoPipe>
+template <bool CV, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
                                             double4 *sm, const Pipe &pipe = Pipe()) {
     const DevStore &sLo = a.st.s[0];
@@ -846,6 +851,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 m4 = has4 ? sLi.meta[h4] : z;
     const uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
     const double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
+    /* CV lookup at this vertex = Lo\E query of the Lo key: speculate its home record too */
+    const double4 scv = CV && live ? sLoe.com[h1s] : z4;
 
     double3 loNext = make_double3(0.0, 0.0, 0.0), loeNext = make_double3(0.0, 0.0, 0.0);
     if (look) {
@@ -922,6 +929,44 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const bool agg = (a.dbg & 16) != 0; /* warp aggregation measured slower on config 2 */
     const PendSink ps{a.pend, a.pend_count, a.pend_cap};
 
+    if (CV && live) {
+        /* ---- fused CV lookup (estimators.cpp:453-462; k_cv_lookup semantics): the Lo\E query
+         * at (position, wo, footprint) on the frame-start table.  Its first level's key is the
+         * Lo key, whose Lo\E probe r1 is already settled ---- */
+        double3 cv = make_double3(0.0, 0.0, 0.0);
+        bool ok = false;
+        if (r1 >= 0) {
+            const double4 c = r1 == (int)h1s ? scv : sLoe.com[r1];
+            ok = c.w > 0.0;
+            if (ok) cv = make_double3(c.x, c.y, c.z);
+        }
+        for (int l = level + 1; !ok && l <= kp.max_level; ++l) {
+            const double px = S.f(PS_POS), py = S.f(PS_POS + 1), pz = S.f(PS_POS + 2);
+            const PosQ q = pos_q(fq, px, py, pz);
+            int lx = 0;
+            int32_t a0 = cell_try(q.q[0], px, l, &lx), a1 = cell_try(q.q[1], py, l, &lx),
+                    a2 = cell_try(q.q[2], pz, l, &lx);
+            if (lx) {
+                a0 = cell_exact(kp, px, l);
+                a1 = cell_exact(kp, py, l);
+                a2 = cell_exact(kp, pz, l);
+            }
+            const uint64_t pk =
+                pack_key_fields(l, a0, a1, a2, dir_cell_f8(fo.u, l), dir_cell_f8(fo.v, l));
+            const int idx = probe_find(sLoe, (uint32_t)pk & sLoe.mask, checksum_of(pk));
+            if (idx >= 0) {
+                const double4 c = sLoe.com[idx];
+                ok = c.w > 0.0;
+                if (ok) cv = make_double3(c.x, c.y, c.z);
+            }
+        }
+        const uint64_t i = S.index();
+        a.cv[0][i] = cv.x;
+        a.cv[1][i] = cv.y;
+        a.cv[2][i] = cv.z;
+        a.cv_valid[i] = ok ? 1 : 0;
+    }
+
     /* ---- update values (field.cpp:13-25 evaluation order), each built from the staged inputs
      * just before its contribution; one rolled loop over the five contributions keeps a single
      * copy of the probe/RED/pending code in the instruction stream ---- */
@@ -992,7 +1037,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     pipe.values_done();
 }
 
-template <int STAGES, int MINB, bool TMAP>
+template <int STAGES, int MINB, bool TMAP, bool CV = false>
 __global__ void __launch_bounds__(VT, MINB)
     k_vertex_pass_tiled(VPArgs2 a, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1037,7 +1082,7 @@ __global__ void __launch_bounds__(VT, MINB)
             for (int k = 0; k < PS_NUM_F64; ++k) stages[s].f[k][tid] = live ? a.fld[k][v] : 0.0;
             stages[s].flags[tid] = live ? a.flags[v] : 0u;
         }
-        SmemSrc src{&stages[s], tid};
+        SmemSrc src{&stages[s], tid, tile * VT + tid};
         const uint64_t nt = tile + (uint64_t)STAGES * gridDim.x;
         const auto issue_next = [&]() {
             if (nt < nfull) {
@@ -1055,7 +1100,7 @@ __global__ void __launch_bounds__(VT, MINB)
         if (a.dbg & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body(a, src, live, sm);
+            vertex_body<CV>(a, src, live, sm);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
@@ -2792,9 +2837,15 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
     return PSTF_OK;
 }
 
+struct CvOut { /* fused CV-lookup outputs (pstf_vertex_pass_cv) */
+    double *r, *g, *b;
+    uint8_t *valid;
+};
+
 static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
                          const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
-                         uint32_t fli_mask, int mode, cudaStream_t st) {
+                         uint32_t fli_mask, int mode, cudaStream_t st,
+                         const CvOut *cv = nullptr) {
     VPArgs a;
     memset(&a, 0, sizeof(a));
     pstf_field *fs[4] = {lo, loe, fli, li};
@@ -2871,22 +2922,44 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
         const size_t smem = stages * sizeof(TileStage) + 64;
-        const int fi = cfg == 0 ? 0 : cfg == 2 ? 1 : tmap ? 3 : 2;
-        static bool attr[4] = {false, false, false, false};
+        const bool cvf = cv && cfg == 1; /* the CV lookup fused into the default kernel */
+        if (cv && !cvf)
+            LAUNCH(k_cv_lookup, grid_for(n, 256), 256, 0, st, loe->d, *v, n, cv->r, cv->g, cv->b,
+                   cv->valid);
+        if (cvf) {
+            b.cv[0] = cv->r;
+            b.cv[1] = cv->g;
+            b.cv[2] = cv->b;
+            b.cv_valid = cv->valid;
+        }
+        const int fi = cfg == 0 ? 0 : cfg == 2 ? 1 : (tmap ? 3 : 2) + (cvf ? 2 : 0);
+        static bool attr[6] = {false, false, false, false, false, false};
         if (!attr[fi]) {
-            const void *fn = fi == 0 ? (const void *)k_vertex_pass_tiled<2, 3, false>
-                           : fi == 1 ? (const void *)k_vertex_pass_tiled<1, 5, false>
-                           : fi == 2 ? (const void *)k_vertex_pass_tiled<1, VT_MINB, false>
-                                     : (const void *)k_vertex_pass_tiled<1, VT_MINB, true>;
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const void *fns[6] = {(const void *)k_vertex_pass_tiled<2, 3, false>,
+                                  (const void *)k_vertex_pass_tiled<1, 5, false>,
+                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, false>,
+                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, true>,
+                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, false, true>,
+                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, true, true>};
+            CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
             attr[fi] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
-        if (fi == 0) LAUNCH((k_vertex_pass_tiled<2, 3, false>), grid, VT, smem, st, b, tm);
-        else if (fi == 1) LAUNCH((k_vertex_pass_tiled<1, 5, false>), grid, VT, smem, st, b, tm);
-        else if (fi == 2) LAUNCH((k_vertex_pass_tiled<1, VT_MINB, false>), grid, VT, smem, st, b, tm);
-        else LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true>), grid, VT, smem, st, b, tm);
-    } else if (mode == PSTF_MODE_ATOMIC)
+        switch (fi) {
+        case 0: LAUNCH((k_vertex_pass_tiled<2, 3, false>), grid, VT, smem, st, b, tm); break;
+        case 1: LAUNCH((k_vertex_pass_tiled<1, 5, false>), grid, VT, smem, st, b, tm); break;
+        case 2: LAUNCH((k_vertex_pass_tiled<1, 4, false>), grid, VT, smem, st, b, tm); break;
+        case 3: LAUNCH((k_vertex_pass_tiled<1, 4, true>), grid, VT, smem, st, b, tm); break;
+        case 4: LAUNCH((k_vertex_pass_tiled<1, 4, false, true>), grid, VT, smem, st, b, tm); break;
+        default: LAUNCH((k_vertex_pass_tiled<1, 4, true, true>), grid, VT, smem, st, b, tm);
+        }
+        return PSTF_OK;
+    }
+    if (cv)
+        LAUNCH(k_cv_lookup, grid_for(n, 256), 256, 0, st, loe->d, *v, n, cv->r, cv->g, cv->b,
+               cv->valid);
+    if (mode == PSTF_MODE_ATOMIC)
         LAUNCH(k_vertex_pass<PSTF_MODE_ATOMIC>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
     else
         LAUNCH(k_vertex_pass<PSTF_MODE_ORDERED>, grid_for(n, VP_BLOCK), VP_BLOCK, 0, st, a);
@@ -2918,6 +2991,28 @@ int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_fiel
     if (rc) return rc;
     if (n) {
         rc = vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, mode, st);
+        if (rc) return rc;
+    }
+    pstf_field *fs[4] = {lo, loe, fli, li};
+    return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
+}
+
+int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
+                        const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
+                        uint32_t fli_mask, int mode, double *cv_r, double *cv_g, double *cv_b,
+                        uint8_t *cv_valid, void *stream) {
+    int rc = vertex_checks(lo, loe, fli, li, mode);
+    if (rc) return rc;
+    if (!v) return set_err(PSTF_E_INVALID, "NULL vertex record");
+    if (n && (!cv_r || !cv_g || !cv_b || !cv_valid))
+        return set_err(PSTF_E_INVALID, "CV outputs required");
+    CK(cudaSetDevice(lo->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
+    if (rc) return rc;
+    if (n) {
+        const CvOut cv{cv_r, cv_g, cv_b, cv_valid};
+        rc = vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, mode, st, &cv);
         if (rc) return rc;
     }
     pstf_field *fs[4] = {lo, loe, fli, li};

@@ -105,6 +105,8 @@ def lib():
         "pstf_field_slots": ([vp, u64, u64, vp], i32),
         "pstf_vertex_pass": ([vp, vp, vp, vp, vp, u64, u32, u32, i32, vp], i32),
         "pstf_vertex_pass_host": ([vp, vp, vp, vp, vp, u64, u32, u32, i32, vp], i32),
+        "pstf_vertex_pass_cv": ([vp, vp, vp, vp, vp, u64, u32, u32, i32, vp, vp, vp, vp, vp],
+                                i32),
         "pstf_cv_lookup": ([vp, vp, u64, vp, vp, vp, vp, vp], i32),
         "pstf_synth_generate": ([i32, i32, i32, u64, u64, d, vp, vp], i32),
         "pstf_synth_generate_stripe": ([i32, i32, i32, u64, u64, d, u64, u64, vp, vp], i32),
@@ -587,6 +589,26 @@ def vertex_pass_host(lo, loe, fli, li, host_buf: np.ndarray, n, loe_mask=TECH_AL
     v = vertex_soa(p, n)
     _check(lib().pstf_vertex_pass_host(lo._h, loe._h, fli._h, li._h if li is not None else None,
                                        C.byref(v), n, loe_mask, fli_mask, mode, _stream()))
+
+
+def vertex_pass_cv(lo, loe, fli, li, buf, n, loe_mask=TECH_ALL, fli_mask=TECH_ALL,
+                   mode=MODE_ATOMIC, out=None, soa=None):
+    """vertex_pass plus the CV lookup of every vertex on the frame-start table, fused into the
+    vertex kernel (== cv_lookup before vertex_pass) -> (value (3,n), valid (n,) uint8).
+    out: optional preallocated (value, valid) pair."""
+    t = _torch()
+    for s in (lo, loe, fli, li):
+        if s is not None:
+            s.flush()
+    v = soa if soa is not None else vertex_soa(buf, n)
+    if out is None:
+        dev = buf.device if buf is not None else "cuda"
+        out = (t.empty((3, n), dtype=t.float64, device=dev), t.empty(n, dtype=t.uint8, device=dev))
+    val, ok = out
+    _check(lib().pstf_vertex_pass_cv(lo._h, loe._h, fli._h, li._h if li is not None else None,
+                                     C.byref(v), n, loe_mask, fli_mask, mode, _ptr(val[0]),
+                                     _ptr(val[1]), _ptr(val[2]), _ptr(ok), _stream()))
+    return val, ok
 
 
 def cv_lookup(loe, buf, n):

@@ -48,6 +48,9 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic-json")
     ap.add_argument("--title", default="ncu summary")
+    ap.add_argument("--skip-steps", type=int, default=0,
+                    help="launch list: drop everything before the (N+1)-th vertex-pass launch "
+                         "(the bench's warm-up steps) and the input generator k_synth")
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
     traffic = {}
@@ -83,7 +86,12 @@ def main():
         ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
         tot = collections.defaultdict(float)
         cnt = collections.Counter()
+        seen_vp = 0
         for r in rows[1:]:
+            if "k_vertex_pass" in r[ik]:
+                seen_vp += 1
+            if seen_vp <= a.skip_steps or r[ik].startswith("k_synth"):
+                continue
             v = float(r[iv].replace(",", ""))
             v = v / 1e3 if r[iu] == "ns" else (v if r[iu] == "us" else v * 1e3)
             name = r[ik].split("(")[0]
@@ -91,7 +99,9 @@ def main():
             cnt[name] += 1
         allt = sum(tot.values())
         lines += ["## Launch list (`ncu --metrics gpu__time_duration.sum`, serialised, cold-cache)",
-                  "", "| kernel | launches | total us | share |", "|---|---|---|---|"]
+                  "", f"Timed steps only (first {a.skip_steps} vertex-pass steps and the input "
+                  "generator dropped).", "",
+                  "| kernel | launches | total us | share |", "|---|---|---|---|"]
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / allt:.1f}% |")
         lines.append("")

@@ -278,6 +278,32 @@ def test_vertex_pass_field_layouts():
                 assert a.stats()[k] == b.stats()[k] == c.stats()[k]
 
 
+@pytest.mark.parametrize("mode", ["atomic", "ordered"])
+def test_vertex_pass_cv_fused(mode):
+    """pstf_vertex_pass_cv == pstf_cv_lookup on the frame-start table (bitwise) followed by
+    pstf_vertex_pass (same stores afterwards), on both the fused tiled kernel (ATOMIC) and the
+    separate-kernel path (ORDERED)."""
+    gm = pb.MODE_ATOMIC if mode == "atomic" else pb.MODE_ORDERED
+    _, g1 = _vertex_stores(14, inputs.BASE_CORNELL * 6.0, li=True, evict=2)
+    _, g2 = _vertex_stores(14, inputs.BASE_CORNELL * 6.0, li=True, evict=2)
+    for it in range(4):
+        buf, n = pb.synth_generate(128, 72, 4, iteration=it % 2)
+        ref_val, ref_ok = pb.cv_lookup(g2[1], buf, n)  # read-only: the frame-start table
+        pb.vertex_pass(*g1, buf, n, mode=gm)
+        val, ok = pb.vertex_pass_cv(*g2, buf, n, mode=gm)
+        np.testing.assert_array_equal(ok.cpu().numpy().astype(bool), ref_ok.cpu().numpy())
+        np.testing.assert_array_equal(gu.bits(val.cpu().numpy()), gu.bits(ref_val.cpu().numpy()))
+        if it:
+            assert ok.cpu().numpy().mean() > 0.3
+        for a, b in zip(g1, g2):
+            a.end_frame()
+            b.end_frame()
+            if mode == "ordered":
+                gu.assert_slots_bitwise(a.slots(), b.slots())
+            else:
+                gu.assert_slots_close(a.slots(), b.slots(), rtol=1e-9)
+
+
 def test_vertex_pass_matches_reference_replay():
     """Against the reference FieldStore itself (EstimatorRun deterministic-mode replay)."""
     if not po.ref_available():
