@@ -301,6 +301,8 @@ def run_b200(args):
     if dist:
         dist.barrier()
     touched0 = sum(s.stats()["touched_total"] for s in stores)
+    reds0 = stores[0].stats()["reds_total"]
+    dropped0 = [s.stats()["dropped"] for s in stores]
     launches0 = pb.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pb.profile_collect()
@@ -348,6 +350,11 @@ def run_b200(args):
     vp_bytes = BYTES_PER_VERTEX * n + cv_bytes  # the CV outputs are written by the fused kernel
     ach = vp_bytes / (vp_avg / 1e3) / 1e9
     mean_touched = (sum(s["touched_total"] for s in st) - touched0) / args.steps
+    # atomic roofline: fp64 RED element updates the fused kernel issued (after the
+    # per-vertex aggregation) over its time, against this GPU's measured RED peak
+    reds_step = (st[0]["reds_total"] - reds0) / args.steps
+    red_peak = pb.red_peak(local)
+    red_ach = reds_step / (vp_avg / 1e3) if reds_step else 0.0
     step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched + cv_bytes
     step_ach = step_bytes / (ms_step / 1e3) / 1e9
     traffic = None
@@ -391,12 +398,26 @@ def run_b200(args):
         "step_roofline": {"achieved": step_ach, "peak": peak, "unit": "GB/s",
                           "frac": step_ach / peak,
                           "bytes_per_step": step_bytes, "touched_cells_per_step": mean_touched},
+        "atomic_roofline": {"bound": "l2_atomic", "achieved": red_ach / 1e9,
+                            "peak": red_peak / 1e9, "unit": "Gop/s (fp64 RED elements)",
+                            "frac": red_ach / red_peak if red_peak else None,
+                            "reds_per_vertex": reds_step / n,
+                            "peak_source": "pstf_diag_red_peak: 8 distinct L2-resident 32 B "
+                                           "cells x 4 components per warp instruction"},
         "kernels": kernels,
         "field_stats": {k: [s[k] for s in st] for k in ("live", "dropped", "rejected",
                                                          "new_keys_last", "touched_last",
                                                          "placement_rounds_last")},
         "clocks": clk.summary(),
     }
+    if drift:  # config 5 (probe-length stress): probe distances, drops and evictions
+        line["probe_stress"] = {
+            "probe_hist_lo_loe_fli": [s.probe_histogram().tolist() for s in stores],
+            "dropped_per_iteration": [(s["dropped"] - d0) / args.steps
+                                      for s, d0 in zip(st, dropped0)],
+            "evicted_last": [s["evicted_last"] for s in st],
+            "load_factor": [s["live"] / float(1 << args.capacity_log2) for s in st],
+        }
 
     # e2e: same metric through the C ABI with pinned HOST vertex arrays (H2D every step)
     if not args.no_e2e:

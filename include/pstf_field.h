@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PSTF_ABI_VERSION 1
+#define PSTF_ABI_VERSION 2
 
 enum {
     PSTF_OK = 0,
@@ -106,6 +106,8 @@ typedef struct pstf_field_stats {
     uint64_t evicted_last;    /* slots evicted by the last endFrame */
     uint64_t placement_rounds_last; /* deterministic-placement rounds of the last pass */
     uint64_t touched_total;   /* touched slots summed over all committed frames */
+    uint64_t reds_total;      /* fp64 RED element updates issued by fused (ATOMIC, tiled) vertex
+                               * passes in which this store was the Lo store, all stores summed */
 } pstf_field_stats;
 
 /* Three coordinate arrays of one fp64 vector field (device pointers) */
@@ -227,6 +229,16 @@ int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_f
                         const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
                         uint32_t fli_mask, int mode, double *cv_r, double *cv_g, double *cv_b,
                         uint8_t *cv_valid, void *stream);
+
+/* Probe-distance histogram of the live slots: hist[d] = number of live slots at distance d =
+ * (slot - home) & mask from their key's home slot, d >= 32 counted in hist[32] (SURVEY.md
+ * 8(b) stats probe_hist[33]; config 5 reports it per iteration).  Reads the device table. */
+int pstf_field_probe_histogram(pstf_field *f, uint64_t hist[33]);
+
+/* Diagnostic: sustained fp64 RED throughput of this GPU (element updates per second) for the
+ * vertex pass's access pattern (each warp instruction = 8 distinct 32 B cells x 4 components)
+ * on distinct L2-resident addresses: the atomic roofline's peak. */
+int pstf_diag_red_peak(int device, double *ops_per_second);
 
 /* CV / guiding lookup at the current vertex (estimators.cpp:438-462): out = Lo\E query at
  * (position, wo, footprint) for every vertex of the record (config 3 "CV lookup"). */

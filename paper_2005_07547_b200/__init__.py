@@ -12,6 +12,6 @@ from .field import (  # noqa: F401
     FieldStore, FieldStoreConfig, FieldUpdateQueue, PstfError, SpatioDirectionalKey,
     SNAPSHOT_DTYPE, SLOT_DTYPE, KEY_DTYPE, lib, library_path, read_snapshot, synth_generate,
     vertex_pass, vertex_pass_host, vertex_pass_cv, cv_lookup, vertex_soa, vertex_soa_from_fields,
-    kernel_launch_count,
+    kernel_launch_count, red_peak,
     VERTEX_BYTES, VERTEX_F64_FIELDS, profile_enable, profile_collect, end_frame_all,
 )

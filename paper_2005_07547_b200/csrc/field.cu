@@ -328,7 +328,8 @@ template <class Store>
 __device__ __forceinline__ void apply_contribution(const Store &s, const PendSink &a,
                                                    double4 *sm, int sid, const Key &k, double4 v,
                                                    uint32_t ncalls, int res, uint32_t mark,
-                                                   bool do_red = true, bool aggregate = true) {
+                                                   bool do_red = true, bool aggregate = true,
+                                                   uint32_t *nred = nullptr) {
     unsigned lane = lane_id();
     unsigned long long gk = res >= 0 ? (((unsigned long long)sid << 32) | (unsigned)res)
                                      : (0xffffffff00000000ull | lane);
@@ -348,7 +349,10 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
             const int cell = 8 * k + (lane >> 2);
             const int rs = rsm[cell];
             const double val = flat[4 * cell + comp];
-            if (rs >= 0 && val != 0.0) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+            if (rs >= 0 && val != 0.0) {
+                atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+                if (nred) ++*nred;
+            }
         }
         __syncwarp();
         if (res >= 0) touch_slot(s, (uint32_t)res, mark);
@@ -778,7 +782,8 @@ struct NoPipe {
 
 template <bool CV, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
-                                            double4 *sm, const Pipe &pipe = Pipe()) {
+                                            double4 *sm, uint32_t &nred,
+                                            const Pipe &pipe = Pipe()) {
     const DevStore &sLo = a.st.s[0];
     const DevStore &sLoe = a.st.s[1];
     const DevStore &sFli = a.st.s[2];
@@ -1032,7 +1037,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
         const int res = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : c == 3 ? r3 : r4;
         const uint32_t mark = c == 0 ? k0 : c == 1 ? k1 : c == 2 ? k2 : c == 3 ? k3 : k4;
-        apply_contribution(s, ps, sm, sid, k, v, nc, res, mark, red, agg);
+        apply_contribution(s, ps, sm, sid, k, v, nc, res, mark, red, agg, &nred);
     }
     pipe.values_done();
 }
@@ -1067,7 +1072,7 @@ __global__ void __launch_bounds__(VT, MINB)
                     else prefetch_tile(a, t + (uint64_t)d * gridDim.x);
                 }
         }
-    uint32_t it = 0;
+    uint32_t it = 0, nred = 0;
     const uint64_t ntiles = (a.n + VT - 1) / VT;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = (int)(it % STAGES);
@@ -1100,11 +1105,14 @@ __global__ void __launch_bounds__(VT, MINB)
         if (a.dbg & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body<CV>(a, src, live, sm);
+            vertex_body<CV>(a, src, live, sm, nred);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
     }
+    /* RED element updates issued (atomic-roofline accounting, one atomic per warp) */
+    for (int o = 16; o; o >>= 1) nred += __shfl_xor_sync(0xffffffffu, nred, o);
+    if ((tid & 31) == 0 && nred) atomicAdd(&a.st.s[0].ctr[C_REDS], (unsigned long long)nred);
 }
 
 /* CV lookup at the current vertex (estimators.cpp:453-462) */
@@ -2672,6 +2680,77 @@ int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out) {
     out->evicted_last = c[C_EVICTED];
     out->placement_rounds_last = f->rounds_last;
     out->touched_total = c[C_TOUCHED_TOTAL];
+    out->reds_total = c[C_REDS];
+    return PSTF_OK;
+}
+
+__global__ void k_probe_hist(DevStore s, unsigned long long *hist) {
+    __shared__ unsigned h[33];
+    for (int i = threadIdx.x; i < 33; i += blockDim.x) h[i] = 0u;
+    __syncthreads();
+    const uint64_t cap = (uint64_t)s.mask + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (s.meta[i].x == 0u) continue;
+        const KeyFields k = s.keyf[i];
+        const uint32_t home = (uint32_t)pack_key_fields(k.level, k.c0, k.c1, k.c2, k.d0, k.d1) &
+                              s.mask;
+        const uint32_t d = ((uint32_t)i - home) & s.mask;
+        atomicAdd(&h[d < 32u ? d : 32u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 33; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+int pstf_field_probe_histogram(pstf_field *f, uint64_t hist[33]) {
+    if (!f || !hist) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    Scratch &sc = f->sc;
+    ENSURE(sc.ranges, 33 * 8);
+    CK(cudaMemset(sc.ranges.p, 0, 33 * 8));
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    unsigned g = std::min<unsigned>(grid_for(cap, 256), (unsigned)sm_count() * 8);
+    LAUNCH(k_probe_hist, g, 256, 0, (cudaStream_t)0, f->d, sc.ranges.as<unsigned long long>());
+    CK(cudaMemcpy(hist, sc.ranges.p, 33 * 8, cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
+/* RED peak: lane -> cell 8k + lane/4 (k = instruction), component lane%4, cells spread over an
+ * L2-resident array so the updates of one instruction hit 8 distinct sectors */
+__global__ void k_red_peak(double4 *cells, uint32_t mask, int iters) {
+    const unsigned lane = threadIdx.x & 31u;
+    uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        h = h * 1664525u + 1013904223u; /* per-warp LCG: warp-uniform */
+        const uint32_t cell = ((h >> 8) * 8u + (lane >> 2)) & mask;
+        atomicAdd(reinterpret_cast<double *>(&cells[cell]) + (lane & 3u), 1.0);
+    }
+}
+
+int pstf_diag_red_peak(int device, double *ops_per_second) {
+    if (!ops_per_second) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(device));
+    const uint32_t ncell = 1u << 21; /* 64 MiB of double4: L2-resident (126 MB L2) */
+    double4 *cells = nullptr;
+    CK(cudaMalloc(&cells, (size_t)ncell * sizeof(double4)));
+    CK(cudaMemset(cells, 0, (size_t)ncell * sizeof(double4)));
+    const unsigned grid = (unsigned)sm_count() * 8, block = 256;
+    const int iters = 256;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_red_peak<<<grid, block>>>(cells, ncell - 1, iters); /* warm-up */
+    CK(cudaEventRecord(e0));
+    for (int r = 0; r < 4; ++r) k_red_peak<<<grid, block>>>(cells, ncell - 1, iters);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ops_per_second = 4.0 * grid * block * (double)iters / (ms * 1e-3);
+    CK(cudaEventDestroy(e0));
+    CK(cudaEventDestroy(e1));
+    CK(cudaFree(cells));
     return PSTF_OK;
 }
 

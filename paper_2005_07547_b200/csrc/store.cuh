@@ -38,6 +38,7 @@ enum Ctr : int {
     C_LIVE_SNAP,    // endFrame: live count before eviction (field.cpp:205-212)
     C_TOUCHED_LAST, // touched slots of the last committed frame
     C_TOUCHED_TOTAL, // touched slots summed over all committed frames
+    C_REDS,          // fp64 RED element updates issued by fused vertex passes (Lo store)
     C_NUM
 };
 

@@ -51,7 +51,7 @@ class _Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("frame", "rejected", "dropped", "internal_errors",
                                           "live", "touched_last", "new_keys_last",
                                           "evicted_last", "placement_rounds_last",
-                                          "touched_total")]
+                                          "touched_total", "reds_total")]
 
 
 class _Vec3(C.Structure):
@@ -112,6 +112,8 @@ def lib():
         "pstf_synth_generate_stripe": ([i32, i32, i32, u64, u64, d, u64, u64, vp, vp], i32),
         "pstf_vertex_soa_from_buffer": ([vp, u64, vp], None),
         "pstf_profile_enable": ([i32], i32),
+        "pstf_field_probe_histogram": ([vp, vp], i32),
+        "pstf_diag_red_peak": ([i32, vp], i32),
         "pstf_profile_collect": ([vp, vp, vp, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
@@ -125,6 +127,13 @@ def lib():
 def _check(rc):
     if rc != 0:
         raise PstfError(f"pstf error {rc}: {lib().pstf_last_error().decode()}")
+
+
+def red_peak(device: int = 0) -> float:
+    """Measured fp64 RED element updates/s (the vertex pass's pattern, L2-resident)."""
+    out = C.c_double()
+    _check(lib().pstf_diag_red_peak(device, C.byref(out)))
+    return out.value
 
 
 def kernel_launch_count() -> int:
@@ -407,6 +416,13 @@ class FieldStore:
 
     def liveCellCount(self):
         return self.stats()["live"]
+
+    def probe_histogram(self) -> np.ndarray:
+        """hist[d] = live slots at probe distance d from their home slot (d >= 32 in [32])."""
+        self.flush()
+        h = np.zeros(33, np.uint64)
+        _check(lib().pstf_field_probe_histogram(self._h, h.ctypes.data_as(C.c_void_p)))
+        return h
 
     def weightedMeanValue(self):
         self.flush()

@@ -46,7 +46,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.pstf_abi_version() == 1
+    assert lib.pstf_abi_version() == 2
 
 
 def test_library_is_sm100a_only(lib):

@@ -304,6 +304,45 @@ def test_vertex_pass_cv_fused(mode):
                 gu.assert_slots_close(a.slots(), b.slots(), rtol=1e-9)
 
 
+def test_probe_histogram_vs_oracle_slots():
+    """pstf_field_probe_histogram == the distances of the oracle's live slots from their homes
+    (home = packKeyFields(key) & mask, field.cpp:104), on a crowded table with drops."""
+    from shard_cpu_backend import pack
+    o, g = _vertex_stores(12, inputs.BASE_CORNELL * 2.0, li=False, evict=64)
+    for it in range(3):
+        buf, n = pb.synth_generate(96, 54, 4, iteration=it)
+        pb.vertex_pass(*g, buf, n, mode=pb.MODE_ATOMIC)
+        po.vertex_pass_oracle(*o, buf.cpu().numpy(), n, deterministic=True)
+        for a, b in zip(g[:3], o[:3]):
+            a.end_frame()
+            b.end_frame()
+    for a, b in zip(g[:3], o[:3]):
+        sl = b.slots()
+        mask = len(sl) - 1
+        want = np.zeros(33, np.uint64)
+        for i in np.nonzero(sl["checksum"])[0]:
+            k = (int(sl["level"][i]), *[int(c) for c in sl["cell"][i]], *[int(d) for d in sl["dir"][i]])
+            d = (int(i) - (pack(k) & mask)) & mask
+            want[min(d, 32)] += 1
+        got = a.probe_histogram()
+        np.testing.assert_array_equal(got, want)
+        assert got.sum() == a.stats()["live"]
+    assert any(a.probe_histogram()[1:].sum() > 0 for a in g[:3])  # collisions exercised
+
+
+def test_red_counter_and_peak():
+    """The fused kernel's RED accounting is positive and below the unaggregated bound, and the
+    RED peak diagnostic returns a plausible rate."""
+    _, g = _vertex_stores(16, inputs.BASE_CORNELL, li=False)
+    buf, n = pb.synth_generate(128, 72, 4, iteration=0)
+    pb.vertex_pass(*g, buf, n, mode=pb.MODE_ATOMIC)
+    pb.vertex_pass(*g, buf, n, mode=pb.MODE_ATOMIC)
+    reds = g[0].stats()["reds_total"]
+    assert 0 < reds <= 2 * n * 4 * 4
+    peak = pb.red_peak(0)
+    assert 1e9 < peak < 1e13
+
+
 def test_vertex_pass_matches_reference_replay():
     """Against the reference FieldStore itself (EstimatorRun deterministic-mode replay)."""
     if not po.ref_available():
