@@ -31,7 +31,9 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
+namespace cg = cooperative_groups;
 
 #include "../../include/pstf_field.h"
 #include "kernels.cuh"
@@ -1422,55 +1424,104 @@ struct PlaceArgs {
     int parity;                 // which hold array is "prev"
 };
 
-__global__ void k_place_round(PlaceArgs a, const unsigned long long *res_prev,
-                              unsigned long long *res_next, int *changed) {
-    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (u >= a.nu) return;
+/* One key's step of a placement round (deferred acceptance over the frame-start table): the
+ * first equal-checksum resident (FIXED), else the first slot held by a higher-priority key with
+ * an equal checksum (MERGE), else the first free slot not held by a higher-priority key
+ * (PROPOSE), else DROP.  The window's home words are loaded 8 at a time (independent loads:
+ * one round trip per 8 probes on crowded tables). */
+__device__ __forceinline__ unsigned long long place_step(const PlaceArgs &a, uint64_t u,
+                                                         int parity) {
     const DevStore &s = a.st.s[a.usid[u]];
-    const uint32_t *hold_prev = a.parity ? s.hold1 : s.hold0;
-    uint32_t *hold_next = a.parity ? s.hold0 : s.hold1;
+    const uint32_t *hold_prev = parity ? s.hold1 : s.hold0;
     const uint32_t r = a.rank ? a.rank[u] : (uint32_t)u;
     const uint32_t cs = a.ucs[u];
     const uint32_t home = a.uhome[u];
-    unsigned long long res = PSTF_RES(R_DROP, 0);
-    for (uint32_t i = 0; i < s.window; ++i) {
-        uint32_t idx = (home + i) & s.mask;
-        uint32_t c = s.meta[idx].x;
-        if (c != 0) {
-            if (c == cs) { /* an older resident with this checksum (field.cpp:122) */
-                res = PSTF_RES(R_FIXED, idx);
-                break;
+    for (uint32_t i0 = 0; i0 < s.window; i0 += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            c[j] = i0 + j < s.window ? s.meta[(home + i0 + j) & s.mask].x : 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (i0 + j >= s.window) return PSTF_RES(R_DROP, 0);
+            const uint32_t idx = (home + i0 + j) & s.mask;
+            if (c[j] != 0) {
+                if (c[j] == cs) return PSTF_RES(R_FIXED, idx); /* older resident (field.cpp:122) */
+                continue;
             }
-            continue;
-        }
-        uint32_t h = hold_prev[idx];
-        if (h < r) {
-            if (a.cs_by_rank[h] == cs) { /* a higher-priority new key with equal checksum */
-                res = PSTF_RES(R_MERGE, idx);
-                break;
+            const uint32_t h = hold_prev[idx];
+            if (h < r) {
+                if (a.cs_by_rank[h] == cs) return PSTF_RES(R_MERGE, idx); /* higher-priority twin */
+                continue;
             }
-            continue;
+            return PSTF_RES(R_PROPOSE, idx);
         }
-        res = PSTF_RES(R_PROPOSE, idx);
-        break;
     }
-    if (PSTF_RES_T(res) == R_PROPOSE) atomicMin(&hold_next[PSTF_RES_SLOT(res)], r);
-    res_next[u] = res;
-    if (res != res_prev[u]) *changed = 1;
+    return PSTF_RES(R_DROP, 0);
 }
 
-/* reset the previous round's proposals in hold_prev (so it is all-empty for reuse) */
-__global__ void k_place_clear(PlaceArgs a, const unsigned long long *res_prev) {
-    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (u >= a.nu) return;
-    unsigned long long r = res_prev[u];
-    if (PSTF_RES_T(r) != R_PROPOSE) return;
-    const DevStore &s = a.st.s[a.usid[u]];
-    uint32_t *hold_prev = a.parity ? s.hold1 : s.hold0;
-    hold_prev[PSTF_RES_SLOT(r)] = PSTF_HOLD_NONE;
+__device__ __forceinline__ uint32_t *hold_array(const DevStore &s, int which) {
+    return which ? s.hold1 : s.hold0;
 }
 
-/* commit placement: owners write the slot; everyone adds its sums (ATOMIC) and touches */
+/* All placement rounds in one cooperative launch (grid-wide barriers instead of host round
+ * trips): round k reads hold[parity_k] and res[k&1], proposes into hold[parity_k^1] and writes
+ * res[(k+1)&1]; then the previous round's proposals are cleared from hold[parity_k].  Stops at
+ * the fixpoint (no result changed).  Epilogue: the final results land in r0, the last round's
+ * proposals are cleared, and every store of the batch records the round count. */
+__global__ void __launch_bounds__(256) k_place_loop(PlaceArgs a, unsigned long long *r0,
+                                                    unsigned long long *r1, int *ctl,
+                                                    uint32_t max_rounds) {
+    cg::grid_group g = cg::this_grid();
+    const uint64_t tid0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    int parity = a.parity;
+    unsigned long long *prev = r0, *next = r1;
+    uint32_t k = 0;
+    for (;; ++k) {
+        bool changed = false;
+        for (uint64_t u = tid0; u < a.nu; u += stride) {
+            const unsigned long long res = place_step(a, u, parity);
+            if (PSTF_RES_T(res) == R_PROPOSE)
+                atomicMin(&hold_array(a.st.s[a.usid[u]], parity ^ 1)[PSTF_RES_SLOT(res)],
+                          a.rank ? a.rank[u] : (uint32_t)u);
+            next[u] = res;
+            changed |= res != prev[u];
+        }
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(&ctl[k & 1], 1);
+        g.sync();
+        for (uint64_t u = tid0; u < a.nu; u += stride) { /* clear the previous round's holds */
+            const unsigned long long res = prev[u];
+            if (PSTF_RES_T(res) == R_PROPOSE)
+                hold_array(a.st.s[a.usid[u]], parity)[PSTF_RES_SLOT(res)] = PSTF_HOLD_NONE;
+        }
+        const int ch = *(volatile int *)&ctl[k & 1];
+        g.sync(); /* everyone has read the flag before it is reset for round k + 2 */
+        if (tid0 == 0) ctl[k & 1] = 0;
+        unsigned long long *t = prev;
+        prev = next;
+        next = t;
+        parity ^= 1;
+        if (!ch) break;
+        if (k + 1 > max_rounds) {
+            if (tid0 == 0) ctl[3] = 1;
+            break;
+        }
+    }
+    /* prev = the last round's results; its proposals sit in hold[parity ^ 1] */
+    for (uint64_t u = tid0; u < a.nu; u += stride) {
+        const unsigned long long res = prev[u];
+        if (prev != r0) r0[u] = res;
+        if (PSTF_RES_T(res) == R_PROPOSE)
+            hold_array(a.st.s[a.usid[u]], parity ^ 1)[PSTF_RES_SLOT(res)] = PSTF_HOLD_NONE;
+    }
+    if (tid0 == 0) {
+        ctl[2] = (int)(k + 1);
+        for (int i = 0; i < 4; ++i)
+            if (a.st.s[i].ctr) a.st.s[i].ctr[C_ROUNDS] = k + 1;
+    }
+}
+
 __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFields *ukey,
                          const uint32_t *ucalls, const double4 *usum, int atomic_mode) {
     uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -1483,9 +1534,7 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
         return;
     }
     if (t == R_PROPOSE) {
-        uint32_t *hold_cur = a.parity ? s.hold0 : s.hold1; /* the array the last round wrote */
-        hold_cur[slot] = PSTF_HOLD_NONE;
-        s.meta[slot].x = a.ucs[u];
+        s.meta[slot].x = a.ucs[u]; /* (k_place_loop has released the slot's hold) */
         s.keyf[slot] = ukey[u];
         atomicAdd(&s.ctr[C_LIVE], 1ull);
         atomicAdd(&s.ctr[C_NEW_KEYS], 1ull);
@@ -2042,8 +2091,8 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     for (int i = 0; i < nf; ++i)
         if (fs[i]) {
             fs[i]->new_keys_last = 0;
-            fs[i]->rounds_last = 0;
             CK(cudaMemsetAsync(&fs[i]->d.ctr[C_NEW_KEYS], 0, 8, st));
+            CK(cudaMemsetAsync(&fs[i]->d.ctr[C_ROUNDS], 0, 8, st));
         }
     if (n == 0) return PSTF_OK;
     if (n > sc.pend.bytes / sizeof(PendRec))
@@ -2129,7 +2178,7 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     ENSURE(sc.usum, nu * sizeof(double4));
     ENSURE(sc.ures0, nu * 8);
     ENSURE(sc.ures1, nu * 8);
-    ENSURE(sc.changed, 4);
+    ENSURE(sc.changed, 16);
     UniqArgs U;
     U.ufirst = sc.ufirst.as<uint32_t>();
     U.ukey = sc.ukey.as<KeyFields>();
@@ -2184,34 +2233,30 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
         P.cs_by_rank = sc.csr.as<uint32_t>();
     }
 
-    /* 4. deterministic placement: Jacobi rounds to the unique fixpoint */
-    unsigned long long *rprev = sc.ures0.as<unsigned long long>(),
-                       *rnext = sc.ures1.as<unsigned long long>();
+    /* 4. deterministic placement: Jacobi rounds to the unique fixpoint, on the device */
+    unsigned long long *rprev = sc.ures0.as<unsigned long long>();
     CK(cudaMemsetAsync(rprev, 0, nu * 8, st));
-    int parity = 0;
-    uint64_t rounds = 0;
-    const uint64_t max_rounds = nu + 2;
-    for (;;) {
-        P.parity = parity;
-        CK(cudaMemsetAsync(sc.changed.p, 0, 4, st));
-        LAUNCH(k_place_round, grid_for(nu, 256), 256, 0, st, P, rprev, rnext,
-               sc.changed.as<int>());
-        LAUNCH(k_place_clear, grid_for(nu, 256), 256, 0, st, P, rprev);
-        ++rounds;
-        std::swap(rprev, rnext);
-        parity ^= 1;
-        int rc = read_small(sc, sc.changed.p, 4, st);
-        if (rc) return rc;
-        if (((int *)sc.h_small)[0] == 0) break;
-        if (rounds > max_rounds) return set_err(PSTF_E_CUDA, "placement did not converge");
+    CK(cudaMemsetAsync(sc.changed.p, 0, 16, st));
+    P.parity = 0;
+    {
+        static int blocks_per_sm = -1;
+        if (blocks_per_sm < 0) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_place_loop, 256, 0));
+            blocks_per_sm = std::max(1, std::min(blocks_per_sm, 4));
+        }
+        const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(nu, 256),
+                                                           (uint64_t)sm_count() * blocks_per_sm);
+        unsigned long long *r1 = sc.ures1.as<unsigned long long>();
+        int *ctl = sc.changed.as<int>();
+        uint32_t max_rounds = (uint32_t)std::min<uint64_t>(nu + 2, 0x7fffffffu);
+        void *args[] = {&P, &rprev, &r1, &ctl, &max_rounds};
+        ProfScope ps_("k_place_loop", st);
+        CK(cudaLaunchCooperativeKernel((const void *)k_place_loop, grid, 256, args, 0, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    /* rprev now holds the fixpoint; the last round wrote hold[parity ^ 1]... after the swap the
-     * array written last is "prev" for parity, i.e. hold[parity] (cleared in k_commit) */
-    P.parity = parity ^ 1;
+    P.parity = -1;
     LAUNCH(k_commit, grid_for(nu, 256), 256, 0, st, P, rprev, U.ukey, U.ucalls, U.usum,
            mode == PSTF_MODE_ATOMIC ? 1 : 0);
-    for (int i = 0; i < nf; ++i)
-        if (fs[i]) fs[i]->rounds_last = rounds;
 
     /* 5. ORDERED / SEQUENTIAL: sequential fold per slot */
     if (mode != PSTF_MODE_ATOMIC) {
@@ -2678,7 +2723,7 @@ int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out) {
     out->touched_last = c[C_TOUCHED_LAST];
     out->new_keys_last = c[C_NEW_KEYS];
     out->evicted_last = c[C_EVICTED];
-    out->placement_rounds_last = f->rounds_last;
+    out->placement_rounds_last = c[C_ROUNDS];
     out->touched_total = c[C_TOUCHED_TOTAL];
     out->reds_total = c[C_REDS];
     return PSTF_OK;

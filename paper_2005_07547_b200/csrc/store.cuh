@@ -39,6 +39,7 @@ enum Ctr : int {
     C_TOUCHED_LAST, // touched slots of the last committed frame
     C_TOUCHED_TOTAL, // touched slots summed over all committed frames
     C_REDS,          // fp64 RED element updates issued by fused vertex passes (Lo store)
+    C_ROUNDS,        // deterministic-placement rounds of the last update pass
     C_NUM
 };
 
