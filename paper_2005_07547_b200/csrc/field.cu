@@ -1610,126 +1610,181 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 /* Pass 1 (field.cpp:205-216) for every store of the batch: compact the touched-slot bitmap into
  * tlist (clearing it), sum c_new over those slots (untouched slots have zero accumulators by
  * construction) and snapshot `live` for the eviction rule. */
+#define PICK4(a, j) ((j) == 0 ? (a)[0] : (j) == 1 ? (a)[1] : (j) == 2 ? (a)[2] : (a)[3])
+
+/* store j of a batch with segment boundaries seg[1..3] (seg[nst..3] = the total) */
+#define SEG_OF(i, seg) (((i) >= (seg)[1]) + ((i) >= (seg)[2]) + ((i) >= (seg)[3]))
+
+/* endFrame pass 1 for every store of the batch at once: the touched bitmaps become touched lists
+ * (tbits cleared) and Σ c_new / #(c_new > 0) are reduced (field.cpp:201-214).  The stores'
+ * bitmap words form one flat index space, each store's range padded to whole warps, so a warp
+ * never straddles two stores; the c_new gathers of a word's set bits are issued 8 at a time. */
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
-    __shared__ double ssum[EF_BLOCK / 32];
-    __shared__ unsigned long long scnt[EF_BLOCK / 32];
-    for (int j = 0; j < nst; ++j) {
-        const DevStore &s = st.s[j];
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
-            s.ctr[C_EVICTED] = 0;
-        }
-        const uint64_t nwords = ((uint64_t)s.mask + 32) / 32;
-        double sum = 0.0;
-        unsigned cnt = 0;
-        const unsigned lane = lane_id();
-        /* every lane of a warp runs the same number of iterations (shuffles below) */
-        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-        const uint64_t iters = (nwords + stride - 1) / stride;
-        for (uint64_t it = 0; it < iters; ++it) {
-            const uint64_t wi = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-            uint32_t w = wi < nwords ? s.tbits[wi] : 0u;
-            if (w) s.tbits[wi] = 0u;
-            const unsigned c = __popc(w);
-            unsigned incl = c;
-            for (int o = 1; o < 32; o <<= 1) {
-                unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)lane >= o) incl += t;
-            }
-            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-            if (!total) continue;
-            unsigned long long base = 0;
-            if (lane == 31) base = atomicAdd(&s.ctr[C_TOUCHED_N], (unsigned long long)total);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            unsigned long long pos = base + (incl - c);
-            while (w) {
-                const uint32_t slot = (uint32_t)(wi * 32 + (uint64_t)(__ffs(w) - 1));
-                w &= w - 1;
-                s.tlist[pos++] = slot;
-                const double cn = s.acc[slot].w;
-                if (cn > 0.0) {
-                    sum += cn;
-                    ++cnt;
-                }
-            }
-        }
-        sum = warp_sum_d(sum);
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) {
-            ssum[threadIdx.x >> 5] = sum;
-            scnt[threadIdx.x >> 5] = cnt;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            unsigned long long c = 0;
-            for (int w = 0; w < EF_BLOCK / 32; ++w) {
-                t += ssum[w];
-                c += scnt[w];
-            }
-            if (c) {
-                atomicAdd(s.cn_sum, t);
-                atomicAdd(&s.ctr[C_CN_COUNT], c);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-/* Pass 2 (field.cpp:218-245) over the touched list: blend + cap, zero the accumulators. */
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
-    for (int j = 0; j < nst; ++j) {
-        const DevStore &s = st.s[j];
-        const uint64_t n = s.ctr[C_TOUCHED_N];
-        const unsigned long long cnt = s.ctr[C_CN_COUNT];
-        const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
-        const double tMax = s.t_max;
-        const bool limited = tMax > 0.0 && isfinite(tMax);
-        const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
-        unsigned internal = 0;
-        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-        /* two list entries per iteration, acc and com loads of both in flight together */
-        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
-            const bool two = i + stride < n;
-            const uint32_t sl[2] = {s.tlist[i], two ? s.tlist[i + stride] : s.tlist[i]};
-            const double4 av[2] = {s.acc[sl[0]], s.acc[sl[1]]};
-            const double4 cv[2] = {s.com[sl[0]], s.com[sl[1]]};
+    __shared__ double ssum[4][EF_BLOCK / 32];
+    __shared__ unsigned long long scnt[4][EF_BLOCK / 32];
+    uint64_t seg[4], nw[4];
+    uint64_t acc_w = 0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (k == 1 && !two) break;
-                const uint32_t slot = sl[k];
-                const double4 a = av[k];
-                const double cn = a.w;
-                if (cn > 0.0) {
-                    double4 c = cv[k];
-                    const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
-                    double alpha =
-                        s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
-                    if (limited) {
-                        const double fl = 1.0 / tMax;
-                        alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
-                    }
-                    const double oma = 1.0 - alpha;
-                    c.x = c.x * oma + cx * alpha;
-                    c.y = c.y * oma + cy * alpha;
-                    c.z = c.z * oma + cz * alpha;
-                    c.w = c.w + cn;
-                    if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
-                    s.com[slot] = c;
-                } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
-                    ++internal;
-                }
-                if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
-                    s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
-            }
+    for (int j = 0; j < 4; ++j) { /* static indices only: the arrays stay in registers */
+        nw[j] = j < nst ? ((uint64_t)st.s[j].mask + 32) / 32 : 0;
+        seg[j] = acc_w;
+        acc_w += (nw[j] + 31) & ~31ull;
+    }
+    const uint64_t total = acc_w; /* stores >= nst have no words: seg[j >= nst] == total */
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)nst) {
+        const DevStore &s = st.s[threadIdx.x];
+        s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+        s.ctr[C_EVICTED] = 0;
+    }
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned cnt[4] = {0u, 0u, 0u, 0u};
+    const unsigned lane = lane_id();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t iters = (total + stride - 1) / stride;
+    for (uint64_t it = 0; it < iters; ++it) { /* warp-uniform trip count (shuffles below) */
+        const uint64_t gi = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const int j = min(SEG_OF(gi, seg), nst - 1);
+        const uint64_t wi = gi - PICK4(seg, j);
+        const DevStore &s = st.s[j];
+        uint32_t w = gi < total && wi < PICK4(nw, j) ? s.tbits[wi] : 0u;
+        if (w) s.tbits[wi] = 0u;
+        const unsigned c = __popc(w);
+        unsigned incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += t;
         }
-        internal = __reduce_add_sync(0xffffffffu, internal);
-        if (lane_id() == 0 && internal) atomicAdd(&s.ctr[C_INTERNAL], (unsigned long long)internal);
+        const unsigned wtotal = __shfl_sync(0xffffffffu, incl, 31);
+        if (!wtotal) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(&s.ctr[C_TOUCHED_N], (unsigned long long)wtotal);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long pos = base + (incl - c);
+        double lsum = 0.0;
+        unsigned lcnt = 0;
+        while (w) {
+            uint32_t sl[8];
+            double cn[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sl[q] = w ? (uint32_t)(wi * 32 + (uint64_t)(__ffs(w) - 1)) : 0xffffffffu;
+                w &= w - 1;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cn[q] = sl[q] != 0xffffffffu ? s.acc[sl[q]].w : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (sl[q] != 0xffffffffu) {
+                    s.tlist[pos++] = sl[q];
+                    if (cn[q] > 0.0) {
+                        lsum += cn[q];
+                        ++lcnt;
+                    }
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q == j) {
+                sum[q] += lsum;
+                cnt[q] += lcnt;
+            }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double t = warp_sum_d(sum[q]);
+        const unsigned cc = __reduce_add_sync(0xffffffffu, cnt[q]);
+        if (lane == 0) {
+            ssum[q][threadIdx.x >> 5] = t;
+            scnt[q][threadIdx.x >> 5] = cc;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)nst) {
+        const int q = threadIdx.x;
+        double t = 0.0;
+        unsigned long long c = 0;
+        for (int w = 0; w < EF_BLOCK / 32; ++w) {
+            t += ssum[q][w];
+            c += scnt[q][w];
+        }
+        if (c) {
+            atomicAdd(st.s[q].cn_sum, t);
+            atomicAdd(&st.s[q].ctr[C_CN_COUNT], c);
+        }
     }
 }
 
-/* Pass 3 (field.cpp:247-260): age eviction, only when live*4 > capacity*3 (live before
- * eviction); the kernel exits at once otherwise. */
+/* endFrame pass 2 (field.cpp:216-246) over every store's touched list at once (one flat index
+ * space), two entries per thread per iteration with their acc/com loads in flight together */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
+    uint64_t seg[4];
+    uint64_t total = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        seg[j] = total;
+        total += j < nst ? st.s[j].ctr[C_TOUCHED_N] : 0;
+    }
+    unsigned internal[4] = {0u, 0u, 0u, 0u};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += 2 * stride) {
+        const bool two = i + stride < total;
+        int jj[2];
+        uint32_t sl[2];
+        double4 av[2], cv[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint64_t e = k == 0 || !two ? i : i + stride;
+            jj[k] = min(SEG_OF(e, seg), nst - 1);
+            sl[k] = st.s[jj[k]].tlist[e - PICK4(seg, jj[k])];
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            av[k] = st.s[jj[k]].acc[sl[k]];
+            cv[k] = st.s[jj[k]].com[sl[k]];
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (k == 1 && !two) break;
+            const DevStore &s = st.s[jj[k]];
+            const uint32_t slot = sl[k];
+            const double4 a = av[k];
+            const double cn = a.w;
+            if (cn > 0.0) {
+                const unsigned long long cnt = s.ctr[C_CN_COUNT];
+                const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
+                const double tMax = s.t_max;
+                const bool limited = tMax > 0.0 && isfinite(tMax);
+                const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
+                double4 c = cv[k];
+                const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+                double alpha =
+                    s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+                if (limited) {
+                    const double fl = 1.0 / tMax;
+                    alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+                }
+                const double oma = 1.0 - alpha;
+                c.x = c.x * oma + cx * alpha;
+                c.y = c.y * oma + cy * alpha;
+                c.z = c.z * oma + cz * alpha;
+                c.w = c.w + cn;
+                if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+                s.com[slot] = c;
+            } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q == jj[k]) ++internal[q];
+            }
+            if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
+                s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const unsigned t = __reduce_add_sync(0xffffffffu, internal[q]);
+        if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
+    }
+}
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish) {
     if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
         const DevStore &s = st.s[threadIdx.x];
