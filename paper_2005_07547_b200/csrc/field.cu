@@ -173,6 +173,20 @@ struct Scratch {
     }
 };
 
+/* A vertex pass whose phase 2 (new-key placement) may still be owed: pstf_vertex_pass returns
+ * right after phase 1 with the pending count on its way to pinned host memory, and the next
+ * entry point that touches one of its stores settles it.  pstf_fields_end_frame settles it for
+ * free in the common case: it enqueues endFrame guarded by the device-side count (the kernels
+ * return at once when new keys are pending), so when there are none the GPU never idles. */
+struct DeferredPass {
+    bool active = false;
+    pstf_field *fs[4] = {nullptr, nullptr, nullptr, nullptr};
+    int nf = 0, mode = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    unsigned long long *h_count = nullptr; /* pinned */
+};
+
 struct pstf_field {
     pstf_field_config cfg;
     int device = 0;
@@ -185,6 +199,12 @@ struct pstf_field {
     std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
     int world = 1;      /* key-owner sharding */
     std::vector<uint32_t> sc_px_scan_copy;
+    DeferredPass dp;              /* owned by the Lo store of a deferred vertex pass */
+    pstf_field *owed_by = nullptr; /* the Lo store whose deferred pass involves this store */
+    ~pstf_field() {
+        if (dp.ev) cudaEventDestroy(dp.ev);
+        if (dp.h_count) cudaFreeHost(dp.h_count);
+    }
 };
 
 static DevStore dev_view(const pstf_field *f) {
@@ -1619,7 +1639,9 @@ __device__ __forceinline__ double warp_sum_d(double v) {
  * (tbits cleared) and Σ c_new / #(c_new > 0) are reduced (field.cpp:201-214).  The stores'
  * bitmap words form one flat index space, each store's range padded to whole warps, so a warp
  * never straddles two stores; the c_new gathers of a word's set bits are issued 8 at a time. */
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst,
+                                                        const unsigned long long *guard) {
+    if (guard && *guard) return; /* new keys still pending: the host places them first */
     __shared__ double ssum[4][EF_BLOCK / 32];
     __shared__ unsigned long long scnt[4][EF_BLOCK / 32];
     uint64_t seg[4], nw[4];
@@ -1716,7 +1738,9 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst) {
 
 /* endFrame pass 2 (field.cpp:216-246) over every store's touched list at once (one flat index
  * space), two entries per thread per iteration with their acc/com loads in flight together */
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst,
+                                                       const unsigned long long *guard) {
+    if (guard && *guard) return;
     uint64_t seg[4];
     uint64_t total = 0;
 #pragma unroll
@@ -1785,7 +1809,9 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst) {
         if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
     }
 }
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish) {
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish,
+                                                       const unsigned long long *guard) {
+    if (guard && *guard) return;
     if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
         const DevStore &s = st.s[threadIdx.x];
         s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
@@ -2339,6 +2365,50 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     return PSTF_OK;
 }
 
+/* Completes the deferred vertex pass (if any) that involves store cf: waits for its pending
+ * count and places the new keys (phase 2). */
+static int settle(const pstf_field *cf) {
+    pstf_field *o = cf ? cf->owed_by : nullptr;
+    if (!o || !o->dp.active) return PSTF_OK;
+    DeferredPass &d = o->dp;
+    d.active = false;
+    for (int i = 0; i < 4; ++i)
+        if (d.fs[i]) d.fs[i]->owed_by = nullptr;
+    CK(cudaSetDevice(o->device));
+    CK(cudaEventSynchronize(d.ev));
+    const uint64_t n = *d.h_count;
+    if (n == 0) return PSTF_OK;
+    return resolve_pending(o->sc, d.fs, d.nf, d.mode, n, d.st);
+}
+
+#define SETTLE(f)                                                                                  \
+    do {                                                                                           \
+        int rc_ = settle(f);                                                                       \
+        if (rc_) return rc_;                                                                       \
+    } while (0)
+
+/* Ends a vertex pass: phase 2 now (PSTF_NO_DEFER), or deferred (see DeferredPass). */
+static int finish_vertex_pass(pstf_field *const fs[4], int mode, cudaStream_t st) {
+    pstf_field *lo = fs[0];
+    const int nf = fs[3] ? 4 : 3;
+    static const bool no_defer = getenv("PSTF_NO_DEFER") != nullptr;
+    if (no_defer) return resolve_pending(lo->sc, fs, nf, mode, (uint64_t)-1, st);
+    DeferredPass &d = lo->dp;
+    if (!d.ev) CK(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
+    if (!d.h_count) CK(cudaMallocHost(&d.h_count, 8));
+    CK(cudaMemcpyAsync(d.h_count, lo->sc.pend_count.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(d.ev, st));
+    for (int i = 0; i < 4; ++i) {
+        d.fs[i] = fs[i];
+        if (fs[i]) fs[i]->owed_by = lo;
+    }
+    d.nf = nf;
+    d.mode = mode;
+    d.st = st;
+    d.active = true;
+    return PSTF_OK;
+}
+
 static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t st) {
     ENSURE(sc.pend, cap * sizeof(PendRec));
     ENSURE(sc.pend_count, 8);
@@ -2484,6 +2554,7 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
 int pstf_field_destroy(pstf_field *f) {
     if (!f) return PSTF_OK;
     cudaSetDevice(f->device);
+    settle(f); /* no dangling deferred pass may reference this store */
     cudaDeviceSynchronize();
     if (f->arena) cudaFree(f->arena);
     delete f;
@@ -2524,6 +2595,7 @@ int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *v
     if (!n) return PSTF_OK;
     if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "batch too large");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     cudaStream_t st = (cudaStream_t)stream;
     Scratch &sc = f->sc;
     ApplyArgs a;
@@ -2642,6 +2714,7 @@ int pstf_field_apply_host(pstf_field *f, const pstf_key *keys, const double *rgb
     if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     CK(cudaDeviceSynchronize());
     std::vector<double> v;
     if (rgb_xyz) aos_to_soa(rgb_xyz, n, v);
@@ -2680,6 +2753,7 @@ int pstf_field_query_host(const pstf_field *f, const double *pos_xyz, const doub
         return set_err(PSTF_E_INVALID, "exactly one of footprint / level must be given");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     CK(cudaDeviceSynchronize());
     std::vector<double> p, d;
     aos_to_soa(pos_xyz, n, p);
@@ -2719,6 +2793,7 @@ int pstf_field_query(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_v
         return set_err(PSTF_E_INVALID, "exactly one of footprint / level must be given");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     LAUNCH(k_query, grid_for(n, 256), 256, 0, (cudaStream_t)stream, dev_view(f), *pos, *dir,
            footprint, level, n, value_r, value_g, value_b, valid, fallback, out_level);
     return PSTF_OK;
@@ -2735,13 +2810,38 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     }
     CK(cudaSetDevice(fs[0]->device));
     cudaStream_t st = (cudaStream_t)stream;
+    /* a deferred vertex pass of these stores on this stream: enqueue endFrame guarded by its
+     * device-side pending count, then look at the count; other deferred passes settle first */
+    pstf_field *owner = nullptr;
+    for (int i = 0; i < n; ++i) {
+        pstf_field *o = fs[i]->owed_by;
+        if (o && o->dp.active && o->dp.st == st && (!owner || owner == o)) owner = o;
+        else SETTLE(fs[i]);
+    }
     Stores4 S = stores4(fs, n);
     uint64_t maxcap = 0;
     for (int i = 0; i < n; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)fs[i]->d.mask + 1);
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
-    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n);
-    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n);
-    LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n, 1); /* + the per-frame scratch roll */
+    const unsigned long long *guard =
+        owner ? owner->sc.pend_count.as<const unsigned long long>() : nullptr;
+    auto launch = [&](const unsigned long long *gd) -> int {
+        LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n, gd);
+        LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n, gd);
+        LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n, 1, gd); /* + the per-frame scratch roll */
+        return PSTF_OK;
+    };
+    int rc = launch(guard);
+    if (rc) return rc;
+    if (owner) {
+        CK(cudaEventSynchronize(owner->dp.ev));
+        if (*owner->dp.h_count) { /* the guarded sweeps did nothing: place, then sweep */
+            SETTLE(owner);
+            rc = launch(nullptr);
+            if (rc) return rc;
+        } else {
+            SETTLE(owner); /* nothing pending: just retire the deferred pass */
+        }
+    }
     for (int i = 0; i < n; ++i) fs[i]->frame += 1;
     return PSTF_OK;
 }
@@ -2754,6 +2854,7 @@ int pstf_field_end_frame(pstf_field *f, void *stream) {
 int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream) {
     if (!f) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     const uint64_t cap = (uint64_t)f->d.mask + 1;
     unsigned g = std::min<unsigned>(grid_for(cap, 256), (unsigned)sm_count() * 8);
     if (aabb)
@@ -2767,6 +2868,7 @@ int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream) {
 int pstf_field_get_stats(pstf_field *f, pstf_field_stats *out) {
     if (!f || !out) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     CK(cudaDeviceSynchronize());
     unsigned long long c[C_NUM];
     CK(cudaMemcpy(c, f->d.ctr, sizeof(c), cudaMemcpyDeviceToHost));
@@ -2806,6 +2908,7 @@ __global__ void k_probe_hist(DevStore s, unsigned long long *hist) {
 int pstf_field_probe_histogram(pstf_field *f, uint64_t hist[33]) {
     if (!f || !hist) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     Scratch &sc = f->sc;
     ENSURE(sc.ranges, 33 * 8);
     CK(cudaMemset(sc.ranges.p, 0, 33 * 8));
@@ -2857,6 +2960,7 @@ int pstf_diag_red_peak(int device, double *ops_per_second) {
 int pstf_field_weighted_mean(pstf_field *f, double out[3]) {
     if (!f || !out) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     Scratch &sc = f->sc;
     ENSURE(sc.ranges, 64);
     CK(cudaMemset(sc.ranges.p, 0, 32));
@@ -2904,6 +3008,7 @@ int pstf_field_snapshot(pstf_field *f, pstf_snapshot_record *records, uint64_t c
                         uint64_t *count) {
     if (!f || !count || (cap && !records)) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     uint64_t n = 0;
     pstf_snapshot_record *d = nullptr;
     int rc = snapshot_device(f, &n, &d);
@@ -2917,6 +3022,7 @@ int pstf_field_snapshot(pstf_field *f, pstf_snapshot_record *records, uint64_t c
 int pstf_field_dump_snapshot(pstf_field *f, const char *path) {
     if (!f || !path) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     uint64_t n = 0;
     pstf_snapshot_record *d = nullptr;
     int rc = snapshot_device(f, &n, &d);
@@ -2985,6 +3091,7 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
     if (begin > cap || count > cap - begin) return set_err(PSTF_E_INVALID, "slot range out of bounds");
     if (!count) return PSTF_OK;
     CK(cudaSetDevice(f->device));
+    SETTLE(f);
     CK(cudaDeviceSynchronize());
     std::vector<uint2> meta(count);
     std::vector<double4> com(count), acc(count);
@@ -3165,6 +3272,10 @@ int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_fiel
     if (rc) return rc;
     if (!v) return set_err(PSTF_E_INVALID, "NULL vertex record");
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
+    SETTLE(loe);
+    SETTLE(fli);
+    SETTLE(li);
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
@@ -3173,7 +3284,11 @@ int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_fiel
         if (rc) return rc;
     }
     pstf_field *fs[4] = {lo, loe, fli, li};
-    return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
+    for (int i = 0; i < 4; ++i) /* "new keys / rounds of the last pass" start at 0 */
+        if (fs[i]) CK(cudaMemsetAsync(&fs[i]->d.ctr[C_NEW_KEYS], 0, 8, st));
+    for (int i = 0; i < 4; ++i)
+        if (fs[i]) CK(cudaMemsetAsync(&fs[i]->d.ctr[C_ROUNDS], 0, 8, st));
+    return finish_vertex_pass(fs, mode, st);
 }
 
 int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
@@ -3186,6 +3301,10 @@ int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_f
     if (n && (!cv_r || !cv_g || !cv_b || !cv_valid))
         return set_err(PSTF_E_INVALID, "CV outputs required");
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
+    SETTLE(loe);
+    SETTLE(fli);
+    SETTLE(li);
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
@@ -3195,7 +3314,11 @@ int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_f
         if (rc) return rc;
     }
     pstf_field *fs[4] = {lo, loe, fli, li};
-    return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
+    for (int i = 0; i < 4; ++i) /* "new keys / rounds of the last pass" start at 0 */
+        if (fs[i]) CK(cudaMemsetAsync(&fs[i]->d.ctr[C_NEW_KEYS], 0, 8, st));
+    for (int i = 0; i < 4; ++i)
+        if (fs[i]) CK(cudaMemsetAsync(&fs[i]->d.ctr[C_ROUNDS], 0, 8, st));
+    return finish_vertex_pass(fs, mode, st);
 }
 
 void pstf_vertex_soa_from_buffer(const double *b, uint64_t n, pstf_vertex_soa *o) {
@@ -3233,6 +3356,10 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
     if (rc) return rc;
     if (!hv) return set_err(PSTF_E_INVALID, "NULL vertex record");
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
+    SETTLE(loe);
+    SETTLE(fli);
+    SETTLE(li);
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
@@ -3294,6 +3421,7 @@ int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, 
     if (!loe || !v) return set_err(PSTF_E_INVALID, "NULL argument");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(loe->device));
+    SETTLE(loe);
     LAUNCH(k_cv_lookup, grid_for(n, 256), 256, 0, (cudaStream_t)stream, dev_view(loe), *v, n,
            value_r, value_g, value_b, valid);
     return PSTF_OK;
@@ -3339,6 +3467,7 @@ static int shard_checks(pstf_field *const *fs, int n) {
 
 int pstf_shard_set(pstf_field *f, int rank, int world) {
     if (!f) return set_err(PSTF_E_INVALID, "NULL store");
+    SETTLE(f);
     if (world < 1 || world > 32 || (world & (world - 1)))
         return set_err(PSTF_E_INVALID, "world must be a power of two in [1, 32]");
     if (rank < 0 || rank >= world) return set_err(PSTF_E_INVALID, "bad rank");
@@ -3359,6 +3488,10 @@ int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pst
     if (rc) return rc;
     if (!v) return set_err(PSTF_E_INVALID, "NULL vertex record");
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
+    SETTLE(loe);
+    SETTLE(fli);
+    SETTLE(li);
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(PSTF_MODE_ATOMIC, li)),
                         false, st);
@@ -3370,6 +3503,7 @@ int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pst
 int pstf_pending_count(pstf_field *lo, uint64_t *n) {
     if (!lo || !n) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
     CK(cudaDeviceSynchronize());
     unsigned long long c = 0;
     if (lo->sc.pend_count.p) CK(cudaMemcpy(&c, lo->sc.pend_count.p, 8, cudaMemcpyDeviceToHost));
@@ -3381,6 +3515,7 @@ int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream) {
     if (!lo || (n && !dst)) return set_err(PSTF_E_INVALID, "NULL argument");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
     CK(cudaMemcpyAsync(dst, lo->sc.pend.p, n * sizeof(PendRec), cudaMemcpyDeviceToDevice,
                        (cudaStream_t)stream));
     return PSTF_OK;
@@ -3391,6 +3526,7 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, u
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     Scratch &sc = stores[0]->sc;
     rc = ensure_pending(sc, std::max<uint64_t>(n, 1), false, st);
@@ -3405,6 +3541,7 @@ int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t
     if (rc) return rc;
     if (!counts) return set_err(PSTF_E_INVALID, "NULL counts");
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     const int world = stores[0]->world;
     Scratch &sc = stores[0]->sc;
@@ -3470,6 +3607,7 @@ int pstf_partials_import(pstf_field *const *stores, int nst, const void *recs, u
     if (rc) return rc;
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     LAUNCH(k_px_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
            (const PartialRec *)recs, n);
     return PSTF_OK;
@@ -3480,6 +3618,7 @@ int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, v
     if (rc) return rc;
     if (!sum_cnt) return set_err(PSTF_E_INVALID, "NULL sum_cnt");
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     uint64_t maxcap = 0;
     for (int i = 0; i < nst; ++i) {
@@ -3487,7 +3626,8 @@ int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, v
         CK(cudaMemsetAsync(&stores[i]->d.ctr[C_EVICTED], 0, 8, st));
     }
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
-    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, stores4(stores, nst), nst);
+    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, stores4(stores, nst), nst,
+           (const unsigned long long *)nullptr);
     CK(cudaStreamSynchronize(st));
     for (int i = 0; i < nst; ++i) {
         unsigned long long c = 0;
@@ -3504,6 +3644,7 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
     if (rc) return rc;
     if (!global_sum_cnt || !ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     Scratch &sc = stores[0]->sc;
     for (int i = 0; i < nst; ++i) { /* the batch-wide mean c_new of pass 1 */
@@ -3516,7 +3657,7 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
     for (int i = 0; i < nst; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
     Stores4 S = stores4(stores, nst);
-    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, nst);
+    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, nst, (const unsigned long long *)nullptr);
     ENSURE(sc.changed, 16);
     CK(cudaMemsetAsync(sc.changed.p, 0, 8, st));
     unsigned long long *dcount = (unsigned long long *)sc.changed.p;
@@ -3530,7 +3671,7 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
             LAUNCH(k_ef_evict_range, g, EF_BLOCK, 0, st, s, (uint32_t)i, lo, hi, (DeltaRec *)deltas,
                    dcount);
     }
-    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0);
+    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0, (const unsigned long long *)nullptr);
     LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
     for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
     unsigned long long nd = 0;
@@ -3547,6 +3688,7 @@ int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, u
     if (rc) return rc;
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     LAUNCH(k_dx_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
            (const DeltaRec *)deltas, n);
     return PSTF_OK;
