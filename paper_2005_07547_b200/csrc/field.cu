@@ -367,15 +367,16 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
         const double *flat = reinterpret_cast<const double *>(sm);
         const int comp = lane & 3;
 #pragma unroll
+        uint32_t cnt = 0;
         for (int k = 0; k < 4; ++k) {
             const int cell = 8 * k + (lane >> 2);
             const int rs = rsm[cell];
             const double val = flat[4 * cell + comp];
-            if (rs >= 0 && val != 0.0) {
-                atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
-                if (nred) ++*nred;
-            }
+            const bool on = rs >= 0 && val != 0.0;
+            if (on) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+            cnt += on;
         }
+        if (nred) *nred += cnt;
         __syncwarp();
         if (res >= 0) touch_slot(s, (uint32_t)res, mark);
     } else if (__all_sync(0xffffffffu, peers == (1u << lane))) {
