@@ -90,7 +90,7 @@ def main():
         for r in rows[1:]:
             if "k_vertex_pass" in r[ik]:
                 seen_vp += 1
-            if seen_vp <= a.skip_steps or r[ik].startswith("k_synth"):
+            if seen_vp <= a.skip_steps or r[ik].startswith(("k_synth", "k_red_peak")):
                 continue
             v = float(r[iv].replace(",", ""))
             v = v / 1e3 if r[iu] == "ns" else (v if r[iu] == "us" else v * 1e3)
@@ -100,7 +100,7 @@ def main():
         allt = sum(tot.values())
         lines += ["## Launch list (`ncu --metrics gpu__time_duration.sum`, serialised, cold-cache)",
                   "", f"Timed steps only (first {a.skip_steps} vertex-pass steps and the input "
-                  "generator dropped).", "",
+                  "generator and the RED-peak diagnostic dropped).", "",
                   "| kernel | launches | total us | share |", "|---|---|---|---|"]
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / allt:.1f}% |")
