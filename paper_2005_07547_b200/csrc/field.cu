@@ -822,26 +822,36 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     /* ---- keys (estimators.cpp:195, 215, 226, 242, 248, 257): one level, one cell triple and
      * one packKeyFields prefix for all update keys of the vertex ---- */
     int nx = 0; /* set when any quantity lies too close to a cell boundary for the fast path */
-    int level = select_level_try(fq, S.f(PS_FP), &nx);
-    const double px = S.f(PS_POS), py = S.f(PS_POS + 1), pz = S.f(PS_POS + 2);
-    const PosQ q = pos_q(fq, px, py, pz);
-    int32_t c0 = cell_try(q.q[0], px, level, &nx), c1 = cell_try(q.q[1], py, level, &nx),
-            c2 = cell_try(q.q[2], pz, level, &nx);
     DirF8 fo, fi, fin, fn, ftmp;
-    const double wox = S.f(PS_WO), woy = S.f(PS_WO + 1), woz = S.f(PS_WO + 2);
+    const uint2 z = make_uint2(0u, 0u);
+    const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
+    /* the first lookup key at the next vertex goes first (estimators.cpp:198-206): its home words
+     * and speculative committed records then travel while the update keys are built */
     const double wix = S.f(PS_WI), wiy = S.f(PS_WI + 1), wiz = S.f(PS_WI + 2);
-    /* lanes without NEE use a fixed generic direction so a speculated evaluation never lands
-     * near a boundary for their zero nee.dir */
-    const double ndx = nee ? S.f(PS_NDIR) : 0.36, ndy = nee ? S.f(PS_NDIR + 1) : 0.48,
-                 ndz = nee ? S.f(PS_NDIR + 2) : 0.8;
-    octa_f8_try(wox, woy, woz, 0, &fo, &ftmp, &nx);
     octa_f8_try(wix, wiy, wiz, look, &fi, &fin, &nx);
-    octa_f8_try(ndx, ndy, ndz, 0, &fn, &ftmp, &nx);
     const double qx = S.f(PS_NPOS), qy = S.f(PS_NPOS + 1), qz = S.f(PS_NPOS + 2);
     const PosQ nq = pos_q(fq, qx, qy, qz);
     int l0 = select_level_try(fq, S.f(PS_NFP), &nx);
     int32_t n0 = cell_try(nq.q[0], qx, l0, &nx), n1 = cell_try(nq.q[1], qy, l0, &nx),
             n2 = cell_try(nq.q[2], qz, l0, &nx);
+    uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
+    uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
+    uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
+    double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
+
+    /* ---- the update keys: one level, one cell triple, one packKeyFields prefix ---- */
+    int level = select_level_try(fq, S.f(PS_FP), &nx);
+    const double px = S.f(PS_POS), py = S.f(PS_POS + 1), pz = S.f(PS_POS + 2);
+    const PosQ q = pos_q(fq, px, py, pz);
+    int32_t c0 = cell_try(q.q[0], px, level, &nx), c1 = cell_try(q.q[1], py, level, &nx),
+            c2 = cell_try(q.q[2], pz, level, &nx);
+    const double wox = S.f(PS_WO), woy = S.f(PS_WO + 1), woz = S.f(PS_WO + 2);
+    /* lanes without NEE use a fixed generic direction so a speculated evaluation never lands
+     * near a boundary for their zero nee.dir */
+    const double ndx = nee ? S.f(PS_NDIR) : 0.36, ndy = nee ? S.f(PS_NDIR + 1) : 0.48,
+                 ndz = nee ? S.f(PS_NDIR + 2) : 0.8;
+    octa_f8_try(wox, woy, woz, 0, &fo, &ftmp, &nx);
+    octa_f8_try(ndx, ndy, ndz, 0, &fn, &ftmp, &nx);
     if (nx) { /* rare: the vertex's quantities through the exact reference operations (one
                * out-of-the-way block instead of a fallback at every use) */
         level = select_level(kp, S.f(PS_FP));
@@ -855,6 +865,13 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         n0 = cell_exact(kp, qx, l0);
         n1 = cell_exact(kp, qy, l0);
         n2 = cell_exact(kp, qz, l0);
+        qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
+        ql = (uint32_t)qpk & sLo.mask;
+        qe = (uint32_t)qpk & sLoe.mask;
+        wl = look ? sLo.meta[ql].x : 0u;
+        we = look ? sLoe.meta[qe].x : 0u;
+        sl = look ? sLo.com[ql] : z4;
+        se = look ? sLoe.com[qe] : z4;
     }
     pipe.key_inputs_done();
     const uint64_t h1 = pack_h1(level, c0, c1);
@@ -862,23 +879,14 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const Key kFc = make_key(h1, level, c0, c1, c2, dir_cell_f8(fi.u, level), dir_cell_f8(fi.v, level));
     const Key kFn = make_key(h1, level, c0, c1, c2, dir_cell_f8(fn.u, level), dir_cell_f8(fn.v, level));
 
-    /* ---- first lookup key at the next vertex (estimators.cpp:198-206) ---- */
-    uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
-
-    /* ---- one round trip: the five update home words, the two lookup home words and (on
-     * speculation that the lookup key sits at its home slot) the two committed records ---- */
+    /* ---- the five update home words in one round trip ---- */
     const bool has2 = live && cont, has3 = live && nee, has4 = a.has_li && live && cont;
     const uint32_t h0 = kLo.pack_lo & sLo.mask, h1s = kLo.pack_lo & sLoe.mask,
                    h2 = kFc.pack_lo & sFli.mask, h3 = kFn.pack_lo & sFli.mask,
                    h4 = kFc.pack_lo & sLi.mask;
-    const uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
-    const uint2 z = make_uint2(0u, 0u);
-    const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
     const uint2 m0 = live ? sLo.meta[h0] : z, m1 = live ? sLoe.meta[h1s] : z,
                 m2 = has2 ? sFli.meta[h2] : z, m3 = has3 ? sFli.meta[h3] : z,
                 m4 = has4 ? sLi.meta[h4] : z;
-    const uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
-    const double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
     /* CV lookup at this vertex = Lo\E query of the Lo key: speculate its home record too */
     const double4 scv = CV && live ? sLoe.com[h1s] : z4;
 
