@@ -650,6 +650,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
  * cell once and each direction goes through atan2 once (pos_q / octa_pair), shared by the Lo,
  * Lo\E, FLi and Li keys and by every level of the next-vertex lookup chain.
  */
+#ifndef PSTF_FLI_NEXT_WORD
+#define PSTF_FLI_NEXT_WORD 1
+#endif
 #ifndef VT_THREADS
 #define VT_THREADS 128 /* vertices (= threads) per tile and CTA */
 #endif
@@ -887,6 +890,11 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const uint2 m0 = live ? sLo.meta[h0] : z, m1 = live ? sLoe.meta[h1s] : z,
                 m2 = has2 ? sFli.meta[h2] : z, m3 = has3 ? sFli.meta[h3] : z,
                 m4 = has4 ? sLi.meta[h4] : z;
+#if PSTF_FLI_NEXT_WORD
+    /* the FLi store is the crowded one: its two probes also preload the word after home */
+    const uint2 m2b = has2 ? sFli.meta[(h2 + 1) & sFli.mask] : z,
+                m3b = has3 ? sFli.meta[(h3 + 1) & sFli.mask] : z;
+#endif
     /* CV lookup at this vertex = Lo\E query of the Lo key: speculate its home record too */
     const double4 scv = CV && live ? sLoe.com[h1s] : z4;
 
@@ -958,8 +966,13 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
     const int r0 = live ? resolve_probe(sLo, h0, kLo.checksum, m0, &k0) : -3;
     const int r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
+#if PSTF_FLI_NEXT_WORD
+    const int r2 = has2 ? resolve_probe2(sFli, h2, kFc.checksum, m2, m2b, &k2) : -3;
+    const int r3 = has3 ? resolve_probe2(sFli, h3, kFn.checksum, m3, m3b, &k3) : -3;
+#else
     const int r2 = has2 ? resolve_probe(sFli, h2, kFc.checksum, m2, &k2) : -3;
     const int r3 = has3 ? resolve_probe(sFli, h3, kFn.checksum, m3, &k3) : -3;
+#endif
     const int r4 = has4 ? resolve_probe(sLi, h4, kFc.checksum, m4, &k4) : -3;
     const bool red = !(a.dbg & 2);
     const bool agg = (a.dbg & 16) != 0; /* warp aggregation measured slower on config 2 */

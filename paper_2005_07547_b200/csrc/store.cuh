@@ -154,6 +154,32 @@ __device__ __forceinline__ int resolve_probe(const DevStore &s, uint32_t home, u
     return -2;
 }
 
+/* same with the word after home also preloaded (one round trip settles a single collision) */
+__device__ __forceinline__ int resolve_probe2(const DevStore &s, uint32_t home, uint32_t cs,
+                                              uint2 m0, uint2 m1, uint32_t *mark) {
+    if (m0.x == cs) {
+        *mark = m0.y;
+        return (int)home;
+    }
+    if (m0.x == 0) return -1;
+    if (s.window < 2) return -2;
+    if (m1.x == cs) {
+        *mark = m1.y;
+        return (int)((home + 1) & s.mask);
+    }
+    if (m1.x == 0) return -1;
+    for (uint32_t i = 2; i < s.window; ++i) {
+        uint32_t idx = (home + i) & s.mask;
+        uint2 m = s.meta[idx];
+        if (m.x == cs) {
+            *mark = m.y;
+            return (int)idx;
+        }
+        if (m.x == 0) return -1;
+    }
+    return -2;
+}
+
 /* finish a findSlot (lookup) whose home word was already loaded: slot or -1 */
 __device__ __forceinline__ int resolve_find(const DevStore &s, uint32_t home, uint32_t cs,
                                             uint32_t c0) {
