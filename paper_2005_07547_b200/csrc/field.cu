@@ -366,8 +366,8 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
         __syncwarp();
         const double *flat = reinterpret_cast<const double *>(sm);
         const int comp = lane & 3;
-#pragma unroll
         uint32_t cnt = 0;
+#pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int cell = 8 * k + (lane >> 2);
             const int rs = rsm[cell];
@@ -650,6 +650,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
  * cell once and each direction goes through atan2 once (pos_q / octa_pair), shared by the Lo,
  * Lo\E, FLi and Li keys and by every level of the next-vertex lookup chain.
  */
+#ifndef PSTF_VP_DBG_BUILD
+#define PSTF_VP_DBG_BUILD 0 /* experiment builds: 1 no lookups, 2 no RED, 4 keys only, 32 stream */
+#endif
 #ifndef PSTF_FLI_NEXT_WORD
 #define PSTF_FLI_NEXT_WORD 1
 #endif
@@ -820,7 +823,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const bool cont = (fl & PSTF_VERTEX_CONT_EXTENDED) != 0;
     const bool nsurf = (fl & PSTF_VERTEX_NEXT_IS_SURFACE) != 0;
     const bool nee = (fl & PSTF_VERTEX_NEE_SAMPLED) != 0;
-    const bool look = cont && nsurf && !(a.dbg & 1);
+    const bool look = cont && nsurf && !(PSTF_VP_DBG_BUILD & 1);
 
     /* ---- keys (estimators.cpp:195, 215, 226, 242, 248, 257): one level, one cell triple and
      * one packKeyFields prefix for all update keys of the vertex ---- */
@@ -952,7 +955,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         }
     }
 
-    if (a.dbg & 4) {
+    if (PSTF_VP_DBG_BUILD & 4) {
         if ((m0.x ^ m1.x ^ m2.x ^ m3.x ^ m4.x ^ kLo.checksum ^ kFc.checksum ^ kFn.checksum) ==
                 0x12345u && loNext.x + loeNext.y == 1.2345)
             atomicAdd(&sLo.ctr[C_INTERNAL], 1ull);
@@ -974,8 +977,6 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const int r3 = has3 ? resolve_probe(sFli, h3, kFn.checksum, m3, &k3) : -3;
 #endif
     const int r4 = has4 ? resolve_probe(sLi, h4, kFc.checksum, m4, &k4) : -3;
-    const bool red = !(a.dbg & 2);
-    const bool agg = (a.dbg & 16) != 0; /* warp aggregation measured slower on config 2 */
     const PendSink ps{a.pend, a.pend_count, a.pend_cap};
 
     if (CV && live) {
@@ -1037,12 +1038,17 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             ++rej;
         }
     };
-    unsigned rej = 0;
+    /* contribution c: store sid(c) = {Lo, Lo\E, FLi, FLi, Li}; its probe result and touch mark
+     * shift down one register per iteration (no select chains) */
+    int rr0 = r0, rr1 = r1, rr2 = r2, rr3 = r3, rr4 = r4;
+    uint32_t kk0 = k0, kk1 = k1, kk2 = k2, kk3 = k3, kk4 = k4;
+    uint32_t rejpack = 0; /* rejected calls per store, one byte each (at most 3 per vertex) */
     const int ncontrib = a.has_li ? 5 : 4;
 #pragma unroll 1
     for (int c = 0; c < ncontrib; ++c) {
         double4 v = make_double4(0.0, 0.0, 0.0, 1.0); /* the counter call */
         uint32_t nc = 1;
+        unsigned rej = 0;
         if (c == 0) { /* Lo: emission, transport (estimators.cpp:210-224) */
             add3(v, nc, rej, S.f(PS_EMIS), S.f(PS_EMIS + 1), S.f(PS_EMIS + 2));
             if (transp) {
@@ -1073,16 +1079,52 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                      li(2, loeNext.z) * 1.0);
         }
         const int sid = c < 2 ? c : (c < 4 ? 2 : 3);
-        const StoreRef s = store_ref(sid == 0 ? sLo : sid == 1 ? sLoe : sid == 2 ? sFli : sLi);
-        if (c != 2) { /* the two FLi contributions share one rejected-counter update */
-            if (live && rej) atomicAdd(&s.ctr[C_REJECTED], (unsigned long long)rej);
-            rej = 0;
+        rejpack += rej << (8 * sid);
+        const DevStore &s = a.st.s[sid];
+        const int res = rr0;
+        const uint32_t mark = kk0;
+        /* sector-coalesced REDs: the warp's 32 cells x 4 components are transposed through
+         * shared memory so each RED instruction covers 8 cells x {r,g,b,c}; the 4 lanes of a
+         * cell hit one 32 B sector, so L1 sends 8 sector requests per instruction, not 32 */
+        int *rsm = reinterpret_cast<int *>(sm + 32);
+        const unsigned lane = lane_id();
+        sm[lane] = v;
+        rsm[lane] = (PSTF_VP_DBG_BUILD & 2) ? -3 : res;
+        __syncwarp();
+        const double *flat = reinterpret_cast<const double *>(sm);
+        const int comp = lane & 3;
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int cell = 8 * q + (lane >> 2);
+            const int rs = rsm[cell];
+            const double val = flat[4 * cell + comp];
+            const bool on = rs >= 0 && val != 0.0;
+            if (on) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+            cnt += on;
         }
-        const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
-        const int res = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : c == 3 ? r3 : r4;
-        const uint32_t mark = c == 0 ? k0 : c == 1 ? k1 : c == 2 ? k2 : c == 3 ? k3 : k4;
-        apply_contribution(s, ps, sm, sid, k, v, nc, res, mark, red, agg, &nred);
+        nred += cnt;
+        __syncwarp();
+        if (res >= 0) touch_slot(s, (uint32_t)res, mark);
+        if (PendRec *p = warp_reserve(ps, res == -1)) { /* a new key (rare after warm-up) */
+            const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
+            put_record(p, k, PSTF_META(sid, 0, nc) | ((uint32_t)s.rank << 3), v.x, v.y, v.z, v.w);
+        }
+        if (res == -2) atomicAdd(&s.ctr[C_DROPPED], (unsigned long long)nc); /* per call */
+        rr0 = rr1;
+        rr1 = rr2;
+        rr2 = rr3;
+        rr3 = rr4;
+        kk0 = kk1;
+        kk1 = kk2;
+        kk2 = kk3;
+        kk3 = kk4;
     }
+    if (__any_sync(0xffffffffu, live && rejpack != 0) && live) /* non-finite values (rare) */
+        for (int q = 0; q < 4; ++q) {
+            const unsigned r = (rejpack >> (8 * q)) & 0xffu;
+            if (r) atomicAdd(&a.st.s[q].ctr[C_REJECTED], (unsigned long long)r);
+        }
     pipe.values_done();
 }
 
@@ -1146,7 +1188,7 @@ __global__ void __launch_bounds__(VT, MINB)
                 }
             }
         };
-        if (a.dbg & 32) { /* experiment: stream only */
+        if (PSTF_VP_DBG_BUILD & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
             vertex_body<CV>(a, src, live, sm, nred);
