@@ -507,18 +507,19 @@ PSTF_HD PosQ pos_q(const FastParams &f, double px, double py, double pz) {
 /* Fast cell coordinate floor(pcoord / (base 2^level)) from q = pcoord * fl(1 / base); sets *nx
  * when x' is within 2^-50 |x'| of an integer (or out of the plain range). */
 PSTF_HD int32_t cell_try(double q, double pcoord, int level, int *nx) {
+    /* branch-free: q == 0 exactly when pcoord == 0 (q = pcoord * fl(1/base), no underflow to 0
+     * for nonzero pcoord above 2^-900), and then floor(+-0 / cs) == 0 like the fast path */
+    (void)pcoord;
     const double x = q * pow2d(-level);
     const double ax = fabs(x);
-    if (pcoord == 0.0) return 0; /* floor(+-0 / cs) == 0 (points on the coordinate planes) */
-    if (ax >= 0x1p-900 && ax < 2147483647.0) {
-        const double fl = floor(x); /* in [-2^31 + 1, 2^31 - 2]: a plain conversion is exact */
-        const double e = ax * 0x1p-50;
-        if (x - fl >= e && (fl + 1.0) - x >= e) return (int32_t)fl;
-    } else if (ax >= 4294967296.0 && ax <= 1.7976931348623157e308) {
-        return INT32_MIN; /* far outside int32: the reference's conversion gives INT32_MIN */
-    }
-    *nx = 1;
-    return 0;
+    const double fl = floor(x);
+    const double e = ax * 0x1p-50;
+    const bool ok = ax < 2147483647.0 && (ax >= 0x1p-900 || ax == 0.0) && x - fl >= e &&
+                    (fl + 1.0) - x >= e; /* fl in [-2^31 + 1, 2^31 - 2]: exact conversion */
+    /* far outside int32 (finite): the reference's conversion gives INT32_MIN */
+    const bool far = ax >= 4294967296.0 && ax <= 1.7976931348623157e308;
+    *nx |= !(ok || far);
+    return ok ? (int32_t)fl : INT32_MIN;
 }
 
 PSTF_HD int32_t cell_at(const FastParams &f, double q, double pcoord, int level) {
@@ -609,6 +610,20 @@ PSTF_HD double atan2_try(double y, double x, int *nx) {
     return swap ? 1.5707963267948966 - th : th;
 }
 
+/* sqrt(w) for w in [0, 1] from the hardware reciprocal square root plus one fp32 Newton
+ * correction: within 1.5 ulp (branch-free, 0 -> 0) */
+PSTF_HD float sqrt_fast(float w) {
+#if defined(__CUDA_ARCH__)
+    const float y = rsqrtf(w);
+#else
+    const float y = 1.0f / sqrtf(w);
+#endif
+    const float r = w * y;
+    const float e = fmaf(-r, r, w);
+    const float s = fmaf(e, 0.5f * y, r);
+    return w > 0.0f ? s : 0.0f;
+}
+
 /* floor(q) of q = 8 U in single precision; near when q is within 2e-5 of an integer (the
  * single-precision U below is within 1e-6 of the exact one, see octa_f8_try) */
 PSTF_HD int32_t f8_of32(float U, int *near) {
@@ -622,7 +637,7 @@ PSTF_HD int32_t f8_of32(float U, int *near) {
  * fast path; *nx set when any coordinate may lie within its error of a cell boundary or the
  * inputs are outside the fast path's domain (the caller then recomputes with octa_f8_exact).
  * Error budget (|.| in U units): w = 1 - |z| is formed in double precision and rounded once
- * (6e-8 relative), r = sqrtf(w) correctly rounded, phi from a degree-4 minimax polynomial in t^2
+ * (6e-8 relative), r = sqrt_fast(w) within 1.5 ulp, phi from a degree-4 minimax polynomial in t^2
  * after an octant reduction with a correctly rounded reciprocal (|error| < 3e-7), then four
  * rounded products/sums: |U' - U| < 1e-6, so q' = 8 U' is within 8e-6 of q, well inside the
  * 2e-5 margin.  NaN, infinite and denormal-scale x, y always take the exact path. */
@@ -630,7 +645,8 @@ PSTF_HD void octa_f8_try(double dx, double dy, double dz, int want_neg, DirF8 *p
                          int *nx) {
     const double x = fabs(dx), y = fabs(dy), z = fabs(dz);
     const double omz = 1.0 - z;
-    const float r = sqrtf((float)((0.0 < omz) ? omz : 0.0)); /* safeSqrt (vecmath.h:22) */
+    const float wf = (float)((0.0 < omz) ? omz : 0.0); /* safeSqrt (vecmath.h:22) */
+    const float r = sqrt_fast(wf);
     float phi = 0.0f;
     if (!(x == 0.0 && y == 0.0)) {
         const double mx = x > y ? x : y;
@@ -683,11 +699,11 @@ PSTF_HD void octa_f8(double dx, double dy, double dz, int want_neg, DirF8 *pos, 
 
 /* dirCell at a level from floor(U*8): min(floor(U*d), d-1) (field.cpp:93-95) */
 PSTF_HD int32_t dir_cell_f8(int32_t f8, int level) {
-    if (f8 == INT32_MIN) return INT32_MIN;
     const int sh = level < 2 ? level : 2;
     const int32_t d = 8 >> sh;
     const int32_t c = f8 >> sh;
-    return c < d - 1 ? c : d - 1;
+    const int32_t r = c < d - 1 ? c : d - 1;
+    return f8 == INT32_MIN ? INT32_MIN : r; /* NaN direction (select, no branch) */
 }
 
 } // namespace pstf_b200
