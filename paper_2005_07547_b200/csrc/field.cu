@@ -653,6 +653,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #ifndef PSTF_VP_DBG_BUILD
 #define PSTF_VP_DBG_BUILD 0 /* experiment builds: 1 no lookups, 2 no RED, 4 keys only, 32 stream */
 #endif
+#ifndef PSTF_PRED_RED
+#define PSTF_PRED_RED 1
+#endif
 #ifndef PSTF_FLI_NEXT_WORD
 #define PSTF_FLI_NEXT_WORD 1
 #endif
@@ -1100,7 +1103,16 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             const int rs = rsm[cell];
             const double val = flat[4 * cell + comp];
             const bool on = rs >= 0 && val != 0.0;
+#if PSTF_PRED_RED
+            /* predicated RED, no branch around it (no memory clobber: the RED is unordered
+             * with the thread's other accesses, which never touch acc this pass) */
+            double *dst = reinterpret_cast<double *>(&s.acc[on ? rs : 0]) + comp;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                         "@p red.relaxed.gpu.global.add.f64 [%0], %1;\n\t}" ::"l"(dst),
+                         "d"(val), "r"((uint32_t)on));
+#else
             if (on) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+#endif
             cnt += on;
         }
         nred += cnt;
