@@ -1096,6 +1096,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         __syncwarp();
         const double *flat = reinterpret_cast<const double *>(sm);
         const int comp = lane & 3;
+        double *const accc = reinterpret_cast<double *>(s.acc) + comp; /* component column */
         uint32_t cnt = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -1105,8 +1106,9 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             const bool on = rs >= 0 && val != 0.0;
 #if PSTF_PRED_RED
             /* predicated RED, no branch around it (no memory clobber: the RED is unordered
-             * with the thread's other accesses, which never touch acc this pass) */
-            double *dst = reinterpret_cast<double *>(&s.acc[on ? rs : 0]) + comp;
+             * with the thread's other accesses, which never touch acc this pass); 32-bit slot
+             * index, one wide multiply-add for the address */
+            double *dst = accc + (uint64_t)(on ? (uint32_t)rs : 0u) * 4u;
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
                          "@p red.relaxed.gpu.global.add.f64 [%0], %1;\n\t}" ::"l"(dst),
                          "d"(val), "r"((uint32_t)on));
