@@ -1717,9 +1717,39 @@ __device__ __forceinline__ double warp_sum_d(double v) {
  * (tbits cleared) and Σ c_new / #(c_new > 0) are reduced (field.cpp:201-214).  The stores'
  * bitmap words form one flat index space, each store's range padded to whole warps, so a warp
  * never straddles two stores; the c_new gathers of a word's set bits are issued 8 at a time. */
+__device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst);
+__device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst);
+__device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int finish);
+
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst,
                                                         const unsigned long long *guard) {
     if (guard && *guard) return; /* new keys still pending: the host places them first */
+    ef_reduce_body(st, nst);
+}
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst,
+                                                       const unsigned long long *guard) {
+    if (guard && *guard) return;
+    ef_blend_body(st, nst);
+}
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish,
+                                                       const unsigned long long *guard) {
+    if (guard && *guard) return;
+    ef_evict_body(st, nst, finish);
+}
+
+/* the three endFrame passes in one cooperative launch (grid barriers between them) */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_fused(Stores4 st, int nst,
+                                                       const unsigned long long *guard) {
+    if (guard && *guard) return; /* uniform across the grid: every block returns */
+    cg::grid_group g = cg::this_grid();
+    ef_reduce_body(st, nst);
+    g.sync();
+    ef_blend_body(st, nst);
+    g.sync();
+    ef_evict_body(st, nst, 1);
+}
+
+__device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst) {
     __shared__ double ssum[4][EF_BLOCK / 32];
     __shared__ unsigned long long scnt[4][EF_BLOCK / 32];
     uint64_t seg[4], nw[4];
@@ -1816,9 +1846,7 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_reduce(Stores4 st, int nst,
 
 /* endFrame pass 2 (field.cpp:216-246) over every store's touched list at once (one flat index
  * space), two entries per thread per iteration with their acc/com loads in flight together */
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst,
-                                                       const unsigned long long *guard) {
-    if (guard && *guard) return;
+__device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
     uint64_t seg[4];
     uint64_t total = 0;
 #pragma unroll
@@ -1887,9 +1915,7 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_blend(Stores4 st, int nst,
         if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
     }
 }
-__global__ void __launch_bounds__(EF_BLOCK) k_ef_evict(Stores4 st, int nst, int finish,
-                                                       const unsigned long long *guard) {
-    if (guard && *guard) return;
+__device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int finish) {
     if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
         const DevStore &s = st.s[threadIdx.x];
         s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
@@ -2902,7 +2928,21 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
     const unsigned long long *guard =
         owner ? owner->sc.pend_count.as<const unsigned long long>() : nullptr;
+    static int fused_blocks = -1; /* co-resident blocks per SM of the cooperative kernel */
+    if (fused_blocks < 0) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fused_blocks, k_ef_fused, EF_BLOCK, 0));
+        if (getenv("PSTF_NO_FUSED_EF")) fused_blocks = 0;
+    }
     auto launch = [&](const unsigned long long *gd) -> int {
+        if (fused_blocks > 0) { /* one cooperative launch: reduce | blend | evict */
+            unsigned gf = std::min<unsigned>(g, (unsigned)(sm_count() * fused_blocks));
+            int nn = n;
+            void *args[] = {&S, &nn, &gd};
+            ProfScope ps_("k_ef_fused", st);
+            CK(cudaLaunchCooperativeKernel((const void *)k_ef_fused, gf, EF_BLOCK, args, 0, st));
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            return PSTF_OK;
+        }
         LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, n, gd);
         LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, n, gd);
         LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, n, 1, gd); /* + the per-frame scratch roll */
