@@ -3293,19 +3293,21 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         b.pend = a.pend;
         b.pend_count = a.pend_count;
         b.pend_cap = a.pend_cap;
-        /* (stages, CTAs/SM): 1x4 (cfg 1, default) measured fastest on config 2; 2x3 (cfg 0,
-         * double buffering) and 1x5 (cfg 2, 96 registers) are slower, as were VT = 64 / 96,
+        /* (stages, CTAs/SM): 1x4 (cfg 1, default, 0.84 ms) measured fastest on config 2; 2x3
+         * (cfg 0, double buffering), 1x5 (cfg 2, 93 registers, no spills: 0.95 ms) and 1x3
+         * (cfg 3: 0.97 ms) are slower (fewer warps, or less L1 next to the stages), as were
+         * VT = 64 / 96,
          * L2-prefetch-only loads without staging, refilling the stage before the
          * contributions (mid-tile barrier, or last-warp refill without one), and two stage
          * groups refilled at different points of the tile. */
         const char *cfgs = getenv("PSTF_TILED_CFG");
-        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 2) : 1;
+        const int cfg = cfgs ? std::min(std::max(atoi(cfgs), 0), 3) : 1;
         const uint64_t tiles = (n + VT - 1) / VT;
         /* one 2-D tensor map over the 34 f64 fields when they sit at a uniform stride */
         CUtensorMap tm;
         memset(&tm, 0, sizeof(tm));
         bool tmap = false;
-        if (cfg == 1 && !getenv("PSTF_NO_TMAP")) {
+        if (cfg >= 1 && !getenv("PSTF_NO_TMAP")) {
             const long long stride = (const char *)ptrs[1] - (const char *)ptrs[0];
             bool uniform = stride > 0 && stride % 16 == 0 && (uint64_t)stride >= n * 8 &&
                            n < (1ull << 31);
@@ -3324,7 +3326,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             }
         }
         const int stages = cfg == 0 ? 2 : 1;
-        const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : 5;
+        const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : cfg == 2 ? 5 : 3;
         const size_t smem = stages * sizeof(TileStage) + 64;
         const bool cvf = cv && cfg == 1; /* the CV lookup fused into the default kernel */
         if (cv && !cvf)
@@ -3336,15 +3338,18 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             b.cv[2] = cv->b;
             b.cv_valid = cv->valid;
         }
-        const int fi = cfg == 0 ? 0 : cfg == 2 ? 1 : (tmap ? 3 : 2) + (cvf ? 2 : 0);
-        static bool attr[6] = {false, false, false, false, false, false};
+        const int fi = cfg == 0 ? 0 : cfg == 2 ? (tmap ? 6 : 1) : cfg == 3 ? 7
+                     : (tmap ? 3 : 2) + (cvf ? 2 : 0);
+        static bool attr[8] = {false, false, false, false, false, false, false, false};
         if (!attr[fi]) {
-            const void *fns[6] = {(const void *)k_vertex_pass_tiled<2, 3, false>,
+            const void *fns[8] = {(const void *)k_vertex_pass_tiled<2, 3, false>,
                                   (const void *)k_vertex_pass_tiled<1, 5, false>,
                                   (const void *)k_vertex_pass_tiled<1, VT_MINB, false>,
                                   (const void *)k_vertex_pass_tiled<1, VT_MINB, true>,
                                   (const void *)k_vertex_pass_tiled<1, VT_MINB, false, true>,
-                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, true, true>};
+                                  (const void *)k_vertex_pass_tiled<1, VT_MINB, true, true>,
+                                  (const void *)k_vertex_pass_tiled<1, 5, true>,
+                                  (const void *)k_vertex_pass_tiled<1, 3, true>};
             CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
             attr[fi] = true;
@@ -3356,6 +3361,8 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         case 2: LAUNCH((k_vertex_pass_tiled<1, 4, false>), grid, VT, smem, st, b, tm); break;
         case 3: LAUNCH((k_vertex_pass_tiled<1, 4, true>), grid, VT, smem, st, b, tm); break;
         case 4: LAUNCH((k_vertex_pass_tiled<1, 4, false, true>), grid, VT, smem, st, b, tm); break;
+        case 6: LAUNCH((k_vertex_pass_tiled<1, 5, true>), grid, VT, smem, st, b, tm); break;
+        case 7: LAUNCH((k_vertex_pass_tiled<1, 3, true>), grid, VT, smem, st, b, tm); break;
         default: LAUNCH((k_vertex_pass_tiled<1, 4, true, true>), grid, VT, smem, st, b, tm);
         }
         return PSTF_OK;
