@@ -42,9 +42,9 @@ class Collectives:
         """buf: 1-D uint8 tensor; returns the concatenation of every rank's buffer (rank order)."""
         import torch
         n = self._t([buf.numel()], dtype=torch.int64, device=self.device)
-        sizes = [torch.zeros_like(n) for _ in range(self.world)]
-        self.dist.all_gather(sizes, n)
-        sizes = [int(s.item()) for s in sizes]
+        sizes = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        self.dist.all_gather_into_tensor(sizes, n)
+        sizes = [int(x) for x in sizes.tolist()]  # one host round trip for all ranks
         mx = max(sizes)
         if mx == 0:
             return torch.empty(0, dtype=torch.uint8, device=self.device)
