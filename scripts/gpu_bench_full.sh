@@ -7,4 +7,4 @@ LCMD="python bench.py --no-e2e --no-cpu-baseline"
 timeout 300 $LCMD > gpurun_out/plain_l.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $LCMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
 CMD="python bench.py --steps 3 --warmup 3 --streams 2 --no-e2e --no-cpu-baseline"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_vertex_pass_tiled|k_ef_blend|k_ef_reduce" -s 9 -c 3 -o gpurun_out/full $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_vertex_pass_tiled|k_ef_fused" -s 6 -c 2 -o gpurun_out/full $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
