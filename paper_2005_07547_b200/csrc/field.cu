@@ -1634,8 +1634,12 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
     if (t == R_PROPOSE) {
         s.meta[slot].x = a.ucs[u]; /* (k_place_loop has released the slot's hold) */
         s.keyf[slot] = ukey[u];
-        atomicAdd(&s.ctr[C_LIVE], 1ull);
-        atomicAdd(&s.ctr[C_NEW_KEYS], 1ull);
+        /* live / new-key counters: one atomic per group of lanes of the same store */
+        const unsigned grp = __match_any_sync(__activemask(), a.usid[u]);
+        if ((int)lane_id() == __ffs(grp) - 1) {
+            atomicAdd(&s.ctr[C_LIVE], (unsigned long long)__popc(grp));
+            atomicAdd(&s.ctr[C_NEW_KEYS], (unsigned long long)__popc(grp));
+        }
     }
     if (atomic_mode) {
         double4 v = usum[u];
