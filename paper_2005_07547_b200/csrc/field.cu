@@ -2358,6 +2358,8 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
         if (rc) return rc;
         nu = ((uint32_t *)sc.h_small)[0];
     }
+    if (getenv("PSTF_DEBUG_PHASE2")) fprintf(stderr, "phase2: %llu records, %llu unique keys\n",
+                                            (unsigned long long)n, (unsigned long long)nu);
     ENSURE(sc.ufirst, nu * 4);
     ENSURE(sc.ukey, nu * sizeof(KeyFields));
     ENSURE(sc.ucs, nu * 4);
