@@ -209,7 +209,11 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
 /* Fused per-vertex pass: FieldRecorder::onVertex (estimators.cpp:194-262) for n vertices, i.e.
  * next-vertex Lo/LoE lookups on committed state, key generation, update values, and the
  * counter/accumulate updates into Lo, LoE, FLi (and Li when li != NULL).  Device pointers.
- * mode = PSTF_MODE_ATOMIC (fast) or PSTF_MODE_ORDERED (== EstimatorRun deterministic mode). */
+ * mode = PSTF_MODE_ATOMIC (fast) or PSTF_MODE_ORDERED (== EstimatorRun deterministic mode).
+ * Returns once phase 1 is enqueued on the stream: the placement of new keys (phase 2) is
+ * completed by the next entry point that touches one of these stores, and pstf_fields_end_frame
+ * on the same stream needs no host round trip when there are none (PSTF_NO_DEFER=1 places them
+ * before returning).  Results are identical either way. */
 int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
                      const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask, uint32_t fli_mask,
                      int mode, void *stream);
