@@ -2,6 +2,8 @@
 the reference itself (oracle/_ref).  Keys, levels, slot occupancy, probe placement, counters,
 ages and query results are compared bitwise; ORDERED/SEQUENTIAL modes are bitwise in values
 too; ATOMIC-mode values must agree within rtol 1e-9 (north star: 1e-5)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -341,6 +343,32 @@ def test_red_counter_and_peak():
     assert 0 < reds <= 2 * n * 4 * 4
     peak = pb.red_peak(0)
     assert 1e9 < peak < 1e13
+
+
+def test_deferred_phase2_identical(tmp_path):
+    """The deferred phase 2 (pstf_vertex_pass returns after phase 1; endFrame guarded by the
+    device-side pending count; other entry points settle first) gives the same stores, stats and
+    slot arrays as placing the new keys before returning (PSTF_NO_DEFER=1)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for env_extra in ({}, {"PSTF_NO_DEFER": "1"}):
+        out = str(tmp_path / f"d{len(outs)}.npz")
+        env = dict(os.environ, **env_extra)
+        r = subprocess.run([sys.executable, os.path.join(here, "defer_probe.py"), out], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs.append(np.load(out))
+    a, b = outs
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        if k.startswith("slots"):
+            sa = a[k].view(pb.SLOT_DTYPE)
+            sb = b[k].view(pb.SLOT_DTYPE)
+            gu.assert_slots_close(sa, sb, rtol=1e-9)
+        else:
+            np.testing.assert_array_equal(a[k], b[k])
 
 
 def test_vertex_pass_matches_reference_replay():
