@@ -756,9 +756,11 @@ __device__ __forceinline__ void issue_tile_tmap(const VPArgs2 &a, const CUtensor
 }
 
 __device__ __forceinline__ void prefetch_tile_tmap(const VPArgs2 &a, const CUtensorMap *tm,
-                                                   uint64_t tile) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tm),
-                 "r"((int)(tile * VT)), "r"(0)
+                                                   uint64_t tile, uint64_t policy) {
+    /* evict-first like the copies themselves: the prefetched stream must not push the hash
+     * tables' lines out of L2 */
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;"
+                 ::"l"(tm), "r"((int)(tile * VT)), "r"(0), "l"(policy)
                  : "memory");
     prefetch_l2(a.flags + tile * VT, VT * 4);
 }
@@ -1167,7 +1169,7 @@ __global__ void __launch_bounds__(VT, MINB)
             }
             for (int d = 1; d <= a.pf; ++d)
                 if (t + (uint64_t)d * gridDim.x < nfull) {
-                    if (TMAP) prefetch_tile_tmap(a, &tm, t + (uint64_t)d * gridDim.x);
+                    if (TMAP) prefetch_tile_tmap(a, &tm, t + (uint64_t)d * gridDim.x, policy);
                     else prefetch_tile(a, t + (uint64_t)d * gridDim.x);
                 }
         }
@@ -1194,7 +1196,7 @@ __global__ void __launch_bounds__(VT, MINB)
                 const uint64_t pt = nt + (uint64_t)a.pf * gridDim.x;
                 if (TMAP) {
                     issue_tile_tmap(a, &tm, &stages[s], &bars[s], nt, policy);
-                    if (pt < nfull) prefetch_tile_tmap(a, &tm, pt);
+                    if (pt < nfull) prefetch_tile_tmap(a, &tm, pt, policy);
                 } else {
                     issue_tile(a, &stages[s], &bars[s], nt, policy);
                     if (pt < nfull) prefetch_tile(a, pt);
