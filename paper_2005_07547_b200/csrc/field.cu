@@ -164,6 +164,7 @@ struct Scratch {
     DBuf ktmp0, ktmp1, perm0, perm1, cub;   // radix sort
     DBuf head, uid, ufirst, ukey, ucs, usid, uhome, ucalls, usum, ures0, ures1, rank, csr, useq;
     DBuf changed;
+    DBuf ddtab, rep_of, uidx, ukw, nudev;   // sort-free ATOMIC phase 2
     DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
     DBuf snap;                              // snapshot gather
     DBuf hio;                               // host-pointer API staging
@@ -199,6 +200,7 @@ struct pstf_field {
     std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
     int world = 1;      /* key-owner sharding */
     std::vector<uint32_t> sc_px_scan_copy;
+    DBuf hold64;                  /* 2 x capacity 64-bit priority holds (sort-free phase 2) */
     DeferredPass dp;              /* owned by the Lo store of a deferred vertex pass */
     pstf_field *owed_by = nullptr; /* the Lo store whose deferred pass involves this store */
     ~pstf_field() {
@@ -1522,7 +1524,31 @@ struct PlaceArgs {
     const uint32_t *rank;       // NULL -> rank = u
     const uint32_t *cs_by_rank; // checksum of the key holding rank r
     int parity;                 // which hold array is "prev"
+    const unsigned *nu_dev;     // unique count on the device (sort-free path), else NULL
 };
+
+__device__ __forceinline__ uint64_t place_nu(const PlaceArgs &a) {
+    return a.nu_dev ? (uint64_t)*a.nu_dev : a.nu;
+}
+
+/* sort-free ATOMIC phase 2: dedup hash table over the records' order-preserving key words */
+struct Dedup {
+    const uint64_t *words; /* words[i]: (store, level, cells, dirs) of record i, key order */
+    const uint32_t *tab;   /* open addressing, record index of the representative, ~0 empty */
+    uint32_t mask;
+    const PendRec *pend;
+};
+
+__device__ __forceinline__ uint32_t dd_hash(uint64_t w) { return (uint32_t)mix_bits(w); }
+
+/* checksum of the unique key whose key word is w (present in the table) */
+__device__ __forceinline__ uint32_t dd_checksum(const Dedup &d, uint64_t w) {
+    for (uint32_t h = dd_hash(w) & d.mask;; h = (h + 1) & d.mask) {
+        const uint32_t r = d.tab[h];
+        if (r == 0xffffffffu) return 0u; /* not reachable: every hold value is a present key */
+        if (d.words[r] == w) return d.pend[r].cs;
+    }
+}
 
 /* One key's step of a placement round (deferred acceptance over the frame-start table): the
  * first equal-checksum resident (FIXED), else the first slot held by a higher-priority key with
@@ -1622,10 +1648,169 @@ __global__ void __launch_bounds__(256) k_place_loop(PlaceArgs a, unsigned long l
     }
 }
 
+/* ---- sort-free ATOMIC phase 2 ------------------------------------------------------------ */
+/* every record finds (or becomes) the representative of its key word */
+__global__ void k_dd_insert(const uint64_t *words, uint64_t n, uint32_t *tab, uint32_t mask,
+                            uint32_t *rep_of) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t w = words[i];
+    for (uint32_t h = dd_hash(w) & mask;; h = (h + 1) & mask) {
+        uint32_t cur = tab[h];
+        if (cur == 0xffffffffu) {
+            cur = atomicCAS(&tab[h], 0xffffffffu, (uint32_t)i);
+            if (cur == 0xffffffffu) {
+                rep_of[i] = (uint32_t)i;
+                return;
+            }
+        }
+        if (words[cur] == w) {
+            rep_of[i] = cur;
+            return;
+        }
+    }
+}
+
+/* representatives become unique keys (unique ids in arbitrary order; priority = key word) */
+__global__ void k_dd_unique(const PendRec *pend, const uint64_t *words, const uint32_t *rep_of,
+                            uint64_t n, Stores4 st, UniqArgs u, uint64_t *ukw, uint32_t *uidx,
+                            unsigned *nu) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool rep = i < n && rep_of[i] == (uint32_t)i;
+    const unsigned m = __ballot_sync(0xffffffffu, rep);
+    if (!m) return;
+    unsigned base = 0;
+    if ((int)lane_id() == __ffs(m) - 1) base = atomicAdd(nu, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (!rep) return;
+    const uint32_t q = base + __popc(m & ((1u << lane_id()) - 1u));
+    uidx[i] = q;
+    const PendRec p = pend[i];
+    u.ufirst[q] = (uint32_t)i;
+    u.ukey[q] = KeyFields{p.k[0], p.k[1], p.k[2], p.k[3], p.k[4], p.k[5]};
+    u.ucs[q] = p.cs;
+    const uint32_t sid = PSTF_META_SID(p.meta);
+    u.usid[q] = sid;
+    u.uhome[q] = (uint32_t)pack_key_fields(p.k[0], p.k[1], p.k[2], p.k[3], p.k[4], p.k[5]) &
+                 st.s[sid].mask;
+    u.ucalls[q] = 0u;
+    u.usum[q] = make_double4(0.0, 0.0, 0.0, 0.0);
+    ukw[q] = words[i];
+}
+
+/* per-unique sums and call counts (ATOMIC: any order) */
+__global__ void k_dd_sums(const PendRec *pend, const uint32_t *rep_of, const uint32_t *uidx,
+                          uint64_t n, UniqArgs u, int own_origin) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const PendRec p = pend[i];
+    /* sharded: only this rank's records add values / count calls (see k_unique_sums) */
+    if (own_origin >= 0 && (int)PSTF_META_ORIGIN(p.meta) != own_origin) return;
+    const uint32_t q = uidx[rep_of[i]];
+    if (p.v[0] != 0.0) atomicAdd(&u.usum[q].x, p.v[0]);
+    if (p.v[1] != 0.0) atomicAdd(&u.usum[q].y, p.v[1]);
+    if (p.v[2] != 0.0) atomicAdd(&u.usum[q].z, p.v[2]);
+    if (p.v[3] != 0.0) atomicAdd(&u.usum[q].w, p.v[3]);
+    atomicAdd(&u.ucalls[q], PSTF_META_CALLS(p.meta));
+}
+
+/* placement with 64-bit key-word priorities: the same deferred acceptance as k_place_loop
+ * (sequential insertion in ascending key order), the holder of a slot identified by its key
+ * word, its checksum found through the dedup table */
+__device__ __forceinline__ unsigned long long place_step64(const PlaceArgs &a, const uint64_t *ukw,
+                                                           const Dedup &dd, uint64_t u,
+                                                           int parity) {
+    const DevStore &s = a.st.s[a.usid[u]];
+    const unsigned long long *hold_prev = parity ? s.hold64_1 : s.hold64_0;
+    const uint64_t r = ukw[u];
+    const uint32_t cs = a.ucs[u];
+    const uint32_t home = a.uhome[u];
+    for (uint32_t i0 = 0; i0 < s.window; i0 += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            c[j] = i0 + j < s.window ? s.meta[(home + i0 + j) & s.mask].x : 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (i0 + j >= s.window) return PSTF_RES(R_DROP, 0);
+            const uint32_t idx = (home + i0 + j) & s.mask;
+            if (c[j] != 0) {
+                if (c[j] == cs) return PSTF_RES(R_FIXED, idx); /* older resident (field.cpp:122) */
+                continue;
+            }
+            const unsigned long long h = hold_prev[idx];
+            if (h < r) {
+                if (dd_checksum(dd, h) == cs) return PSTF_RES(R_MERGE, idx); /* higher-priority twin */
+                continue;
+            }
+            return PSTF_RES(R_PROPOSE, idx);
+        }
+    }
+    return PSTF_RES(R_DROP, 0);
+}
+
+__device__ __forceinline__ unsigned long long *hold64(const DevStore &s, int which) {
+    return which ? s.hold64_1 : s.hold64_0;
+}
+
+__global__ void __launch_bounds__(256) k_place_loop64(PlaceArgs a, const uint64_t *ukw, Dedup dd,
+                                                      unsigned long long *r0,
+                                                      unsigned long long *r1, int *ctl,
+                                                      uint32_t max_rounds) {
+    cg::grid_group g = cg::this_grid();
+    const uint64_t tid0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t nu = place_nu(a);
+    int parity = a.parity;
+    unsigned long long *prev = r0, *next = r1;
+    uint32_t k = 0;
+    for (;; ++k) {
+        bool changed = false;
+        for (uint64_t u = tid0; u < nu; u += stride) {
+            const unsigned long long res = place_step64(a, ukw, dd, u, parity);
+            if (PSTF_RES_T(res) == R_PROPOSE)
+                atomicMin(&hold64(a.st.s[a.usid[u]], parity ^ 1)[PSTF_RES_SLOT(res)],
+                          (unsigned long long)ukw[u]);
+            next[u] = res;
+            changed |= res != prev[u];
+        }
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(&ctl[k & 1], 1);
+        g.sync();
+        for (uint64_t u = tid0; u < nu; u += stride) {
+            const unsigned long long res = prev[u];
+            if (PSTF_RES_T(res) == R_PROPOSE)
+                hold64(a.st.s[a.usid[u]], parity)[PSTF_RES_SLOT(res)] = ~0ull;
+        }
+        const int ch = *(volatile int *)&ctl[k & 1];
+        g.sync();
+        if (tid0 == 0) ctl[k & 1] = 0;
+        unsigned long long *t = prev;
+        prev = next;
+        next = t;
+        parity ^= 1;
+        if (!ch) break;
+        if (k + 1 > max_rounds) {
+            if (tid0 == 0) ctl[3] = 1;
+            break;
+        }
+    }
+    for (uint64_t u = tid0; u < nu; u += stride) {
+        const unsigned long long res = prev[u];
+        if (prev != r0) r0[u] = res;
+        if (PSTF_RES_T(res) == R_PROPOSE)
+            hold64(a.st.s[a.usid[u]], parity ^ 1)[PSTF_RES_SLOT(res)] = ~0ull;
+    }
+    if (tid0 == 0) {
+        ctl[2] = (int)(k + 1);
+        for (int i = 0; i < 4; ++i)
+            if (a.st.s[i].ctr) a.st.s[i].ctr[C_ROUNDS] = k + 1;
+    }
+}
+
 __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFields *ukey,
                          const uint32_t *ucalls, const double4 *usum, int atomic_mode) {
     uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (u >= a.nu) return;
+    if (u >= place_nu(a)) return;
     const DevStore &s = a.st.s[a.usid[u]];
     unsigned long long r = res[u];
     uint32_t t = PSTF_RES_T(r), slot = PSTF_RES_SLOT(r);
@@ -2269,6 +2454,91 @@ static int read_small(Scratch &sc, const void *dev, size_t bytes, cudaStream_t s
     return PSTF_OK;
 }
 
+/* Sort-free phase 2 for ATOMIC mode (one 64-bit key word per record): a dedup hash table
+ * groups the records by key, the unique keys take ids in any order, and the placement compares
+ * the order-preserving key words themselves (64-bit holds), which is the ascending-key priority
+ * the sorted path derives from its ranks.  No sort, no host round trip for the unique count. */
+static int phase2_atomic_fast(Scratch &sc, pstf_field *const *fs, int nf, uint64_t n,
+                              const PendRec *pend, int own_origin, cudaStream_t st) {
+    uint64_t T = 64;
+    while (T < 2 * n) T <<= 1;
+    ENSURE(sc.ddtab, T * 4);
+    ENSURE(sc.rep_of, n * 4);
+    ENSURE(sc.uidx, n * 4);
+    ENSURE(sc.ukw, n * 8);
+    ENSURE(sc.nudev, 16);
+    ENSURE(sc.ufirst, n * 4);
+    ENSURE(sc.ukey, n * sizeof(KeyFields));
+    ENSURE(sc.ucs, n * 4);
+    ENSURE(sc.usid, n * 4);
+    ENSURE(sc.uhome, n * 4);
+    ENSURE(sc.ucalls, n * 4);
+    ENSURE(sc.usum, n * sizeof(double4));
+    ENSURE(sc.ures0, n * 8);
+    ENSURE(sc.ures1, n * 8);
+    ENSURE(sc.changed, 16);
+    for (int i = 0; i < nf; ++i) { /* 64-bit holds, all "none" between passes */
+        pstf_field *f = fs[i];
+        if (!f || f->d.hold64_0) continue;
+        const uint64_t cap = (uint64_t)f->d.mask + 1;
+        CK(f->hold64.ensure(2 * cap * 8));
+        CK(cudaMemsetAsync(f->hold64.p, 0xff, 2 * cap * 8, st));
+        f->d.hold64_0 = f->hold64.as<unsigned long long>();
+        f->d.hold64_1 = f->hold64.as<unsigned long long>() + cap;
+    }
+    Stores4 S = stores4(fs, nf);
+    CK(cudaMemsetAsync(sc.ddtab.p, 0xff, T * 4, st));
+    CK(cudaMemsetAsync(sc.nudev.p, 0, 16, st));
+    UniqArgs U;
+    U.ufirst = sc.ufirst.as<uint32_t>();
+    U.ukey = sc.ukey.as<KeyFields>();
+    U.ucs = sc.ucs.as<uint32_t>();
+    U.usid = sc.usid.as<uint32_t>();
+    U.uhome = sc.uhome.as<uint32_t>();
+    U.ucalls = sc.ucalls.as<uint32_t>();
+    U.usum = sc.usum.as<double4>();
+    U.useq = nullptr;
+    const uint64_t *words = sc.words.as<uint64_t>();
+    LAUNCH(k_dd_insert, grid_for(n, 256), 256, 0, st, words, n, sc.ddtab.as<uint32_t>(),
+           (uint32_t)(T - 1), sc.rep_of.as<uint32_t>());
+    LAUNCH(k_dd_unique, grid_for(n, 256), 256, 0, st, pend, words,
+           (const uint32_t *)sc.rep_of.as<uint32_t>(), n, S, U, sc.ukw.as<uint64_t>(),
+           sc.uidx.as<uint32_t>(), sc.nudev.as<unsigned>());
+    LAUNCH(k_dd_sums, grid_for(n, 256), 256, 0, st, pend, (const uint32_t *)sc.rep_of.as<uint32_t>(),
+           (const uint32_t *)sc.uidx.as<uint32_t>(), n, U, own_origin);
+    PlaceArgs P;
+    memset(&P, 0, sizeof(P));
+    P.st = S;
+    P.nu = n; /* upper bound; the kernels read the count from nu_dev */
+    P.usid = U.usid;
+    P.uhome = U.uhome;
+    P.ucs = U.ucs;
+    P.parity = 0;
+    P.nu_dev = sc.nudev.as<unsigned>();
+    Dedup dd{words, sc.ddtab.as<uint32_t>(), (uint32_t)(T - 1), pend};
+    unsigned long long *r0 = sc.ures0.as<unsigned long long>(), *r1 = sc.ures1.as<unsigned long long>();
+    CK(cudaMemsetAsync(r0, 0, n * 8, st));
+    CK(cudaMemsetAsync(sc.changed.p, 0, 16, st));
+    {
+        static int blocks_per_sm = -1;
+        if (blocks_per_sm < 0) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_place_loop64, 256, 0));
+            blocks_per_sm = std::max(1, std::min(blocks_per_sm, 4));
+        }
+        const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(n, 256),
+                                                           (uint64_t)sm_count() * blocks_per_sm);
+        const uint64_t *ukw = sc.ukw.as<uint64_t>();
+        int *ctl = sc.changed.as<int>();
+        uint32_t max_rounds = (uint32_t)std::min<uint64_t>(n + 2, 0x7fffffffu);
+        void *args[] = {&P, &ukw, &dd, &r0, &r1, &ctl, &max_rounds};
+        ProfScope ps_("k_place_loop64", st);
+        CK(cudaLaunchCooperativeKernel((const void *)k_place_loop64, grid, 256, args, 0, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    LAUNCH(k_commit, grid_for(n, 256), 256, 0, st, P, r0, U.ukey, U.ucalls, U.usum, 1);
+    return PSTF_OK;
+}
+
 /* Phase 2 for the records sitting in sc.pend (count on device in sc.pend_count).
  * fs[0..nf) are the stores addressed by record store ids. */
 static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode, uint64_t n_known,
@@ -2333,6 +2603,9 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
 
     ENSURE(sc.words, (size_t)L.nwords * n * 8);
     LAUNCH(k_encode, grid_for(n, 256), 256, 0, st, pend, seq, n, L, sc.words.as<uint64_t>());
+    static const bool no_fast = getenv("PSTF_NO_FAST_PHASE2") != nullptr;
+    if (mode == PSTF_MODE_ATOMIC && L.nwords == 1 && !no_fast)
+        return phase2_atomic_fast(sc, fs, nf, n, pend, own_origin, st);
     uint32_t *perm = nullptr;
     {
         int rc = sort_multiword(sc, sc.words.as<uint64_t>(), L.begin_bit, L.nwords, n, &perm, st);
@@ -2394,6 +2667,7 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
 
     /* 3. priority ranks */
     PlaceArgs P;
+    memset(&P, 0, sizeof(P));
     P.st = S;
     P.nu = nu;
     P.usid = U.usid;

@@ -51,6 +51,8 @@ struct DevStore {
     uint32_t *tbits;
     uint32_t *tlist;
     uint32_t *hold0, *hold1;
+    unsigned long long *hold64_0, *hold64_1; /* 64-bit priority holds (sort-free ATOMIC phase 2),
+                                                allocated on first use, ~0 = none */
     unsigned long long *ctr; // C_NUM counters
     double *cn_sum;          // endFrame scratch
     uint32_t mask;
