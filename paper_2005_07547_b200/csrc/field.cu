@@ -196,7 +196,6 @@ struct pstf_field {
     uint32_t *hold[2] = {nullptr, nullptr};
     void *arena = nullptr;
     Scratch sc;
-    uint64_t new_keys_last = 0, rounds_last = 0;
     std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
     int world = 1;      /* key-owner sharding */
     std::vector<uint32_t> sc_px_scan_copy;
@@ -2551,7 +2550,6 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     }
     for (int i = 0; i < nf; ++i)
         if (fs[i]) {
-            fs[i]->new_keys_last = 0;
             CK(cudaMemsetAsync(&fs[i]->d.ctr[C_NEW_KEYS], 0, 8, st));
             CK(cudaMemsetAsync(&fs[i]->d.ctr[C_ROUNDS], 0, 8, st));
         }
