@@ -198,7 +198,6 @@ struct pstf_field {
     Scratch sc;
     std::mutex host_mu; /* serialises the host-pointer (scalar facade) entry points */
     int world = 1;      /* key-owner sharding */
-    std::vector<uint32_t> sc_px_scan_copy;
     DBuf hold64;                  /* 2 x capacity 64-bit priority holds (sort-free phase 2) */
     DeferredPass dp;              /* owned by the Lo store of a deferred vertex pass */
     pstf_field *owed_by = nullptr; /* the Lo store whose deferred pass involves this store */
@@ -3950,28 +3949,38 @@ int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t
     cudaStream_t st = (cudaStream_t)stream;
     const int world = stores[0]->world;
     Scratch &sc = stores[0]->sc;
-    /* per store: word popcounts -> scan -> per-destination counts */
-    std::vector<std::vector<uint64_t>> cnt(nst, std::vector<uint64_t>(world, 0));
+    /* per store: word popcounts -> exclusive scan, all stores side by side on the device; only
+     * the scan values at the rank boundaries come back to the host (one round trip) */
+    std::vector<uint64_t> nw(nst), off(nst + 1, 0);
+    for (int j = 0; j < nst; ++j) {
+        nw[j] = ((uint64_t)stores[j]->d.mask + 1) / 32;
+        off[j + 1] = off[j] + nw[j] + 1;
+    }
+    ENSURE(sc.head, off[nst] * 4);
+    ENSURE(sc.uid, off[nst] * 4);
+    ENSURE(sc.ranges, (size_t)nst * (world + 1) * 8 + 64);
+    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+    if ((size_t)nst * (world + 1) * 4 > 4096) return set_err(PSTF_E_INVALID, "world too large");
+    uint32_t *hb = reinterpret_cast<uint32_t *>(sc.h_small);
     for (int j = 0; j < nst; ++j) {
         DevStore s = dev_view(stores[j]);
-        const uint64_t nwords = ((uint64_t)s.mask + 1) / 32;
-        ENSURE(sc.head, (nwords + 1) * 4);
-        ENSURE(sc.uid, (nwords + 1) * 4);
-        LAUNCH(k_px_count, grid_for(nwords + 1, 256), 256, 0, st, s, sc.head.as<uint32_t>(), nwords);
+        uint32_t *h = sc.head.as<uint32_t>() + off[j], *u = sc.uid.as<uint32_t>() + off[j];
+        LAUNCH(k_px_count, grid_for(nw[j] + 1, 256), 256, 0, st, s, h, nw[j]);
         size_t bytes = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sc.head.as<uint32_t>(),
-                                         sc.uid.as<uint32_t>(), (int64_t)(nwords + 1), st));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, h, u, (int64_t)(nw[j] + 1), st));
         ENSURE(sc.cub, bytes);
         bytes = sc.cub.bytes;
-        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, sc.head.as<uint32_t>(),
-                                         sc.uid.as<uint32_t>(), (int64_t)(nwords + 1), st));
-        std::vector<uint32_t> hs(nwords + 1);
-        CK(cudaMemcpyAsync(hs.data(), sc.uid.p, (nwords + 1) * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        const uint64_t wpr = nwords / (uint64_t)world;
-        for (int r = 0; r < world; ++r) cnt[j][r] = hs[(r + 1) * wpr] - hs[r * wpr];
-        stores[j]->sc_px_scan_copy = hs; /* kept for the write pass (scratch is reused) */
+        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, h, u, (int64_t)(nw[j] + 1), st));
+        const uint64_t wpr = nw[j] / (uint64_t)world;
+        for (int r = 0; r <= world; ++r) /* scan value at each rank's first word */
+            CK(cudaMemcpyAsync(hb + j * (world + 1) + r, u + (uint64_t)r * wpr, 4,
+                               cudaMemcpyDeviceToHost, st));
     }
+    CK(cudaStreamSynchronize(st));
+    std::vector<std::vector<uint64_t>> cnt(nst, std::vector<uint64_t>(world, 0));
+    for (int j = 0; j < nst; ++j)
+        for (int r = 0; r < world; ++r)
+            cnt[j][r] = hb[j * (world + 1) + r + 1] - hb[j * (world + 1) + r];
     uint64_t total = 0;
     for (int r = 0; r < world; ++r) {
         counts[r] = 0;
@@ -3981,28 +3990,21 @@ int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t
     if (total > cap) return set_err(PSTF_E_NOMEM, "partials buffer too small");
     std::vector<uint64_t> rbase(world, 0);
     for (int r = 1; r < world; ++r) rbase[r] = rbase[r - 1] + counts[r - 1];
-    ENSURE(sc.ranges, (size_t)world * 8 + 64);
-    for (int j = 0; j < nst; ++j) {
-        DevStore s = dev_view(stores[j]);
-        const uint64_t nwords = ((uint64_t)s.mask + 1) / 32;
-        std::vector<unsigned long long> db(world);
+    std::vector<unsigned long long> db((size_t)nst * world);
+    for (int j = 0; j < nst; ++j)
         for (int r = 0; r < world; ++r) {
             uint64_t b = rbase[r];
             for (int jj = 0; jj < j; ++jj) b += cnt[jj][r];
-            db[r] = b;
+            db[(size_t)j * world + r] = b;
         }
-        /* rescan this store (the scratch was reused by the next store) */
-        ENSURE(sc.head, (nwords + 1) * 4);
-        ENSURE(sc.uid, (nwords + 1) * 4);
-        CK(cudaMemcpyAsync(sc.uid.p, stores[j]->sc_px_scan_copy.data(), (nwords + 1) * 4,
-                           cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(sc.ranges.p, db.data(), world * 8, cudaMemcpyHostToDevice, st));
-        LAUNCH(k_px_write, grid_for(nwords, 256), 256, 0, st, s, (uint32_t)j, sc.uid.as<uint32_t>(),
-               nwords, nwords / (uint64_t)world, sc.ranges.as<unsigned long long>(),
-               (PartialRec *)out);
-        CK(cudaStreamSynchronize(st));
-        stores[j]->sc_px_scan_copy.clear();
+    CK(cudaMemcpyAsync(sc.ranges.p, db.data(), db.size() * 8, cudaMemcpyHostToDevice, st));
+    for (int j = 0; j < nst; ++j) {
+        DevStore s = dev_view(stores[j]);
+        LAUNCH(k_px_write, grid_for(nw[j], 256), 256, 0, st, s, (uint32_t)j,
+               sc.uid.as<uint32_t>() + off[j], nw[j], nw[j] / (uint64_t)world,
+               sc.ranges.as<unsigned long long>() + (size_t)j * world, (PartialRec *)out);
     }
+    CK(cudaStreamSynchronize(st)); /* db (pageable) and the caller's counts are consumed */
     return PSTF_OK;
 }
 
