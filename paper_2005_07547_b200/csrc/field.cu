@@ -4035,12 +4035,17 @@ int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, v
     const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
     LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, stores4(stores, nst), nst,
            (const unsigned long long *)nullptr);
+    Scratch &sc = stores[0]->sc;
+    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+    for (int i = 0; i < nst; ++i) { /* all values in one round trip */
+        CK(cudaMemcpyAsync(&sc.h_small[2 * i], stores[i]->d.cn_sum, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&sc.h_small[2 * i + 1], &stores[i]->d.ctr[C_CN_COUNT], 8,
+                           cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     for (int i = 0; i < nst; ++i) {
-        unsigned long long c = 0;
-        CK(cudaMemcpy(&sum_cnt[2 * i], stores[i]->d.cn_sum, 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(&c, &stores[i]->d.ctr[C_CN_COUNT], 8, cudaMemcpyDeviceToHost));
-        sum_cnt[2 * i + 1] = (double)c;
+        memcpy(&sum_cnt[2 * i], &sc.h_small[2 * i], 8);
+        sum_cnt[2 * i + 1] = (double)sc.h_small[2 * i + 1];
     }
     return PSTF_OK;
 }
@@ -4054,11 +4059,14 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     Scratch &sc = stores[0]->sc;
+    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+    unsigned long long *hv = sc.h_small + 256; /* pinned staging, consumed before the final sync */
     for (int i = 0; i < nst; ++i) { /* the batch-wide mean c_new of pass 1 */
-        unsigned long long c = (unsigned long long)global_sum_cnt[2 * i + 1];
-        CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &global_sum_cnt[2 * i], 8, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &c, 8, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
+        memcpy(&hv[2 * i], &global_sum_cnt[2 * i], 8);
+        hv[2 * i + 1] = (unsigned long long)global_sum_cnt[2 * i + 1];
+        CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &hv[2 * i], 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &hv[2 * i + 1], 8,
+                           cudaMemcpyHostToDevice, st));
     }
     uint64_t maxcap = 0;
     for (int i = 0; i < nst; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
@@ -4081,9 +4089,9 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
     if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0, (const unsigned long long *)nullptr);
     LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
     for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
-    unsigned long long nd = 0;
-    CK(cudaMemcpyAsync(&nd, dcount, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(sc.h_small, dcount, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    const unsigned long long nd = sc.h_small[0];
     if (out && nd > cap) return set_err(PSTF_E_NOMEM, "deltas buffer overflow");
     *ndeltas = nd;
     return PSTF_OK;
