@@ -293,6 +293,12 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
                           void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
 int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,
                        void *stream);
+/* Same two steps with the (sum c_new, count) pairs in DEVICE memory (2*nst doubles), so the
+ * all-reduce between them needs no host round trip. */
+int pstf_end_frame_reduce_dev(pstf_field *const *stores, int nst, double *dev_sum_count,
+                              void *stream);
+int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *dev_sum_count,
+                              void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
 uint64_t pstf_pending_record_bytes(void); /* 64 */
 uint64_t pstf_partial_record_bytes(void); /* 40: {u32 store, u32 slot, f64 acc[4]} */
 uint64_t pstf_delta_record_bytes(void);   /* 48: {u32 store, slot, checksum, last+1; f64 com[4]} */

@@ -4020,6 +4020,45 @@ int pstf_partials_import(pstf_field *const *stores, int nst, const void *recs, u
     return PSTF_OK;
 }
 
+}  /* extern "C" (kernels below) */
+
+__global__ void k_sums_out(Stores4 st, int nst, double *out) {
+    const int i = threadIdx.x;
+    if (i < nst) {
+        out[2 * i] = *st.s[i].cn_sum;
+        out[2 * i + 1] = (double)st.s[i].ctr[C_CN_COUNT];
+    }
+}
+__global__ void k_sums_in(Stores4 st, int nst, const double *in) {
+    const int i = threadIdx.x;
+    if (i < nst) {
+        *st.s[i].cn_sum = in[2 * i];
+        st.s[i].ctr[C_CN_COUNT] = (unsigned long long)in[2 * i + 1];
+    }
+}
+
+extern "C" {
+
+int pstf_end_frame_reduce_dev(pstf_field *const *stores, int nst, double *dev_sum_count,
+                              void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!dev_sum_count) return set_err(PSTF_E_INVALID, "NULL sum_count");
+    CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t maxcap = 0;
+    for (int i = 0; i < nst; ++i) {
+        maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
+        CK(cudaMemsetAsync(&stores[i]->d.ctr[C_EVICTED], 0, 8, st));
+    }
+    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
+    const Stores4 S = stores4(stores, nst);
+    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, nst, (const unsigned long long *)nullptr);
+    LAUNCH(k_sums_out, 1, 32, 0, st, S, nst, dev_sum_count);
+    return PSTF_OK;
+}
+
 int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
@@ -4050,23 +4089,28 @@ int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, v
     return PSTF_OK;
 }
 
-int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_cnt,
-                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
+static int end_frame_commit_impl(pstf_field *const *stores, int nst, const double *host_sums,
+                                 const double *dev_sums, void *deltas, uint64_t cap,
+                                 uint64_t *ndeltas, void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if (!global_sum_cnt || !ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
+    if ((!host_sums && !dev_sums) || !ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
     Scratch &sc = stores[0]->sc;
     if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
-    unsigned long long *hv = sc.h_small + 256; /* pinned staging, consumed before the final sync */
-    for (int i = 0; i < nst; ++i) { /* the batch-wide mean c_new of pass 1 */
-        memcpy(&hv[2 * i], &global_sum_cnt[2 * i], 8);
-        hv[2 * i + 1] = (unsigned long long)global_sum_cnt[2 * i + 1];
-        CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &hv[2 * i], 8, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &hv[2 * i + 1], 8,
-                           cudaMemcpyHostToDevice, st));
+    if (dev_sums) { /* the batch-wide mean c_new of pass 1, straight from the device */
+        LAUNCH(k_sums_in, 1, 32, 0, st, stores4(stores, nst), nst, dev_sums);
+    } else {
+        unsigned long long *hv = sc.h_small + 256; /* pinned staging, used before the sync */
+        for (int i = 0; i < nst; ++i) {
+            memcpy(&hv[2 * i], &host_sums[2 * i], 8);
+            hv[2 * i + 1] = (unsigned long long)host_sums[2 * i + 1];
+            CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &hv[2 * i], 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &hv[2 * i + 1], 8,
+                               cudaMemcpyHostToDevice, st));
+        }
     }
     uint64_t maxcap = 0;
     for (int i = 0; i < nst; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
@@ -4095,6 +4139,18 @@ int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *glob
     if (out && nd > cap) return set_err(PSTF_E_NOMEM, "deltas buffer overflow");
     *ndeltas = nd;
     return PSTF_OK;
+}
+
+int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_cnt,
+                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
+    return end_frame_commit_impl(stores, nst, global_sum_cnt, nullptr, deltas, cap, ndeltas,
+                                 stream);
+}
+
+int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *dev_sum_count,
+                              void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
+    return end_frame_commit_impl(stores, nst, nullptr, dev_sum_count, deltas, cap, ndeltas,
+                                 stream);
 }
 
 int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,

@@ -68,7 +68,12 @@ class Collectives:
         return out, recv_counts
 
     def all_reduce_sum(self, arr):
+        """Sum over ranks: a device tensor is reduced in place (no host round trip), anything
+        else goes through a float64 device tensor and comes back as numpy."""
         import torch
+        if isinstance(arr, torch.Tensor) and arr.device.type == "cuda":
+            self.dist.all_reduce(arr)
+            return arr
         t = torch.as_tensor(np.asarray(arr, np.float64), device=self.device)
         self.dist.all_reduce(t)
         return t.cpu().numpy()
@@ -126,6 +131,8 @@ class CudaBackend:
             "pstf_partials_import": [vp, i32, vp, u64, vp],
             "pstf_end_frame_reduce": [vp, i32, vp, vp],
             "pstf_end_frame_commit": [vp, i32, vp, vp, u64, vp, vp],
+            "pstf_end_frame_reduce_dev": [vp, i32, vp, vp],
+            "pstf_end_frame_commit_dev": [vp, i32, vp, vp, u64, vp, vp],
             "pstf_deltas_import": [vp, i32, vp, u64, vp], "pstf_shard_set": [vp, i32, i32],
         }.items():
             fn = getattr(L, name)
@@ -178,22 +185,31 @@ class CudaBackend:
                                                       self.F._stream()))
 
     def end_frame_reduce(self):
-        sums = np.zeros(2 * len(self.stores))
-        self.F._check(self.L.pstf_end_frame_reduce(self._arr, len(self.stores),
-                                                   sums.ctypes.data_as(C.c_void_p),
-                                                   self.F._stream()))
+        """(sum c_new, count) per store as a device tensor (all-reduced in place next)"""
+        torch = self._torch()
+        sums = torch.empty(2 * len(self.stores), dtype=torch.float64, device="cuda")
+        self.F._check(self.L.pstf_end_frame_reduce_dev(self._arr, len(self.stores),
+                                                       C.c_void_p(sums.data_ptr()),
+                                                       self.F._stream()))
         return sums
 
     def end_frame_commit(self, sums):
         torch = self._torch()
-        sums = np.ascontiguousarray(sums, np.float64)
         cap = sum(s.capacity for s in self.stores) // self.world
         out = torch.empty(max(cap, 1) * DELTA_BYTES, dtype=torch.uint8, device="cuda")
         nd = C.c_uint64()
-        self.F._check(self.L.pstf_end_frame_commit(self._arr, len(self.stores),
-                                                   sums.ctypes.data_as(C.c_void_p),
-                                                   C.c_void_p(out.data_ptr()), max(cap, 1),
-                                                   C.byref(nd), self.F._stream()))
+        if isinstance(sums, torch.Tensor) and sums.device.type == "cuda":
+            sums = sums.to(torch.float64).contiguous()
+            self.F._check(self.L.pstf_end_frame_commit_dev(self._arr, len(self.stores),
+                                                           C.c_void_p(sums.data_ptr()),
+                                                           C.c_void_p(out.data_ptr()), max(cap, 1),
+                                                           C.byref(nd), self.F._stream()))
+        else:
+            sums = np.ascontiguousarray(sums, np.float64)
+            self.F._check(self.L.pstf_end_frame_commit(self._arr, len(self.stores),
+                                                       sums.ctypes.data_as(C.c_void_p),
+                                                       C.c_void_p(out.data_ptr()), max(cap, 1),
+                                                       C.byref(nd), self.F._stream()))
         return out[:nd.value * DELTA_BYTES]
 
     def deltas_import(self, recs):
