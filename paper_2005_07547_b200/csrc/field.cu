@@ -2195,8 +2195,17 @@ __global__ void k_px_import(Stores4 st, const PartialRec *recs, uint64_t n) {
 /* after the blend: every slot of the touched list (all owned) becomes a delta */
 __global__ void k_dx_touched(DevStore s, uint32_t sid, DeltaRec *out, unsigned long long *count) {
     const uint64_t n = s.ctr[C_TOUCHED_N];
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    /* warp-uniform trip count: one output reservation per warp */
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+         i0 += stride) {
+        const uint64_t i = i0 + lane_id();
+        const bool live = i < n;
+        const unsigned wm = __ballot_sync(0xffffffffu, live);
+        unsigned long long base = 0;
+        if (lane_id() == 0) base = atomicAdd(count, (unsigned long long)__popc(wm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (!live) continue;
         const uint32_t slot = s.tlist[i];
         const uint2 m = s.meta[slot];
         const double4 c = s.com[slot];
@@ -2209,7 +2218,7 @@ __global__ void k_dx_touched(DevStore s, uint32_t sid, DeltaRec *out, unsigned l
         d.com[1] = c.y;
         d.com[2] = c.z;
         d.com[3] = c.w;
-        out[atomicAdd(count, 1ull)] = d;
+        out[base + __popc(wm & ((1u << lane_id()) - 1u))] = d;
     }
 }
 
