@@ -48,11 +48,16 @@ class Collectives:
         mx = max(sizes)
         if mx == 0:
             return torch.empty(0, dtype=torch.uint8, device=self.device)
-        pad = torch.zeros(mx, dtype=torch.uint8, device=self.device)
-        pad[:buf.numel()] = buf
-        outs = [torch.empty(mx, dtype=torch.uint8, device=self.device) for _ in range(self.world)]
-        self.dist.all_gather(outs, pad)
-        return torch.cat([o[:s] for o, s in zip(outs, sizes)])
+        if buf.numel() == mx:
+            pad = buf.contiguous()
+        else:
+            pad = torch.zeros(mx, dtype=torch.uint8, device=self.device)
+            pad[:buf.numel()] = buf
+        out = torch.empty(self.world * mx, dtype=torch.uint8, device=self.device)
+        self.dist.all_gather_into_tensor(out, pad)  # one contiguous collective
+        if all(sz == mx for sz in sizes):
+            return out
+        return torch.cat([out[r * mx:r * mx + sz] for r, sz in enumerate(sizes)])
 
     def all_to_all_bytes(self, buf, send_counts, rec_bytes):
         """buf holds world consecutive segments of send_counts[r] records (rec_bytes each)."""
