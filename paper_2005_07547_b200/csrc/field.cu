@@ -674,7 +674,7 @@ struct TileStage {
 struct VPArgs2 {
     Stores4 st;
     FastParams fp;
-    int dbg; /* experiment switches (PSTF_VP_DBG): 1 no lookups, 2 no RED, 4 keys only */
+    int dbg; /* unused: the experiment switches are compile-time (PSTF_VP_DBG_BUILD) */
     int pf;  /* L2 prefetch distance in tiles of this CTA (PSTF_VP_PF, default 1) */
     int has_li;
     uint32_t loe_mask, fli_mask;
@@ -3570,7 +3570,6 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         memset(&b, 0, sizeof(b));
         b.st = a.st;
         b.fp = make_fast_params(lo->d.kp);
-        b.dbg = getenv("PSTF_VP_DBG") ? atoi(getenv("PSTF_VP_DBG")) : 0;
         b.pf = getenv("PSTF_VP_PF") ? std::max(0, atoi(getenv("PSTF_VP_PF"))) : 1;
         b.has_li = a.has_li;
         b.loe_mask = loe_mask;
