@@ -302,6 +302,7 @@ def run_b200(args):
         dist.barrier()
     touched0 = sum(s.stats()["touched_total"] for s in stores)
     reds0 = stores[0].stats()["reds_total"]
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size  # cudaDevAttrL2CacheSize
     dropped0 = [s.stats()["dropped"] for s in stores]
     launches0 = pb.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -384,13 +385,15 @@ def run_b200(args):
                             "2^20 slots (eviction engages), inputs regenerated untimed"}[args.config],
             "vertices_per_iter": n, "capacity_log2": args.capacity_log2, "stores": 3,
             "mode": args.mode, "iteration_streams": S,
-            "l2": "inputs larger than L2 (2.29 GB per iteration stream, %d streams cycled)" % S,
+            "l2": "inputs larger than L2 (%.2f GB per iteration stream vs %d MB L2 read from the "
+                  "device, %d streams cycled)" % (BYTES_PER_VERTEX * n / 1e9, l2_bytes >> 20, S),
             "parallelism": "single GPU" if world == 1 else
                            f"{world} ranks, 1 spp of the 1080p frame each (weak scaling), one "
                            f"field cache sharded by key owner (NCCL all-gather / all-to-all)",
         },
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "spec_peak": 8000.0, "frac_of_spec": ach / 8000.0,
                      "frac": ach / peak, "traffic": traffic,
                      "kernel": vp[0][0] if vp else None,
                      "bytes_per_launch": vp_bytes, "avg_launch_ms": vp_avg,
