@@ -3,7 +3,7 @@
 // either against the reference's own field.cpp (CPU) or against the B200 drop-in facade
 // (paper_2005_07547_b200/cxx).  Writes the Lo, Lo\E and FLi field snapshots and the image after
 // N frames, so the two builds can be compared byte for byte.
-//   config1_{ref,b200} <scene> <size> <frames> <out-prefix>
+//   config1_{ref,b200} <scene> <size> <frames> <out-prefix> [estimator: cv | is | is-cv | b]
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -24,6 +24,10 @@ int main(int argc, char **argv) {
     scene.camera.height = size;
     pstf::EstimatorConfig c;
     c.kind = pstf::EstimatorKind::CV;
+    if (argc > 5 && !pstf::parseEstimatorKind(argv[5], c.kind)) {
+        std::fprintf(stderr, "unknown estimator %s\n", argv[5]);
+        return 2;
+    }
     c.deterministic = true;
     c.threads = 4;
     c.seed = 7;
