@@ -203,6 +203,16 @@ int pstf_field_dump_snapshot(pstf_field *f, const char *path);
 int pstf_read_snapshot(const char *path, pstf_snapshot_record *records, uint64_t cap,
                        uint64_t *count, uint32_t *kind);
 
+/* Snapshot restore (the reference writes snapshots, field.cpp:311-386, but
+ * has no restore).  records: host array, any order; each checksum must match its key
+ * (field.cpp:98-99), else PSTF_E_FORMAT and the store is unchanged.  Semantics, in ascending key
+ * order (stable): findOrInsertSlot(key) (field.cpp:116-146: lastTouched = frame, a full window
+ * counts one droppedInserts), then valueOld = value, cOld = c_old at the slot it returned; of
+ * several records resolving to one slot the last wins.  accum/cNew are untouched.  Synchronous. */
+int pstf_field_restore(pstf_field *f, const pstf_snapshot_record *records, uint64_t n);
+/* readSnapshot(path) + pstf_field_restore; PSTF_E_FORMAT when the file's kind is not the store's */
+int pstf_field_load_snapshot(pstf_field *f, const char *path);
+
 /* Slot-array dump (host) of slots [begin, begin+count) for occupancy parity. */
 int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_record *out);
 

@@ -365,6 +365,44 @@ size_t po_snapshot(const po_store *s, po_snapshot_record *out, size_t cap) {
     return m;
 }
 
+/* Snapshot restore (no reference counterpart: field.cpp:311-386 only writes/reads the file; the
+ * semantics are those of include/pstf_field.h pstf_field_restore).  Records in ascending key
+ * order (stable: ties keep input order), each inserted by findOrInsertSlot (field.cpp:116-146),
+ * then valueOld/cOld set at the slot it returned; later records overwrite earlier ones. */
+typedef struct {
+    const po_snapshot_record *r;
+    size_t i;
+} po_snap_ref;
+
+static int po_snap_ref_cmp(const void *pa, const void *pb) {
+    const po_snap_ref *a = (const po_snap_ref *)pa, *b = (const po_snap_ref *)pb;
+    int c = po_snap_cmp(a->r, b->r);
+    if (c) return c;
+    return a->i < b->i ? -1 : (a->i > b->i ? 1 : 0);
+}
+
+void po_restore(po_store *s, const po_snapshot_record *recs, size_t n) {
+    po_snap_ref *ord = (po_snap_ref *)malloc((n ? n : 1) * sizeof(po_snap_ref));
+    for (size_t i = 0; i < n; ++i) {
+        ord[i].r = &recs[i];
+        ord[i].i = i;
+    }
+    qsort(ord, n, sizeof(po_snap_ref), po_snap_ref_cmp);
+    for (size_t j = 0; j < n; ++j) {
+        const po_snapshot_record *r = ord[j].r;
+        po_key k;
+        k.level = r->level;
+        memcpy(k.cell, r->cell, sizeof(k.cell));
+        memcpy(k.dir, r->dir, sizeof(k.dir));
+        k.checksum = r->checksum;
+        int idx = po_find_or_insert(s, &k);
+        if (idx < 0) continue;
+        memcpy(s->slots[idx].value_old, r->value, sizeof(r->value));
+        s->slots[idx].c_old = r->c_old;
+    }
+    free(ord);
+}
+
 static uint64_t po_bits(double v) {
     uint64_t b;
     memcpy(&b, &v, sizeof(b));

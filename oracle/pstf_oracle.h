@@ -107,6 +107,8 @@ void po_weighted_mean(const po_store *s, double out[3]);
 void po_slots(const po_store *s, po_slot *out);
 /* key-sorted live records (field.cpp:311-337); returns the count written (<= cap) */
 size_t po_snapshot(const po_store *s, po_snapshot_record *out, size_t cap);
+/* snapshot restore, the semantics of pstf_field_restore (include/pstf_field.h) */
+void po_restore(po_store *s, const po_snapshot_record *recs, size_t n);
 
 /* FieldUpdateQueue::apply (field.cpp:396-420): sorts in place, then applies sequentially */
 void po_queue_apply(po_store *s, po_update *updates, size_t n);

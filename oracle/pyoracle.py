@@ -110,6 +110,7 @@ def oracle_lib():
         lib.po_slots.argtypes = [vp, vp]
         lib.po_snapshot.argtypes = [vp, vp, sz]
         lib.po_snapshot.restype = sz
+        lib.po_restore.argtypes = [vp, vp, sz]
         lib.po_queue_apply.argtypes = [vp, vp, sz]
         lib.po_vertex_pass_contig.argtypes = [vp, vp, vp, vp, vp, sz, u32, u32, i32]
         lib.po_synth_generate.argtypes = [i32, i32, i32, u64, u64, d, vp, i32]
@@ -150,6 +151,7 @@ def ref_lib():
         lib.pr_dump_snapshot.argtypes = [vp, C.c_char_p]
         lib.pr_dump_snapshot.restype = i32
         lib.pr_slots.argtypes = [vp, vp]
+        lib.pr_restore.argtypes = [vp, vp, i64]
         lib.pr_queue_create.restype = vp
         lib.pr_queue_destroy.argtypes = [vp]
         lib.pr_queue_push_counter.argtypes = [vp, vp, d]
@@ -284,6 +286,11 @@ class OracleStore(_StoreBase):
         n = self.lib.po_snapshot(self.h, _p(out), live)
         return out[:n]
 
+    def restore(self, records):
+        """snapshot restore (pstf_field_restore semantics, oracle/pstf_oracle.c po_restore)"""
+        r = np.ascontiguousarray(records, SNAP_DTYPE)
+        self.lib.po_restore(self.h, _p(r), len(r))
+
     def queue_apply(self, updates):
         u = np.ascontiguousarray(updates.copy())
         self.lib.po_queue_apply(self.h, _p(u), len(u))
@@ -389,6 +396,11 @@ class RefStore(_StoreBase):
         with tempfile.NamedTemporaryFile(suffix=".snap") as f:
             self.dump_snapshot(f.name)
             return read_snapshot(f.name)[1]
+
+    def restore(self, records):
+        """restore through the reference's own findOrInsertSlot (oracle/ref_shim.cpp pr_restore)"""
+        r = np.ascontiguousarray(records, SNAP_DTYPE)
+        self.lib.pr_restore(self.h, _p(r), len(r))
 
     def queue_apply(self, updates):
         q = self.lib.pr_queue_create()

@@ -212,6 +212,37 @@ int pr_dump_snapshot(void *s, const char *path) {
     }
 }
 
+// Snapshot restore over the reference's own insert (the reference has no restore API; this is
+// the restore a maintainer would add to FieldStore): records in ascending key order (stable),
+// FieldStore::findOrInsertSlot (field.cpp:116-146), then valueOld/cOld at the returned slot.
+struct pr_snap {
+    int32_t level, cell[3], dir[2];
+    uint32_t checksum;
+    double value[3];
+    double c_old;
+};
+
+void pr_restore(void *s, const pr_snap *recs, int64_t n) {
+    FieldStore *st = static_cast<FieldStore *>(s);
+    std::vector<const pr_snap *> ord(size_t(n > 0 ? n : 0));
+    for (int64_t i = 0; i < n; ++i) ord[size_t(i)] = &recs[i];
+    std::stable_sort(ord.begin(), ord.end(), [](const pr_snap *a, const pr_snap *b) {
+        return std::tie(a->level, a->cell[0], a->cell[1], a->cell[2], a->dir[0], a->dir[1]) <
+               std::tie(b->level, b->cell[0], b->cell[1], b->cell[2], b->dir[0], b->dir[1]);
+    });
+    for (const pr_snap *r : ord) {
+        SpatioDirectionalKey k;
+        k.level = r->level;
+        std::copy(r->cell, r->cell + 3, k.cell);
+        std::copy(r->dir, r->dir + 2, k.dirCell);
+        k.checksum = r->checksum;
+        int idx = st->findOrInsertSlot(k);
+        if (idx < 0) continue;
+        st->m_slots[idx].valueOld = RGB{r->value[0], r->value[1], r->value[2]};
+        st->m_slots[idx].cOld = r->c_old;
+    }
+}
+
 // slot array (private state, exposed by `#define private public`)
 void pr_slots(void *s, pr_slot *out) {
     FieldStore *st = static_cast<FieldStore *>(s);

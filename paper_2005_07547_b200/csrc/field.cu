@@ -167,6 +167,7 @@ struct Scratch {
     DBuf ddtab, rep_of, uidx, ukw, nudev;   // sort-free ATOMIC phase 2
     DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
     DBuf snap;                              // snapshot gather
+    DBuf winner;                            // snapshot restore: last record per slot
     DBuf hio;                               // host-pointer API staging
     unsigned long long *h_small = nullptr;  // pinned readback
     ~Scratch() {
@@ -3489,6 +3490,118 @@ int pstf_read_snapshot(const char *path, pstf_snapshot_record *records, uint64_t
     *count = n;
     if (kind_out) *kind_out = kind;
     return PSTF_OK;
+}
+
+/* ---- snapshot restore (the reference writes snapshots but has no restore) */
+
+__device__ __forceinline__ uint32_t snap_home(const pstf_snapshot_record &q, uint32_t mask) {
+    return (uint32_t)pack_key_fields(q.level, q.cell[0], q.cell[1], q.cell[2], q.dir_cell[0],
+                                     q.dir_cell[1]) & mask;
+}
+
+/* record i -> a zero-weight counter update of its key: phase 2 (ORDERED) then inserts the keys
+ * exactly as findOrInsertSlot in ascending key order would (field.cpp:116-146, 402-419) */
+__global__ void k_restore_records(const pstf_snapshot_record *r, uint64_t n, PendRec *pend) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const pstf_snapshot_record q = r[i];
+    Key k;
+    k.level = q.level;
+    k.cell[0] = q.cell[0];
+    k.cell[1] = q.cell[1];
+    k.cell[2] = q.cell[2];
+    k.dir[0] = q.dir_cell[0];
+    k.dir[1] = q.dir_cell[1];
+    k.checksum = q.checksum;
+    put_record(&pend[i], k, PSTF_META(0, 1, 1), 0.0, 0.0, 0.0, 0.0);
+}
+
+/* the slot a record's key resolves to after the inserts (findSlot, field.cpp:103-114; no slot
+ * empties during a restore, so it is the slot findOrInsertSlot returned); the last record in
+ * key order that resolves to a slot owns its committed value */
+__global__ void k_restore_claim(DevStore s, const pstf_snapshot_record *r, uint64_t n,
+                                uint32_t *winner) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int slot = probe_find(s, snap_home(r[i], s.mask), r[i].checksum);
+    if (slot >= 0) atomicMax(&winner[slot], (uint32_t)i + 1u);
+}
+
+__global__ void k_restore_write(DevStore s, const pstf_snapshot_record *r, uint64_t n,
+                                const uint32_t *winner) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const pstf_snapshot_record q = r[i];
+    const int slot = probe_find(s, snap_home(q, s.mask), q.checksum);
+    if (slot >= 0 && winner[slot] == (uint32_t)i + 1u)
+        s.com[slot] = make_double4(q.value[0], q.value[1], q.value[2], q.c_old);
+}
+
+static bool snap_key_less(const pstf_snapshot_record &a, const pstf_snapshot_record &b) {
+    const int32_t ka[6] = {a.level, a.cell[0], a.cell[1], a.cell[2], a.dir_cell[0], a.dir_cell[1]};
+    const int32_t kb[6] = {b.level, b.cell[0], b.cell[1], b.cell[2], b.dir_cell[0], b.dir_cell[1]};
+    return std::lexicographical_compare(ka, ka + 6, kb, kb + 6); /* field.cpp:334-337 */
+}
+
+extern "C" int pstf_field_restore(pstf_field *f, const pstf_snapshot_record *records, uint64_t n) {
+    if (!f || (n && !records)) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "too many records");
+    for (uint64_t i = 0; i < n; ++i) { /* keyFor's checksum (field.cpp:98-99) */
+        const pstf_snapshot_record &q = records[i];
+        const uint32_t cs = checksum_of(pack_key_fields(q.level, q.cell[0], q.cell[1], q.cell[2],
+                                                        q.dir_cell[0], q.dir_cell[1]));
+        if (cs != q.checksum)
+            return set_err(PSTF_E_FORMAT, "snapshot record " + std::to_string(i) +
+                                              ": checksum does not match its key");
+    }
+    CK(cudaSetDevice(f->device));
+    SETTLE(f);
+    if (!n) return PSTF_OK;
+    /* ascending key order, stable (snapshots are written sorted: usually nothing to do) */
+    std::vector<pstf_snapshot_record> sorted;
+    const pstf_snapshot_record *src = records;
+    if (!std::is_sorted(records, records + n, snap_key_less)) {
+        sorted.assign(records, records + n);
+        std::stable_sort(sorted.begin(), sorted.end(), snap_key_less);
+        src = sorted.data();
+    }
+    Scratch &sc = f->sc;
+    const cudaStream_t st = 0;
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    ENSURE(sc.snap, n * sizeof(pstf_snapshot_record));
+    ENSURE(sc.winner, cap * 4);
+    pstf_snapshot_record *d = sc.snap.as<pstf_snapshot_record>();
+    CK(cudaMemcpy(d, src, n * sizeof(pstf_snapshot_record), cudaMemcpyHostToDevice));
+    int rc = ensure_pending(sc, n, false, st);
+    if (rc) return rc;
+    LAUNCH(k_restore_records, grid_for(n, 256), 256, 0, st, d, n, sc.pend.as<PendRec>());
+    const unsigned long long cnt = n;
+    CK(cudaMemcpyAsync(sc.pend_count.p, &cnt, 8, cudaMemcpyHostToDevice, st));
+    pstf_field *fs[1] = {f};
+    rc = resolve_pending(sc, fs, 1, PSTF_MODE_ORDERED, n, st);
+    if (rc) return rc;
+    const DevStore ds = dev_view(f);
+    CK(cudaMemsetAsync(sc.winner.p, 0, cap * 4, st));
+    LAUNCH(k_restore_claim, grid_for(n, 256), 256, 0, st, ds, d, n, sc.winner.as<uint32_t>());
+    LAUNCH(k_restore_write, grid_for(n, 256), 256, 0, st, ds, d, n, sc.winner.as<uint32_t>());
+    CK(cudaStreamSynchronize(st));
+    return PSTF_OK;
+}
+
+extern "C" int pstf_field_load_snapshot(pstf_field *f, const char *path) {
+    if (!f || !path) return set_err(PSTF_E_INVALID, "NULL argument");
+    uint64_t n = 0;
+    uint32_t kind = 0;
+    int rc = pstf_read_snapshot(path, nullptr, 0, &n, &kind);
+    if (rc) return rc;
+    if (kind != f->cfg.kind)
+        return set_err(PSTF_E_FORMAT, std::string("'") + path + "': snapshot of field kind " +
+                                          std::to_string(kind) + ", store is kind " +
+                                          std::to_string(f->cfg.kind));
+    std::vector<pstf_snapshot_record> h(n);
+    rc = pstf_read_snapshot(path, h.data(), n, &n, nullptr);
+    if (rc) return rc;
+    return pstf_field_restore(f, h.data(), n);
 }
 
 int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_record *out) {

@@ -229,6 +229,11 @@ void FieldStore::dumpSnapshot(const std::string &path) const {
     check(pstf_field_dump_snapshot(m_impl->h, path.c_str()), "dumpSnapshot");
 }
 
+void FieldStore::loadSnapshot(const std::string &path) {
+    flush();
+    check(pstf_field_load_snapshot(m_impl->h, path.c_str()), "loadSnapshot");
+}
+
 std::vector<FieldStore::SnapshotRecord> FieldStore::readSnapshot(const std::string &path) {
     uint64_t n = 0;
     check(pstf_read_snapshot(path.c_str(), nullptr, 0, &n, nullptr), "readSnapshot");

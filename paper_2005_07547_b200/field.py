@@ -102,6 +102,8 @@ def lib():
         "pstf_field_snapshot": ([vp, vp, u64, vp], i32),
         "pstf_field_dump_snapshot": ([vp, C.c_char_p], i32),
         "pstf_read_snapshot": ([C.c_char_p, vp, u64, vp, vp], i32),
+        "pstf_field_restore": ([vp, vp, u64], i32),
+        "pstf_field_load_snapshot": ([vp, C.c_char_p], i32),
         "pstf_field_slots": ([vp, u64, u64, vp], i32),
         "pstf_vertex_pass": ([vp, vp, vp, vp, vp, u64, u32, u32, i32, vp], i32),
         "pstf_vertex_pass_host": ([vp, vp, vp, vp, vp, u64, u32, u32, i32, vp], i32),
@@ -449,6 +451,21 @@ class FieldStore:
     @staticmethod
     def readSnapshot(path: str) -> np.ndarray:
         return read_snapshot(path)[1]
+
+    def restore(self, records) -> None:
+        """Insert snapshot records (SNAPSHOT_DTYPE, any order) and set their committed values;
+        the semantics are pstf_field_restore's (include/pstf_field.h).  Extension: the
+        reference writes snapshots (field.cpp:311-386) but cannot load them."""
+        self.flush()
+        r = np.ascontiguousarray(records, SNAPSHOT_DTYPE)
+        _check(lib().pstf_field_restore(self._h, r.ctypes.data_as(C.c_void_p), len(r)))
+
+    def loadSnapshot(self, path: str) -> None:
+        """readSnapshot(path) + restore; the file's kind must be the store's"""
+        self.flush()
+        _check(lib().pstf_field_load_snapshot(self._h, path.encode()))
+
+    load_snapshot = loadSnapshot
 
     def slots(self, begin=0, count=None) -> np.ndarray:
         self.flush()

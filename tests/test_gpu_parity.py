@@ -10,6 +10,7 @@ import pytest
 import gpu_util as gu
 import inputs
 import pyoracle as po
+import restore_cases as rc
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -477,6 +478,71 @@ def test_snapshot_file_matches_reference(tmp_path):
         bad = tmp_path / "bad.snap"
         bad.write_bytes(b"NOTASNAP0000")
         pb.read_snapshot(str(bad))
+
+
+# ------------------------------------------------------------------ snapshot restore (§8f row 3)
+@pytest.mark.parametrize("cap,window,prefill", [(13, 32, False), (10, 8, False), (11, 32, True),
+                                                (8, 4, True)])
+def test_restore_vs_oracle(cap, window, prefill):
+    """pstf_field_restore == the reference's own findOrInsertSlot in ascending key order
+    (oracle/ref_shim.cpp pr_restore, pinned in test_oracle_pin): slots, ages, drops bitwise;
+    then one more ORDERED frame on top stays bitwise (restored cells blend like native ones)."""
+    rng = np.random.default_rng(cap * 7 + window)
+    recs = rc.restore_records(rng)
+    cfg = po.Config.make(capacity_log2=cap, base_cell_size=0.5, probe_window=window)
+    o = _checker(cfg)
+    g = pb.FieldStore(_pcfg(cfg))
+    if prefill:
+        u = rc.random_updates(po.OracleStore(cfg), rng, 2000, 700)
+        o.queue_apply(u)
+        _apply_gpu(g, u, pb.MODE_ORDERED)
+        o.end_frame()
+        g.end_frame()
+    o.restore(recs)
+    g.restore(recs)
+    gu.assert_slots_bitwise(g.slots(), o.slots())
+    st, so = g.stats(), o.stats()
+    for k in ("frame", "rejected", "dropped", "internal_errors", "live"):
+        assert st[k] == so[k], k
+    u = rc.random_updates(po.OracleStore(cfg), rng, 3000, 1000)
+    o.queue_apply(u)
+    _apply_gpu(g, u, pb.MODE_ORDERED)
+    o.end_frame()
+    g.end_frame()
+    gu.assert_slots_bitwise(g.slots(), o.slots())
+    if cap == 13 and not prefill:
+        assert st["dropped"] == 0
+
+
+def test_snapshot_dump_load_round_trip(tmp_path):
+    """dump -> loadSnapshot into a fresh store -> dump: byte-identical files (checkpoint/resume
+    of the cache); bad checksums and a wrong field kind are rejected with the store unchanged."""
+    cfg = po.Config.make(capacity_log2=14, base_cell_size=0.5)
+    g = pb.FieldStore(_pcfg(cfg))
+    rng = np.random.default_rng(31)
+    for _ in range(3):
+        _apply_gpu(g, rc.random_updates(po.OracleStore(cfg), rng, 20000, 6000, levels=5),
+                   pb.MODE_ATOMIC)
+        g.end_frame()
+    a, b = str(tmp_path / "a.snap"), str(tmp_path / "b.snap")
+    g.dump_snapshot(a)
+    h = pb.FieldStore(_pcfg(cfg))
+    h.load_snapshot(a)
+    h.dump_snapshot(b)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    assert h.liveCellCount() == g.liveCellCount() > 5000
+    o = _checker(cfg)
+    o.restore(pb.read_snapshot(a)[1])
+    gu.assert_slots_bitwise(h.slots(), o.slots())
+    recs = g.snapshot()
+    recs["checksum"][len(recs) // 2] ^= 1
+    e = pb.FieldStore(_pcfg(cfg))
+    with pytest.raises(pb.PstfError, match="checksum"):
+        e.restore(recs)
+    assert e.liveCellCount() == 0
+    fli = pb.FieldStore(_pcfg(po.Config.make(kind=po.KIND_FLI, capacity_log2=14, base_cell_size=0.5)))
+    with pytest.raises(pb.PstfError, match="kind"):
+        fli.load_snapshot(a)
 
 
 # ------------------------------------------------------------------ full-size properties

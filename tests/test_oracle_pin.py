@@ -7,6 +7,7 @@ import pytest
 
 import inputs
 import pyoracle as po
+import restore_cases as rc
 
 pytestmark = pytest.mark.skipif(not po.ref_available(), reason="oracle/_ref not built")
 
@@ -193,3 +194,31 @@ def test_snapshot_records_match_reference_file(tmp_path):
     assert kind == 0 and len(recs) == len(mine)
     for f in po.SNAP_DTYPE.names:
         np.testing.assert_array_equal(recs[f], mine[f])
+
+
+@pytest.mark.parametrize("cap,window,prefill", [(13, 32, False), (10, 8, False), (11, 32, True),
+                                                (8, 4, True)])
+def test_restore_matches_reference_insert(cap, window, prefill):
+    """po_restore (the oracle's snapshot restore) == restore through the reference's own
+    findOrInsertSlot (oracle/ref_shim.cpp pr_restore): slots and counters bitwise, including
+    drops (small tables), duplicate keys (the last in key order wins) and restores into a
+    store that already holds cells."""
+    rng = np.random.default_rng(cap * 7 + window)
+    recs = rc.restore_records(rng)
+    cfg = po.Config.make(capacity_log2=cap, base_cell_size=0.5, probe_window=window)
+    o, r = po.OracleStore(cfg), po.RefStore(cfg)
+    if prefill:
+        u = rc.random_updates(o, rng, 2000, 700)
+        for s in (o, r):
+            s.queue_apply(u)
+            s.end_frame()
+    o.restore(recs)
+    r.restore(recs)
+    _slots_equal(o.slots(), r.slots())
+    assert o.stats() == r.stats()
+    if cap == 13 and not prefill:  # no drops: the snapshot is the input, last duplicate wins
+        assert o.stats()["dropped"] == 0
+        snap, want = o.snapshot(), rc.expected_restore(recs)
+        for f in po.SNAP_DTYPE.names:  # per field: the records' padding bytes are unspecified
+            np.testing.assert_array_equal(np.ascontiguousarray(snap[f]).view(np.uint8),
+                                          np.ascontiguousarray(want[f]).view(np.uint8), err_msg=f)
