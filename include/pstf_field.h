@@ -322,6 +322,76 @@ uint64_t pstf_kernel_launch_count(void);
 int pstf_profile_enable(int on);
 int pstf_profile_collect(char *names, double *ms, uint64_t *counts, int n_max, int *n_out);
 
+/* ---- CV-profile / guiding model store -------------------------------
+ * ModelStore (estimators.h:124-150, estimators.cpp:104-144) with the DirGrid model
+ * (models.h:30-52, models.cpp:16-94): the ModelKind::Grid store, which is what the CV profiles
+ * always use (estimators.cpp:336-339) and the guiding models' default kind (models.h:186).
+ * Keyed by the field's SpatioDirectionalKey with key-field equality (the unordered_map's
+ * operator==, field.h:38-41).  The reference map grows without bound; here the table has
+ * 2^capacity_log2 entries and records of keys that find no free entry are counted as dropped. */
+typedef struct pstf_model_config {
+    int32_t grid_resolution; /* ModelConfig::gridResolution (models.h:187), >= 1 */
+    double t_max;            /* EstimatorConfig::tMax (the blend cap, estimators.cpp:119-144) */
+    int32_t min_samples;     /* minModelSamples / profileMinSamples (warm threshold) */
+    uint32_t capacity_log2;  /* entries in the device table */
+} pstf_model_config;
+
+typedef struct pstf_model_store pstf_model_store;
+
+/* One entry (ModelStore::Entry + its DirGrid), for parity dumps */
+typedef struct pstf_model_entry {
+    int32_t level;
+    int32_t cell[3];
+    int32_t dir_cell[2];
+    uint32_t warm;         /* Entry::warm */
+    double c_old, c_new;   /* Entry::cOld, cNew */
+    uint64_t records;      /* Entry::records (applyRecord calls) */
+    uint64_t record_count; /* DirGrid::m_recordCount (accepted contributions) */
+    double total;          /* DirGrid::m_total */
+} pstf_model_entry;
+
+typedef struct pstf_model_stats {
+    uint64_t entries;         /* ModelStore::size() */
+    uint64_t warm;            /* entries with warm set */
+    uint64_t dropped_records; /* records whose key found no free entry (device table full) */
+    uint64_t capacity;
+} pstf_model_stats;
+
+int pstf_model_create(const pstf_model_config *config, int device, pstf_model_store **out);
+int pstf_model_destroy(pstf_model_store *m);
+/* applyRecord (estimators.cpp:109-117) for n records, device arrays.  Applied in the canonical
+ * deterministic order of estimators.cpp:633-637 (key fields, uv.x, uv.y, contribution), so the
+ * result is bitwise that of the reference's deterministic mode for the same record set. */
+int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
+                     const double *contribution, uint64_t n, void *stream);
+/* ModelStore::endFrame (estimators.cpp:119-144) */
+int pstf_model_end_frame(pstf_model_store *m, void *stream);
+/* lookupWarm (estimators.cpp:104-107): entry index of a warm model, else -1 */
+int pstf_model_lookup_warm(const pstf_model_store *m, const pstf_key *keys, uint64_t n,
+                           int32_t *entry, void *stream);
+/* The estimator's hierarchical lookup (estimators.cpp:464-469 and 475-480): for
+ * l = selectLevel(footprint) .. maxLevel, lookupWarm(keyFor(pos, dir, l)) with the keyer
+ * field's quantisation; the first warm entry, else -1. */
+int pstf_model_lookup_warm_levels(const pstf_model_store *m, const pstf_field *keyer,
+                                  const pstf_vec3_soa *pos, const pstf_vec3_soa *dir,
+                                  const double *footprint, uint64_t n, int32_t *entry,
+                                  void *stream);
+/* DirGrid::pdf (models.cpp:52-56) of entry[i] at (u[i], v[i]); entry < 0 gives 1.0 (the
+ * uniform square density the callers use without a model, estimators.cpp:485-487).  uv
+ * outside [0,1] indexes outside the grid in the reference (undefined); here it is clamped. */
+int pstf_model_pdf(const pstf_model_store *m, const int32_t *entry, const double *u,
+                   const double *v, uint64_t n, double *pdf, void *stream);
+/* DirGrid::sample(u) (models.cpp:58-92): square sample + pdf; entry < 0 gives (u, 1.0) */
+int pstf_model_sample(const pstf_model_store *m, const int32_t *entry, const double *u1,
+                      const double *u2, uint64_t n, double *su, double *sv, double *pdf,
+                      void *stream);
+int pstf_model_get_stats(pstf_model_store *m, pstf_model_stats *out);
+/* Host dump of every entry, sorted by key; weights (and accum when non-NULL) receive
+ * grid_resolution^2 doubles per entry in the same order.  *count = entries; at most cap
+ * are written. */
+int pstf_model_dump(pstf_model_store *m, pstf_model_entry *entries, double *weights,
+                    double *accum, uint64_t cap, uint64_t *count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,156 @@
+// model_shim.cpp — extern "C" wrapper around the UNMODIFIED reference ModelStore / DirGrid
+// (TEST INFRASTRUCTURE ONLY; built into oracle/_ref/libpstf_model_ref.so by oracle/Makefile).
+//
+// /root/reference/proj/core/src/estimators.cpp (ModelStore, estimators.cpp:104-144) and
+// models.cpp (DirGrid, models.cpp:16-94) are compiled in place (#included, never copied) with
+// `#define private public`, so the store's map and each DirGrid's weights/accumulators are
+// observable.  The rest of the core (tracer, scene, image, field) is linked as separate
+// translation units compiled in place.  Records are applied exactly as
+// EstimatorRun::renderFrame does in deterministic mode (estimators.cpp:625-645): sorted by
+// (key fields, uv.x, uv.y, contribution), then applyRecord in that order.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cassert>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <ostream>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <unordered_map>
+#include <variant>
+#include <vector>
+
+#define private public
+#include PSTF_REF_MODELS_CPP
+#include PSTF_REF_ESTIMATORS_CPP
+#undef private
+
+using namespace pstf;
+
+extern "C" {
+
+struct pm_key {
+    int32_t level, cell[3], dir[2];
+    uint32_t checksum;
+};
+
+struct pm_entry { // == po_model_entry / pstf_model_entry
+    int32_t level, cell[3], dir[2];
+    uint32_t warm;
+    double c_old, c_new;
+    uint64_t records, record_count;
+    double total;
+};
+
+static SpatioDirectionalKey toKey(const pm_key &k) {
+    SpatioDirectionalKey s;
+    s.level = k.level;
+    std::copy(k.cell, k.cell + 3, s.cell);
+    std::copy(k.dir, k.dir + 2, s.dirCell);
+    s.checksum = k.checksum;
+    return s;
+}
+
+void *pm_create(int res, double t_max, int min_samples) {
+    ModelConfig cfg;
+    cfg.kind = ModelKind::Grid;
+    cfg.gridResolution = res;
+    return new ModelStore(cfg, t_max, min_samples);
+}
+
+void pm_destroy(void *m) { delete static_cast<ModelStore *>(m); }
+
+void pm_apply(void *m, const pm_key *keys, const double *u, const double *v, const double *c,
+              int64_t n) {
+    std::vector<ModelRecord> records;
+    records.reserve(size_t(n));
+    for (int64_t i = 0; i < n; ++i) {
+        ModelRecord r{};
+        r.key = toKey(keys[i]);
+        r.uv = Vec2{u[i], v[i]};
+        r.contribution = c[i];
+        r.profile = true;
+        records.push_back(r);
+    }
+    // estimators.cpp:633-637, restated over the file-local ModelRecord
+    std::sort(records.begin(), records.end(), [](const ModelRecord &a, const ModelRecord &b) {
+        return std::tie(a.profile, a.key.level, a.key.cell[0], a.key.cell[1], a.key.cell[2],
+                        a.key.dirCell[0], a.key.dirCell[1], a.uv.x, a.uv.y, a.contribution) <
+               std::tie(b.profile, b.key.level, b.key.cell[0], b.key.cell[1], b.key.cell[2],
+                        b.key.dirCell[0], b.key.dirCell[1], b.uv.x, b.uv.y, b.contribution);
+    });
+    ModelStore *st = static_cast<ModelStore *>(m);
+    for (const ModelRecord &r : records) st->applyRecord(r.key, r.uv, r.contribution);
+}
+
+void pm_end_frame(void *m) { static_cast<ModelStore *>(m)->endFrame(); }
+
+// lookupWarm + DirGrid::pdf; *found = 0 and 1.0 without a warm model
+double pm_pdf(void *m, const pm_key *k, double u, double v, int *found) {
+    const DirectionalModel *d = static_cast<ModelStore *>(m)->lookupWarm(toKey(*k));
+    *found = d != nullptr;
+    return d ? d->pdf(Vec2{u, v}) : 1.0;
+}
+
+// lookupWarm + DirGrid::sample(u)
+void pm_sample(void *m, const pm_key *k, double u1, double u2, double *su, double *sv,
+               double *pdf, int *found) {
+    const DirectionalModel *d = static_cast<ModelStore *>(m)->lookupWarm(toKey(*k));
+    *found = d != nullptr;
+    if (!d) {
+        *su = u1;
+        *sv = u2;
+        *pdf = 1.0;
+        return;
+    }
+    Sample2D s = std::get<DirGrid>(d->m_impl).sample(Vec2{u1, u2});
+    *su = s.uv.x;
+    *sv = s.uv.y;
+    *pdf = s.pdf;
+}
+
+// every entry sorted by key, with its DirGrid state (private members)
+int64_t pm_dump(void *m, pm_entry *out, double *weights, double *accum, int64_t cap) {
+    ModelStore *st = static_cast<ModelStore *>(m);
+    std::vector<const std::pair<const SpatioDirectionalKey, ModelStore::Entry> *> ord;
+    for (const auto &kv : st->m_map) ord.push_back(&kv);
+    std::sort(ord.begin(), ord.end(), [](auto *a, auto *b) {
+        const SpatioDirectionalKey &x = a->first, &y = b->first;
+        return std::tie(x.level, x.cell[0], x.cell[1], x.cell[2], x.dirCell[0], x.dirCell[1]) <
+               std::tie(y.level, y.cell[0], y.cell[1], y.cell[2], y.dirCell[0], y.dirCell[1]);
+    });
+    const int64_t n = int64_t(ord.size()), k = std::min(n, cap);
+    for (int64_t i = 0; i < k; ++i) {
+        const SpatioDirectionalKey &key = ord[size_t(i)]->first;
+        const ModelStore::Entry &e = ord[size_t(i)]->second;
+        const DirGrid &g = std::get<DirGrid>(e.model->m_impl);
+        pm_entry &o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.level = key.level;
+        std::copy(key.cell, key.cell + 3, o.cell);
+        std::copy(key.dirCell, key.dirCell + 2, o.dir);
+        o.warm = e.warm;
+        o.c_old = e.cOld;
+        o.c_new = e.cNew;
+        o.records = e.records;
+        o.record_count = g.m_recordCount;
+        o.total = g.m_total;
+        const size_t r2 = g.m_weights.size();
+        if (weights) std::copy(g.m_weights.begin(), g.m_weights.end(), weights + size_t(i) * r2);
+        if (accum) std::copy(g.m_accum.begin(), g.m_accum.end(), accum + size_t(i) * r2);
+    }
+    return n;
+}
+
+} // extern "C"

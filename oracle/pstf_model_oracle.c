@@ -1,0 +1,291 @@
+/* pstf_model_oracle.c — CPU restatement of the reference's ModelStore with DirGrid models
+ * (TEST INFRASTRUCTURE ONLY: the checker of the B200 model store, never the product path).
+ *
+ *   ModelStore      estimators.h:124-150, estimators.cpp:104-144
+ *   DirGrid         models.h:30-52, models.cpp:16-94
+ *   record order    estimators.cpp:625-645 (deterministic mode: sorted, then applied in order)
+ *
+ * Pinned bitwise against the reference's own ModelStore compiled in place
+ * (oracle/model_shim.cpp -> oracle/_ref/libpstf_model_ref.so, tests/test_oracle_pin.py).
+ * The map is an open-addressing table that doubles when half full: unbounded like the
+ * reference's std::unordered_map; iteration order is never observable (dumps sort by key). */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "pstf_oracle.h"
+
+typedef struct {
+    po_key key; /* checksum ignored: equality on the key fields (field.h:38-41) */
+    double *w, *acc;
+    double total, c_old, c_new;
+    uint64_t records, rec_count;
+    int warm, used;
+} pm_entry;
+
+struct po_model {
+    int res;
+    double t_max;
+    int min_samples;
+    size_t cap, size;
+    pm_entry *tab;
+};
+
+static uint64_t pm_hash(const po_key *k) { return po_pack_key_fields(k); }
+
+static int pm_eq(const po_key *a, const po_key *b) {
+    return a->level == b->level && a->cell[0] == b->cell[0] && a->cell[1] == b->cell[1] &&
+           a->cell[2] == b->cell[2] && a->dir[0] == b->dir[0] && a->dir[1] == b->dir[1];
+}
+
+po_model *po_model_create(int res, double t_max, int min_samples) {
+    po_model *m = (po_model *)calloc(1, sizeof(po_model));
+    m->res = res;
+    m->t_max = t_max;
+    m->min_samples = min_samples;
+    m->cap = 1024;
+    m->tab = (pm_entry *)calloc(m->cap, sizeof(pm_entry));
+    return m;
+}
+
+void po_model_destroy(po_model *m) {
+    for (size_t i = 0; i < m->cap; ++i)
+        if (m->tab[i].used) {
+            free(m->tab[i].w);
+            free(m->tab[i].acc);
+        }
+    free(m->tab);
+    free(m);
+}
+
+static pm_entry *pm_find(const po_model *m, const po_key *k) {
+    size_t i = (size_t)(pm_hash(k) & (m->cap - 1));
+    for (;;) {
+        pm_entry *e = &m->tab[i];
+        if (!e->used) return NULL;
+        if (pm_eq(&e->key, k)) return e;
+        i = (i + 1) & (m->cap - 1);
+    }
+}
+
+static pm_entry *pm_slot_for_insert(pm_entry *tab, size_t cap, const po_key *k) {
+    size_t i = (size_t)(pm_hash(k) & (cap - 1));
+    while (tab[i].used && !pm_eq(&tab[i].key, k)) i = (i + 1) & (cap - 1);
+    return &tab[i];
+}
+
+/* m_map[key] (estimators.cpp:111) + the DirGrid constructor (models.cpp:16-22) */
+static pm_entry *pm_get_or_create(po_model *m, const po_key *k) {
+    pm_entry *e = pm_find(m, k);
+    if (e) return e;
+    if (2 * (m->size + 1) > m->cap) {
+        size_t nc = m->cap * 2;
+        pm_entry *nt = (pm_entry *)calloc(nc, sizeof(pm_entry));
+        for (size_t i = 0; i < m->cap; ++i)
+            if (m->tab[i].used) *pm_slot_for_insert(nt, nc, &m->tab[i].key) = m->tab[i];
+        free(m->tab);
+        m->tab = nt;
+        m->cap = nc;
+    }
+    e = pm_slot_for_insert(m->tab, m->cap, k);
+    memset(e, 0, sizeof(*e));
+    e->used = 1;
+    e->key = *k;
+    size_t r2 = (size_t)m->res * m->res;
+    e->w = (double *)malloc(r2 * sizeof(double));
+    e->acc = (double *)calloc(r2, sizeof(double));
+    for (size_t j = 0; j < r2; ++j) e->w[j] = 1.0 / ((double)m->res * m->res);
+    e->total = 1.0;
+    m->size++;
+    return e;
+}
+
+/* DirGrid::cellIndex (models.cpp:24-28); int(double) with x86 truncation, uv < 0 clamped as on
+ * the device (the reference indexes outside the grid there) */
+static int pm_cell(int res, double u, double v) {
+    double fx = u * res, fy = v * res;
+    int ix = (fx >= -2147483648.0 && fx < 2147483648.0) ? (int)fx : INT32_MIN;
+    int iy = (fy >= -2147483648.0 && fy < 2147483648.0) ? (int)fy : INT32_MIN;
+    if (ix > res - 1) ix = res - 1;
+    if (iy > res - 1) iy = res - 1;
+    if (ix < 0) ix = 0;
+    if (iy < 0) iy = 0;
+    return iy * res + ix;
+}
+
+typedef struct {
+    const po_key *k;
+    double u, v, c;
+} pm_rec;
+
+static int pm_cmp_d(double a, double b) { return a < b ? -1 : (b < a ? 1 : 0); }
+
+/* std::tie(level, cell..., dirCell..., uv.x, uv.y, contribution) < (estimators.cpp:633-637) */
+static int pm_rec_cmp(const void *pa, const void *pb) {
+    const pm_rec *a = (const pm_rec *)pa, *b = (const pm_rec *)pb;
+    const int32_t ka[6] = {a->k->level, a->k->cell[0], a->k->cell[1], a->k->cell[2], a->k->dir[0],
+                           a->k->dir[1]};
+    const int32_t kb[6] = {b->k->level, b->k->cell[0], b->k->cell[1], b->k->cell[2], b->k->dir[0],
+                           b->k->dir[1]};
+    for (int i = 0; i < 6; ++i)
+        if (ka[i] != kb[i]) return ka[i] < kb[i] ? -1 : 1;
+    int c = pm_cmp_d(a->u, b->u);
+    if (c) return c;
+    c = pm_cmp_d(a->v, b->v);
+    if (c) return c;
+    return pm_cmp_d(a->c, b->c);
+}
+
+/* applyRecord (estimators.cpp:109-117) with DirGrid::record (models.cpp:30-35) */
+static void pm_apply_one(po_model *m, const po_key *k, double u, double v, double c) {
+    pm_entry *e = pm_get_or_create(m, k);
+    if (c >= 0.0 && isfinite(c)) {
+        e->acc[pm_cell(m->res, u, v)] += c;
+        e->rec_count++;
+    }
+    e->c_new += 1.0;
+    e->records++;
+}
+
+void po_model_apply(po_model *m, const po_key *keys, const double *u, const double *v,
+                    const double *c, size_t n) {
+    pm_rec *r = (pm_rec *)malloc((n ? n : 1) * sizeof(pm_rec));
+    for (size_t i = 0; i < n; ++i) {
+        r[i].k = &keys[i];
+        r[i].u = u[i];
+        r[i].v = v[i];
+        r[i].c = c[i];
+    }
+    qsort(r, n, sizeof(pm_rec), pm_rec_cmp);
+    for (size_t i = 0; i < n; ++i) pm_apply_one(m, r[i].k, r[i].u, r[i].v, r[i].c);
+    free(r);
+}
+
+/* ModelStore::endFrame (estimators.cpp:119-144) with DirGrid::endFrame (models.cpp:37-50) */
+void po_model_end_frame(po_model *m) {
+    int limited = m->t_max > 0.0 && isfinite(m->t_max);
+    double sum_c = 0.0;
+    size_t touched = 0;
+    for (size_t i = 0; i < m->cap; ++i)
+        if (m->tab[i].used && m->tab[i].c_new > 0.0) {
+            sum_c += m->tab[i].c_new;
+            ++touched;
+        }
+    double cap = limited && touched ? (m->t_max * m->t_max - m->t_max) * (sum_c / (double)touched)
+                                    : 0.0;
+    size_t r2 = (size_t)m->res * m->res;
+    for (size_t i = 0; i < m->cap; ++i) {
+        pm_entry *e = &m->tab[i];
+        if (!e->used || e->c_new <= 0.0) continue;
+        double alpha = sqrt(e->c_new / (e->c_old + e->c_new));
+        if (limited && alpha < 1.0 / m->t_max) alpha = 1.0 / m->t_max;
+        double s = 0.0;
+        for (size_t j = 0; j < r2; ++j) s += e->acc[j];
+        if (s > 0.0) {
+            for (size_t j = 0; j < r2; ++j)
+                e->w[j] = (1.0 - alpha) * e->w[j] + alpha * (e->acc[j] / s);
+            e->total = 0.0;
+            for (size_t j = 0; j < r2; ++j) e->total += e->w[j];
+        }
+        memset(e->acc, 0, r2 * sizeof(double));
+        e->c_old += e->c_new;
+        if (limited && cap < e->c_old) e->c_old = cap;
+        e->c_new = 0.0;
+        e->warm = e->records >= (uint64_t)(int64_t)m->min_samples;
+    }
+}
+
+/* lookupWarm (estimators.cpp:104-107) + DirGrid::pdf (models.cpp:52-56); no warm model -> 1.0
+ * with *found = 0 */
+double po_model_pdf(const po_model *m, const po_key *k, double u, double v, int *found) {
+    const pm_entry *e = pm_find(m, k);
+    *found = e && e->warm;
+    if (!*found || e->total <= 0.0) return 1.0;
+    return e->w[pm_cell(m->res, u, v)] / e->total * (double)m->res * m->res;
+}
+
+static double pm_clamp(double x, double lo, double hi) { /* vecmath.h:19 */
+    double a = x < lo ? lo : x;
+    return hi < a ? hi : a;
+}
+
+/* lookupWarm + DirGrid::sample (models.cpp:58-92); no warm model -> (u, 1.0), *found = 0 */
+void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double *su,
+                     double *sv, double *pdf, int *found) {
+    const pm_entry *e = pm_find(m, k);
+    *found = e && e->warm;
+    if (!*found || e->total <= 0.0) {
+        *su = u1;
+        *sv = u2;
+        *pdf = 1.0;
+        return;
+    }
+    const int R = m->res;
+    double target = u2 * e->total;
+    int row = 0;
+    double row_sum = 0.0, acc = 0.0;
+    for (; row < R; ++row) {
+        row_sum = 0.0;
+        for (int x = 0; x < R; ++x) row_sum += e->w[(size_t)row * R + x];
+        if (acc + row_sum > target || row == R - 1) break;
+        acc += row_sum;
+    }
+    double vin = row_sum > 0.0 ? pm_clamp((target - acc) / row_sum, 0.0, 1.0) : u2;
+    double col_target = u1 * row_sum;
+    int col = 0;
+    double col_acc = 0.0, w = 0.0;
+    for (; col < R; ++col) {
+        w = e->w[(size_t)row * R + col];
+        if (col_acc + w > col_target || col == R - 1) break;
+        col_acc += w;
+    }
+    double uin = w > 0.0 ? pm_clamp((col_target - col_acc) / w, 0.0, 1.0) : u1;
+    double x = (col + uin) / R, y = (row + vin) / R;
+    const double below_one = nextafter(1.0, 0.0);
+    if (below_one < x) x = below_one;
+    if (below_one < y) y = below_one;
+    *su = x;
+    *sv = y;
+    *pdf = e->w[pm_cell(R, x, y)] / e->total * (double)R * R;
+}
+
+static int pm_entry_cmp(const void *pa, const void *pb) {
+    const pm_entry *a = *(const pm_entry *const *)pa, *b = *(const pm_entry *const *)pb;
+    const int32_t ka[6] = {a->key.level, a->key.cell[0], a->key.cell[1], a->key.cell[2],
+                           a->key.dir[0], a->key.dir[1]};
+    const int32_t kb[6] = {b->key.level, b->key.cell[0], b->key.cell[1], b->key.cell[2],
+                           b->key.dir[0], b->key.dir[1]};
+    for (int i = 0; i < 6; ++i)
+        if (ka[i] != kb[i]) return ka[i] < kb[i] ? -1 : 1;
+    return 0;
+}
+
+/* every entry sorted by key; weights/accum: res^2 doubles per entry (may be NULL) */
+size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, double *accum,
+                     size_t cap) {
+    const pm_entry **ord = (const pm_entry **)malloc((m->size ? m->size : 1) * sizeof(void *));
+    size_t n = 0;
+    for (size_t i = 0; i < m->cap; ++i)
+        if (m->tab[i].used) ord[n++] = &m->tab[i];
+    qsort(ord, n, sizeof(void *), pm_entry_cmp);
+    size_t r2 = (size_t)m->res * m->res, k = n < cap ? n : cap;
+    for (size_t i = 0; i < k; ++i) {
+        const pm_entry *e = ord[i];
+        po_model_entry *o = &out[i];
+        memset(o, 0, sizeof(*o));
+        o->level = e->key.level;
+        memcpy(o->cell, e->key.cell, sizeof(o->cell));
+        memcpy(o->dir, e->key.dir, sizeof(o->dir));
+        o->warm = (uint32_t)e->warm;
+        o->c_old = e->c_old;
+        o->c_new = e->c_new;
+        o->records = e->records;
+        o->record_count = e->rec_count;
+        o->total = e->total;
+        if (weights) memcpy(weights + i * r2, e->w, r2 * sizeof(double));
+        if (accum) memcpy(accum + i * r2, e->acc, r2 * sizeof(double));
+    }
+    free(ord);
+    return n;
+}

@@ -107,6 +107,25 @@ void po_weighted_mean(const po_store *s, double out[3]);
 void po_slots(const po_store *s, po_slot *out);
 /* key-sorted live records (field.cpp:311-337); returns the count written (<= cap) */
 size_t po_snapshot(const po_store *s, po_snapshot_record *out, size_t cap);
+/* ModelStore<DirGrid> (pstf_model_oracle.c; estimators.cpp:104-144, models.cpp:16-94) */
+typedef struct po_model po_model;
+typedef struct {
+    int32_t level, cell[3], dir[2];
+    uint32_t warm;
+    double c_old, c_new;
+    uint64_t records, record_count;
+    double total;
+} po_model_entry; /* == pstf_model_entry */
+po_model *po_model_create(int res, double t_max, int min_samples);
+void po_model_destroy(po_model *m);
+void po_model_apply(po_model *m, const po_key *keys, const double *u, const double *v,
+                    const double *c, size_t n);
+void po_model_end_frame(po_model *m);
+double po_model_pdf(const po_model *m, const po_key *k, double u, double v, int *found);
+void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double *su,
+                     double *sv, double *pdf, int *found);
+size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, double *accum,
+                     size_t cap);
 /* snapshot restore, the semantics of pstf_field_restore (include/pstf_field.h) */
 void po_restore(po_store *s, const po_snapshot_record *recs, size_t n);
 

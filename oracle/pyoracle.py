@@ -471,3 +471,107 @@ def soa_views(buf, n):
     f64 = buf[:34 * n].reshape(34, n)
     flags = buf[34 * n:].view(np.uint32)[:n]
     return f64, flags
+
+
+# ---------------------------------------------------------------- ModelStore<DirGrid> (§8f row 2)
+MODEL_ENTRY_DTYPE = np.dtype([("level", "<i4"), ("cell", "<i4", (3,)), ("dir", "<i4", (2,)),
+                              ("warm", "<u4"), ("c_old", "<f8"), ("c_new", "<f8"),
+                              ("records", "<u8"), ("record_count", "<u8"), ("total", "<f8")],
+                             align=True)
+assert MODEL_ENTRY_DTYPE.itemsize == 72
+MODEL_REF_SO = os.path.join(HERE, "_ref", "libpstf_model_ref.so")
+
+
+def model_ref_available() -> bool:
+    return os.path.exists(MODEL_REF_SO)
+
+
+class _ModelBase:
+    """ModelStore (estimators.h:124-150) with DirGrid models; the C restatement
+    (OracleModelStore) or the reference compiled in place (RefModelStore)."""
+    P = ""
+
+    def __init__(self, res=16, t_max=64.0, min_samples=32):
+        self.res, self.r2 = res, res * res
+        self.h = self._fn("create")(res, t_max, min_samples)
+
+    def _fn(self, name):
+        return getattr(self.lib, self.P + name)
+
+    def __del__(self):
+        try:
+            self._fn("destroy")(self.h)
+        except Exception:
+            pass
+
+    def apply(self, keys, u, v, c):
+        k = np.ascontiguousarray(keys, KEY_DTYPE)
+        u, v, c = (np.ascontiguousarray(x, np.float64) for x in (u, v, c))
+        self._fn("apply")(self.h, _p(k), _p(u), _p(v), _p(c), len(k))
+
+    def end_frame(self):
+        self._fn("end_frame")(self.h)
+
+    def pdf(self, keys, u, v):
+        out, found = np.zeros(len(keys)), np.zeros(len(keys), bool)
+        f = C.c_int()
+        for i in range(len(keys)):
+            ks = key_from_np(keys[i])
+            out[i] = self._fn("pdf")(self.h, C.byref(ks), float(u[i]), float(v[i]), C.byref(f))
+            found[i] = f.value
+        return out, found
+
+    def sample(self, keys, u1, u2):
+        n = len(keys)
+        su, sv, pdf, found = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(n, bool)
+        a, b, p, f = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+        for i in range(n):
+            ks = key_from_np(keys[i])
+            self._fn("sample")(self.h, C.byref(ks), float(u1[i]), float(u2[i]), C.byref(a),
+                               C.byref(b), C.byref(p), C.byref(f))
+            su[i], sv[i], pdf[i], found[i] = a.value, b.value, p.value, f.value
+        return su, sv, pdf, found
+
+    def dump(self):
+        """(entries sorted by key, weights (n, R^2), accumulators (n, R^2))"""
+        n = self._fn("dump")(self.h, None, None, None, 0)
+        e = np.zeros(max(n, 1), MODEL_ENTRY_DTYPE)
+        w, a = np.zeros((max(n, 1), self.r2)), np.zeros((max(n, 1), self.r2))
+        self._fn("dump")(self.h, _p(e), _p(w), _p(a), n)
+        return e[:n], w[:n], a[:n]
+
+
+def _type_model_lib(lib, p, n_t):
+    vp, d, i32 = C.c_void_p, C.c_double, C.c_int
+    getattr(lib, p + "create").restype = vp
+    getattr(lib, p + "create").argtypes = [i32, d, i32]
+    getattr(lib, p + "destroy").argtypes = [vp]
+    getattr(lib, p + "apply").argtypes = [vp, vp, vp, vp, vp, n_t]
+    getattr(lib, p + "end_frame").argtypes = [vp]
+    getattr(lib, p + "pdf").argtypes = [vp, vp, d, d, vp]
+    getattr(lib, p + "pdf").restype = d
+    getattr(lib, p + "sample").argtypes = [vp, vp, d, d, vp, vp, vp, vp]
+    getattr(lib, p + "dump").argtypes = [vp, vp, vp, vp, n_t]
+    getattr(lib, p + "dump").restype = n_t
+
+
+class OracleModelStore(_ModelBase):
+    P = "po_model_"
+
+    def __init__(self, *a, **k):
+        self.lib = oracle_lib()
+        if not getattr(self.lib, "_model_typed", False):
+            _type_model_lib(self.lib, self.P, C.c_size_t)
+            self.lib._model_typed = True
+        super().__init__(*a, **k)
+
+
+class RefModelStore(_ModelBase):
+    P = "pm_"
+
+    def __init__(self, *a, **k):
+        self.lib = _load(MODEL_REF_SO)
+        if not getattr(self.lib, "_model_typed", False):
+            _type_model_lib(self.lib, self.P, C.c_int64)
+            self.lib._model_typed = True
+        super().__init__(*a, **k)

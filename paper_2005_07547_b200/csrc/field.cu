@@ -4292,3 +4292,6 @@ uint64_t pstf_delta_record_bytes(void) { return sizeof(DeltaRec); }
 
 } // extern "C"
 
+
+/* CV-profile / guiding model store: same translation unit */
+#include "model_store.cuh"

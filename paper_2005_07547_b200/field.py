@@ -117,6 +117,16 @@ def lib():
         "pstf_field_probe_histogram": ([vp, vp], i32),
         "pstf_diag_red_peak": ([i32, vp], i32),
         "pstf_profile_collect": ([vp, vp, vp, i32, vp], i32),
+        "pstf_model_create": ([vp, i32, vp], i32),
+        "pstf_model_destroy": ([vp], i32),
+        "pstf_model_apply": ([vp, vp, vp, vp, vp, u64, vp], i32),
+        "pstf_model_end_frame": ([vp, vp], i32),
+        "pstf_model_lookup_warm": ([vp, vp, u64, vp, vp], i32),
+        "pstf_model_lookup_warm_levels": ([vp, vp, vp, vp, vp, u64, vp, vp], i32),
+        "pstf_model_pdf": ([vp, vp, vp, vp, u64, vp, vp], i32),
+        "pstf_model_sample": ([vp, vp, vp, vp, u64, vp, vp, vp, vp], i32),
+        "pstf_model_get_stats": ([vp, vp], i32),
+        "pstf_model_dump": ([vp, vp, vp, vp, u64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

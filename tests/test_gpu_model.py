@@ -1,0 +1,126 @@
+"""GPU parity of the model store (ModelStore<DirGrid>, the CV-profile /
+guiding store keyed by the field's keys) against the reference's own ModelStore compiled in
+place (oracle/_ref/libpstf_model_ref.so) or, without it, the C restatement pinned to it
+(tests/test_oracle_pin.py).  Entries, grid weights and accumulators, warm flags, pdf and
+sample results are compared bitwise."""
+import numpy as np
+import pytest
+
+import inputs
+import model_cases as mc
+import pyoracle as po
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2005_07547_b200 as pb  # noqa: E402
+
+
+def _checker(*a):
+    return po.RefModelStore(*a) if po.model_ref_available() else po.OracleModelStore(*a)
+
+
+def _same_dump(g, r):
+    eg, wg, ag = g.dump()
+    er, wr, ar = r.dump()
+    assert len(eg) == len(er) > 0
+    for f in po.MODEL_ENTRY_DTYPE.names:
+        np.testing.assert_array_equal(np.ascontiguousarray(eg[f]).view(np.uint8),
+                                      np.ascontiguousarray(er[f]).view(np.uint8), err_msg=f)
+    np.testing.assert_array_equal(wg.view(np.uint64), wr.view(np.uint64))
+    np.testing.assert_array_equal(ag.view(np.uint64), ar.view(np.uint64))
+    return eg
+
+
+@pytest.mark.parametrize("res,t_max,min_samples", [(16, 64.0, 32), (5, 2.0, 1), (1, np.inf, 4)])
+def test_model_store_bitwise(res, t_max, min_samples):
+    rng = np.random.default_rng(res * 31 + min_samples)
+    g = pb.ModelStore(res, t_max, min_samples, capacity_log2=12)
+    r = _checker(res, t_max, min_samples)
+    for frame in range(4):
+        k, u, v, c, keys = mc.model_records(rng, 6000, 400)
+        perm = rng.permutation(len(k))  # the device sorts: input order is irrelevant
+        g.apply(k[perm], u[perm], v[perm], c[perm])
+        r.apply(k, u, v, c)
+        _same_dump(g, r)
+        g.end_frame()
+        r.end_frame()
+        e = _same_dump(g, r)
+    st = g.stats()
+    assert st["entries"] == len(e) and st["warm"] == int(e["warm"].sum()) and st["dropped_records"] == 0
+    q, u, v = mc.probe_points(rng, keys, 5000)
+    ent = g.lookup_warm(q).cpu().numpy()
+    pr, found = r.pdf(q, u, v)
+    np.testing.assert_array_equal(ent >= 0, found)
+    assert found.sum() > 50
+    pg = g.pdf(torch.from_numpy(ent), u, v).cpu().numpy()
+    np.testing.assert_array_equal(pg.view(np.uint64), pr.view(np.uint64))
+    sg = [x.cpu().numpy() for x in g.sample(torch.from_numpy(ent), u, v)]
+    sr = r.sample(q, u, v)[:3]
+    for a, b in zip(sg, sr):
+        np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_model_lookup_levels():
+    """the estimator's coarse-to-fine search (estimators.cpp:464-469): first warm model over
+    levels selectLevel(footprint)..maxLevel of keyFor(pos, wo, l) with the Lo store's keys"""
+    cfg = po.Config.make(capacity_log2=10, base_cell_size=0.5)
+    keyer = pb.FieldStore(pb.FieldStoreConfig(capacity_log2=10, base_cell_size=0.5))
+    ok = po.OracleStore(cfg)
+    rng = np.random.default_rng(77)
+    n = 4000
+    pos = rng.uniform(-4, 4, size=(n, 3))
+    d = inputs.random_dirs(rng, n)
+    fp = np.exp(rng.uniform(np.log(0.01), np.log(20.0), size=n))
+    g = pb.ModelStore(8, 64.0, 2, capacity_log2=14)
+    r = _checker(8, 64.0, 2)
+    # records at levels 0-2 for 30% of the points each: searches stop early, fall back to a
+    # coarser level, or find nothing (footprints selecting levels 3-4)
+    for l in range(3):
+        sel = rng.random(n) < 0.3
+        kk = ok.keys_for(pos[sel], d[sel], np.full(int(sel.sum()), l, np.int32))
+        kk = np.concatenate([kk] * 3)
+        u, v, c = rng.random(len(kk)), rng.random(len(kk)), rng.exponential(1.0, len(kk))
+        g.apply(kk, u, v, c)
+        r.apply(kk, u, v, c)
+    g.end_frame()
+    r.end_frame()
+    got = g.lookup_warm_levels(keyer, pos, d, fp).cpu().numpy()
+    want = np.full(n, -1)
+    lv0 = ok.select_levels(fp)
+    for l in range(cfg.max_level, -1, -1):
+        kk = ok.keys_for(pos, d, np.full(n, l, np.int32))
+        ent = g.lookup_warm(kk).cpu().numpy()
+        _, found = r.pdf(kk, np.zeros(n), np.zeros(n))
+        np.testing.assert_array_equal(ent >= 0, found)
+        hit = (l >= lv0) & found
+        want[hit] = ent[hit]
+    np.testing.assert_array_equal(got, want)
+    assert (got >= 0).sum() > 500 and (got < 0).sum() > 100
+
+
+def test_model_table_full_counts_drops():
+    """the device table is bounded (the reference map is not): keys beyond capacity are
+    counted, never written over other entries"""
+    rng = np.random.default_rng(3)
+    g = pb.ModelStore(4, 64.0, 1, capacity_log2=5)
+    k, u, v, c, keys = mc.model_records(rng, 3000, 200)
+    g.apply(k, u, v, c)
+    g.end_frame()
+    st = g.stats()
+    e, _, _ = g.dump()
+    assert st["entries"] == 32 == len(e)
+    assert st["dropped_records"] == len(k) - int(e["records"].sum()) > 0
+    r = _checker(4, 64.0, 1)
+    r.apply(k, u, v, c)
+    r.end_frame()
+    er, wr, _ = r.dump()
+    eg, wg, _ = g.dump()
+    idx = {tuple(x["cell"]) + tuple(x["dir"]) + (int(x["level"]),): i for i, x in enumerate(er)}
+    for i, x in enumerate(eg):  # every stored entry equals the unbounded reference's
+        j = idx[tuple(x["cell"]) + tuple(x["dir"]) + (int(x["level"]),)]
+        assert x["records"] == er[j]["records"]
+        np.testing.assert_array_equal(wg[i].view(np.uint64), wr[j].view(np.uint64))

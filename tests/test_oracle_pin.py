@@ -222,3 +222,45 @@ def test_restore_matches_reference_insert(cap, window, prefill):
         for f in po.SNAP_DTYPE.names:  # per field: the records' padding bytes are unspecified
             np.testing.assert_array_equal(np.ascontiguousarray(snap[f]).view(np.uint8),
                                           np.ascontiguousarray(want[f]).view(np.uint8), err_msg=f)
+
+
+# ---------------------------------------------------------------- ModelStore<DirGrid> (§8f row 2)
+def _model_equal(a, b):
+    ea, wa, aa = a.dump()
+    eb, wb, ab = b.dump()
+    assert len(ea) == len(eb)
+    for f in po.MODEL_ENTRY_DTYPE.names:
+        np.testing.assert_array_equal(np.ascontiguousarray(ea[f]).view(np.uint8),
+                                      np.ascontiguousarray(eb[f]).view(np.uint8), err_msg=f)
+    np.testing.assert_array_equal(wa.view(np.uint64), wb.view(np.uint64))
+    np.testing.assert_array_equal(aa.view(np.uint64), ab.view(np.uint64))
+
+
+@pytest.mark.skipif(not po.model_ref_available(), reason="oracle/_ref model store not built")
+@pytest.mark.parametrize("res,t_max,min_samples", [(16, 64.0, 32), (5, 2.0, 1), (1, np.inf, 4)])
+def test_model_store_matches_reference(res, t_max, min_samples):
+    """po_model_* (C restatement) == the reference's ModelStore/DirGrid compiled in place: every
+    entry (cOld, cNew, records, recordCount, warm, total), weights and accumulators bitwise over
+    apply/endFrame frames, then pdf and sample of warm models bitwise."""
+    import model_cases as mc
+    rng = np.random.default_rng(res * 31 + min_samples)
+    o = po.OracleModelStore(res, t_max, min_samples)
+    r = po.RefModelStore(res, t_max, min_samples)
+    for frame in range(4):
+        k, u, v, c, keys = mc.model_records(rng, 6000, 400)
+        o.apply(k, u, v, c)
+        r.apply(k, u, v, c)
+        _model_equal(o, r)  # accumulators before the blend
+        o.end_frame()
+        r.end_frame()
+        _model_equal(o, r)
+    q, u, v = mc.probe_points(rng, keys, 3000)
+    po_, fo = o.pdf(q, u, v)
+    pr_, fr = r.pdf(q, u, v)
+    np.testing.assert_array_equal(fo, fr)
+    np.testing.assert_array_equal(po_.view(np.uint64), pr_.view(np.uint64))
+    so = o.sample(q, u, v)
+    sr = r.sample(q, u, v)
+    for a, b in zip(so, sr):
+        np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+    assert fo.sum() > 100
