@@ -359,11 +359,13 @@ typedef struct pstf_model_stats {
 
 int pstf_model_create(const pstf_model_config *config, int device, pstf_model_store **out);
 int pstf_model_destroy(pstf_model_store *m);
-/* applyRecord (estimators.cpp:109-117) for n records, device arrays.  Applied in the canonical
- * deterministic order of estimators.cpp:633-637 (key fields, uv.x, uv.y, contribution), so the
- * result is bitwise that of the reference's deterministic mode for the same record set. */
+/* applyRecord (estimators.cpp:109-117) for n records, device arrays.
+ * PSTF_MODE_ORDERED: applied in the canonical deterministic order of estimators.cpp:633-637
+ *   (key fields, uv.x, uv.y, contribution): bitwise the reference's deterministic mode.
+ * PSTF_MODE_ATOMIC: no sort, fp64 atomics into the grids; accumulator sums within 1e-12
+ *   relative (their order is the atomics'), everything else exact. */
 int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
-                     const double *contribution, uint64_t n, void *stream);
+                     const double *contribution, uint64_t n, int mode, void *stream);
 /* ModelStore::endFrame (estimators.cpp:119-144) */
 int pstf_model_end_frame(pstf_model_store *m, void *stream);
 /* lookupWarm (estimators.cpp:104-107): entry index of a warm model, else -1 */

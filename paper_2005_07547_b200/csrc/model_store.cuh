@@ -11,11 +11,13 @@
  *   ent[e]     {total, cOld, cNew, records, recordCount, warm, touched}
  *   w[e][R^2], acc[e][R^2]  f64 DirGrid weights / accumulators, row-major (iy * R + ix)
  *
- * apply:  records sorted by (key, uv.x, uv.y, contribution) (estimators.cpp:633-637), one
- *         thread per distinct key folds its records in that order, so every accumulator sum
- *         has the reference's deterministic order; new keys are inserted with a CAS on state.
+ * apply:  every record finds (or inserts, CAS on state) its key's entry; the records are then
+ *         radix-sorted by (entry, grid cell, uv.x, uv.y, contribution), which within one key
+ *         is the canonical order of estimators.cpp:633-637, and one thread per (entry, cell)
+ *         run folds it in a register: each accumulator sum has the reference's order.  No host
+ *         round trip.
  * endFrame: the touched entries only (a list built by apply): Σ cNew (integer-valued, exact in
- *         any order), then one thread per entry blends its grid with sequential sums. */
+ *         any order), then one warp per entry blends its grid, the grid sums in index order. */
 
 struct ModelEnt {
     double total, c_old, c_new;
@@ -43,7 +45,7 @@ struct pstf_model_store {
     int r2 = 0;
     DBuf state, keyf, ent, w, acc, ctr, tlist, sums;
     Scratch sc;
-    DBuf words, head, uid, seg, slot_of;
+    DBuf words;
     MdlDev dev() const {
         MdlDev d;
         d.state = state.as<uint32_t>();
@@ -93,51 +95,12 @@ __device__ __forceinline__ uint64_t ord_f64(double d) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
 }
 
-__device__ __forceinline__ uint64_t ord_i32(int32_t x) { return (uint64_t)((uint32_t)x ^ 0x80000000u); }
-
-/* sort words (most significant first): key fields in 3 words, then uv.x, uv.y, contribution */
-__global__ void k_mdl_encode(const pstf_key *keys, const double *u, const double *v,
-                             const double *c, uint64_t n, uint64_t *words) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const pstf_key k = keys[i];
-    words[0 * n + i] = ord_i32(k.level) << 32 | ord_i32(k.cell[0]);
-    words[1 * n + i] = ord_i32(k.cell[1]) << 32 | ord_i32(k.cell[2]);
-    words[2 * n + i] = ord_i32(k.dir_cell[0]) << 32 | ord_i32(k.dir_cell[1]);
-    words[3 * n + i] = ord_f64(u[i]);
-    words[4 * n + i] = ord_f64(v[i]);
-    words[5 * n + i] = ord_f64(c[i]);
-}
-
-__global__ void k_mdl_heads(const uint64_t *words, const uint32_t *perm, uint64_t n, uint32_t *head) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint32_t h = 1;
-    if (i > 0) {
-        const uint32_t a = perm[i], b = perm[i - 1];
-        h = words[a] != words[b] || words[n + a] != words[n + b] ||
-            words[2 * n + a] != words[2 * n + b];
-    }
-    head[i] = h;
-}
-
-/* seg[u] = first sorted position of distinct key u; seg[nu] = n */
-__global__ void k_mdl_segs(const uint32_t *head, const uint32_t *uid, uint64_t n, uint32_t *seg,
-                           uint64_t nu) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i < n && head[i]) seg[uid[i] - 1] = (uint32_t)i;
-    if (i == 0) seg[nu] = (uint32_t)n;
-}
-
-/* find-or-insert one distinct key (no two threads carry the same key); -1 when the table is
- * full.  A new entry is a fresh DirGrid: uniform weights 1/R^2, total 1 (models.cpp:16-22). */
-__global__ void k_mdl_insert(MdlDev m, const pstf_key *keys, const uint32_t *perm,
-                             const uint32_t *seg, uint64_t nu, int32_t *slot_of) {
-    uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (u >= nu) return;
-    const KeyFields k = kf_of(keys[perm[seg[u]]]);
+/* find-or-insert a key (field.h:38-41 equality); -1 when the table is full.  Threads carrying
+ * the same new key meet at the entry the first of them claims (same probe sequence; a claimed
+ * entry is waited for until published).  A new entry is a fresh DirGrid: uniform weights
+ * 1/R^2, total 1 (models.cpp:16-22), zero counters (estimators.cpp:111-113). */
+__device__ int32_t mdl_find_or_insert(const MdlDev &m, const KeyFields &k) {
     const uint32_t home = mdl_home(k, m.mask);
-    int32_t found = -1;
     for (uint32_t i = 0; i <= m.mask; ++i) {
         const uint32_t e = (home + i) & m.mask;
         uint32_t s = ld_state(&m.state[e]);
@@ -159,48 +122,100 @@ __global__ void k_mdl_insert(MdlDev m, const pstf_key *keys, const uint32_t *per
                 __threadfence();
                 atomicExch(&m.state[e], 2u);
                 atomicAdd(&m.ctr[MC_ENTRIES], 1ull);
-                found = (int32_t)e;
-                break;
+                return (int32_t)e;
             }
         }
         while (s == 1) s = ld_state(&m.state[e]); /* another key is being written here */
-        if (kf_equal(m.keyf[e], k)) {
-            found = (int32_t)e;
-            break;
-        }
+        if (kf_equal(m.keyf[e], k)) return (int32_t)e;
     }
-    slot_of[u] = found;
+    return -1;
 }
 
-/* applyRecord (estimators.cpp:109-117) + DirGrid::record (models.cpp:30-35), in sorted order */
-__global__ void k_mdl_fold(MdlDev m, const uint32_t *perm, const uint32_t *seg, uint64_t nu,
-                           const int32_t *slot_of, const double *u, const double *v,
-                           const double *c) {
-    uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (q >= nu) return;
-    const int32_t e = slot_of[q];
-    const uint32_t b = seg[q], end = seg[q + 1];
-    if (e < 0) {
-        atomicAdd(&m.ctr[MC_DROPPED], (unsigned long long)(end - b));
-        return;
-    }
-    ModelEnt x = m.ent[e];
-    double *acc = m.acc + (uint64_t)e * m.r2;
-    for (uint32_t j = b; j < end; ++j) {
+/* per record: its entry (inserting new keys) and the sort words, most significant first:
+ * (entry, grid cell) in the top bits of word 0, then uv.x, uv.y, contribution.  Sorting on them
+ * puts each (entry, cell)'s records in the canonical order of estimators.cpp:633-637 (only the
+ * order within one key matters: records of different keys never share an accumulator).
+ * Records of keys without an entry (table full) sort last and are counted as dropped. */
+__global__ void k_mdl_records(MdlDev m, const pstf_key *keys, const double *u, const double *v,
+                              const double *c, uint64_t n, int shift, uint64_t *words) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t e = mdl_find_or_insert(m, kf_of(keys[i]));
+    uint64_t w0 = ~0ull;
+    if (e >= 0)
+        w0 = ((uint64_t)e << 16 | (uint32_t)mdl_cell(u[i], v[i], m.res)) << shift;
+    else
+        atomicAdd(&m.ctr[MC_DROPPED], 1ull);
+    words[0 * n + i] = w0;
+    words[1 * n + i] = ord_f64(u[i]);
+    words[2 * n + i] = ord_f64(v[i]);
+    words[3 * n + i] = ord_f64(c[i]);
+}
+
+/* one thread per (entry, cell) run of the sorted records: DirGrid::record (models.cpp:30-35)
+ * folded in a register in the canonical order, and applyRecord's counters (estimators.cpp:
+ * 114-116; cNew += 1 per record is integer-valued, so adding the run length is exact) */
+__global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm, uint64_t n,
+                           int shift, const double *c) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t w = words[perm[i]];
+    if (w == ~0ull || (i > 0 && words[perm[i - 1]] == w)) return; /* dropped, or not a run head */
+    const uint64_t ec = w >> shift;
+    const uint32_t e = (uint32_t)(ec >> 16);
+    double *acc = m.acc + (uint64_t)e * m.r2 + (uint32_t)(ec & 0xffffu);
+    double s = *acc;
+    unsigned long long cnt = 0, len = 0;
+    for (uint64_t j = i; j < n; ++j) {
         const uint32_t r = perm[j];
+        if (words[r] != w) break;
         const double cv = c[r];
         if (cv >= 0.0 && isfinite(cv)) {
-            acc[mdl_cell(u[r], v[r], m.res)] += cv;
-            ++x.rec_count;
+            s += cv;
+            ++cnt;
         }
-        x.c_new += 1.0;
-        ++x.records;
+        ++len;
     }
-    if (!x.touched) {
-        x.touched = 1;
-        m.tlist[atomicAdd(&m.ctr[MC_TOUCHED], 1ull)] = (uint32_t)e;
+    *acc = s;
+    ModelEnt &x = m.ent[e];
+    if (cnt) atomicAdd(&x.rec_count, cnt);
+    atomicAdd(&x.records, len);
+    atomicAdd(&x.c_new, (double)len);
+    if (atomicExch(&x.touched, 1u) == 0u) m.tlist[atomicAdd(&m.ctr[MC_TOUCHED], 1ull)] = e;
+}
+
+/* ATOMIC mode: records applied straight into the entries, no sort.  Accumulator sums then
+ * depend on the atomic order (within 1e-12 relative of the canonical order); entries, counts,
+ * warm flags and every integer-valued field stay exact.  Counters are aggregated over the lanes
+ * of a warp that share an entry. */
+__global__ void k_mdl_atomic(MdlDev m, const pstf_key *keys, const double *u, const double *v,
+                             const double *c, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    int32_t e = -2;
+    bool ok = false;
+    if (live) {
+        e = mdl_find_or_insert(m, kf_of(keys[i]));
+        if (e >= 0) {
+            const double cv = c[i];
+            ok = cv >= 0.0 && isfinite(cv);
+            if (ok) atomicAdd(m.acc + (uint64_t)e * m.r2 + mdl_cell(u[i], v[i], m.res), cv);
+        }
     }
-    m.ent[e] = x;
+    const unsigned grp = __match_any_sync(0xffffffffu, e);
+    const unsigned okm = __ballot_sync(0xffffffffu, ok);
+    const unsigned lane = lane_id();
+    if (e == -2 || lane != (unsigned)(__ffs(grp) - 1)) return;
+    const unsigned len = __popc(grp), acc_n = __popc(okm & grp);
+    if (e < 0) {
+        atomicAdd(&m.ctr[MC_DROPPED], (unsigned long long)len);
+        return;
+    }
+    ModelEnt &x = m.ent[e];
+    if (acc_n) atomicAdd(&x.rec_count, (unsigned long long)acc_n);
+    atomicAdd(&x.records, (unsigned long long)len);
+    atomicAdd(&x.c_new, (double)len);
+    if (atomicExch(&x.touched, 1u) == 0u) m.tlist[atomicAdd(&m.ctr[MC_TOUCHED], 1ull)] = (uint32_t)e;
 }
 
 /* endFrame pass 1: Σ cNew over touched entries and their number (estimators.cpp:122-128) */
@@ -223,43 +238,58 @@ __global__ void k_mdl_sums(MdlDev m, double *sums) {
     }
 }
 
-/* endFrame pass 2 (estimators.cpp:129-143) with DirGrid::endFrame (models.cpp:37-50) */
+/* sum of x[0..n) in index order (the reference's sequential loop), by one warp: lanes load
+ * 32 consecutive values, every lane adds them in order via broadcasts (identical results) */
+__device__ __forceinline__ double warp_ordered_sum(const double *x, int n, unsigned lane) {
+    double s = 0.0;
+    for (int b = 0; b < n; b += 32) {
+        const double mine = b + (int)lane < n ? x[b + lane] : 0.0;
+        const int k = min(32, n - b);
+        for (int l = 0; l < k; ++l) s += __shfl_sync(0xffffffffu, mine, l);
+    }
+    return s;
+}
+
+/* endFrame pass 2 (estimators.cpp:129-143) with DirGrid::endFrame (models.cpp:37-50), one warp
+ * per touched entry: elementwise blend across lanes, the two grid sums in index order */
 __global__ void k_mdl_blend(MdlDev m, const double *sums, double t_max, int limited,
                             int min_samples) {
     const uint64_t nt = m.ctr[MC_TOUCHED];
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= nt) return;
-    const uint32_t e = m.tlist[i];
-    ModelEnt x = m.ent[e];
-    x.touched = 0;
-    if (x.c_new > 0.0) {
-        const double touched = sums[1];
-        const double cap = limited && touched > 0.0 ? (t_max * t_max - t_max) * (sums[0] / touched)
-                                                    : 0.0;
-        double alpha = sqrt(x.c_new / (x.c_old + x.c_new));
-        if (limited) {
-            const double fl = 1.0 / t_max;
-            alpha = alpha < fl ? fl : alpha; /* std::max */
-        }
-        double *w = m.w + (uint64_t)e * m.r2, *acc = m.acc + (uint64_t)e * m.r2;
-        double sum = 0.0;
-        for (int j = 0; j < m.r2; ++j) sum += acc[j];
-        if (sum > 0.0) {
-            double tot = 0.0;
-            for (int j = 0; j < m.r2; ++j) {
-                const double nw = (1.0 - alpha) * w[j] + alpha * (acc[j] / sum);
-                w[j] = nw;
-                tot += nw;
+    const unsigned lane = lane_id();
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nt;
+         i += nwarps) { /* persistent: the touched count is known only on the device */
+        const uint32_t e = m.tlist[i];
+        ModelEnt x = m.ent[e];
+        x.touched = 0;
+        if (x.c_new > 0.0) {
+            double *w = m.w + (uint64_t)e * m.r2, *acc = m.acc + (uint64_t)e * m.r2;
+            double alpha = sqrt(x.c_new / (x.c_old + x.c_new));
+            if (limited) {
+                const double fl = 1.0 / t_max;
+                alpha = alpha < fl ? fl : alpha; /* std::max */
             }
-            x.total = tot;
+            const double sum = warp_ordered_sum(acc, m.r2, lane);
+            __syncwarp();
+            if (sum > 0.0) {
+                for (int j = lane; j < m.r2; j += 32)
+                    w[j] = (1.0 - alpha) * w[j] + alpha * (acc[j] / sum);
+                __syncwarp();
+                x.total = warp_ordered_sum(w, m.r2, lane);
+            }
+            for (int j = lane; j < m.r2; j += 32) acc[j] = 0.0;
+            const double touched = sums[1];
+            const double cap = limited && touched > 0.0
+                                   ? (t_max * t_max - t_max) * (sums[0] / touched)
+                                   : 0.0;
+            x.c_old += x.c_new;
+            if (limited) x.c_old = cap < x.c_old ? cap : x.c_old; /* std::min */
+            x.c_new = 0.0;
+            x.warm = x.records >= (unsigned long long)(long long)min_samples;
         }
-        for (int j = 0; j < m.r2; ++j) acc[j] = 0.0;
-        x.c_old += x.c_new;
-        if (limited) x.c_old = cap < x.c_old ? cap : x.c_old; /* std::min */
-        x.c_new = 0.0;
-        x.warm = x.records >= (unsigned long long)(long long)min_samples;
+        __syncwarp();
+        if (lane == 0) m.ent[e] = x;
     }
-    m.ent[e] = x;
 }
 
 __device__ __forceinline__ int32_t mdl_find_warm(const MdlDev &m, const KeyFields &k) {
@@ -394,47 +424,31 @@ int pstf_model_destroy(pstf_model_store *m) {
 }
 
 int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
-                     const double *contribution, uint64_t n, void *stream) {
+                     const double *contribution, uint64_t n, int mode, void *stream) {
     if (!m || (n && (!keys || !u || !v || !contribution)))
         return set_err(PSTF_E_INVALID, "NULL argument");
+    if (mode != PSTF_MODE_ATOMIC && mode != PSTF_MODE_ORDERED)
+        return set_err(PSTF_E_INVALID, "mode must be PSTF_MODE_ATOMIC or PSTF_MODE_ORDERED");
     if (!n) return PSTF_OK;
     if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "batch too large");
     CK(cudaSetDevice(m->device));
     const cudaStream_t st = (cudaStream_t)stream;
-    Scratch &sc = m->sc;
-    ENSURE(m->words, 6 * n * 8);
-    uint64_t *words = m->words.as<uint64_t>();
-    LAUNCH(k_mdl_encode, grid_for(n, 256), 256, 0, st, keys, u, v, contribution, n, words);
-    const int bb[6] = {0, 0, 0, 0, 0, 0};
-    uint32_t *perm = nullptr;
-    int rc = sort_multiword(sc, words, bb, 6, n, &perm, st);
-    if (rc) return rc;
-    ENSURE(m->head, n * 4);
-    ENSURE(m->uid, n * 4);
-    LAUNCH(k_mdl_heads, grid_for(n, 256), 256, 0, st, words, perm, n, m->head.as<uint32_t>());
-    {
-        size_t bytes = 0;
-        CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, m->head.as<uint32_t>(),
-                                         m->uid.as<uint32_t>(), (int64_t)n, st));
-        ENSURE(sc.cub, bytes);
-        bytes = sc.cub.bytes;
-        ProfScope ps_("cub::DeviceScan", st);
-        CK(cub::DeviceScan::InclusiveSum(sc.cub.p, bytes, m->head.as<uint32_t>(),
-                                         m->uid.as<uint32_t>(), (int64_t)n, st));
-        g_launches.fetch_add(2, std::memory_order_relaxed);
+    if (mode == PSTF_MODE_ATOMIC) {
+        LAUNCH(k_mdl_atomic, grid_for(n, 256), 256, 0, st, m->dev(), keys, u, v, contribution, n);
+        return PSTF_OK;
     }
-    rc = read_small(sc, m->uid.as<uint32_t>() + (n - 1), 4, st);
-    if (rc) return rc;
-    const uint64_t nu = ((uint32_t *)sc.h_small)[0];
-    ENSURE(m->seg, (nu + 1) * 4);
-    ENSURE(m->slot_of, nu * 4);
-    LAUNCH(k_mdl_segs, grid_for(n, 256), 256, 0, st, m->head.as<uint32_t>(),
-           m->uid.as<uint32_t>(), n, m->seg.as<uint32_t>(), nu);
+    ENSURE(m->words, 4 * n * 8);
+    uint64_t *words = m->words.as<uint64_t>();
+    const int bits = 16 + (int)m->cfg.capacity_log2 + 1; /* entry index, cell, and the drop tag */
+    const int shift = 64 - bits;
     const MdlDev d = m->dev();
-    LAUNCH(k_mdl_insert, grid_for(nu, 128), 128, 0, st, d, keys, perm, m->seg.as<uint32_t>(), nu,
-           m->slot_of.as<int32_t>());
-    LAUNCH(k_mdl_fold, grid_for(nu, 128), 128, 0, st, d, perm, m->seg.as<uint32_t>(), nu,
-           m->slot_of.as<int32_t>(), u, v, contribution);
+    LAUNCH(k_mdl_records, grid_for(n, 256), 256, 0, st, d, keys, u, v, contribution, n, shift,
+           words);
+    const int bb[4] = {shift, 0, 0, 0};
+    uint32_t *perm = nullptr;
+    int rc = sort_multiword(m->sc, words, bb, 4, n, &perm, st);
+    if (rc) return rc;
+    LAUNCH(k_mdl_fold, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, contribution);
     return PSTF_OK;
 }
 
@@ -448,8 +462,8 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
     CK(cudaMemsetAsync(m->sums.p, 0, 16, st));
     LAUNCH(k_mdl_sums, (unsigned)sm_count() * 2, 256, 0, st, d, m->sums.as<double>());
     const uint64_t cap = (uint64_t)m->mask + 1;
-    LAUNCH(k_mdl_blend, grid_for(cap, 128), 128, 0, st, d, m->sums.as<double>(), t_max, limited,
-           m->cfg.min_samples);
+    LAUNCH(k_mdl_blend, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(), t_max,
+           limited, m->cfg.min_samples);
     CK(cudaMemsetAsync(&m->ctr.as<unsigned long long>()[MC_TOUCHED], 0, 8, st));
     return PSTF_OK;
 }

@@ -119,7 +119,7 @@ def lib():
         "pstf_profile_collect": ([vp, vp, vp, i32, vp], i32),
         "pstf_model_create": ([vp, i32, vp], i32),
         "pstf_model_destroy": ([vp], i32),
-        "pstf_model_apply": ([vp, vp, vp, vp, vp, u64, vp], i32),
+        "pstf_model_apply": ([vp, vp, vp, vp, vp, u64, i32, vp], i32),
         "pstf_model_end_frame": ([vp, vp], i32),
         "pstf_model_lookup_warm": ([vp, vp, u64, vp, vp], i32),
         "pstf_model_lookup_warm_levels": ([vp, vp, vp, vp, vp, u64, vp, vp], i32),

@@ -11,7 +11,7 @@ import ctypes as C
 
 import numpy as np
 
-from .field import PstfError, _check, _ptr, _soa3, _stream, _torch, _vec3, lib
+from .field import MODE_ATOMIC, MODE_ORDERED, PstfError, _check, _ptr, _soa3, _stream, _torch, _vec3, lib
 
 MODEL_ENTRY_DTYPE = np.dtype([("level", "<i4"), ("cell", "<i4", (3,)), ("dir", "<i4", (2,)),
                               ("warm", "<u4"), ("c_old", "<f8"), ("c_new", "<f8"),
@@ -68,14 +68,15 @@ class ModelStore:
             keys = np.ascontiguousarray(keys).view(np.int32).reshape(-1, 7)
         return t.as_tensor(keys).to(device=self._dev(), dtype=t.int32).contiguous()
 
-    def apply(self, keys, u, v, contribution):
-        """applyRecord for every record (estimators.cpp:109-117), in the deterministic order"""
+    def apply(self, keys, u, v, contribution, mode=MODE_ORDERED):
+        """applyRecord for every record (estimators.cpp:109-117).  MODE_ORDERED: the
+        deterministic order, bitwise; MODE_ATOMIC: no sort, sums within 1e-12 relative."""
         k = self._keys(keys)
         uu, vv, cc = self._f64(u), self._f64(v), self._f64(contribution)
         n = k.shape[0]
         if not (uu.numel() == vv.numel() == cc.numel() == n):
             raise PstfError("apply: keys, u, v and contribution must have one entry per record")
-        _check(lib().pstf_model_apply(self._h, _ptr(k), _ptr(uu), _ptr(vv), _ptr(cc), n,
+        _check(lib().pstf_model_apply(self._h, _ptr(k), _ptr(uu), _ptr(vv), _ptr(cc), n, mode,
                                       _stream()))
 
     def end_frame(self):

@@ -124,3 +124,28 @@ def test_model_table_full_counts_drops():
         j = idx[tuple(x["cell"]) + tuple(x["dir"]) + (int(x["level"]),)]
         assert x["records"] == er[j]["records"]
         np.testing.assert_array_equal(wg[i].view(np.uint64), wr[j].view(np.uint64))
+
+
+def test_model_store_atomic_mode():
+    """ATOMIC mode (no sort): entries, counts, warm flags exact; accumulators and weights within
+    1e-12 relative of the canonical order."""
+    rng = np.random.default_rng(123)
+    g = pb.ModelStore(16, 64.0, 8, capacity_log2=12)
+    r = _checker(16, 64.0, 8)
+    for frame in range(3):
+        k, u, v, c, keys = mc.model_records(rng, 20000, 600)
+        g.apply(k, u, v, c, mode=pb.MODE_ATOMIC)
+        r.apply(k, u, v, c)
+        for end in (False, True):
+            if end:
+                g.end_frame()
+                r.end_frame()
+            eg, wg, ag = g.dump()
+            er, wr, ar = r.dump()
+            assert len(eg) == len(er)
+            for f in ("level", "cell", "dir", "warm", "c_old", "c_new", "records", "record_count"):
+                np.testing.assert_array_equal(eg[f], er[f], err_msg=f)
+            np.testing.assert_allclose(eg["total"], er["total"], rtol=1e-12)
+            np.testing.assert_allclose(wg, wr, rtol=1e-12, atol=1e-300)
+            np.testing.assert_allclose(ag, ar, rtol=1e-12, atol=1e-300)
+
