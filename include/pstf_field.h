@@ -322,18 +322,24 @@ uint64_t pstf_kernel_launch_count(void);
 int pstf_profile_enable(int on);
 int pstf_profile_collect(char *names, double *ms, uint64_t *counts, int n_max, int *n_out);
 
-/* ---- CV-profile / guiding model store -------------------------------
- * ModelStore (estimators.h:124-150, estimators.cpp:104-144) with the DirGrid model
- * (models.h:30-52, models.cpp:16-94): the ModelKind::Grid store, which is what the CV profiles
- * always use (estimators.cpp:336-339) and the guiding models' default kind (models.h:186).
+/* ---- CV-profile / guiding model store ------------------------
+ * ModelStore (estimators.h:124-150, estimators.cpp:104-144) with DirGrid models
+ * (models.h:30-52, models.cpp:16-94; what the CV profiles always use, estimators.cpp:336-339,
+ * and the guiding models' default kind, models.h:186) or SphericalKdTree models
+ * (models.h:59-109, models.cpp:96-298: the split-collapse learner).
  * Keyed by the field's SpatioDirectionalKey with key-field equality (the unordered_map's
  * operator==, field.h:38-41).  The reference map grows without bound; here the table has
  * 2^capacity_log2 entries and records of keys that find no free entry are counted as dropped. */
+enum { PSTF_MODEL_GRID = 0, PSTF_MODEL_KDTREE = 1 }; /* ModelKind (models.h:183); no Gmm */
+
 typedef struct pstf_model_config {
-    int32_t grid_resolution; /* ModelConfig::gridResolution (models.h:187), >= 1 */
-    double t_max;            /* EstimatorConfig::tMax (the blend cap, estimators.cpp:119-144) */
-    int32_t min_samples;     /* minModelSamples / profileMinSamples (warm threshold) */
-    uint32_t capacity_log2;  /* entries in the device table */
+    int32_t kind;               /* PSTF_MODEL_GRID (DirGrid) or PSTF_MODEL_KDTREE */
+    int32_t grid_resolution;    /* ModelConfig::gridResolution (models.h:187), >= 1 */
+    int32_t kd_leaf_count;      /* ModelConfig::kdLeafCount (models.h:188), power of two >= 2 */
+    double kd_split_threshold;  /* ModelConfig::kdSplitThreshold (models.h:189), > 1 */
+    double t_max;               /* EstimatorConfig::tMax (the blend cap, estimators.cpp:119-144) */
+    int32_t min_samples;        /* minModelSamples / profileMinSamples (warm threshold) */
+    uint32_t capacity_log2;     /* entries in the device table */
 } pstf_model_config;
 
 typedef struct pstf_model_store pstf_model_store;
@@ -388,11 +394,15 @@ int pstf_model_sample(const pstf_model_store *m, const int32_t *entry, const dou
                       const double *u2, uint64_t n, double *su, double *sv, double *pdf,
                       void *stream);
 int pstf_model_get_stats(pstf_model_store *m, pstf_model_stats *out);
-/* Host dump of every entry, sorted by key; weights (and accum when non-NULL) receive
- * grid_resolution^2 doubles per entry in the same order.  *count = entries; at most cap
- * are written. */
+/* Host dump of every entry, sorted by key.  Per entry, weights and accum (when non-NULL)
+ * receive S doubles: Grid: the R^2 weights / accumulators; KdTree: each of the 2L-1 nodes'
+ * prob / accum (node order).  *count = entries; at most cap are written. */
 int pstf_model_dump(pstf_model_store *m, pstf_model_entry *entries, double *weights,
                     double *accum, uint64_t cap, uint64_t *count);
+/* KdTree topology in the same entry order: per node {leaf, axis, left, right, parent} int32 and
+ * {split, mass} double (SphericalKdTree::Node, models.h:91-99). */
+int pstf_model_dump_tree(pstf_model_store *m, int32_t *node_i32, double *node_f64, uint64_t cap,
+                         uint64_t *count);
 
 #ifdef __cplusplus
 }

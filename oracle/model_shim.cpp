@@ -1,4 +1,5 @@
-// model_shim.cpp — extern "C" wrapper around the UNMODIFIED reference ModelStore / DirGrid
+// model_shim.cpp — extern "C" wrapper around the UNMODIFIED reference ModelStore with DirGrid /
+// SphericalKdTree models
 // (TEST INFRASTRUCTURE ONLY; built into oracle/_ref/libpstf_model_ref.so by oracle/Makefile).
 //
 // /root/reference/proj/core/src/estimators.cpp (ModelStore, estimators.cpp:104-144) and
@@ -62,10 +63,12 @@ static SpatioDirectionalKey toKey(const pm_key &k) {
     return s;
 }
 
-void *pm_create(int res, double t_max, int min_samples) {
+void *pm_create(int kind, int res, int leaves, double tsplit, double t_max, int min_samples) {
     ModelConfig cfg;
-    cfg.kind = ModelKind::Grid;
+    cfg.kind = kind == 1 ? ModelKind::KdTree : ModelKind::Grid;
     cfg.gridResolution = res;
+    cfg.kdLeafCount = leaves;
+    cfg.kdSplitThreshold = tsplit;
     return new ModelStore(cfg, t_max, min_samples);
 }
 
@@ -114,7 +117,11 @@ void pm_sample(void *m, const pm_key *k, double u1, double u2, double *su, doubl
         *pdf = 1.0;
         return;
     }
-    Sample2D s = std::get<DirGrid>(d->m_impl).sample(Vec2{u1, u2});
+    Sample2D s;
+    if (const DirGrid *g = std::get_if<DirGrid>(&d->m_impl))
+        s = g->sample(Vec2{u1, u2});
+    else
+        s = std::get<SphericalKdTree>(d->m_impl).sample(Vec2{u1, u2});
     *su = s.uv.x;
     *sv = s.uv.y;
     *pdf = s.pdf;
@@ -134,7 +141,6 @@ int64_t pm_dump(void *m, pm_entry *out, double *weights, double *accum, int64_t 
     for (int64_t i = 0; i < k; ++i) {
         const SpatioDirectionalKey &key = ord[size_t(i)]->first;
         const ModelStore::Entry &e = ord[size_t(i)]->second;
-        const DirGrid &g = std::get<DirGrid>(e.model->m_impl);
         pm_entry &o = out[i];
         std::memset(&o, 0, sizeof(o));
         o.level = key.level;
@@ -144,11 +150,51 @@ int64_t pm_dump(void *m, pm_entry *out, double *weights, double *accum, int64_t 
         o.c_old = e.cOld;
         o.c_new = e.cNew;
         o.records = e.records;
-        o.record_count = g.m_recordCount;
-        o.total = g.m_total;
-        const size_t r2 = g.m_weights.size();
-        if (weights) std::copy(g.m_weights.begin(), g.m_weights.end(), weights + size_t(i) * r2);
-        if (accum) std::copy(g.m_accum.begin(), g.m_accum.end(), accum + size_t(i) * r2);
+        if (const DirGrid *g = std::get_if<DirGrid>(&e.model->m_impl)) {
+            o.record_count = g->m_recordCount;
+            o.total = g->m_total;
+            const size_t r2 = g->m_weights.size();
+            if (weights) std::copy(g->m_weights.begin(), g->m_weights.end(), weights + size_t(i) * r2);
+            if (accum) std::copy(g->m_accum.begin(), g->m_accum.end(), accum + size_t(i) * r2);
+        } else { // SphericalKdTree: per node prob / accum in node order
+            const SphericalKdTree &t = std::get<SphericalKdTree>(e.model->m_impl);
+            o.record_count = t.m_recordCount;
+            o.total = 0.0;
+            const size_t nn = t.m_nodes.size();
+            for (size_t j = 0; j < nn; ++j) {
+                if (weights) weights[size_t(i) * nn + j] = t.m_nodes[j].prob;
+                if (accum) accum[size_t(i) * nn + j] = t.m_nodes[j].accum;
+            }
+        }
+    }
+    return n;
+}
+
+// k-d tree topology (SphericalKdTree::Node, models.h:91-99), same entry order as pm_dump
+int64_t pm_dump_tree(void *m, int32_t *node_i32, double *node_f64, int64_t cap) {
+    ModelStore *st = static_cast<ModelStore *>(m);
+    std::vector<const std::pair<const SpatioDirectionalKey, ModelStore::Entry> *> ord;
+    for (const auto &kv : st->m_map) ord.push_back(&kv);
+    std::sort(ord.begin(), ord.end(), [](auto *a, auto *b) {
+        const SpatioDirectionalKey &x = a->first, &y = b->first;
+        return std::tie(x.level, x.cell[0], x.cell[1], x.cell[2], x.dirCell[0], x.dirCell[1]) <
+               std::tie(y.level, y.cell[0], y.cell[1], y.cell[2], y.dirCell[0], y.dirCell[1]);
+    });
+    const int64_t n = int64_t(ord.size()), k = std::min(n, cap);
+    for (int64_t i = 0; i < k; ++i) {
+        const SphericalKdTree &t = std::get<SphericalKdTree>(ord[size_t(i)]->second.model->m_impl);
+        const size_t nn = t.m_nodes.size();
+        for (size_t j = 0; j < nn; ++j) {
+            const auto &nd = t.m_nodes[j];
+            int32_t *o = node_i32 + (size_t(i) * nn + j) * 5;
+            o[0] = nd.leaf;
+            o[1] = nd.axis;
+            o[2] = nd.left;
+            o[3] = nd.right;
+            o[4] = nd.parent;
+            node_f64[(size_t(i) * nn + j) * 2] = nd.split;
+            node_f64[(size_t(i) * nn + j) * 2 + 1] = nd.mass;
+        }
     }
     return n;
 }

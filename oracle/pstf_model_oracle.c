@@ -1,8 +1,10 @@
 /* pstf_model_oracle.c — CPU restatement of the reference's ModelStore with DirGrid models
- * (TEST INFRASTRUCTURE ONLY: the checker of the B200 model store, never the product path).
+ * and SphericalKdTree models (TEST INFRASTRUCTURE ONLY: the checker of the B200 model store,
+ * never the product path).
  *
  *   ModelStore      estimators.h:124-150, estimators.cpp:104-144
  *   DirGrid         models.h:30-52, models.cpp:16-94
+ *   SphericalKdTree models.h:59-109, models.cpp:96-298
  *   record order    estimators.cpp:625-645 (deterministic mode: sorted, then applied in order)
  *
  * Pinned bitwise against the reference's own ModelStore compiled in place
@@ -16,15 +18,28 @@
 
 #include "pstf_oracle.h"
 
+/* SphericalKdTree::Node (models.h:91-99) */
+typedef struct {
+    int leaf, axis;
+    double split;
+    int32_t left, right, parent;
+    double prob, accum, mass;
+} pm_node;
+
 typedef struct {
     po_key key; /* checksum ignored: equality on the key fields (field.h:38-41) */
-    double *w, *acc;
+    double *w, *acc; /* DirGrid */
+    pm_node *nodes;  /* SphericalKdTree: 2L-1 nodes */
     double total, c_old, c_new;
     uint64_t records, rec_count;
     int warm, used;
 } pm_entry;
 
 struct po_model {
+    int kind; /* 0 DirGrid, 1 SphericalKdTree (ModelKind, models.h:183) */
+    int leaves;
+    double tsplit;
+    pm_node *tmpl; /* the constructor's uniform tree */
     int res;
     double t_max;
     int min_samples;
@@ -39,14 +54,64 @@ static int pm_eq(const po_key *a, const po_key *b) {
            a->cell[2] == b->cell[2] && a->dir[0] == b->dir[0] && a->dir[1] == b->dir[1];
 }
 
-po_model *po_model_create(int res, double t_max, int min_samples) {
+/* SphericalKdTree(leafCount) (models.cpp:96-127): children are appended when their parent is
+ * visited, the left subtree is built first, axes alternate with depth, splits at the midpoint */
+static int pm_kd_add(pm_node *t, int *n) {
+    pm_node *z = &t[*n];
+    memset(z, 0, sizeof(*z));
+    z->leaf = 1;
+    z->split = 0.5;
+    z->left = z->right = z->parent = -1;
+    return (*n)++;
+}
+
+static void pm_kd_build(pm_node *t, int *n, int node, int depth, int below, int leaves) {
+    if (below == 1) {
+        t[node].leaf = 1;
+        t[node].prob = 1.0 / leaves;
+        return;
+    }
+    int l = pm_kd_add(t, n), r = pm_kd_add(t, n);
+    t[node].leaf = 0;
+    t[node].axis = depth & 1;
+    t[node].split = 0.5;
+    t[node].left = l;
+    t[node].right = r;
+    t[l].parent = node;
+    t[r].parent = node;
+    pm_kd_build(t, n, l, depth + 1, below / 2, leaves);
+    pm_kd_build(t, n, r, depth + 1, below / 2, leaves);
+}
+
+/* refreshMass (models.cpp:129-138) */
+static double pm_kd_mass(pm_node *t, int n) {
+    t[n].mass = t[n].leaf ? t[n].prob : pm_kd_mass(t, t[n].left) + pm_kd_mass(t, t[n].right);
+    return t[n].mass;
+}
+
+po_model *po_model_create(int kind, int res, int leaves, double tsplit, double t_max,
+                          int min_samples) {
     po_model *m = (po_model *)calloc(1, sizeof(po_model));
+    m->kind = kind;
     m->res = res;
+    m->leaves = leaves;
+    m->tsplit = tsplit;
     m->t_max = t_max;
     m->min_samples = min_samples;
     m->cap = 1024;
     m->tab = (pm_entry *)calloc(m->cap, sizeof(pm_entry));
+    if (kind == 1) {
+        int n = 0;
+        m->tmpl = (pm_node *)calloc((size_t)(2 * leaves - 1), sizeof(pm_node));
+        pm_kd_add(m->tmpl, &n);
+        pm_kd_build(m->tmpl, &n, 0, 0, leaves, leaves);
+        pm_kd_mass(m->tmpl, 0);
+    }
     return m;
+}
+
+static size_t pm_slots(const po_model *m) {
+    return m->kind == 1 ? (size_t)(2 * m->leaves - 1) : (size_t)m->res * m->res;
 }
 
 void po_model_destroy(po_model *m) {
@@ -54,8 +119,10 @@ void po_model_destroy(po_model *m) {
         if (m->tab[i].used) {
             free(m->tab[i].w);
             free(m->tab[i].acc);
+            free(m->tab[i].nodes);
         }
     free(m->tab);
+    free(m->tmpl);
     free(m);
 }
 
@@ -92,11 +159,17 @@ static pm_entry *pm_get_or_create(po_model *m, const po_key *k) {
     memset(e, 0, sizeof(*e));
     e->used = 1;
     e->key = *k;
-    size_t r2 = (size_t)m->res * m->res;
-    e->w = (double *)malloc(r2 * sizeof(double));
-    e->acc = (double *)calloc(r2, sizeof(double));
-    for (size_t j = 0; j < r2; ++j) e->w[j] = 1.0 / ((double)m->res * m->res);
-    e->total = 1.0;
+    if (m->kind == 1) {
+        size_t nn = pm_slots(m);
+        e->nodes = (pm_node *)malloc(nn * sizeof(pm_node));
+        memcpy(e->nodes, m->tmpl, nn * sizeof(pm_node));
+    } else {
+        size_t r2 = (size_t)m->res * m->res;
+        e->w = (double *)malloc(r2 * sizeof(double));
+        e->acc = (double *)calloc(r2, sizeof(double));
+        for (size_t j = 0; j < r2; ++j) e->w[j] = 1.0 / ((double)m->res * m->res);
+        e->total = 1.0;
+    }
     m->size++;
     return e;
 }
@@ -137,11 +210,116 @@ static int pm_rec_cmp(const void *pa, const void *pb) {
     return pm_cmp_d(a->c, b->c);
 }
 
+static double pm_lerp(double a, double b, double t) { return a + (b - a) * t; } /* vecmath.h:22 */
+
+/* findLeaf (models.cpp:140-159) */
+static int pm_kd_find(const pm_node *t, double u, double v, double lo[2], double hi[2]) {
+    lo[0] = lo[1] = 0.0;
+    hi[0] = hi[1] = 1.0;
+    int node = 0;
+    while (!t[node].leaf) {
+        const pm_node *n = &t[node];
+        double split_abs = pm_lerp(lo[n->axis], hi[n->axis], n->split);
+        double coord = n->axis == 0 ? u : v;
+        if (coord <= split_abs) {
+            hi[n->axis] = split_abs;
+            node = n->left;
+        } else {
+            lo[n->axis] = split_abs;
+            node = n->right;
+        }
+    }
+    return node;
+}
+
+static double pm_max(double a, double b) { return a < b ? b : a; } /* std::max */
+
+/* SphericalKdTree::endFrame (models.cpp:202-298) */
+static void pm_kd_end_frame(po_model *m, pm_node *t, double blend) {
+    int nn = 2 * m->leaves - 1;
+    double total = 0.0;
+    for (int i = 0; i < nn; ++i)
+        if (t[i].leaf) total += t[i].accum;
+    if (total > 0.0) {
+        double floor_prob = 1e-4 / m->leaves, norm_sum = 0.0;
+        for (int i = 0; i < nn; ++i)
+            if (t[i].leaf) norm_sum += pm_max(t[i].accum / total, floor_prob);
+        for (int i = 0; i < nn; ++i) {
+            if (!t[i].leaf) continue;
+            double target = pm_max(t[i].accum / total, floor_prob) / norm_sum;
+            t[i].prob = (1.0 - blend) * t[i].prob + blend * target;
+        }
+        double prob_sum = 0.0;
+        for (int i = 0; i < nn; ++i)
+            if (t[i].leaf) prob_sum += t[i].prob;
+        for (int i = 0; i < nn; ++i)
+            if (t[i].leaf) t[i].prob /= prob_sum;
+    }
+    int l_max = -1, p_min = -1;
+    double p_max = -1.0, p_min_mass = 2.0;
+    for (int i = 0; i < nn; ++i)
+        if (t[i].leaf && t[i].prob > p_max) {
+            p_max = t[i].prob;
+            l_max = i;
+        }
+    for (int i = 0; i < nn; ++i) {
+        const pm_node *n = &t[i];
+        if (n->leaf || !t[n->left].leaf || !t[n->right].leaf) continue;
+        double mass = t[n->left].prob + t[n->right].prob;
+        if (mass < p_min_mass) {
+            p_min_mass = mass;
+            p_min = i;
+        }
+    }
+    if (l_max >= 0 && p_min >= 0 && t[l_max].parent != p_min && p_max > m->tsplit * p_min_mass) {
+        int fl = t[p_min].left, fr = t[p_min].right;
+        t[p_min].leaf = 1;
+        t[p_min].prob = p_min_mass;
+        t[p_min].accum = 0.0;
+        t[p_min].left = t[p_min].right = -1;
+        int chain[1024], nc = 0;
+        for (int n = l_max; n != -1; n = t[n].parent) chain[nc++] = n;
+        double lo[2] = {0.0, 0.0}, hi[2] = {1.0, 1.0};
+        for (int i = nc - 1; i >= 1; --i) {
+            const pm_node *n = &t[chain[i]];
+            double split_abs = pm_lerp(lo[n->axis], hi[n->axis], n->split);
+            if (chain[i - 1] == n->left)
+                hi[n->axis] = split_abs;
+            else
+                lo[n->axis] = split_abs;
+        }
+        pm_node *hot = &t[l_max];
+        hot->leaf = 0;
+        hot->axis = (hi[0] - lo[0]) >= (hi[1] - lo[1]) ? 0 : 1;
+        hot->split = 0.5;
+        hot->left = fl;
+        hot->right = fr;
+        int kids[2] = {fl, fr};
+        for (int c = 0; c < 2; ++c) {
+            pm_node *z = &t[kids[c]];
+            memset(z, 0, sizeof(*z));
+            z->split = 0.5;
+            z->left = z->right = -1;
+            z->leaf = 1;
+            z->prob = p_max * 0.5;
+            z->parent = l_max;
+        }
+        hot->prob = 0.0;
+    }
+    for (int i = 0; i < nn; ++i) t[i].accum = 0.0;
+    pm_kd_mass(t, 0);
+}
+
 /* applyRecord (estimators.cpp:109-117) with DirGrid::record (models.cpp:30-35) */
 static void pm_apply_one(po_model *m, const po_key *k, double u, double v, double c) {
     pm_entry *e = pm_get_or_create(m, k);
-    if (c >= 0.0 && isfinite(c)) {
-        e->acc[pm_cell(m->res, u, v)] += c;
+    if (c >= 0.0 && isfinite(c)) { /* DirGrid::record / SphericalKdTree::record (models.cpp:161-167) */
+        if (m->kind == 1) {
+            double lo[2], hi[2];
+            e->nodes[pm_kd_find(e->nodes, u, v, lo, hi)].accum += c;
+        } else {
+            e->acc[pm_cell(m->res, u, v)] += c;
+        }
         e->rec_count++;
     }
     e->c_new += 1.0;
@@ -180,6 +358,10 @@ void po_model_end_frame(po_model *m) {
         if (!e->used || e->c_new <= 0.0) continue;
         double alpha = sqrt(e->c_new / (e->c_old + e->c_new));
         if (limited && alpha < 1.0 / m->t_max) alpha = 1.0 / m->t_max;
+        if (m->kind == 1) {
+            pm_kd_end_frame(m, e->nodes, alpha);
+            goto close;
+        }
         double s = 0.0;
         for (size_t j = 0; j < r2; ++j) s += e->acc[j];
         if (s > 0.0) {
@@ -189,6 +371,7 @@ void po_model_end_frame(po_model *m) {
             for (size_t j = 0; j < r2; ++j) e->total += e->w[j];
         }
         memset(e->acc, 0, r2 * sizeof(double));
+    close:
         e->c_old += e->c_new;
         if (limited && cap < e->c_old) e->c_old = cap;
         e->c_new = 0.0;
@@ -201,6 +384,12 @@ void po_model_end_frame(po_model *m) {
 double po_model_pdf(const po_model *m, const po_key *k, double u, double v, int *found) {
     const pm_entry *e = pm_find(m, k);
     *found = e && e->warm;
+    if (*found && m->kind == 1) { /* SphericalKdTree::pdf (models.cpp:169-174) */
+        double lo[2], hi[2];
+        int leaf = pm_kd_find(e->nodes, u, v, lo, hi);
+        double area = (hi[0] - lo[0]) * (hi[1] - lo[1]);
+        return area > 0.0 ? e->nodes[leaf].prob / area : 0.0;
+    }
     if (!*found || e->total <= 0.0) return 1.0;
     return e->w[pm_cell(m->res, u, v)] / e->total * (double)m->res * m->res;
 }
@@ -215,6 +404,35 @@ void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, d
                      double *sv, double *pdf, int *found) {
     const pm_entry *e = pm_find(m, k);
     *found = e && e->warm;
+    if (*found && m->kind == 1) { /* SphericalKdTree::sample (models.cpp:176-200) */
+        const pm_node *t = e->nodes;
+        const double below_one = nextafter(1.0, 0.0);
+        double r[2] = {u1, u2}, lo[2] = {0.0, 0.0}, hi[2] = {1.0, 1.0};
+        int node = 0;
+        while (!t[node].leaf) {
+            const pm_node *n = &t[node];
+            double mass = n->mass;
+            double left_frac = mass > 0.0 ? t[n->left].mass / mass : 0.5;
+            double split_abs = pm_lerp(lo[n->axis], hi[n->axis], n->split);
+            double *coord = &r[n->axis];
+            if (left_frac > 0.0 && (*coord < left_frac || left_frac >= 1.0)) {
+                double q = *coord / left_frac;
+                *coord = below_one < q ? below_one : q;
+                hi[n->axis] = split_abs;
+                node = n->left;
+            } else {
+                double q = (*coord - left_frac) / (1.0 - left_frac);
+                *coord = below_one < q ? below_one : q;
+                lo[n->axis] = split_abs;
+                node = n->right;
+            }
+        }
+        *su = pm_lerp(lo[0], hi[0], r[0]);
+        *sv = pm_lerp(lo[1], hi[1], r[1]);
+        double area = (hi[0] - lo[0]) * (hi[1] - lo[1]);
+        *pdf = area > 0.0 ? t[node].prob / area : 0.0;
+        return;
+    }
     if (!*found || e->total <= 0.0) {
         *su = u1;
         *sv = u2;
@@ -269,7 +487,7 @@ size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, do
     for (size_t i = 0; i < m->cap; ++i)
         if (m->tab[i].used) ord[n++] = &m->tab[i];
     qsort(ord, n, sizeof(void *), pm_entry_cmp);
-    size_t r2 = (size_t)m->res * m->res, k = n < cap ? n : cap;
+    size_t r2 = pm_slots(m), k = n < cap ? n : cap;
     for (size_t i = 0; i < k; ++i) {
         const pm_entry *e = ord[i];
         po_model_entry *o = &out[i];
@@ -282,10 +500,36 @@ size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, do
         o->c_new = e->c_new;
         o->records = e->records;
         o->record_count = e->rec_count;
-        o->total = e->total;
-        if (weights) memcpy(weights + i * r2, e->w, r2 * sizeof(double));
-        if (accum) memcpy(accum + i * r2, e->acc, r2 * sizeof(double));
+        o->total = m->kind == 1 ? 0.0 : e->total;
+        for (size_t j = 0; j < r2; ++j) {
+            if (weights) weights[i * r2 + j] = m->kind == 1 ? e->nodes[j].prob : e->w[j];
+            if (accum) accum[i * r2 + j] = m->kind == 1 ? e->nodes[j].accum : e->acc[j];
+        }
     }
+    free(ord);
+    return n;
+}
+
+/* k-d tree topology, same entry order: {leaf, axis, left, right, parent}, {split, mass} */
+size_t po_model_dump_tree(const po_model *m, int32_t *node_i32, double *node_f64, size_t cap) {
+    const pm_entry **ord = (const pm_entry **)malloc((m->size ? m->size : 1) * sizeof(void *));
+    size_t n = 0;
+    for (size_t i = 0; i < m->cap; ++i)
+        if (m->tab[i].used) ord[n++] = &m->tab[i];
+    qsort(ord, n, sizeof(void *), pm_entry_cmp);
+    size_t nn = pm_slots(m), k = n < cap ? n : cap;
+    for (size_t i = 0; i < k && m->kind == 1; ++i)
+        for (size_t j = 0; j < nn; ++j) {
+            const pm_node *t = &ord[i]->nodes[j];
+            int32_t *o = node_i32 + (i * nn + j) * 5;
+            o[0] = t->leaf;
+            o[1] = t->axis;
+            o[2] = t->left;
+            o[3] = t->right;
+            o[4] = t->parent;
+            node_f64[(i * nn + j) * 2] = t->split;
+            node_f64[(i * nn + j) * 2 + 1] = t->mass;
+        }
     free(ord);
     return n;
 }

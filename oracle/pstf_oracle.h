@@ -116,7 +116,8 @@ typedef struct {
     uint64_t records, record_count;
     double total;
 } po_model_entry; /* == pstf_model_entry */
-po_model *po_model_create(int res, double t_max, int min_samples);
+po_model *po_model_create(int kind, int res, int leaves, double tsplit, double t_max,
+                          int min_samples); /* kind 0 DirGrid, 1 SphericalKdTree */
 void po_model_destroy(po_model *m);
 void po_model_apply(po_model *m, const po_key *keys, const double *u, const double *v,
                     const double *c, size_t n);
@@ -126,6 +127,7 @@ void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, d
                      double *sv, double *pdf, int *found);
 size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, double *accum,
                      size_t cap);
+size_t po_model_dump_tree(const po_model *m, int32_t *node_i32, double *node_f64, size_t cap);
 /* snapshot restore, the semantics of pstf_field_restore (include/pstf_field.h) */
 void po_restore(po_store *s, const po_snapshot_record *recs, size_t n);
 

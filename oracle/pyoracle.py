@@ -491,9 +491,10 @@ class _ModelBase:
     (OracleModelStore) or the reference compiled in place (RefModelStore)."""
     P = ""
 
-    def __init__(self, res=16, t_max=64.0, min_samples=32):
-        self.res, self.r2 = res, res * res
-        self.h = self._fn("create")(res, t_max, min_samples)
+    def __init__(self, res=16, t_max=64.0, min_samples=32, kind=0, leaves=64, tsplit=4.0):
+        self.kind = kind
+        self.res, self.r2 = res, (2 * leaves - 1 if kind == 1 else res * res)
+        self.h = self._fn("create")(kind, res, leaves, tsplit, t_max, min_samples)
 
     def _fn(self, name):
         return getattr(self.lib, self.P + name)
@@ -540,11 +541,26 @@ class _ModelBase:
         self._fn("dump")(self.h, _p(e), _p(w), _p(a), n)
         return e[:n], w[:n], a[:n]
 
+    def _initial_parents(self, leaves):
+        """parent of every node of the constructor's uniform tree (one fresh entry)"""
+        k = np.zeros(1, KEY_DTYPE)
+        self.apply(k, [0.5], [0.5], [0.0])
+        return self.dump_tree()[0][0, :, 4]
+
+    def dump_tree(self):
+        """k-d tree topology: (n, 2L-1, 5) int32 {leaf, axis, left, right, parent},
+        (n, 2L-1, 2) float64 {split, mass}"""
+        n = self._fn("dump")(self.h, None, None, None, 0)
+        ti = np.zeros((max(n, 1), self.r2, 5), np.int32)
+        tf = np.zeros((max(n, 1), self.r2, 2))
+        self._fn("dump_tree")(self.h, _p(ti), _p(tf), n)
+        return ti[:n], tf[:n]
+
 
 def _type_model_lib(lib, p, n_t):
     vp, d, i32 = C.c_void_p, C.c_double, C.c_int
     getattr(lib, p + "create").restype = vp
-    getattr(lib, p + "create").argtypes = [i32, d, i32]
+    getattr(lib, p + "create").argtypes = [i32, i32, i32, d, d, i32]
     getattr(lib, p + "destroy").argtypes = [vp]
     getattr(lib, p + "apply").argtypes = [vp, vp, vp, vp, vp, n_t]
     getattr(lib, p + "end_frame").argtypes = [vp]
@@ -553,6 +569,8 @@ def _type_model_lib(lib, p, n_t):
     getattr(lib, p + "sample").argtypes = [vp, vp, d, d, vp, vp, vp, vp]
     getattr(lib, p + "dump").argtypes = [vp, vp, vp, vp, n_t]
     getattr(lib, p + "dump").restype = n_t
+    getattr(lib, p + "dump_tree").argtypes = [vp, vp, vp, n_t]
+    getattr(lib, p + "dump_tree").restype = n_t
 
 
 class OracleModelStore(_ModelBase):

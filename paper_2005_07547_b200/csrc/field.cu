@@ -26,6 +26,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <tuple>
 #include <mutex>
 #include <new>
 #include <string>

@@ -25,15 +25,24 @@ struct ModelEnt {
     uint32_t warm, touched;
 };
 
+/* SphericalKdTree::Node (models.h:91-99) minus prob/accum, which live in w/acc */
+struct KdNode {
+    double split, mass;
+    int32_t left, right, parent;
+    uint8_t leaf, axis;
+};
+
 struct MdlDev {
     uint32_t *state;
     KeyFields *keyf;
     ModelEnt *ent;
-    double *w, *acc;
+    double *w, *acc; /* ns per entry: Grid weights / accumulators, or KdTree node prob / accum */
+    KdNode *kn;      /* KdTree: ns nodes per entry; entry `mask + 1` holds the initial tree */
     unsigned long long *ctr; /* [0] entries, [1] dropped records, [2] touched-list length */
     uint32_t *tlist;
     uint32_t mask;
-    int res, r2;
+    int kind, res, ns, leaves; /* ns: slots per entry (R^2, or 2L-1 nodes) */
+    double tsplit;
 };
 
 enum { MC_ENTRIES = 0, MC_DROPPED = 1, MC_TOUCHED = 2, MC_N = 4 };
@@ -42,8 +51,8 @@ struct pstf_model_store {
     pstf_model_config cfg;
     int device = 0;
     uint32_t mask = 0;
-    int r2 = 0;
-    DBuf state, keyf, ent, w, acc, ctr, tlist, sums;
+    int ns = 0;
+    DBuf state, keyf, ent, w, acc, kn, ctr, tlist, sums;
     Scratch sc;
     DBuf words;
     MdlDev dev() const {
@@ -53,11 +62,15 @@ struct pstf_model_store {
         d.ent = ent.as<ModelEnt>();
         d.w = w.as<double>();
         d.acc = acc.as<double>();
+        d.kn = kn.as<KdNode>();
         d.ctr = ctr.as<unsigned long long>();
         d.tlist = tlist.as<uint32_t>();
         d.mask = mask;
+        d.kind = cfg.kind;
         d.res = cfg.grid_resolution;
-        d.r2 = r2;
+        d.ns = ns;
+        d.leaves = cfg.kd_leaf_count;
+        d.tsplit = cfg.kd_split_threshold;
         return d;
     }
 };
@@ -95,6 +108,149 @@ __device__ __forceinline__ uint64_t ord_f64(double d) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
 }
 
+/* ---- SphericalKdTree (models.cpp:96-298) on one entry's node arrays ---- */
+__device__ __forceinline__ double lerp_ref(double a, double b, double t) { /* vecmath.h:22 */
+    return a + (b - a) * t;
+}
+
+__device__ __forceinline__ double min_ref(double a, double b) { return b < a ? b : a; } /* std::min */
+__device__ __forceinline__ double max_ref(double a, double b) { return a < b ? b : a; } /* std::max */
+
+/* findLeaf (models.cpp:140-159): boundary ties go to the lower child */
+__device__ int kd_find_leaf(const KdNode *K, double u, double v, double2 *lo_out, double2 *hi_out) {
+    double2 lo = make_double2(0.0, 0.0), hi = make_double2(1.0, 1.0);
+    int node = 0; /* m_root */
+    while (!K[node].leaf) {
+        const KdNode n = K[node];
+        const double split_abs = n.axis == 0 ? lerp_ref(lo.x, hi.x, n.split)
+                                             : lerp_ref(lo.y, hi.y, n.split);
+        const double coord = n.axis == 0 ? u : v;
+        if (coord <= split_abs) {
+            if (n.axis == 0) hi.x = split_abs; else hi.y = split_abs;
+            node = n.left;
+        } else {
+            if (n.axis == 0) lo.x = split_abs; else lo.y = split_abs;
+            node = n.right;
+        }
+    }
+    if (lo_out) *lo_out = lo;
+    if (hi_out) *hi_out = hi;
+    return node;
+}
+
+/* refreshMass (models.cpp:129-138): mass = prob at leaves, left + right above; computed in
+ * reverse breadth-first order (children before parents), each sum being the same single add */
+__device__ void kd_refresh_mass(KdNode *K, const double *P, int nn) {
+    int order[511];
+    int head = 0, tail = 0;
+    order[tail++] = 0;
+    while (head < tail) {
+        const int n = order[head++];
+        if (!K[n].leaf) {
+            order[tail++] = K[n].left;
+            order[tail++] = K[n].right;
+        }
+    }
+    for (int i = tail - 1; i >= 0; --i) {
+        const int n = order[i];
+        K[n].mass = K[n].leaf ? P[n] : K[K[n].left].mass + K[K[n].right].mass;
+    }
+}
+
+/* SphericalKdTree::endFrame (models.cpp:202-298): blend toward the frame's floored,
+ * normalized leaf sums, renormalize, then one split-collapse step; every loop in node order */
+__device__ void kd_end_frame(KdNode *K, double *P, double *A, int nn, int leaves, double blend,
+                             double tsplit) {
+    double total = 0.0;
+    for (int i = 0; i < nn; ++i)
+        if (K[i].leaf) total += A[i];
+    if (total > 0.0) {
+        const double floor_prob = 1e-4 / leaves;
+        double norm_sum = 0.0;
+        for (int i = 0; i < nn; ++i)
+            if (K[i].leaf) norm_sum += max_ref(A[i] / total, floor_prob);
+        for (int i = 0; i < nn; ++i) {
+            if (!K[i].leaf) continue;
+            const double target = max_ref(A[i] / total, floor_prob) / norm_sum;
+            P[i] = (1.0 - blend) * P[i] + blend * target;
+        }
+        double prob_sum = 0.0;
+        for (int i = 0; i < nn; ++i)
+            if (K[i].leaf) prob_sum += P[i];
+        for (int i = 0; i < nn; ++i)
+            if (K[i].leaf) P[i] /= prob_sum;
+    }
+    int l_max = -1;
+    double p_max = -1.0;
+    for (int i = 0; i < nn; ++i)
+        if (K[i].leaf && P[i] > p_max) {
+            p_max = P[i];
+            l_max = i;
+        }
+    int p_min = -1;
+    double p_min_mass = 2.0;
+    for (int i = 0; i < nn; ++i) {
+        const KdNode &n = K[i];
+        if (n.leaf || !K[n.left].leaf || !K[n.right].leaf) continue;
+        const double mass = P[n.left] + P[n.right];
+        if (mass < p_min_mass) {
+            p_min_mass = mass;
+            p_min = i;
+        }
+    }
+    if (l_max >= 0 && p_min >= 0 && K[l_max].parent != p_min && p_max > tsplit * p_min_mass) {
+        const int freed_l = K[p_min].left, freed_r = K[p_min].right;
+        K[p_min].leaf = 1; /* the coldest leaf pair collapses into its parent */
+        P[p_min] = p_min_mass;
+        A[p_min] = 0.0;
+        K[p_min].left = K[p_min].right = -1;
+        /* the hot leaf's rectangle, from the root down its ancestor chain */
+        int chain[512];
+        int nc = 0;
+        for (int n = l_max; n != -1; n = K[n].parent) chain[nc++] = n;
+        double2 lo = make_double2(0.0, 0.0), hi = make_double2(1.0, 1.0);
+        for (int i = nc - 1; i >= 1; --i) {
+            const KdNode &n = K[chain[i]];
+            const double split_abs = n.axis == 0 ? lerp_ref(lo.x, hi.x, n.split)
+                                                 : lerp_ref(lo.y, hi.y, n.split);
+            const bool to_left = chain[i - 1] == n.left;
+            if (n.axis == 0) {
+                if (to_left) hi.x = split_abs; else lo.x = split_abs;
+            } else {
+                if (to_left) hi.y = split_abs; else lo.y = split_abs;
+            }
+        }
+        KdNode &hot = K[l_max]; /* splits at the midpoint of its longer axis */
+        hot.leaf = 0;
+        hot.axis = (hi.x - lo.x) >= (hi.y - lo.y) ? 0 : 1;
+        hot.split = 0.5;
+        hot.left = freed_l;
+        hot.right = freed_r;
+        const int kids[2] = {freed_l, freed_r};
+        for (int c : kids) {
+            KdNode z;
+            z.split = 0.5;
+            z.mass = 0.0;
+            z.left = z.right = -1;
+            z.parent = l_max;
+            z.leaf = 1;
+            z.axis = 0;
+            K[c] = z;
+            P[c] = p_max * 0.5;
+            A[c] = 0.0;
+        }
+        P[l_max] = 0.0;
+    }
+    for (int i = 0; i < nn; ++i) A[i] = 0.0;
+    kd_refresh_mass(K, P, nn);
+}
+
+/* accumulator slot of a record: the DirGrid cell or the k-d tree leaf */
+__device__ __forceinline__ int mdl_slot(const MdlDev &m, uint32_t e, double u, double v) {
+    if (m.kind == PSTF_MODEL_GRID) return mdl_cell(u, v, m.res);
+    return kd_find_leaf(m.kn + (uint64_t)e * m.ns, u, v, nullptr, nullptr);
+}
+
 /* find-or-insert a key (field.h:38-41 equality); -1 when the table is full.  Threads carrying
  * the same new key meet at the entry the first of them claims (same probe sequence; a claimed
  * entry is waited for until published).  A new entry is a fresh DirGrid: uniform weights
@@ -114,10 +270,19 @@ __device__ int32_t mdl_find_or_insert(const MdlDev &m, const KeyFields &k) {
                 z.records = z.rec_count = 0;
                 z.warm = z.touched = 0;
                 m.ent[e] = z;
-                const double w0 = 1.0 / ((double)m.res * m.res);
-                for (int j = 0; j < m.r2; ++j) {
-                    m.w[(uint64_t)e * m.r2 + j] = w0;
-                    m.acc[(uint64_t)e * m.r2 + j] = 0.0;
+                if (m.kind == PSTF_MODEL_GRID) {
+                    const double w0 = 1.0 / ((double)m.res * m.res);
+                    for (int j = 0; j < m.ns; ++j) {
+                        m.w[(uint64_t)e * m.ns + j] = w0;
+                        m.acc[(uint64_t)e * m.ns + j] = 0.0;
+                    }
+                } else { /* the uniform tree (models.cpp:96-127), built once on the host */
+                    const uint64_t t = (uint64_t)(m.mask + 1ull) * m.ns;
+                    for (int j = 0; j < m.ns; ++j) {
+                        m.w[(uint64_t)e * m.ns + j] = m.w[t + j];
+                        m.acc[(uint64_t)e * m.ns + j] = 0.0;
+                        m.kn[(uint64_t)e * m.ns + j] = m.kn[t + j];
+                    }
                 }
                 __threadfence();
                 atomicExch(&m.state[e], 2u);
@@ -143,7 +308,7 @@ __global__ void k_mdl_records(MdlDev m, const pstf_key *keys, const double *u, c
     const int32_t e = mdl_find_or_insert(m, kf_of(keys[i]));
     uint64_t w0 = ~0ull;
     if (e >= 0)
-        w0 = ((uint64_t)e << 16 | (uint32_t)mdl_cell(u[i], v[i], m.res)) << shift;
+        w0 = ((uint64_t)e << 16 | (uint32_t)mdl_slot(m, (uint32_t)e, u[i], v[i])) << shift;
     else
         atomicAdd(&m.ctr[MC_DROPPED], 1ull);
     words[0 * n + i] = w0;
@@ -163,7 +328,7 @@ __global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm
     if (w == ~0ull || (i > 0 && words[perm[i - 1]] == w)) return; /* dropped, or not a run head */
     const uint64_t ec = w >> shift;
     const uint32_t e = (uint32_t)(ec >> 16);
-    double *acc = m.acc + (uint64_t)e * m.r2 + (uint32_t)(ec & 0xffffu);
+    double *acc = m.acc + (uint64_t)e * m.ns + (uint32_t)(ec & 0xffffu);
     double s = *acc;
     unsigned long long cnt = 0, len = 0;
     for (uint64_t j = i; j < n; ++j) {
@@ -199,7 +364,7 @@ __global__ void k_mdl_atomic(MdlDev m, const pstf_key *keys, const double *u, co
         if (e >= 0) {
             const double cv = c[i];
             ok = cv >= 0.0 && isfinite(cv);
-            if (ok) atomicAdd(m.acc + (uint64_t)e * m.r2 + mdl_cell(u[i], v[i], m.res), cv);
+            if (ok) atomicAdd(m.acc + (uint64_t)e * m.ns + mdl_slot(m, (uint32_t)e, u[i], v[i]), cv);
         }
     }
     const unsigned grp = __match_any_sync(0xffffffffu, e);
@@ -252,6 +417,25 @@ __device__ __forceinline__ double warp_ordered_sum(const double *x, int n, unsig
 
 /* endFrame pass 2 (estimators.cpp:129-143) with DirGrid::endFrame (models.cpp:37-50), one warp
  * per touched entry: elementwise blend across lanes, the two grid sums in index order */
+/* ModelStore::endFrame's per-entry step (estimators.cpp:133-142) around the model's own
+ * endFrame: the blend weight first, then cOld, the cap, cNew and warm */
+__device__ __forceinline__ double mdl_alpha(const ModelEnt &x, double t_max, int limited) {
+    double alpha = sqrt(x.c_new / (x.c_old + x.c_new));
+    if (limited) alpha = max_ref(alpha, 1.0 / t_max);
+    return alpha;
+}
+
+__device__ __forceinline__ void mdl_close(ModelEnt &x, const double *sums, double t_max,
+                                          int limited, int min_samples) {
+    const double touched = sums[1];
+    const double cap = limited && touched > 0.0 ? (t_max * t_max - t_max) * (sums[0] / touched)
+                                                : 0.0;
+    x.c_old += x.c_new;
+    if (limited) x.c_old = min_ref(x.c_old, cap);
+    x.c_new = 0.0;
+    x.warm = x.records >= (unsigned long long)(long long)min_samples;
+}
+
 __global__ void k_mdl_blend(MdlDev m, const double *sums, double t_max, int limited,
                             int min_samples) {
     const uint64_t nt = m.ctr[MC_TOUCHED];
@@ -263,32 +447,40 @@ __global__ void k_mdl_blend(MdlDev m, const double *sums, double t_max, int limi
         ModelEnt x = m.ent[e];
         x.touched = 0;
         if (x.c_new > 0.0) {
-            double *w = m.w + (uint64_t)e * m.r2, *acc = m.acc + (uint64_t)e * m.r2;
-            double alpha = sqrt(x.c_new / (x.c_old + x.c_new));
-            if (limited) {
-                const double fl = 1.0 / t_max;
-                alpha = alpha < fl ? fl : alpha; /* std::max */
-            }
-            const double sum = warp_ordered_sum(acc, m.r2, lane);
+            double *w = m.w + (uint64_t)e * m.ns, *acc = m.acc + (uint64_t)e * m.ns;
+            const double alpha = mdl_alpha(x, t_max, limited);
+            const double sum = warp_ordered_sum(acc, m.ns, lane);
             __syncwarp();
             if (sum > 0.0) {
-                for (int j = lane; j < m.r2; j += 32)
+                for (int j = lane; j < m.ns; j += 32)
                     w[j] = (1.0 - alpha) * w[j] + alpha * (acc[j] / sum);
                 __syncwarp();
-                x.total = warp_ordered_sum(w, m.r2, lane);
+                x.total = warp_ordered_sum(w, m.ns, lane);
             }
-            for (int j = lane; j < m.r2; j += 32) acc[j] = 0.0;
-            const double touched = sums[1];
-            const double cap = limited && touched > 0.0
-                                   ? (t_max * t_max - t_max) * (sums[0] / touched)
-                                   : 0.0;
-            x.c_old += x.c_new;
-            if (limited) x.c_old = cap < x.c_old ? cap : x.c_old; /* std::min */
-            x.c_new = 0.0;
-            x.warm = x.records >= (unsigned long long)(long long)min_samples;
+            for (int j = lane; j < m.ns; j += 32) acc[j] = 0.0;
+            mdl_close(x, sums, t_max, limited, min_samples);
         }
         __syncwarp();
         if (lane == 0) m.ent[e] = x;
+    }
+}
+
+/* the same for k-d tree entries: one thread per touched entry (the tree update is sequential) */
+__global__ void k_mdl_blend_kd(MdlDev m, const double *sums, double t_max, int limited,
+                               int min_samples) {
+    const uint64_t nt = m.ctr[MC_TOUCHED];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = m.tlist[i];
+        ModelEnt x = m.ent[e];
+        x.touched = 0;
+        if (x.c_new > 0.0) {
+            const uint64_t b = (uint64_t)e * m.ns;
+            kd_end_frame(m.kn + b, m.w + b, m.acc + b, m.ns, m.leaves,
+                         mdl_alpha(x, t_max, limited), m.tsplit);
+            mdl_close(x, sums, t_max, limited, min_samples);
+        }
+        m.ent[e] = x;
     }
 }
 
@@ -320,12 +512,54 @@ __global__ void k_mdl_lookup_levels(MdlDev m, KeyParams kp, pstf_vec3_soa pos, p
     out[i] = e;
 }
 
-/* DirGrid::pdf (models.cpp:52-56) */
+/* SphericalKdTree::pdf (models.cpp:169-174) */
+__device__ __forceinline__ double kd_pdf(const MdlDev &m, int32_t e, double u, double v) {
+    const uint64_t b = (uint64_t)e * m.ns;
+    double2 lo, hi;
+    const int leaf = kd_find_leaf(m.kn + b, u, v, &lo, &hi);
+    const double area = (hi.x - lo.x) * (hi.y - lo.y);
+    return area > 0.0 ? m.w[b + leaf] / area : 0.0;
+}
+
+/* SphericalKdTree::sample (models.cpp:176-200): hierarchical warping by subtree mass */
+__device__ void kd_sample(const MdlDev &m, int32_t e, double ux, double uy, double *su,
+                          double *sv, double *spdf) {
+    const uint64_t b = (uint64_t)e * m.ns;
+    const KdNode *K = m.kn + b;
+    const double below_one = 0x1.fffffffffffffp-1; /* nexttoward(1.0, 0.0) */
+    double rx = ux, ry = uy;
+    double2 lo = make_double2(0.0, 0.0), hi = make_double2(1.0, 1.0);
+    int node = 0;
+    while (!K[node].leaf) {
+        const KdNode n = K[node];
+        const double mass = n.mass;
+        const double left_frac = mass > 0.0 ? K[n.left].mass / mass : 0.5;
+        double &coord = n.axis == 0 ? rx : ry;
+        const double split_abs = n.axis == 0 ? lerp_ref(lo.x, hi.x, n.split)
+                                             : lerp_ref(lo.y, hi.y, n.split);
+        if (left_frac > 0.0 && (coord < left_frac || left_frac >= 1.0)) {
+            coord = min_ref(coord / left_frac, below_one);
+            if (n.axis == 0) hi.x = split_abs; else hi.y = split_abs;
+            node = n.left;
+        } else {
+            coord = min_ref((coord - left_frac) / (1.0 - left_frac), below_one);
+            if (n.axis == 0) lo.x = split_abs; else lo.y = split_abs;
+            node = n.right;
+        }
+    }
+    *su = lerp_ref(lo.x, hi.x, rx);
+    *sv = lerp_ref(lo.y, hi.y, ry);
+    const double area = (hi.x - lo.x) * (hi.y - lo.y);
+    *spdf = area > 0.0 ? m.w[b + node] / area : 0.0;
+}
+
+/* DirGrid::pdf (models.cpp:52-56) / SphericalKdTree::pdf */
 __device__ __forceinline__ double mdl_pdf(const MdlDev &m, int32_t e, double u, double v) {
     if (e < 0) return 1.0;
+    if (m.kind != PSTF_MODEL_GRID) return kd_pdf(m, e, u, v);
     const double tot = m.ent[e].total;
     if (tot <= 0.0) return 1.0;
-    return m.w[(uint64_t)e * m.r2 + mdl_cell(u, v, m.res)] / tot * (double)m.res * (double)m.res;
+    return m.w[(uint64_t)e * m.ns + mdl_cell(u, v, m.res)] / tot * (double)m.res * (double)m.res;
 }
 
 __global__ void k_mdl_pdf(MdlDev m, const int32_t *ent, const double *u, const double *v,
@@ -346,6 +580,10 @@ __global__ void k_mdl_sample(MdlDev m, const int32_t *ent, const double *u1, con
     if (i >= n) return;
     const int32_t e = ent[i];
     const double ux = u1[i], uy = u2[i];
+    if (e >= 0 && m.kind != PSTF_MODEL_GRID) {
+        kd_sample(m, e, ux, uy, &su[i], &sv[i], &spdf[i]);
+        return;
+    }
     if (e < 0 || m.ent[e].total <= 0.0) {
         su[i] = ux;
         sv[i] = uy;
@@ -353,7 +591,7 @@ __global__ void k_mdl_sample(MdlDev m, const int32_t *ent, const double *u1, con
         return;
     }
     const int R = m.res;
-    const double *w = m.w + (uint64_t)e * m.r2;
+    const double *w = m.w + (uint64_t)e * m.ns;
     const double target = uy * m.ent[e].total;
     int row = 0;
     double row_sum = 0.0, acc = 0.0;
@@ -384,11 +622,62 @@ __global__ void k_mdl_sample(MdlDev m, const int32_t *ent, const double *u1, con
 
 extern "C" {
 
+/* the uniform tree of SphericalKdTree's constructor (models.cpp:96-127): nodes appended in
+ * the constructor's order (children allocated when their parent is visited, left subtree
+ * first), axis alternating with depth, midpoint splits, leaf prob 1/L, then the masses */
+static void kd_initial_tree(int leaves, std::vector<KdNode> &K, std::vector<double> &P) {
+    K.clear();
+    P.clear();
+    auto add = [&]() {
+        KdNode z;
+        z.split = 0.5;
+        z.mass = 0.0;
+        z.left = z.right = z.parent = -1;
+        z.leaf = 1;
+        z.axis = 0;
+        K.push_back(z);
+        P.push_back(0.0);
+        return (int)K.size() - 1;
+    };
+    add();
+    std::function<void(int, int, int)> build = [&](int node, int depth, int below) {
+        if (below == 1) {
+            K[node].leaf = 1;
+            P[node] = 1.0 / leaves;
+            return;
+        }
+        const int l = add(), r = add();
+        K[node].leaf = 0;
+        K[node].axis = (uint8_t)(depth & 1);
+        K[node].split = 0.5;
+        K[node].left = l;
+        K[node].right = r;
+        K[l].parent = node;
+        K[r].parent = node;
+        build(l, depth + 1, below / 2);
+        build(r, depth + 1, below / 2);
+    };
+    build(0, 0, leaves);
+    std::function<double(int)> mass = [&](int n) {
+        K[n].mass = K[n].leaf ? P[n] : mass(K[n].left) + mass(K[n].right);
+        return K[n].mass;
+    };
+    mass(0);
+}
+
 int pstf_model_create(const pstf_model_config *config, int device, pstf_model_store **out) {
     if (!config || !out) return set_err(PSTF_E_INVALID, "NULL argument");
     *out = nullptr;
-    if (config->grid_resolution < 1 || config->grid_resolution > 256)
+    const bool kd = config->kind == PSTF_MODEL_KDTREE;
+    if (!kd && config->kind != PSTF_MODEL_GRID)
+        return set_err(PSTF_E_INVALID, "kind must be PSTF_MODEL_GRID or PSTF_MODEL_KDTREE");
+    if (!kd && (config->grid_resolution < 1 || config->grid_resolution > 256))
         return set_err(PSTF_E_INVALID, "grid_resolution must be in [1, 256]"); /* models.cpp:17-18 */
+    if (kd && (config->kd_leaf_count < 2 || config->kd_leaf_count > 256 ||
+               (config->kd_leaf_count & (config->kd_leaf_count - 1)) != 0)) /* models.cpp:99-101 */
+        return set_err(PSTF_E_INVALID, "kd_leaf_count must be a power of two in [2, 256]");
+    if (kd && !(config->kd_split_threshold > 1.0)) /* models.cpp:203-204 */
+        return set_err(PSTF_E_INVALID, "kd_split_threshold must be > 1");
     if (config->capacity_log2 < 1 || config->capacity_log2 > 26)
         return set_err(PSTF_E_INVALID, "capacity_log2 must be in [1, 26]");
     CK(cudaSetDevice(device));
@@ -397,8 +686,8 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
     m->device = device;
     const uint64_t cap = 1ull << config->capacity_log2;
     m->mask = (uint32_t)(cap - 1);
-    m->r2 = config->grid_resolution * config->grid_resolution;
-    const uint64_t cells = cap * (uint64_t)m->r2;
+    m->ns = kd ? 2 * config->kd_leaf_count - 1 : config->grid_resolution * config->grid_resolution;
+    const uint64_t cells = (cap + 1) * (uint64_t)m->ns; /* + the k-d template entry */
     if (cells * 16 > (64ull << 30)) return set_err(PSTF_E_INVALID, "model table too large");
     ENSURE(m->state, cap * 4);
     ENSURE(m->keyf, cap * sizeof(KeyFields));
@@ -410,6 +699,15 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
     ENSURE(m->sums, 16);
     CK(cudaMemset(m->state.p, 0, cap * 4));
     CK(cudaMemset(m->ctr.p, 0, MC_N * 8));
+    if (kd) {
+        ENSURE(m->kn, cells * sizeof(KdNode));
+        std::vector<KdNode> K;
+        std::vector<double> P;
+        kd_initial_tree(config->kd_leaf_count, K, P);
+        CK(cudaMemcpy(m->kn.as<KdNode>() + cap * m->ns, K.data(), m->ns * sizeof(KdNode),
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(m->w.as<double>() + cap * m->ns, P.data(), m->ns * 8, cudaMemcpyHostToDevice));
+    }
     CK(cudaDeviceSynchronize());
     *out = m.release();
     return PSTF_OK;
@@ -462,8 +760,12 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
     CK(cudaMemsetAsync(m->sums.p, 0, 16, st));
     LAUNCH(k_mdl_sums, (unsigned)sm_count() * 2, 256, 0, st, d, m->sums.as<double>());
     const uint64_t cap = (uint64_t)m->mask + 1;
-    LAUNCH(k_mdl_blend, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(), t_max,
-           limited, m->cfg.min_samples);
+    if (m->cfg.kind == PSTF_MODEL_GRID)
+        LAUNCH(k_mdl_blend, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(), t_max,
+               limited, m->cfg.min_samples);
+    else
+        LAUNCH(k_mdl_blend_kd, (unsigned)sm_count() * 2, 128, 0, st, d, m->sums.as<double>(),
+               t_max, limited, m->cfg.min_samples);
     CK(cudaMemsetAsync(&m->ctr.as<unsigned long long>()[MC_TOUCHED], 0, 8, st));
     return PSTF_OK;
 }
@@ -536,7 +838,7 @@ int pstf_model_dump(pstf_model_store *m, pstf_model_entry *entries, double *weig
     if (!m || !count || (cap_out && !entries)) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(m->device));
     CK(cudaDeviceSynchronize());
-    const uint64_t cap = (uint64_t)m->mask + 1, r2 = (uint64_t)m->r2;
+    const uint64_t cap = (uint64_t)m->mask + 1, ns = (uint64_t)m->ns;
     std::vector<uint32_t> state(cap);
     std::vector<KeyFields> kf(cap);
     std::vector<ModelEnt> ent(cap);
@@ -568,11 +870,53 @@ int pstf_model_dump(pstf_model_store *m, pstf_model_entry *entries, double *weig
         o.c_new = ent[e].c_new;
         o.records = ent[e].records;
         o.record_count = ent[e].rec_count;
-        o.total = ent[e].total;
-        if (weights) CK(cudaMemcpy(weights + i * r2, m->w.as<double>() + (uint64_t)e * r2, r2 * 8,
+        o.total = m->cfg.kind == PSTF_MODEL_GRID ? ent[e].total : 0.0; /* DirGrid::m_total */
+        if (weights) CK(cudaMemcpy(weights + i * ns, m->w.as<double>() + (uint64_t)e * ns, ns * 8,
                                    cudaMemcpyDeviceToHost));
-        if (accum) CK(cudaMemcpy(accum + i * r2, m->acc.as<double>() + (uint64_t)e * r2, r2 * 8,
+        if (accum) CK(cudaMemcpy(accum + i * ns, m->acc.as<double>() + (uint64_t)e * ns, ns * 8,
                                  cudaMemcpyDeviceToHost));
+    }
+    return PSTF_OK;
+}
+
+int pstf_model_dump_tree(pstf_model_store *m, int32_t *node_i32, double *node_f64, uint64_t cap_out,
+                         uint64_t *count) {
+    if (!m || !count) return set_err(PSTF_E_INVALID, "NULL argument");
+    if (m->cfg.kind != PSTF_MODEL_KDTREE) return set_err(PSTF_E_INVALID, "not a k-d tree store");
+    CK(cudaSetDevice(m->device));
+    CK(cudaDeviceSynchronize());
+    const uint64_t cap = (uint64_t)m->mask + 1, ns = (uint64_t)m->ns;
+    std::vector<uint32_t> state(cap);
+    std::vector<KeyFields> kf(cap);
+    CK(cudaMemcpy(state.data(), m->state.p, cap * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(kf.data(), m->keyf.p, cap * sizeof(KeyFields), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> live;
+    for (uint64_t e = 0; e < cap; ++e)
+        if (state[e] == 2) live.push_back((uint32_t)e);
+    std::sort(live.begin(), live.end(), [&](uint32_t a, uint32_t b) {
+        const KeyFields &x = kf[a], &y = kf[b];
+        return std::tie(x.level, x.c0, x.c1, x.c2, x.d0, x.d1) <
+               std::tie(y.level, y.c0, y.c1, y.c2, y.d0, y.d1);
+    });
+    *count = live.size();
+    std::vector<KdNode> K(ns);
+    for (uint64_t i = 0; i < std::min<uint64_t>(live.size(), cap_out); ++i) {
+        CK(cudaMemcpy(K.data(), m->kn.as<KdNode>() + (uint64_t)live[i] * ns, ns * sizeof(KdNode),
+                      cudaMemcpyDeviceToHost));
+        for (uint64_t j = 0; j < ns; ++j) {
+            if (node_i32) {
+                int32_t *o = node_i32 + (i * ns + j) * 5;
+                o[0] = K[j].leaf;
+                o[1] = K[j].axis;
+                o[2] = K[j].left;
+                o[3] = K[j].right;
+                o[4] = K[j].parent;
+            }
+            if (node_f64) {
+                node_f64[(i * ns + j) * 2] = K[j].split;
+                node_f64[(i * ns + j) * 2 + 1] = K[j].mass;
+            }
+        }
     }
     return PSTF_OK;
 }

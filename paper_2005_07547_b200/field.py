@@ -127,6 +127,7 @@ def lib():
         "pstf_model_sample": ([vp, vp, vp, vp, u64, vp, vp, vp, vp], i32),
         "pstf_model_get_stats": ([vp, vp], i32),
         "pstf_model_dump": ([vp, vp, vp, vp, u64, vp], i32),
+        "pstf_model_dump_tree": ([vp, vp, vp, u64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

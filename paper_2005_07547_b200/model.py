@@ -1,7 +1,8 @@
-"""CV-profile / guiding model store on the B200 (SURVEY.md §8f row 2).
+"""CV-profile / guiding model store on the B200 (SURVEY.md §8f rows 2 and 4).
 
 Python mirror of the reference's ``ModelStore`` (estimators.h:124-150, estimators.cpp:104-144)
-with ``DirGrid`` models (models.h:30-52, models.cpp:16-94) over the C ABI
+with ``DirGrid`` (models.h:30-52, models.cpp:16-94) or ``SphericalKdTree`` models
+(models.h:59-109, models.cpp:96-298) over the C ABI
 (``pstf_model_*`` in include/pstf_field.h).  Keys are the field's SpatioDirectionalKeys;
 records are applied in the reference's deterministic order, so entries, weights and
 accumulators are bitwise those of ``EstimatorRun`` in deterministic mode."""
@@ -20,9 +21,13 @@ MODEL_ENTRY_DTYPE = np.dtype([("level", "<i4"), ("cell", "<i4", (3,)), ("dir", "
 assert MODEL_ENTRY_DTYPE.itemsize == 72
 
 
+MODEL_GRID, MODEL_KDTREE = 0, 1  # ModelKind (models.h:183); Gmm is not built
+
+
 class _ModelConfig(C.Structure):
-    _fields_ = [("grid_resolution", C.c_int32), ("t_max", C.c_double),
-                ("min_samples", C.c_int32), ("capacity_log2", C.c_uint32)]
+    _fields_ = [("kind", C.c_int32), ("grid_resolution", C.c_int32),
+                ("kd_leaf_count", C.c_int32), ("kd_split_threshold", C.c_double),
+                ("t_max", C.c_double), ("min_samples", C.c_int32), ("capacity_log2", C.c_uint32)]
 
 
 class _ModelStats(C.Structure):
@@ -37,12 +42,14 @@ class ModelStore:
     estimators.h:32,56-57); capacity_log2 sizes the device table (the reference map grows)."""
 
     def __init__(self, grid_resolution=16, t_max=64.0, min_samples=32, capacity_log2=16,
-                 device=0):
+                 device=0, kind=MODEL_GRID, kd_leaf_count=64, kd_split_threshold=4.0):
+        self.kind = kind
         self.res = int(grid_resolution)
-        self.r2 = self.res * self.res
+        self.r2 = 2 * kd_leaf_count - 1 if kind == MODEL_KDTREE else self.res * self.res
         self.device = device
         self._h = C.c_void_p()
-        cfg = _ModelConfig(self.res, float(t_max), int(min_samples), int(capacity_log2))
+        cfg = _ModelConfig(int(kind), self.res, int(kd_leaf_count), float(kd_split_threshold),
+                           float(t_max), int(min_samples), int(capacity_log2))
         _check(lib().pstf_model_create(C.byref(cfg), device, C.byref(self._h)))
 
     def __del__(self):
@@ -146,3 +153,16 @@ class ModelStore:
                                      w.ctypes.data_as(C.c_void_p), a.ctypes.data_as(C.c_void_p),
                                      n, C.byref(cnt)))
         return e[:n], w[:n], a[:n]
+
+    def dump_tree(self):
+        """k-d tree topology in dump() order: (n, 2L-1, 5) int32 {leaf, axis, left, right,
+        parent} and (n, 2L-1, 2) float64 {split, mass}"""
+        cnt = C.c_uint64()
+        _check(lib().pstf_model_dump(self._h, None, None, None, 0, C.byref(cnt)))
+        n = cnt.value
+        ti = np.zeros((max(n, 1), self.r2, 5), np.int32)
+        tf = np.zeros((max(n, 1), self.r2, 2))
+        _check(lib().pstf_model_dump_tree(self._h, ti.ctypes.data_as(C.c_void_p),
+                                          tf.ctypes.data_as(C.c_void_p), n, C.byref(cnt)))
+        return ti[:n], tf[:n]
+

@@ -9,7 +9,7 @@ import inputs
 import pyoracle as po
 
 
-def model_records(rng, n, n_keys, base=0.5, levels=3):
+def model_records(rng, n, n_keys, base=0.5, levels=3, skew=1.0):
     ks = po.OracleStore(po.Config.make(capacity_log2=10, base_cell_size=base))
     pos = rng.uniform(-4, 4, size=(n_keys, 3))
     dirs = inputs.random_dirs(rng, n_keys)
@@ -18,7 +18,7 @@ def model_records(rng, n, n_keys, base=0.5, levels=3):
     idx = np.minimum((rng.pareto(1.1, n) * 3).astype(np.int64), n_keys - 1)  # hot keys first
     idx = rng.permutation(n_keys)[idx]
     k = keys[idx]
-    u, v = rng.random(n), rng.random(n)
+    u, v = rng.random(n) ** skew, rng.random(n) ** skew  # skew > 1: hot corner (k-d splits)
     c = rng.exponential(1.0, n)
     e = rng.random(n)
     u[e < 0.02] = 1.0

@@ -149,3 +149,39 @@ def test_model_store_atomic_mode():
             np.testing.assert_allclose(wg, wr, rtol=1e-12, atol=1e-300)
             np.testing.assert_allclose(ag, ar, rtol=1e-12, atol=1e-300)
 
+
+
+@pytest.mark.parametrize("leaves,tsplit,t_max", [(64, 4.0, 64.0), (8, 1.5, 3.0), (2, 1.01, np.inf)])
+def test_kdtree_model_store_bitwise(leaves, tsplit, t_max):
+    """SphericalKdTree kind (models.cpp:96-298, the split-collapse
+    learner): node probabilities, accumulators, masses and topology bitwise over frames with a
+    hot corner, then lookup, pdf and sample."""
+    rng = np.random.default_rng(leaves * 7)
+    g = pb.ModelStore(16, t_max, 4, capacity_log2=10, kind=pb.MODEL_KDTREE, kd_leaf_count=leaves,
+                      kd_split_threshold=tsplit)
+    if po.model_ref_available():
+        r = po.RefModelStore(16, t_max, 4, kind=1, leaves=leaves, tsplit=tsplit)
+    else:
+        r = po.OracleModelStore(16, t_max, 4, kind=1, leaves=leaves, tsplit=tsplit)
+    for frame in range(6):
+        k, u, v, c, keys = mc.model_records(rng, 5000, 150, skew=3.0)
+        perm = rng.permutation(len(k))
+        g.apply(k[perm], u[perm], v[perm], c[perm])
+        r.apply(k, u, v, c)
+        _same_dump(g, r)
+        g.end_frame()
+        r.end_frame()
+        _same_dump(g, r)
+        (gi, gf), (ri, rf) = g.dump_tree(), r.dump_tree()
+        np.testing.assert_array_equal(gi, ri)
+        np.testing.assert_array_equal(gf.view(np.uint64), rf.view(np.uint64))
+    q, u, v = mc.probe_points(rng, keys, 3000)
+    ent = g.lookup_warm(q).cpu().numpy()
+    pr, found = r.pdf(q, u, v)
+    np.testing.assert_array_equal(ent >= 0, found)
+    assert found.sum() > 50
+    pg = g.pdf(torch.from_numpy(ent), u, v).cpu().numpy()
+    np.testing.assert_array_equal(pg.view(np.uint64), pr.view(np.uint64))
+    sg = [x.cpu().numpy() for x in g.sample(torch.from_numpy(ent), u, v)]
+    for a, b in zip(sg, r.sample(q, u, v)[:3]):
+        np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))

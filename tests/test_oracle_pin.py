@@ -264,3 +264,37 @@ def test_model_store_matches_reference(res, t_max, min_samples):
     for a, b in zip(so, sr):
         np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
     assert fo.sum() > 100
+
+
+@pytest.mark.skipif(not po.model_ref_available(), reason="oracle/_ref model store not built")
+@pytest.mark.parametrize("leaves,tsplit,t_max", [(64, 4.0, 64.0), (8, 1.5, 3.0), (2, 1.01, np.inf)])
+def test_kdtree_model_store_matches_reference(leaves, tsplit, t_max):
+    """SphericalKdTree kind (models.cpp:96-298): node probabilities, accumulators, masses and the
+    split-collapse topology bitwise against the reference over frames with a hot corner, then
+    pdf and sample."""
+    import model_cases as mc
+    rng = np.random.default_rng(leaves * 7)
+    o = po.OracleModelStore(16, t_max, 4, kind=1, leaves=leaves, tsplit=tsplit)
+    r = po.RefModelStore(16, t_max, 4, kind=1, leaves=leaves, tsplit=tsplit)
+    for frame in range(6):
+        k, u, v, c, keys = mc.model_records(rng, 5000, 150, skew=3.0)
+        o.apply(k, u, v, c)
+        r.apply(k, u, v, c)
+        _model_equal(o, r)
+        o.end_frame()
+        r.end_frame()
+        _model_equal(o, r)
+        (ti, tf), (ri, rf) = o.dump_tree(), r.dump_tree()
+        np.testing.assert_array_equal(ti, ri)
+        np.testing.assert_array_equal(tf.view(np.uint64), rf.view(np.uint64))
+    moved = (ti[:, :, 4] != po.OracleModelStore(16, t_max, 4, kind=1, leaves=leaves,
+                                                tsplit=tsplit)._initial_parents(leaves)).any(1)
+    q, u, v = mc.probe_points(rng, keys, 3000)
+    po_, fo = o.pdf(q, u, v)
+    pr_, fr = r.pdf(q, u, v)
+    np.testing.assert_array_equal(fo, fr)
+    np.testing.assert_array_equal(po_.view(np.uint64), pr_.view(np.uint64))
+    for a, b in zip(o.sample(q, u, v), r.sample(q, u, v)):
+        np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+    assert fo.sum() > 50 and (moved.sum() > 0 or leaves == 2)  # warm; split-collapse happened
+
