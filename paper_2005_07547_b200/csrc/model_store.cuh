@@ -140,8 +140,7 @@ __device__ int kd_find_leaf(const KdNode *K, double u, double v, double2 *lo_out
 
 /* refreshMass (models.cpp:129-138): mass = prob at leaves, left + right above; computed in
  * reverse breadth-first order (children before parents), each sum being the same single add */
-__device__ void kd_refresh_mass(KdNode *K, const double *P, int nn) {
-    int order[511];
+__device__ void kd_refresh_mass(KdNode *K, const double *P, int nn, int *order) {
     int head = 0, tail = 0;
     order[tail++] = 0;
     while (head < tail) {
@@ -157,55 +156,88 @@ __device__ void kd_refresh_mass(KdNode *K, const double *P, int nn) {
     }
 }
 
-/* SphericalKdTree::endFrame (models.cpp:202-298): blend toward the frame's floored,
- * normalized leaf sums, renormalize, then one split-collapse step; every loop in node order */
-__device__ void kd_end_frame(KdNode *K, double *P, double *A, int nn, int leaves, double blend,
-                             double tsplit) {
-    double total = 0.0;
-    for (int i = 0; i < nn; ++i)
-        if (K[i].leaf) total += A[i];
+/* sum over i in [0, n) of f(i) in index order, by one warp (every lane gets the same value):
+ * lanes evaluate 32 consecutive terms, every lane adds them in order via broadcasts.  Terms
+ * that the reference skips are +0.0 here, which leaves a non-negative sum unchanged. */
+template <class F>
+__device__ __forceinline__ double warp_ordered_sum_f(int n, unsigned lane, F f) {
+    double s = 0.0;
+    for (int b = 0; b < n; b += 32) {
+        const double mine = b + (int)lane < n ? f(b + (int)lane) : 0.0;
+        const int k = min(32, n - b);
+        for (int l = 0; l < k; ++l) s += __shfl_sync(0xffffffffu, mine, l);
+    }
+    return s;
+}
+
+/* first index of the extreme value (strict comparison, as the reference's loops): best = lowest
+ * (sign -1) or highest (sign +1) value, ties to the lower index; idx -1 when no candidate */
+__device__ __forceinline__ void warp_first_extreme(double &val, int &idx, double sign) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        const bool better = oi >= 0 && (idx < 0 || sign * ov > sign * val ||
+                                        (ov == val && oi < idx));
+        if (better) {
+            val = ov;
+            idx = oi;
+        }
+    }
+}
+
+/* SphericalKdTree::endFrame (models.cpp:202-298), one warp per tree: the node loops run across
+ * lanes (sums in node order, first-index extremes), the split-collapse step on lane 0 */
+__device__ void kd_end_frame_warp(KdNode *K, double *P, double *A, int nn, int leaves,
+                                  double blend, double tsplit, unsigned lane, int *scratch) {
+    const double total = warp_ordered_sum_f(nn, lane, [&](int i) { return K[i].leaf ? A[i] : 0.0; });
     if (total > 0.0) {
         const double floor_prob = 1e-4 / leaves;
-        double norm_sum = 0.0;
-        for (int i = 0; i < nn; ++i)
-            if (K[i].leaf) norm_sum += max_ref(A[i] / total, floor_prob);
-        for (int i = 0; i < nn; ++i) {
-            if (!K[i].leaf) continue;
-            const double target = max_ref(A[i] / total, floor_prob) / norm_sum;
-            P[i] = (1.0 - blend) * P[i] + blend * target;
-        }
-        double prob_sum = 0.0;
-        for (int i = 0; i < nn; ++i)
-            if (K[i].leaf) prob_sum += P[i];
-        for (int i = 0; i < nn; ++i)
+        const double norm_sum = warp_ordered_sum_f(nn, lane, [&](int i) {
+            return K[i].leaf ? max_ref(A[i] / total, floor_prob) : 0.0;
+        });
+        for (int i = lane; i < nn; i += 32)
+            if (K[i].leaf) {
+                const double target = max_ref(A[i] / total, floor_prob) / norm_sum;
+                P[i] = (1.0 - blend) * P[i] + blend * target;
+            }
+        __syncwarp();
+        const double prob_sum =
+            warp_ordered_sum_f(nn, lane, [&](int i) { return K[i].leaf ? P[i] : 0.0; });
+        __syncwarp();
+        for (int i = lane; i < nn; i += 32)
             if (K[i].leaf) P[i] /= prob_sum;
+        __syncwarp();
     }
-    int l_max = -1;
-    double p_max = -1.0;
-    for (int i = 0; i < nn; ++i)
-        if (K[i].leaf && P[i] > p_max) {
-            p_max = P[i];
-            l_max = i;
-        }
-    int p_min = -1;
-    double p_min_mass = 2.0;
-    for (int i = 0; i < nn; ++i) {
-        const KdNode &n = K[i];
-        if (n.leaf || !K[n.left].leaf || !K[n.right].leaf) continue;
-        const double mass = P[n.left] + P[n.right];
-        if (mass < p_min_mass) {
-            p_min_mass = mass;
-            p_min = i;
+    /* l_max: first leaf of highest prob (the reference starts from pMax = -1: every leaf
+     * qualifies); p_min: first internal node over two leaves of lowest pair mass below 2 */
+    double p_max = -1.0, p_min_mass = 2.0;
+    int l_max = -1, p_min = -1;
+    for (int i = lane; i < nn; i += 32) {
+        const KdNode n = K[i];
+        if (n.leaf) {
+            if (P[i] > p_max) {
+                p_max = P[i];
+                l_max = i;
+            }
+        } else if (K[n.left].leaf && K[n.right].leaf) {
+            const double mass = P[n.left] + P[n.right];
+            if (mass < p_min_mass) {
+                p_min_mass = mass;
+                p_min = i;
+            }
         }
     }
-    if (l_max >= 0 && p_min >= 0 && K[l_max].parent != p_min && p_max > tsplit * p_min_mass) {
+    warp_first_extreme(p_max, l_max, 1.0);
+    warp_first_extreme(p_min_mass, p_min, -1.0);
+    if (lane == 0 && l_max >= 0 && p_min >= 0 && K[l_max].parent != p_min &&
+        p_max > tsplit * p_min_mass) {
         const int freed_l = K[p_min].left, freed_r = K[p_min].right;
         K[p_min].leaf = 1; /* the coldest leaf pair collapses into its parent */
         P[p_min] = p_min_mass;
         A[p_min] = 0.0;
         K[p_min].left = K[p_min].right = -1;
         /* the hot leaf's rectangle, from the root down its ancestor chain */
-        int chain[512];
+        int *chain = scratch;
         int nc = 0;
         for (int n = l_max; n != -1; n = K[n].parent) chain[nc++] = n;
         double2 lo = make_double2(0.0, 0.0), hi = make_double2(1.0, 1.0);
@@ -237,12 +269,14 @@ __device__ void kd_end_frame(KdNode *K, double *P, double *A, int nn, int leaves
             z.axis = 0;
             K[c] = z;
             P[c] = p_max * 0.5;
-            A[c] = 0.0;
         }
         P[l_max] = 0.0;
     }
-    for (int i = 0; i < nn; ++i) A[i] = 0.0;
-    kd_refresh_mass(K, P, nn);
+    __syncwarp();
+    for (int i = lane; i < nn; i += 32) A[i] = 0.0;
+    __syncwarp();
+    if (lane == 0) kd_refresh_mass(K, P, nn, scratch);
+    __syncwarp();
 }
 
 /* accumulator slot of a record: the DirGrid cell or the k-d tree leaf */
@@ -465,22 +499,48 @@ __global__ void k_mdl_blend(MdlDev m, const double *sums, double t_max, int limi
     }
 }
 
-/* the same for k-d tree entries: one thread per touched entry (the tree update is sequential) */
-__global__ void k_mdl_blend_kd(MdlDev m, const double *sums, double t_max, int limited,
-                               int min_samples) {
+/* the same for k-d tree entries, one warp per touched entry; the tree (nodes, prob, accum) is
+ * staged in the warp's slice of shared memory, so the sequential steps (split-collapse,
+ * refreshMass) run at shared-memory rather than L2 latency */
+#define KD_WARPS 4
+#define KD_SMEM_PER_NODE 56 /* node 32 + prob 8 + accum 8 + scratch int 4, 8-aligned */
+__global__ void __launch_bounds__(KD_WARPS * 32) k_mdl_blend_kd(MdlDev m, const double *sums,
+                                                                double t_max, int limited,
+                                                                int min_samples) {
+    extern __shared__ __align__(16) unsigned char kd_smem[];
     const uint64_t nt = m.ctr[MC_TOUCHED];
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned lane = lane_id();
+    const int nn = m.ns;
+    unsigned char *mine = kd_smem + (size_t)(threadIdx.x >> 5) * nn * KD_SMEM_PER_NODE;
+    KdNode *Ks = reinterpret_cast<KdNode *>(mine);
+    double *Ps = reinterpret_cast<double *>(mine + (size_t)nn * 32);
+    double *As = Ps + nn;
+    int *scratch = reinterpret_cast<int *>(As + nn); /* ancestor chain, then the BFS order */
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nt;
+         i += nwarps) {
         const uint32_t e = m.tlist[i];
         ModelEnt x = m.ent[e];
         x.touched = 0;
         if (x.c_new > 0.0) {
-            const uint64_t b = (uint64_t)e * m.ns;
-            kd_end_frame(m.kn + b, m.w + b, m.acc + b, m.ns, m.leaves,
-                         mdl_alpha(x, t_max, limited), m.tsplit);
+            const uint64_t b = (uint64_t)e * nn;
+            for (int j = lane; j < nn; j += 32) {
+                Ks[j] = m.kn[b + j];
+                Ps[j] = m.w[b + j];
+                As[j] = m.acc[b + j];
+            }
+            __syncwarp();
+            kd_end_frame_warp(Ks, Ps, As, nn, m.leaves, mdl_alpha(x, t_max, limited), m.tsplit,
+                              lane, scratch);
+            for (int j = lane; j < nn; j += 32) {
+                m.kn[b + j] = Ks[j];
+                m.w[b + j] = Ps[j];
+                m.acc[b + j] = 0.0;
+            }
+            __syncwarp();
             mdl_close(x, sums, t_max, limited, min_samples);
         }
-        m.ent[e] = x;
+        if (lane == 0) m.ent[e] = x;
     }
 }
 
@@ -700,6 +760,9 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
     CK(cudaMemset(m->state.p, 0, cap * 4));
     CK(cudaMemset(m->ctr.p, 0, MC_N * 8));
     if (kd) {
+        static_assert(sizeof(KdNode) == 32, "KdNode staging assumes 32 B nodes");
+        CK(cudaFuncSetAttribute(k_mdl_blend_kd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                KD_WARPS * 511 * KD_SMEM_PER_NODE));
         ENSURE(m->kn, cells * sizeof(KdNode));
         std::vector<KdNode> K;
         std::vector<double> P;
@@ -764,8 +827,9 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
         LAUNCH(k_mdl_blend, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(), t_max,
                limited, m->cfg.min_samples);
     else
-        LAUNCH(k_mdl_blend_kd, (unsigned)sm_count() * 2, 128, 0, st, d, m->sums.as<double>(),
-               t_max, limited, m->cfg.min_samples);
+        LAUNCH(k_mdl_blend_kd, (unsigned)sm_count() * 8, KD_WARPS * 32,
+               (size_t)KD_WARPS * m->ns * KD_SMEM_PER_NODE, st, d, m->sums.as<double>(), t_max, limited,
+               m->cfg.min_samples);
     CK(cudaMemsetAsync(&m->ctr.as<unsigned long long>()[MC_TOUCHED], 0, 8, st));
     return PSTF_OK;
 }
