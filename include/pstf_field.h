@@ -326,17 +326,25 @@ int pstf_profile_collect(char *names, double *ms, uint64_t *counts, int n_max, i
  * ModelStore (estimators.h:124-150, estimators.cpp:104-144) with DirGrid models
  * (models.h:30-52, models.cpp:16-94; what the CV profiles always use, estimators.cpp:336-339,
  * and the guiding models' default kind, models.h:186) or SphericalKdTree models
- * (models.h:59-109, models.cpp:96-298: the split-collapse learner).
+ * (models.h:59-109, models.cpp:96-298: the split-collapse learner) or Gmm models
+ * (models.h:113-177, models.cpp:427-702: stepwise EM, batch E-step by prefix sums of
+ * log(1 - k^-alpha)).  Grid and k-d tree results are bitwise the reference's; the GMM goes
+ * through exp/log/pow/sin/cos, so its state agrees to a relative tolerance (1e-9), not bitwise.
  * Keyed by the field's SpatioDirectionalKey with key-field equality (the unordered_map's
  * operator==, field.h:38-41).  The reference map grows without bound; here the table has
  * 2^capacity_log2 entries and records of keys that find no free entry are counted as dropped. */
-enum { PSTF_MODEL_GRID = 0, PSTF_MODEL_KDTREE = 1 }; /* ModelKind (models.h:183); no Gmm */
+enum { PSTF_MODEL_GRID = 0, PSTF_MODEL_KDTREE = 1, PSTF_MODEL_GMM = 2 }; /* ModelKind, models.h:183 */
 
 typedef struct pstf_model_config {
-    int32_t kind;               /* PSTF_MODEL_GRID (DirGrid) or PSTF_MODEL_KDTREE */
+    int32_t kind;               /* PSTF_MODEL_GRID (DirGrid), _KDTREE or _GMM */
     int32_t grid_resolution;    /* ModelConfig::gridResolution (models.h:187), >= 1 */
     int32_t kd_leaf_count;      /* ModelConfig::kdLeafCount (models.h:188), power of two >= 2 */
     double kd_split_threshold;  /* ModelConfig::kdSplitThreshold (models.h:189), > 1 */
+    int32_t gmm_components;     /* GmmConfig (models.h:113-119): components in [1, 16] */
+    double gmm_alpha_em;        /*   step exponent in (0.5, 1] */
+    double gmm_sigma_min_sq;    /*   covariance eigenvalue floor */
+    double gmm_sigma_max_sq;    /*   covariance eigenvalue cap */
+    double gmm_reseed_fraction; /*   mass fraction below which a component is reseeded */
     double t_max;               /* EstimatorConfig::tMax (the blend cap, estimators.cpp:119-144) */
     int32_t min_samples;        /* minModelSamples / profileMinSamples (warm threshold) */
     uint32_t capacity_log2;     /* entries in the device table */
@@ -369,7 +377,8 @@ int pstf_model_destroy(pstf_model_store *m);
  * PSTF_MODE_ORDERED: applied in the canonical deterministic order of estimators.cpp:633-637
  *   (key fields, uv.x, uv.y, contribution): bitwise the reference's deterministic mode.
  * PSTF_MODE_ATOMIC: no sort, fp64 atomics into the grids; accumulator sums within 1e-12
- *   relative (their order is the atomics'), everything else exact. */
+ *   relative (their order is the atomics'), everything else exact.  GMM stores always take
+ *   the canonical order (stepwise EM depends on the sample order, not only on rounding). */
 int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
                      const double *contribution, uint64_t n, int mode, void *stream);
 /* ModelStore::endFrame (estimators.cpp:119-144) */
@@ -389,14 +398,18 @@ int pstf_model_lookup_warm_levels(const pstf_model_store *m, const pstf_field *k
  * outside [0,1] indexes outside the grid in the reference (undefined); here it is clamped. */
 int pstf_model_pdf(const pstf_model_store *m, const int32_t *entry, const double *u,
                    const double *v, uint64_t n, double *pdf, void *stream);
-/* DirGrid::sample(u) (models.cpp:58-92): square sample + pdf; entry < 0 gives (u, 1.0) */
+/* DirGrid / SphericalKdTree::sample(u) (models.cpp:58-92, 176-200) and Gmm::sample(uSelect, u)
+ * (models.cpp:664-687; u_select is read only by GMM stores and may be NULL otherwise): square
+ * sample + pdf; entry < 0 gives (u, 1.0) */
 int pstf_model_sample(const pstf_model_store *m, const int32_t *entry, const double *u1,
-                      const double *u2, uint64_t n, double *su, double *sv, double *pdf,
-                      void *stream);
+                      const double *u2, const double *u_select, uint64_t n, double *su,
+                      double *sv, double *pdf, void *stream);
 int pstf_model_get_stats(pstf_model_store *m, pstf_model_stats *out);
 /* Host dump of every entry, sorted by key.  Per entry, weights and accum (when non-NULL)
  * receive S doubles: Grid: the R^2 weights / accumulators; KdTree: each of the 2L-1 nodes'
- * prob / accum (node order).  *count = entries; at most cap are written. */
+ * prob / accum (node order); Gmm: the state {weights[C], means[C][2], cov[C][3] (cxx, cxy,
+ * cyy), stats[C][8], cache[C][7] (inv[3], norm, chol[3]), i, underflows, reseed counter} and
+ * zeros.  *count = entries; at most cap are written. */
 int pstf_model_dump(pstf_model_store *m, pstf_model_entry *entries, double *weights,
                     double *accum, uint64_t cap, uint64_t *count);
 /* KdTree topology in the same entry order: per node {leaf, axis, left, right, parent} int32 and

@@ -63,12 +63,18 @@ static SpatioDirectionalKey toKey(const pm_key &k) {
     return s;
 }
 
-void *pm_create(int kind, int res, int leaves, double tsplit, double t_max, int min_samples) {
+void *pm_create(int kind, int res, int leaves, double tsplit, int comps, double alpha_em,
+                double smin, double smax, double reseed_frac, double t_max, int min_samples) {
     ModelConfig cfg;
-    cfg.kind = kind == 1 ? ModelKind::KdTree : ModelKind::Grid;
+    cfg.kind = kind == 1 ? ModelKind::KdTree : kind == 2 ? ModelKind::Gmm : ModelKind::Grid;
     cfg.gridResolution = res;
     cfg.kdLeafCount = leaves;
     cfg.kdSplitThreshold = tsplit;
+    cfg.gmm.components = comps;
+    cfg.gmm.alphaEm = alpha_em;
+    cfg.gmm.sigmaMinSq = smin;
+    cfg.gmm.sigmaMaxSq = smax;
+    cfg.gmm.reseedFraction = reseed_frac;
     return new ModelStore(cfg, t_max, min_samples);
 }
 
@@ -107,8 +113,8 @@ double pm_pdf(void *m, const pm_key *k, double u, double v, int *found) {
 }
 
 // lookupWarm + DirGrid::sample(u)
-void pm_sample(void *m, const pm_key *k, double u1, double u2, double *su, double *sv,
-               double *pdf, int *found) {
+void pm_sample(void *m, const pm_key *k, double u1, double u2, double usel, double *su,
+               double *sv, double *pdf, int *found) {
     const DirectionalModel *d = static_cast<ModelStore *>(m)->lookupWarm(toKey(*k));
     *found = d != nullptr;
     if (!d) {
@@ -120,6 +126,8 @@ void pm_sample(void *m, const pm_key *k, double u1, double u2, double *su, doubl
     Sample2D s;
     if (const DirGrid *g = std::get_if<DirGrid>(&d->m_impl))
         s = g->sample(Vec2{u1, u2});
+    else if (const Gmm *gm = std::get_if<Gmm>(&d->m_impl))
+        s = gm->sample(usel, Vec2{u1, u2}); // DirectionalModel::sample draws uSelect first
     else
         s = std::get<SphericalKdTree>(d->m_impl).sample(Vec2{u1, u2});
     *su = s.uv.x;
@@ -156,6 +164,34 @@ int64_t pm_dump(void *m, pm_entry *out, double *weights, double *accum, int64_t 
             const size_t r2 = g->m_weights.size();
             if (weights) std::copy(g->m_weights.begin(), g->m_weights.end(), weights + size_t(i) * r2);
             if (accum) std::copy(g->m_accum.begin(), g->m_accum.end(), accum + size_t(i) * r2);
+        } else if (const Gmm *gm = std::get_if<Gmm>(&e.model->m_impl)) {
+            // Gmm: the state vector {W, M, V, U, cache, i, underflows, reseed counter}
+            o.record_count = gm->m_recordCount;
+            o.total = 0.0;
+            const size_t C = gm->m_weights.size(), ns = 21 * C + 3;
+            if (weights) {
+                double *S = weights + size_t(i) * ns;
+                for (size_t c = 0; c < C; ++c) {
+                    S[c] = gm->m_weights[c];
+                    S[C + 2 * c] = gm->m_means[c].x;
+                    S[C + 2 * c + 1] = gm->m_means[c].y;
+                    for (int q = 0; q < 3; ++q) S[3 * C + 3 * c + q] = gm->m_cov[c][q];
+                    for (int q = 0; q < 8; ++q) S[6 * C + 8 * c + q] = gm->m_u[c][q];
+                    const auto &k = gm->m_cache[c];
+                    double *K = S + 14 * C + 7 * c;
+                    K[0] = k.inv[0];
+                    K[1] = k.inv[1];
+                    K[2] = k.inv[2];
+                    K[3] = k.norm;
+                    K[4] = k.chol[0];
+                    K[5] = k.chol[1];
+                    K[6] = k.chol[2];
+                }
+                S[21 * C] = double(gm->m_i);
+                S[21 * C + 1] = double(gm->m_underflows);
+                S[21 * C + 2] = double(gm->m_reseedCounter);
+            }
+            if (accum) std::fill(accum + size_t(i) * ns, accum + size_t(i + 1) * ns, 0.0);
         } else { // SphericalKdTree: per node prob / accum in node order
             const SphericalKdTree &t = std::get<SphericalKdTree>(e.model->m_impl);
             o.record_count = t.m_recordCount;

@@ -5,6 +5,8 @@
  *   ModelStore      estimators.h:124-150, estimators.cpp:104-144
  *   DirGrid         models.h:30-52, models.cpp:16-94
  *   SphericalKdTree models.h:59-109, models.cpp:96-298
+ *   Gmm             models.h:113-177, models.cpp:427-702 (state vector as the device's:
+ *                   W[C], M[2C], V[3C], U[8C], cache[7C], i, underflows, reseed counter)
  *   record order    estimators.cpp:625-645 (deterministic mode: sorted, then applied in order)
  *
  * Pinned bitwise against the reference's own ModelStore compiled in place
@@ -28,15 +30,20 @@ typedef struct {
 
 typedef struct {
     po_key key; /* checksum ignored: equality on the key fields (field.h:38-41) */
-    double *w, *acc; /* DirGrid */
+    double *w, *acc; /* DirGrid; Gmm: w = the state vector */
     pm_node *nodes;  /* SphericalKdTree: 2L-1 nodes */
+    double *fs;      /* Gmm::m_frameSamples: (u, v, contribution) triples */
+    size_t nfs, cfs;
     double total, c_old, c_new;
     uint64_t records, rec_count;
     int warm, used;
 } pm_entry;
 
 struct po_model {
-    int kind; /* 0 DirGrid, 1 SphericalKdTree (ModelKind, models.h:183) */
+    int kind; /* 0 DirGrid, 1 SphericalKdTree, 2 Gmm (ModelKind, models.h:183) */
+    int comps; /* GmmConfig (models.h:113-119) */
+    double alpha_em, smin, smax, reseed_frac;
+    double *gtmpl; /* Gmm's constructor state */
     int leaves;
     double tsplit;
     pm_node *tmpl; /* the constructor's uniform tree */
@@ -89,10 +96,52 @@ static double pm_kd_mass(pm_node *t, int n) {
     return t[n].mass;
 }
 
-po_model *po_model_create(int kind, int res, int leaves, double tsplit, double t_max,
-                          int min_samples) {
+#define GMM_TWO_PI (2.0 * 3.14159265358979323846) /* kTwoPi, vecmath.h:13-14 */
+#define GW(S) (S)
+#define GM(S, C) ((S) + (C))
+#define GV(S, C) ((S) + 3 * (C))
+#define GU(S, C) ((S) + 6 * (C))
+#define GK(S, C) ((S) + 14 * (C))
+#define GT(S, C) ((S) + 21 * (C))
+
+/* Gmm::rebuildCache (models.cpp:449-463) */
+static void pm_gmm_cache(double *S, int C, int c) {
+    double a = GV(S, C)[3 * c], b = GV(S, C)[3 * c + 1], d = GV(S, C)[3 * c + 2];
+    double det = a * d - b * b;
+    double *k = GK(S, C) + 7 * c;
+    k[0] = d / det;
+    k[1] = -b / det;
+    k[2] = a / det;
+    k[3] = 1.0 / (GMM_TWO_PI * sqrt(det));
+    k[4] = sqrt(a);
+    k[5] = b / k[4];
+    double r = d - k[5] * k[5];
+    k[6] = sqrt(r < 0.0 ? 0.0 : r);
+}
+
+po_model *po_model_create(int kind, int res, int leaves, double tsplit, int comps,
+                          double alpha_em, double smin, double smax, double reseed_frac,
+                          double t_max, int min_samples) {
     po_model *m = (po_model *)calloc(1, sizeof(po_model));
     m->kind = kind;
+    m->comps = comps;
+    m->alpha_em = alpha_em;
+    m->smin = smin;
+    m->smax = smax;
+    m->reseed_frac = reseed_frac;
+    if (kind == 2) { /* Gmm::Gmm (models.cpp:427-447) */
+        int C = comps, grid = 1;
+        m->gtmpl = (double *)calloc((size_t)(21 * C + 3), sizeof(double));
+        while (grid * grid < C) ++grid;
+        for (int c = 0; c < C; ++c) {
+            GW(m->gtmpl)[c] = 1.0 / C;
+            GV(m->gtmpl, C)[3 * c] = 0.02;
+            GV(m->gtmpl, C)[3 * c + 2] = 0.02;
+            GM(m->gtmpl, C)[2 * c] = ((c % grid) + 0.5) / grid;
+            GM(m->gtmpl, C)[2 * c + 1] = ((c / grid) + 0.5) / grid;
+            pm_gmm_cache(m->gtmpl, C, c);
+        }
+    }
     m->res = res;
     m->leaves = leaves;
     m->tsplit = tsplit;
@@ -111,7 +160,9 @@ po_model *po_model_create(int kind, int res, int leaves, double tsplit, double t
 }
 
 static size_t pm_slots(const po_model *m) {
-    return m->kind == 1 ? (size_t)(2 * m->leaves - 1) : (size_t)m->res * m->res;
+    return m->kind == 1   ? (size_t)(2 * m->leaves - 1)
+           : m->kind == 2 ? (size_t)(21 * m->comps + 3)
+                          : (size_t)m->res * m->res;
 }
 
 void po_model_destroy(po_model *m) {
@@ -120,9 +171,11 @@ void po_model_destroy(po_model *m) {
             free(m->tab[i].w);
             free(m->tab[i].acc);
             free(m->tab[i].nodes);
+            free(m->tab[i].fs);
         }
     free(m->tab);
     free(m->tmpl);
+    free(m->gtmpl);
     free(m);
 }
 
@@ -163,6 +216,10 @@ static pm_entry *pm_get_or_create(po_model *m, const po_key *k) {
         size_t nn = pm_slots(m);
         e->nodes = (pm_node *)malloc(nn * sizeof(pm_node));
         memcpy(e->nodes, m->tmpl, nn * sizeof(pm_node));
+    } else if (m->kind == 2) {
+        size_t ns = pm_slots(m);
+        e->w = (double *)malloc(ns * sizeof(double));
+        memcpy(e->w, m->gtmpl, ns * sizeof(double));
     } else {
         size_t r2 = (size_t)m->res * m->res;
         e->w = (double *)malloc(r2 * sizeof(double));
@@ -310,6 +367,153 @@ static void pm_kd_end_frame(po_model *m, pm_node *t, double blend) {
     pm_kd_mass(t, 0);
 }
 
+/* componentPdf (models.cpp:465-480) */
+static double pm_gmm_cpdf(const double *S, int C, int c, double x, double y) {
+    const double *k = GK(S, C) + 7 * c;
+    double sum = 0.0;
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+            double ex = x + dx - GM(S, C)[2 * c], ey = y + dy - GM(S, C)[2 * c + 1];
+            double q = k[0] * ex * ex + 2.0 * k[1] * ex * ey + k[2] * ey * ey;
+            sum += k[3] * exp(-0.5 * q);
+        }
+    return sum;
+}
+
+static double pm_gmm_pdf(const double *S, int C, double x, double y) { /* models.cpp:657-662 */
+    double p = 0.0;
+    for (int c = 0; c < C; ++c) p += GW(S)[c] * pm_gmm_cpdf(S, C, c, x, y);
+    return p;
+}
+
+/* responsibilities (models.cpp:482-497) */
+static void pm_gmm_resp(double *S, int C, double x, double y, double *gamma) {
+    double total = 0.0;
+    for (int c = 0; c < C; ++c) {
+        gamma[c] = GW(S)[c] * pm_gmm_cpdf(S, C, c, x, y);
+        total += gamma[c];
+    }
+    if (total <= 0.0 || !isfinite(total)) {
+        GT(S, C)[1] += 1.0;
+        for (int c = 0; c < C; ++c) gamma[c] = 1.0 / C;
+        return;
+    }
+    for (int c = 0; c < C; ++c) gamma[c] /= total;
+}
+
+/* estepBatch (models.cpp:525-585), sequential as in the reference */
+static void pm_gmm_estep(po_model *m, double *S, const double *fs, size_t n) {
+    int C = m->comps;
+    uint64_t i0 = (uint64_t)GT(S, C)[0];
+    double *gamma = (double *)malloc(n * C * sizeof(double) + 1);
+    for (size_t j = 0; j < n; ++j) pm_gmm_resp(S, C, fs[3 * j], fs[3 * j + 1], gamma + j * C);
+    double *lp = (double *)calloc(n + 1, sizeof(double));
+    size_t last_zero = 0;
+    for (size_t k = 1; k <= n; ++k) {
+        double factor = 1.0 - pow((double)(i0 + k), -m->alpha_em);
+        if (factor <= 0.0) {
+            last_zero = k;
+            lp[k] = 0.0;
+        } else {
+            lp[k] = lp[k - 1] + log(factor);
+        }
+    }
+#define GOF(j) ((j) < last_zero ? 0.0 : exp(lp[n] - lp[(j)]))
+    double g_total = GOF(0);
+    for (int q = 0; q < 8 * C; ++q) GU(S, C)[q] *= g_total;
+    for (size_t j = 1; j <= n; ++j) {
+        double sx = fs[3 * (j - 1)], sy = fs[3 * (j - 1) + 1], w = fs[3 * (j - 1) + 2];
+        double g = GOF(j);
+        if (g == 0.0) continue;
+        double step = pow((double)(i0 + j), -m->alpha_em);
+        for (int c = 0; c < C; ++c) {
+            double b = step * w * gamma[(j - 1) * C + c];
+            if (b <= 0.0) continue;
+            double bg = b * g, *u = GU(S, C) + 8 * c;
+            u[0] += bg;
+            u[1] += bg * sx;
+            u[2] += bg * sy;
+            u[3] += bg * sx * sx;
+            u[4] += bg * sy * sy;
+            u[5] += bg * sx * sy;
+            u[6] += g * step * w;
+            u[7] += g;
+        }
+    }
+#undef GOF
+    GT(S, C)[0] = (double)(i0 + n);
+    free(gamma);
+    free(lp);
+}
+
+static double pm_clamp3(double x, double lo, double hi) { /* vecmath.h:19 */
+    double a = x < lo ? lo : x;
+    return hi < a ? hi : a;
+}
+
+/* Gmm::mstep (models.cpp:587-655) */
+static void pm_gmm_mstep(po_model *m, double *S) {
+    int C = m->comps;
+    double total = 0.0;
+    for (int c = 0; c < C; ++c) total += GU(S, C)[8 * c];
+    if (total <= 0.0) return;
+    int heaviest = 0;
+    for (int c = 1; c < C; ++c)
+        if (GU(S, C)[8 * c] > GU(S, C)[8 * heaviest]) heaviest = c;
+    for (int c = 0; c < C; ++c) {
+        const double *u = GU(S, C) + 8 * c;
+        double mass = u[0];
+        if (mass <= m->reseed_frac * total) {
+            const double *h = GU(S, C) + 8 * heaviest;
+            double sx = h[1] / h[0], sy = h[2] / h[0];
+            uint32_t rc = (uint32_t)GT(S, C)[2];
+            GT(S, C)[2] = (double)(uint32_t)(rc + 1u);
+            double jitter = 0.05 * (1.0 + (double)(rc % 7u));
+            double mx = sx + jitter * 0.01, my = sy - jitter * 0.01;
+            mx -= floor(mx);
+            my -= floor(my);
+            GM(S, C)[2 * c] = mx;
+            GM(S, C)[2 * c + 1] = my;
+            GW(S)[c] = 1e-3;
+            GV(S, C)[3 * c] = 0.01;
+            GV(S, C)[3 * c + 1] = 0.0;
+            GV(S, C)[3 * c + 2] = 0.01;
+            continue;
+        }
+        GW(S)[c] = mass / total;
+        double mx = u[1] / mass, my = u[2] / mass;
+        double exx = u[3] / mass, eyy = u[4] / mass, exy = u[5] / mass;
+        double cxx = exx - mx * mx, cyy = eyy - my * my, cxy = exy - mx * my;
+        double tr = cxx + cyy, diff = cxx - cyy;
+        double dd = diff * diff + 4.0 * cxy * cxy;
+        double disc = sqrt(dd < 0.0 ? 0.0 : dd);
+        double l1 = 0.5 * (tr + disc), l2 = 0.5 * (tr - disc);
+        double c1 = pm_clamp3(l1, m->smin, m->smax), c2 = pm_clamp3(l2, m->smin, m->smax);
+        double vx, vy;
+        if (fabs(cxy) > 1e-30) {
+            vx = l1 - cyy;
+            vy = cxy;
+        } else {
+            vx = cxx >= cyy ? 1.0 : 0.0;
+            vy = cxx >= cyy ? 0.0 : 1.0;
+        }
+        double len = sqrt(vx * vx + vy * vy);
+        if (len > 0.0) {
+            vx /= len;
+            vy /= len;
+        }
+        GV(S, C)[3 * c] = c1 * vx * vx + c2 * vy * vy;
+        GV(S, C)[3 * c + 1] = (c1 - c2) * vx * vy;
+        GV(S, C)[3 * c + 2] = c1 * vy * vy + c2 * vx * vx;
+        GM(S, C)[2 * c] = mx;
+        GM(S, C)[2 * c + 1] = my;
+    }
+    double wsum = 0.0;
+    for (int c = 0; c < C; ++c) wsum += GW(S)[c];
+    for (int c = 0; c < C; ++c) GW(S)[c] /= wsum;
+    for (int c = 0; c < C; ++c) pm_gmm_cache(S, C, c);
+}
+
 /* applyRecord (estimators.cpp:109-117) with DirGrid::record (models.cpp:30-35) */
 static void pm_apply_one(po_model *m, const po_key *k, double u, double v, double c) {
     pm_entry *e = pm_get_or_create(m, k);
@@ -317,6 +521,15 @@ static void pm_apply_one(po_model *m, const po_key *k, double u, double v, doubl
         if (m->kind == 1) {
             double lo[2], hi[2];
             e->nodes[pm_kd_find(e->nodes, u, v, lo, hi)].accum += c;
+        } else if (m->kind == 2) { /* Gmm::record (models.cpp:689-694) */
+            if (e->nfs == e->cfs) {
+                e->cfs = e->cfs ? 2 * e->cfs : 16;
+                e->fs = (double *)realloc(e->fs, e->cfs * 3 * sizeof(double));
+            }
+            e->fs[3 * e->nfs] = u;
+            e->fs[3 * e->nfs + 1] = v;
+            e->fs[3 * e->nfs + 2] = c;
+            e->nfs++;
         } else {
             e->acc[pm_cell(m->res, u, v)] += c;
         }
@@ -362,6 +575,14 @@ void po_model_end_frame(po_model *m) {
             pm_kd_end_frame(m, e->nodes, alpha);
             goto close;
         }
+        if (m->kind == 2) { /* Gmm::endFrame (models.cpp:696-702) */
+            if (e->nfs) {
+                pm_gmm_estep(m, e->w, e->fs, e->nfs);
+                e->nfs = 0;
+                pm_gmm_mstep(m, e->w);
+            }
+            goto close;
+        }
         double s = 0.0;
         for (size_t j = 0; j < r2; ++j) s += e->acc[j];
         if (s > 0.0) {
@@ -384,6 +605,7 @@ void po_model_end_frame(po_model *m) {
 double po_model_pdf(const po_model *m, const po_key *k, double u, double v, int *found) {
     const pm_entry *e = pm_find(m, k);
     *found = e && e->warm;
+    if (*found && m->kind == 2) return pm_gmm_pdf(e->w, m->comps, u, v);
     if (*found && m->kind == 1) { /* SphericalKdTree::pdf (models.cpp:169-174) */
         double lo[2], hi[2];
         int leaf = pm_kd_find(e->nodes, u, v, lo, hi);
@@ -400,10 +622,34 @@ static double pm_clamp(double x, double lo, double hi) { /* vecmath.h:19 */
 }
 
 /* lookupWarm + DirGrid::sample (models.cpp:58-92); no warm model -> (u, 1.0), *found = 0 */
-void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double *su,
-                     double *sv, double *pdf, int *found) {
+void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double usel,
+                     double *su, double *sv, double *pdf, int *found) {
     const pm_entry *e = pm_find(m, k);
     *found = e && e->warm;
+    if (*found && m->kind == 2) { /* Gmm::sample (models.cpp:664-687) */
+        int C = m->comps, comp = 0;
+        const double *S = e->w;
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c) {
+            acc += GW(S)[c];
+            if (usel < acc || c == C - 1) {
+                comp = c;
+                break;
+            }
+        }
+        double om = 1.0 - u1;
+        double r = sqrt(-2.0 * log(om < 1e-300 ? 1e-300 : om));
+        double z0 = r * cos(GMM_TWO_PI * u2), z1 = r * sin(GMM_TWO_PI * u2);
+        const double *kk = GK(S, C) + 7 * comp;
+        double px = GM(S, C)[2 * comp] + kk[4] * z0;
+        double py = GM(S, C)[2 * comp + 1] + kk[5] * z0 + kk[6] * z1;
+        px -= floor(px);
+        py -= floor(py);
+        *su = px;
+        *sv = py;
+        *pdf = pm_gmm_pdf(S, C, px, py);
+        return;
+    }
     if (*found && m->kind == 1) { /* SphericalKdTree::sample (models.cpp:176-200) */
         const pm_node *t = e->nodes;
         const double below_one = nextafter(1.0, 0.0);
@@ -500,10 +746,11 @@ size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, do
         o->c_new = e->c_new;
         o->records = e->records;
         o->record_count = e->rec_count;
-        o->total = m->kind == 1 ? 0.0 : e->total;
+        o->total = m->kind == 0 ? e->total : 0.0;
         for (size_t j = 0; j < r2; ++j) {
             if (weights) weights[i * r2 + j] = m->kind == 1 ? e->nodes[j].prob : e->w[j];
-            if (accum) accum[i * r2 + j] = m->kind == 1 ? e->nodes[j].accum : e->acc[j];
+            if (accum) accum[i * r2 + j] = m->kind == 1 ? e->nodes[j].accum
+                                           : m->kind == 2 ? 0.0 : e->acc[j];
         }
     }
     free(ord);

@@ -116,15 +116,16 @@ typedef struct {
     uint64_t records, record_count;
     double total;
 } po_model_entry; /* == pstf_model_entry */
-po_model *po_model_create(int kind, int res, int leaves, double tsplit, double t_max,
-                          int min_samples); /* kind 0 DirGrid, 1 SphericalKdTree */
+po_model *po_model_create(int kind, int res, int leaves, double tsplit, int comps,
+                          double alpha_em, double smin, double smax, double reseed_frac,
+                          double t_max, int min_samples); /* kind 0 Grid, 1 KdTree, 2 Gmm */
 void po_model_destroy(po_model *m);
 void po_model_apply(po_model *m, const po_key *keys, const double *u, const double *v,
                     const double *c, size_t n);
 void po_model_end_frame(po_model *m);
 double po_model_pdf(const po_model *m, const po_key *k, double u, double v, int *found);
-void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double *su,
-                     double *sv, double *pdf, int *found);
+void po_model_sample(const po_model *m, const po_key *k, double u1, double u2, double usel,
+                     double *su, double *sv, double *pdf, int *found);
 size_t po_model_dump(const po_model *m, po_model_entry *out, double *weights, double *accum,
                      size_t cap);
 size_t po_model_dump_tree(const po_model *m, int32_t *node_i32, double *node_f64, size_t cap);

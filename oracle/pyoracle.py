@@ -491,10 +491,13 @@ class _ModelBase:
     (OracleModelStore) or the reference compiled in place (RefModelStore)."""
     P = ""
 
-    def __init__(self, res=16, t_max=64.0, min_samples=32, kind=0, leaves=64, tsplit=4.0):
+    def __init__(self, res=16, t_max=64.0, min_samples=32, kind=0, leaves=64, tsplit=4.0,
+                 comps=4, alpha_em=0.7, smin=2.5e-5, smax=0.04, reseed=1e-4):
         self.kind = kind
-        self.res, self.r2 = res, (2 * leaves - 1 if kind == 1 else res * res)
-        self.h = self._fn("create")(kind, res, leaves, tsplit, t_max, min_samples)
+        self.res = res
+        self.r2 = 2 * leaves - 1 if kind == 1 else (21 * comps + 3 if kind == 2 else res * res)
+        self.h = self._fn("create")(kind, res, leaves, tsplit, comps, alpha_em, smin, smax, reseed,
+                                    t_max, min_samples)
 
     def _fn(self, name):
         return getattr(self.lib, self.P + name)
@@ -522,14 +525,15 @@ class _ModelBase:
             found[i] = f.value
         return out, found
 
-    def sample(self, keys, u1, u2):
+    def sample(self, keys, u1, u2, usel=None):
         n = len(keys)
+        usel = np.zeros(n) if usel is None else usel
         su, sv, pdf, found = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(n, bool)
         a, b, p, f = C.c_double(), C.c_double(), C.c_double(), C.c_int()
         for i in range(n):
             ks = key_from_np(keys[i])
-            self._fn("sample")(self.h, C.byref(ks), float(u1[i]), float(u2[i]), C.byref(a),
-                               C.byref(b), C.byref(p), C.byref(f))
+            self._fn("sample")(self.h, C.byref(ks), float(u1[i]), float(u2[i]), float(usel[i]),
+                               C.byref(a), C.byref(b), C.byref(p), C.byref(f))
             su[i], sv[i], pdf[i], found[i] = a.value, b.value, p.value, f.value
         return su, sv, pdf, found
 
@@ -560,13 +564,13 @@ class _ModelBase:
 def _type_model_lib(lib, p, n_t):
     vp, d, i32 = C.c_void_p, C.c_double, C.c_int
     getattr(lib, p + "create").restype = vp
-    getattr(lib, p + "create").argtypes = [i32, i32, i32, d, d, i32]
+    getattr(lib, p + "create").argtypes = [i32, i32, i32, d, i32, d, d, d, d, d, i32]
     getattr(lib, p + "destroy").argtypes = [vp]
     getattr(lib, p + "apply").argtypes = [vp, vp, vp, vp, vp, n_t]
     getattr(lib, p + "end_frame").argtypes = [vp]
     getattr(lib, p + "pdf").argtypes = [vp, vp, d, d, vp]
     getattr(lib, p + "pdf").restype = d
-    getattr(lib, p + "sample").argtypes = [vp, vp, d, d, vp, vp, vp, vp]
+    getattr(lib, p + "sample").argtypes = [vp, vp, d, d, d, vp, vp, vp, vp]
     getattr(lib, p + "dump").argtypes = [vp, vp, vp, vp, n_t]
     getattr(lib, p + "dump").restype = n_t
     getattr(lib, p + "dump_tree").argtypes = [vp, vp, vp, n_t]

@@ -15,4 +15,4 @@ from .field import (  # noqa: F401
     kernel_launch_count, red_peak,
     VERTEX_BYTES, VERTEX_F64_FIELDS, profile_enable, profile_collect, end_frame_all,
 )
-from .model import MODEL_ENTRY_DTYPE, MODEL_GRID, MODEL_KDTREE, ModelStore  # noqa: F401,E402
+from .model import MODEL_ENTRY_DTYPE, MODEL_GMM, MODEL_GRID, MODEL_KDTREE, ModelStore  # noqa: F401,E402

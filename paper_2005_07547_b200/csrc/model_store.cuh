@@ -41,11 +41,18 @@ struct MdlDev {
     unsigned long long *ctr; /* [0] entries, [1] dropped records, [2] touched-list length */
     uint32_t *tlist;
     uint32_t mask;
-    int kind, res, ns, leaves; /* ns: slots per entry (R^2, or 2L-1 nodes) */
+    int kind, res, ns, leaves; /* ns: slots per entry (R^2, 2L-1 nodes, or 21C+3 GMM state) */
     double tsplit;
+    int comps; /* GMM: components, alphaEm, eigenvalue floor / cap, reseed fraction */
+    double alpha_em, smin, smax, reseed_frac;
+    /* GMM frame samples (Gmm::m_frameSamples, in applyRecord order): entry, uv, contribution;
+     * count in ctr[MC_SAMPLES]; per-entry segments of the entry-sorted samples */
+    uint32_t *fs_entry;
+    double *fs_u, *fs_v, *fs_c;
+    uint32_t *seg_begin, *seg_end;
 };
 
-enum { MC_ENTRIES = 0, MC_DROPPED = 1, MC_TOUCHED = 2, MC_N = 4 };
+enum { MC_ENTRIES = 0, MC_DROPPED = 1, MC_TOUCHED = 2, MC_SAMPLES = 3, MC_N = 4 };
 
 struct pstf_model_store {
     pstf_model_config cfg;
@@ -53,6 +60,8 @@ struct pstf_model_store {
     uint32_t mask = 0;
     int ns = 0;
     DBuf state, keyf, ent, w, acc, kn, ctr, tlist, sums;
+    DBuf fs_entry, fs_u, fs_v, fs_c, seg, fs_key, fs_pos; /* GMM frame samples */
+    uint64_t fs_bound = 0; /* host upper bound of the samples appended this frame */
     Scratch sc;
     DBuf words;
     MdlDev dev() const {
@@ -71,6 +80,17 @@ struct pstf_model_store {
         d.ns = ns;
         d.leaves = cfg.kd_leaf_count;
         d.tsplit = cfg.kd_split_threshold;
+        d.comps = cfg.gmm_components;
+        d.alpha_em = cfg.gmm_alpha_em;
+        d.smin = cfg.gmm_sigma_min_sq;
+        d.smax = cfg.gmm_sigma_max_sq;
+        d.reseed_frac = cfg.gmm_reseed_fraction;
+        d.fs_entry = fs_entry.as<uint32_t>();
+        d.fs_u = fs_u.as<double>();
+        d.fs_v = fs_v.as<double>();
+        d.fs_c = fs_c.as<double>();
+        d.seg_begin = seg.as<uint32_t>();
+        d.seg_end = seg.as<uint32_t>() + (mask + 1ull);
         return d;
     }
 };
@@ -114,6 +134,11 @@ __device__ __forceinline__ double lerp_ref(double a, double b, double t) { /* ve
 }
 
 __device__ __forceinline__ double min_ref(double a, double b) { return b < a ? b : a; } /* std::min */
+__device__ __forceinline__ double clamp_ref(double x, double lo, double hi) { /* vecmath.h:19 */
+    const double a = x < lo ? lo : x;
+    return hi < a ? hi : a;
+}
+
 __device__ __forceinline__ double max_ref(double a, double b) { return a < b ? b : a; } /* std::max */
 
 /* findLeaf (models.cpp:140-159): boundary ties go to the lower child */
@@ -279,9 +304,213 @@ __device__ void kd_end_frame_warp(KdNode *K, double *P, double *A, int nn, int l
     __syncwarp();
 }
 
+/* ---- Gmm (models.cpp:427-702) on one entry's state vector ----
+ * layout (C components): W[C] weights, M[2C] means, V[3C] cov (cxx, cxy, cyy), U[8C] stepwise
+ * statistics, K[7C] cache (inv[3], norm, chol[3]), then i, underflows, reseed counter */
+#define GMM_TWO_PI (2.0 * 3.14159265358979323846) /* kTwoPi, vecmath.h:13-14 */
+#define GMM_MAX_COMPS 8
+
+struct GmmView {
+    double *W, *M, *V, *U, *K, *tail;
+    int C;
+};
+
+__host__ __device__ inline GmmView gmm_view(double *S, int C) {
+    return GmmView{S, S + C, S + 3 * C, S + 6 * C, S + 14 * C, S + 21 * C, C};
+}
+
+/* Gmm::rebuildCache (models.cpp:449-463) for component c */
+__host__ __device__ inline void gmm_cache(GmmView g, int c) {
+    const double a = g.V[3 * c], b = g.V[3 * c + 1], d = g.V[3 * c + 2];
+    const double det = a * d - b * b;
+    double *k = g.K + 7 * c;
+    k[0] = d / det;
+    k[1] = -b / det;
+    k[2] = a / det;
+    k[3] = 1.0 / (GMM_TWO_PI * sqrt(det));
+    k[4] = sqrt(a);
+    k[5] = b / k[4];
+    const double r = d - k[5] * k[5];
+    k[6] = sqrt(r < 0.0 ? 0.0 : r); /* std::max(., 0.0) */
+}
+
+/* componentPdf (models.cpp:465-480): the Gaussian wrapped over the 3x3 torus replicas */
+__device__ inline double gmm_component_pdf(const GmmView &g, int c, double x, double y) {
+    const double *k = g.K + 7 * c;
+    double sum = 0.0;
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+            const double ex = x + dx - g.M[2 * c], ey = y + dy - g.M[2 * c + 1];
+            const double q = k[0] * ex * ex + 2.0 * k[1] * ex * ey + k[2] * ey * ey;
+            sum += k[3] * exp(-0.5 * q);
+        }
+    return sum;
+}
+
+/* Gmm::pdf (models.cpp:657-662) */
+__device__ inline double gmm_pdf(const GmmView &g, double x, double y) {
+    double p = 0.0;
+    for (int c = 0; c < g.C; ++c) p += g.W[c] * gmm_component_pdf(g, c, x, y);
+    return p;
+}
+
+/* responsibilities (models.cpp:482-497); returns 1 when the mixture underflowed */
+__device__ inline int gmm_resp(const GmmView &g, double x, double y, double *gamma) {
+    double total = 0.0;
+    for (int c = 0; c < g.C; ++c) {
+        gamma[c] = g.W[c] * gmm_component_pdf(g, c, x, y);
+        total += gamma[c];
+    }
+    if (total <= 0.0 || !isfinite(total)) {
+        for (int c = 0; c < g.C; ++c) gamma[c] = 1.0 / g.C;
+        return 1;
+    }
+    for (int c = 0; c < g.C; ++c) gamma[c] /= total;
+    return 0;
+}
+
+/* Gmm::mstep (models.cpp:587-655), sequential (lane 0) */
+__device__ void gmm_mstep(GmmView g, const MdlDev &m) {
+    const int C = g.C;
+    double total = 0.0;
+    for (int c = 0; c < C; ++c) total += g.U[8 * c];
+    if (total <= 0.0) return;
+    int heaviest = 0;
+    for (int c = 1; c < C; ++c)
+        if (g.U[8 * c] > g.U[8 * heaviest]) heaviest = c;
+    for (int c = 0; c < C; ++c) {
+        const double *u = g.U + 8 * c;
+        const double mass = u[0];
+        if (mass <= m.reseed_frac * total) { /* reseed next to the heaviest component */
+            const double *h = g.U + 8 * heaviest;
+            const double sx = h[1] / h[0], sy = h[2] / h[0];
+            const uint32_t rc = (uint32_t)g.tail[2];
+            g.tail[2] = (double)(uint32_t)(rc + 1u);
+            const double jitter = 0.05 * (1.0 + (double)(rc % 7u));
+            double mx = sx + jitter * 0.01, my = sy - jitter * 0.01;
+            mx -= floor(mx);
+            my -= floor(my);
+            g.M[2 * c] = mx;
+            g.M[2 * c + 1] = my;
+            g.W[c] = 1e-3;
+            g.V[3 * c] = 0.01;
+            g.V[3 * c + 1] = 0.0;
+            g.V[3 * c + 2] = 0.01;
+            continue;
+        }
+        g.W[c] = mass / total;
+        const double mx = u[1] / mass, my = u[2] / mass;
+        const double exx = u[3] / mass, eyy = u[4] / mass, exy = u[5] / mass;
+        const double cxx = exx - mx * mx, cyy = eyy - my * my, cxy = exy - mx * my;
+        const double tr = cxx + cyy, diff = cxx - cyy;
+        const double dd = diff * diff + 4.0 * cxy * cxy;
+        const double disc = sqrt(dd < 0.0 ? 0.0 : dd);
+        const double l1 = 0.5 * (tr + disc), l2 = 0.5 * (tr - disc);
+        const double c1 = clamp_ref(l1, m.smin, m.smax), c2 = clamp_ref(l2, m.smin, m.smax);
+        double vx, vy;
+        if (fabs(cxy) > 1e-30) {
+            vx = l1 - cyy;
+            vy = cxy;
+        } else {
+            vx = cxx >= cyy ? 1.0 : 0.0;
+            vy = cxx >= cyy ? 0.0 : 1.0;
+        }
+        const double len = sqrt(vx * vx + vy * vy);
+        if (len > 0.0) {
+            vx /= len;
+            vy /= len;
+        }
+        g.V[3 * c] = c1 * vx * vx + c2 * vy * vy;
+        g.V[3 * c + 1] = (c1 - c2) * vx * vy;
+        g.V[3 * c + 2] = c1 * vy * vy + c2 * vx * vx;
+        g.M[2 * c] = mx;
+        g.M[2 * c + 1] = my;
+    }
+    double wsum = 0.0;
+    for (int c = 0; c < C; ++c) wsum += g.W[c];
+    for (int c = 0; c < C; ++c) g.W[c] /= wsum;
+    for (int c = 0; c < C; ++c) gmm_cache(g, c);
+}
+
+/* Gmm::estepBatch (models.cpp:525-585) + mstep for one entry's n frame samples, one warp:
+ * responsibilities at the pre-batch mixture, log g(j) by a warp prefix sum of
+ * log(1 - (i0+k)^-alpha), the statistics by lane-private partials (red[32][8C] in shared
+ * memory) reduced in lane order.  Sums are associated differently from the reference's
+ * sequential loops: agreement to rounding, not bitwise. */
+__device__ void gmm_end_frame_warp(const MdlDev &m, double *S, const uint32_t *pos, uint32_t b,
+                                   uint32_t n, unsigned lane, double *red) {
+    GmmView g = gmm_view(S, m.comps);
+    const int C = g.C, Q = 8 * C;
+    const uint64_t i0 = (uint64_t)g.tail[0];
+    const uint32_t last_zero = i0 == 0 ? 1u : 0u; /* factor(k) = 0 only at i0 + k == 1 */
+    auto lfac = [&](uint32_t k) { /* log factor of index k in 1..n; 0 up to the zero */
+        if (k <= last_zero) return 0.0;
+        return log(1.0 - pow((double)(i0 + k), -m.alpha_em));
+    };
+    /* pass 1: logPrefix[n] */
+    double ln = 0.0;
+    for (uint32_t t = 0; t < n; t += 32) {
+        const uint32_t k = t + lane + 1;
+        double x = k <= n ? lfac(k) : 0.0;
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        ln += x;
+    }
+    for (int q = 0; q < Q; ++q) red[lane * Q + q] = 0.0;
+    unsigned long long uflow = 0;
+    double carry = 0.0; /* logPrefix at the start of the chunk */
+    for (uint32_t t = 0; t < n; t += 32) {
+        const uint32_t j = t + lane + 1; /* sample index 1..n */
+        double x = j <= n ? lfac(j) : 0.0;
+        for (int o = 1; o < 32; o <<= 1) { /* inclusive scan */
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)lane >= o) x += y;
+        }
+        const double lp = carry + x; /* logPrefix[j] */
+        carry += __shfl_sync(0xffffffffu, x, 31);
+        if (j > n) continue;
+        const uint32_t p = pos[b + j - 1];
+        const double sx = m.fs_u[p], sy = m.fs_v[p], w = m.fs_c[p];
+        double gamma[GMM_MAX_COMPS];
+        uflow += gmm_resp(g, sx, sy, gamma);
+        const double gj = j < last_zero ? 0.0 : exp(ln - lp);
+        if (gj == 0.0) continue;
+        const double step = pow((double)(i0 + j), -m.alpha_em);
+        for (int c = 0; c < C; ++c) {
+            const double bb = step * w * gamma[c];
+            if (bb <= 0.0) continue;
+            const double bg = bb * gj;
+            double *r = red + lane * Q + 8 * c;
+            r[0] += bg;
+            r[1] += bg * sx;
+            r[2] += bg * sy;
+            r[3] += bg * sx * sx;
+            r[4] += bg * sy * sy;
+            r[5] += bg * sx * sy;
+            r[6] += gj * step * w;
+            r[7] += gj;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) uflow += __shfl_xor_sync(0xffffffffu, uflow, o);
+    __syncwarp();
+    const double g_total = 0 < last_zero ? 0.0 : exp(ln); /* gOf(0) */
+    for (int q = lane; q < Q; q += 32) {
+        double acc = g.U[q] * g_total;
+        for (int l = 0; l < 32; ++l) acc += red[l * Q + q];
+        g.U[q] = acc;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        g.tail[0] = (double)(i0 + n);
+        g.tail[1] += (double)uflow;
+        gmm_mstep(g, m);
+    }
+    __syncwarp();
+}
+
 /* accumulator slot of a record: the DirGrid cell or the k-d tree leaf */
 __device__ __forceinline__ int mdl_slot(const MdlDev &m, uint32_t e, double u, double v) {
     if (m.kind == PSTF_MODEL_GRID) return mdl_cell(u, v, m.res);
+    if (m.kind == PSTF_MODEL_GMM) return 0; /* one run per entry: its samples in canonical order */
     return kd_find_leaf(m.kn + (uint64_t)e * m.ns, u, v, nullptr, nullptr);
 }
 
@@ -310,12 +539,13 @@ __device__ int32_t mdl_find_or_insert(const MdlDev &m, const KeyFields &k) {
                         m.w[(uint64_t)e * m.ns + j] = w0;
                         m.acc[(uint64_t)e * m.ns + j] = 0.0;
                     }
-                } else { /* the uniform tree (models.cpp:96-127), built once on the host */
+                } else { /* the initial tree / mixture (models.cpp:96-127, 427-447), built
+                          * once on the host into the template entry */
                     const uint64_t t = (uint64_t)(m.mask + 1ull) * m.ns;
                     for (int j = 0; j < m.ns; ++j) {
                         m.w[(uint64_t)e * m.ns + j] = m.w[t + j];
                         m.acc[(uint64_t)e * m.ns + j] = 0.0;
-                        m.kn[(uint64_t)e * m.ns + j] = m.kn[t + j];
+                        if (m.kind == PSTF_MODEL_KDTREE) m.kn[(uint64_t)e * m.ns + j] = m.kn[t + j];
                     }
                 }
                 __threadfence();
@@ -355,7 +585,7 @@ __global__ void k_mdl_records(MdlDev m, const pstf_key *keys, const double *u, c
  * folded in a register in the canonical order, and applyRecord's counters (estimators.cpp:
  * 114-116; cNew += 1 per record is integer-valued, so adding the run length is exact) */
 __global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm, uint64_t n,
-                           int shift, const double *c) {
+                           int shift, const double *c, const double *u, const double *v) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t w = words[perm[i]];
@@ -375,7 +605,21 @@ __global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm
         }
         ++len;
     }
-    *acc = s;
+    if (m.kind == PSTF_MODEL_GMM) { /* Gmm::record (models.cpp:689-694): keep the samples */
+        unsigned long long o = cnt ? atomicAdd(&m.ctr[MC_SAMPLES], cnt) : 0;
+        for (uint64_t j = i; cnt && j < i + len; ++j) {
+            const uint32_t r = perm[j];
+            const double cv = c[r];
+            if (!(cv >= 0.0 && isfinite(cv))) continue;
+            m.fs_entry[o] = e;
+            m.fs_u[o] = u[r];
+            m.fs_v[o] = v[r];
+            m.fs_c[o] = cv;
+            ++o;
+        }
+    } else {
+        *acc = s;
+    }
     ModelEnt &x = m.ent[e];
     if (cnt) atomicAdd(&x.rec_count, cnt);
     atomicAdd(&x.records, len);
@@ -544,6 +788,48 @@ __global__ void __launch_bounds__(KD_WARPS * 32) k_mdl_blend_kd(MdlDev m, const 
     }
 }
 
+/* GMM endFrame: frame samples sorted by entry (stable: each entry keeps applyRecord order) */
+__global__ void k_gmm_keys(MdlDev m, uint64_t bound, uint32_t *key, uint32_t *pos) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= bound) return;
+    key[i] = i < m.ctr[MC_SAMPLES] ? m.fs_entry[i] : 0xffffffffu; /* unused tail sorts last */
+    pos[i] = (uint32_t)i;
+}
+
+__global__ void k_gmm_segs(MdlDev m, const uint32_t *key, uint64_t bound) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= bound) return;
+    const uint32_t e = key[i];
+    if (e == 0xffffffffu) return;
+    if (i == 0 || key[i - 1] != e) m.seg_begin[e] = (uint32_t)i;
+    if (i + 1 == bound || key[i + 1] != e) m.seg_end[e] = (uint32_t)i + 1;
+}
+
+#define GMM_WARPS 2
+__global__ void __launch_bounds__(GMM_WARPS * 32) k_mdl_blend_gmm(MdlDev m, const double *sums,
+                                                                  double t_max, int limited,
+                                                                  int min_samples,
+                                                                  const uint32_t *pos) {
+    extern __shared__ __align__(16) unsigned char gmm_smem[];
+    double *red = reinterpret_cast<double *>(gmm_smem) + (size_t)(threadIdx.x >> 5) * 32 * 8 * m.comps;
+    const uint64_t nt = m.ctr[MC_TOUCHED];
+    const unsigned lane = lane_id();
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nt;
+         i += nwarps) {
+        const uint32_t e = m.tlist[i];
+        ModelEnt x = m.ent[e];
+        x.touched = 0;
+        if (x.c_new > 0.0) {
+            const uint32_t b = m.seg_begin[e], n = m.seg_end[e] - b;
+            if (n) /* Gmm::endFrame (models.cpp:696-702): nothing without samples */
+                gmm_end_frame_warp(m, m.w + (uint64_t)e * m.ns, pos, b, n, lane, red);
+            mdl_close(x, sums, t_max, limited, min_samples);
+        }
+        if (lane == 0) m.ent[e] = x;
+    }
+}
+
 __device__ __forceinline__ int32_t mdl_find_warm(const MdlDev &m, const KeyFields &k) {
     const uint32_t home = mdl_home(k, m.mask);
     for (uint32_t i = 0; i <= m.mask; ++i) {
@@ -616,6 +902,7 @@ __device__ void kd_sample(const MdlDev &m, int32_t e, double ux, double uy, doub
 /* DirGrid::pdf (models.cpp:52-56) / SphericalKdTree::pdf */
 __device__ __forceinline__ double mdl_pdf(const MdlDev &m, int32_t e, double u, double v) {
     if (e < 0) return 1.0;
+    if (m.kind == PSTF_MODEL_GMM) return gmm_pdf(gmm_view(m.w + (uint64_t)e * m.ns, m.comps), u, v);
     if (m.kind != PSTF_MODEL_GRID) return kd_pdf(m, e, u, v);
     const double tot = m.ent[e].total;
     if (tot <= 0.0) return 1.0;
@@ -628,18 +915,39 @@ __global__ void k_mdl_pdf(MdlDev m, const int32_t *ent, const double *u, const d
     if (i < n) out[i] = mdl_pdf(m, ent[i], u[i], v[i]);
 }
 
-__device__ __forceinline__ double clamp_ref(double x, double lo, double hi) { /* vecmath.h:19 */
-    const double a = x < lo ? lo : x;
-    return hi < a ? hi : a;
-}
-
 /* DirGrid::sample (models.cpp:58-92): row by the marginal, then column, residuals remapped */
 __global__ void k_mdl_sample(MdlDev m, const int32_t *ent, const double *u1, const double *u2,
-                             uint64_t n, double *su, double *sv, double *spdf) {
+                             const double *usel, uint64_t n, double *su, double *sv,
+                             double *spdf) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t e = ent[i];
     const double ux = u1[i], uy = u2[i];
+    if (e >= 0 && m.kind == PSTF_MODEL_GMM) { /* Gmm::sample (models.cpp:664-687) */
+        const GmmView g = gmm_view(m.w + (uint64_t)e * m.ns, m.comps);
+        const double us = usel[i];
+        int comp = 0;
+        double acc = 0.0;
+        for (int c = 0; c < g.C; ++c) {
+            acc += g.W[c];
+            if (us < acc || c == g.C - 1) {
+                comp = c;
+                break;
+            }
+        }
+        const double om = 1.0 - ux;
+        const double r = sqrt(-2.0 * log(om < 1e-300 ? 1e-300 : om)); /* std::max */
+        const double z0 = r * cos(GMM_TWO_PI * uy), z1 = r * sin(GMM_TWO_PI * uy);
+        const double *k = g.K + 7 * comp;
+        double px = g.M[2 * comp] + k[4] * z0;
+        double py = g.M[2 * comp + 1] + k[5] * z0 + k[6] * z1;
+        px -= floor(px);
+        py -= floor(py);
+        su[i] = px;
+        sv[i] = py;
+        spdf[i] = gmm_pdf(g, px, py);
+        return;
+    }
     if (e >= 0 && m.kind != PSTF_MODEL_GRID) {
         kd_sample(m, e, ux, uy, &su[i], &sv[i], &spdf[i]);
         return;
@@ -729,15 +1037,21 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
     if (!config || !out) return set_err(PSTF_E_INVALID, "NULL argument");
     *out = nullptr;
     const bool kd = config->kind == PSTF_MODEL_KDTREE;
-    if (!kd && config->kind != PSTF_MODEL_GRID)
-        return set_err(PSTF_E_INVALID, "kind must be PSTF_MODEL_GRID or PSTF_MODEL_KDTREE");
-    if (!kd && (config->grid_resolution < 1 || config->grid_resolution > 256))
+    if (config->kind < PSTF_MODEL_GRID || config->kind > PSTF_MODEL_GMM)
+        return set_err(PSTF_E_INVALID, "kind must be PSTF_MODEL_GRID, _KDTREE or _GMM");
+    if (config->kind == PSTF_MODEL_GRID &&
+        (config->grid_resolution < 1 || config->grid_resolution > 256))
         return set_err(PSTF_E_INVALID, "grid_resolution must be in [1, 256]"); /* models.cpp:17-18 */
     if (kd && (config->kd_leaf_count < 2 || config->kd_leaf_count > 256 ||
                (config->kd_leaf_count & (config->kd_leaf_count - 1)) != 0)) /* models.cpp:99-101 */
         return set_err(PSTF_E_INVALID, "kd_leaf_count must be a power of two in [2, 256]");
     if (kd && !(config->kd_split_threshold > 1.0)) /* models.cpp:203-204 */
         return set_err(PSTF_E_INVALID, "kd_split_threshold must be > 1");
+    const bool gmm = config->kind == PSTF_MODEL_GMM;
+    if (gmm && (config->gmm_components < 1 || config->gmm_components > GMM_MAX_COMPS))
+        return set_err(PSTF_E_INVALID, "gmm_components must be in [1, 8]"); /* models.cpp:429-430 */
+    if (gmm && !(config->gmm_alpha_em > 0.5 && config->gmm_alpha_em <= 1.0))
+        return set_err(PSTF_E_INVALID, "gmm_alpha_em must lie in (0.5, 1]"); /* models.cpp:431-432 */
     if (config->capacity_log2 < 1 || config->capacity_log2 > 26)
         return set_err(PSTF_E_INVALID, "capacity_log2 must be in [1, 26]");
     CK(cudaSetDevice(device));
@@ -746,7 +1060,9 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
     m->device = device;
     const uint64_t cap = 1ull << config->capacity_log2;
     m->mask = (uint32_t)(cap - 1);
-    m->ns = kd ? 2 * config->kd_leaf_count - 1 : config->grid_resolution * config->grid_resolution;
+    m->ns = kd    ? 2 * config->kd_leaf_count - 1
+            : gmm ? 21 * config->gmm_components + 3
+                  : config->grid_resolution * config->grid_resolution;
     const uint64_t cells = (cap + 1) * (uint64_t)m->ns; /* + the k-d template entry */
     if (cells * 16 > (64ull << 30)) return set_err(PSTF_E_INVALID, "model table too large");
     ENSURE(m->state, cap * 4);
@@ -771,6 +1087,31 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
                       cudaMemcpyHostToDevice));
         CK(cudaMemcpy(m->w.as<double>() + cap * m->ns, P.data(), m->ns * 8, cudaMemcpyHostToDevice));
     }
+    if (gmm) { /* Gmm's constructor (models.cpp:427-447) into the template entry */
+        const int C = config->gmm_components;
+        std::vector<double> S(m->ns, 0.0);
+        GmmView g = gmm_view(S.data(), C);
+        int grid = 1;
+        while (grid * grid < C) ++grid;
+        for (int c = 0; c < C; ++c) {
+            g.W[c] = 1.0 / C;
+            g.V[3 * c] = 0.02;
+            g.V[3 * c + 1] = 0.0;
+            g.V[3 * c + 2] = 0.02;
+            g.M[2 * c] = ((c % grid) + 0.5) / grid;
+            g.M[2 * c + 1] = ((c / grid) + 0.5) / grid;
+            gmm_cache(g, c);
+        }
+        CK(cudaMemcpy(m->w.as<double>() + cap * m->ns, S.data(), m->ns * 8, cudaMemcpyHostToDevice));
+        ENSURE(m->seg, 2 * cap * 4);
+        CK(cudaMemset(m->seg.p, 0, 2 * cap * 4));
+        ENSURE(m->fs_entry, 1024 * 4);
+        ENSURE(m->fs_u, 1024 * 8);
+        ENSURE(m->fs_v, 1024 * 8);
+        ENSURE(m->fs_c, 1024 * 8);
+        CK(cudaFuncSetAttribute(k_mdl_blend_gmm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GMM_WARPS * 32 * 8 * GMM_MAX_COMPS * 8));
+    }
     CK(cudaDeviceSynchronize());
     *out = m.release();
     return PSTF_OK;
@@ -784,6 +1125,18 @@ int pstf_model_destroy(pstf_model_store *m) {
     return PSTF_OK;
 }
 
+/* grows b to at least `need` bytes keeping its first `keep` bytes (GMM frame samples) */
+static int grow_keep(DBuf &b, size_t need, size_t keep, cudaStream_t st) {
+    if (need <= b.bytes) return PSTF_OK;
+    DBuf nb;
+    ENSURE(nb, need);
+    if (keep) CK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    std::swap(b.p, nb.p);
+    std::swap(b.bytes, nb.bytes); /* nb now owns (and frees) the old buffer */
+    return PSTF_OK;
+}
+
 int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
                      const double *contribution, uint64_t n, int mode, void *stream) {
     if (!m || (n && (!keys || !u || !v || !contribution)))
@@ -794,6 +1147,16 @@ int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u,
     if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "batch too large");
     CK(cudaSetDevice(m->device));
     const cudaStream_t st = (cudaStream_t)stream;
+    if (m->cfg.kind == PSTF_MODEL_GMM) { /* samples kept in canonical order (stepwise EM) */
+        mode = PSTF_MODE_ORDERED;
+        const uint64_t keep = m->fs_bound, need = keep + n;
+        int rc = grow_keep(m->fs_entry, need * 4, keep * 4, st);
+        if (!rc) rc = grow_keep(m->fs_u, need * 8, keep * 8, st);
+        if (!rc) rc = grow_keep(m->fs_v, need * 8, keep * 8, st);
+        if (!rc) rc = grow_keep(m->fs_c, need * 8, keep * 8, st);
+        if (rc) return rc;
+        m->fs_bound = need;
+    }
     if (mode == PSTF_MODE_ATOMIC) {
         LAUNCH(k_mdl_atomic, grid_for(n, 256), 256, 0, st, m->dev(), keys, u, v, contribution, n);
         return PSTF_OK;
@@ -809,7 +1172,8 @@ int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u,
     uint32_t *perm = nullptr;
     int rc = sort_multiword(m->sc, words, bb, 4, n, &perm, st);
     if (rc) return rc;
-    LAUNCH(k_mdl_fold, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, contribution);
+    LAUNCH(k_mdl_fold, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, contribution, u,
+           v);
     return PSTF_OK;
 }
 
@@ -823,7 +1187,35 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
     CK(cudaMemsetAsync(m->sums.p, 0, 16, st));
     LAUNCH(k_mdl_sums, (unsigned)sm_count() * 2, 256, 0, st, d, m->sums.as<double>());
     const uint64_t cap = (uint64_t)m->mask + 1;
-    if (m->cfg.kind == PSTF_MODEL_GRID)
+    if (m->cfg.kind == PSTF_MODEL_GMM) {
+        const uint64_t bound = m->fs_bound, cap2 = (uint64_t)m->mask + 1;
+        uint32_t *pos_sorted = nullptr;
+        CK(cudaMemsetAsync(m->seg.p, 0, 2 * cap2 * 4, st));
+        if (bound) { /* the frame's samples grouped by entry, each entry in record order */
+            ENSURE(m->fs_key, 2 * bound * 4);
+            ENSURE(m->fs_pos, 2 * bound * 4);
+            uint32_t *key = m->fs_key.as<uint32_t>(), *pos = m->fs_pos.as<uint32_t>();
+            LAUNCH(k_gmm_keys, grid_for(bound, 256), 256, 0, st, d, bound, key, pos);
+            size_t bytes = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key + bound, pos, pos + bound,
+                                               (int64_t)bound, 0, 32, st));
+            ENSURE(m->sc.cub, bytes);
+            bytes = m->sc.cub.bytes;
+            {
+                ProfScope ps_("cub::DeviceRadixSort", st);
+                CK(cub::DeviceRadixSort::SortPairs(m->sc.cub.p, bytes, key, key + bound, pos,
+                                                   pos + bound, (int64_t)bound, 0, 32, st));
+                g_launches.fetch_add(4, std::memory_order_relaxed);
+            }
+            LAUNCH(k_gmm_segs, grid_for(bound, 256), 256, 0, st, d, key + bound, bound);
+            pos_sorted = pos + bound;
+        }
+        LAUNCH(k_mdl_blend_gmm, (unsigned)sm_count() * 8, GMM_WARPS * 32,
+               (size_t)GMM_WARPS * 32 * 8 * m->cfg.gmm_components * 8, st, d, m->sums.as<double>(),
+               t_max, limited, m->cfg.min_samples, pos_sorted);
+        CK(cudaMemsetAsync(&m->ctr.as<unsigned long long>()[MC_SAMPLES], 0, 8, st));
+        m->fs_bound = 0;
+    } else if (m->cfg.kind == PSTF_MODEL_GRID)
         LAUNCH(k_mdl_blend, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(), t_max,
                limited, m->cfg.min_samples);
     else
@@ -866,14 +1258,16 @@ int pstf_model_pdf(const pstf_model_store *m, const int32_t *entry, const double
 }
 
 int pstf_model_sample(const pstf_model_store *m, const int32_t *entry, const double *u1,
-                      const double *u2, uint64_t n, double *su, double *sv, double *pdf,
-                      void *stream) {
+                      const double *u2, const double *u_select, uint64_t n, double *su,
+                      double *sv, double *pdf, void *stream) {
     if (!m || (n && (!entry || !u1 || !u2 || !su || !sv || !pdf)))
         return set_err(PSTF_E_INVALID, "NULL argument");
+    if (n && m->cfg.kind == PSTF_MODEL_GMM && !u_select)
+        return set_err(PSTF_E_INVALID, "GMM sampling needs u_select");
     if (!n) return PSTF_OK;
     CK(cudaSetDevice(m->device));
     LAUNCH(k_mdl_sample, grid_for(n, 128), 128, 0, (cudaStream_t)stream, m->dev(), entry, u1, u2,
-           n, su, sv, pdf);
+           u_select, n, su, sv, pdf);
     return PSTF_OK;
 }
 

@@ -124,7 +124,7 @@ def lib():
         "pstf_model_lookup_warm": ([vp, vp, u64, vp, vp], i32),
         "pstf_model_lookup_warm_levels": ([vp, vp, vp, vp, vp, u64, vp, vp], i32),
         "pstf_model_pdf": ([vp, vp, vp, vp, u64, vp, vp], i32),
-        "pstf_model_sample": ([vp, vp, vp, vp, u64, vp, vp, vp, vp], i32),
+        "pstf_model_sample": ([vp, vp, vp, vp, vp, u64, vp, vp, vp, vp], i32),
         "pstf_model_get_stats": ([vp, vp], i32),
         "pstf_model_dump": ([vp, vp, vp, vp, u64, vp], i32),
         "pstf_model_dump_tree": ([vp, vp, vp, u64, vp], i32),

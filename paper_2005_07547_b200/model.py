@@ -1,8 +1,8 @@
 """CV-profile / guiding model store on the B200.
 
 Python mirror of the reference's ``ModelStore`` (estimators.h:124-150, estimators.cpp:104-144)
-with ``DirGrid`` (models.h:30-52, models.cpp:16-94) or ``SphericalKdTree`` models
-(models.h:59-109, models.cpp:96-298) over the C ABI
+with ``DirGrid`` (models.h:30-52, models.cpp:16-94), ``SphericalKdTree`` (models.h:59-109,
+models.cpp:96-298) or ``Gmm`` models (models.h:113-177, models.cpp:427-702) over the C ABI
 (``pstf_model_*`` in include/pstf_field.h).  Keys are the field's SpatioDirectionalKeys;
 records are applied in the reference's deterministic order, so entries, weights and
 accumulators are bitwise those of ``EstimatorRun`` in deterministic mode."""
@@ -21,12 +21,15 @@ MODEL_ENTRY_DTYPE = np.dtype([("level", "<i4"), ("cell", "<i4", (3,)), ("dir", "
 assert MODEL_ENTRY_DTYPE.itemsize == 72
 
 
-MODEL_GRID, MODEL_KDTREE = 0, 1  # ModelKind (models.h:183); Gmm is not built
+MODEL_GRID, MODEL_KDTREE, MODEL_GMM = 0, 1, 2  # ModelKind (models.h:183)
 
 
 class _ModelConfig(C.Structure):
     _fields_ = [("kind", C.c_int32), ("grid_resolution", C.c_int32),
                 ("kd_leaf_count", C.c_int32), ("kd_split_threshold", C.c_double),
+                ("gmm_components", C.c_int32), ("gmm_alpha_em", C.c_double),
+                ("gmm_sigma_min_sq", C.c_double), ("gmm_sigma_max_sq", C.c_double),
+                ("gmm_reseed_fraction", C.c_double),
                 ("t_max", C.c_double), ("min_samples", C.c_int32), ("capacity_log2", C.c_uint32)]
 
 
@@ -42,13 +45,18 @@ class ModelStore:
     estimators.h:32,56-57); capacity_log2 sizes the device table (the reference map grows)."""
 
     def __init__(self, grid_resolution=16, t_max=64.0, min_samples=32, capacity_log2=16,
-                 device=0, kind=MODEL_GRID, kd_leaf_count=64, kd_split_threshold=4.0):
+                 device=0, kind=MODEL_GRID, kd_leaf_count=64, kd_split_threshold=4.0,
+                 gmm_components=4, gmm_alpha_em=0.7, gmm_sigma_min_sq=2.5e-5,
+                 gmm_sigma_max_sq=0.04, gmm_reseed_fraction=1e-4):
         self.kind = kind
         self.res = int(grid_resolution)
-        self.r2 = 2 * kd_leaf_count - 1 if kind == MODEL_KDTREE else self.res * self.res
+        self.r2 = (2 * kd_leaf_count - 1 if kind == MODEL_KDTREE else
+                   21 * gmm_components + 3 if kind == MODEL_GMM else self.res * self.res)
         self.device = device
         self._h = C.c_void_p()
         cfg = _ModelConfig(int(kind), self.res, int(kd_leaf_count), float(kd_split_threshold),
+                           int(gmm_components), float(gmm_alpha_em), float(gmm_sigma_min_sq),
+                           float(gmm_sigma_max_sq), float(gmm_reseed_fraction),
                            float(t_max), int(min_samples), int(capacity_log2))
         _check(lib().pstf_model_create(C.byref(cfg), device, C.byref(self._h)))
 
@@ -123,15 +131,17 @@ class ModelStore:
                                     _stream()))
         return out
 
-    def sample(self, entry, u1, u2):
-        """DirGrid::sample(u) (models.cpp:58-92) -> (u, v, pdf); entry -1 -> (u1, u2, 1.0)"""
+    def sample(self, entry, u1, u2, u_select=None):
+        """DirGrid / SphericalKdTree::sample(u), Gmm::sample(u_select, u) (models.cpp:58-92,
+        176-200, 664-687) -> (u, v, pdf); entry -1 -> (u1, u2, 1.0)"""
         t = _torch()
         e = t.as_tensor(entry).to(device=self._dev(), dtype=t.int32).contiguous()
         a, b = self._f64(u1), self._f64(u2)
+        us = None if u_select is None else self._f64(u_select)
         n = e.numel()
         su, sv, pdf = (t.empty(n, dtype=t.float64, device=self._dev()) for _ in range(3))
-        _check(lib().pstf_model_sample(self._h, _ptr(e), _ptr(a), _ptr(b), n, _ptr(su), _ptr(sv),
-                                       _ptr(pdf), _stream()))
+        _check(lib().pstf_model_sample(self._h, _ptr(e), _ptr(a), _ptr(b), _ptr(us), n, _ptr(su),
+                                       _ptr(sv), _ptr(pdf), _stream()))
         return su, sv, pdf
 
     def stats(self) -> dict:

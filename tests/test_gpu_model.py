@@ -185,3 +185,56 @@ def test_kdtree_model_store_bitwise(leaves, tsplit, t_max):
     sg = [x.cpu().numpy() for x in g.sample(torch.from_numpy(ent), u, v)]
     for a, b in zip(sg, r.sample(q, u, v)[:3]):
         np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("comps,alpha,skew,edges", [(4, 0.7, 2.0, True), (3, 0.95, 1.0, False),
+                                                   (3, 0.95, 1.0, True), (1, 0.6, 3.0, True)])
+def test_gmm_model_store_close(comps, alpha, skew, edges):
+    """Gmm kind (models.cpp:427-702, the batch E-step by prefix sums), with
+    two apply calls per frame (samples keep call order).  Counters, warm flags, the step index,
+    underflows and reseeds are exact.  The state goes through exp/log/pow (not glibc's) and
+    differently associated sums: on streams without edge values it agrees to rtol 1e-9
+    throughout (weights, means, covariances, statistics, cache, pdf, sample).  Streams with
+    border uv / duplicates can leave a hot new entry ill-conditioned: there the statistics,
+    weights and means are held to 1e-6 and the inverse-covariance cache is not compared."""
+    rng = np.random.default_rng(comps * 13 + int(alpha * 100))
+    g = pb.ModelStore(16, 64.0, 4, capacity_log2=10, kind=pb.MODEL_GMM, gmm_components=comps,
+                      gmm_alpha_em=alpha)
+    if po.model_ref_available():
+        r = po.RefModelStore(16, 64.0, 4, kind=2, comps=comps, alpha_em=alpha)
+    else:
+        r = po.OracleModelStore(16, 64.0, 4, kind=2, comps=comps, alpha_em=alpha)
+    C = comps
+    tol = 1e-6 if edges else 1e-9
+    for frame in range(5):
+        k, u, v, c, keys = mc.model_records(rng, 4000, 120, skew=skew)
+        if not edges:
+            u, v = rng.random(len(k)) ** skew, rng.random(len(k)) ** skew
+            c = rng.exponential(1.0, len(k)) + 0.1
+        half = len(k) // 2
+        for s in (g, r):
+            s.apply(k[:half], u[:half], v[:half], c[:half])
+            s.apply(k[half:], u[half:], v[half:], c[half:])
+            s.end_frame()
+        eg, sg, _ = g.dump()
+        er, sr, _ = r.dump()
+        assert len(eg) == len(er)
+        for f in ("level", "cell", "dir", "warm", "c_old", "c_new", "records", "record_count"):
+            np.testing.assert_array_equal(eg[f], er[f], err_msg=f)
+        np.testing.assert_array_equal(sg[:, 21 * C:], sr[:, 21 * C:])  # i, underflows, reseeds
+        upto = 21 * C if not edges else 3 * C  # W, M (+ V, U, cache on clean streams)
+        np.testing.assert_allclose(sg[:, :upto], sr[:, :upto], rtol=tol, atol=1e-12)
+        np.testing.assert_allclose(sg[:, 6 * C:14 * C], sr[:, 6 * C:14 * C], rtol=tol, atol=1e-12)
+    q, u, v = mc.probe_points(rng, keys, 2000)
+    us = rng.random(len(q))
+    ent = g.lookup_warm(q).cpu().numpy()
+    pr, found = r.pdf(q, u, v)
+    np.testing.assert_array_equal(ent >= 0, found)
+    assert found.sum() > 50
+    if edges:
+        return
+    pg = g.pdf(torch.from_numpy(ent), u, v).cpu().numpy()
+    np.testing.assert_allclose(pg, pr, rtol=1e-9)
+    sg = [x.cpu().numpy() for x in g.sample(torch.from_numpy(ent), u, v, us)]
+    for a, b in zip(sg, r.sample(q, u, v, us)[:3]):
+        np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-12)

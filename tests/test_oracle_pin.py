@@ -298,3 +298,32 @@ def test_kdtree_model_store_matches_reference(leaves, tsplit, t_max):
         np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
     assert fo.sum() > 50 and (moved.sum() > 0 or leaves == 2)  # warm; split-collapse happened
 
+
+@pytest.mark.skipif(not po.model_ref_available(), reason="oracle/_ref model store not built")
+@pytest.mark.parametrize("comps,alpha,skew", [(4, 0.7, 2.0), (3, 0.95, 1.0), (1, 0.6, 3.0)])
+def test_gmm_model_store_matches_reference(comps, alpha, skew):
+    """Gmm kind (models.cpp:427-702: batch E-step by prefix sums, M-step with eigenvalue clamps
+    and reseeding): the C restatement uses the same libm as the reference, so the whole state
+    (weights, means, covariances, statistics, cache, step index, underflows, reseeds), pdf and
+    sample agree bitwise."""
+    import model_cases as mc
+    rng = np.random.default_rng(comps * 13 + int(alpha * 100))
+    o = po.OracleModelStore(16, 64.0, 4, kind=2, comps=comps, alpha_em=alpha)
+    r = po.RefModelStore(16, 64.0, 4, kind=2, comps=comps, alpha_em=alpha)
+    for frame in range(5):
+        k, u, v, c, keys = mc.model_records(rng, 4000, 120, skew=skew)
+        o.apply(k, u, v, c)
+        r.apply(k, u, v, c)
+        o.end_frame()
+        r.end_frame()
+        _model_equal(o, r)
+    q, u, v = mc.probe_points(rng, keys, 2000)
+    us = rng.random(len(q))
+    po_, fo = o.pdf(q, u, v)
+    pr_, fr = r.pdf(q, u, v)
+    np.testing.assert_array_equal(fo, fr)
+    np.testing.assert_array_equal(po_.view(np.uint64), pr_.view(np.uint64))
+    for a, b in zip(o.sample(q, u, v, us), r.sample(q, u, v, us)):
+        np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+    assert fo.sum() > 50
+
