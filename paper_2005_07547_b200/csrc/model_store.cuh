@@ -61,6 +61,7 @@ struct pstf_model_store {
     int ns = 0;
     DBuf state, keyf, ent, w, acc, kn, ctr, tlist, sums;
     DBuf fs_entry, fs_u, fs_v, fs_c, seg, fs_key, fs_pos; /* GMM frame samples */
+    DBuf gch_n, gch_f;                                     /* GMM E-step chunks */
     uint64_t fs_bound = 0; /* host upper bound of the samples appended this frame */
     Scratch sc;
     DBuf words;
@@ -432,79 +433,39 @@ __device__ void gmm_mstep(GmmView g, const MdlDev &m) {
     for (int c = 0; c < C; ++c) gmm_cache(g, c);
 }
 
-/* Gmm::estepBatch (models.cpp:525-585) + mstep for one entry's n frame samples, one warp:
- * responsibilities at the pre-batch mixture, log g(j) by a warp prefix sum of
- * log(1 - (i0+k)^-alpha), the statistics by lane-private partials (red[32][8C] in shared
- * memory) reduced in lane order.  Sums are associated differently from the reference's
- * sequential loops: agreement to rounding, not bitwise. */
-__device__ void gmm_end_frame_warp(const MdlDev &m, double *S, const uint32_t *pos, uint32_t b,
-                                   uint32_t n, unsigned lane, double *red) {
-    GmmView g = gmm_view(S, m.comps);
-    const int C = g.C, Q = 8 * C;
-    const uint64_t i0 = (uint64_t)g.tail[0];
-    const uint32_t last_zero = i0 == 0 ? 1u : 0u; /* factor(k) = 0 only at i0 + k == 1 */
-    auto lfac = [&](uint32_t k) { /* log factor of index k in 1..n; 0 up to the zero */
-        if (k <= last_zero) return 0.0;
-        return log(1.0 - pow((double)(i0 + k), -m.alpha_em));
-    };
-    /* pass 1: logPrefix[n] */
-    double ln = 0.0;
-    for (uint32_t t = 0; t < n; t += 32) {
-        const uint32_t k = t + lane + 1;
-        double x = k <= n ? lfac(k) : 0.0;
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        ln += x;
+/* Gmm::estepBatch (models.cpp:525-585), sample-parallel.  An entry's n frame samples are cut
+ * into chunks of GMM_CHUNK; every chunk is one warp in each of two passes:
+ *   A  the chunk's sum of log(1 - (i0+k)^-alpha) (the factor of index k; zero up to the
+ *      restart at i0 + k == 1, as the reference's lastZero);
+ *   (per entry, sequential over its chunks: the chunk offsets of logPrefix and logPrefix[n])
+ *   C  per sample: responsibilities at the pre-batch mixture, g(j) = exp(logPrefix[n] -
+ *      logPrefix[j]), the stepScale-weighted terms, summed per chunk in lane order;
+ * then per entry: U = U * g(0) + the chunk partials in chunk order, i += n, mstep.  The sums
+ * associate differently from the reference's sequential loops: agreement to rounding. */
+#define GMM_CHUNK 256
+
+struct GmmChunks {
+    const uint32_t *chbase; /* exclusive scan of the chunk counts over the touched list */
+    double *lsum, *off, *ln; /* per chunk: log-factor sum, logPrefix at its start; per entry: total */
+    double *part;            /* per chunk: 8C partial statistics */
+    unsigned long long *uflow;
+    const uint32_t *pos;     /* frame samples in entry order */
+};
+
+__device__ __forceinline__ double gmm_lfac(uint64_t i0, uint32_t k, double alpha) {
+    if (i0 + k <= 1) return 0.0; /* factor 0 at i0 + k == 1: logPrefix restarts there */
+    return log(1.0 - pow((double)(i0 + k), -alpha));
+}
+
+/* chunk q -> (touched index t, chunk k of that entry); chbase[t] <= q < chbase[t + 1] */
+__device__ __forceinline__ uint32_t gmm_chunk_owner(const uint32_t *chbase, uint32_t nt,
+                                                    uint32_t q) {
+    uint32_t lo = 0, hi = nt; /* chbase[lo] <= q < chbase[hi] */
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (chbase[mid] <= q) lo = mid; else hi = mid;
     }
-    for (int q = 0; q < Q; ++q) red[lane * Q + q] = 0.0;
-    unsigned long long uflow = 0;
-    double carry = 0.0; /* logPrefix at the start of the chunk */
-    for (uint32_t t = 0; t < n; t += 32) {
-        const uint32_t j = t + lane + 1; /* sample index 1..n */
-        double x = j <= n ? lfac(j) : 0.0;
-        for (int o = 1; o < 32; o <<= 1) { /* inclusive scan */
-            const double y = __shfl_up_sync(0xffffffffu, x, o);
-            if ((int)lane >= o) x += y;
-        }
-        const double lp = carry + x; /* logPrefix[j] */
-        carry += __shfl_sync(0xffffffffu, x, 31);
-        if (j > n) continue;
-        const uint32_t p = pos[b + j - 1];
-        const double sx = m.fs_u[p], sy = m.fs_v[p], w = m.fs_c[p];
-        double gamma[GMM_MAX_COMPS];
-        uflow += gmm_resp(g, sx, sy, gamma);
-        const double gj = j < last_zero ? 0.0 : exp(ln - lp);
-        if (gj == 0.0) continue;
-        const double step = pow((double)(i0 + j), -m.alpha_em);
-        for (int c = 0; c < C; ++c) {
-            const double bb = step * w * gamma[c];
-            if (bb <= 0.0) continue;
-            const double bg = bb * gj;
-            double *r = red + lane * Q + 8 * c;
-            r[0] += bg;
-            r[1] += bg * sx;
-            r[2] += bg * sy;
-            r[3] += bg * sx * sx;
-            r[4] += bg * sy * sy;
-            r[5] += bg * sx * sy;
-            r[6] += gj * step * w;
-            r[7] += gj;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) uflow += __shfl_xor_sync(0xffffffffu, uflow, o);
-    __syncwarp();
-    const double g_total = 0 < last_zero ? 0.0 : exp(ln); /* gOf(0) */
-    for (int q = lane; q < Q; q += 32) {
-        double acc = g.U[q] * g_total;
-        for (int l = 0; l < 32; ++l) acc += red[l * Q + q];
-        g.U[q] = acc;
-    }
-    __syncwarp();
-    if (lane == 0) {
-        g.tail[0] = (double)(i0 + n);
-        g.tail[1] += (double)uflow;
-        gmm_mstep(g, m);
-    }
-    __syncwarp();
+    return lo;
 }
 
 /* accumulator slot of a record: the DirGrid cell or the k-d tree leaf */
@@ -585,7 +546,7 @@ __global__ void k_mdl_records(MdlDev m, const pstf_key *keys, const double *u, c
  * folded in a register in the canonical order, and applyRecord's counters (estimators.cpp:
  * 114-116; cNew += 1 per record is integer-valued, so adding the run length is exact) */
 __global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm, uint64_t n,
-                           int shift, const double *c, const double *u, const double *v) {
+                           int shift, const double *c) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t w = words[perm[i]];
@@ -605,26 +566,62 @@ __global__ void k_mdl_fold(MdlDev m, const uint64_t *words, const uint32_t *perm
         }
         ++len;
     }
-    if (m.kind == PSTF_MODEL_GMM) { /* Gmm::record (models.cpp:689-694): keep the samples */
-        unsigned long long o = cnt ? atomicAdd(&m.ctr[MC_SAMPLES], cnt) : 0;
-        for (uint64_t j = i; cnt && j < i + len; ++j) {
-            const uint32_t r = perm[j];
-            const double cv = c[r];
-            if (!(cv >= 0.0 && isfinite(cv))) continue;
-            m.fs_entry[o] = e;
-            m.fs_u[o] = u[r];
-            m.fs_v[o] = v[r];
-            m.fs_c[o] = cv;
-            ++o;
-        }
-    } else {
-        *acc = s;
-    }
+    *acc = s;
     ModelEnt &x = m.ent[e];
     if (cnt) atomicAdd(&x.rec_count, cnt);
     atomicAdd(&x.records, len);
     atomicAdd(&x.c_new, (double)len);
     if (atomicExch(&x.touched, 1u) == 0u) m.tlist[atomicAdd(&m.ctr[MC_TOUCHED], 1ull)] = e;
+}
+
+/* GMM apply: Gmm::record keeps the accepted samples in applyRecord order (models.cpp:689-694),
+ * so each accepted record, in the call's canonical order, goes to position count + rank of the
+ * frame-sample list (rank = exclusive scan of the accepted flags); ModelStore's counters are
+ * added per warp-run of equal entries (integer-valued: any order is exact) */
+__global__ void k_gmm_flags(const uint64_t *words, const uint32_t *perm, uint64_t n,
+                            const double *c, uint32_t *flag) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = perm[i];
+    const double cv = c[r];
+    flag[i] = words[r] != ~0ull && cv >= 0.0 && isfinite(cv);
+}
+
+__global__ void k_gmm_append(MdlDev m, const uint64_t *words, const uint32_t *perm, uint64_t n,
+                             int shift, const uint32_t *flag, const uint32_t *rank,
+                             const double *u, const double *v, const double *c) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    int64_t e = -1;
+    bool ok = false;
+    if (live) {
+        const uint32_t r = perm[i];
+        const uint64_t w = words[r];
+        if (w != ~0ull) {
+            e = (int64_t)((w >> shift) >> 16);
+            ok = flag[i] != 0;
+            if (ok) {
+                const uint64_t o = m.ctr[MC_SAMPLES] + rank[i];
+                m.fs_entry[o] = (uint32_t)e;
+                m.fs_u[o] = u[r];
+                m.fs_v[o] = v[r];
+                m.fs_c[o] = c[r];
+            }
+        }
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, (long long)e);
+    const unsigned okm = __ballot_sync(0xffffffffu, ok);
+    if (e < 0 || lane_id() != (unsigned)(__ffs(grp) - 1)) return;
+    const unsigned len = __popc(grp), acc_n = __popc(okm & grp);
+    ModelEnt &x = m.ent[e];
+    if (acc_n) atomicAdd(&x.rec_count, (unsigned long long)acc_n);
+    atomicAdd(&x.records, (unsigned long long)len);
+    atomicAdd(&x.c_new, (double)len);
+    if (atomicExch(&x.touched, 1u) == 0u) m.tlist[atomicAdd(&m.ctr[MC_TOUCHED], 1ull)] = (uint32_t)e;
+}
+
+__global__ void k_gmm_count(MdlDev m, const uint32_t *flag, const uint32_t *rank, uint64_t n) {
+    m.ctr[MC_SAMPLES] += rank[n - 1] + flag[n - 1];
 }
 
 /* ATOMIC mode: records applied straight into the entries, no sort.  Accumulator sums then
@@ -805,13 +802,119 @@ __global__ void k_gmm_segs(MdlDev m, const uint32_t *key, uint64_t bound) {
     if (i + 1 == bound || key[i + 1] != e) m.seg_end[e] = (uint32_t)i + 1;
 }
 
+/* chunk counts per touched entry (0 without samples or past the touched list) */
+__global__ void k_gmm_nchunks(MdlDev m, uint64_t cap, uint32_t *nch) {
+    uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t > cap) return;
+    uint32_t c = 0;
+    if (t < m.ctr[MC_TOUCHED]) {
+        const uint32_t e = m.tlist[t];
+        const uint32_t n = m.seg_end[e] - m.seg_begin[e];
+        c = (n + GMM_CHUNK - 1) / GMM_CHUNK;
+    }
+    nch[t] = c;
+}
+
+/* pass A: log-factor sum of each chunk */
+__global__ void k_gmm_chunk_logs(MdlDev m, GmmChunks ch) {
+    const uint32_t nt = (uint32_t)m.ctr[MC_TOUCHED];
+    const uint32_t total = ch.chbase[nt];
+    const unsigned lane = lane_id();
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < total; q += nwarps) {
+        const uint32_t t = gmm_chunk_owner(ch.chbase, nt, q), e = m.tlist[t];
+        const uint32_t n = m.seg_end[e] - m.seg_begin[e];
+        const uint64_t i0 = (uint64_t)gmm_view(m.w + (uint64_t)e * m.ns, m.comps).tail[0];
+        const uint32_t j0 = (q - ch.chbase[t]) * GMM_CHUNK; /* samples j0+1 .. */
+        double x = 0.0;
+        for (uint32_t j = j0 + lane + 1; j <= min(n, j0 + GMM_CHUNK); j += 32)
+            x += gmm_lfac(i0, j, m.alpha_em);
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) ch.lsum[q] = x;
+    }
+}
+
+/* per entry: logPrefix at each chunk start and logPrefix[n] */
+__global__ void k_gmm_chunk_offsets(MdlDev m, GmmChunks ch) {
+    const uint32_t nt = (uint32_t)m.ctr[MC_TOUCHED];
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    double run = 0.0;
+    for (uint32_t q = ch.chbase[t]; q < ch.chbase[t + 1]; ++q) {
+        ch.off[q] = run;
+        run += ch.lsum[q];
+    }
+    ch.ln[t] = run;
+}
+
+/* pass C: each chunk's statistics at the pre-batch mixture */
 #define GMM_WARPS 2
-__global__ void __launch_bounds__(GMM_WARPS * 32) k_mdl_blend_gmm(MdlDev m, const double *sums,
-                                                                  double t_max, int limited,
-                                                                  int min_samples,
-                                                                  const uint32_t *pos) {
+__global__ void __launch_bounds__(GMM_WARPS * 32) k_gmm_chunk_stats(MdlDev m, GmmChunks ch) {
     extern __shared__ __align__(16) unsigned char gmm_smem[];
-    double *red = reinterpret_cast<double *>(gmm_smem) + (size_t)(threadIdx.x >> 5) * 32 * 8 * m.comps;
+    const int C = m.comps, Q = 8 * C;
+    double *red = reinterpret_cast<double *>(gmm_smem) + (size_t)(threadIdx.x >> 5) * 32 * Q;
+    const uint32_t nt = (uint32_t)m.ctr[MC_TOUCHED];
+    const uint32_t total = ch.chbase[nt];
+    const unsigned lane = lane_id();
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < total; q += nwarps) {
+        const uint32_t t = gmm_chunk_owner(ch.chbase, nt, q), e = m.tlist[t];
+        const uint32_t b = m.seg_begin[e], n = m.seg_end[e] - b;
+        const GmmView g = gmm_view(m.w + (uint64_t)e * m.ns, C);
+        const uint64_t i0 = (uint64_t)g.tail[0];
+        const uint32_t j0 = (q - ch.chbase[t]) * GMM_CHUNK, j1 = min(n, j0 + GMM_CHUNK);
+        const double ln = ch.ln[t];
+        for (int k = 0; k < Q; ++k) red[lane * Q + k] = 0.0;
+        unsigned long long uflow = 0;
+        double carry = ch.off[q];
+        for (uint32_t jb = j0; jb < j1; jb += 32) {
+            const uint32_t j = jb + lane + 1; /* sample index 1..n */
+            double x = j <= j1 ? gmm_lfac(i0, j, m.alpha_em) : 0.0;
+            for (int o = 1; o < 32; o <<= 1) { /* inclusive scan */
+                const double y = __shfl_up_sync(0xffffffffu, x, o);
+                if ((int)lane >= o) x += y;
+            }
+            const double lp = carry + x; /* logPrefix[j] */
+            carry += __shfl_sync(0xffffffffu, x, 31);
+            if (j > j1) continue;
+            const uint32_t p = ch.pos[b + j - 1];
+            const double sx = m.fs_u[p], sy = m.fs_v[p], w = m.fs_c[p];
+            double gamma[GMM_MAX_COMPS];
+            uflow += gmm_resp(g, sx, sy, gamma);
+            const double gj = exp(ln - lp); /* gOf(j): j >= 1 >= lastZero */
+            if (gj == 0.0) continue;
+            const double step = pow((double)(i0 + j), -m.alpha_em);
+            for (int c = 0; c < C; ++c) {
+                const double bb = step * w * gamma[c];
+                if (bb <= 0.0) continue;
+                const double bg = bb * gj;
+                double *r = red + lane * Q + 8 * c;
+                r[0] += bg;
+                r[1] += bg * sx;
+                r[2] += bg * sy;
+                r[3] += bg * sx * sx;
+                r[4] += bg * sy * sy;
+                r[5] += bg * sx * sy;
+                r[6] += gj * step * w;
+                r[7] += gj;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) uflow += __shfl_xor_sync(0xffffffffu, uflow, o);
+        __syncwarp();
+        for (int k = lane; k < Q; k += 32) { /* lanes in order */
+            double acc = 0.0;
+            for (int l = 0; l < 32; ++l) acc += red[l * Q + k];
+            ch.part[(uint64_t)q * Q + k] = acc;
+        }
+        if (lane == 0) ch.uflow[q] = uflow;
+        __syncwarp();
+    }
+}
+
+/* per touched entry: U = U * g(0) + the chunk partials (chunk order), i += n, mstep, then
+ * ModelStore's bookkeeping (estimators.cpp:129-143) */
+__global__ void k_mdl_blend_gmm(MdlDev m, const double *sums, double t_max, int limited,
+                                int min_samples, GmmChunks ch) {
     const uint64_t nt = m.ctr[MC_TOUCHED];
     const unsigned lane = lane_id();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -821,9 +924,29 @@ __global__ void __launch_bounds__(GMM_WARPS * 32) k_mdl_blend_gmm(MdlDev m, cons
         ModelEnt x = m.ent[e];
         x.touched = 0;
         if (x.c_new > 0.0) {
-            const uint32_t b = m.seg_begin[e], n = m.seg_end[e] - b;
-            if (n) /* Gmm::endFrame (models.cpp:696-702): nothing without samples */
-                gmm_end_frame_warp(m, m.w + (uint64_t)e * m.ns, pos, b, n, lane, red);
+            const uint32_t n = m.seg_end[e] - m.seg_begin[e];
+            if (n) { /* Gmm::endFrame (models.cpp:696-702): nothing without samples */
+                GmmView g = gmm_view(m.w + (uint64_t)e * m.ns, m.comps);
+                const int Q = 8 * m.comps;
+                const uint64_t i0 = (uint64_t)g.tail[0];
+                const double g0 = i0 == 0 ? 0.0 : exp(ch.ln[i]); /* gOf(0) */
+                const uint32_t q0 = ch.chbase[i], q1 = ch.chbase[i + 1];
+                for (int k = lane; k < Q; k += 32) {
+                    double acc = g.U[k] * g0;
+                    for (uint32_t q = q0; q < q1; ++q) acc += ch.part[(uint64_t)q * Q + k];
+                    g.U[k] = acc;
+                }
+                unsigned long long uf = 0;
+                for (uint32_t q = q0 + lane; q < q1; q += 32) uf += ch.uflow[q];
+                for (int o = 16; o > 0; o >>= 1) uf += __shfl_xor_sync(0xffffffffu, uf, o);
+                __syncwarp();
+                if (lane == 0) {
+                    g.tail[0] = (double)(i0 + n);
+                    g.tail[1] += (double)uf;
+                    gmm_mstep(g, m);
+                }
+                __syncwarp();
+            }
             mdl_close(x, sums, t_max, limited, min_samples);
         }
         if (lane == 0) m.ent[e] = x;
@@ -1109,7 +1232,7 @@ int pstf_model_create(const pstf_model_config *config, int device, pstf_model_st
         ENSURE(m->fs_u, 1024 * 8);
         ENSURE(m->fs_v, 1024 * 8);
         ENSURE(m->fs_c, 1024 * 8);
-        CK(cudaFuncSetAttribute(k_mdl_blend_gmm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_gmm_chunk_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GMM_WARPS * 32 * 8 * GMM_MAX_COMPS * 8));
     }
     CK(cudaDeviceSynchronize());
@@ -1172,8 +1295,25 @@ int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u,
     uint32_t *perm = nullptr;
     int rc = sort_multiword(m->sc, words, bb, 4, n, &perm, st);
     if (rc) return rc;
-    LAUNCH(k_mdl_fold, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, contribution, u,
-           v);
+    if (m->cfg.kind == PSTF_MODEL_GMM) {
+        ENSURE(m->fs_key, 2 * n * 4);
+        uint32_t *flag = m->fs_key.as<uint32_t>(), *rank = flag + n;
+        LAUNCH(k_gmm_flags, grid_for(n, 256), 256, 0, st, words, perm, n, contribution, flag);
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, rank, (int64_t)n, st));
+        ENSURE(m->sc.cub, bytes);
+        bytes = m->sc.cub.bytes;
+        {
+            ProfScope ps_("cub::DeviceScan", st);
+            CK(cub::DeviceScan::ExclusiveSum(m->sc.cub.p, bytes, flag, rank, (int64_t)n, st));
+            g_launches.fetch_add(2, std::memory_order_relaxed);
+        }
+        LAUNCH(k_gmm_append, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, flag, rank,
+               u, v, contribution);
+        LAUNCH(k_gmm_count, 1, 1, 0, st, d, flag, rank, n);
+        return PSTF_OK;
+    }
+    LAUNCH(k_mdl_fold, grid_for(n, 256), 256, 0, st, d, words, perm, n, shift, contribution);
     return PSTF_OK;
 }
 
@@ -1210,9 +1350,39 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
             LAUNCH(k_gmm_segs, grid_for(bound, 256), 256, 0, st, d, key + bound, bound);
             pos_sorted = pos + bound;
         }
-        LAUNCH(k_mdl_blend_gmm, (unsigned)sm_count() * 8, GMM_WARPS * 32,
-               (size_t)GMM_WARPS * 32 * 8 * m->cfg.gmm_components * 8, st, d, m->sums.as<double>(),
-               t_max, limited, m->cfg.min_samples, pos_sorted);
+        /* chunked E-step: chunk counts -> their scan over the touched list -> passes A, C */
+        ENSURE(m->gch_n, (cap2 + 2) * 4 * 2);
+        uint32_t *nch = m->gch_n.as<uint32_t>(), *chbase = nch + cap2 + 2;
+        LAUNCH(k_gmm_nchunks, grid_for(cap2 + 1, 256), 256, 0, st, d, cap2, nch);
+        {
+            size_t bytes = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, nch, chbase, (int64_t)(cap2 + 1), st));
+            ENSURE(m->sc.cub, bytes);
+            bytes = m->sc.cub.bytes;
+            ProfScope ps_("cub::DeviceScan", st);
+            CK(cub::DeviceScan::ExclusiveSum(m->sc.cub.p, bytes, nch, chbase, (int64_t)(cap2 + 1),
+                                             st));
+            g_launches.fetch_add(2, std::memory_order_relaxed);
+        }
+        const uint64_t max_chunks = bound / GMM_CHUNK + cap2 + 1;
+        const int Q = 8 * m->cfg.gmm_components;
+        ENSURE(m->gch_f, (max_chunks * (3 + Q) + cap2 + 1) * 8);
+        GmmChunks gc;
+        gc.chbase = chbase;
+        gc.lsum = m->gch_f.as<double>();
+        gc.off = gc.lsum + max_chunks;
+        gc.part = gc.off + max_chunks;
+        gc.ln = gc.part + max_chunks * Q;
+        gc.uflow = reinterpret_cast<unsigned long long *>(gc.ln + cap2 + 1);
+        gc.pos = pos_sorted;
+        if (bound) {
+            LAUNCH(k_gmm_chunk_logs, (unsigned)sm_count() * 8, 256, 0, st, d, gc);
+            LAUNCH(k_gmm_chunk_offsets, grid_for(cap2, 128), 128, 0, st, d, gc);
+            LAUNCH(k_gmm_chunk_stats, (unsigned)sm_count() * 16, GMM_WARPS * 32,
+                   (size_t)GMM_WARPS * 32 * Q * 8, st, d, gc);
+        }
+        LAUNCH(k_mdl_blend_gmm, (unsigned)sm_count() * 8, 256, 0, st, d, m->sums.as<double>(),
+               t_max, limited, m->cfg.min_samples, gc);
         CK(cudaMemsetAsync(&m->ctr.as<unsigned long long>()[MC_SAMPLES], 0, 8, st));
         m->fs_bound = 0;
     } else if (m->cfg.kind == PSTF_MODEL_GRID)

@@ -37,7 +37,7 @@ def frame_records(it, rng):
 
 res = int(os.environ.get("RES", "16"))
 mode = pb.MODE_ATOMIC if os.environ.get("MODE", "ordered") == "atomic" else pb.MODE_ORDERED
-kind = pb.MODEL_KDTREE if os.environ.get("KIND", "grid") == "kdtree" else pb.MODEL_GRID
+kind = {"grid": pb.MODEL_GRID, "kdtree": pb.MODEL_KDTREE, "gmm": pb.MODEL_GMM}[os.environ.get("KIND", "grid")]
 ms = pb.ModelStore(res, 64.0, 32, capacity_log2=int(os.environ.get("CAP", "22")), kind=kind)
 rng = np.random.default_rng(0)
 frames = [frame_records(i, rng) for i in range(6)]
@@ -69,7 +69,7 @@ if os.environ.get("PROFILE"):
     for name, (t, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         print(f"  {name[:40]:40s} {t:8.3f} ms x{cnt}")
 st = ms.stats()
-out = {"kind": "kdtree" if kind == pb.MODEL_KDTREE else "grid",
+out = {"kind": ["grid", "kdtree", "gmm"][kind],
        "mode": "atomic" if mode == pb.MODE_ATOMIC else "ordered", "records_per_frame": nrec // nf, "entries": st["entries"], "warm": st["warm"],
        "grid_resolution": res, "apply_ms": t_apply / nf, "end_frame_ms": t_ef / nf,
        "gpu_records_per_s": nrec / ((t_apply + t_ef) / 1e3)}
@@ -79,7 +79,7 @@ if po.model_ref_available():
     k, u, v, c = frames[2]
     m = k.shape[0] // 16  # bounded sample: 1/16 of a frame
     kn = k[:m].cpu().numpy().view(po.KEY_DTYPE).reshape(m)
-    r = po.RefModelStore(res, 64.0, 32, kind=1 if kind == pb.MODEL_KDTREE else 0)
+    r = po.RefModelStore(res, 64.0, 32, kind=kind)
     t0 = time.perf_counter()
     r.apply(kn, u[:m].cpu().numpy(), v[:m].cpu().numpy(), c[:m].cpu().numpy())
     r.end_frame()
