@@ -102,3 +102,17 @@ def test_read_snapshot_matches_reference_writer(tmp_path, lib):
     bad.write_bytes(b"NOTASNAP0000")
     with pytest.raises(pb.PstfError, match="not a field snapshot"):
         pb.read_snapshot(str(bad))
+
+
+@pytest.mark.parametrize("kw", [dict(grid_resolution=0), dict(grid_resolution=300),
+                                dict(kind=1, kd_leaf_count=48), dict(kind=1, kd_leaf_count=1),
+                                dict(kind=1, kd_split_threshold=1.0),
+                                dict(kind=2, gmm_components=0), dict(kind=2, gmm_components=9),
+                                dict(kind=2, gmm_alpha_em=0.5), dict(kind=2, gmm_alpha_em=1.2),
+                                dict(kind=3), dict(capacity_log2=0)])
+def test_invalid_model_config_rejected(lib, kw):
+    """the model store validates its configuration as the reference constructors do
+    (models.cpp:17-18, 99-101, 203-204, 429-432) before touching the device"""
+    import paper_2005_07547_b200 as pb
+    with pytest.raises(pb.PstfError, match="must|kind"):
+        pb.ModelStore(**kw)
