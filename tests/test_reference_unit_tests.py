@@ -56,3 +56,18 @@ def test_reference_unit_tests_on_reference(case):
 @pytest.mark.parametrize("case", FIELD_CASES)
 def test_reference_unit_tests_on_b200(case):
     _run("unit_field_b200", case)
+
+
+@pytest.mark.gpu
+def test_facade_load_snapshot_round_trip(tmp_path):
+    """checkpoint/resume through the drop-in C++ facade: dumpSnapshot -> loadSnapshot (the
+    facade's extension over pstf_field_load_snapshot) -> dumpSnapshot gives byte-identical files
+    and identical queries; a snapshot of another field kind is refused (tests/native/
+    facade_restore.cpp)."""
+    exe = os.path.join(BIN, "facade_restore")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "facade restore ok" in r.stdout
+
