@@ -291,6 +291,9 @@ int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pst
                            const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
                            uint32_t fli_mask, void *stream);
 int pstf_pending_count(pstf_field *lo, uint64_t *n);
+/* the same count written to a device int64 on the stream (no host round trip): the ranks
+ * all-gather it on the device and read every size with one synchronisation */
+int pstf_pending_count_dev(pstf_field *lo, int64_t *dev_count, void *stream);
 int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream);
 int pstf_resolve_records(pstf_field *const *stores, int nst, const void *records, uint64_t n,
                          void *stream);
@@ -309,6 +312,10 @@ int pstf_end_frame_reduce_dev(pstf_field *const *stores, int nst, double *dev_su
                               void *stream);
 int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *dev_sum_count,
                               void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
+/* ... and with the delta count written to a device int64 instead of returned (no host round
+ * trip); cap must cover every owned slot (sum of capacity / world), else PSTF_E_INVALID */
+int pstf_end_frame_commit_async(pstf_field *const *stores, int nst, const double *dev_sum_count,
+                                void *deltas, uint64_t cap, int64_t *dev_ndeltas, void *stream);
 uint64_t pstf_pending_record_bytes(void); /* 64 */
 uint64_t pstf_partial_record_bytes(void); /* 40: {u32 store, u32 slot, f64 acc[4]} */
 uint64_t pstf_delta_record_bytes(void);   /* 48: {u32 store, slot, checksum, last+1; f64 com[4]} */

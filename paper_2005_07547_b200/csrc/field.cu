@@ -4038,6 +4038,20 @@ int pstf_pending_count(pstf_field *lo, uint64_t *n) {
     return PSTF_OK;
 }
 
+__global__ void k_count_out(const unsigned long long *src, uint64_t cap, long long *dst) {
+    if (threadIdx.x == 0) dst[0] = (long long)(src ? (*src < cap ? *src : cap) : 0ull);
+}
+
+int pstf_pending_count_dev(pstf_field *lo, int64_t *dev_count, void *stream) {
+    if (!lo || !dev_count) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(lo->device));
+    SETTLE(lo);
+    LAUNCH(k_count_out, 1, 32, 0, (cudaStream_t)stream,
+           lo->sc.pend_count.as<unsigned long long>(), lo->sc.pend.bytes / sizeof(PendRec),
+           reinterpret_cast<long long *>(dev_count));
+    return PSTF_OK;
+}
+
 int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream) {
     if (!lo || (n && !dst)) return set_err(PSTF_E_INVALID, "NULL argument");
     if (!n) return PSTF_OK;
@@ -4127,7 +4141,8 @@ int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t
                sc.uid.as<uint32_t>() + off[j], nw[j], nw[j] / (uint64_t)world,
                sc.ranges.as<unsigned long long>() + (size_t)j * world, (PartialRec *)out);
     }
-    CK(cudaStreamSynchronize(st)); /* db (pageable) and the caller's counts are consumed */
+    /* no sync: the pageable db was staged by cudaMemcpyAsync before it returned, and the
+     * caller's counts are host values already */
     return PSTF_OK;
 }
 
@@ -4214,10 +4229,11 @@ int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, v
 
 static int end_frame_commit_impl(pstf_field *const *stores, int nst, const double *host_sums,
                                  const double *dev_sums, void *deltas, uint64_t cap,
-                                 uint64_t *ndeltas, void *stream) {
+                                 uint64_t *ndeltas, void *stream, int64_t *dev_ndeltas = nullptr) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if ((!host_sums && !dev_sums) || !ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
+    if ((!host_sums && !dev_sums) || (!ndeltas && !dev_ndeltas))
+        return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
@@ -4256,6 +4272,10 @@ static int end_frame_commit_impl(pstf_field *const *stores, int nst, const doubl
     if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0, (const unsigned long long *)nullptr);
     LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
     for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
+    if (dev_ndeltas) { /* no host round trip; cap covers every owned slot (checked by caller) */
+        LAUNCH(k_count_out, 1, 32, 0, st, dcount, cap, reinterpret_cast<long long *>(dev_ndeltas));
+        return PSTF_OK;
+    }
     CK(cudaMemcpyAsync(sc.h_small, dcount, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const unsigned long long nd = sc.h_small[0];
@@ -4274,6 +4294,16 @@ int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *
                               void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
     return end_frame_commit_impl(stores, nst, nullptr, dev_sum_count, deltas, cap, ndeltas,
                                  stream);
+}
+int pstf_end_frame_commit_async(pstf_field *const *stores, int nst, const double *dev_sum_count,
+                                void *deltas, uint64_t cap, int64_t *dev_ndeltas, void *stream) {
+    if (!deltas || !dev_ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
+    uint64_t owned = 0; /* deltas are the owned touched or evicted slots: at most every one */
+    for (int i = 0; i < nst; ++i)
+        if (stores[i]) owned += ((uint64_t)stores[i]->d.mask + 1) / (uint64_t)std::max(1, stores[i]->world);
+    if (cap < owned) return set_err(PSTF_E_INVALID, "deltas buffer smaller than the owned slots");
+    return end_frame_commit_impl(stores, nst, nullptr, dev_sum_count, deltas, cap, nullptr,
+                                 stream, dev_ndeltas);
 }
 
 int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,

@@ -59,6 +59,33 @@ class Collectives:
             return out
         return torch.cat([out[r * mx:r * mx + sz] for r, sz in enumerate(sizes)])
 
+    def all_gather_counted(self, count, make_buf):
+        """Variable-length all-gather when the local length is only known on the device:
+        count is a 1-element int64 device tensor (bytes), make_buf(n) returns the local n-byte
+        buffer.  One host synchronisation for every rank's size (instead of a local readback
+        followed by the size exchange)."""
+        import torch
+        sizes = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        self.dist.all_gather_into_tensor(sizes, count)
+        sizes = [int(x) for x in sizes.tolist()]
+        return self._gather_known(make_buf(sizes[self.rank]), sizes)
+
+    def _gather_known(self, buf, sizes):
+        import torch
+        mx = max(sizes)
+        if mx == 0:
+            return torch.empty(0, dtype=torch.uint8, device=self.device)
+        if buf.numel() == mx:
+            pad = buf.contiguous()
+        else:
+            pad = torch.zeros(mx, dtype=torch.uint8, device=self.device)
+            pad[:buf.numel()] = buf
+        out = torch.empty(self.world * mx, dtype=torch.uint8, device=self.device)
+        self.dist.all_gather_into_tensor(out, pad)
+        if all(sz == mx for sz in sizes):
+            return out
+        return torch.cat([out[r * mx:r * mx + sz] for r, sz in enumerate(sizes)])
+
     def all_to_all_bytes(self, buf, send_counts, rec_bytes):
         """buf holds world consecutive segments of send_counts[r] records (rec_bytes each)."""
         import torch
@@ -93,15 +120,23 @@ class ShardedFieldCache:
 
     def iteration(self, stripe):
         b, c = self.b, self.c
+        counted = hasattr(b, "pending_count_dev") and hasattr(c, "all_gather_counted")
         b.vertex_pass_local(stripe)                                    # 1
-        recs = c.all_gather_bytes(b.pending_bytes())                   # 2
+        if counted:  # device-side sizes: one host sync per variable-size exchange
+            recs = c.all_gather_counted(b.pending_count_dev(), b.pending_bytes_n)
+        else:
+            recs = c.all_gather_bytes(b.pending_bytes())               # 2
         b.resolve(recs)
         out, counts = b.partials_export()                              # 3
         recv, _ = c.all_to_all_bytes(out, counts, PARTIAL_BYTES)
         b.partials_import(recv)
         sums = c.all_reduce_sum(b.end_frame_reduce())                  # 4
-        deltas = b.end_frame_commit(sums)                              # 5
-        b.deltas_import(c.all_gather_bytes(deltas))
+        if counted:                                                    # 5
+            buf, nd = b.end_frame_commit_async(sums)
+            b.deltas_import(c.all_gather_counted(nd, lambda n: buf[:n]))
+        else:
+            deltas = b.end_frame_commit(sums)
+            b.deltas_import(c.all_gather_bytes(deltas))
 
 
 def stripe_of(n_paths, bounces, rank, world):
@@ -138,6 +173,8 @@ class CudaBackend:
             "pstf_end_frame_commit": [vp, i32, vp, vp, u64, vp, vp],
             "pstf_end_frame_reduce_dev": [vp, i32, vp, vp],
             "pstf_end_frame_commit_dev": [vp, i32, vp, vp, u64, vp, vp],
+            "pstf_end_frame_commit_async": [vp, i32, vp, vp, u64, vp, vp],
+            "pstf_pending_count_dev": [vp, vp, vp],
             "pstf_deltas_import": [vp, i32, vp, u64, vp], "pstf_shard_set": [vp, i32, i32],
         }.items():
             fn = getattr(L, name)
@@ -165,6 +202,38 @@ class CudaBackend:
             self.F._check(self.L.pstf_pending_copy(self.stores[0].handle, C.c_void_p(out.data_ptr()),
                                                    n.value, self.F._stream()))
         return out
+
+    def pending_count_dev(self):
+        """pending-record bytes of this rank as a 1-element int64 device tensor"""
+        torch = self._torch()
+        n = torch.empty(1, dtype=torch.int64, device="cuda")
+        self.F._check(self.L.pstf_pending_count_dev(self.stores[0].handle, C.c_void_p(n.data_ptr()),
+                                                    self.F._stream()))
+        return n * PENDING_BYTES
+
+    def pending_bytes_n(self, nbytes):
+        """the pending records (nbytes known from the size exchange) as a uint8 device tensor"""
+        torch = self._torch()
+        out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        n = nbytes // PENDING_BYTES
+        if n:
+            self.F._check(self.L.pstf_pending_copy(self.stores[0].handle, C.c_void_p(out.data_ptr()),
+                                                   n, self.F._stream()))
+        return out
+
+    def end_frame_commit_async(self, sums):
+        """owners blend + evict; (delta buffer, its byte count as a device int64 tensor)"""
+        torch = self._torch()
+        cap = sum(s.capacity // self.world for s in self.stores)
+        out = torch.empty(max(cap, 1) * DELTA_BYTES, dtype=torch.uint8, device="cuda")
+        nd = torch.empty(1, dtype=torch.int64, device="cuda")
+        sums = sums.to(torch.float64).contiguous()
+        self.F._check(self.L.pstf_end_frame_commit_async(self._arr, len(self.stores),
+                                                         C.c_void_p(sums.data_ptr()),
+                                                         C.c_void_p(out.data_ptr()), max(cap, 1),
+                                                         C.c_void_p(nd.data_ptr()),
+                                                         self.F._stream()))
+        return out, nd * DELTA_BYTES
 
     def resolve(self, recs):
         n = recs.numel() // PENDING_BYTES

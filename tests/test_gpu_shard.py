@@ -23,9 +23,14 @@ def _stores(cap, base, evict):
             for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
 
 
-@pytest.mark.parametrize("world,cap,mult,evict", [(2, 12, 8.0, 2), (4, 14, 1.0, 64),
-                                                  (2, 10, 30.0, 2)])
-def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict):
+@pytest.mark.parametrize("world,cap,mult,evict,counted", [(2, 12, 8.0, 2, False),
+                                                          (4, 14, 1.0, 64, False),
+                                                          (2, 10, 30.0, 2, False),
+                                                          (2, 12, 8.0, 2, True),
+                                                          (4, 14, 1.0, 64, True)])
+def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict, counted):
+    """counted: the exchanges whose sizes stay on the device (pstf_pending_count_dev,
+    pstf_end_frame_commit_async), as ShardedFieldCache uses them over NCCL"""
     W, H, B, frames = 96, 54, 4, 4
     base = inputs.BASE_CORNELL * mult
     single = _stores(cap, base, evict)
@@ -42,7 +47,11 @@ def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict):
             sb, sn = pb.synth_generate(W, H, B, iteration=it, path0=p0, npaths=p1 - p0)
             be.vertex_pass_local((sb, sn))
         # 2: all-gather pending records, identical placement everywhere
-        allrec = torch.cat([be.pending_bytes() for be in bes])
+        if counted:
+            allrec = torch.cat([be.pending_bytes_n(int(be.pending_count_dev().item()))
+                                for be in bes])
+        else:
+            allrec = torch.cat([be.pending_bytes() for be in bes])
         for be in bes:
             be.resolve(allrec)
         # 3: partials to owners (all-to-all)
@@ -56,7 +65,11 @@ def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict):
         # 4: global pass-1 sums
         sums = sum(be.end_frame_reduce() for be in bes)
         # 5: commit + all-gather deltas
-        deltas = torch.cat([be.end_frame_commit(sums) for be in bes])
+        if counted:
+            parts = [be.end_frame_commit_async(sums) for be in bes]
+            deltas = torch.cat([buf[:int(nd.item())] for buf, nd in parts])
+        else:
+            deltas = torch.cat([be.end_frame_commit(sums) for be in bes])
         for be in bes:
             be.deltas_import(deltas)
         torch.cuda.synchronize()
