@@ -1377,13 +1377,26 @@ __global__ void k_ranges(const PendRec *pend, const unsigned long long *count, u
             mx[f] = max(mx[f], v);
         }
     }
+    /* warp, then block reduction: one pair of atomics per field per block (the 14 global
+     * words are shared by every block, so per-warp atomics serialise) */
+    __shared__ int smn[NF_KEY], smx[NF_KEY];
+    if (threadIdx.x < NF_KEY) {
+        smn[threadIdx.x] = INT32_MAX;
+        smx[threadIdx.x] = INT32_MIN;
+    }
+    __syncthreads();
     for (int f = 0; f < NF_KEY; ++f) {
         int a = __reduce_min_sync(0xffffffffu, mn[f]);
         int b = __reduce_max_sync(0xffffffffu, mx[f]);
         if (lane_id() == 0) {
-            atomicMin(&out[2 * f], a);
-            atomicMax(&out[2 * f + 1], b);
+            atomicMin(&smn[f], a);
+            atomicMax(&smx[f], b);
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < NF_KEY) {
+        atomicMin(&out[2 * threadIdx.x], smn[threadIdx.x]);
+        atomicMax(&out[2 * threadIdx.x + 1], smx[threadIdx.x]);
     }
 }
 
