@@ -202,9 +202,17 @@ def cpu_reference_run(args, steps, warmup, budget_s):
         t_pass += a
         t_ef += b
     value = tot_v / tot_t
+    phases = None
+    if kind == "reference":  # keygen / lookup / insert / endFrame separately
+        sbuf, m = samples[0]
+        ph = po.vertex_pass_phases_ref(*stores[:3], sbuf, m, threads)
+        scale = n_full / m
+        phases = {k: round(v * scale, 2) for k, v in ph.items()}
+        phases["endFrame"] = round(t_ef / steps * 1e3, 2)
     return {
         "value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
-        "kind": kind,
+        "kind": kind, "host": po.host_info(),
+        "phases_ms_per_iteration": phases,
         "sample": (f"{frac:.4f} of the {n_full}-vertex config-2 iteration per step "
                    f"({samples[0][1]} vertices = all {B} bounces of a random path subset), "
                    f"{steps} steps after {warmup} warm-up; each step = onVertex replay "
@@ -230,7 +238,8 @@ def run_reference_arm(args):
                                "stream, Lo/LoE/FLi stores x 2^22 slots (reference FieldStore on "
                                "host cores)", "vertices_per_iter": args.width * args.height * args.bounces},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-                         "sample": r["sample"]},
+                         "sample": r["sample"], "host": r["host"],
+                         "phases_ms_per_iteration": r["phases_ms_per_iteration"]},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -461,7 +470,8 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference_run(args, 2, 1, budget_s=args.cpu_seconds)
-            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                       "host", "phases_ms_per_iteration")}
         except Exception as e:  # report, never fail the GPU line
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                                     "sample": f"error: {e}"}

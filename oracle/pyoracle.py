@@ -455,6 +455,33 @@ def vertex_pass_ref(lo, loe, fli, li, buf, n, loe_mask=TECH_ALL, fli_mask=TECH_A
                        loe_mask, fli_mask, 1 if deterministic else 0, threads, chunk)
 
 
+def vertex_pass_phases_ref(lo, loe, fli, buf, n, threads, loe_mask=TECH_ALL, fli_mask=TECH_ALL):
+    """the reference replay timed by phase (keygen, lookup, insert; ms), SURVEY.md §8(d)"""
+    lib = ref_lib()
+    fn = lib.pr_vertex_pass_phases
+    fn.argtypes = [C.c_void_p] * 4 + [C.c_int64, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p]
+    out = np.zeros(3)
+    fn(lo.h, loe.h, fli.h, _p(buf), n, loe_mask, fli_mask, threads, _p(out))
+    return {"keygen": float(out[0]), "lookup": float(out[1]), "insert": float(out[2])}
+
+
+def host_info() -> dict:
+    """CPU model, hardware threads and libc of this host (the CPU timing protocol's record)"""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        libc = os.confstr("CS_GNU_LIBC_VERSION")
+    except (ValueError, OSError):
+        libc = ""
+    return {"cpu_model": model, "hardware_concurrency": os.cpu_count(), "libc": libc}
+
+
 def synth_generate(width, height, bounces, seed=0x5EED, iteration=0, cam_shift_x=0.0,
                    threads=None):
     """Host generator (pstf_synth.h) -> contiguous buffer (34*n fp64 + n u32 as fp64 words)."""

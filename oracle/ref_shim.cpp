@@ -10,6 +10,7 @@
 // std::thread workers writing straight into the stores (non-deterministic mode) or into
 // per-worker FieldUpdateQueues merged and applied at the barrier (deterministic mode).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -393,6 +394,86 @@ void pr_vertex_pass(void *lo, void *loe, void *fli, void *li, const double *buf,
         qFli.apply(*static_cast<FieldStore *>(fli));
         if (li) qLi.apply(*static_cast<FieldStore *>(li));
     }
+}
+
+// The same replay timed by phase (SURVEY.md §8(d) CPU protocol, Appendix B probe 2): all
+// workers run keygen (selectLevel + keyFor of every key of their vertices), then the next-vertex
+// queries, then the counter/accumulate calls with the precomputed keys and values, with a join
+// between phases.  Queries read committed state only (field.h:73-75), so the phase order does
+// not change what they see.  ms_out = {keygen, lookup, insert} wall milliseconds.
+void pr_vertex_pass_phases(void *lo_, void *loe_, void *fli_, const double *buf, int64_t n,
+                           uint32_t loeMask, uint32_t fliMask, int threads, double *ms_out) {
+    FieldStore *lo = static_cast<FieldStore *>(lo_), *loe = static_cast<FieldStore *>(loe_),
+               *fli = static_cast<FieldStore *>(fli_);
+    const double *F[34];
+    for (int k = 0; k < 34; ++k) F[k] = buf + size_t(k) * size_t(n);
+    const uint32_t *flags = reinterpret_cast<const uint32_t *>(buf + size_t(34) * size_t(n));
+    if (threads < 1) threads = 1;
+    struct Keys {
+        SpatioDirectionalKey lo, loe, fc, fn;
+    };
+    std::vector<Keys> keys(static_cast<size_t>(n));
+    std::vector<RGB> loNext(static_cast<size_t>(n)), loeNext(static_cast<size_t>(n));
+    auto run = [&](auto &&body) {
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                for (int64_t i = int64_t(t); i < n; i += threads) body(size_t(i));
+            });
+        for (auto &th : pool) th.join();
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+            .count();
+    };
+    auto v3 = [&](int k, size_t i) { return Vec3(F[k][i], F[k + 1][i], F[k + 2][i]); };
+    auto rgb = [&](int k, size_t i) { return RGB(F[k][i], F[k + 1][i], F[k + 2][i]); };
+    ms_out[0] = run([&](size_t i) { // keygen (estimators.cpp:205, 218, 226, 242, 248)
+        const int level = lo->selectLevel(F[15][i]);
+        Keys &k = keys[i];
+        k.lo = lo->keyFor(v3(0, i), v3(3, i), level);
+        k.loe = loe->keyFor(v3(0, i), v3(3, i), level);
+        if (flags[i] & 1u) k.fc = fli->keyFor(v3(0, i), v3(6, i), level);
+        if (flags[i] & 4u) k.fn = fli->keyFor(v3(0, i), v3(12, i), level);
+    });
+    ms_out[1] = run([&](size_t i) { // next-vertex lookups (estimators.cpp:207-216)
+        RGB a(0.0), b(0.0);
+        if ((flags[i] & 1u) && (flags[i] & 2u)) {
+            const Vec3 woNext = -v3(6, i);
+            auto qa = lo->query(v3(9, i), woNext, F[16][i]);
+            if (qa.valid) a = qa.value;
+            auto qb = loe->query(v3(9, i), woNext, F[16][i]);
+            if (qb.valid) b = qb.value;
+        } else if (flags[i] & 1u) {
+            a = rgb(25, i);
+        }
+        loNext[i] = a;
+        loeNext[i] = b;
+    });
+    ms_out[2] = run([&](size_t i) { // inserts (estimators.cpp:218-254)
+        const Keys &k = keys[i];
+        const bool cont = flags[i] & 1u, nee = flags[i] & 4u;
+        const double ratio = F[17][i], emis = F[18][i];
+        const RGB f = rgb(22, i), nextEmission = rgb(25, i);
+        lo->incrementCounter(k.lo, 1.0);
+        lo->accumulate(k.lo, rgb(19, i), 1.0);
+        if (cont && ratio > 0.0)
+            lo->accumulate(k.lo, computeUpdateValue(FieldKind::Lo, loNext[i], RGB(0.0), f, ratio),
+                           1.0);
+        loe->incrementCounter(k.loe, 1.0);
+        if (cont && ratio > 0.0 && (loeMask & TechContinuation))
+            loe->accumulate(k.loe, computeUpdateValue(FieldKind::LoMinusE, loeNext[i],
+                                                      nextEmission * emis, f, ratio), 1.0);
+        if (nee && (loeMask & TechNee)) loe->accumulate(k.loe, rgb(28, i), 1.0);
+        const RGB lIncoming = nextEmission * emis + loeNext[i];
+        if (cont) {
+            fli->incrementCounter(k.fc, 1.0);
+            if (fliMask & TechContinuation) fli->accumulate(k.fc, f * lIncoming, 1.0);
+        }
+        if (nee) {
+            fli->incrementCounter(k.fn, 1.0);
+            if (fliMask & TechNee) fli->accumulate(k.fn, rgb(31, i), 1.0);
+        }
+    });
 }
 
 int pr_hardware_concurrency() { return int(std::thread::hardware_concurrency()); }
