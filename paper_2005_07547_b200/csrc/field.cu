@@ -169,6 +169,7 @@ struct Scratch {
     DBuf ddtab, rep_of, uidx, ukw, nudev;   // sort-free ATOMIC phase 2
     DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
     DBuf snap;                              // snapshot gather
+    DBuf fterms, fisc;                      // ORDERED/SEQUENTIAL fold terms in fold order
     DBuf winner;                            // snapshot restore: last record per slot
     DBuf hio;                               // host-pointer API staging
     unsigned long long *h_small = nullptr;  // pinned readback
@@ -1876,7 +1877,24 @@ __global__ void k_fold_targets(const uint32_t *perm, const uint32_t *uid, uint64
 }
 
 /* one thread per run of equal targets: sequential fold in the sorted order (field.cpp:413-418) */
-__global__ void k_fold(const PendRec *pend, const uint64_t *tgt, const uint32_t *recs, uint64_t n,
+/* the fold's terms in final (slot, canonical) order, computed in parallel: value.c * w of an
+ * accumulate (field.cpp:168-170), w of a counter (field.cpp:157); contiguous, so the
+ * sequential per-slot fold below streams instead of gathering 64 B records */
+__global__ void k_fold_terms(const PendRec *pend, const uint32_t *recs, uint64_t n, double4 *T,
+                             uint8_t *isc) {
+    uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const PendRec r = pend[recs[q]];
+    const double w = r.v[3];
+    const bool c = PSTF_META_ISC(r.meta) != 0;
+    T[q] = c ? make_double4(0.0, 0.0, 0.0, w)
+             : make_double4(r.v[0] * w, r.v[1] * w, r.v[2] * w, 0.0);
+    isc[q] = c;
+}
+
+/* sequential fold per target slot in canonical order (FieldUpdateQueue::apply, field.cpp:
+ * 396-420): one thread per run of equal targets */
+__global__ void k_fold(const double4 *T, const uint8_t *isc, const uint64_t *tgt, uint64_t n,
                        Stores4 st) {
     uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -1887,14 +1905,13 @@ __global__ void k_fold(const PendRec *pend, const uint64_t *tgt, const uint32_t 
     uint32_t slot = (uint32_t)t;
     double4 acc = s.acc[slot];
     for (uint64_t q = p; q < n && tgt[q] == t; ++q) {
-        PendRec r = pend[recs[q]];
-        double w = r.v[3];
-        if (PSTF_META_ISC(r.meta)) {
-            if (w > 0.0) acc.w += w; /* field.cpp:157 */
+        const double4 v = T[q];
+        if (isc[q]) {
+            if (v.w > 0.0) acc.w += v.w; /* field.cpp:157 */
         } else {
-            acc.x += r.v[0] * w; /* field.cpp:168-170 */
-            acc.y += r.v[1] * w;
-            acc.z += r.v[2] * w;
+            acc.x += v.x; /* field.cpp:168-170 */
+            acc.y += v.y;
+            acc.z += v.z;
         }
     }
     s.acc[slot] = acc;
@@ -2767,8 +2784,12 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
                                            sc.fkey_out.as<uint64_t>(), sc.fperm.as<uint32_t>(),
                                            sc.fperm_out.as<uint32_t>(), (int64_t)n, 0, 64, st));
         g_launches.fetch_add(4, std::memory_order_relaxed); }
-        LAUNCH(k_fold, grid_for(n, 256), 256, 0, st, pend, sc.fkey_out.as<uint64_t>(),
-               sc.fperm_out.as<uint32_t>(), n, S);
+        ENSURE(sc.fterms, n * sizeof(double4));
+        ENSURE(sc.fisc, n);
+        LAUNCH(k_fold_terms, grid_for(n, 256), 256, 0, st, pend, sc.fperm_out.as<uint32_t>(), n,
+               sc.fterms.as<double4>(), sc.fisc.as<uint8_t>());
+        LAUNCH(k_fold, grid_for(n, 256), 256, 0, st, sc.fterms.as<double4>(), sc.fisc.as<uint8_t>(),
+               sc.fkey_out.as<uint64_t>(), n, S);
     }
     return PSTF_OK;
 }
