@@ -169,7 +169,7 @@ struct Scratch {
     DBuf ddtab, rep_of, uidx, ukw, nudev;   // sort-free ATOMIC phase 2
     DBuf ftgt, fperm, fkey_out, fperm_out;  // ORDERED / SEQUENTIAL fold
     DBuf snap;                              // snapshot gather
-    DBuf fterms, fisc;                      // ORDERED/SEQUENTIAL fold terms in fold order
+    DBuf fterms, fisc, fstart, fnruns;      // ORDERED/SEQUENTIAL fold: terms, run starts
     DBuf winner;                            // snapshot restore: last record per slot
     DBuf hio;                               // host-pointer API staging
     unsigned long long *h_small = nullptr;  // pinned readback
@@ -1892,30 +1892,112 @@ __global__ void k_fold_terms(const PendRec *pend, const uint32_t *recs, uint64_t
     isc[q] = c;
 }
 
-/* sequential fold per target slot in canonical order (FieldUpdateQueue::apply, field.cpp:
- * 396-420): one thread per run of equal targets */
-__global__ void k_fold(const double4 *T, const uint8_t *isc, const uint64_t *tgt, uint64_t n,
-                       Stores4 st) {
+/* run starts of the target-sorted terms: head flags, then (after a scan) their positions */
+__global__ void k_fold_heads(const uint64_t *tgt, uint64_t n, uint32_t *head) {
     uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    uint64_t t = tgt[p];
-    if (t == ~0ull) return;
-    if (p > 0 && tgt[p - 1] == t) return;
-    const DevStore &s = st.s[t >> 32];
-    uint32_t slot = (uint32_t)t;
-    double4 acc = s.acc[slot];
-    for (uint64_t q = p; q < n && tgt[q] == t; ++q) {
-        const double4 v = T[q];
-        if (isc[q]) {
-            if (v.w > 0.0) acc.w += v.w; /* field.cpp:157 */
-        } else {
-            acc.x += v.x; /* field.cpp:168-170 */
-            acc.y += v.y;
-            acc.z += v.z;
-        }
+    if (p < n) head[p] = p == 0 || tgt[p] != tgt[p - 1];
+}
+
+__global__ void k_fold_starts(const uint32_t *head, const uint32_t *run, uint64_t n,
+                              uint32_t *start) {
+    uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (p < n && head[p]) start[run[p]] = (uint32_t)p;
+    if (p == n - 1) start[run[p] + head[p]] = (uint32_t)n; /* sentinel: end of the last run */
+}
+
+__global__ void k_fold_nruns(const uint32_t *head, const uint32_t *run, uint64_t n, uint32_t *nr) {
+    nr[0] = run[n - 1] + head[n - 1];
+}
+
+/* sequential fold per target slot in canonical order (FieldUpdateQueue::apply, field.cpp:
+ * 396-420), one thread per run.  The run's bounds are known, so the term loads are issued 8
+ * at a time ahead of the dependent fp64 adds (the hottest slots take tens of thousands of
+ * calls: their chains would otherwise wait on a load per call). */
+__device__ __forceinline__ void fold_one(double4 &acc, const double4 v, bool c) {
+    if (c) {
+        if (v.w > 0.0) acc.w += v.w; /* field.cpp:157 */
+    } else {
+        acc.x += v.x; /* field.cpp:168-170 */
+        acc.y += v.y;
+        acc.z += v.z;
     }
+}
+
+#define FOLD_LONG 256 /* runs at least this long are folded by a warp (k_fold_long) */
+
+__global__ void k_fold(const double4 *__restrict__ T, const uint8_t *__restrict__ isc,
+                       const uint64_t *tgt, const uint32_t *start, const uint32_t *nruns,
+                       Stores4 st) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= *nruns) return;
+    const uint32_t q0 = start[r], q1 = start[r + 1];
+    if (q1 - q0 >= FOLD_LONG) return;
+    const uint64_t t = tgt[q0];
+    if (t == ~0ull) return;
+    const DevStore &s = st.s[t >> 32];
+    const uint32_t slot = (uint32_t)t;
+    double4 acc = s.acc[slot];
+    uint32_t q = q0;
+    for (; q + 8 <= q1; q += 8) {
+        double4 v[8];
+        bool c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = T[q + k];
+            c[k] = isc[q + k] != 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fold_one(acc, v[k], c[k]);
+    }
+    for (; q < q1; ++q) fold_one(acc, T[q], isc[q] != 0);
     s.acc[slot] = acc;
 }
+
+/* the long runs, one warp each: lanes load 32 consecutive terms (one memory latency per 32
+ * calls instead of per call, the next 32 prefetched), every lane applies them in order from
+ * broadcasts, so each lane carries the same sequential sum */
+__global__ void k_fold_long(const double4 *__restrict__ T, const uint8_t *__restrict__ isc,
+                            const uint64_t *tgt, const uint32_t *start, const uint32_t *nruns,
+                            Stores4 st) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nr = *nruns;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < nr;
+         r += nwarps) {
+        const uint32_t q0 = start[r], q1 = start[r + 1];
+        if (q1 - q0 < FOLD_LONG) continue; /* warp-uniform */
+        const uint64_t t = tgt[q0];
+        if (t == ~0ull) continue;
+        const DevStore &s = st.s[t >> 32];
+        const uint32_t slot = (uint32_t)t;
+        double4 acc = s.acc[slot];
+        double4 nv = q0 + lane < q1 ? T[q0 + lane] : make_double4(0.0, 0.0, 0.0, 0.0);
+        int nc = q0 + lane < q1 ? isc[q0 + lane] : 0;
+        for (uint32_t b = q0; b < q1; b += 32) {
+            const double4 v = nv;
+            const int c = nc;
+            const uint32_t nb = b + 32; /* prefetch the next 32 */
+            if (nb + lane < q1) {
+                nv = T[nb + lane];
+                nc = isc[nb + lane];
+            }
+            const int k = (int)min(32u, q1 - b);
+            /* fully unrolled: the broadcasts do not depend on acc, so they run ahead of the
+             * dependent adds */
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                const double4 u = make_double4(__shfl_sync(0xffffffffu, v.x, l),
+                                               __shfl_sync(0xffffffffu, v.y, l),
+                                               __shfl_sync(0xffffffffu, v.z, l),
+                                               __shfl_sync(0xffffffffu, v.w, l));
+                const int cu = __shfl_sync(0xffffffffu, c, l);
+                if (l < k) fold_one(acc, u, cu != 0);
+            }
+        }
+        if (lane == 0) s.acc[slot] = acc;
+    }
+}
+
 
 /* ------------------------------------------------------------------------------------------ */
 /* K3: endFrame (field.cpp:197-263), all stores of a batch in one launch per pass            */
@@ -2788,8 +2870,32 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
         ENSURE(sc.fisc, n);
         LAUNCH(k_fold_terms, grid_for(n, 256), 256, 0, st, pend, sc.fperm_out.as<uint32_t>(), n,
                sc.fterms.as<double4>(), sc.fisc.as<uint8_t>());
+        /* runs of equal targets: heads -> scan -> start positions (+ sentinel) */
+        ENSURE(sc.head, n * 4);
+        ENSURE(sc.uid, n * 4);
+        ENSURE(sc.fstart, (n + 1) * 4);
+        const uint64_t *ftgt = sc.fkey_out.as<uint64_t>();
+        LAUNCH(k_fold_heads, grid_for(n, 256), 256, 0, st, ftgt, n, sc.head.as<uint32_t>());
+        {
+            size_t bytes = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sc.head.as<uint32_t>(),
+                                             sc.uid.as<uint32_t>(), (int64_t)n, st));
+            ENSURE(sc.cub, bytes);
+            bytes = sc.cub.bytes;
+            ProfScope ps_("cub::DeviceScan", st);
+            CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, sc.head.as<uint32_t>(),
+                                             sc.uid.as<uint32_t>(), (int64_t)n, st));
+            g_launches.fetch_add(2, std::memory_order_relaxed);
+        }
+        LAUNCH(k_fold_starts, grid_for(n, 256), 256, 0, st, sc.head.as<uint32_t>(),
+               sc.uid.as<uint32_t>(), n, sc.fstart.as<uint32_t>());
+        ENSURE(sc.fnruns, 8);
+        LAUNCH(k_fold_nruns, 1, 1, 0, st, sc.head.as<uint32_t>(), sc.uid.as<uint32_t>(), n,
+               sc.fnruns.as<uint32_t>());
         LAUNCH(k_fold, grid_for(n, 256), 256, 0, st, sc.fterms.as<double4>(), sc.fisc.as<uint8_t>(),
-               sc.fkey_out.as<uint64_t>(), n, S);
+               ftgt, sc.fstart.as<uint32_t>(), sc.fnruns.as<uint32_t>(), S);
+        LAUNCH(k_fold_long, (unsigned)sm_count() * 8, 256, 0, st, sc.fterms.as<double4>(),
+               sc.fisc.as<uint8_t>(), ftgt, sc.fstart.as<uint32_t>(), sc.fnruns.as<uint32_t>(), S);
     }
     return PSTF_OK;
 }
