@@ -93,3 +93,28 @@ def test_sharded_protocol_matches_single_rank_semantics(tmp_path, world, cap, ev
         np.testing.assert_allclose(got[f"com{s}"][live, :3], sl["value_old"][live], rtol=1e-9)
         assert got["live"][s] == ref[s].stats()["live"]
         assert sum(rr["dropped"][s] for rr in res) == ref[s].stats()["dropped"]
+
+
+def _counted_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path[:0] = [os.path.join(HERE, "..")]
+    from paper_2005_07547_b200.shard import Collectives
+    c = Collectives(dist, "cpu")
+    n = 64 * (rank + 1) if rank != 1 else 0  # unequal sizes, one empty
+    payload = (torch.arange(n, dtype=torch.int64) % 251 + rank).to(torch.uint8)
+    got = c.all_gather_counted(torch.tensor([n], dtype=torch.int64), lambda m: payload[:m])
+    torch.save(got, os.path.join(outdir, f"g{rank}.pt"))
+    dist.destroy_process_group()
+
+
+def test_all_gather_counted_gloo(tmp_path):
+    """the device-count variable-length all-gather the CUDA path uses (one host sync per
+    exchange), here over gloo with CPU tensors: rank order, unequal and empty contributions"""
+    world = 3
+    mp.spawn(_counted_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    want = torch.cat([(torch.arange(64 * (r + 1) if r != 1 else 0, dtype=torch.int64) % 251 + r)
+                      .to(torch.uint8) for r in range(world)])
+    for r in range(world):
+        assert torch.equal(torch.load(os.path.join(tmp_path, f"g{r}.pt")), want)
