@@ -423,7 +423,26 @@ __device__ __forceinline__ void contribute_atomic(const DevStore &s, const PendS
     apply_contribution(s, a, sm, sid, k, v, ncalls, res, mark, do_red);
 }
 
-/* ORDERED mode: every call becomes a record. */
+/* ORDERED mode, counter calls of the vertex pass (weight 1.0, estimators.cpp:219,227,243,249):
+ * cNew only ever receives whole numbers, so its sum is exact in any order.  An existing key's
+ * counter is therefore applied in place (cNew += 1, lastTouched = frame: field.cpp:122-124,
+ * 157) and only a new key's counter becomes a record (its placement needs one); a full window
+ * counts the drop (field.cpp:145).  This halves the records the canonical sort has to order. */
+__device__ __forceinline__ void count_call(const DevStore &s, const PendSink &a, bool want,
+                                           int sid, const Key &k) {
+    int res = -3;
+    uint32_t mark = 0;
+    if (want) res = probe_existing(s, k.pack_lo & s.mask, k.checksum, &mark);
+    if (res >= 0) {
+        atomicAdd(&s.acc[res].w, 1.0);
+        touch_slot(s, (uint32_t)res, mark);
+    }
+    if (PendRec *p = warp_reserve(a, res == -1))
+        put_record(p, k, PSTF_META(sid, 1, 1) | ((uint32_t)s.rank << 3), 0.0, 0.0, 0.0, 1.0);
+    if (res == -2) atomicAdd(&s.ctr[C_DROPPED], 1ull);
+}
+
+/* ORDERED mode: every other call becomes a record. */
 __device__ __forceinline__ void emit_call(const PendSink &a, bool want, int sid, const Key &k,
                                           bool is_counter, double r_, double g_, double b_,
                                           double w) {
@@ -608,30 +627,30 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
         /* ORDERED: the reference's individual calls, in any order (the sort canonicalises) */
         const PendSink ps{a.pend, a.pend_count, a.pend_cap};
         unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
-        emit_call(ps, live, 0, kLo, true, 0.0, 0.0, 0.0, 1.0);
+        count_call(sLo, ps, live, 0, kLo);
         bool ok = finite3(ehx, ehy, ehz);
         rejLo += live && !ok;
         emit_call(ps, live && ok, 0, kLo, false, ehx, ehy, ehz, 1.0);
         ok = finite3(ulx, uly, ulz);
         rejLo += live && transp && !ok;
         emit_call(ps, live && transp && ok, 0, kLo, false, ulx, uly, ulz, 1.0);
-        emit_call(ps, live, 1, kLoe, true, 0.0, 0.0, 0.0, 1.0);
+        count_call(sLoe, ps, live, 1, kLoe);
         ok = finite3(uex, uey, uez);
         rejLoe += live && loeCont && !ok;
         emit_call(ps, live && loeCont && ok, 1, kLoe, false, uex, uey, uez, 1.0);
         ok = finite3(nlx, nly, nlz);
         rejLoe += live && loeNee && !ok;
         emit_call(ps, live && loeNee && ok, 1, kLoe, false, nlx, nly, nlz, 1.0);
-        emit_call(ps, live && cont, 2, kFc, true, 0.0, 0.0, 0.0, 1.0);
+        count_call(sFli, ps, live && cont, 2, kFc);
         ok = finite3(fcx, fcy, fcz);
         rejFli += live && fliCont && !ok;
         emit_call(ps, live && fliCont && ok, 2, kFc, false, fcx, fcy, fcz, 1.0);
-        emit_call(ps, live && nee, 2, kFn, true, 0.0, 0.0, 0.0, 1.0);
+        count_call(sFli, ps, live && nee, 2, kFn);
         ok = finite3(nfx, nfy, nfz);
         rejFli += live && fliNee && !ok;
         emit_call(ps, live && fliNee && ok, 2, kFn, false, nfx, nfy, nfz, 1.0);
         if (a.has_li) {
-            emit_call(ps, live && cont, 3, kLi, true, 0.0, 0.0, 0.0, 1.0);
+            count_call(sLi, ps, live && cont, 3, kLi);
             ok = finite3(lvx, lvy, lvz);
             rejLi += live && cont && !ok;
             emit_call(ps, live && cont && ok, 3, kLi, false, lvx, lvy, lvz, 1.0);
