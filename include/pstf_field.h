@@ -299,6 +299,10 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *records
                          void *stream);
 int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
                          uint64_t *counts_per_rank, void *stream);
+/* ... without a host round trip: the per-rank counts land in dev_counts[world] (device int64)
+ * for a device-side count exchange; cap must be at least the sum of the stores' capacities */
+int pstf_partials_export_async(pstf_field *const *stores, int nst, void *out, uint64_t cap,
+                               int64_t *dev_counts, void *stream);
 int pstf_partials_import(pstf_field *const *stores, int nst, const void *records, uint64_t n,
                          void *stream);
 int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_count, void *stream);

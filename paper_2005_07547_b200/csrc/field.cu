@@ -4235,6 +4235,81 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, u
     return resolve_pending(sc, stores, nst, PSTF_MODE_ATOMIC, n, st, stores[0]->d.rank);
 }
 
+/* per (store, rank) partial counts from the word scans' values at the rank boundaries, their
+ * destination-major offsets (rank, then store) and each rank's total: all on the device */
+__global__ void k_px_plan(const uint32_t *scan, const unsigned long long *soff, int nst,
+                          int world, const unsigned long long *wpr,
+                          unsigned long long *dest_base, long long *counts) {
+    if (threadIdx.x != 0) return;
+    unsigned long long base = 0;
+    for (int r = 0; r < world; ++r) {
+        unsigned long long tot = 0;
+        for (int j = 0; j < nst; ++j) {
+            const uint32_t *u = scan + soff[j];
+            const unsigned long long c = u[(uint64_t)(r + 1) * wpr[j]] - u[(uint64_t)r * wpr[j]];
+            dest_base[(size_t)j * world + r] = base + tot;
+            tot += c;
+        }
+        counts[r] = (long long)tot;
+        base += tot;
+    }
+}
+
+/* pstf_partials_export without any host round trip: per-rank record counts land in
+ * dev_counts[world] (device int64); cap must cover every touched non-owned slot (the sum of
+ * capacities is always enough) */
+int pstf_partials_export_async(pstf_field *const *stores, int nst, void *out, uint64_t cap,
+                               int64_t *dev_counts, void *stream) {
+    int rc = shard_checks(stores, nst);
+    if (rc) return rc;
+    if (!dev_counts || !out) return set_err(PSTF_E_INVALID, "NULL argument");
+    uint64_t total_cap = 0;
+    for (int j = 0; j < nst; ++j) total_cap += (uint64_t)stores[j]->d.mask + 1;
+    if (cap < total_cap) return set_err(PSTF_E_INVALID, "partials buffer smaller than the stores");
+    CK(cudaSetDevice(stores[0]->device));
+    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int world = stores[0]->world;
+    Scratch &sc = stores[0]->sc;
+    std::vector<uint64_t> nw(nst);
+    std::vector<unsigned long long> off(nst + 1, 0), wpr(nst);
+    for (int j = 0; j < nst; ++j) {
+        nw[j] = ((uint64_t)stores[j]->d.mask + 1) / 32;
+        off[j + 1] = off[j] + nw[j] + 1;
+        wpr[j] = nw[j] / (uint64_t)world;
+    }
+    ENSURE(sc.head, off[nst] * 4);
+    ENSURE(sc.uid, off[nst] * 4);
+    ENSURE(sc.ranges, ((size_t)nst * world + 2 * nst + 2) * 8);
+    unsigned long long *dest = sc.ranges.as<unsigned long long>();
+    unsigned long long *d_off = dest + (size_t)nst * world, *d_wpr = d_off + nst + 1;
+    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
+    unsigned long long *hp = sc.h_small + 128; /* pinned staging for the small plan inputs */
+    if ((size_t)(2 * nst + 1) + 128 > 512) return set_err(PSTF_E_INVALID, "too many stores");
+    for (int j = 0; j <= nst; ++j) hp[j] = off[j];
+    for (int j = 0; j < nst; ++j) hp[nst + 1 + j] = wpr[j];
+    CK(cudaMemcpyAsync(d_off, hp, (size_t)(2 * nst + 1) * 8, cudaMemcpyHostToDevice, st));
+    for (int j = 0; j < nst; ++j) {
+        DevStore s = dev_view(stores[j]);
+        uint32_t *h = sc.head.as<uint32_t>() + off[j], *u = sc.uid.as<uint32_t>() + off[j];
+        LAUNCH(k_px_count, grid_for(nw[j] + 1, 256), 256, 0, st, s, h, nw[j]);
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, h, u, (int64_t)(nw[j] + 1), st));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, h, u, (int64_t)(nw[j] + 1), st));
+    }
+    LAUNCH(k_px_plan, 1, 32, 0, st, sc.uid.as<uint32_t>(), d_off, nst, world, d_wpr, dest,
+           reinterpret_cast<long long *>(dev_counts));
+    for (int j = 0; j < nst; ++j) {
+        DevStore s = dev_view(stores[j]);
+        LAUNCH(k_px_write, grid_for(nw[j], 256), 256, 0, st, s, (uint32_t)j,
+               sc.uid.as<uint32_t>() + off[j], nw[j], wpr[j], dest + (size_t)j * world,
+               (PartialRec *)out);
+    }
+    return PSTF_OK;
+}
+
 int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
                          uint64_t *counts, void *stream) {
     int rc = shard_checks(stores, nst);

@@ -99,6 +99,19 @@ class Collectives:
                                     [c * rec_bytes for c in send_counts])
         return out, recv_counts
 
+    def all_to_all_counted(self, buf, send_counts_dev, rec_bytes):
+        """all_to_all_bytes with the send counts (records per destination) on the device: the
+        count exchange runs there too, and one host synchronisation reads both sides"""
+        import torch
+        rc = torch.empty_like(send_counts_dev)
+        self.dist.all_to_all_single(rc, send_counts_dev)
+        both = [int(x) for x in torch.cat([send_counts_dev, rc]).tolist()]
+        send, recv = both[:self.world], both[self.world:]
+        out = torch.empty(sum(recv) * rec_bytes, dtype=torch.uint8, device=self.device)
+        self.dist.all_to_all_single(out, buf[:sum(send) * rec_bytes],
+                                    [c * rec_bytes for c in recv], [c * rec_bytes for c in send])
+        return out, recv
+
     def all_reduce_sum(self, arr):
         """Sum over ranks: a device tensor is reduced in place (no host round trip), anything
         else goes through a float64 device tensor and comes back as numpy."""
@@ -120,15 +133,20 @@ class ShardedFieldCache:
 
     def iteration(self, stripe):
         b, c = self.b, self.c
-        counted = hasattr(b, "pending_count_dev") and hasattr(c, "all_gather_counted")
+        counted = hasattr(b, "pending_count_dev") and hasattr(c, "all_gather_counted") and \
+            hasattr(c, "all_to_all_counted")
         b.vertex_pass_local(stripe)                                    # 1
         if counted:  # device-side sizes: one host sync per variable-size exchange
             recs = c.all_gather_counted(b.pending_count_dev(), b.pending_bytes_n)
         else:
             recs = c.all_gather_bytes(b.pending_bytes())               # 2
         b.resolve(recs)
-        out, counts = b.partials_export()                              # 3
-        recv, _ = c.all_to_all_bytes(out, counts, PARTIAL_BYTES)
+        if counted:                                                    # 3
+            out, counts_dev = b.partials_export_async()
+            recv, _ = c.all_to_all_counted(out, counts_dev, PARTIAL_BYTES)
+        else:
+            out, counts = b.partials_export()
+            recv, _ = c.all_to_all_bytes(out, counts, PARTIAL_BYTES)
         b.partials_import(recv)
         sums = c.all_reduce_sum(b.end_frame_reduce())                  # 4
         if counted:                                                    # 5
@@ -175,6 +193,7 @@ class CudaBackend:
             "pstf_end_frame_commit_dev": [vp, i32, vp, vp, u64, vp, vp],
             "pstf_end_frame_commit_async": [vp, i32, vp, vp, u64, vp, vp],
             "pstf_pending_count_dev": [vp, vp, vp],
+            "pstf_partials_export_async": [vp, i32, vp, u64, vp, vp],
             "pstf_deltas_import": [vp, i32, vp, u64, vp], "pstf_shard_set": [vp, i32, i32],
         }.items():
             fn = getattr(L, name)
@@ -250,6 +269,19 @@ class CudaBackend:
                                                   C.c_void_p(out.data_ptr()), cap, counts,
                                                   self.F._stream()))
         return out, [int(x) for x in counts]
+
+    def partials_export_async(self):
+        """partial records (destination-major) and the per-rank counts as a device int64
+        tensor, no host round trip"""
+        torch = self._torch()
+        cap = sum(s.capacity for s in self.stores)
+        out = torch.empty(cap * PARTIAL_BYTES, dtype=torch.uint8, device="cuda")
+        counts = torch.empty(self.world, dtype=torch.int64, device="cuda")
+        self.F._check(self.L.pstf_partials_export_async(self._arr, len(self.stores),
+                                                        C.c_void_p(out.data_ptr()), cap,
+                                                        C.c_void_p(counts.data_ptr()),
+                                                        self.F._stream()))
+        return out, counts
 
     def partials_import(self, recs):
         n = recs.numel() // PARTIAL_BYTES

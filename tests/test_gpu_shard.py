@@ -30,7 +30,8 @@ def _stores(cap, base, evict):
                                                           (4, 14, 1.0, 64, True)])
 def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict, counted):
     """counted: the exchanges whose sizes stay on the device (pstf_pending_count_dev,
-    pstf_end_frame_commit_async), as ShardedFieldCache uses them over NCCL"""
+    pstf_partials_export_async, pstf_end_frame_commit_async), as ShardedFieldCache uses them
+    over NCCL"""
     W, H, B, frames = 96, 54, 4, 4
     base = inputs.BASE_CORNELL * mult
     single = _stores(cap, base, evict)
@@ -55,7 +56,13 @@ def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict, counted):
         for be in bes:
             be.resolve(allrec)
         # 3: partials to owners (all-to-all)
-        outs = [be.partials_export() for be in bes]
+        if counted:
+            outs = []
+            for be in bes:
+                buf_s, cnt = be.partials_export_async()
+                outs.append((buf_s, [int(x) for x in cnt.tolist()]))
+        else:
+            outs = [be.partials_export() for be in bes]
         for r, be in enumerate(bes):
             parts = []
             for src, (buf_s, counts) in enumerate(outs):
