@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--force-sharded", action="store_true",
+                   help="testing: run the key-owner-sharded iteration (NCCL) even at world 1")
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                    help="BASELINE.json config: 2 = 1080p x4 (default, the metric's workload); "
                         "3 = + CV lookup at every vertex; 4 = 4K x6 at 2^24 slots; 5 = drifting "
@@ -255,8 +257,13 @@ def run_b200(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
+        if world == 1:  # a one-rank NCCL group exercises the multi-GPU code path on one GPU
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     W, H, B = args.width, args.height, args.bounces
     base = DIAMETER / 256.0
@@ -396,7 +403,7 @@ def run_b200(args):
             "mode": args.mode, "iteration_streams": S,
             "l2": "inputs larger than L2 (%.2f GB per iteration stream vs %d MB L2 read from the "
                   "device, %d streams cycled)" % (BYTES_PER_VERTEX * n / 1e9, l2_bytes >> 20, S),
-            "parallelism": "single GPU" if world == 1 else
+            "parallelism": "single GPU" if sharded is None else
                            f"{world} ranks, 1 spp of the 1080p frame each (weak scaling), one "
                            f"field cache sharded by key owner (NCCL all-gather / all-to-all)",
         },

@@ -51,3 +51,12 @@ def test_reference_arm_line():
         return
     assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"]
+
+
+def test_sharded_branch_on_one_rank():
+    """the multi-GPU branch (NCCL group, key-owner-sharded iteration with device-side exchange
+    sizes, sharded e2e) run as a one-rank group: it must complete and print a valid line"""
+    d = _line(SMALL + ["--force-sharded", "--no-cpu-baseline", "--e2e-steps", "2"])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "sharded by key owner" in d["config"]["parallelism"]
+
