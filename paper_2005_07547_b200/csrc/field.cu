@@ -4232,6 +4232,10 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, u
     rc = ensure_pending(sc, std::max<uint64_t>(n, 1), false, st);
     if (rc) return rc;
     if (n) CK(cudaMemcpyAsync(sc.pend.p, recs, n * sizeof(PendRec), cudaMemcpyDeviceToDevice, st));
+    /* the device count too: phase 2's key-range pass reads it (an empty range would force the
+     * multi-word sort path instead of the sort-free one) */
+    const unsigned long long cnt = n; /* pageable: staged before cudaMemcpyAsync returns */
+    CK(cudaMemcpyAsync(sc.pend_count.p, &cnt, 8, cudaMemcpyHostToDevice, st));
     return resolve_pending(sc, stores, nst, PSTF_MODE_ATOMIC, n, st, stores[0]->d.rank);
 }
 
