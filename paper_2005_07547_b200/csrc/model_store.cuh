@@ -1,23 +1,29 @@
-/* CV-profile / guiding model store on the device (SURVEY.md §8f row 2).
+/* CV-profile / guiding model store on the device (SURVEY.md §8f rows 2 and 4).
  *
- * ModelStore (estimators.h:124-150, estimators.cpp:104-144) holding DirGrid models
- * (models.h:30-52, models.cpp:16-94).  Included at the end of field.cu (one translation unit:
- * it shares the scratch buffers, the multi-word radix sort and the exact key functions).
+ * ModelStore (estimators.h:124-150, estimators.cpp:104-144) holding DirGrid (models.h:30-52,
+ * models.cpp:16-94), SphericalKdTree (models.h:59-109, models.cpp:96-298) or Gmm models
+ * (models.h:113-177, models.cpp:427-702).  Included at the end of field.cu (one translation
+ * unit: it shares the scratch buffers, the multi-word radix sort and the exact key functions).
  *
  * Layout (per entry e of a 2^k open-addressing table, home = packKeyFields(key) & mask):
  *   state[e]   u32   0 empty, 1 being written, 2 ready (entries are never removed, as in the
  *                    reference's unordered_map)
  *   keyf[e]    6 x i32 key fields (equality ignores the checksum, field.h:38-41)
  *   ent[e]     {total, cOld, cNew, records, recordCount, warm, touched}
- *   w[e][R^2], acc[e][R^2]  f64 DirGrid weights / accumulators, row-major (iy * R + ix)
+ *   w[e][ns], acc[e][ns]  f64: DirGrid weights / accumulators (row-major, ns = R^2); k-d tree
+ *                    node prob / accum (ns = 2L-1, topology in kn[e][ns]); Gmm state vector
+ *   entry 2^k        the template a new k-d tree / Gmm entry is copied from
  *
  * apply:  every record finds (or inserts, CAS on state) its key's entry; the records are then
- *         radix-sorted by (entry, grid cell, uv.x, uv.y, contribution), which within one key
- *         is the canonical order of estimators.cpp:633-637, and one thread per (entry, cell)
- *         run folds it in a register: each accumulator sum has the reference's order.  No host
- *         round trip.
+ *         radix-sorted by (entry, slot, uv.x, uv.y, contribution) (slot = grid cell or tree
+ *         leaf, 0 for Gmm), which within one key is the canonical order of
+ *         estimators.cpp:633-637; one thread per (entry, slot) run folds it in a register, so
+ *         each accumulator sum has the reference's order (Gmm: the samples are appended in that
+ *         order instead).  ATOMIC: no sort, fp64 atomics.  No host round trip.
  * endFrame: the touched entries only (a list built by apply): Σ cNew (integer-valued, exact in
- *         any order), then one warp per entry blends its grid, the grid sums in index order. */
+ *         any order), then per entry: one warp blends a grid (sums in index order); one warp
+ *         runs a staged k-d tree update; Gmm runs a chunked, sample-parallel E-step, then the
+ *         M-step per entry. */
 
 struct ModelEnt {
     double total, c_old, c_new;
