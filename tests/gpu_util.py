@@ -27,3 +27,27 @@ def assert_slots_close(gpu_slots, ref_slots, rtol=1e-9, atol=0.0):
     np.testing.assert_array_equal(gpu_slots["c_old"][live], ref_slots["c_old"][live])
     for f in ("value_old",):
         np.testing.assert_allclose(gpu_slots[f][live], ref_slots[f][live], rtol=rtol, atol=atol)
+
+
+def device_stream(buf, n, pad=True):
+    """Upload a contiguous host SoA buffer (34 fp64 fields of n, then u32 flags).  pad=True lays
+    the fields at an even stride (16 B aligned: the fused kernel's TMA tile path); pad=False
+    keeps stride n (odd n: unaligned fields, the per-thread kernel).  -> (device tensor, soa)"""
+    import torch
+    import crafted
+    import paper_2005_07547_b200 as pb
+    if pad:
+        host, m = crafted.pad_even(buf, n)
+    else:
+        host, m = buf, n
+    dev = torch.from_numpy(host).cuda()
+    base = dev.data_ptr()
+    fields = [base + k * m * 8 for k in range(34)]
+    soa = pb.vertex_soa_from_fields(fields, base + 34 * m * 8)
+    return dev, soa
+
+
+def launched(prefix):
+    """names of profiled launches that start with prefix (pb.profile_enable must be on)"""
+    import paper_2005_07547_b200 as pb
+    return [k for k in pb.profile_collect() if prefix in k]

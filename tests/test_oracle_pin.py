@@ -327,3 +327,30 @@ def test_gmm_model_store_matches_reference(comps, alpha, skew):
         np.testing.assert_array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
     assert fo.sum() > 50
 
+
+
+@pytest.mark.parametrize("extreme", [False, True])
+def test_crafted_stream_oracle_vs_reference(extreme):
+    """the adversarial streams of tests/crafted.py (escapes, NaN/inf values, ratio <= 0,
+    boundary-hugging keys) replayed through the C restatement and the reference: bitwise"""
+    import crafted
+    if not po.ref_available():
+        pytest.skip("oracle/_ref not built")
+    base = (12.0 ** 0.5) / 256.0
+    kinds = (po.KIND_LO, po.KIND_LOE, po.KIND_FLI, po.KIND_LI)
+    ref = [po.RefStore(po.Config.make(kind=k, capacity_log2=13, base_cell_size=base)) for k in kinds]
+    orc = [po.OracleStore(po.Config.make(kind=k, capacity_log2=13, base_cell_size=base)) for k in kinds]
+    for f in range(4):
+        buf, n = po.synth_generate(40, 30, 4, iteration=f)
+        crafted.mutate(buf, n, seed=77 + f, base=base, extreme=extreme)
+        masks = (1 + f % 7, 1 + (2 * f + 3) % 7)
+        po.vertex_pass_ref(ref[0], ref[1], ref[2], ref[3], buf, n, masks[0], masks[1],
+                           deterministic=True)
+        po.vertex_pass_oracle(orc[0], orc[1], orc[2], orc[3], buf, n, masks[0], masks[1],
+                              deterministic=True)
+        for s in ref + orc:
+            s.end_frame()
+        for a, b in zip(ref, orc):
+            assert a.slots().tobytes() == b.slots().tobytes(), f
+            assert a.stats() == b.stats()
+    assert sum(s.stats()["rejected"] for s in ref) > 0
