@@ -514,11 +514,13 @@ PSTF_HD int32_t cell_try(double q, double pcoord, int level, int *nx) {
     const double ax = fabs(x);
     const double fl = floor(x);
     const double e = ax * 0x1p-50;
-    const bool ok = ax < 2147483647.0 && (ax >= 0x1p-900 || ax == 0.0) && x - fl >= e &&
-                    (fl + 1.0) - x >= e; /* fl in [-2^31 + 1, 2^31 - 2]: exact conversion */
+    /* non-short-circuit & and |: no branches, so the three coordinates of a position (and
+     * the surrounding work) interleave */
+    const bool ok = (ax < 2147483647.0) & ((ax >= 0x1p-900) | (ax == 0.0)) & (x - fl >= e) &
+                    ((fl + 1.0) - x >= e); /* fl in [-2^31 + 1, 2^31 - 2]: exact conversion */
     /* far outside int32 (finite): the reference's conversion gives INT32_MIN */
-    const bool far = ax >= 4294967296.0 && ax <= 1.7976931348623157e308;
-    *nx |= !(ok || far);
+    const bool far = (ax >= 4294967296.0) & (ax <= 1.7976931348623157e308);
+    *nx |= !(ok | far);
     return ok ? (int32_t)fl : INT32_MIN;
 }
 
@@ -638,26 +640,31 @@ PSTF_HD int32_t f8_of32(float U, int *near) {
  * inputs are outside the fast path's domain (the caller then recomputes with octa_f8_exact).
  * Error budget (|.| in U units): w = 1 - |z| is formed in double precision and rounded once
  * (6e-8 relative), r = sqrt_fast(w) within 1.5 ulp, phi from a degree-4 minimax polynomial in t^2
- * after an octant reduction with a correctly rounded reciprocal (|error| < 3e-7), then four
- * rounded products/sums: |U' - U| < 1e-6, so q' = 8 U' is within 8e-6 of q, well inside the
- * 2e-5 margin.  NaN, infinite and denormal-scale x, y always take the exact path. */
+ * (|error| < 3e-7) after an octant reduction with the hardware reciprocal estimate (t within
+ * 3e-7 relative), then four rounded products/sums: |U' - U| < 1.5e-6, so q' = 8 U' is within
+ * 1.2e-5 of q, inside the 2e-5 margin.  NaN, infinite and denormal-scale x, y (either one)
+ * always take the exact path. */
 PSTF_HD void octa_f8_try(double dx, double dy, double dz, int want_neg, DirF8 *pos, DirF8 *neg,
                          int *nx) {
     const double x = fabs(dx), y = fabs(dy), z = fabs(dz);
-    const double omz = 1.0 - z;
-    const float wf = (float)((0.0 < omz) ? omz : 0.0); /* safeSqrt (vecmath.h:22) */
+    /* safeSqrt(1 - |z|) (vecmath.h:22): the difference in double precision (exact for |z| in
+     * [0.5, 1]), rounded once; NaN and negative -> 0 like std::max(0.0, .) */
+    const float wf = fmaxf((float)(1.0 - z), 0.0f);
     const float r = sqrt_fast(wf);
     float phi = 0.0f;
     if (!(x == 0.0 && y == 0.0)) {
-        const double mx = x > y ? x : y;
-        *nx |= !(mx >= 1e-30 && mx <= 1e30); /* also NaN */
         const float xf = (float)x, yf = (float)y;
+        /* fast-path domain: x and y finite (a NaN fails the comparisons) and the larger one in
+         * [1e-30, 1e30] */
+        *nx |= !(xf <= 1e30f && yf <= 1e30f && (xf >= 1e-30f || yf >= 1e-30f));
         const bool swap = yf > xf;
         const float a = swap ? xf : yf, b = swap ? yf : xf; /* 0 <= a <= b */
         const bool small = a <= b * 0.41421356f;
         const float num = small ? a : a - b, den = small ? b : a + b;
 #if defined(__CUDA_ARCH__)
-        const float t = num * __frcp_rn(den);
+        float rc; /* hardware reciprocal estimate, relative error < 2^-22 (den is a normal) */
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));
+        const float t = num * rc;
 #else
         const float t = num * (1.0f / den);
 #endif

@@ -50,6 +50,7 @@ def _boundary_positions(rng, m, base, max_level):
 
 def _pick_dirs(rng, m):
     pool = np.concatenate([inputs.structured_dirs(), inputs.special_dirs(),
+                           inputs.special_dirs_extra(), inputs.special_dirs_extra(),
                            inputs.boundary_dirs(rng, 256), inputs.random_dirs(rng, 64),
                            -inputs.boundary_dirs(rng, 64)])
     return pool[rng.integers(0, len(pool), size=m)]

@@ -46,6 +46,15 @@ def special_dirs():
                     dtype=np.float64)
 
 
+def special_dirs_extra():
+    """one non-finite component next to finite in-range ones (x NaN with y finite, ...): the
+    fast octahedral path must hand them to the exact one (not in the golden fixtures)"""
+    nan, inf = float("nan"), float("inf")
+    return np.array([(nan, 0.5, 0.5), (nan, -0.6, -0.8), (0.6, nan, 0.8), (-0.6, nan, -0.8),
+                     (0.3, 0.4, nan), (-inf, 0.5, 0.5), (0.5, -inf, 0.5), (1e-40, 0.6, 0.8),
+                     (0.6, 1e-320, -0.8), (1e35, 1.0, 0.0), (nan, nan, 0.5)], dtype=np.float64)
+
+
 def random_dirs(rng, n):
     v = rng.normal(size=(n, 3))
     v /= np.linalg.norm(v, axis=1, keepdims=True)

@@ -42,7 +42,8 @@ def test_keys_device_bitwise(base):
     g = pb.FieldStore(_pcfg(cfg))
     rng = np.random.default_rng(11)
     d = np.concatenate([inputs.random_dirs(rng, 300000), inputs.boundary_dirs(rng, 200000),
-                        inputs.structured_dirs(), inputs.special_dirs()])
+                        inputs.structured_dirs(), inputs.special_dirs(),
+                        inputs.special_dirs_extra()])
     n = len(d)
     pos = np.concatenate([inputs.random_positions(rng, n - 8), inputs.special_positions()])
     for level in range(cfg.max_level + 1):

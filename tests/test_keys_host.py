@@ -58,7 +58,8 @@ def test_keys_match_reference(kh, base):
     ref = _checker(cfg)
     rng = np.random.default_rng(int(base * 1e6))
     d = np.concatenate([inputs.random_dirs(rng, 100000), inputs.boundary_dirs(rng, 100000),
-                        inputs.structured_dirs(), inputs.special_dirs()])
+                        inputs.structured_dirs(), inputs.special_dirs(),
+                        inputs.special_dirs_extra()])
     n = len(d)
     pos = np.concatenate([inputs.random_positions(rng, n - 8), inputs.special_positions()])
     for level in range(cfg.max_level + 1):
@@ -102,7 +103,8 @@ def test_shared_quantisation_identities(kh, negate, base):
     ref = _checker(cfg)
     rng = np.random.default_rng(77 + negate)
     d = np.concatenate([inputs.random_dirs(rng, 40000), inputs.boundary_dirs(rng, 40000),
-                        inputs.structured_dirs(), inputs.special_dirs()])
+                        inputs.structured_dirs(), inputs.special_dirs(),
+                        inputs.special_dirs_extra()])
     n = len(d)
     pos = np.concatenate([inputs.random_positions(rng, n - 8), inputs.special_positions()])
     pos[:200] *= 1e-310  # subnormal positions exercise the direct-division fallback
