@@ -34,6 +34,7 @@ METRIC = "filtered path vertices/sec (insert+blend+lookup) 1080p×4 bounces; % H
 UNIT = "vertices/s"
 BYTES_PER_VERTEX = 276
 BYTES_PER_TOUCHED = 172
+DATA = "synthetic (pstf_synth.h Cornell-box generator, IEEE-exact, seed 0x5EED)"
 DIAMETER = math.sqrt(12.0)
 
 
@@ -54,17 +55,53 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--force-sharded", action="store_true",
-                   help="testing: run the key-owner-sharded iteration (NCCL) even at world 1")
+                   help="testing: run the multi-GPU iteration (NCCL) even at world 1")
+    p.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                   help="N>1: weak = every rank traces its own 1 spp of the frame (default for "
+                        "configs 2/3/5); strong = the ranks split one frame into image stripes "
+                        "(default for config 4)")
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                    help="BASELINE.json config: 2 = 1080p x4 (default, the metric's workload); "
                         "3 = + CV lookup at every vertex; 4 = 4K x6 at 2^24 slots; 5 = drifting "
                         "camera (+0.02/iter), 2^20 slots so eviction engages")
     a = p.parse_args()
+    if a.scaling is None:
+        a.scaling = "strong" if a.config == 4 else "weak"
     if a.config == 4:
         a.width, a.height, a.bounces, a.capacity_log2, a.streams = 3840, 2160, 6, 24, 2
     if a.config == 5:
         a.capacity_log2 = 20
     return a
+
+
+WORKLOADS = {
+    2: "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, spatio-directional "
+       "keys, Lo/LoE/FLi stores x 2^22 slots, base=diam/256",
+    3: "config3: config 2 + CV lookup (Lo\\E query) at every vertex",
+    4: "config4: 3840x2160 1spp x6 bounces, Lo/LoE/FLi x 2^24 slots",
+    5: "config5: config 2 with the camera drifting +0.02/iteration, 2^20 slots (eviction "
+       "engages), inputs regenerated untimed",
+}
+
+
+def bench_config(args, streams, world, multi=None):
+    """the `config` object both arms print (identical for the same command line); multi: the
+    multi-GPU protocol runs (default: world > 1; --force-sharded runs it on one rank)"""
+    multi = world > 1 if multi is None else multi
+    W, H, B = args.width, args.height, args.bounces
+    return {
+        "workload": WORKLOADS[args.config], "vertices_per_iter": W * H * B,
+        "capacity_log2": args.capacity_log2, "stores": 3, "mode": args.mode,
+        "iteration_streams": streams,
+        "inputs": "%d distinct iteration streams of %.2f GB cycled (inputs larger than L2)"
+                  % (streams, BYTES_PER_VERTEX * W * H * B / 1e9),
+        "parallelism": "single GPU" if not multi else
+                       (f"{world} ranks, each tracing its own 1 spp of the frame (weak scaling)"
+                        if args.scaling == "weak" else
+                        f"{world} ranks, one frame split into {world} image stripes (strong "
+                        "scaling)") + ", one field cache: replicated stores, live-slot "
+                        "accumulators all-reduced over NCCL",
+    }
 
 
 def peaks():
@@ -136,7 +173,7 @@ def dist_env():
 
 
 # ---------------------------------------------------------------- CPU reference leg
-def cpu_reference_run(args, steps, warmup, budget_s):
+def cpu_reference_run(args, steps, warmup, budget_s, streams=2):
     """The reference FieldStore (oracle/_ref) + onVertex replay, non-deterministic mode on all host
     threads (EstimatorRun::renderFrame threading, estimators.cpp:566-608).  Each step replays a
     path sample (all bounces of a random subset of the frame's paths) and runs endFrame on the
@@ -151,8 +188,6 @@ def cpu_reference_run(args, steps, warmup, budget_s):
     n_paths = W * H
     n_full = n_paths * B
     gen_threads = max(1, threads)
-    bufs = [po.synth_generate(W, H, B, iteration=i, threads=gen_threads)[0] for i in range(2)]
-
     def sample(buf, frac, seed):
         k = max(1, int(n_paths * frac))
         rng = np.random.default_rng(seed)
@@ -186,18 +221,26 @@ def cpu_reference_run(args, steps, warmup, budget_s):
         t2 = time.perf_counter()
         return t1 - t0, t2 - t1
 
-    # calibrate on a small sample, then size the sample to the budget
-    cal, cm = sample(bufs[0], 1.0 / 64, 1)
+    # calibrate on a small sample, then size the sample to the budget; the iteration streams
+    # are generated one at a time and only their samples kept (the GPU arm cycles the same
+    # `streams` iteration streams)
+    buf0 = po.synth_generate(W, H, B, iteration=0, threads=gen_threads)[0]
+    cal, cm = sample(buf0, 1.0 / 64, 1)
     tp, te = step(cal, cm)
     rate = cm / max(tp, 1e-9)
     per_step = budget_s / max(1, steps + warmup)
     frac = max(1.0 / 64, min(1.0, (per_step - te) * rate / n_full)) if per_step > te else 1.0 / 64
-    samples = [sample(bufs[i % 2], frac, 100 + i) for i in range(2)]
+    samples = [sample(buf0, frac, 100)]
+    del buf0
+    for i in range(1, streams):
+        bi = po.synth_generate(W, H, B, iteration=i, threads=gen_threads)[0]
+        samples.append(sample(bi, frac, 100 + i))
+        del bi
     for i in range(warmup):
-        step(*samples[i % 2])
+        step(*samples[i % len(samples)])
     tot_v, tot_t, t_pass, t_ef = 0, 0.0, 0.0, 0.0
     for i in range(steps):
-        sbuf, m = samples[i % 2]
+        sbuf, m = samples[(warmup + i) % len(samples)]
         a, b = step(sbuf, m)
         tot_v += m
         tot_t += a + b
@@ -215,7 +258,8 @@ def cpu_reference_run(args, steps, warmup, budget_s):
         "value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
         "kind": kind, "host": po.host_info(),
         "phases_ms_per_iteration": phases,
-        "sample": (f"{frac:.4f} of the {n_full}-vertex config-2 iteration per step "
+        "sample": (f"{frac:.4f} of the {n_full}-vertex iteration per step, {len(samples)} "
+                   f"iteration streams cycled "
                    f"({samples[0][1]} vertices = all {B} bounces of a random path subset), "
                    f"{steps} steps after {warmup} warm-up; each step = onVertex replay "
                    f"({'non-deterministic, ' + str(threads) + ' std::threads' if kind == 'reference' else '1 thread'}) "
@@ -229,16 +273,15 @@ def cpu_reference_run(args, steps, warmup, budget_s):
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
-        return 0
-    r = cpu_reference_run(args, args.steps, args.warmup, budget_s=150.0)
+        return 0  # under a launcher rank 0 alone times the host path
+    r = cpu_reference_run(args, args.steps, args.warmup, budget_s=150.0,
+                          streams=max(1, args.streams))
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex "
-                               "stream, Lo/LoE/FLi stores x 2^22 slots (reference FieldStore on "
-                               "host cores)", "vertices_per_iter": args.width * args.height * args.bounces},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64", "data": DATA, "impl": "reference", "launched_ranks": world,
+        "config": bench_config(args, max(1, args.streams), args.gpus),
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                          "sample": r["sample"], "host": r["host"],
                          "phases_ms_per_iteration": r["phases_ms_per_iteration"]},
@@ -271,12 +314,18 @@ def run_b200(args):
     stores = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=args.capacity_log2,
                                                 base_cell_size=base), device=local)
               for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
-    n = W * H * B
     S = max(1, args.streams)
     drift = args.config == 5
+    strong = world > 1 and args.scaling == "strong"
+    n_paths = W * H
+    p0, p1 = (n_paths * rank // world, n_paths * (rank + 1) // world) if strong else (0, n_paths)
+    n = (p1 - p0) * B  # this rank's vertices per iteration
+    # weak: rank r traces its own 1 spp of the frame (its own seed); strong: rank r traces the
+    # image stripe [p0, p1) of the one frame (all bounces of its paths)
+    seed = 0x5EED + (0 if strong else 7919 * rank)
     bufs = []
-    for i in range(1 if drift else S):  # rank r traces its own 1 spp of the frame: weak scaling
-        b, _ = pb.synth_generate(W, H, B, seed=0x5EED + 7919 * rank, iteration=i)
+    for i in range(1 if drift else S):
+        b, _ = pb.synth_generate(W, H, B, seed=seed, iteration=i, path0=p0, npaths=p1 - p0)
         bufs.append(b)
     if drift:
         S = 1
@@ -289,11 +338,11 @@ def run_b200(args):
     def regenerate(i):
         """config 5: the camera drifts +0.02 per iteration (untimed input production)"""
         shift = ((0.02 * i + 0.9) % 1.8) - 0.9
-        pb.synth_generate(W, H, B, seed=0x5EED + 7919 * rank, iteration=i, cam_shift_x=shift,
-                          out=bufs[0])
+        pb.synth_generate(W, H, B, seed=seed, iteration=i, cam_shift_x=shift, out=bufs[0],
+                          path0=p0, npaths=p1 - p0)
     sharded = None
     if dist is not None:
-        # one global field cache, hash space sharded by key owner across the ranks
+        # one field cache over the ranks: replicated stores, all-reduced accumulators
         from paper_2005_07547_b200.shard import Collectives, CudaBackend, ShardedFieldCache
         sharded = ShardedFieldCache(CudaBackend(stores, rank, world),
                                     Collectives(dist, torch.device("cuda", local)))
@@ -353,7 +402,7 @@ def run_b200(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_vertices = n * args.steps * world
+    total_vertices = (W * H * B if strong else n * world) * args.steps
     value = total_vertices / (ms / 1e3)
     ms_step = ms / args.steps
     st = [s.stats() for s in stores]
@@ -374,12 +423,17 @@ def run_b200(args):
     red_ach = reds_step / (vp_avg / 1e3) if reds_step else 0.0
     step_bytes = BYTES_PER_VERTEX * n + BYTES_PER_TOUCHED * mean_touched + cv_bytes
     step_ach = step_bytes / (ms_step / 1e3) / 1e9
-    traffic = None
+    # DRAM traffic of the dominant kernel: not measurable inside this run (it needs an ncu
+    # capture); the value comes from the committed capture named in traffic_source
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_vertex_pass_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_src = ("past capture, not this run: profiles/ncu_vertex_pass_traffic.json (%s)"
+                           % tj.get("source", "ncu --set full"))
         except Exception:
             traffic = None
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]}
@@ -388,29 +442,14 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (pstf_synth.h Cornell-box generator, IEEE-exact, seed 0x5EED)",
-        "config": {
-            "workload": {2: "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, "
-                            "spatio-directional keys, Lo/LoE/FLi stores x 2^22 slots, "
-                            "base=diam/256",
-                         3: "config3: config 2 + CV lookup (Lo\\E query) at every vertex "
-                            "(Lambertian synthetic scene, not glossy)",
-                         4: "config4: 3840x2160 1spp x6 bounces, Lo/LoE/FLi x 2^24 slots",
-                         5: "config5: config 2 with the camera drifting +0.02/iteration, "
-                            "2^20 slots (eviction engages), inputs regenerated untimed"}[args.config],
-            "vertices_per_iter": n, "capacity_log2": args.capacity_log2, "stores": 3,
-            "mode": args.mode, "iteration_streams": S,
-            "l2": "inputs larger than L2 (%.2f GB per iteration stream vs %d MB L2 read from the "
-                  "device, %d streams cycled)" % (BYTES_PER_VERTEX * n / 1e9, l2_bytes >> 20, S),
-            "parallelism": "single GPU" if sharded is None else
-                           f"{world} ranks, 1 spp of the 1080p frame each (weak scaling), one "
-                           f"field cache sharded by key owner (NCCL all-gather / all-to-all)",
-        },
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "impl": "b200",
+        "config": bench_config(args, S, world, multi=sharded is not None),
+        "l2_bytes": l2_bytes,  # cudaDevAttrL2CacheSize (inputs per step are larger)
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "spec_peak": 8000.0, "frac_of_spec": ach / 8000.0,
-                     "frac": ach / peak, "traffic": traffic,
+                     "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": vp[0][0] if vp else None,
                      "bytes_per_launch": vp_bytes, "avg_launch_ms": vp_avg,
                      "peak_source": peak_src},
@@ -466,13 +505,13 @@ def run_b200(args):
             t = torch.tensor([et], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
-        line["e2e"] = {"value": n * E * world / et, "unit": UNIT,
+        line["e2e"] = {"value": (W * H * B if strong else n * world) * E / et, "unit": UNIT,
                        "h2d_bytes_per_step": BYTES_PER_VERTEX * n,
                        "d2h_bytes_per_step": 3 * 8 * 11, "steps": E,
                        "path": ("pstf_vertex_pass_host (pinned host SoA, chunked H2D overlapped "
                                 "with phase 1) + pstf_fields_end_frame + stats readback")
                        if sharded is None else
-                       "pinned host SoA -> HBM copy + sharded iteration + stats readback"}
+                       "pinned host SoA -> HBM copy + multi-GPU iteration + stats readback"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -490,8 +529,26 @@ def run_b200(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-run this command as N ranks (one process per GPU) under
+    torch.distributed.run on this node; rank 0's JSON line is the output"""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200(args)

@@ -271,21 +271,23 @@ int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed
 /* Fills a pstf_vertex_soa view of such a contiguous buffer (host or device memory). */
 void pstf_vertex_soa_from_buffer(const double *buffer, uint64_t n, pstf_vertex_soa *out);
 
-/* ---- key-owner sharding across ranks (one process per GPU) ----
- * Every rank holds a full replica of each store's occupancy and committed state; rank r owns
- * the contiguous slot range [r*cap/world, (r+1)*cap/world) and alone blends / evicts it.
- * Per frame (collectives are the caller's, e.g. NCCL via torch.distributed):
- *   1. pstf_vertex_pass_local on the rank's image stripe (lookups on the replica, REDs into a
- *      local partial accumulator; new keys stay pending)
- *   2. all-gather the pending records (pstf_pending_count/_copy) and pstf_resolve_records on
- *      every rank: identical deterministic placement everywhere, own records' sums applied
- *   3. pstf_partials_export (touched non-owned slots, destination-major) -> all-to-all ->
- *      pstf_partials_import on the owners
- *   4. pstf_end_frame_reduce -> all-reduce the (sum c_new, count) pairs ->
- *      pstf_end_frame_commit (blend + evict the owned range, emit deltas)
- *   5. all-gather deltas -> pstf_deltas_import (replicas converge)
- * Slot placement equals the single-GPU layout; values differ only in summation order.
- * Only the ATOMIC mode is sharded. */
+/* ---- multi-GPU: one field cache over several ranks (one process per GPU) ----
+ * Replaces the reference's shared-memory std::thread workers (estimators.cpp:566-623) with one
+ * process per GPU, each tracing its own vertices (an image stripe, or its own samples).  Every
+ * rank holds a bitwise-identical replica of each store; per frame (collectives are the
+ * caller's, e.g. NCCL via torch.distributed):
+ *   1. pstf_vertex_pass_local on the rank's vertices: lookups on the replica (committed state,
+ *      field.h:73-75), REDs into the replica's accumulators, new keys stay pending
+ *   2. the pstf_shard_info vectors (pending sizes, live count) are all-gathered on the device
+ *      and read with ONE host synchronisation; all-gather the pending records;
+ *      pstf_resolve_records on every rank: identical deterministic placement (the single-GPU
+ *      layout), each rank adds only its own records' sums
+ *   3. pstf_shard_live_pack: the accumulators of the live slots, packed in slot order (entry i
+ *      is the same slot on every rank), zero-padded to `bound` entries -> all-reduce (sum) ->
+ *      pstf_shard_live_unpack (sums back, slots touched on any rank marked touched)
+ *   4. pstf_fields_end_frame on every rank: identical inputs, identical committed state
+ * Slot placement, ages and counts equal the single-GPU run; values differ from it only in fp64
+ * summation order.  Only the ATOMIC mode is sharded. */
 int pstf_shard_set(pstf_field *f, int rank, int world);
 int pstf_vertex_pass_local(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
                            const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
@@ -297,32 +299,21 @@ int pstf_pending_count_dev(pstf_field *lo, int64_t *dev_count, void *stream);
 int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream);
 int pstf_resolve_records(pstf_field *const *stores, int nst, const void *records, uint64_t n,
                          void *stream);
-int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
-                         uint64_t *counts_per_rank, void *stream);
-/* ... without a host round trip: the per-rank counts land in dev_counts[world] (device int64)
- * for a device-side count exchange; cap must be at least the sum of the stores' capacities */
-int pstf_partials_export_async(pstf_field *const *stores, int nst, void *out, uint64_t cap,
-                               int64_t *dev_counts, void *stream);
-int pstf_partials_import(pstf_field *const *stores, int nst, const void *records, uint64_t n,
-                         void *stream);
-int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_count, void *stream);
-int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_count,
-                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
-int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,
-                       void *stream);
-/* Same two steps with the (sum c_new, count) pairs in DEVICE memory (2*nst doubles), so the
- * all-reduce between them needs no host round trip. */
-int pstf_end_frame_reduce_dev(pstf_field *const *stores, int nst, double *dev_sum_count,
-                              void *stream);
-int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *dev_sum_count,
-                              void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream);
-/* ... and with the delta count written to a device int64 instead of returned (no host round
- * trip); cap must cover every owned slot (sum of capacity / world), else PSTF_E_INVALID */
-int pstf_end_frame_commit_async(pstf_field *const *stores, int nst, const double *dev_sum_count,
-                                void *deltas, uint64_t cap, int64_t *dev_ndeltas, void *stream);
+/* dev_out3 (device int64[3]) = {this rank's pending records, live slots over the stores (after
+ * the last endFrame: with every rank's pending records an upper bound of the live count after
+ * placement), packs whose live count exceeded their bound (must stay 0)} */
+int pstf_shard_info(pstf_field *const *stores, int nst, int64_t *dev_out3, void *stream);
+/* packed[bound][4] (device f64) <- acc of every live slot of the stores, in (store, slot)
+ * order; dev_live_total <- the live count (device int64).  The packed list stays with the
+ * stores' scratch until pstf_shard_live_unpack. */
+int pstf_shard_live_pack(pstf_field *const *stores, int nst, double *packed, uint64_t bound,
+                         int64_t *dev_live_total, void *stream);
+int pstf_shard_live_unpack(pstf_field *const *stores, int nst, const double *packed,
+                           void *stream);
+/* steps 3b + 4 in one: endFrame (field.cpp:197-263) of every store straight from the
+ * all-reduced packed accumulators (== pstf_shard_live_unpack then pstf_fields_end_frame) */
+int pstf_shard_end_frame(pstf_field *const *stores, int nst, const double *packed, void *stream);
 uint64_t pstf_pending_record_bytes(void); /* 64 */
-uint64_t pstf_partial_record_bytes(void); /* 40: {u32 store, u32 slot, f64 acc[4]} */
-uint64_t pstf_delta_record_bytes(void);   /* 48: {u32 store, slot, checksum, last+1; f64 com[4]} */
 
 /* Number of kernels this library launched since load (bench evidence). */
 uint64_t pstf_kernel_launch_count(void);
@@ -389,7 +380,11 @@ int pstf_model_destroy(pstf_model_store *m);
  *   (key fields, uv.x, uv.y, contribution): bitwise the reference's deterministic mode.
  * PSTF_MODE_ATOMIC: no sort, fp64 atomics into the grids; accumulator sums within 1e-12
  *   relative (their order is the atomics'), everything else exact.  GMM stores always take
- *   the canonical order (stepwise EM depends on the sample order, not only on rounding). */
+ *   the canonical order (stepwise EM depends on the sample order, not only on rounding).
+ * Precondition of the bitwise claim: ONE apply call per store per frame, carrying all of the
+ * frame's records.  The reference sorts the whole frame's records once (estimators.cpp:
+ * 625-643); records split over several calls are canonicalised per call, which changes the
+ * per-cell accumulation order (and the GMM EM sample order) against the reference. */
 int pstf_model_apply(pstf_model_store *m, const pstf_key *keys, const double *u, const double *v,
                      const double *contribution, uint64_t n, int mode, void *stream);
 /* ModelStore::endFrame (estimators.cpp:119-144) */

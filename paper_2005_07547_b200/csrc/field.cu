@@ -172,6 +172,10 @@ struct Scratch {
     DBuf fterms, fisc, fstart, fnruns;      // ORDERED/SEQUENTIAL fold: terms, run starts
     DBuf winner;                            // snapshot restore: last record per slot
     DBuf hio;                               // host-pointer API staging
+    DBuf ulist, overflow;                   // sharding: packed live list, pack-overflow flag
+    uint64_t live_bound = 0;
+    long long *live_total_dev = nullptr;
+    bool overflow_zeroed = false;
     unsigned long long *h_small = nullptr;  // pinned readback
     ~Scratch() {
         if (h_small) cudaFreeHost(h_small);
@@ -1512,7 +1516,6 @@ __global__ void k_unique_sums(const PendRec *pend, const uint32_t *perm, const u
     }
     unsigned peers = __match_any_sync(0xffffffffu, q);
     sm[lane_id()] = v;
-    unsigned tot = 0;
     __syncwarp();
     if (live && (int)lane_id() == __ffs(peers) - 1) {
         double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -1526,7 +1529,6 @@ __global__ void k_unique_sums(const PendRec *pend, const uint32_t *perm, const u
             t.z += x.z;
             t.w += x.w;
         }
-        (void)tot;
         if (atomic_mode) {
             if (t.x != 0.0) atomicAdd(&u.usum[q].x, t.x);
             if (t.y != 0.0) atomicAdd(&u.usum[q].y, t.y);
@@ -1854,6 +1856,7 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
     }
     if (t == R_PROPOSE) {
         s.meta[slot].x = a.ucs[u]; /* (k_place_loop has released the slot's hold) */
+        atomicOr(&s.lbits[slot >> 5], 1u << (slot & 31u));
         s.keyf[slot] = ukey[u];
         /* live / new-key counters: one atomic per group of lanes of the same store */
         const unsigned grp = __match_any_sync(__activemask(), a.usid[u]);
@@ -1870,8 +1873,9 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
         if (v.z != 0.0) atomicAdd(&dst->z, v.z);
         if (v.w != 0.0) atomicAdd(&dst->w, v.w);
     }
-    /* sharded: a replica touches a slot only for its own records or as the slot's owner */
-    if (ucalls[u] != 0 || owned(s, slot)) touch_slot(s, slot);
+    /* sharded: a replica touches a slot for its own records only (the all-reduce of the
+     * accumulators marks the slots the other ranks touched) */
+    if (ucalls[u] != 0) touch_slot(s, slot);
 }
 
 /* ORDERED / SEQUENTIAL: per-record fold target (store << 32 | slot), dropped -> ~0 */
@@ -2167,6 +2171,30 @@ __device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst) {
     }
 }
 
+/* the blend of one slot with c_new > 0 (field.cpp:218-241): candidate, alpha with the 1/T floor,
+ * mix, cOld capped at (T^2 - T) * mean c_new (the store's Σc_new / count of this frame) */
+__device__ __forceinline__ double4 blend_one(const DevStore &s, double4 a, double4 c) {
+    const double cn = a.w;
+    const unsigned long long cnt = s.ctr[C_CN_COUNT];
+    const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
+    const double tMax = s.t_max;
+    const bool limited = tMax > 0.0 && isfinite(tMax);
+    const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
+    const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
+    double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
+    if (limited) {
+        const double fl = 1.0 / tMax;
+        alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
+    }
+    const double oma = 1.0 - alpha;
+    c.x = c.x * oma + cx * alpha;
+    c.y = c.y * oma + cy * alpha;
+    c.z = c.z * oma + cz * alpha;
+    c.w = c.w + cn;
+    if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+    return c;
+}
+
 /* endFrame pass 2 (field.cpp:216-246) over every store's touched list at once (one flat index
  * space), two entries per thread per iteration with their acc/com loads in flight together */
 __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
@@ -2203,26 +2231,7 @@ __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
             const double4 a = av[k];
             const double cn = a.w;
             if (cn > 0.0) {
-                const unsigned long long cnt = s.ctr[C_CN_COUNT];
-                const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
-                const double tMax = s.t_max;
-                const bool limited = tMax > 0.0 && isfinite(tMax);
-                const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
-                double4 c = cv[k];
-                const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
-                double alpha =
-                    s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
-                if (limited) {
-                    const double fl = 1.0 / tMax;
-                    alpha = (alpha < fl) ? fl : alpha; /* std::max(alpha, 1/tMax) */
-                }
-                const double oma = 1.0 - alpha;
-                c.x = c.x * oma + cx * alpha;
-                c.y = c.y * oma + cy * alpha;
-                c.z = c.z * oma + cz * alpha;
-                c.w = c.w + cn;
-                if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
-                s.com[slot] = c;
+                s.com[slot] = blend_one(s, a, cv[k]);
             } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -2257,6 +2266,7 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
             const uint2 m = s.meta[i];
             if (m.x != 0 && (uint32_t)(s.frame - (m.y - 1u)) >= s.evict_age) {
                 s.meta[i].x = 0;
+                atomicAnd(&s.lbits[i >> 5], ~(1u << (i & 31u)));
                 s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
                 ++ev;
             }
@@ -2269,145 +2279,186 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
     }
 }
 
-/* ---------------- key-owner sharding (multi-GPU) ---------------- */
-struct PartialRec { /* 40 B: one touched non-owned slot's partial accumulators */
-    uint32_t store, slot;
-    double acc[4];
-};
-struct DeltaRec { /* 48 B: one committed slot of the owner's range */
-    uint32_t store, slot, checksum, last_biased;
-    double com[4];
+/* ---------------- multi-GPU: replicated stores, all-reduced accumulators ----
+ * Every rank holds a bitwise-identical replica of each store.  After phase 1 on its own
+ * vertices and the identical placement of every rank's new keys, the ranks all-reduce the
+ * accumulators of the live slots — packed in slot order, so entry i is the same slot on every
+ * rank — and every rank then runs the ordinary endFrame on identical inputs. */
+
+struct WSeg { /* word offsets of the stores in one flat word space; o[nst] = total */
+    uint32_t o[5];
 };
 
-/* words of the touched bitmap owned by another rank: popcounts */
-__global__ void k_px_count(DevStore s, uint32_t *cnt, uint64_t nwords) {
-    uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (w > nwords) return;
-    if (w == nwords) {
+/* live-slot counts of the 32-slot words of the stores' flat word space (store j's words at
+ * [wseg.o[j], wseg.o[j+1])), from the live bitmaps; cnt has one extra trailing word so the
+ * exclusive scan also yields the total */
+__global__ void k_live_count(Stores4 st, int nst, WSeg wseg, uint32_t *cnt) {
+    const uint64_t total = wseg.o[nst];
+    const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (w > total) return;
+    if (w == total) {
         cnt[w] = 0;
         return;
     }
-    cnt[w] = owned(s, (uint32_t)(w * 32)) ? 0u : (uint32_t)__popc(s.tbits[w]);
+    int j = 0;
+    while (j + 1 < nst && w >= wseg.o[j + 1]) ++j;
+    cnt[w] = (uint32_t)__popc(st.s[j].lbits[w - wseg.o[j]]);
 }
 
-/* export touched non-owned slots (slot order == owner order), zero them, clear their bits */
-__global__ void k_px_write(DevStore s, uint32_t sid, const uint32_t *scan, uint64_t nwords,
-                           uint64_t words_per_rank, const unsigned long long *dest_base,
-                           PartialRec *out) {
-    uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (w >= nwords || owned(s, (uint32_t)(w * 32))) return;
-    uint32_t bits = s.tbits[w];
-    if (!bits) return;
-    s.tbits[w] = 0;
-    const uint64_t r = w / words_per_rank;
-    unsigned long long pos = dest_base[r] + (scan[w] - scan[r * words_per_rank]);
-    while (bits) {
-        const uint32_t slot = (uint32_t)(w * 32 + (uint64_t)(__ffs(bits) - 1));
-        bits &= bits - 1;
-        const double4 a = s.acc[slot];
-        PartialRec rec;
-        rec.store = sid;
-        rec.slot = slot;
-        rec.acc[0] = a.x;
-        rec.acc[1] = a.y;
-        rec.acc[2] = a.z;
-        rec.acc[3] = a.w;
-        out[pos++] = rec;
-        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
-    }
-}
-
-__global__ void k_px_import(Stores4 st, const PartialRec *recs, uint64_t n) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const PartialRec r = recs[i];
-    const DevStore &s = st.s[r.store & 3];
-    red_add4(&s.acc[r.slot], make_double4(r.acc[0], r.acc[1], r.acc[2], r.acc[3]));
-    touch_slot(s, r.slot);
-}
-
-/* after the blend: every slot of the touched list (all owned) becomes a delta */
-__global__ void k_dx_touched(DevStore s, uint32_t sid, DeltaRec *out, unsigned long long *count) {
-    const uint64_t n = s.ctr[C_TOUCHED_N];
+/* entry scan[w] + k of the packed list = the k-th live slot of word w: its (store, slot) and
+ * its accumulators (a word per thread, its set bits in slot order); entries
+ * [live_total, bound) are zero */
+__global__ void k_live_pack(Stores4 st, int nst, WSeg wseg, const uint32_t *scan,
+                            uint64_t bound, unsigned long long *list, double4 *packed,
+                            long long *live_total, unsigned long long *overflow) {
+    const uint64_t total = wseg.o[nst];
+    const uint64_t n = scan[total];
+    const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    /* warp-uniform trip count: one output reservation per warp */
-    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
-         i0 += stride) {
-        const uint64_t i = i0 + lane_id();
-        const bool live = i < n;
-        const unsigned wm = __ballot_sync(0xffffffffu, live);
-        unsigned long long base = 0;
-        if (lane_id() == 0) base = atomicAdd(count, (unsigned long long)__popc(wm));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (!live) continue;
-        const uint32_t slot = s.tlist[i];
-        const uint2 m = s.meta[slot];
-        const double4 c = s.com[slot];
-        DeltaRec d;
-        d.store = sid;
-        d.slot = slot;
-        d.checksum = m.x;
-        d.last_biased = m.y;
-        d.com[0] = c.x;
-        d.com[1] = c.y;
-        d.com[2] = c.z;
-        d.com[3] = c.w;
-        out[base + __popc(wm & ((1u << lane_id()) - 1u))] = d;
+    if (t0 == 0) {
+        *live_total = (long long)n;
+        if (n > bound) atomicAdd(overflow, 1ull);
     }
-}
-
-/* age eviction of the owned slot range only; evicted slots become deltas */
-__global__ void k_ef_evict_range(DevStore s, uint32_t sid, uint64_t lo, uint64_t hi, DeltaRec *out,
-                                 unsigned long long *count) {
-    const uint64_t cap = (uint64_t)s.mask + 1;
-    if (!(s.ctr[C_LIVE_SNAP] * 4ull > (unsigned long long)cap * 3ull)) return;
-    unsigned ev = 0;
-    for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint2 m = s.meta[i];
-        if (m.x != 0 && (uint32_t)(s.frame - (m.y - 1u)) >= s.evict_age) {
-            s.meta[i].x = 0;
-            s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
-            ++ev;
-            DeltaRec d;
-            d.store = sid;
-            d.slot = (uint32_t)i;
-            d.checksum = 0;
-            d.last_biased = m.y;
-            d.com[0] = d.com[1] = d.com[2] = d.com[3] = 0.0;
-            out[atomicAdd(count, 1ull)] = d;
+    for (uint64_t w = t0; w < total; w += stride) {
+        int j = 0;
+        while (j + 1 < nst && w >= wseg.o[j + 1]) ++j;
+        const DevStore &s = st.s[j];
+        const uint64_t wl = w - wseg.o[j];
+        uint32_t bits = s.lbits[wl];
+        uint64_t pos = scan[w];
+        while (bits && pos < bound) {
+            const uint32_t slot = (uint32_t)(wl * 32 + (uint64_t)(__ffs(bits) - 1));
+            bits &= bits - 1;
+            list[pos] = ((unsigned long long)j << 32) | slot;
+            packed[pos] = s.acc[slot];
+            ++pos;
         }
     }
-    ev = __reduce_add_sync(0xffffffffu, ev);
-    if (lane_id() == 0 && ev) {
-        atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
-        atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
+    for (uint64_t i = n + t0; i < bound; i += stride) packed[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+}
+
+/* the all-reduced accumulators back into every replica; a slot touched on any rank (a nonzero
+ * sum: every update call of a vertex pass carries weight 1 in c_new) gets lastTouched = frame
+ * and its touched bit, exactly as a local touch would have set them */
+__global__ void k_live_unpack(Stores4 st, const unsigned long long *list, const double4 *packed,
+                              const long long *live_total, uint64_t bound) {
+    const uint64_t n = min((uint64_t)*live_total, bound);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long e = list[i];
+        const DevStore &s = st.s[(e >> 32) & 3];
+        const uint32_t slot = (uint32_t)e;
+        const double4 v = packed[i];
+        s.acc[slot] = v;
+        if (v.x != 0.0 || v.y != 0.0 || v.z != 0.0 || v.w != 0.0) touch_slot(s, slot);
     }
 }
 
-/* replicas apply the other owners' committed slots (own deltas are already in place) */
-__global__ void k_dx_import(Stores4 st, const DeltaRec *recs, uint64_t n) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const DeltaRec d = recs[i];
-    const DevStore &s = st.s[d.store & 3];
-    if (owned(s, d.slot)) return;
-    const uint32_t old = s.meta[d.slot].x;
-    s.meta[d.slot] = make_uint2(d.checksum, d.last_biased);
-    s.com[d.slot] = make_double4(d.com[0], d.com[1], d.com[2], d.com[3]);
-    if (old != 0 && d.checksum == 0) atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-1ll));
+/* endFrame (field.cpp:197-263) of a multi-GPU frame straight from the all-reduced packed
+ * accumulators (one cooperative launch, no unpack into acc): pass 1 sums c_new per store over
+ * the packed entries; pass 2 blends the touched entries (a nonzero sum: every update call of a
+ * vertex pass carries weight 1 in c_new), marks them touched this frame and zeroes the
+ * replica's own partial accumulators; pass 3 is the usual age eviction (identical on every
+ * replica: same live counts, same ages). */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_packed(Stores4 st, int nst,
+                                                        const unsigned long long *list,
+                                                        const double4 *packed,
+                                                        const long long *live_total,
+                                                        uint64_t bound) {
+    cg::grid_group g = cg::this_grid();
+    __shared__ double ssum[4][EF_BLOCK / 32];
+    __shared__ unsigned long long scnt[4][EF_BLOCK / 32], stch[4][EF_BLOCK / 32];
+    const uint64_t n = min((uint64_t)*live_total, bound);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)nst) {
+        const DevStore &s = st.s[threadIdx.x];
+        s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+        s.ctr[C_EVICTED] = 0;
+    }
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned cnt[4] = {0u, 0u, 0u, 0u}, tch[4] = {0u, 0u, 0u, 0u};
+    for (uint64_t i = t0; i < n; i += stride) {
+        const int j = (int)((list[i] >> 32) & 3);
+        const double4 v = packed[i];
+        const bool touched = v.x != 0.0 || v.y != 0.0 || v.z != 0.0 || v.w != 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q == j) {
+                if (v.w > 0.0) {
+                    sum[q] += v.w;
+                    ++cnt[q];
+                }
+                tch[q] += touched;
+            }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double t = warp_sum_d(sum[q]);
+        const unsigned cc = __reduce_add_sync(0xffffffffu, cnt[q]);
+        const unsigned tt = __reduce_add_sync(0xffffffffu, tch[q]);
+        if (lane_id() == 0) {
+            ssum[q][threadIdx.x >> 5] = t;
+            scnt[q][threadIdx.x >> 5] = cc;
+            stch[q][threadIdx.x >> 5] = tt;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)nst) {
+        const int q = threadIdx.x;
+        double t = 0.0;
+        unsigned long long c = 0, tc = 0;
+        for (int w = 0; w < EF_BLOCK / 32; ++w) {
+            t += ssum[q][w];
+            c += scnt[q][w];
+            tc += stch[q][w];
+        }
+        if (c) {
+            atomicAdd(st.s[q].cn_sum, t);
+            atomicAdd(&st.s[q].ctr[C_CN_COUNT], c);
+        }
+        if (tc) atomicAdd(&st.s[q].ctr[C_TOUCHED_N], tc);
+    }
+    g.sync();
+    unsigned internal[4] = {0u, 0u, 0u, 0u};
+    for (uint64_t i = t0; i < n; i += stride) {
+        const unsigned long long e = list[i];
+        const int j = (int)((e >> 32) & 3);
+        const DevStore &s = st.s[j];
+        const uint32_t slot = (uint32_t)e;
+        const double4 v = packed[i];
+        if (!(v.x != 0.0 || v.y != 0.0 || v.z != 0.0 || v.w != 0.0)) continue;
+        if (v.w > 0.0) {
+            s.com[slot] = blend_one(s, v, s.com[slot]);
+        } else if (!(v.x == 0.0 && v.y == 0.0 && v.z == 0.0)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q == j) ++internal[q];
+        }
+        s.meta[slot].y = s.frame + 1u; /* lastTouched = frame (field.cpp:123,133,137) */
+        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const unsigned t = __reduce_add_sync(0xffffffffu, internal[q]);
+        if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
+    }
+    g.sync();
+    ef_evict_body(st, nst, 1);
 }
 
-/* roll the per-frame scratch of every store of the batch */
-__global__ void k_ef_finish(Stores4 st, int nst) {
-    const int j = threadIdx.x;
-    if (j >= nst) return;
-    const DevStore &s = st.s[j];
-    s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
-    s.ctr[C_TOUCHED_TOTAL] += s.ctr[C_TOUCHED_N];
-    s.ctr[C_TOUCHED_N] = 0;
-    s.ctr[C_CN_COUNT] = 0;
-    *s.cn_sum = 0.0;
+/* the vector the one host synchronisation of a multi-GPU frame reads: {pending records of this
+ * rank, live slots over the stores (after the last endFrame), pack overflows} */
+__global__ void k_shard_info(Stores4 st, int nst, const unsigned long long *pend_count,
+                             uint64_t pend_cap, const unsigned long long *overflow,
+                             long long *out) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long pc = pend_count ? *pend_count : 0ull;
+    out[0] = (long long)(pc < pend_cap ? pc : pend_cap);
+    long long live = 0;
+    for (int j = 0; j < nst; ++j) live += (long long)st.s[j].ctr[C_LIVE];
+    out[1] = live;
+    out[2] = (long long)(overflow ? *overflow : 0ull);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -3061,7 +3112,8 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     };
     size_t o_meta = take(cap * 8), o_com = take(cap * 32), o_acc = take(cap * 32),
            o_keyf = take(cap * sizeof(KeyFields)), o_h0 = take(cap * 4), o_h1 = take(cap * 4),
-           o_tbits = take(((cap + 31) / 32) * 4), o_tlist = take(cap * 4), o_ctr = take(C_NUM * 8),
+           o_tbits = take(((cap + 31) / 32) * 4), o_lbits = take(((cap + 31) / 32) * 4),
+           o_tlist = take(cap * 4), o_ctr = take(C_NUM * 8),
            o_sum = take(8);
     cudaError_t e = cudaMalloc(&f->arena, off);
     if (e != cudaSuccess) {
@@ -3076,6 +3128,7 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     d.acc = (double4 *)(base + o_acc);
     d.keyf = (KeyFields *)(base + o_keyf);
     d.tbits = (uint32_t *)(base + o_tbits);
+    d.lbits = (uint32_t *)(base + o_lbits);
     d.tlist = (uint32_t *)(base + o_tlist);
     d.hold0 = (uint32_t *)(base + o_h0);
     d.hold1 = (uint32_t *)(base + o_h1);
@@ -3090,7 +3143,6 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
     d.blend = config->blend;
     d.evict_age = config->evict_age_frames;
     d.rank = 0;
-    d.owner_shift = config->capacity_log2; /* unsharded: every slot is owned by rank 0 */
     /* value-initialised slots (field.cpp:232: make_unique<Slot[]>) */
     e = cudaMemset(f->arena, 0, off);
     if (e == cudaSuccess) e = cudaMemset(d.hold0, 0xff, cap * 4);
@@ -4071,8 +4123,6 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
         const uint64_t m = std::min(chunk, n - off);
         CK(cudaStreamWaitEvent(cs, ev_done[b], 0));
         double *d = stage[b].as<double>();
-        const double *src3[15][3] = {};
-        (void)src3;
         const pstf_vec3_soa *v3s[10] = {&hv->position, &hv->wo, &hv->wi, &hv->next_position,
                                         &hv->nee_dir, &hv->emission_here, &hv->f,
                                         &hv->next_emission, &hv->nee_loe, &hv->nee_fli};
@@ -4154,15 +4204,9 @@ static int shard_checks(pstf_field *const *fs, int n) {
 int pstf_shard_set(pstf_field *f, int rank, int world) {
     if (!f) return set_err(PSTF_E_INVALID, "NULL store");
     SETTLE(f);
-    if (world < 1 || world > 32 || (world & (world - 1)))
-        return set_err(PSTF_E_INVALID, "world must be a power of two in [1, 32]");
+    if (world < 1 || world > 32) return set_err(PSTF_E_INVALID, "world must be in [1, 32]");
     if (rank < 0 || rank >= world) return set_err(PSTF_E_INVALID, "bad rank");
-    const uint64_t cap = (uint64_t)f->d.mask + 1;
-    if (cap / (uint64_t)world < 32) return set_err(PSTF_E_INVALID, "capacity/world must be >= 32");
-    int lw = 0;
-    while ((1 << lw) < world) ++lw;
-    f->d.rank = rank;
-    f->d.owner_shift = f->cfg.capacity_log2 - (uint32_t)lw;
+    f->d.rank = rank; /* origin tag of this rank's pending records */
     f->world = world;
     return PSTF_OK;
 }
@@ -4221,6 +4265,8 @@ int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream) {
     return PSTF_OK;
 }
 
+__global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
+
 int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, uint64_t n,
                          void *stream) {
     int rc = shard_checks(stores, nst);
@@ -4234,331 +4280,137 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, u
     if (n) CK(cudaMemcpyAsync(sc.pend.p, recs, n * sizeof(PendRec), cudaMemcpyDeviceToDevice, st));
     /* the device count too: phase 2's key-range pass reads it (an empty range would force the
      * multi-word sort path instead of the sort-free one) */
-    const unsigned long long cnt = n; /* pageable: staged before cudaMemcpyAsync returns */
-    CK(cudaMemcpyAsync(sc.pend_count.p, &cnt, 8, cudaMemcpyHostToDevice, st));
+    LAUNCH(k_set_u64, 1, 1, 0, st, sc.pend_count.as<unsigned long long>(),
+           (unsigned long long)n); /* stream-ordered, no host staging (capture-safe) */
     return resolve_pending(sc, stores, nst, PSTF_MODE_ATOMIC, n, st, stores[0]->d.rank);
 }
 
-/* per (store, rank) partial counts from the word scans' values at the rank boundaries, their
- * destination-major offsets (rank, then store) and each rank's total: all on the device */
-__global__ void k_px_plan(const uint32_t *scan, const unsigned long long *soff, int nst,
-                          int world, const unsigned long long *wpr,
-                          unsigned long long *dest_base, long long *counts) {
-    if (threadIdx.x != 0) return;
-    unsigned long long base = 0;
-    for (int r = 0; r < world; ++r) {
-        unsigned long long tot = 0;
-        for (int j = 0; j < nst; ++j) {
-            const uint32_t *u = scan + soff[j];
-            const unsigned long long c = u[(uint64_t)(r + 1) * wpr[j]] - u[(uint64_t)r * wpr[j]];
-            dest_base[(size_t)j * world + r] = base + tot;
-            tot += c;
-        }
-        counts[r] = (long long)tot;
-        base += tot;
+static WSeg live_word_segments(pstf_field *const *stores, int nst) {
+    WSeg w;
+    uint64_t t = 0;
+    for (int j = 0; j < nst; ++j) {
+        w.o[j] = (uint32_t)t;
+        t += ((uint64_t)stores[j]->d.mask + 1) / 32;
     }
+    for (int j = nst; j < 5; ++j) w.o[j] = (uint32_t)t;
+    return w;
 }
 
-/* pstf_partials_export without any host round trip: per-rank record counts land in
- * dev_counts[world] (device int64); cap must cover every touched non-owned slot (the sum of
- * capacities is always enough) */
-int pstf_partials_export_async(pstf_field *const *stores, int nst, void *out, uint64_t cap,
-                               int64_t *dev_counts, void *stream) {
+int pstf_shard_live_pack(pstf_field *const *stores, int nst, double *packed, uint64_t bound,
+                         int64_t *dev_live_total, void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if (!dev_counts || !out) return set_err(PSTF_E_INVALID, "NULL argument");
-    uint64_t total_cap = 0;
-    for (int j = 0; j < nst; ++j) total_cap += (uint64_t)stores[j]->d.mask + 1;
-    if (cap < total_cap) return set_err(PSTF_E_INVALID, "partials buffer smaller than the stores");
+    if ((bound && !packed) || !dev_live_total) return set_err(PSTF_E_INVALID, "NULL argument");
+    for (int j = 0; j < nst; ++j)
+        if ((uint64_t)stores[j]->d.mask + 1 < 32)
+            return set_err(PSTF_E_INVALID, "sharding needs capacity >= 32");
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
-    const int world = stores[0]->world;
     Scratch &sc = stores[0]->sc;
-    std::vector<uint64_t> nw(nst);
-    std::vector<unsigned long long> off(nst + 1, 0), wpr(nst);
-    for (int j = 0; j < nst; ++j) {
-        nw[j] = ((uint64_t)stores[j]->d.mask + 1) / 32;
-        off[j + 1] = off[j] + nw[j] + 1;
-        wpr[j] = nw[j] / (uint64_t)world;
+    const WSeg wseg = live_word_segments(stores, nst);
+    const uint64_t words = wseg.o[nst];
+    ENSURE(sc.head, (words + 1) * 4);   /* word counts */
+    ENSURE(sc.scan, (words + 1) * 4);   /* their exclusive scan */
+    ENSURE(sc.ulist, std::max<uint64_t>(bound, 1) * 8);
+    ENSURE(sc.overflow, 8);
+    if (!sc.overflow_zeroed) {
+        CK(cudaMemsetAsync(sc.overflow.p, 0, 8, st));
+        sc.overflow_zeroed = true;
     }
-    ENSURE(sc.head, off[nst] * 4);
-    ENSURE(sc.uid, off[nst] * 4);
-    ENSURE(sc.ranges, ((size_t)nst * world + 2 * nst + 2) * 8);
-    unsigned long long *dest = sc.ranges.as<unsigned long long>();
-    unsigned long long *d_off = dest + (size_t)nst * world, *d_wpr = d_off + nst + 1;
-    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
-    unsigned long long *hp = sc.h_small + 128; /* pinned staging for the small plan inputs */
-    if ((size_t)(2 * nst + 1) + 128 > 512) return set_err(PSTF_E_INVALID, "too many stores");
-    for (int j = 0; j <= nst; ++j) hp[j] = off[j];
-    for (int j = 0; j < nst; ++j) hp[nst + 1 + j] = wpr[j];
-    CK(cudaMemcpyAsync(d_off, hp, (size_t)(2 * nst + 1) * 8, cudaMemcpyHostToDevice, st));
-    for (int j = 0; j < nst; ++j) {
-        DevStore s = dev_view(stores[j]);
-        uint32_t *h = sc.head.as<uint32_t>() + off[j], *u = sc.uid.as<uint32_t>() + off[j];
-        LAUNCH(k_px_count, grid_for(nw[j] + 1, 256), 256, 0, st, s, h, nw[j]);
-        size_t bytes = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, h, u, (int64_t)(nw[j] + 1), st));
-        ENSURE(sc.cub, bytes);
-        bytes = sc.cub.bytes;
-        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, h, u, (int64_t)(nw[j] + 1), st));
-    }
-    LAUNCH(k_px_plan, 1, 32, 0, st, sc.uid.as<uint32_t>(), d_off, nst, world, d_wpr, dest,
-           reinterpret_cast<long long *>(dev_counts));
-    for (int j = 0; j < nst; ++j) {
-        DevStore s = dev_view(stores[j]);
-        LAUNCH(k_px_write, grid_for(nw[j], 256), 256, 0, st, s, (uint32_t)j,
-               sc.uid.as<uint32_t>() + off[j], nw[j], wpr[j], dest + (size_t)j * world,
-               (PartialRec *)out);
-    }
+    uint32_t *cnt = sc.head.as<uint32_t>(), *scan = sc.scan.as<uint32_t>();
+    const Stores4 S = stores4(stores, nst);
+    LAUNCH(k_live_count, grid_for(words + 1, 256), 256, 0, st, S, nst, wseg, cnt);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, scan, (int64_t)(words + 1), st));
+    ENSURE(sc.cub, tmp);
+    CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, tmp, cnt, scan, (int64_t)(words + 1), st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const unsigned g = std::min<unsigned>(grid_for(std::max(words, bound), 256),
+                                          (unsigned)sm_count() * 8);
+    LAUNCH(k_live_pack, g, 256, 0, st, S, nst, wseg, scan, bound,
+           sc.ulist.as<unsigned long long>(), reinterpret_cast<double4 *>(packed),
+           reinterpret_cast<long long *>(dev_live_total), sc.overflow.as<unsigned long long>());
+    sc.live_bound = bound;
+    sc.live_total_dev = reinterpret_cast<long long *>(dev_live_total);
     return PSTF_OK;
 }
 
-int pstf_partials_export(pstf_field *const *stores, int nst, void *out, uint64_t cap,
-                         uint64_t *counts, void *stream) {
+int pstf_shard_live_unpack(pstf_field *const *stores, int nst, const double *packed,
+                           void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if (!counts) return set_err(PSTF_E_INVALID, "NULL counts");
-    CK(cudaSetDevice(stores[0]->device));
-    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
-    cudaStream_t st = (cudaStream_t)stream;
-    const int world = stores[0]->world;
     Scratch &sc = stores[0]->sc;
-    /* per store: word popcounts -> exclusive scan, all stores side by side on the device; only
-     * the scan values at the rank boundaries come back to the host (one round trip) */
-    std::vector<uint64_t> nw(nst), off(nst + 1, 0);
-    for (int j = 0; j < nst; ++j) {
-        nw[j] = ((uint64_t)stores[j]->d.mask + 1) / 32;
-        off[j + 1] = off[j] + nw[j] + 1;
-    }
-    ENSURE(sc.head, off[nst] * 4);
-    ENSURE(sc.uid, off[nst] * 4);
-    ENSURE(sc.ranges, (size_t)nst * (world + 1) * 8 + 64);
-    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
-    if ((size_t)nst * (world + 1) * 4 > 4096) return set_err(PSTF_E_INVALID, "world too large");
-    uint32_t *hb = reinterpret_cast<uint32_t *>(sc.h_small);
-    for (int j = 0; j < nst; ++j) {
-        DevStore s = dev_view(stores[j]);
-        uint32_t *h = sc.head.as<uint32_t>() + off[j], *u = sc.uid.as<uint32_t>() + off[j];
-        LAUNCH(k_px_count, grid_for(nw[j] + 1, 256), 256, 0, st, s, h, nw[j]);
-        size_t bytes = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, h, u, (int64_t)(nw[j] + 1), st));
-        ENSURE(sc.cub, bytes);
-        bytes = sc.cub.bytes;
-        CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, h, u, (int64_t)(nw[j] + 1), st));
-        const uint64_t wpr = nw[j] / (uint64_t)world;
-        for (int r = 0; r <= world; ++r) /* scan value at each rank's first word */
-            CK(cudaMemcpyAsync(hb + j * (world + 1) + r, u + (uint64_t)r * wpr, 4,
-                               cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
-    std::vector<std::vector<uint64_t>> cnt(nst, std::vector<uint64_t>(world, 0));
-    for (int j = 0; j < nst; ++j)
-        for (int r = 0; r < world; ++r)
-            cnt[j][r] = hb[j * (world + 1) + r + 1] - hb[j * (world + 1) + r];
-    uint64_t total = 0;
-    for (int r = 0; r < world; ++r) {
-        counts[r] = 0;
-        for (int j = 0; j < nst; ++j) counts[r] += cnt[j][r];
-        total += counts[r];
-    }
-    if (total > cap) return set_err(PSTF_E_NOMEM, "partials buffer too small");
-    std::vector<uint64_t> rbase(world, 0);
-    for (int r = 1; r < world; ++r) rbase[r] = rbase[r - 1] + counts[r - 1];
-    std::vector<unsigned long long> db((size_t)nst * world);
-    for (int j = 0; j < nst; ++j)
-        for (int r = 0; r < world; ++r) {
-            uint64_t b = rbase[r];
-            for (int jj = 0; jj < j; ++jj) b += cnt[jj][r];
-            db[(size_t)j * world + r] = b;
-        }
-    CK(cudaMemcpyAsync(sc.ranges.p, db.data(), db.size() * 8, cudaMemcpyHostToDevice, st));
-    for (int j = 0; j < nst; ++j) {
-        DevStore s = dev_view(stores[j]);
-        LAUNCH(k_px_write, grid_for(nw[j], 256), 256, 0, st, s, (uint32_t)j,
-               sc.uid.as<uint32_t>() + off[j], nw[j], nw[j] / (uint64_t)world,
-               sc.ranges.as<unsigned long long>() + (size_t)j * world, (PartialRec *)out);
-    }
-    /* no sync: the pageable db was staged by cudaMemcpyAsync before it returned, and the
-     * caller's counts are host values already */
+    if (!sc.live_total_dev) return set_err(PSTF_E_INVALID, "pstf_shard_live_pack first");
+    if (sc.live_bound && !packed) return set_err(PSTF_E_INVALID, "NULL packed");
+    CK(cudaSetDevice(stores[0]->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = std::min<unsigned>(grid_for(sc.live_bound, 256), (unsigned)sm_count() * 8);
+    if (sc.live_bound)
+        LAUNCH(k_live_unpack, g, 256, 0, st, stores4(stores, nst),
+               sc.ulist.as<unsigned long long>(), reinterpret_cast<const double4 *>(packed),
+               sc.live_total_dev, sc.live_bound);
     return PSTF_OK;
 }
 
-int pstf_partials_import(pstf_field *const *stores, int nst, const void *recs, uint64_t n,
+int pstf_shard_end_frame(pstf_field *const *stores, int nst, const double *packed,
                          void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if (!n) return PSTF_OK;
-    CK(cudaSetDevice(stores[0]->device));
-    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
-    LAUNCH(k_px_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
-           (const PartialRec *)recs, n);
-    return PSTF_OK;
-}
-
-}  /* extern "C" (kernels below) */
-
-__global__ void k_sums_out(Stores4 st, int nst, double *out) {
-    const int i = threadIdx.x;
-    if (i < nst) {
-        out[2 * i] = *st.s[i].cn_sum;
-        out[2 * i + 1] = (double)st.s[i].ctr[C_CN_COUNT];
-    }
-}
-__global__ void k_sums_in(Stores4 st, int nst, const double *in) {
-    const int i = threadIdx.x;
-    if (i < nst) {
-        *st.s[i].cn_sum = in[2 * i];
-        st.s[i].ctr[C_CN_COUNT] = (unsigned long long)in[2 * i + 1];
-    }
-}
-
-extern "C" {
-
-int pstf_end_frame_reduce_dev(pstf_field *const *stores, int nst, double *dev_sum_count,
-                              void *stream) {
-    int rc = shard_checks(stores, nst);
-    if (rc) return rc;
-    if (!dev_sum_count) return set_err(PSTF_E_INVALID, "NULL sum_count");
-    CK(cudaSetDevice(stores[0]->device));
-    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
-    cudaStream_t st = (cudaStream_t)stream;
-    uint64_t maxcap = 0;
-    for (int i = 0; i < nst; ++i) {
-        maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
-        CK(cudaMemsetAsync(&stores[i]->d.ctr[C_EVICTED], 0, 8, st));
-    }
-    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
-    const Stores4 S = stores4(stores, nst);
-    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, S, nst, (const unsigned long long *)nullptr);
-    LAUNCH(k_sums_out, 1, 32, 0, st, S, nst, dev_sum_count);
-    return PSTF_OK;
-}
-
-int pstf_end_frame_reduce(pstf_field *const *stores, int nst, double *sum_cnt, void *stream) {
-    int rc = shard_checks(stores, nst);
-    if (rc) return rc;
-    if (!sum_cnt) return set_err(PSTF_E_INVALID, "NULL sum_cnt");
-    CK(cudaSetDevice(stores[0]->device));
-    for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
-    cudaStream_t st = (cudaStream_t)stream;
-    uint64_t maxcap = 0;
-    for (int i = 0; i < nst; ++i) {
-        maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
-        CK(cudaMemsetAsync(&stores[i]->d.ctr[C_EVICTED], 0, 8, st));
-    }
-    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
-    LAUNCH(k_ef_reduce, g, EF_BLOCK, 0, st, stores4(stores, nst), nst,
-           (const unsigned long long *)nullptr);
+    for (int i = 0; i < nst; ++i)
+        for (int j = 0; j < i; ++j)
+            if (stores[j] == stores[i]) return set_err(PSTF_E_INVALID, "store listed twice");
     Scratch &sc = stores[0]->sc;
-    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
-    for (int i = 0; i < nst; ++i) { /* all values in one round trip */
-        CK(cudaMemcpyAsync(&sc.h_small[2 * i], stores[i]->d.cn_sum, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&sc.h_small[2 * i + 1], &stores[i]->d.ctr[C_CN_COUNT], 8,
-                           cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
-    for (int i = 0; i < nst; ++i) {
-        memcpy(&sum_cnt[2 * i], &sc.h_small[2 * i], 8);
-        sum_cnt[2 * i + 1] = (double)sc.h_small[2 * i + 1];
-    }
-    return PSTF_OK;
-}
-
-static int end_frame_commit_impl(pstf_field *const *stores, int nst, const double *host_sums,
-                                 const double *dev_sums, void *deltas, uint64_t cap,
-                                 uint64_t *ndeltas, void *stream, int64_t *dev_ndeltas = nullptr) {
-    int rc = shard_checks(stores, nst);
-    if (rc) return rc;
-    if ((!host_sums && !dev_sums) || (!ndeltas && !dev_ndeltas))
-        return set_err(PSTF_E_INVALID, "NULL argument");
+    if (!sc.live_total_dev) return set_err(PSTF_E_INVALID, "pstf_shard_live_pack first");
+    if (sc.live_bound && !packed) return set_err(PSTF_E_INVALID, "NULL packed");
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
-    Scratch &sc = stores[0]->sc;
-    if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
-    if (dev_sums) { /* the batch-wide mean c_new of pass 1, straight from the device */
-        LAUNCH(k_sums_in, 1, 32, 0, st, stores4(stores, nst), nst, dev_sums);
-    } else {
-        unsigned long long *hv = sc.h_small + 256; /* pinned staging, used before the sync */
-        for (int i = 0; i < nst; ++i) {
-            memcpy(&hv[2 * i], &host_sums[2 * i], 8);
-            hv[2 * i + 1] = (unsigned long long)host_sums[2 * i + 1];
-            CK(cudaMemcpyAsync(stores[i]->d.cn_sum, &hv[2 * i], 8, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(&stores[i]->d.ctr[C_CN_COUNT], &hv[2 * i + 1], 8,
-                               cudaMemcpyHostToDevice, st));
-        }
-    }
+    static int blocks = -1; /* co-resident blocks per SM of the cooperative kernel */
+    if (blocks < 0)
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_ef_packed, EF_BLOCK, 0));
     uint64_t maxcap = 0;
     for (int i = 0; i < nst; ++i) maxcap = std::max<uint64_t>(maxcap, (uint64_t)stores[i]->d.mask + 1);
-    const unsigned g = std::min<unsigned>(grid_for(maxcap, EF_BLOCK), (unsigned)sm_count() * 8);
+    const unsigned gf = std::min<unsigned>(grid_for(std::max(maxcap, sc.live_bound), EF_BLOCK),
+                                           (unsigned)(sm_count() * std::max(blocks, 1)));
     Stores4 S = stores4(stores, nst);
-    LAUNCH(k_ef_blend, g, EF_BLOCK, 0, st, S, nst, (const unsigned long long *)nullptr);
-    ENSURE(sc.changed, 16);
-    CK(cudaMemsetAsync(sc.changed.p, 0, 8, st));
-    unsigned long long *dcount = (unsigned long long *)sc.changed.p;
-    const bool out = deltas != nullptr && cap > 0;
-    for (int i = 0; i < nst; ++i) {
-        DevStore s = dev_view(stores[i]);
-        if (out) LAUNCH(k_dx_touched, g, EF_BLOCK, 0, st, s, (uint32_t)i, (DeltaRec *)deltas, dcount);
-        const uint64_t per = ((uint64_t)s.mask + 1) / (uint64_t)stores[i]->world; /* owned range */
-        const uint64_t lo = (uint64_t)s.rank * per, hi = lo + per;
-        if (out)
-            LAUNCH(k_ef_evict_range, g, EF_BLOCK, 0, st, s, (uint32_t)i, lo, hi, (DeltaRec *)deltas,
-                   dcount);
+    int nn = nst;
+    const unsigned long long *list = sc.ulist.as<const unsigned long long>();
+    const double4 *pk = reinterpret_cast<const double4 *>(packed);
+    const long long *lt = sc.live_total_dev;
+    uint64_t bound = sc.live_bound;
+    void *args[] = {&S, &nn, &list, &pk, &lt, &bound};
+    {
+        ProfScope ps_("k_ef_packed", st);
+        CK(cudaLaunchCooperativeKernel((const void *)k_ef_packed, gf, EF_BLOCK, args, 0, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    if (!out) LAUNCH(k_ef_evict, g, EF_BLOCK, 0, st, S, nst, 0, (const unsigned long long *)nullptr);
-    LAUNCH(k_ef_finish, 1, 32, 0, st, S, nst);
-    for (int i = 0; i < nst; ++i) stores[i]->frame += 1;
-    if (dev_ndeltas) { /* no host round trip; cap covers every owned slot (checked by caller) */
-        LAUNCH(k_count_out, 1, 32, 0, st, dcount, cap, reinterpret_cast<long long *>(dev_ndeltas));
-        return PSTF_OK;
+    for (int i = 0; i < nst; ++i) { /* the phase-1 touch marks of this replica */
+        CK(cudaMemsetAsync(stores[i]->d.tbits, 0, (((uint64_t)stores[i]->d.mask + 32) / 32) * 4, st));
+        stores[i]->frame += 1;
     }
-    CK(cudaMemcpyAsync(sc.h_small, dcount, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const unsigned long long nd = sc.h_small[0];
-    if (out && nd > cap) return set_err(PSTF_E_NOMEM, "deltas buffer overflow");
-    *ndeltas = nd;
     return PSTF_OK;
 }
 
-int pstf_end_frame_commit(pstf_field *const *stores, int nst, const double *global_sum_cnt,
-                          void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
-    return end_frame_commit_impl(stores, nst, global_sum_cnt, nullptr, deltas, cap, ndeltas,
-                                 stream);
-}
-
-int pstf_end_frame_commit_dev(pstf_field *const *stores, int nst, const double *dev_sum_count,
-                              void *deltas, uint64_t cap, uint64_t *ndeltas, void *stream) {
-    return end_frame_commit_impl(stores, nst, nullptr, dev_sum_count, deltas, cap, ndeltas,
-                                 stream);
-}
-int pstf_end_frame_commit_async(pstf_field *const *stores, int nst, const double *dev_sum_count,
-                                void *deltas, uint64_t cap, int64_t *dev_ndeltas, void *stream) {
-    if (!deltas || !dev_ndeltas) return set_err(PSTF_E_INVALID, "NULL argument");
-    uint64_t owned = 0; /* deltas are the owned touched or evicted slots: at most every one */
-    for (int i = 0; i < nst; ++i)
-        if (stores[i]) owned += ((uint64_t)stores[i]->d.mask + 1) / (uint64_t)std::max(1, stores[i]->world);
-    if (cap < owned) return set_err(PSTF_E_INVALID, "deltas buffer smaller than the owned slots");
-    return end_frame_commit_impl(stores, nst, nullptr, dev_sum_count, deltas, cap, nullptr,
-                                 stream, dev_ndeltas);
-}
-
-int pstf_deltas_import(pstf_field *const *stores, int nst, const void *deltas, uint64_t n,
-                       void *stream) {
+int pstf_shard_info(pstf_field *const *stores, int nst, int64_t *dev_out3, void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
-    if (!n) return PSTF_OK;
+    if (!dev_out3) return set_err(PSTF_E_INVALID, "NULL argument");
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
-    LAUNCH(k_dx_import, grid_for(n, 256), 256, 0, (cudaStream_t)stream, stores4(stores, nst),
-           (const DeltaRec *)deltas, n);
+    Scratch &sc = stores[0]->sc;
+    ENSURE(sc.overflow, 8);
+    if (!sc.overflow_zeroed) {
+        CK(cudaMemsetAsync(sc.overflow.p, 0, 8, (cudaStream_t)stream));
+        sc.overflow_zeroed = true;
+    }
+    LAUNCH(k_shard_info, 1, 32, 0, (cudaStream_t)stream, stores4(stores, nst), nst,
+           sc.pend_count.as<unsigned long long>(), sc.pend.bytes / sizeof(PendRec),
+           sc.overflow.as<unsigned long long>(), reinterpret_cast<long long *>(dev_out3));
     return PSTF_OK;
 }
 
 uint64_t pstf_pending_record_bytes(void) { return sizeof(PendRec); }
-uint64_t pstf_partial_record_bytes(void) { return sizeof(PartialRec); }
-uint64_t pstf_delta_record_bytes(void) { return sizeof(DeltaRec); }
 
 } // extern "C"
 

@@ -1332,7 +1332,6 @@ int pstf_model_end_frame(pstf_model_store *m, void *stream) {
     const int limited = t_max > 0.0 && std::isfinite(t_max);
     CK(cudaMemsetAsync(m->sums.p, 0, 16, st));
     LAUNCH(k_mdl_sums, (unsigned)sm_count() * 2, 256, 0, st, d, m->sums.as<double>());
-    const uint64_t cap = (uint64_t)m->mask + 1;
     if (m->cfg.kind == PSTF_MODEL_GMM) {
         const uint64_t bound = m->fs_bound, cap2 = (uint64_t)m->mask + 1;
         uint32_t *pos_sorted = nullptr;

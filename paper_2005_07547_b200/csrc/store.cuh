@@ -12,6 +12,8 @@
  *   tbits u32[cap/32]    touched-this-frame bitmap: a slot's first touch in a frame (seen via
  *                       meta.y != frame + 1) sets its bit with a fire-and-forget RED.OR
  *   tlist u32[cap]       endFrame compacts the bitmap into this list and blends only those slots
+ *   lbits u32[cap/32]    live bitmap (checksum != 0), kept by placement and eviction: the
+ *                       multi-GPU path packs the live slots from it
  *   hold  u32[2][cap]   deterministic-placement scratch (rank of the proposing key, ~0 = none)
  */
 #pragma once
@@ -49,6 +51,7 @@ struct DevStore {
     double4 *acc;
     KeyFields *keyf;
     uint32_t *tbits;
+    uint32_t *lbits; // live bitmap (meta.x != 0): set at placement, cleared at eviction
     uint32_t *tlist;
     uint32_t *hold0, *hold1;
     unsigned long long *hold64_0, *hold64_1; /* 64-bit priority holds (sort-free ATOMIC phase 2),
@@ -62,8 +65,7 @@ struct DevStore {
     uint32_t blend;
     uint32_t evict_age;
     uint32_t frame;       // uint32_t(m_frame) for this launch
-    int32_t rank;         // key-owner sharding: this rank (0 when not sharded)
-    uint32_t owner_shift; // owner(slot) = slot >> owner_shift (capacity_log2 - log2 world)
+    int32_t rank;         // multi-GPU: this rank (origin tag of pending records; 0 unsharded)
 };
 
 /* the members of a store that a contribution touches, selectable per loop iteration */
@@ -80,9 +82,6 @@ __device__ __forceinline__ StoreRef store_ref(const DevStore &s) {
     return StoreRef{s.meta, s.acc, s.tbits, s.ctr, s.frame, s.rank};
 }
 
-__device__ __forceinline__ bool owned(const DevStore &s, uint32_t slot) {
-    return (int32_t)(slot >> s.owner_shift) == s.rank;
-}
 
 #define PSTF_HOLD_NONE 0xffffffffu
 

@@ -1,7 +1,7 @@
-"""Fixed cost of the key-owner-sharded iteration (paper_2005_07547_b200.shard) on one GPU: a
-world-size-1 NCCL group runs the whole protocol (collectives degenerate to copies), compared
-with the plain single-GPU step.  Upper bound on what the protocol adds per rank besides the
-data exchange itself."""
+"""Fixed cost of the multi-GPU iteration (paper_2005_07547_b200.shard) on one GPU: a world-size-1
+NCCL group runs the whole protocol (collectives degenerate to copies), compared with the plain
+single-GPU step, plus a synchronised per-phase breakdown and the bytes each collective moves
+(the inputs of the N-GPU projection in DESIGN.md section 6)."""
 import math
 import os
 import sys
@@ -61,17 +61,19 @@ def t(name, fn):
 
 
 K = 8
+from paper_2005_07547_b200.shard import PENDING_BYTES  # noqa: E402
 for i in range(K):
     t("vertex_pass_local", lambda: b.vertex_pass_local((bufs[i % 8], n)))
-    recs = t("pending+allgather", lambda: c.all_gather_bytes(b.pending_bytes()))
+    info = t("sync (all_gather_vec + host read)", lambda: c.all_gather_vec(b.sync_vector()))
+    pend = [int(r[0]) for r in info]
+    recs = t("pending all_gather", lambda: c.gather_known(b.pending_bytes_n(pend[0] * PENDING_BYTES),
+                                                          [p * PENDING_BYTES for p in pend]))
     t("resolve", lambda: b.resolve(recs))
-    out, counts = t("partials_export", lambda: b.partials_export())
-    recv = t("all_to_all", lambda: c.all_to_all_bytes(out, counts, 40)[0])
-    t("partials_import", lambda: b.partials_import(recv))
-    sums = t("ef_reduce+allreduce", lambda: c.all_reduce_sum(b.end_frame_reduce()))
-    deltas = t("ef_commit", lambda: b.end_frame_commit(sums))
-    g = t("deltas_allgather", lambda: c.all_gather_bytes(deltas))
-    t("deltas_import", lambda: b.deltas_import(g))
+    bound = int(info[0][1]) + sum(pend)
+    packed = t("live pack", lambda: b.pack(bound))
+    t("all_reduce", lambda: c.all_reduce_sum(packed))
+    t("end_frame from the packed sums", lambda: b.commit(packed))
+print(f"  live slots packed per frame {bound}, all-reduce payload {bound * 32 / 1e6:.1f} MB")
 for k, v in acc.items():
     print(f"  {k:22s} {v / K:.3f} ms")
 dist.destroy_process_group()

@@ -1,19 +1,16 @@
-"""CPU reference backend for the sharding protocol (TEST INFRASTRUCTURE ONLY).
+"""CPU reference backend for the multi-GPU protocol (TEST INFRASTRUCTURE ONLY).
 
 Implements the operations of paper_2005_07547_b200.shard.CudaBackend on numpy replicas of the
 Lo / Lo\\E / FLi stores, with the reference semantics (keys and levels from the C restatement in
-oracle/, sequential insertion in key order, field.cpp endFrame) and the same record byte layouts,
-so tests/test_shard_gloo.py can run the multi-rank protocol with gloo on CPU and compare the
-result with a single-process oracle run."""
+oracle/, sequential insertion in key order, field.cpp:197-263 endFrame) and the same pending
+record layout and live-slot packing order, so tests/test_shard_gloo.py can run the multi-rank
+protocol with gloo on CPU and compare the result with a single-process oracle run."""
 import numpy as np
 
 import pyoracle as po
 
 PEND_DT = np.dtype([("k", "<i4", (6,)), ("cs", "<u4"), ("meta", "<u4"), ("v", "<f8", (4,))])
-PART_DT = np.dtype([("store", "<u4"), ("slot", "<u4"), ("acc", "<f8", (4,))])
-DELTA_DT = np.dtype([("store", "<u4"), ("slot", "<u4"), ("chk", "<u4"), ("lastb", "<u4"),
-                     ("com", "<f8", (4,))])
-assert PEND_DT.itemsize == 64 and PART_DT.itemsize == 40 and DELTA_DT.itemsize == 48
+assert PEND_DT.itemsize == 64
 M64 = (1 << 64) - 1
 
 
@@ -50,10 +47,7 @@ class Replica:
         self.live = 0
         self.dropped = 0
         self.rank = rank
-        self.shift = cfg.capacity_log2 - (world.bit_length() - 1)
-
-    def owned(self, slot):
-        return (slot >> self.shift) == self.rank
+        self.internal = 0
 
     def touch(self, slot):
         self.lastb[slot] = (self.frame + 1) & 0xffffffff
@@ -170,8 +164,14 @@ class CpuBackend:
                     rep.dropped += int(calls[i])
         self.pending = np.concatenate(recs) if recs else np.zeros(0, PEND_DT)
 
-    def pending_bytes(self):
+    def sync_vector(self):
         import torch
+        return torch.tensor([len(self.pending), sum(r.live for r in self.reps), 0],
+                            dtype=torch.int64)
+
+    def pending_bytes_n(self, nbytes):
+        import torch
+        assert nbytes == self.pending.nbytes
         return torch.from_numpy(self.pending.view(np.uint8).copy())
 
     # ---------------------------------------------------------------- placement
@@ -208,53 +208,45 @@ class CpuBackend:
                     continue
                 for i in own:
                     rep.acc[target] += recs["v"][i]
-                if own_calls or rep.owned(target):
+                if own_calls:
                     rep.touch(target)
 
     # ---------------------------------------------------------------- exchange
-    def partials_export(self):
+    def pack(self, bound):
+        """accumulators of the live slots in (store, slot) order, zero-padded to bound"""
         import torch
-        per_dest = [[] for _ in range(self.world)]
-        for s, rep in enumerate(self.reps):
-            for slot in np.nonzero(rep.touched)[0]:
-                if rep.owned(slot):
-                    continue
-                r = np.zeros(1, PART_DT)
-                r["store"], r["slot"], r["acc"] = s, slot, rep.acc[slot]
-                per_dest[slot >> rep.shift].append(r)
-                rep.acc[slot] = 0.0
-                rep.touched[slot] = False
-        counts = [len(x) for x in per_dest]
-        flat = [r for d in per_dest for r in d]
-        arr = np.concatenate(flat) if flat else np.zeros(0, PART_DT)
-        return torch.from_numpy(arr.view(np.uint8).copy()), counts
+        self.plist = [(s, int(slot)) for s, rep in enumerate(self.reps)
+                      for slot in np.nonzero(rep.chk)[0]]
+        assert len(self.plist) <= bound
+        out = np.zeros((bound, 4))
+        for i, (s, slot) in enumerate(self.plist):
+            out[i] = self.reps[s].acc[slot]
+        return torch.from_numpy(out.reshape(-1))
 
-    def partials_import(self, recs_t):
-        recs = np.frombuffer(recs_t.numpy().tobytes(), PART_DT)
-        for r in recs:
-            rep = self.reps[r["store"]]
-            assert rep.owned(int(r["slot"]))
-            rep.acc[r["slot"]] += r["acc"]
-            rep.touch(int(r["slot"]))
+    def unpack(self, packed):
+        v = packed.numpy().reshape(-1, 4)
+        for i, (s, slot) in enumerate(self.plist):
+            rep = self.reps[s]
+            rep.acc[slot] = v[i]
+            if (v[i] != 0).any():
+                rep.touch(slot)
 
     # ---------------------------------------------------------------- endFrame
-    def end_frame_reduce(self):
-        out = []
-        for rep in self.reps:
-            rep.live_snap = rep.live
-            cn = rep.acc[rep.touched, 3]
-            out += [float(cn[cn > 0].sum()), float((cn > 0).sum())]
-        return np.array(out)
+    def commit(self, packed):
+        self.unpack(packed)
+        self.end_frame()
 
-    def end_frame_commit(self, sums):
-        import torch
-        deltas = []
-        for s, rep in enumerate(self.reps):
-            mean = sums[2 * s] / sums[2 * s + 1] if sums[2 * s + 1] > 0 else 0.0
+    def end_frame(self):
+        """field.cpp:197-263 on every store (all slots; untouched ones have zero accumulators)"""
+        for rep in self.reps:
+            live_snap = rep.live
+            cn_all = rep.acc[:, 3]
+            pos = (rep.chk != 0) & (cn_all > 0)
+            mean = float(cn_all[pos].sum()) / pos.sum() if pos.any() else 0.0
             T = rep.cfg.t_max
             limited = T > 0 and np.isfinite(T)
             cap = (T * T - T) * mean if limited else 0.0
-            for slot in np.nonzero(rep.touched)[0]:
+            for slot in np.nonzero(rep.chk)[0]:
                 a = rep.acc[slot]
                 cn = a[3]
                 if cn > 0:
@@ -267,37 +259,15 @@ class CpuBackend:
                     c[3] = c[3] + cn
                     if limited:
                         c[3] = cap if cap < c[3] else c[3]
+                elif (a[:3] != 0).any():
+                    rep.internal += 1
                 rep.acc[slot] = 0.0
-                d = np.zeros(1, DELTA_DT)
-                d["store"], d["slot"], d["chk"], d["lastb"], d["com"] = (s, slot, rep.chk[slot],
-                                                                         rep.lastb[slot],
-                                                                         rep.com[slot])
-                deltas.append(d)
-            if rep.live_snap * 4 > rep.cap * 3:
-                lo = rep.rank << rep.shift
-                for slot in range(lo, lo + (1 << rep.shift)):
-                    if rep.chk[slot] != 0 and ((rep.frame - (int(rep.lastb[slot]) - 1)) &
-                                               0xffffffff) >= rep.cfg.evict_age_frames:
+            if live_snap * 4 > rep.cap * 3:
+                for slot in np.nonzero(rep.chk)[0]:
+                    if ((rep.frame - (int(rep.lastb[slot]) - 1)) & 0xffffffff) >= \
+                            rep.cfg.evict_age_frames:
                         rep.chk[slot] = 0
                         rep.com[slot] = 0.0
                         rep.live -= 1
-                        d = np.zeros(1, DELTA_DT)
-                        d["store"], d["slot"], d["lastb"] = s, slot, rep.lastb[slot]
-                        deltas.append(d)
             rep.touched[:] = False
             rep.frame += 1
-        arr = np.concatenate(deltas) if deltas else np.zeros(0, DELTA_DT)
-        return torch.from_numpy(arr.view(np.uint8).copy())
-
-    def deltas_import(self, recs_t):
-        recs = np.frombuffer(recs_t.numpy().tobytes(), DELTA_DT)
-        for d in recs:
-            rep = self.reps[d["store"]]
-            slot = int(d["slot"])
-            if rep.owned(slot):
-                continue
-            if rep.chk[slot] != 0 and d["chk"] == 0:
-                rep.live -= 1
-            rep.chk[slot] = d["chk"]
-            rep.lastb[slot] = d["lastb"]
-            rep.com[slot] = d["com"]

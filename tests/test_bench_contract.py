@@ -58,5 +58,15 @@ def test_sharded_branch_on_one_rank():
     sizes, sharded e2e) run as a one-rank group: it must complete and print a valid line"""
     d = _line(SMALL + ["--force-sharded", "--no-cpu-baseline", "--e2e-steps", "2"])
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert "sharded by key owner" in d["config"]["parallelism"]
+    assert "all-reduced" in d["config"]["parallelism"]
 
+
+
+def test_reference_arm_config_matches_b200_arm():
+    """both arms print the same `config` object for the same command line (the driver compares
+    them), and the B200 line names its arm"""
+    b = _line(SMALL + ["--no-e2e", "--no-cpu-baseline"])
+    r = _line(SMALL + ["--impl", "reference"])
+    assert b["impl"] == "b200" and r["impl"] == "reference"
+    if "unavailable" not in r:
+        assert b["config"] == r["config"]

@@ -1,6 +1,8 @@
-"""Multi-rank key-owner sharding protocol (paper_2005_07547_b200.shard) on CPU: world size 2
-(and 4) over gloo with the CPU reference backend.  After several frames every rank's replica
-must be identical, and equal to the single-process reference semantics (the C restatement's
+"""Multi-rank protocol of the field cache (paper_2005_07547_b200.shard) on CPU: world size 2
+(and 4) over gloo with the numpy reference backend (tests/shard_cpu_backend.py): each rank runs
+phase 1 on its image stripe, the ranks place the union of new keys identically, all-reduce the
+live slots' accumulators and run endFrame.  After several frames every rank's replica must be
+identical, and equal to the single-process reference semantics (the C restatement's
 deterministic onVertex over the whole frame): occupancy, keys, ages and c_old exactly, values to
 1e-9 (summation order differs)."""
 import os
@@ -95,26 +97,33 @@ def test_sharded_protocol_matches_single_rank_semantics(tmp_path, world, cap, ev
         assert sum(rr["dropped"][s] for rr in res) == ref[s].stats()["dropped"]
 
 
-def _counted_worker(rank, world, port, outdir):
+def _gather_worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path[:0] = [os.path.join(HERE, "..")]
     from paper_2005_07547_b200.shard import Collectives
     c = Collectives(dist, "cpu")
-    n = 64 * (rank + 1) if rank != 1 else 0  # unequal sizes, one empty
-    payload = (torch.arange(n, dtype=torch.int64) % 251 + rank).to(torch.uint8)
-    got = c.all_gather_counted(torch.tensor([n], dtype=torch.int64), lambda m: payload[:m])
-    torch.save(got, os.path.join(outdir, f"g{rank}.pt"))
+    info = c.all_gather_vec(torch.tensor([rank * 10 + 1, 7, rank], dtype=torch.int64))
+    sizes = [64 * (r + 1) if r != 1 else 0 for r in range(world)]  # unequal, one empty
+    payload = (torch.arange(sizes[rank], dtype=torch.int64) % 251 + rank).to(torch.uint8)
+    got = c.gather_known(payload, sizes)
+    x = torch.full((5,), float(rank + 1), dtype=torch.float64)
+    c.all_reduce_sum(x)
+    torch.save({"info": info, "got": got, "sum": x}, os.path.join(outdir, f"g{rank}.pt"))
     dist.destroy_process_group()
 
 
-def test_all_gather_counted_gloo(tmp_path):
-    """the device-count variable-length all-gather the CUDA path uses (one host sync per
-    exchange), here over gloo with CPU tensors: rank order, unequal and empty contributions"""
+def test_collectives_gloo(tmp_path):
+    """the protocol's collectives over gloo with CPU tensors: the small-vector all-gather that
+    carries the frame's one host read, the known-size byte all-gather (rank order, unequal and
+    empty contributions) and the in-place all-reduce"""
     world = 3
-    mp.spawn(_counted_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_gather_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     want = torch.cat([(torch.arange(64 * (r + 1) if r != 1 else 0, dtype=torch.int64) % 251 + r)
                       .to(torch.uint8) for r in range(world)])
     for r in range(world):
-        assert torch.equal(torch.load(os.path.join(tmp_path, f"g{r}.pt")), want)
+        d = torch.load(os.path.join(tmp_path, f"g{r}.pt"))
+        assert d["info"] == [[q * 10 + 1, 7, q] for q in range(world)]
+        assert torch.equal(d["got"], want)
+        assert torch.equal(d["sum"], torch.full((5,), 6.0, dtype=torch.float64))
