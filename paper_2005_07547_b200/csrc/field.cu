@@ -173,6 +173,7 @@ struct Scratch {
     DBuf winner;                            // snapshot restore: last record per slot
     DBuf hio;                               // host-pointer API staging
     DBuf ulist, overflow;                   // sharding: packed live list, pack-overflow flag
+    DBuf ef_done;                           // one-pass endFrame: blocks done (last rolls)
     uint64_t live_bound = 0;
     long long *live_total_dev = nullptr;
     bool overflow_zeroed = false;
@@ -209,6 +210,10 @@ struct pstf_field {
     DBuf hold64;                  /* 2 x capacity 64-bit priority holds (sort-free phase 2) */
     DeferredPass dp;              /* owned by the Lo store of a deferred vertex pass */
     pstf_field *owed_by = nullptr; /* the Lo store whose deferred pass involves this store */
+    /* every update of the current frame carried unit counter weights and was counted in
+     * C_F_CN (tiled ATOMIC vertex passes + their placement): endFrame may run in one pass
+     * (k_ef_onepass + k_ef_tail).  Any other update path clears it until the next endFrame. */
+    bool unit_frame = true;
     ~pstf_field() {
         if (dp.ev) cudaEventDestroy(dp.ev);
         if (dp.h_count) cudaFreeHost(dp.h_count);
@@ -255,7 +260,7 @@ __device__ __forceinline__ bool lookup_level_chain(const DevStore &s, double px,
         Key k = key_for(s.kp, px, py, pz, dx, dy, dz, l);
         int idx = probe_find(s, (uint32_t)key_pack(k) & s.mask, k.checksum);
         if (idx >= 0) {
-            double4 c = s.com[idx];
+            double4 c = ld4_ro(com_ptr(s, idx));
             if (c.w > 0.0) {
                 *val = make_double3(c.x, c.y, c.z);
                 *lev_out = l;
@@ -381,7 +386,7 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
             const int rs = rsm[cell];
             const double val = flat[4 * cell + comp];
             const bool on = rs >= 0 && val != 0.0;
-            if (on) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+            if (on) atomicAdd(reinterpret_cast<double *>(acc_ptr(s, rs)) + comp, val);
             cnt += on;
         }
         if (nred) *nred += cnt;
@@ -390,7 +395,7 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
     } else if (__all_sync(0xffffffffu, peers == (1u << lane))) {
         /* no two lanes share a slot: one RED per component, no shared-memory round trip */
         if (res >= 0) {
-            if (do_red) red_add4(&s.acc[res], v);
+            if (do_red) red_add4(acc_ptr(s, res), v);
             touch_slot(s, (uint32_t)res, mark);
         }
     } else {
@@ -408,7 +413,7 @@ __device__ __forceinline__ void apply_contribution(const Store &s, const PendSin
                 t.z += x.z;
                 t.w += x.w;
             }
-            if (do_red) red_add4(&s.acc[res], t);
+            if (do_red) red_add4(acc_ptr(s, res), t);
             touch_slot(s, (uint32_t)res, mark);
         }
         __syncwarp();
@@ -438,7 +443,7 @@ __device__ __forceinline__ void count_call(const DevStore &s, const PendSink &a,
     uint32_t mark = 0;
     if (want) res = probe_existing(s, k.pack_lo & s.mask, k.checksum, &mark);
     if (res >= 0) {
-        atomicAdd(&s.acc[res].w, 1.0);
+        atomicAdd(&acc_ptr(s, res)->w, 1.0);
         touch_slot(s, (uint32_t)res, mark);
     }
     if (PendRec *p = warp_reserve(a, res == -1))
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
                     if (!doneLo) {
                         int idx = probe_find(sLo, (uint32_t)pk & sLo.mask, k.checksum);
                         if (idx >= 0) {
-                            double4 c = sLo.com[idx];
+                            double4 c = ld4_ro(com_ptr(sLo, idx));
                             if (c.w > 0.0) {
                                 loNext = make_double3(c.x, c.y, c.z);
                                 doneLo = true;
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
                     if (!doneLoe) {
                         int idx = probe_find(sLoe, (uint32_t)pk & sLoe.mask, k.checksum);
                         if (idx >= 0) {
-                            double4 c = sLoe.com[idx];
+                            double4 c = ld4_ro(com_ptr(sLoe, idx));
                             if (c.w > 0.0) {
                                 loeNext = make_double3(c.x, c.y, c.z);
                                 doneLoe = true;
@@ -843,7 +848,7 @@ struct NoPipe {
 
 template <bool CV, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
-                                            double4 *sm, uint32_t &nred,
+                                            double4 *sm, uint32_t &nred, uint64_t &ef_cn,
                                             const Pipe &pipe = Pipe()) {
     const DevStore &sLo = a.st.s[0];
     const DevStore &sLoe = a.st.s[1];
@@ -875,7 +880,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
     uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
     uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
-    double4 sl = look ? sLo.com[ql] : z4, se = look ? sLoe.com[qe] : z4;
+    double4 sl = look ? ld4_ro(com_ptr(sLo, ql)) : z4, se = look ? ld4_ro(com_ptr(sLoe, qe)) : z4;
 
     /* ---- the update keys: one level, one cell triple, one packKeyFields prefix ---- */
     int level = select_level_try(fq, S.f(PS_FP), &nx);
@@ -908,8 +913,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         qe = (uint32_t)qpk & sLoe.mask;
         wl = look ? sLo.meta[ql].x : 0u;
         we = look ? sLoe.meta[qe].x : 0u;
-        sl = look ? sLo.com[ql] : z4;
-        se = look ? sLoe.com[qe] : z4;
+        sl = look ? ld4_ro(com_ptr(sLo, ql)) : z4;
+        se = look ? ld4_ro(com_ptr(sLoe, qe)) : z4;
     }
     pipe.key_inputs_done();
     const uint64_t h1 = pack_h1(level, c0, c1);
@@ -931,7 +936,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 m3b = has3 ? sFli.meta[(h3 + 1) & sFli.mask] : z;
 #endif
     /* CV lookup at this vertex = Lo\E query of the Lo key: speculate its home record too */
-    const double4 scv = CV && live ? sLoe.com[h1s] : z4;
+    const double4 scv = CV && live ? ld4_ro(com_ptr(sLoe, h1s)) : z4;
 
     double3 loNext = make_double3(0.0, 0.0, 0.0), loeNext = make_double3(0.0, 0.0, 0.0);
     if (look) {
@@ -973,8 +978,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                     if (l == l0 && homeLoe) ie = -1;
                     else ie = resolve_find(sLoe, he, ccs, l == l0 ? we : sLoe.meta[he].x);
                 }
-                const double4 cl = il >= 0 ? sLo.com[il] : z4;
-                const double4 ce = ie >= 0 ? sLoe.com[ie] : z4;
+                const double4 cl = il >= 0 ? ld4_ro(com_ptr(sLo, il)) : z4;
+                const double4 ce = ie >= 0 ? ld4_ro(com_ptr(sLoe, ie)) : z4;
                 if (il >= 0 && cl.w > 0.0) {
                     loNext = make_double3(cl.x, cl.y, cl.z);
                     doneLo = true;
@@ -1018,7 +1023,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         double3 cv = make_double3(0.0, 0.0, 0.0);
         bool ok = false;
         if (r1 >= 0) {
-            const double4 c = r1 == (int)h1s ? scv : sLoe.com[r1];
+            const double4 c = r1 == (int)h1s ? scv : ld4_ro(com_ptr(sLoe, r1));
             ok = c.w > 0.0;
             if (ok) cv = make_double3(c.x, c.y, c.z);
         }
@@ -1037,7 +1042,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 pack_key_fields(l, a0, a1, a2, dir_cell_f8(fo.u, l), dir_cell_f8(fo.v, l));
             const int idx = probe_find(sLoe, (uint32_t)pk & sLoe.mask, checksum_of(pk));
             if (idx >= 0) {
-                const double4 c = sLoe.com[idx];
+                const double4 c = ld4_ro(com_ptr(sLoe, idx));
                 ok = c.w > 0.0;
                 if (ok) cv = make_double3(c.x, c.y, c.z);
             }
@@ -1142,13 +1147,18 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                          "@p red.relaxed.gpu.global.add.f64 [%0], %1;\n\t}" ::"l"(dst),
                          "d"(val), "r"((uint32_t)on));
 #else
-            if (on) atomicAdd(reinterpret_cast<double *>(&s.acc[rs]) + comp, val);
+            if (on) atomicAdd(reinterpret_cast<double *>(acc_ptr(s, rs)) + comp, val);
 #endif
             cnt += on;
         }
         nred += cnt;
         __syncwarp();
-        if (res >= 0) touch_slot(s, (uint32_t)res, mark);
+        /* unit-weight frame accounting (k_ef_onepass): one counter call of weight 1 per
+         * contribution with a slot; 16-bit fields per store */
+        if (res >= 0) {
+            touch_slot(s, (uint32_t)res, mark);
+            ef_cn += 1ull << (16 * sid);
+        }
         if (PendRec *p = warp_reserve(ps, res == -1)) { /* a new key (rare after warm-up) */
             const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
             put_record(p, k, PSTF_META(sid, 0, nc) | ((uint32_t)s.rank << 3), v.x, v.y, v.z, v.w);
@@ -1202,6 +1212,15 @@ __global__ void __launch_bounds__(VT, MINB)
                 }
         }
     uint32_t it = 0, nred = 0;
+    uint64_t ef_cn = 0; /* per-store 16-bit counters, flushed every 1024 tiles */
+    const auto flush_ef = [&]() {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)(ef_cn >> (16 * q)) & 0xffffu);
+            if ((tid & 31) == 0 && c) atomicAdd(&a.st.s[q].ctr[C_F_CN], (unsigned long long)c);
+        }
+        ef_cn = 0;
+    };
     const uint64_t ntiles = (a.n + VT - 1) / VT;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = (int)(it % STAGES);
@@ -1234,11 +1253,13 @@ __global__ void __launch_bounds__(VT, MINB)
         if (PSTF_VP_DBG_BUILD & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body<CV>(a, src, live, sm, nred);
+            vertex_body<CV>(a, src, live, sm, nred, ef_cn);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
+        if ((it & 1023u) == 1023u) flush_ef();
     }
+    flush_ef();
     /* RED element updates issued (atomic-roofline accounting, one atomic per warp) */
     for (int o = 16; o; o >>= 1) nred += __shfl_xor_sync(0xffffffffu, nred, o);
     if ((tid & 31) == 0 && nred) atomicAdd(&a.st.s[0].ctr[C_REDS], (unsigned long long)nred);
@@ -1299,7 +1320,7 @@ __global__ void k_apply_atomic(ApplyArgs a, PendRec *pend, unsigned long long *p
     uint32_t mark = 0;
     int res = probe_existing(a.s, (uint32_t)pk & a.s.mask, k.checksum, &mark);
     if (res >= 0) {
-        red_add4(&a.s.acc[res], v);
+        red_add4(acc_ptr(a.s, res), v);
         touch_slot(a.s, (uint32_t)res, mark);
     } else if (res == -2) {
         atomicAdd(&a.s.ctr[C_DROPPED], 1ull);
@@ -1867,7 +1888,7 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
     }
     if (atomic_mode) {
         double4 v = usum[u];
-        double4 *dst = &s.acc[slot];
+        double4 *dst = acc_ptr(s, slot);
         if (v.x != 0.0) atomicAdd(&dst->x, v.x);
         if (v.y != 0.0) atomicAdd(&dst->y, v.y);
         if (v.z != 0.0) atomicAdd(&dst->z, v.z);
@@ -1875,7 +1896,11 @@ __global__ void k_commit(PlaceArgs a, const unsigned long long *res, const KeyFi
     }
     /* sharded: a replica touches a slot for its own records only (the all-reduce of the
      * accumulators marks the slots the other ranks touched) */
-    if (ucalls[u] != 0) touch_slot(s, slot);
+    if (ucalls[u] != 0) {
+        /* unit-weight frame accounting (k_ef_onepass): the counter calls of these records */
+        touch_slot(s, slot);
+        if (atomic_mode) atomicAdd(&s.ctr[C_F_CN], (unsigned long long)usum[u].w);
+    }
 }
 
 /* ORDERED / SEQUENTIAL: per-record fold target (store << 32 | slot), dropped -> ~0 */
@@ -1959,7 +1984,7 @@ __global__ void k_fold(const double4 *__restrict__ T, const uint8_t *__restrict_
     if (t == ~0ull) return;
     const DevStore &s = st.s[t >> 32];
     const uint32_t slot = (uint32_t)t;
-    double4 acc = s.acc[slot];
+    double4 acc = *acc_ptr(s, slot);
     uint32_t q = q0;
     for (; q + 8 <= q1; q += 8) {
         double4 v[8];
@@ -1973,7 +1998,7 @@ __global__ void k_fold(const double4 *__restrict__ T, const uint8_t *__restrict_
         for (int k = 0; k < 8; ++k) fold_one(acc, v[k], c[k]);
     }
     for (; q < q1; ++q) fold_one(acc, T[q], isc[q] != 0);
-    s.acc[slot] = acc;
+    *acc_ptr(s, slot) = acc;
 }
 
 /* the long runs, one warp each: lanes load 32 consecutive terms (one memory latency per 32
@@ -1993,7 +2018,7 @@ __global__ void k_fold_long(const double4 *__restrict__ T, const uint8_t *__rest
         if (t == ~0ull) continue;
         const DevStore &s = st.s[t >> 32];
         const uint32_t slot = (uint32_t)t;
-        double4 acc = s.acc[slot];
+        double4 acc = *acc_ptr(s, slot);
         double4 nv = q0 + lane < q1 ? T[q0 + lane] : make_double4(0.0, 0.0, 0.0, 0.0);
         int nc = q0 + lane < q1 ? isc[q0 + lane] : 0;
         for (uint32_t b = q0; b < q1; b += 32) {
@@ -2017,7 +2042,7 @@ __global__ void k_fold_long(const double4 *__restrict__ T, const uint8_t *__rest
                 if (l < k) fold_one(acc, u, cu != 0);
             }
         }
-        if (lane == 0) s.acc[slot] = acc;
+        if (lane == 0) *acc_ptr(s, slot) = acc;
     }
 }
 
@@ -2128,7 +2153,7 @@ __device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst) {
                 w &= w - 1;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) cn[q] = sl[q] != 0xffffffffu ? s.acc[sl[q]].w : 0.0;
+            for (int q = 0; q < 8; ++q) cn[q] = sl[q] != 0xffffffffu ? acc_ptr(s, sl[q])->w : 0.0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (sl[q] != 0xffffffffu) {
@@ -2172,13 +2197,20 @@ __device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst) {
 }
 
 /* the blend of one slot with c_new > 0 (field.cpp:218-241): candidate, alpha with the 1/T floor,
- * mix, cOld capped at (T^2 - T) * mean c_new (the store's Σc_new / count of this frame) */
-__device__ __forceinline__ double4 blend_one(const DevStore &s, double4 a, double4 c) {
+ * mix, cOld capped at (T^2 - T) * mean c_new; mean: the frame's Σc_new / count, read from the
+ * store's reduce-pass scratch unless given (use_mean); with use_mean false and mean 0 the cap is
+ * skipped (callers that know it cannot apply) */
+__device__ __forceinline__ double4 blend_one(const DevStore &s, double4 a, double4 c,
+                                            double mean = 0.0, bool use_mean = false,
+                                            bool from_scratch = true) {
     const double cn = a.w;
-    const unsigned long long cnt = s.ctr[C_CN_COUNT];
-    const double meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
     const double tMax = s.t_max;
     const bool limited = tMax > 0.0 && isfinite(tMax);
+    double meanCNew = mean;
+    if (!use_mean && from_scratch) {
+        const unsigned long long cnt = s.ctr[C_CN_COUNT];
+        meanCNew = cnt > 0 ? *s.cn_sum / (double)cnt : 0.0;
+    }
     const double capc = limited ? (tMax * tMax - tMax) * meanCNew : 0.0;
     const double cx = a.x / cn, cy = a.y / cn, cz = a.z / cn;
     double alpha = s.blend == PSTF_BLEND_SQRT ? sqrt(cn / (c.w + cn)) : cn / (c.w + cn);
@@ -2191,7 +2223,8 @@ __device__ __forceinline__ double4 blend_one(const DevStore &s, double4 a, doubl
     c.y = c.y * oma + cy * alpha;
     c.z = c.z * oma + cz * alpha;
     c.w = c.w + cn;
-    if (limited) c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
+    if (limited && (use_mean || from_scratch))
+        c.w = (capc < c.w) ? capc : c.w; /* std::min(cOld, cap) */
     return c;
 }
 
@@ -2220,8 +2253,8 @@ __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            av[k] = st.s[jj[k]].acc[sl[k]];
-            cv[k] = st.s[jj[k]].com[sl[k]];
+            av[k] = ld4(acc_ptr(st.s[jj[k]], sl[k]));
+            cv[k] = ld4(com_ptr(st.s[jj[k]], sl[k]));
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -2231,14 +2264,14 @@ __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
             const double4 a = av[k];
             const double cn = a.w;
             if (cn > 0.0) {
-                s.com[slot] = blend_one(s, a, cv[k]);
+                st4(com_ptr(s, slot), blend_one(s, a, cv[k]));
             } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (q == jj[k]) ++internal[q];
             }
             if (cn != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
-                s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+                st4(acc_ptr(s, slot), make_double4(0.0, 0.0, 0.0, 0.0));
         }
     }
 #pragma unroll
@@ -2254,6 +2287,8 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
         s.ctr[C_TOUCHED_TOTAL] += s.ctr[C_TOUCHED_N];
         s.ctr[C_TOUCHED_N] = 0;
         s.ctr[C_CN_COUNT] = 0;
+        s.ctr[C_F_CN] = 0;
+        s.ctr[C_F_DEFER] = 0;
         *s.cn_sum = 0.0;
     }
     for (int j = 0; j < nst; ++j) {
@@ -2267,7 +2302,7 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
             if (m.x != 0 && (uint32_t)(s.frame - (m.y - 1u)) >= s.evict_age) {
                 s.meta[i].x = 0;
                 atomicAnd(&s.lbits[i >> 5], ~(1u << (i & 31u)));
-                s.com[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+                *com_ptr(s, i) = make_double4(0.0, 0.0, 0.0, 0.0);
                 ++ev;
             }
         }
@@ -2276,6 +2311,157 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
             atomicAdd(&s.ctr[C_EVICTED], (unsigned long long)ev);
             atomicAdd(&s.ctr[C_LIVE], (unsigned long long)(-(long long)ev));
         }
+    }
+}
+
+/* endFrame (field.cpp:197-263) in one pass over the touched slots, for a frame whose updates
+ * all carried unit counter weights (tiled ATOMIC vertex passes and their placement).  Only the
+ * cOld cap min(cOld + c_new, (T^2 - T) * mean c_new) needs the frame's mean c_new; Σc_new was
+ * counted while updating (C_F_CN: whole numbers, exact in any order) and at most `live` slots are
+ * touched, so mean c_new = Σc_new / touched >= Σc_new / live.  A touched slot whose cOld + c_new stays within
+ * (T^2 - T) * Σc_new / live is therefore never capped: it is blended as soon as the walk over
+ * the touched bitmap finds it (acc and com gathered together; no touched list, no grid
+ * barrier).  The few that may be capped go to a short list that k_ef_tail blends with the
+ * exact mean once every touched slot has been counted.  The alpha / mix arithmetic is the
+ * reference's (blend_one), so the result is bitwise the two-pass endFrame's. */
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_onepass(Stores4 st, int nst,
+                                                         const unsigned long long *guard) {
+    if (guard && *guard) return; /* new keys still pending: the host places them first */
+    __shared__ uint32_t wlist[EF_BLOCK / 32][1024]; /* a warp's touched slots of 32 words */
+    uint64_t seg[4], nw[4];
+    uint64_t acc_w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        nw[j] = j < nst ? ((uint64_t)st.s[j].mask + 32) / 32 : 0;
+        seg[j] = acc_w;
+        acc_w += (nw[j] + 31) & ~31ull; /* whole 32-word chunks per store */
+    }
+    const uint64_t total = acc_w;
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)nst) {
+        const DevStore &s = st.s[threadIdx.x];
+        s.ctr[C_LIVE_SNAP] = s.ctr[C_LIVE];
+        s.ctr[C_EVICTED] = 0;
+    }
+    const unsigned lane = lane_id();
+    uint32_t *list = wlist[threadIdx.x >> 5];
+    unsigned internal[4] = {0u, 0u, 0u, 0u}, tch[4] = {0u, 0u, 0u, 0u};
+    const uint64_t nchunks = total / 32;
+    const uint64_t wstride = (uint64_t)gridDim.x * (EF_BLOCK / 32);
+    /* one warp per chunk of 32 bitmap words: the chunk's touched slots are compacted into
+     * shared memory, then blended 32 at a time (every lane gathers one slot's acc and com:
+     * full memory-level parallelism whatever the bits per word) */
+    for (uint64_t ch = blockIdx.x * (uint64_t)(EF_BLOCK / 32) + (threadIdx.x >> 5); ch < nchunks;
+         ch += wstride) {
+        const uint64_t gi = ch * 32 + lane;
+        const int j = min(SEG_OF(ch * 32, seg), nst - 1); /* warp-uniform */
+        const DevStore &s = st.s[j];
+        const uint64_t wi = gi - PICK4(seg, j);
+        uint32_t w = wi < PICK4(nw, j) ? s.tbits[wi] : 0u;
+        if (w) s.tbits[wi] = 0u;
+        const unsigned c = __popc(w);
+        unsigned incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += t;
+        }
+        const unsigned T = __shfl_sync(0xffffffffu, incl, 31);
+        if (!T) continue;
+        unsigned pos = incl - c;
+        while (w) {
+            list[pos++] = (uint32_t)(wi * 32 + (uint64_t)(__ffs(w) - 1));
+            w &= w - 1;
+        }
+        __syncwarp();
+        /* no slot with cOld + c_new <= capLo is capped (mean c_new >= Σc_new / live) */
+        const double tMax = s.t_max;
+        const bool limited = tMax > 0.0 && isfinite(tMax);
+        const unsigned long long live = s.ctr[C_LIVE];
+        const double capLo = limited && live ? (tMax * tMax - tMax) *
+                                                   ((double)s.ctr[C_F_CN] / (double)live)
+                                             : HUGE_VAL;
+        for (unsigned i = lane; i < T; i += 32) {
+            const uint32_t slot = list[i];
+            const double4 a = ld4(acc_ptr(s, slot));
+            const double4 cv = ld4(com_ptr(s, slot));
+            if (a.w > 0.0) {
+                if (limited && !(cv.w + a.w <= capLo)) { /* may be capped: k_ef_tail */
+                    s.tlist[atomicAdd(&s.ctr[C_F_DEFER], 1ull)] = slot;
+                    continue;
+                }
+                st4(com_ptr(s, slot), blend_one(s, a, cv, 0.0, false, false)); /* uncapped */
+            } else if (!(a.x == 0.0 && a.y == 0.0 && a.z == 0.0)) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (r == j) ++internal[r];
+            }
+            if (a.w != 0.0 || a.x != 0.0 || a.y != 0.0 || a.z != 0.0)
+                st4(acc_ptr(s, slot), make_double4(0.0, 0.0, 0.0, 0.0));
+        }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (r == j) tch[r] += T;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const unsigned t = __reduce_add_sync(0xffffffffu, internal[q]);
+        const unsigned tc = __reduce_add_sync(0xffffffffu, tch[q]);
+        if (lane == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
+        if (lane == 0 && tc) atomicAdd(&st.s[q].ctr[C_TOUCHED_N], (unsigned long long)tc);
+    }
+}
+
+/* the rest of a one-pass endFrame: the deferred slots blended with the exact mean c_new
+ * (Σc_new / touched slots, field.cpp:205-216), the age eviction when crowded, and the roll of
+ * the per-frame counters by the last block to finish */
+__device__ __forceinline__ void ef_tail_body(const Stores4 &st, int nst) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (int j = 0; j < nst; ++j) {
+        const DevStore &s = st.s[j];
+        const uint64_t nd = s.ctr[C_F_DEFER];
+        if (!nd) continue;
+        const unsigned long long cnt = s.ctr[C_TOUCHED_N];
+        const double mean = cnt > 0 ? (double)s.ctr[C_F_CN] / (double)cnt : 0.0;
+        for (uint64_t i = t0; i < nd; i += stride) {
+            const uint32_t slot = s.tlist[i];
+            const double4 a = ld4(acc_ptr(s, slot));
+            st4(com_ptr(s, slot), blend_one(s, a, ld4(com_ptr(s, slot)), mean, true));
+            st4(acc_ptr(s, slot), make_double4(0.0, 0.0, 0.0, 0.0));
+        }
+    }
+    ef_evict_body(st, nst, 0);
+}
+
+/* roll the per-frame counters of a store (nobody reads them any more this frame) */
+__device__ __forceinline__ void ef_roll(const DevStore &s) {
+    s.ctr[C_TOUCHED_LAST] = s.ctr[C_TOUCHED_N];
+    s.ctr[C_TOUCHED_TOTAL] += s.ctr[C_TOUCHED_N];
+    s.ctr[C_TOUCHED_N] = 0;
+    s.ctr[C_CN_COUNT] = 0;
+    s.ctr[C_F_CN] = 0;
+    s.ctr[C_F_DEFER] = 0;
+    *s.cn_sum = 0.0;
+}
+
+__global__ void __launch_bounds__(EF_BLOCK) k_ef_tail(Stores4 st, int nst,
+                                                      const unsigned long long *guard,
+                                                      unsigned int *done) {
+    if (guard && *guard) return;
+    ef_tail_body(st, nst);
+    /* last block: roll the per-frame counters */
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < (unsigned)nst) {
+        ef_roll(st.s[threadIdx.x]);
+        if (threadIdx.x == 0) *done = 0u;
     }
 }
 
@@ -2330,7 +2516,7 @@ __global__ void k_live_pack(Stores4 st, int nst, WSeg wseg, const uint32_t *scan
             const uint32_t slot = (uint32_t)(wl * 32 + (uint64_t)(__ffs(bits) - 1));
             bits &= bits - 1;
             list[pos] = ((unsigned long long)j << 32) | slot;
-            packed[pos] = s.acc[slot];
+            st4(&packed[pos], ld4(acc_ptr(s, slot)));
             ++pos;
         }
     }
@@ -2349,7 +2535,7 @@ __global__ void k_live_unpack(Stores4 st, const unsigned long long *list, const 
         const DevStore &s = st.s[(e >> 32) & 3];
         const uint32_t slot = (uint32_t)e;
         const double4 v = packed[i];
-        s.acc[slot] = v;
+        *acc_ptr(s, slot) = v;
         if (v.x != 0.0 || v.y != 0.0 || v.z != 0.0 || v.w != 0.0) touch_slot(s, slot);
     }
 }
@@ -2429,14 +2615,14 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_packed(Stores4 st, int nst,
         const double4 v = packed[i];
         if (!(v.x != 0.0 || v.y != 0.0 || v.z != 0.0 || v.w != 0.0)) continue;
         if (v.w > 0.0) {
-            s.com[slot] = blend_one(s, v, s.com[slot]);
+            st4(com_ptr(s, slot), blend_one(s, v, ld4(com_ptr(s, slot))));
         } else if (!(v.x == 0.0 && v.y == 0.0 && v.z == 0.0)) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (q == j) ++internal[q];
         }
         s.meta[slot].y = s.frame + 1u; /* lastTouched = frame (field.cpp:123,133,137) */
-        s.acc[slot] = make_double4(0.0, 0.0, 0.0, 0.0);
+        st4(acc_ptr(s, slot), make_double4(0.0, 0.0, 0.0, 0.0));
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -2477,7 +2663,7 @@ __global__ void k_invalidate(DevStore s, int use_box, double lx, double ly, doub
                    cz = ((double)k.c2 + 0.5) * cs;
             if (!(cx >= lx && cx <= hx && cy >= ly && cy <= hy && cz >= lz && cz <= hz)) continue;
         }
-        s.com[i].w = 0.0;
+        com_ptr(s, i)->w = 0.0;
     }
 }
 
@@ -2487,7 +2673,7 @@ __global__ void k_weighted_mean(DevStore s, double *out4) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
          i += (uint64_t)gridDim.x * blockDim.x) {
         if (s.meta[i].x == 0) continue;
-        double4 c = s.com[i];
+        double4 c = *com_ptr(s, i);
         if (c.w <= 0.0) continue; /* field.cpp:299 */
         r += c.x * c.w;
         g += c.y * c.w;
@@ -2520,7 +2706,7 @@ __global__ void k_snap_gather(DevStore s, pstf_snapshot_record *out, unsigned lo
     /* slot order is kept by sorting on (key, slot) afterwards */
     unsigned long long pos = base + __popc(m & ((1u << lane_id()) - 1u));
     KeyFields k = s.keyf[i];
-    double4 c = s.com[i];
+    double4 c = *com_ptr(s, i);
     pstf_snapshot_record r;
     r.level = k.level;
     r.cell[0] = k.c0;
@@ -3196,6 +3382,7 @@ int pstf_key_for(const pstf_field *f, const pstf_vec3_soa *pos, const pstf_vec3_
 int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *value,
                      const double *w, const uint8_t *is_counter, uint64_t n, int mode,
                      void *stream) {
+    if (f) f->unit_frame = false; /* arbitrary weights: endFrame's reduce pass */
     if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
     if (mode < 0 || mode > 2) return set_err(PSTF_E_INVALID, "bad mode");
     if (!n) return PSTF_OK;
@@ -3315,6 +3502,7 @@ int pstf_select_level_host(const pstf_field *f, const double *footprint, int32_t
 
 int pstf_field_apply_host(pstf_field *f, const pstf_key *keys, const double *rgb_xyz,
                           const double *w, const uint8_t *is_counter, uint64_t n, int mode) {
+    if (f) f->unit_frame = false; /* arbitrary weights: endFrame's reduce pass */
     if (!f) return set_err(PSTF_E_INVALID, "NULL store");
     std::lock_guard<std::mutex> lk(const_cast<pstf_field *>(f)->host_mu);
     if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
@@ -3435,7 +3623,22 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fused_blocks, k_ef_fused, EF_BLOCK, 0));
         if (getenv("PSTF_NO_FUSED_EF")) fused_blocks = 0;
     }
+    static const bool no_onepass = getenv("PSTF_NO_ONEPASS_EF") != nullptr;
+    bool unit = !no_onepass;
+    for (int i = 0; i < n; ++i) unit = unit && fs[i]->unit_frame;
     auto launch = [&](const unsigned long long *gd) -> int {
+        if (unit) { /* counted frame: one pass over the touched slots, then the tail */
+            Scratch &sc0 = fs[0]->sc;
+            if (!sc0.ef_done.p) {
+                ENSURE(sc0.ef_done, 4);
+                CK(cudaMemsetAsync(sc0.ef_done.p, 0, 4, st));
+            }
+            LAUNCH(k_ef_onepass, g, EF_BLOCK, 0, st, S, n, gd);
+            /* one block per SM: the deferred list is short, eviction rarely runs */
+            LAUNCH(k_ef_tail, std::min<unsigned>(g, (unsigned)sm_count()), EF_BLOCK, 0, st, S, n, gd,
+                   sc0.ef_done.as<unsigned int>());
+            return PSTF_OK;
+        }
         if (fused_blocks > 0) { /* one cooperative launch: reduce | blend | evict */
             unsigned gf = std::min<unsigned>(g, (unsigned)(sm_count() * fused_blocks));
             int nn = n;
@@ -3462,7 +3665,10 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
             SETTLE(owner); /* nothing pending: just retire the deferred pass */
         }
     }
-    for (int i = 0; i < n; ++i) fs[i]->frame += 1;
+    for (int i = 0; i < n; ++i) {
+        fs[i]->frame += 1;
+        fs[i]->unit_frame = true;
+    }
     return PSTF_OK;
 }
 
@@ -3747,7 +3953,7 @@ __global__ void k_restore_write(DevStore s, const pstf_snapshot_record *r, uint6
     const pstf_snapshot_record q = r[i];
     const int slot = probe_find(s, snap_home(q, s.mask), q.checksum);
     if (slot >= 0 && winner[slot] == (uint32_t)i + 1u)
-        s.com[slot] = make_double4(q.value[0], q.value[1], q.value[2], q.c_old);
+        *com_ptr(s, slot) = make_double4(q.value[0], q.value[1], q.value[2], q.c_old);
 }
 
 static bool snap_key_less(const pstf_snapshot_record &a, const pstf_snapshot_record &b) {
@@ -3757,6 +3963,7 @@ static bool snap_key_less(const pstf_snapshot_record &a, const pstf_snapshot_rec
 }
 
 extern "C" int pstf_field_restore(pstf_field *f, const pstf_snapshot_record *records, uint64_t n) {
+    if (f) f->unit_frame = false; /* arbitrary weights: endFrame's reduce pass */
     if (!f || (n && !records)) return set_err(PSTF_E_INVALID, "NULL argument");
     if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "too many records");
     for (uint64_t i = 0; i < n; ++i) { /* keyFor's checksum (field.cpp:98-99) */
@@ -3980,6 +4187,8 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         }
         return PSTF_OK;
     }
+    for (pstf_field *f : fs)
+        if (f) f->unit_frame = false; /* the per-thread kernels do not count (k_ef_onepass) */
     if (cv)
         LAUNCH(k_cv_lookup, grid_for(n, 256), 256, 0, st, loe->d, *v, n, cv->r, cv->g, cv->b,
                cv->valid);
@@ -4343,6 +4552,7 @@ int pstf_shard_live_unpack(pstf_field *const *stores, int nst, const double *pac
     Scratch &sc = stores[0]->sc;
     if (!sc.live_total_dev) return set_err(PSTF_E_INVALID, "pstf_shard_live_pack first");
     if (sc.live_bound && !packed) return set_err(PSTF_E_INVALID, "NULL packed");
+    for (int i_ = 0; i_ < nst; ++i_) stores[i_]->unit_frame = false; /* remote sums */
     CK(cudaSetDevice(stores[0]->device));
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = std::min<unsigned>(grid_for(sc.live_bound, 256), (unsigned)sm_count() * 8);
@@ -4388,6 +4598,7 @@ int pstf_shard_end_frame(pstf_field *const *stores, int nst, const double *packe
     for (int i = 0; i < nst; ++i) { /* the phase-1 touch marks of this replica */
         CK(cudaMemsetAsync(stores[i]->d.tbits, 0, (((uint64_t)stores[i]->d.mask + 32) / 32) * 4, st));
         stores[i]->frame += 1;
+        stores[i]->unit_frame = true;
     }
     return PSTF_OK;
 }

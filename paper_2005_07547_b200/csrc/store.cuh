@@ -24,6 +24,31 @@
 
 namespace pstf_b200 {
 
+/* 32-byte records moved with one 256-bit access (LDG/STG.E.256 on sm_100) instead of two
+ * 128-bit halves: one L1 request and one L2 sector transaction per record.
+ *   ld4_ro  read-only data of the running kernel (committed values in the vertex pass)
+ *   ld4/st4 ordered with the thread's other memory accesses (endFrame read-modify-write) */
+__device__ __forceinline__ double4 ld4_ro(const double4 *p) {
+    double4 v;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double4 ld4(const double4 *p) {
+    double4 v;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st4(double4 *p, double4 v) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "d"(v.z), "d"(v.w)
+                 : "memory");
+}
+
 struct KeyFields {
     int32_t level, c0, c1, c2, d0, d1;
 };
@@ -42,6 +67,9 @@ enum Ctr : int {
     C_TOUCHED_TOTAL, // touched slots summed over all committed frames
     C_REDS,          // fp64 RED element updates issued by fused vertex passes (Lo store)
     C_ROUNDS,        // deterministic-placement rounds of the last update pass
+    C_F_CN,          // this frame: sum of counter weights into existing/placed slots (unit-
+                     // weight frames: an exact integer, = field.cpp:205-212's sum of c_new)
+    C_F_DEFER,       // one-pass endFrame: touched slots deferred to k_ef_tail (may be capped)
     C_NUM
 };
 
@@ -67,6 +95,14 @@ struct DevStore {
     uint32_t frame;       // uint32_t(m_frame) for this launch
     int32_t rank;         // multi-GPU: this rank (origin tag of pending records; 0 unsharded)
 };
+
+/* the accumulator / committed record of a slot */
+__device__ __forceinline__ double4 *acc_ptr(const DevStore &s, uint64_t slot) {
+    return s.acc + slot;
+}
+__device__ __forceinline__ double4 *com_ptr(const DevStore &s, uint64_t slot) {
+    return s.com + slot;
+}
 
 /* the members of a store that a contribution touches, selectable per loop iteration */
 struct StoreRef {
