@@ -215,6 +215,11 @@ int pstf_field_load_snapshot(pstf_field *f, const char *path);
 
 /* Slot-array dump (host) of slots [begin, begin+count) for occupancy parity. */
 int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_record *out);
+/* The committed state (what queries read, field.h:73-75) of every slot, to host memory:
+ * checksum[capacity] (0 = empty) and com4[capacity][4] = {valueOld.rgb, cOld}.  The C++ facade
+ * mirrors it once per frame and answers scalar query()/queryFromLevel() calls from the mirror
+ * (SURVEY.md 8(b)); it changes only at endFrame / invalidate / restore. */
+int pstf_field_committed_host(pstf_field *f, uint32_t *checksum, double *com4);
 
 /* Fused per-vertex pass: FieldRecorder::onVertex (estimators.cpp:194-262) for n vertices, i.e.
  * next-vertex Lo/LoE lookups on committed state, key generation, update values, and the

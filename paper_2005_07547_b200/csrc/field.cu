@@ -4062,6 +4062,26 @@ int pstf_field_slots(pstf_field *f, uint64_t begin, uint64_t count, pstf_slot_re
     return PSTF_OK;
 }
 
+__global__ void k_checksums(const uint2 *meta, uint64_t n, uint32_t *out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = meta[i].x;
+}
+
+int pstf_field_committed_host(pstf_field *f, uint32_t *checksum, double *com4) {
+    if (!f || !checksum || !com4) return set_err(PSTF_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(f->device));
+    SETTLE(f);
+    std::lock_guard<std::mutex> lk(f->host_mu);
+    const uint64_t cap = (uint64_t)f->d.mask + 1;
+    Scratch &sc = f->sc;
+    ENSURE(sc.hio, cap * 4);
+    LAUNCH(k_checksums, grid_for(cap, 256), 256, 0, (cudaStream_t)0, f->d.meta, cap,
+           sc.hio.as<uint32_t>());
+    CK(cudaMemcpy(checksum, sc.hio.p, cap * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(com4, f->d.com, cap * 32, cudaMemcpyDeviceToHost));
+    return PSTF_OK;
+}
+
 struct CvOut { /* fused CV-lookup outputs (pstf_vertex_pass_cv) */
     double *r, *g, *b;
     uint8_t *valid;

@@ -470,20 +470,18 @@ PSTF_HD FastParams make_fast_params(const KeyParams &kp) {
  * ulps of the reference's fl(fl(footprint K) / base); sets *nx when s' is too close to a power of
  * two (or out of range) for that to be certain.  (*nx = "needs the exact reference operation") */
 PSTF_HD int select_level_try(const FastParams &f, double footprint, int *nx) {
-    if (!(footprint > 0.0)) return 0;
+    /* branch-free (selects only): the caller's warp never diverges here */
+    const bool pos = footprint > 0.0;
     const double s = footprint * f.k_inv_base;
-    if (s < 0.9999999999) return 0; /* exact s <= 1: level 0 (field.cpp:71) */
-    if (s > 1.0000000001 && s < 1e300) {
-        const uint64_t b = dbits(s);
-        const uint64_t mant = b & 0x000fffffffffffffULL;
-        /* mantissa not within 2^-40 of either end of [1, 2): exponent == floor(log2(s)) */
-        if (mant > (1ULL << 12) && mant < 0x000fffffffffffffULL - (1ULL << 12)) {
-            int level = (int)((b >> 52) & 0x7ff) - 1023;
-            return level < f.kp.max_level ? level : f.kp.max_level;
-        }
-    }
-    *nx = 1;
-    return 0;
+    const bool low = s < 0.9999999999; /* exact s <= 1: level 0 (field.cpp:71) */
+    const uint64_t b = dbits(s);
+    const uint64_t mant = b & 0x000fffffffffffffULL;
+    /* mantissa not within 2^-40 of either end of [1, 2): exponent == floor(log2(s)) */
+    const bool mid = (s > 1.0000000001) & (s < 1e300) & (mant > (1ULL << 12)) &
+                     (mant < 0x000fffffffffffffULL - (1ULL << 12));
+    const int level = (int)((b >> 52) & 0x7ff) - 1023;
+    *nx |= pos & !low & !mid;
+    return (pos & !low & mid) ? (level < f.kp.max_level ? level : f.kp.max_level) : 0;
 }
 
 PSTF_HD int select_level_fast(const FastParams &f, double footprint) {
@@ -651,32 +649,31 @@ PSTF_HD void octa_f8_try(double dx, double dy, double dz, int want_neg, DirF8 *p
      * [0.5, 1]), rounded once; NaN and negative -> 0 like std::max(0.0, .) */
     const float wf = fmaxf((float)(1.0 - z), 0.0f);
     const float r = sqrt_fast(wf);
-    float phi = 0.0f;
-    if (!(x == 0.0 && y == 0.0)) {
-        const float xf = (float)x, yf = (float)y;
-        /* fast-path domain: x and y finite (a NaN fails the comparisons) and the larger one in
-         * [1e-30, 1e30] */
-        *nx |= !(xf <= 1e30f && yf <= 1e30f && (xf >= 1e-30f || yf >= 1e-30f));
-        const bool swap = yf > xf;
-        const float a = swap ? xf : yf, b = swap ? yf : xf; /* 0 <= a <= b */
-        const bool small = a <= b * 0.41421356f;
-        const float num = small ? a : a - b, den = small ? b : a + b;
+    /* branch-free: phi is computed for x = y = 0 too and replaced by 0 there (mappings.h:39) */
+    const bool zero = x == 0.0 && y == 0.0;
+    const float xf = (float)x, yf = (float)y;
+    /* fast-path domain: x and y finite (a NaN fails the comparisons) and the larger one in
+     * [1e-30, 1e30] */
+    *nx |= !zero & !(xf <= 1e30f && yf <= 1e30f && (xf >= 1e-30f || yf >= 1e-30f));
+    const bool swap = yf > xf;
+    const float a = swap ? xf : yf, b = swap ? yf : xf; /* 0 <= a <= b */
+    const bool small = a <= b * 0.41421356f;
+    const float num = small ? a : a - b, den = small ? b : a + b;
 #if defined(__CUDA_ARCH__)
-        float rc; /* hardware reciprocal estimate, relative error < 2^-22 (den is a normal) */
-        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));
-        const float t = num * rc;
+    float rc; /* hardware reciprocal estimate, relative error < 2^-22 (den is a normal) */
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));
+    const float t = num * rc;
 #else
-        const float t = num * (1.0f / den);
+    const float t = num * (1.0f / den);
 #endif
-        const float zz = t * t;
-        float p = 0.07726402580738068f;
-        p = fmaf(p, zz, -0.13751664757728577f);
-        p = fmaf(p, zz, 0.19961561262607574f);
-        p = fmaf(p, zz, -0.33332183957099915f);
-        p = fmaf(p, zz, 0.9999998807907104f);
-        const float th = (small ? 0.0f : 0.78539816f) + t * p;
-        phi = (swap ? 1.57079633f - th : th) * 0.63661977f; /* * 2/pi */
-    }
+    const float zz = t * t;
+    float p = 0.07726402580738068f;
+    p = fmaf(p, zz, -0.13751664757728577f);
+    p = fmaf(p, zz, 0.19961561262607574f);
+    p = fmaf(p, zz, -0.33332183957099915f);
+    p = fmaf(p, zz, 0.9999998807907104f);
+    const float th = (small ? 0.0f : 0.78539816f) + t * p;
+    const float phi = zero ? 0.0f : (swap ? 1.57079633f - th : th) * 0.63661977f; /* * 2/pi */
     const float v0 = phi * r, u0 = r - v0;
     float u = u0, v = v0;
     if (dz < 0.0) { /* hemisphere swap (mappings.h:43-48) */

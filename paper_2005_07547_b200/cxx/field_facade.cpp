@@ -1,12 +1,21 @@
 // C++ drop-in facade: pstf::FieldStore / FieldUpdateQueue (reference field.h) implemented over
-// the B200 C ABI (include/pstf_field.h).  Every key, lookup, update, blend and snapshot runs in
-// the sm_100a library; this file only marshals arguments and stages scalar calls.
+// the B200 C ABI (include/pstf_field.h).  Updates, placement, blends, invalidation, statistics
+// and snapshots run in the sm_100a library.  The per-vertex scalar calls of unmodified reference
+// callers (estimators.cpp:165-206) are served without a device round trip each:
+//   * keyFor / selectLevel evaluate the library's key math (csrc/pstf_keys.cuh, the exact path:
+//     bitwise the reference's, tests/test_keys_host.py) on the calling thread;
+//   * incrementCounter / accumulate are staged and applied in submission order (SEQUENTIAL
+//     mode) before anything observes the store;
+//   * query / queryFromLevel read a host mirror of the committed state, refreshed once after
+//     each endFrame / invalidate / loadSnapshot: queries see committed state only
+//     (field.h:73-75), which changes nowhere else.
 #include "pstf/field.h"
 
 #include <cstring>
 #include <stdexcept>
 
 #include "../../include/pstf_field.h"
+#include "../csrc/pstf_keys.cuh"
 
 namespace pstf {
 
@@ -63,6 +72,23 @@ struct FieldStore::Impl {
     std::vector<pstf_key> keys;
     std::vector<double> rgb, w;
     std::vector<uint8_t> isCounter;
+    pstf_b200::KeyParams kp;
+    uint32_t mask = 0, window = 32;
+    /* committed-state mirror */
+    std::mutex mirror_mu;
+    std::atomic<bool> mirror_ok{false};
+    std::vector<uint32_t> chk;
+    std::vector<double> com; /* 4 per slot */
+    void refresh() {
+        if (mirror_ok.load(std::memory_order_acquire)) return;
+        std::lock_guard<std::mutex> lk(mirror_mu);
+        if (mirror_ok.load(std::memory_order_relaxed)) return;
+        chk.resize(size_t(mask) + 1);
+        com.resize(4 * (size_t(mask) + 1));
+        check(pstf_field_committed_host(h, chk.data(), com.data()), "pstf_field_committed_host");
+        mirror_ok.store(true, std::memory_order_release);
+    }
+    void invalidate_mirror() { mirror_ok.store(false, std::memory_order_release); }
 };
 
 FieldStore::FieldStore(const FieldStoreConfig &config) : m_config(config), m_impl(new Impl) {
@@ -79,6 +105,11 @@ FieldStore::FieldStore(const FieldStoreConfig &config) : m_config(config), m_imp
     c.probe_window = config.probeWindow;
     c.evict_age_frames = config.evictAgeFrames;
     check(pstf_field_create(&c, 0, &m_impl->h), "pstf_field_create");
+    m_impl->kp.base_cell_size = config.baseCellSize;
+    m_impl->kp.level_select_k = config.levelSelectK;
+    m_impl->kp.max_level = config.maxLevel;
+    m_impl->mask = uint32_t((uint64_t(1) << config.capacityLog2) - 1);
+    m_impl->window = config.probeWindow;
 }
 
 FieldStore::~FieldStore() {
@@ -103,10 +134,8 @@ void FieldStore::flush() const {
     s.isCounter.clear();
 }
 
-int FieldStore::selectLevel(double footprint) const {
-    int32_t l = 0;
-    check(pstf_select_level_host(m_impl->h, &footprint, &l, 1), "pstf_select_level_host");
-    return l;
+int FieldStore::selectLevel(double footprint) const { /* field.cpp:68-76 */
+    return pstf_b200::select_level(m_impl->kp, footprint);
 }
 
 double FieldStore::cellSize(int level) const {
@@ -116,13 +145,16 @@ double FieldStore::cellSize(int level) const {
 int FieldStore::dirResolution(int level) const { return 8 >> (level < 2 ? level : 2); }
 
 SpatioDirectionalKey FieldStore::keyFor(const Vec3 &position, const Vec3 &direction,
-                                        int level) const {
-    const double p[3] = {position.x, position.y, position.z};
-    const double d[3] = {direction.x, direction.y, direction.z};
-    const int32_t l = level;
-    pstf_key k;
-    check(pstf_key_for_host(m_impl->h, p, d, &l, 1, &k), "pstf_key_for_host");
-    return fromC(k);
+                                        int level) const { /* field.cpp:86-101 */
+    const pstf_b200::Key k = pstf_b200::key_for(m_impl->kp, position.x, position.y, position.z,
+                                                direction.x, direction.y, direction.z, level);
+    SpatioDirectionalKey o;
+    o.level = k.level;
+    for (int i = 0; i < 3; ++i) o.cell[i] = k.cell[i];
+    o.dirCell[0] = k.dir[0];
+    o.dirCell[1] = k.dir[1];
+    o.checksum = k.checksum;
+    return o;
 }
 
 void FieldStore::incrementCounter(const SpatioDirectionalKey &key, double w) {
@@ -143,44 +175,56 @@ void FieldStore::accumulate(const SpatioDirectionalKey &key, const RGB &value, d
     s.isCounter.push_back(0);
 }
 
-static FieldQueryResult query_impl(pstf_field *h, const Vec3 &position, const Vec3 &direction,
-                                   const double *fp, const int32_t *level) {
-    const double p[3] = {position.x, position.y, position.z};
-    const double d[3] = {direction.x, direction.y, direction.z};
-    double v[3];
-    uint8_t valid = 0, fb = 0;
-    int32_t lv = 0;
-    check(pstf_field_query_host(h, p, d, fp, level, 1, v, &valid, &fb, &lv),
-          "pstf_field_query_host");
+/* queryFromLevel (field.cpp:179-195) on the committed-state mirror: findSlot's linear probe
+ * (checksum identity, stop at an empty slot) at each level up to maxLevel */
+static FieldQueryResult query_mirror(FieldStore::Impl &s, int maxLevel, const Vec3 &position,
+                                     const Vec3 &direction, int level) {
+    s.refresh();
     FieldQueryResult r;
-    r.value = RGB(v[0], v[1], v[2]);
-    r.valid = valid != 0;
-    r.fallback = fb != 0;
-    r.level = lv;
+    r.level = level;
+    for (int l = level; l <= maxLevel; ++l) {
+        const pstf_b200::Key k = pstf_b200::key_for(s.kp, position.x, position.y, position.z,
+                                                    direction.x, direction.y, direction.z, l);
+        const uint32_t home = k.pack_lo & s.mask;
+        for (uint32_t i = 0; i < s.window; ++i) {
+            const uint32_t idx = (home + i) & s.mask;
+            const uint32_t c = s.chk[idx];
+            if (c == 0) break;
+            if (c != k.checksum) continue;
+            const double *cv = &s.com[4 * size_t(idx)];
+            if (cv[3] > 0.0) {
+                r.value = RGB(cv[0], cv[1], cv[2]);
+                r.valid = true;
+                r.fallback = l != level;
+                r.level = l;
+                return r;
+            }
+            break;
+        }
+    }
     return r;
 }
 
 FieldQueryResult FieldStore::query(const Vec3 &position, const Vec3 &direction,
                                    double footprint) const {
-    flush();
-    return query_impl(m_impl->h, position, direction, &footprint, nullptr);
+    return query_mirror(*m_impl, m_config.maxLevel, position, direction, selectLevel(footprint));
 }
 
 FieldQueryResult FieldStore::queryFromLevel(const Vec3 &position, const Vec3 &direction,
                                             int level) const {
-    flush();
-    const int32_t l = level;
-    return query_impl(m_impl->h, position, direction, nullptr, &l);
+    return query_mirror(*m_impl, m_config.maxLevel, position, direction, level);
 }
 
 void FieldStore::endFrame() {
     flush();
     check(pstf_field_end_frame(m_impl->h, nullptr), "pstf_field_end_frame");
+    m_impl->invalidate_mirror();
 }
 
 void FieldStore::invalidate() {
     flush();
     check(pstf_field_invalidate(m_impl->h, nullptr, nullptr), "pstf_field_invalidate");
+    m_impl->invalidate_mirror();
 }
 
 void FieldStore::invalidate(const Aabb &region) {
@@ -188,6 +232,7 @@ void FieldStore::invalidate(const Aabb &region) {
     const double box[6] = {region.lo.x, region.lo.y, region.lo.z,
                            region.hi.x, region.hi.y, region.hi.z};
     check(pstf_field_invalidate(m_impl->h, box, nullptr), "pstf_field_invalidate");
+    m_impl->invalidate_mirror();
 }
 
 static pstf_field_stats stats_of(pstf_field *h) {
@@ -232,6 +277,7 @@ void FieldStore::dumpSnapshot(const std::string &path) const {
 void FieldStore::loadSnapshot(const std::string &path) {
     flush();
     check(pstf_field_load_snapshot(m_impl->h, path.c_str()), "loadSnapshot");
+    m_impl->invalidate_mirror();
 }
 
 std::vector<FieldStore::SnapshotRecord> FieldStore::readSnapshot(const std::string &path) {
