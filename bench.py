@@ -41,13 +41,16 @@ DIAMETER = math.sqrt(12.0)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=None,
+                   help="timed iterations (default 20; config 5: 128, BASELINE configs[4])")
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--bounces", type=int, default=4)
-    p.add_argument("--capacity-log2", type=int, default=22)
+    p.add_argument("--capacity-log2", type=int, default=None,
+                   help="slots per store (default 2^22; config 4: 2^24; config 5: the next power "
+                        "of two >= 2 x L2 / slot bytes, SURVEY.md 8(d))")
     p.add_argument("--streams", type=int, default=8)
     p.add_argument("--mode", default="atomic", choices=["atomic", "ordered"])
     p.add_argument("--e2e-steps", type=int, default=4)
@@ -67,20 +70,40 @@ def parse():
     a = p.parse_args()
     if a.scaling is None:
         a.scaling = "strong" if a.config == 4 else "weak"
+    if a.steps is None:
+        a.steps = 128 if a.config == 5 else 20
     if a.config == 4:
-        a.width, a.height, a.bounces, a.capacity_log2, a.streams = 3840, 2160, 6, 24, 2
-    if a.config == 5:
-        a.capacity_log2 = 20
+        a.width, a.height, a.bounces, a.streams = 3840, 2160, 6, 2
+    if a.capacity_log2 is None:
+        a.capacity_log2 = {4: 24, 5: config5_capacity_log2()}.get(a.config, 22)
     return a
+
+
+SLOT_BYTES = 8 + 32 + 32 + 24 + 8 + 4  # meta, com, acc, key fields, placement holds, list
+
+
+def config5_capacity_log2():
+    """the next power of two >= 2 x L2 / slot bytes (L2 read from the
+    device, cudaDevAttrL2CacheSize; 126.5 MB on B200 -> 2^22)"""
+    l2 = 126 * 1024 * 1024
+    try:
+        import torch
+        if torch.cuda.is_available():
+            l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    except Exception:
+        pass
+    need = 2 * l2 // SLOT_BYTES
+    return max(10, int(need - 1).bit_length())
 
 
 WORKLOADS = {
     2: "config2: 1920x1080 1spp x4 bounces synthetic Cornell vertex stream, spatio-directional "
        "keys, Lo/LoE/FLi stores x 2^22 slots, base=diam/256",
-    3: "config3: config 2 + CV lookup (Lo\\E query) at every vertex",
+    3: "config3: config 2 with the glossy materials of staircase_glossy.scene (Phong albedo 0.6, "
+       "exponent 48 on floor and back wall) + CV lookup (Lo\\E query) at every vertex",
     4: "config4: 3840x2160 1spp x6 bounces, Lo/LoE/FLi x 2^24 slots",
-    5: "config5: config 2 with the camera drifting +0.02/iteration, 2^20 slots (eviction "
-       "engages), inputs regenerated untimed",
+    5: "config5: config 2 with the camera drifting +0.02/iteration, 128 iterations, stores at "
+       "2 x L2 (next power of two), inputs regenerated untimed",
 }
 
 
@@ -224,7 +247,8 @@ def cpu_reference_run(args, steps, warmup, budget_s, streams=2):
     # calibrate on a small sample, then size the sample to the budget; the iteration streams
     # are generated one at a time and only their samples kept (the GPU arm cycles the same
     # `streams` iteration streams)
-    buf0 = po.synth_generate(W, H, B, iteration=0, threads=gen_threads)[0]
+    scene = 1 if args.config == 3 else 0
+    buf0 = po.synth_generate(W, H, B, iteration=0, threads=gen_threads, scene=scene)[0]
     cal, cm = sample(buf0, 1.0 / 64, 1)
     tp, te = step(cal, cm)
     rate = cm / max(tp, 1e-9)
@@ -233,7 +257,7 @@ def cpu_reference_run(args, steps, warmup, budget_s, streams=2):
     samples = [sample(buf0, frac, 100)]
     del buf0
     for i in range(1, streams):
-        bi = po.synth_generate(W, H, B, iteration=i, threads=gen_threads)[0]
+        bi = po.synth_generate(W, H, B, iteration=i, threads=gen_threads, scene=scene)[0]
         samples.append(sample(bi, frac, 100 + i))
         del bi
     for i in range(warmup):
@@ -325,7 +349,8 @@ def run_b200(args):
     seed = 0x5EED + (0 if strong else 7919 * rank)
     bufs = []
     for i in range(1 if drift else S):
-        b, _ = pb.synth_generate(W, H, B, seed=seed, iteration=i, path0=p0, npaths=p1 - p0)
+        b, _ = pb.synth_generate(W, H, B, seed=seed, iteration=i, path0=p0, npaths=p1 - p0,
+                                 scene=1 if args.config == 3 else 0)
         bufs.append(b)
     if drift:
         S = 1
@@ -377,6 +402,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         if drift:  # per-step events: the input regeneration stays outside the timed region
             evs = []
+            per_iter = []
             for i in range(args.steps):
                 pb.profile_enable(False)
                 regenerate(args.warmup + i)
@@ -386,6 +412,10 @@ def run_b200(args):
                 step(args.warmup + i)
                 e1.record()
                 evs.append((e0, e1))
+                pb.profile_enable(False)
+                per_iter.append([(x["evicted_last"], x["dropped"], x["live"], x["new_keys_last"])
+                                 for x in (s.stats() for s in stores)])  # untimed (events)
+                pb.profile_enable(True)
             torch.cuda.synchronize()
             ms = sum(a.elapsed_time(b) for a, b in evs)
         else:
@@ -469,11 +499,19 @@ def run_b200(args):
         "clocks": clk.summary(),
     }
     if drift:  # config 5 (probe-length stress): probe distances, drops and evictions
+        ev = [[it[j][0] for it in per_iter] for j in range(3)]
+        dr = [[it[j][1] for it in per_iter] for j in range(3)]
         line["probe_stress"] = {
+            "capacity_log2": args.capacity_log2,
             "probe_hist_lo_loe_fli": [s.probe_histogram().tolist() for s in stores],
             "dropped_per_iteration": [(s["dropped"] - d0) / args.steps
                                       for s, d0 in zip(st, dropped0)],
-            "evicted_last": [s["evicted_last"] for s in st],
+            "evicted_total_lo_loe_fli": [sum(e) for e in ev],
+            "iterations_with_evictions": [sum(1 for x in e if x) for e in ev],
+            "evicted_per_iteration_fli": ev[2],
+            "dropped_cumulative_fli": dr[2],
+            "live_per_iteration_fli": [it[2][2] for it in per_iter],
+            "new_keys_per_iteration_fli": [it[2][3] for it in per_iter],
             "load_factor": [s["live"] / float(1 << args.capacity_log2) for s in st],
         }
 

@@ -273,6 +273,12 @@ int pstf_synth_generate(int width, int height, int bounces, uint64_t seed, uint6
 int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed,
                                uint64_t iteration, double cam_shift_x, uint64_t path0,
                                uint64_t npaths, double *buffer, void *stream);
+/* ... with a material set: scene 0 = the Lambertian Cornell box (the functions above), scene 1 =
+ * the glossy materials of staircase_glossy.scene:11-22 on the same box (BASELINE config 3:
+ * floor and back wall diffuse 0.2/0.18/0.15 + Phong lobe albedo 0.6, exponent 48) */
+int pstf_synth_generate_scene(int scene, int width, int height, int bounces, uint64_t seed,
+                              uint64_t iteration, double cam_shift_x, uint64_t path0,
+                              uint64_t npaths, double *buffer, void *stream);
 /* Fills a pstf_vertex_soa view of such a contiguous buffer (host or device memory). */
 void pstf_vertex_soa_from_buffer(const double *buffer, uint64_t n, pstf_vertex_soa *out);
 

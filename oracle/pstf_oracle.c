@@ -589,9 +589,18 @@ static void *po_gen_worker(void *arg) {
     return NULL;
 }
 
+void po_synth_generate_scene(int scene, int width, int height, int bounces, uint64_t seed,
+                             uint64_t iter, double cam_shift_x, double *buf, int threads);
+
 void po_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iter,
                        double cam_shift_x, double *buf, int threads) {
+    po_synth_generate_scene(0, width, height, bounces, seed, iter, cam_shift_x, buf, threads);
+}
+
+void po_synth_generate_scene(int scene, int width, int height, int bounces, uint64_t seed,
+                             uint64_t iter, double cam_shift_x, double *buf, int threads) {
     ps_params P;
+    P.glossy = scene;
     P.width = width;
     P.height = height;
     P.bounces = bounces;

@@ -158,6 +158,9 @@ void po_query_batch(const po_store *s, const double *pos, const double *dir, con
 /* synthetic stream generator on the host (pstf_synth.h), n = width*height*bounces */
 void po_synth_generate(int width, int height, int bounces, uint64_t seed, uint64_t iter,
                        double cam_shift_x, double *buf, int threads);
+/* scene 1: the glossy materials (pstf_synth.h glossy mode, BASELINE config 3) */
+void po_synth_generate_scene(int scene, int width, int height, int bounces, uint64_t seed,
+                             uint64_t iter, double cam_shift_x, double *buf, int threads);
 
 #ifdef __cplusplus
 }

@@ -114,6 +114,7 @@ def oracle_lib():
         lib.po_queue_apply.argtypes = [vp, vp, sz]
         lib.po_vertex_pass_contig.argtypes = [vp, vp, vp, vp, vp, sz, u32, u32, i32]
         lib.po_synth_generate.argtypes = [i32, i32, i32, u64, u64, d, vp, i32]
+        lib.po_synth_generate_scene.argtypes = [i32, i32, i32, i32, u64, u64, d, vp, i32]
         lib.po_home_slot.argtypes = [vp, u32]
         lib.po_home_slot.restype = u32
         lib.po_key_for_batch.argtypes = [vp, vp, vp, vp, sz, vp]
@@ -483,14 +484,15 @@ def host_info() -> dict:
 
 
 def synth_generate(width, height, bounces, seed=0x5EED, iteration=0, cam_shift_x=0.0,
-                   threads=None):
-    """Host generator (pstf_synth.h) -> contiguous buffer (34*n fp64 + n u32 as fp64 words)."""
+                   threads=None, scene=0):
+    """Host generator (pstf_synth.h) -> contiguous buffer (34*n fp64 + n u32 as fp64 words).
+    scene 1: the glossy materials (BASELINE config 3)."""
     n = width * height * bounces
     words = 34 * n + (n + 1) // 2
     buf = np.zeros(words, np.float64)
     threads = threads or min(os.cpu_count() or 1, 64)
-    oracle_lib().po_synth_generate(width, height, bounces, seed, iteration, cam_shift_x,
-                                   _p(buf), threads)
+    oracle_lib().po_synth_generate_scene(scene, width, height, bounces, seed, iteration,
+                                         cam_shift_x, _p(buf), threads)
     return buf, n
 
 

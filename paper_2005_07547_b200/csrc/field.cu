@@ -4395,7 +4395,15 @@ int pstf_cv_lookup(const pstf_field *loe, const pstf_vertex_soa *v, uint64_t n, 
 int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed,
                                uint64_t iteration, double cam_shift_x, uint64_t path0,
                                uint64_t npaths, double *buffer, void *stream) {
+    return pstf_synth_generate_scene(0, width, height, bounces, seed, iteration, cam_shift_x,
+                                     path0, npaths, buffer, stream);
+}
+
+int pstf_synth_generate_scene(int scene, int width, int height, int bounces, uint64_t seed,
+                              uint64_t iteration, double cam_shift_x, uint64_t path0,
+                              uint64_t npaths, double *buffer, void *stream) {
     const uint64_t total = (uint64_t)width * (uint64_t)height;
+    if (scene != 0 && scene != 1) return set_err(PSTF_E_INVALID, "scene must be 0 or 1");
     if (width <= 0 || height <= 0 || bounces <= 0 || !buffer || path0 + npaths > total)
         return set_err(PSTF_E_INVALID, "bad synthetic stream arguments");
     ps_params P;
@@ -4407,6 +4415,7 @@ int pstf_synth_generate_stripe(int width, int height, int bounces, uint64_t seed
     P.cam_shift_x = cam_shift_x;
     P.path0 = path0;
     P.n_local = npaths == total && path0 == 0 ? 0 : npaths;
+    P.glossy = scene;
     LAUNCH(k_synth, grid_for(npaths, 128), 128, 0, (cudaStream_t)stream, P, buffer,
            npaths * (uint64_t)bounces);
     return PSTF_OK;

@@ -51,6 +51,8 @@ typedef struct {
     double cam_shift_x; /* config 5: camera translated along x */
     uint64_t path0;     /* image stripe: paths [path0, path0 + n_local) ... */
     uint64_t n_local;   /* ... stored at b * n_local + (p - path0); 0 = whole image */
+    int glossy;         /* config 3: floor and back wall are the glossy "steps" material of
+                           staircase_glossy.scene:11-16 (see ps_material) */
 } ps_params;
 
 typedef struct { double x, y, z; } ps_v3;
@@ -139,6 +141,77 @@ PS_HD ps_v3 ps_to_world(int w, double a, double b, double c) {
 #define PS_LAMP_EMISSION 12.0
 #define PS_LAMP_PDF_AREA (1.0 / 0.36)
 
+/* ---- glossy mode (BASELINE config 3): the materials of staircase_glossy.scene:11-22 ----
+ * floor (wall 2) and back wall (4) are "steps": diffuse 0.2/0.18/0.15 + a Phong lobe of albedo
+ * 0.6, exponent 48 around the mirror direction; the other walls are "wall" (diffuse 0.6).
+ * BSDF value, pdf and lobe choice follow scene.cpp:326-389 (evalBsdf, pdfBsdf, sampleBsdf) with
+ * IEEE-exact operations only: cos^48 by repeated squaring, and the power-cosine lobe sampled as
+ * the maximum of 49 uniforms (P(max <= x) = x^49, exactly samplePowerCosine's distribution for
+ * exponent 48) with a rejection-sampled azimuth. */
+#define PS_GLOSSY_E 48.0
+
+PS_HD int ps_is_steps(const ps_params *P, int w) { return P->glossy && (w == 2 || w == 4); }
+
+PS_HD ps_v3 ps_diffuse_albedo(const ps_params *P, int w) {
+    if (!P->glossy) return ps_albedo(w);
+    if (ps_is_steps(P, w)) return ps_v(0.2, 0.18, 0.15);
+    return ps_v(0.6, 0.6, 0.6);
+}
+
+PS_HD double ps_pow48(double c) { /* c^48 = c^32 c^16, one fixed product sequence */
+    double c2 = c * c, c4 = c2 * c2, c8 = c4 * c4, c16 = c8 * c8, c32 = c16 * c16;
+    return c32 * c16;
+}
+
+PS_HD ps_v3 ps_reflect(ps_v3 wo, ps_v3 n) { /* mirror of wo about n (vecmath reflect) */
+    double k = 2.0 * ps_dot(wo, n);
+    return ps_v(n.x * k - wo.x, n.y * k - wo.y, n.z * k - wo.z);
+}
+
+/* evalBsdf (scene.cpp:342-356) of a steps/wall vertex; lambertian Cornell walls otherwise */
+PS_HD ps_v3 ps_eval_bsdf(const ps_params *P, int w, ps_v3 wi, ps_v3 wo, ps_v3 n) {
+    double cosI = ps_dot(wi, n), cosO = ps_dot(wo, n);
+    if (cosI <= 0.0 || cosO <= 0.0) return ps_v(0.0, 0.0, 0.0);
+    ps_v3 a = ps_diffuse_albedo(P, w);
+    ps_v3 f = ps_v(a.x * PS_INV_PI, a.y * PS_INV_PI, a.z * PS_INV_PI);
+    if (ps_is_steps(P, w)) {
+        double cosA = ps_dot(wi, ps_reflect(wo, n));
+        if (cosA > 0.0) {
+            double g = 0.6 * ((PS_GLOSSY_E + 2.0) * PS_INV_PI * 0.5 * ps_pow48(cosA));
+            f = ps_v(f.x + g, f.y + g, f.z + g);
+        }
+    }
+    return f;
+}
+
+PS_HD double ps_q_diffuse(const ps_params *P, int w) { /* lobeProbs (scene.cpp:331-338) */
+    if (!ps_is_steps(P, w)) return 1.0;
+    double ld = 0.2126 * 0.2 + 0.7152 * 0.18 + 0.0722 * 0.15, lg = 0.6;
+    return ld / (ld + lg);
+}
+
+/* pdfBsdf (scene.cpp:358-368), per steradian */
+PS_HD double ps_pdf_bsdf(const ps_params *P, int w, ps_v3 wi, ps_v3 wo, ps_v3 n) {
+    if (ps_dot(wo, n) <= 0.0) return 0.0;
+    double qd = ps_q_diffuse(P, w);
+    double cosI = ps_dot(wi, n);
+    double pdf = qd * (cosI > 0.0 ? cosI * PS_INV_PI : 0.0);
+    if (qd < 1.0) {
+        double cosA = ps_dot(wi, ps_reflect(wo, n));
+        pdf += (1.0 - qd) * (cosA > 0.0 ? (PS_GLOSSY_E + 1.0) * (0.5 * PS_INV_PI) * ps_pow48(cosA) : 0.0);
+    }
+    return pdf;
+}
+
+/* an orthonormal frame around m (|m| = 1) with exact operations (buildFrame-like) */
+PS_HD void ps_frame(ps_v3 m, ps_v3 *t, ps_v3 *b) {
+    double sign = m.z >= 0.0 ? 1.0 : -1.0;
+    double a = -1.0 / (sign + m.z);
+    double bb = m.x * m.y * a;
+    *t = ps_v(1.0 + sign * m.x * m.x * a, sign * bb, -sign * m.x);
+    *b = ps_v(bb, sign + m.y * m.y * a, -m.y);
+}
+
 /* Writes the B vertices of one path into a contiguous SoA buffer of n_total vertices. */
 PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t *flags,
                        uint64_t n_total) {
@@ -170,7 +243,7 @@ PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t 
     for (int b = 0; b < P->bounces; ++b) {
         const uint64_t vi = (uint64_t)b * n_paths + lpath;
         ps_v3 n = ps_wall_normal(wall);
-        ps_v3 alb = ps_albedo(wall);
+        ps_v3 alb = ps_diffuse_albedo(P, wall);
         ps_v3 wo = ps_v(-d.x, -d.y, -d.z);
         double cosO = ps_dot(wo, n);
         uint32_t fl = 0;
@@ -192,10 +265,17 @@ PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t 
                 double pdfSigma = PS_LAMP_PDF_AREA * distSq / cosLight;
                 double cosX = ps_dot(dl, n);
                 double fr = 0.0, fg = 0.0, fb = 0.0;
-                if (cosX > 0.0 && cosO > 0.0) {
-                    fr = alb.x * PS_INV_PI; fg = alb.y * PS_INV_PI; fb = alb.z * PS_INV_PI;
+                double contPdf;
+                if (P->glossy) {
+                    ps_v3 fv = ps_eval_bsdf(P, wall, dl, wo, n);
+                    fr = fv.x; fg = fv.y; fb = fv.z;
+                    contPdf = ps_pdf_bsdf(P, wall, dl, wo, n);
+                } else {
+                    if (cosX > 0.0 && cosO > 0.0) {
+                        fr = alb.x * PS_INV_PI; fg = alb.y * PS_INV_PI; fb = alb.z * PS_INV_PI;
+                    }
+                    contPdf = cosX > 0.0 ? cosX * PS_INV_PI : 0.0;
                 }
-                double contPdf = cosX > 0.0 ? cosX * PS_INV_PI : 0.0;
                 double mis = pdfSigma / (pdfSigma + contPdf);
                 double rr = fr * PS_LAMP_EMISSION, rg = fg * PS_LAMP_EMISSION, rb = fb * PS_LAMP_EMISSION;
                 neeFli[0] = rr * mis; neeFli[1] = rg * mis; neeFli[2] = rb * mis;
@@ -217,11 +297,40 @@ PS_HD void ps_gen_path(const ps_params *P, uint64_t path, double *f64, uint32_t 
         if (!(r2 < 1.0)) { a = 0.0; c2 = 0.0; r2 = 0.0; }
         double cz = sqrt(1.0 - r2);
         ps_v3 wi = ps_to_world(wall, a, c2, cz);
-        double cosI = ps_dot(wi, n);
-        double pdfSigma = cosI > 0.0 ? cosI * PS_INV_PI : 0.0;
+        double cosI, pdfSigma;
+        double fcont[3] = {alb.x * PS_INV_PI, alb.y * PS_INV_PI, alb.z * PS_INV_PI};
+        if (P->glossy) {
+            /* sampleBsdf (scene.cpp:370-389): lobe by luminance, Phong lobe about the mirror */
+            if (ps_is_steps(P, wall) && ps_rand(base, (uint32_t)b, 200) >= ps_q_diffuse(P, wall)) {
+                double ct = 0.0;
+                for (uint32_t k = 0; k < 49; ++k) { /* cos(theta) = max of 49 uniforms */
+                    double u = ps_rand(base, (uint32_t)b, 300 + k);
+                    ct = u > ct ? u : ct;
+                }
+                double st = sqrt(1.0 - ct * ct);
+                double len = sqrt(r2);
+                double cp = len > 0.0 ? a / len : 1.0, sp = len > 0.0 ? c2 / len : 0.0;
+                ps_v3 m = ps_reflect(wo, n), t, bt;
+                ps_frame(m, &t, &bt);
+                double lx = st * cp, ly = st * sp;
+                wi = ps_v(t.x * lx + bt.x * ly + m.x * ct, t.y * lx + bt.y * ly + m.y * ct,
+                          t.z * lx + bt.z * ly + m.z * ct);
+                if (ps_dot(wi, n) <= 0.0) { /* below the horizon: mirrored back above (the
+                                               synthetic paths keep exactly B vertices) */
+                    double k2 = 2.0 * ps_dot(wi, n);
+                    wi = ps_v(wi.x - n.x * k2, wi.y - n.y * k2, wi.z - n.z * k2);
+                }
+            }
+            ps_v3 fv = ps_eval_bsdf(P, wall, wi, wo, n);
+            fcont[0] = fv.x; fcont[1] = fv.y; fcont[2] = fv.z;
+            cosI = ps_dot(wi, n);
+            pdfSigma = ps_pdf_bsdf(P, wall, wi, wo, n);
+        } else {
+            cosI = ps_dot(wi, n);
+            pdfSigma = cosI > 0.0 ? cosI * PS_INV_PI : 0.0;
+        }
         double ratio = (cosI > 0.0 && pdfSigma > 0.0) ? cosI / (pdfSigma * 1.0) : 0.0;
         double pdfProj = cosI > 0.0 ? pdfSigma / cosI : 0.0;
-        double fcont[3] = {alb.x * PS_INV_PI, alb.y * PS_INV_PI, alb.z * PS_INV_PI};
 
         double nfp = 0.0, nemis = 0.0, nmis = 1.0;
         ps_v3 npos = ps_v(0.0, 0.0, 0.0);

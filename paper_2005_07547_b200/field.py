@@ -112,6 +112,7 @@ def lib():
         "pstf_cv_lookup": ([vp, vp, u64, vp, vp, vp, vp, vp], i32),
         "pstf_synth_generate": ([i32, i32, i32, u64, u64, d, vp, vp], i32),
         "pstf_synth_generate_stripe": ([i32, i32, i32, u64, u64, d, u64, u64, vp, vp], i32),
+        "pstf_synth_generate_scene": ([i32, i32, i32, i32, u64, u64, d, u64, u64, vp, vp], i32),
         "pstf_vertex_soa_from_buffer": ([vp, u64, vp], None),
         "pstf_profile_enable": ([i32], i32),
         "pstf_field_probe_histogram": ([vp, vp], i32),
@@ -578,17 +579,18 @@ def vertex_soa(buf, n) -> _VertexSoa:
 
 
 def synth_generate(width, height, bounces, seed=0x5EED, iteration=0, cam_shift_x=0.0, out=None,
-                   path0=0, npaths=None):
+                   path0=0, npaths=None, scene=0):
     """Synthetic Cornell stream on the device (pstf_synth.h) -> fp64 CUDA tensor buffer.
-    path0/npaths select an image stripe (paths [path0, path0+npaths), all bounces)."""
+    path0/npaths select an image stripe (paths [path0, path0+npaths), all bounces); scene 1:
+    the glossy materials of staircase_glossy.scene (BASELINE config 3)."""
     t = _torch()
     npaths = width * height - path0 if npaths is None else npaths
     n = npaths * bounces
     words = 34 * n + (n + 1) // 2
     if out is None:
         out = t.empty(words, dtype=t.float64, device="cuda")
-    _check(lib().pstf_synth_generate_stripe(width, height, bounces, seed, iteration, cam_shift_x,
-                                            path0, npaths, _ptr(out), _stream()))
+    _check(lib().pstf_synth_generate_scene(scene, width, height, bounces, seed, iteration,
+                                           cam_shift_x, path0, npaths, _ptr(out), _stream()))
     return out, n
 
 

@@ -199,6 +199,39 @@ def test_crafted_streams(li, pad):
     assert sum(s.stats()["rejected"] for s in r_atm) > 0
 
 
+# --------------------------------------------------- config 3: glossy stream + CV at every vertex
+def test_glossy_stream_with_cv_lookup():
+    """BASELINE config 3 shape at a reduced frame: the glossy synthetic stream (scene 1) through
+    the tiled kernel with the fused CV lookup (estimators.cpp:453-462) against the reference
+    replay; the CV outputs equal the reference's LoE query on the frame-start table"""
+    if not po.ref_available():
+        pytest.skip("oracle/_ref not built")
+    base = (12.0 ** 0.5) / 256.0
+    gcfg = dict(capacity_log2=16, max_level=4, base_cell_size=base, level_select_k=4.0,
+                t_max=64.0, probe_window=32, evict_age_frames=64)
+    g = _gpu_stores(gcfg, False)
+    r = _ref_stores(dict(capacity_log2=16, base_cell_size=base), False, (7, 7))
+    for it in range(5):
+        host, n = po.synth_generate(192, 108, 4, iteration=it, scene=1)
+        dev, soa = gu.device_stream(host, n, pad=True)
+        f64, _ = crafted.views(host, n)
+        want_v, want_ok, _, _ = r[1].query_batch(f64[0:3].T, f64[3:6].T, fp=f64[15])
+        pb.profile_enable(True)
+        pb.profile_collect()
+        val, ok = pb.vertex_pass_cv(g[0], g[1], g[2], None, dev, n, soa=soa)
+        assert gu.launched("k_vertex_pass_tiled")
+        pb.profile_enable(False)
+        pb.end_frame_all(g)
+        po.vertex_pass_ref(r[0], r[1], r[2], None, host, n, deterministic=True)
+        for s in r:
+            s.end_frame()
+        np.testing.assert_array_equal(ok.cpu().numpy().astype(bool), np.asarray(want_ok, bool))
+        np.testing.assert_allclose(val.cpu().numpy().T, want_v, rtol=1e-9, atol=1e-300)
+        for a, b in zip(g, r):
+            gu.assert_slots_close(a.slots(), b.slots(), rtol=1e-9, atol=1e-300)
+            _ref_stats_equal(a, b.stats())
+
+
 # ------------------------------------------------------------- one full config-2 iteration
 @pytest.mark.slow
 def test_config2_full_iterations_vs_reference():
