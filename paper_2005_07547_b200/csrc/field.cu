@@ -174,6 +174,9 @@ struct Scratch {
     DBuf hio;                               // host-pointer API staging
     DBuf ulist, overflow;                   // sharding: packed live list, pack-overflow flag
     DBuf ef_done;                           // one-pass endFrame: blocks done (last rolls)
+    DBuf pend2, pend2_slot, pend2_count;    // ORDERED: value calls of existing slots
+    DBuf o_key, o_key2, o_idx, o_idx2, o_tgt, o_flag; // their slot-grouped sort (o_tgt: run marks)
+    DBuf o_fp, o_fk;                                  // its marked runs' re-sort
     uint64_t live_bound = 0;
     long long *live_total_dev = nullptr;
     bool overflow_zeroed = false;
@@ -304,6 +307,12 @@ struct VPArgs {
     PendRec *pend;
     unsigned long long *pend_count;
     uint64_t pend_cap;
+    /* ORDERED: value calls whose key already owns a slot (phase 1 found it) go here with the
+     * slot, for the slot-grouped fold (fold_slot_records) */
+    PendRec *pend2;
+    uint32_t *pend2_slot;
+    unsigned long long *pend2_count;
+    uint64_t pend2_cap;
 };
 
 #define VP_BLOCK 256
@@ -437,8 +446,8 @@ __device__ __forceinline__ void contribute_atomic(const DevStore &s, const PendS
  * counter is therefore applied in place (cNew += 1, lastTouched = frame: field.cpp:122-124,
  * 157) and only a new key's counter becomes a record (its placement needs one); a full window
  * counts the drop (field.cpp:145).  This halves the records the canonical sort has to order. */
-__device__ __forceinline__ void count_call(const DevStore &s, const PendSink &a, bool want,
-                                           int sid, const Key &k) {
+__device__ __forceinline__ int count_call(const DevStore &s, const PendSink &a, bool want,
+                                          int sid, const Key &k) {
     int res = -3;
     uint32_t mark = 0;
     if (want) res = probe_existing(s, k.pack_lo & s.mask, k.checksum, &mark);
@@ -449,15 +458,28 @@ __device__ __forceinline__ void count_call(const DevStore &s, const PendSink &a,
     if (PendRec *p = warp_reserve(a, res == -1))
         put_record(p, k, PSTF_META(sid, 1, 1) | ((uint32_t)s.rank << 3), 0.0, 0.0, 0.0, 1.0);
     if (res == -2) atomicAdd(&s.ctr[C_DROPPED], 1ull);
+    return res;
 }
 
-/* ORDERED mode: every other call becomes a record. */
-__device__ __forceinline__ void emit_call(const PendSink &a, bool want, int sid, const Key &k,
-                                          bool is_counter, double r_, double g_, double b_,
-                                          double w) {
-    if (PendRec *p = warp_reserve(a, want))
-        put_record(p, k, PSTF_META(sid, is_counter ? 1 : 0, 1), r_, g_, b_, w);
+/* ORDERED mode, a value call (weight 1.0) of a key whose counter call just probed the
+ * frame-start table with result res: an existing slot's call goes to the slot-grouped records
+ * (no placement needed; an all-zero value is a no-op on the accumulator — it starts at +0.0 and
+ * can never become -0.0 — and is not emitted), a new key's call to the pending records, and a
+ * call whose window is full counts one drop (field.cpp:145) */
+__device__ __forceinline__ void value_call(const DevStore &s, const PendSink &a,
+                                           const PendSink &a2, uint32_t *slot2, bool want,
+                                           int res, int sid, const Key &k, double r_, double g_,
+                                           double b_) {
+    const bool zero = r_ == 0.0 && g_ == 0.0 && b_ == 0.0;
+    if (PendRec *p = warp_reserve(a2, want && res >= 0 && !zero)) {
+        put_record(p, k, PSTF_META(sid, 0, 1), r_, g_, b_, 1.0);
+        slot2[p - a2.pend] = (uint32_t)res;
+    }
+    if (PendRec *p = warp_reserve(a, want && res == -1))
+        put_record(p, k, PSTF_META(sid, 0, 1), r_, g_, b_, 1.0);
+    if (want && res == -2) atomicAdd(&s.ctr[C_DROPPED], 1ull);
 }
+
 
 template <int MODE>
 __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
@@ -635,34 +657,36 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
     } else {
         /* ORDERED: the reference's individual calls, in any order (the sort canonicalises) */
         const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+        const PendSink ps2{a.pend2, a.pend2_count, a.pend2_cap};
+        uint32_t *const sl2 = a.pend2_slot;
         unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
-        count_call(sLo, ps, live, 0, kLo);
+        int res = count_call(sLo, ps, live, 0, kLo);
         bool ok = finite3(ehx, ehy, ehz);
         rejLo += live && !ok;
-        emit_call(ps, live && ok, 0, kLo, false, ehx, ehy, ehz, 1.0);
+        value_call(sLo, ps, ps2, sl2, live && ok, res, 0, kLo, ehx, ehy, ehz);
         ok = finite3(ulx, uly, ulz);
         rejLo += live && transp && !ok;
-        emit_call(ps, live && transp && ok, 0, kLo, false, ulx, uly, ulz, 1.0);
-        count_call(sLoe, ps, live, 1, kLoe);
+        value_call(sLo, ps, ps2, sl2, live && transp && ok, res, 0, kLo, ulx, uly, ulz);
+        res = count_call(sLoe, ps, live, 1, kLoe);
         ok = finite3(uex, uey, uez);
         rejLoe += live && loeCont && !ok;
-        emit_call(ps, live && loeCont && ok, 1, kLoe, false, uex, uey, uez, 1.0);
+        value_call(sLoe, ps, ps2, sl2, live && loeCont && ok, res, 1, kLoe, uex, uey, uez);
         ok = finite3(nlx, nly, nlz);
         rejLoe += live && loeNee && !ok;
-        emit_call(ps, live && loeNee && ok, 1, kLoe, false, nlx, nly, nlz, 1.0);
-        count_call(sFli, ps, live && cont, 2, kFc);
+        value_call(sLoe, ps, ps2, sl2, live && loeNee && ok, res, 1, kLoe, nlx, nly, nlz);
+        res = count_call(sFli, ps, live && cont, 2, kFc);
         ok = finite3(fcx, fcy, fcz);
         rejFli += live && fliCont && !ok;
-        emit_call(ps, live && fliCont && ok, 2, kFc, false, fcx, fcy, fcz, 1.0);
-        count_call(sFli, ps, live && nee, 2, kFn);
+        value_call(sFli, ps, ps2, sl2, live && fliCont && ok, res, 2, kFc, fcx, fcy, fcz);
+        res = count_call(sFli, ps, live && nee, 2, kFn);
         ok = finite3(nfx, nfy, nfz);
         rejFli += live && fliNee && !ok;
-        emit_call(ps, live && fliNee && ok, 2, kFn, false, nfx, nfy, nfz, 1.0);
+        value_call(sFli, ps, ps2, sl2, live && fliNee && ok, res, 2, kFn, nfx, nfy, nfz);
         if (a.has_li) {
-            count_call(sLi, ps, live && cont, 3, kLi);
+            res = count_call(sLi, ps, live && cont, 3, kLi);
             ok = finite3(lvx, lvy, lvz);
             rejLi += live && cont && !ok;
-            emit_call(ps, live && cont && ok, 3, kLi, false, lvx, lvy, lvz, 1.0);
+            value_call(sLi, ps, ps2, sl2, live && cont && ok, res, 3, kLi, lvx, lvy, lvz);
         }
         if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
         if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
@@ -3156,6 +3180,462 @@ static int resolve_pending(Scratch &sc, pstf_field *const *fs, int nf, int mode,
     return PSTF_OK;
 }
 
+__global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
+
+/* ---- ORDERED vertex passes: the value calls of keys that already own a slot ----
+ * FieldUpdateQueue::apply (field.cpp:396-420) sorts every call by (key, isCounter, bits r, g, b,
+ * w) and applies them in that order; a slot's accumulator therefore sums its value calls in the
+ * order of their value bits (all of one key, weight 1.0).  These calls need no placement:
+ *   1. one 64-bit sort key per record: store and slot in the top S bits, the leading 64 - S bits
+ *      of bits(r) below (one CUB radix sort of (key, index));
+ *   2. the components gathered in that order (three arrays r | g | b);
+ *   3. the only calls that can be out of (r, g, b) order are inside runs of equal sort keys
+ *      (equal leading bits of r: r values an ulp apart, or equal r with different g, b): each
+ *      run holding an out-of-order neighbour pair is re-sorted in place, by one thread
+ *      (insertion, <= 32 calls), by one block (bitonic in shared memory, <= 4096 calls), or,
+ *      longer, compacted with the other such runs and radix-sorted least significant word first
+ *      (b, g, then run start with the low bits of r);
+ *   4. the terms folded sequentially per slot (a warp per long slot: three lanes carry the r, g
+ *      and b sums).
+ * A record whose key is not its slot's (a checksum alias sharing the slot: the queue would order
+ * the two keys' calls apart) or whose weight is not 1 sends all of them through the general
+ * path, decided before anything is folded. */
+__global__ void k_slot_keys(const PendRec *__restrict__ r, const uint32_t *__restrict__ slot,
+                            uint64_t n, int capl, Stores4 st, uint64_t *key, uint32_t *idx,
+                            unsigned int *flag) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 k0 = reinterpret_cast<const int4 *>(r + i)[0];
+    const int4 k1 = reinterpret_cast<const int4 *>(r + i)[1];
+    const double r0 = r[i].v[0], w = r[i].v[3];
+    const uint32_t sid = PSTF_META_SID((uint32_t)k1.w), sl = slot[i];
+    const KeyFields kf = st.s[sid].keyf[sl];
+    const bool bad = kf.level != k0.x || kf.c0 != k0.y || kf.c1 != k0.z || kf.c2 != k0.w ||
+                     kf.d0 != k1.x || kf.d1 != k1.y || dbits(w) != dbits(1.0);
+    if (bad && (atomicOr(flag, 1u) & 1u) == 0) flag[2] = (unsigned int)i; /* first seen */
+    const int S = capl + 2;
+    const uint64_t sk = ((uint64_t)sid << capl) | sl;
+    key[i] = (sk << (64 - S)) | (dbits(r0) >> S);
+    idx[i] = (uint32_t)i;
+}
+
+/* own position at each run head of the sorted keys (0 elsewhere): a max-scan gives every
+ * position its run's start */
+__global__ void k_run_head_pos(const uint64_t *key, uint64_t n, uint32_t *hp) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < n) hp[j] = (j == 0 || key[j] != key[j - 1]) ? (uint32_t)j : 0u;
+}
+
+/* the canonical order of two value calls (weight 1 each): bits of r, then g, then b */
+__device__ __forceinline__ bool t_less(const double *T, uint64_t n, uint64_t a, uint64_t b) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const uint64_t x = dbits(T[c * n + a]), y = dbits(T[c * n + b]);
+        if (x != y) return x < y;
+    }
+    return false;
+}
+
+/* the sorted terms: an out-of-order neighbour pair inside a run of equal keys marks the run (bit
+ * at its start); each run's length is written at its start */
+__global__ void k_run_check(const double *__restrict__ T, const uint64_t *__restrict__ key,
+                            const uint32_t *__restrict__ rstart, uint64_t n, uint32_t *claim,
+                            uint32_t *runlen) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint64_t k = key[j];
+    const uint32_t s0 = rstart[j];
+    if (j > 0 && k == key[j - 1] && t_less(T, n, j, j - 1))
+        atomicOr(&claim[s0 >> 5], 1u << (s0 & 31u));
+    if (j == n - 1 || key[j + 1] != k) runlen[s0] = (uint32_t)(j + 1 - s0);
+}
+
+#define FIX_THREAD 32  /* marked runs up to this long: insertion sort by one thread */
+#define FIX_BLOCK 4096 /* up to this long: bitonic sort in shared memory by one block */
+
+/* the marked runs, by length: lists (start, length) for the thread and block sorters; longer
+ * runs are marked again (claim2) for the radix path and counted (flag bit 2, cnt[3] records) */
+__global__ void k_run_lists(const uint32_t *__restrict__ hp, const uint32_t *__restrict__ claim,
+                            const uint32_t *__restrict__ runlen, uint64_t n, uint2 *lst_t,
+                            uint2 *lst_b, unsigned int *cnt, uint32_t *claim2) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n || (j > 0 && hp[j] == 0)) return; /* run heads only */
+    if (!((claim[j >> 5] >> (j & 31u)) & 1u)) return;
+    const uint32_t len = runlen[j];
+    if (len <= FIX_THREAD) {
+        lst_t[atomicAdd(&cnt[4], 1u)] = make_uint2((uint32_t)j, len);
+    } else if (len <= FIX_BLOCK) {
+        lst_b[atomicAdd(&cnt[5], 1u)] = make_uint2((uint32_t)j, len);
+    } else {
+        atomicOr(&claim2[j >> 5], 1u << (j & 31u));
+        atomicOr(&cnt[0], 2u);
+        atomicAdd(&cnt[3], len);
+    }
+}
+
+__global__ void k_fix_thread(double *T, uint64_t n, const uint2 *lst, const unsigned int *cnt) {
+    const uint32_t nl = cnt[4];
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nl;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j0 = lst[e].x, j1 = j0 + lst[e].y;
+        for (uint32_t p = j0 + 1; p < j1; ++p) {
+            const double r = T[p], g = T[n + p], b = T[2 * n + p];
+            uint32_t t = p;
+            while (t > j0) {
+                const uint64_t x[3] = {dbits(r), dbits(g), dbits(b)};
+                const uint64_t y[3] = {dbits(T[t - 1]), dbits(T[n + t - 1]), dbits(T[2 * n + t - 1])};
+                const bool lt = x[0] != y[0] ? x[0] < y[0] : x[1] != y[1] ? x[1] < y[1] : x[2] < y[2];
+                if (!lt) break;
+                T[t] = T[t - 1];
+                T[n + t] = T[n + t - 1];
+                T[2 * n + t] = T[2 * n + t - 1];
+                --t;
+            }
+            T[t] = r;
+            T[n + t] = g;
+            T[2 * n + t] = b;
+        }
+    }
+}
+
+/* one block per marked run of up to FIX_BLOCK calls: bitonic sort of the (r, g, b) bit triples
+ * in shared memory (padded with all-ones: never a finite value) */
+__global__ void __launch_bounds__(512) k_fix_block(double *T, uint64_t n, const uint2 *lst,
+                                                   const unsigned int *cnt) {
+    extern __shared__ uint64_t fsm[];
+    uint64_t *kr = fsm, *kg = fsm + FIX_BLOCK, *kb = fsm + 2 * FIX_BLOCK;
+    const uint32_t nl = cnt[5];
+    for (uint32_t e = blockIdx.x; e < nl; e += gridDim.x) {
+        const uint32_t j0 = lst[e].x, len = lst[e].y;
+        uint32_t N = 64;
+        while (N < len) N <<= 1;
+        for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+            const bool in = i < len;
+            kr[i] = in ? dbits(T[j0 + i]) : ~0ull;
+            kg[i] = in ? dbits(T[n + j0 + i]) : ~0ull;
+            kb[i] = in ? dbits(T[2 * n + j0 + i]) : ~0ull;
+        }
+        __syncthreads();
+        for (uint32_t k = 2; k <= N; k <<= 1)
+            for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+                for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+                    const uint32_t q = i ^ h;
+                    if (q <= i) continue;
+                    const bool gt = kr[i] != kr[q] ? kr[i] > kr[q]
+                                    : kg[i] != kg[q] ? kg[i] > kg[q] : kb[i] > kb[q];
+                    if (gt == ((i & k) == 0)) {
+                        uint64_t t = kr[i]; kr[i] = kr[q]; kr[q] = t;
+                        t = kg[i]; kg[i] = kg[q]; kg[q] = t;
+                        t = kb[i]; kb[i] = kb[q]; kb[q] = t;
+                    }
+                }
+                __syncthreads();
+            }
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+            T[j0 + i] = __longlong_as_double((long long)kr[i]);
+            T[n + j0 + i] = __longlong_as_double((long long)kg[i]);
+            T[2 * n + j0 + i] = __longlong_as_double((long long)kb[i]);
+        }
+        __syncthreads();
+    }
+}
+
+/* records in the runs too long for a block (claim2 at their start): flags for the compaction */
+__global__ void k_run_marked(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ claim,
+                             uint64_t n, uint8_t *in) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t s0 = rstart[j];
+    in[j] = (claim[s0 >> 5] >> (s0 & 31u)) & 1u;
+}
+
+/* their radix key for the pass c: 0 bits(b), 1 bits(g), 2 (run start, the low S bits of bits(r):
+ * the rest of r is the run's sort key) */
+__global__ void k_fix_keys(const double *__restrict__ T, uint64_t n,
+                           const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ perm,
+                           uint64_t m, int c, int S, uint64_t *out) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const uint32_t j = perm[q];
+    out[q] = c == 2 ? ((uint64_t)rstart[j] << S) | (dbits(T[j]) & ((1ull << S) - 1ull))
+                    : dbits(T[(2 - c) * n + j]);
+}
+
+/* apply the permutation: the terms at positions perm[q] move to positions pos[q] (both lists
+ * hold the same positions) */
+__global__ void k_fix_take(const double *__restrict__ T, uint64_t n, const uint32_t *__restrict__ perm,
+                           uint64_t m, double *tmp) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const uint32_t j = perm[q];
+    tmp[q] = T[j];
+    tmp[m + q] = T[n + j];
+    tmp[2 * m + q] = T[2 * n + j];
+}
+
+__global__ void k_fix_put(const double *__restrict__ tmp, const uint32_t *__restrict__ pos,
+                          uint64_t m, double *T, uint64_t n) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const uint32_t j = pos[q];
+    T[j] = tmp[q];
+    T[n + j] = tmp[m + q];
+    T[2 * n + j] = tmp[2 * m + q];
+}
+
+/* heads of the slots' segments in the sorted order */
+__global__ void k_slot_heads(const uint64_t *key, uint64_t n, int S, uint32_t *head) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < n) head[j] = j == 0 || (key[j] >> (64 - S)) != (key[j - 1] >> (64 - S));
+}
+
+#define SLOT_FOLD_WARP 32 /* slots with more value calls than this are folded by a warp */
+
+/* the value calls' components in the sorted order, one array each (r, g, b) */
+__global__ void k_slot_terms(const PendRec *__restrict__ r, const uint32_t *__restrict__ idx,
+                             uint64_t n, double *__restrict__ T) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const PendRec &p = r[idx[q]];
+    T[q] = p.v[0];
+    T[n + q] = p.v[1];
+    T[2 * n + q] = p.v[2];
+}
+
+__device__ __forceinline__ double4 *slot_acc(const Stores4 &st, uint64_t key, int capl) {
+    const int S = capl + 2;
+    const uint64_t sk = key >> (64 - S);
+    return acc_ptr(st.s[sk >> capl], sk & ((1ull << capl) - 1ull));
+}
+
+/* short slots, one thread each: acc += v (weight 1.0, field.cpp:168-170) in the sorted order */
+__global__ void k_slot_fold(const double *__restrict__ T, uint64_t n,
+                            const uint64_t *__restrict__ key, const uint32_t *__restrict__ start,
+                            const uint32_t *__restrict__ nseg, int capl, Stores4 st) {
+    const uint32_t ns = *nseg;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < ns;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q0 = start[g], q1 = start[g + 1];
+        if (q1 - q0 > SLOT_FOLD_WARP) continue;
+        double4 *dst = slot_acc(st, key[q0], capl);
+        double4 acc = *dst;
+        for (uint32_t q = q0; q < q1; ++q) {
+            acc.x += T[q];
+            acc.y += T[n + q];
+            acc.z += T[2 * n + q];
+        }
+        *dst = acc;
+    }
+}
+
+/* long slots, one warp each: the warp loads the next 8 x 32 terms of each component (coalesced,
+ * in flight while the current ones are summed) and lanes 0, 1, 2 add the r, g, b components in
+ * order from shared memory */
+#define SFL_G 8
+__global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict__ T, uint64_t n,
+                                                        const uint64_t *__restrict__ key,
+                                                        const uint32_t *__restrict__ start,
+                                                        const uint32_t *__restrict__ nseg,
+                                                        int capl, Stores4 st) {
+    __shared__ double sv[8][3][SFL_G * 32];
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const uint32_t ns = *nseg;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; g < ns; g += nwarps) {
+        const uint32_t q0 = start[g], q1 = start[g + 1];
+        if (q1 - q0 <= SLOT_FOLD_WARP) continue; /* warp-uniform */
+        double4 *dst = slot_acc(st, key[q0], capl);
+        const unsigned c = lane < 3 ? lane : 0;
+        double acc = (&dst->x)[c];
+        double nx[3][SFL_G];
+        const auto fetch = [&](uint32_t q) {
+#pragma unroll
+            for (int k = 0; k < SFL_G; ++k) {
+                const uint32_t e = q + k * 32 + lane;
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) nx[cc][k] = e < q1 ? T[cc * n + e] : 0.0;
+            }
+        };
+        fetch(q0);
+        for (uint32_t q = q0; q < q1; q += SFL_G * 32) {
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < SFL_G; ++k)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) sv[w][cc][k * 32 + lane] = nx[cc][k];
+            __syncwarp();
+            if (q + SFL_G * 32 < q1) fetch(q + SFL_G * 32);
+            const uint32_t cnt = min((uint32_t)(SFL_G * 32), q1 - q);
+            if (lane < 3) {
+                const double *v = sv[w][c];
+                if (cnt == SFL_G * 32) {
+#pragma unroll 32
+                    for (int k = 0; k < SFL_G * 32; ++k) acc += v[k];
+                } else {
+                    for (uint32_t k = 0; k < cnt; ++k) acc += v[k];
+                }
+            }
+        }
+        if (lane < 3) (&dst->x)[c] = acc;
+    }
+}
+
+/* returns through *fallback whether the records must take the general path instead */
+static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_t n,
+                             bool *fallback, cudaStream_t st) {
+    *fallback = false;
+    int capl = 0;
+    for (int i = 0; i < nf; ++i)
+        if (fs[i]) capl = std::max<int>(capl, (int)fs[i]->cfg.capacity_log2);
+    if (capl > 30 || n >= (1ull << 31)) {
+        *fallback = true;
+        return PSTF_OK;
+    }
+    const int S = capl + 2;
+    const PendRec *rec = sc.pend2.as<PendRec>();
+    const Stores4 S4 = stores4(fs, nf);
+    const uint64_t nw = (n + 31) / 32;
+    ENSURE(sc.o_key, n * 8);
+    ENSURE(sc.o_key2, n * 8);
+    ENSURE(sc.o_idx, n * 4);
+    ENSURE(sc.o_idx2, n * 4);
+    ENSURE(sc.o_flag, 32); /* [0] flags, [3] records in over-long runs, [4], [5] list sizes */
+    ENSURE(sc.head, n * 4);
+    ENSURE(sc.uid, n * 4);
+    ENSURE(sc.rank, n * 4);       /* run lengths (at run starts) */
+    ENSURE(sc.o_tgt, nw * 8);     /* run-mark bitmaps: marked, over-long */
+    ENSURE(sc.o_fp, n * 8);       /* (start, length) lists of the marked runs */
+    ENSURE(sc.fterms, n * 24);    /* the terms r | g | b in the sorted order */
+    ENSURE(sc.fstart, (n + 1) * 4);
+    ENSURE(sc.fnruns, 8);
+    uint64_t *key = sc.o_key.as<uint64_t>(), *key2 = sc.o_key2.as<uint64_t>();
+    uint32_t *idx0 = sc.o_idx.as<uint32_t>(), *idx = sc.o_idx2.as<uint32_t>();
+    unsigned int *flag = sc.o_flag.as<unsigned int>();
+    uint32_t *hp = sc.head.as<uint32_t>(), *rstart = sc.uid.as<uint32_t>();
+    uint32_t *claim = sc.o_tgt.as<uint32_t>(), *claim2 = claim + nw;
+    uint2 *lst_t = sc.o_fp.as<uint2>();
+    double *T = sc.fterms.as<double>();
+    CK(cudaMemsetAsync(sc.o_flag.p, 0, 32, st));
+    CK(cudaMemsetAsync(sc.o_tgt.p, 0, nw * 8, st));
+    LAUNCH(k_slot_keys, grid_for(n, 256), 256, 0, st, rec, sc.pend2_slot.as<uint32_t>(), n, capl,
+           S4, key, idx0, flag);
+    const auto cub_call = [&](const char *name, int nlaunch, auto &&fn) -> int {
+        size_t bytes = 0;
+        CK(fn((void *)nullptr, bytes));
+        ENSURE(sc.cub, bytes);
+        bytes = sc.cub.bytes;
+        ProfScope ps_(name, st);
+        CK(fn(sc.cub.p, bytes));
+        g_launches.fetch_add(nlaunch, std::memory_order_relaxed);
+        return PSTF_OK;
+    };
+    int rc = cub_call("cub::DeviceRadixSort", 4, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx0, idx, (int64_t)n, 0, 64, st);
+    });
+    if (rc) return rc;
+    LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, rec, idx, n, T);
+    /* runs of equal sort keys holding an out-of-order pair, re-sorted in place by length class */
+    LAUNCH(k_run_head_pos, grid_for(n, 256), 256, 0, st, key2, n, hp);
+    rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
+        return cub::DeviceScan::InclusiveScan(t, b, hp, rstart, cub::Max(), (int64_t)n, st);
+    });
+    if (rc) return rc;
+    LAUNCH(k_run_check, grid_for(n, 256), 256, 0, st, T, key2, rstart, n, claim,
+           sc.rank.as<uint32_t>());
+    /* at most n/2 marked runs in total (each holds two calls or more) */
+    uint2 *lst_b = lst_t + n / 2;
+    LAUNCH(k_run_lists, grid_for(n, 256), 256, 0, st, hp, claim, sc.rank.as<uint32_t>(), n, lst_t,
+           lst_b, flag, claim2);
+    const unsigned grid = (unsigned)sm_count() * 8;
+    LAUNCH(k_fix_thread, grid, 128, 0, st, T, n, lst_t, flag);
+    const size_t fsm = 3 * FIX_BLOCK * 8;
+    CK(cudaFuncSetAttribute(k_fix_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    LAUNCH(k_fix_block, (unsigned)sm_count() * 2, 512, fsm, st, T, n, lst_b, flag);
+    rc = read_small(sc, sc.o_flag.p, 24, st); /* the pass's one host read */
+    if (rc) return rc;
+    const uint32_t *h = (const uint32_t *)sc.h_small;
+    const uint32_t fl = h[0];
+    const uint64_t m = h[3];
+    if (getenv("PSTF_ORDERED_DEBUG"))
+        fprintf(stderr, "[ordered] %llu value calls of existing slots, flag %u, marked runs %u "
+                "(thread) %u (block), %llu calls in longer marked runs\n",
+                (unsigned long long)n, fl, h[4], h[5], (unsigned long long)m);
+    if (fl & 1u) { /* a checksum alias or a weight other than 1 */
+        *fallback = true;
+        return PSTF_OK;
+    }
+    if (m) { /* the runs too long for a block: b, g, then (run start, r) (stable, LSD) */
+        ENSURE(sc.fisc, n);
+        LAUNCH(k_run_marked, grid_for(n, 256), 256, 0, st, rstart, claim2, n, sc.fisc.as<uint8_t>());
+        uint32_t *F = sc.fstart.as<uint32_t>(); /* their positions, ascending */
+        rc = cub_call("cub::DeviceSelect", 2, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, cub::CountingInputIterator<uint32_t>(0),
+                                              sc.fisc.as<uint8_t>(), F, flag + 6, (int64_t)n, st);
+        });
+        if (rc) return rc;
+        ENSURE(sc.o_fk, m * 40);
+        uint32_t *P0 = reinterpret_cast<uint32_t *>(sc.o_fk.as<uint64_t>() + 4 * m), *P1 = P0 + m;
+        uint64_t *K0 = sc.o_fk.as<uint64_t>(), *K1 = K0 + m;
+        CK(cudaMemcpyAsync(P0, F, m * 4, cudaMemcpyDeviceToDevice, st));
+        int nbits = 1;
+        while ((1ull << nbits) < n) ++nbits;
+        for (int c = 0; c < 3; ++c) {
+            LAUNCH(k_fix_keys, grid_for(m, 256), 256, 0, st, T, n, rstart, P0, m, c, S, K0);
+            rc = cub_call("cub::DeviceRadixSort", 4, [&](void *t, size_t &b) {
+                return cub::DeviceRadixSort::SortPairs(t, b, K0, K1, P0, P1, (int64_t)m, 0,
+                                                       c == 2 ? nbits + S : 64, st);
+            });
+            if (rc) return rc;
+            std::swap(P0, P1);
+        }
+        double *tmp = reinterpret_cast<double *>(K0); /* 3m doubles: K0, K1 and the next m */
+        LAUNCH(k_fix_take, grid_for(m, 256), 256, 0, st, T, n, P0, m, tmp);
+        LAUNCH(k_fix_put, grid_for(m, 256), 256, 0, st, tmp, F, m, T, n);
+    }
+    /* one segment per slot, folded in that order */
+    LAUNCH(k_slot_heads, grid_for(n, 256), 256, 0, st, key2, n, S, hp);
+    rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, hp, rstart, (int64_t)n, st);
+    });
+    if (rc) return rc;
+    uint32_t *seg = sc.fstart.as<uint32_t>(); /* segment starts (+ the end sentinel) */
+    LAUNCH(k_fold_starts, grid_for(n, 256), 256, 0, st, hp, rstart, n, seg);
+    LAUNCH(k_fold_nruns, 1, 1, 0, st, hp, rstart, n, sc.fnruns.as<uint32_t>());
+    LAUNCH(k_slot_fold, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl, S4);
+    LAUNCH(k_slot_fold_long, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl,
+           S4);
+    return PSTF_OK;
+}
+
+/* ORDERED vertex pass, phase 2: the slot-grouped fold of existing slots' value calls, then the
+ * general path (sort, placement, fold) for the new keys' calls */
+static int resolve_ordered(Scratch &sc, pstf_field *const *fs, int nf, cudaStream_t st) {
+    int rc = read_small(sc, sc.pend_count.p, 8, st);
+    if (rc) return rc;
+    uint64_t n1 = sc.h_small[0];
+    rc = read_small(sc, sc.pend2_count.p, 8, st);
+    if (rc) return rc;
+    const uint64_t n2 = std::min<uint64_t>(sc.h_small[0], sc.pend2.bytes / sizeof(PendRec));
+    if (n2) {
+        bool fallback = false;
+        const bool force = getenv("PSTF_ORDERED_GENERAL") != nullptr; /* parity tests */
+        if (!force) {
+            rc = fold_slot_records(sc, fs, nf, n2, &fallback, st);
+            if (rc) return rc;
+        }
+        if (force || fallback) { /* append them to the general path's records */
+            if (n1 + n2 > sc.pend.bytes / sizeof(PendRec))
+                return set_err(PSTF_E_NOMEM, "pending-update buffer overflow");
+            CK(cudaMemcpyAsync(sc.pend.as<PendRec>() + n1, sc.pend2.p, n2 * sizeof(PendRec),
+                               cudaMemcpyDeviceToDevice, st));
+            n1 += n2;
+            LAUNCH(k_set_u64, 1, 1, 0, st, sc.pend_count.as<unsigned long long>(),
+                   (unsigned long long)n1);
+        }
+    }
+    return resolve_pending(sc, fs, nf, PSTF_MODE_ORDERED, n1, st);
+}
+
 /* Completes the deferred vertex pass (if any) that involves store cf: waits for its pending
  * count and places the new keys (phase 2). */
 static int settle(const pstf_field *cf) {
@@ -3182,6 +3662,7 @@ static int settle(const pstf_field *cf) {
 static int finish_vertex_pass(pstf_field *const fs[4], int mode, cudaStream_t st) {
     pstf_field *lo = fs[0];
     const int nf = fs[3] ? 4 : 3;
+    if (mode == PSTF_MODE_ORDERED) return resolve_ordered(lo->sc, fs, nf, st);
     static const bool no_defer = getenv("PSTF_NO_DEFER") != nullptr;
     if (no_defer) return resolve_pending(lo->sc, fs, nf, mode, (uint64_t)-1, st);
     DeferredPass &d = lo->dp;
@@ -3205,6 +3686,15 @@ static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t
     ENSURE(sc.pend_count, 8);
     if (with_seq) ENSURE(sc.pend_seq, cap * 8);
     CK(cudaMemsetAsync(sc.pend_count.p, 0, 8, st));
+    ENSURE(sc.pend2_count, 8);
+    CK(cudaMemsetAsync(sc.pend2_count.p, 0, 8, st));
+    return PSTF_OK;
+}
+
+/* ORDERED vertex passes: room for every value call of an existing slot (<= 7 per vertex) */
+static int ensure_pending2(Scratch &sc, uint64_t cap) {
+    ENSURE(sc.pend2, cap * sizeof(PendRec));
+    ENSURE(sc.pend2_slot, cap * 4);
     return PSTF_OK;
 }
 
@@ -4106,6 +4596,12 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
     a.pend = lo->sc.pend.as<PendRec>();
     a.pend_count = lo->sc.pend_count.as<unsigned long long>();
     a.pend_cap = lo->sc.pend.bytes / sizeof(PendRec);
+    if (mode == PSTF_MODE_ORDERED) {
+        a.pend2 = lo->sc.pend2.as<PendRec>();
+        a.pend2_slot = lo->sc.pend2_slot.as<uint32_t>();
+        a.pend2_count = lo->sc.pend2_count.as<unsigned long long>();
+        a.pend2_cap = std::min(lo->sc.pend2.bytes / sizeof(PendRec), lo->sc.pend2_slot.bytes / 4);
+    }
     const bool shared_quant = a.same_lo_loe && a.same_fli_lo && a.same_li_fli;
     /* TMA path: every SoA segment must be 16 B aligned for cp.async.bulk */
     const void *ptrs[35] = {v->position.x, v->position.y, v->position.z, v->wo.x, v->wo.y,
@@ -4246,6 +4742,10 @@ int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_fiel
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
+    if (mode == PSTF_MODE_ORDERED) {
+        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7));
+        if (rc) return rc;
+    }
     if (n) {
         rc = vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, mode, st);
         if (rc) return rc;
@@ -4275,6 +4775,10 @@ int pstf_vertex_pass_cv(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_f
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
+    if (mode == PSTF_MODE_ORDERED) {
+        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7));
+        if (rc) return rc;
+    }
     if (n) {
         const CvOut cv{cv_r, cv_g, cv_b, cv_valid};
         rc = vertex_phase1(lo, loe, fli, li, v, n, loe_mask, fli_mask, mode, st, &cv);
@@ -4330,6 +4834,10 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
+    if (mode == PSTF_MODE_ORDERED) {
+        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7));
+        if (rc) return rc;
+    }
     const uint64_t chunk = std::min<uint64_t>(n, 1ull << 21);
     static thread_local cudaStream_t cs = nullptr;
     static thread_local cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
@@ -4378,6 +4886,7 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
         CK(cudaEventRecord(ev_done[b], st));
     }
     pstf_field *fs[4] = {lo, loe, fli, li};
+    if (mode == PSTF_MODE_ORDERED) return resolve_ordered(lo->sc, fs, li ? 4 : 3, st);
     return resolve_pending(lo->sc, fs, li ? 4 : 3, mode, (uint64_t)-1, st);
 }
 
@@ -4502,8 +5011,6 @@ int pstf_pending_copy(pstf_field *lo, void *dst, uint64_t n, void *stream) {
                        (cudaStream_t)stream));
     return PSTF_OK;
 }
-
-__global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v; }
 
 int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, uint64_t n,
                          void *stream) {

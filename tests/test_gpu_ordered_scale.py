@@ -1,0 +1,58 @@
+"""ORDERED mode's slot-grouped fast path (field.cu, fold_slot_records) against the general path
+(every value call through the full canonical sort, PSTF_ORDERED_GENERAL) at scale: the config-2
+stream (1080p x 4 bounces, 2^22 slots), a coarse-cell stream whose hot slots take tens of
+thousands of calls (long runs of equal sort keys, the re-sorted marked runs), and the glossy
+scene.  Every slot array, accumulators included, must be bitwise identical frame after frame,
+and the fast path must actually have run."""
+import os
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import gpu_util as gu  # noqa: E402
+import inputs  # noqa: E402
+import paper_2005_07547_b200 as pb  # noqa: E402
+
+
+def _run(general, W, H, B, frames, cap, mult, evict, scene):
+    if general:
+        os.environ["PSTF_ORDERED_GENERAL"] = "1"
+    try:
+        gs = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=cap,
+                                                base_cell_size=inputs.BASE_CORNELL * mult,
+                                                evict_age_frames=evict))
+              for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
+        out, kernels = [], set()
+        for it in range(frames):
+            buf, n = pb.synth_generate(W, H, B, iteration=it, scene=scene)
+            pb.profile_enable(True)
+            pb.vertex_pass(gs[0], gs[1], gs[2], None, buf, n, mode=pb.MODE_ORDERED)
+            pb.profile_enable(False)
+            kernels |= set(pb.profile_collect())
+            pb.end_frame_all(gs)
+            out.append([s.slots() for s in gs])
+        return out, kernels
+    finally:
+        os.environ.pop("PSTF_ORDERED_GENERAL", None)
+
+
+@pytest.mark.parametrize("W,H,B,frames,cap,mult,evict,scene,fast_runs", [
+    (1920, 1080, 4, 3, 22, 1.0, 64, 0, True),   # config 2
+    (640, 360, 4, 4, 18, 4.0, 2, 0, True),      # coarser cells: hot slots, long runs, evictions
+    (640, 360, 4, 3, 18, 1.0, 64, 1, True),     # glossy scene
+    # very coarse cells: checksum aliases share slots, so the whole pass takes the general path
+    (640, 360, 4, 3, 16, 30.0, 2, 0, False),
+])
+def test_ordered_fast_path_equals_general(W, H, B, frames, cap, mult, evict, scene, fast_runs):
+    fast, kf = _run(False, W, H, B, frames, cap, mult, evict, scene)
+    gen, kg = _run(True, W, H, B, frames, cap, mult, evict, scene)
+    if fast_runs:
+        assert "k_slot_fold_long" in kf and "k_run_check" in kf  # the fast path ran
+    assert "k_slot_terms" not in kg
+    for it in range(frames):
+        for a, b in zip(fast[it], gen[it]):
+            gu.assert_slots_bitwise(a, b)
