@@ -174,7 +174,7 @@ struct Scratch {
     DBuf hio;                               // host-pointer API staging
     DBuf ulist, overflow;                   // sharding: packed live list, pack-overflow flag
     DBuf ef_done;                           // one-pass endFrame: blocks done (last rolls)
-    DBuf pend2, pend2_slot, pend2_count;    // ORDERED: value calls of existing slots
+    DBuf pend2_key, pend2_val, pend2_count; // ORDERED: value calls of existing slots
     DBuf o_key, o_key2, o_idx, o_idx2, o_tgt, o_flag; // their slot-grouped sort (o_tgt: run marks)
     DBuf o_fp, o_fk;                                  // its marked runs' re-sort
     uint64_t live_bound = 0;
@@ -307,12 +307,13 @@ struct VPArgs {
     PendRec *pend;
     unsigned long long *pend_count;
     uint64_t pend_cap;
-    /* ORDERED: value calls whose key already owns a slot (phase 1 found it) go here with the
-     * slot, for the slot-grouped fold (fold_slot_records) */
-    PendRec *pend2;
-    uint32_t *pend2_slot;
-    unsigned long long *pend2_count;
+    /* ORDERED: value calls whose key already owns a slot (phase 1 found it) go here as (sort
+     * key, value) pairs for the slot-grouped fold (fold_slot_records) */
+    uint64_t *pend2_key;
+    double4 *pend2_val;
+    unsigned long long *pend2_count; /* [0] calls, [1] checksum alias seen */
     uint64_t pend2_cap;
+    int pend2_capl; /* the stores' largest capacity_log2 (the key's slot field width) */
 };
 
 #define VP_BLOCK 256
@@ -445,15 +446,23 @@ __device__ __forceinline__ void contribute_atomic(const DevStore &s, const PendS
  * cNew only ever receives whole numbers, so its sum is exact in any order.  An existing key's
  * counter is therefore applied in place (cNew += 1, lastTouched = frame: field.cpp:122-124,
  * 157) and only a new key's counter becomes a record (its placement needs one); a full window
- * counts the drop (field.cpp:145).  This halves the records the canonical sort has to order. */
+ * counts the drop (field.cpp:145).  A key that matches a slot's checksum but not its key fields
+ * (a checksum alias: the reference shares the slot, field.cpp:103-113) returns -4 and raises
+ * *alias: its value calls become full records, and the pass takes the general path. */
 __device__ __forceinline__ int count_call(const DevStore &s, const PendSink &a, bool want,
-                                          int sid, const Key &k) {
+                                          int sid, const Key &k, unsigned long long *alias) {
     int res = -3;
     uint32_t mark = 0;
     if (want) res = probe_existing(s, k.pack_lo & s.mask, k.checksum, &mark);
     if (res >= 0) {
         atomicAdd(&acc_ptr(s, res)->w, 1.0);
         touch_slot(s, (uint32_t)res, mark);
+        const KeyFields kf = s.keyf[res];
+        if (kf.level != k.level || kf.c0 != k.cell[0] || kf.c1 != k.cell[1] ||
+            kf.c2 != k.cell[2] || kf.d0 != k.dir[0] || kf.d1 != k.dir[1]) {
+            atomicOr(alias, 1ull);
+            res = -4;
+        }
     }
     if (PendRec *p = warp_reserve(a, res == -1))
         put_record(p, k, PSTF_META(sid, 1, 1) | ((uint32_t)s.rank << 3), 0.0, 0.0, 0.0, 1.0);
@@ -461,23 +470,55 @@ __device__ __forceinline__ int count_call(const DevStore &s, const PendSink &a, 
     return res;
 }
 
-/* ORDERED mode, a value call (weight 1.0) of a key whose counter call just probed the
- * frame-start table with result res: an existing slot's call goes to the slot-grouped records
- * (no placement needed; an all-zero value is a no-op on the accumulator — it starts at +0.0 and
- * can never become -0.0 — and is not emitted), a new key's call to the pending records, and a
- * call whose window is full counts one drop (field.cpp:145) */
-__device__ __forceinline__ void value_call(const DevStore &s, const PendSink &a,
-                                           const PendSink &a2, uint32_t *slot2, bool want,
-                                           int res, int sid, const Key &k, double r_, double g_,
-                                           double b_) {
-    const bool zero = r_ == 0.0 && g_ == 0.0 && b_ == 0.0;
-    if (PendRec *p = warp_reserve(a2, want && res >= 0 && !zero)) {
-        put_record(p, k, PSTF_META(sid, 0, 1), r_, g_, b_, 1.0);
-        slot2[p - a2.pend] = (uint32_t)res;
+/* ORDERED mode, the vertex's value calls (weight 1.0), all 32 lanes together.  Calls of a key
+ * whose counter call found its slot become (sort key, value) pairs, one reservation per warp
+ * for all seven call sites (an all-zero value is a no-op on the accumulator — it starts at +0.0
+ * and can never become -0.0 — and is not emitted); a new key's (or an alias's) calls become
+ * full pending records; a call whose window is full counts one drop (field.cpp:145). */
+struct VCall {
+    bool want;
+    int res;
+    double r, g, b;
+};
+
+__device__ __forceinline__ void value_calls(const VPArgs &a, const PendSink &ps, const VCall *c,
+                                            const Key &kLo, const Key &kLoe, const Key &kFc,
+                                            const Key &kFn, const Key &kLi) {
+    const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
+    const int capl = a.pend2_capl, S = capl + 2;
+    unsigned m[7], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        const bool zero = c[q].r == 0.0 && c[q].g == 0.0 && c[q].b == 0.0;
+        m[q] = __ballot_sync(0xffffffffu, c[q].want && c[q].res >= 0 && !zero);
+        tot += __popc(m[q]);
     }
-    if (PendRec *p = warp_reserve(a, want && res == -1))
-        put_record(p, k, PSTF_META(sid, 0, 1), r_, g_, b_, 1.0);
-    if (want && res == -2) atomicAdd(&s.ctr[C_DROPPED], 1ull);
+    if (tot) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.pend2_count, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            if ((m[q] >> lane) & 1u) {
+                const unsigned long long pos = base + __popc(m[q] & lt);
+                if (pos < a.pend2_cap) {
+                    const uint64_t sid = q < 2 ? 0 : q < 4 ? 1 : q < 6 ? 2 : 3;
+                    const uint64_t sk = (sid << capl) | (uint32_t)c[q].res;
+                    a.pend2_key[pos] = (sk << (64 - S)) | (dbits(c[q].r) >> S);
+                    a.pend2_val[pos] = make_double4(c[q].r, c[q].g, c[q].b, 0.0);
+                }
+            }
+            base += __popc(m[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        const int sid = q < 2 ? 0 : q < 4 ? 1 : q < 6 ? 2 : 3;
+        const Key &k = q < 2 ? kLo : q < 4 ? kLoe : q == 4 ? kFc : q == 5 ? kFn : kLi;
+        if (PendRec *p = warp_reserve(ps, c[q].want && (c[q].res == -1 || c[q].res == -4)))
+            put_record(p, k, PSTF_META(sid, 0, 1), c[q].r, c[q].g, c[q].b, 1.0);
+        if (c[q].want && c[q].res == -2) atomicAdd(&a.st.s[sid].ctr[C_DROPPED], 1ull);
+    }
 }
 
 
@@ -657,37 +698,36 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
     } else {
         /* ORDERED: the reference's individual calls, in any order (the sort canonicalises) */
         const PendSink ps{a.pend, a.pend_count, a.pend_cap};
-        const PendSink ps2{a.pend2, a.pend2_count, a.pend2_cap};
-        uint32_t *const sl2 = a.pend2_slot;
+        unsigned long long *alias = a.pend2_count + 1;
         unsigned rejLo = 0, rejLoe = 0, rejFli = 0, rejLi = 0;
-        int res = count_call(sLo, ps, live, 0, kLo);
+        const int rLo = count_call(sLo, ps, live, 0, kLo, alias);
+        const int rLoe = count_call(sLoe, ps, live, 1, kLoe, alias);
+        const int rFc = count_call(sFli, ps, live && cont, 2, kFc, alias);
+        const int rFn = count_call(sFli, ps, live && nee, 2, kFn, alias);
+        const int rLi = a.has_li ? count_call(sLi, ps, live && cont, 3, kLi, alias) : -3;
+        VCall vc[7];
         bool ok = finite3(ehx, ehy, ehz);
         rejLo += live && !ok;
-        value_call(sLo, ps, ps2, sl2, live && ok, res, 0, kLo, ehx, ehy, ehz);
+        vc[0] = {live && ok, rLo, ehx, ehy, ehz};
         ok = finite3(ulx, uly, ulz);
         rejLo += live && transp && !ok;
-        value_call(sLo, ps, ps2, sl2, live && transp && ok, res, 0, kLo, ulx, uly, ulz);
-        res = count_call(sLoe, ps, live, 1, kLoe);
+        vc[1] = {live && transp && ok, rLo, ulx, uly, ulz};
         ok = finite3(uex, uey, uez);
         rejLoe += live && loeCont && !ok;
-        value_call(sLoe, ps, ps2, sl2, live && loeCont && ok, res, 1, kLoe, uex, uey, uez);
+        vc[2] = {live && loeCont && ok, rLoe, uex, uey, uez};
         ok = finite3(nlx, nly, nlz);
         rejLoe += live && loeNee && !ok;
-        value_call(sLoe, ps, ps2, sl2, live && loeNee && ok, res, 1, kLoe, nlx, nly, nlz);
-        res = count_call(sFli, ps, live && cont, 2, kFc);
+        vc[3] = {live && loeNee && ok, rLoe, nlx, nly, nlz};
         ok = finite3(fcx, fcy, fcz);
         rejFli += live && fliCont && !ok;
-        value_call(sFli, ps, ps2, sl2, live && fliCont && ok, res, 2, kFc, fcx, fcy, fcz);
-        res = count_call(sFli, ps, live && nee, 2, kFn);
+        vc[4] = {live && fliCont && ok, rFc, fcx, fcy, fcz};
         ok = finite3(nfx, nfy, nfz);
         rejFli += live && fliNee && !ok;
-        value_call(sFli, ps, ps2, sl2, live && fliNee && ok, res, 2, kFn, nfx, nfy, nfz);
-        if (a.has_li) {
-            res = count_call(sLi, ps, live && cont, 3, kLi);
-            ok = finite3(lvx, lvy, lvz);
-            rejLi += live && cont && !ok;
-            value_call(sLi, ps, ps2, sl2, live && cont && ok, res, 3, kLi, lvx, lvy, lvz);
-        }
+        vc[5] = {live && fliNee && ok, rFn, nfx, nfy, nfz};
+        ok = finite3(lvx, lvy, lvz);
+        rejLi += a.has_li && live && cont && !ok;
+        vc[6] = {a.has_li && live && cont && ok, rLi, lvx, lvy, lvz};
+        value_calls(a, ps, vc, kLo, kLoe, kFc, kFn, kLi);
         if (rejLo) atomicAdd(&sLo.ctr[C_REJECTED], (unsigned long long)rejLo);
         if (rejLoe) atomicAdd(&sLoe.ctr[C_REJECTED], (unsigned long long)rejLoe);
         if (rejFli) atomicAdd(&sFli.ctr[C_REJECTED], (unsigned long long)rejFli);
@@ -3200,23 +3240,32 @@ __global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v;
  * A record whose key is not its slot's (a checksum alias sharing the slot: the queue would order
  * the two keys' calls apart) or whose weight is not 1 sends all of them through the general
  * path, decided before anything is folded. */
-__global__ void k_slot_keys(const PendRec *__restrict__ r, const uint32_t *__restrict__ slot,
-                            uint64_t n, int capl, Stores4 st, uint64_t *key, uint32_t *idx,
-                            unsigned int *flag) {
+__global__ void k_iota32(uint32_t *idx, uint64_t n) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) idx[i] = (uint32_t)i;
+}
+
+/* the general path's full record of a slot-grouped call (the slot's key: no alias reached
+ * this list), exactly as the vertex pass writes a new key's value call */
+__global__ void k_slot_expand(const uint64_t *__restrict__ key, const double4 *__restrict__ val,
+                              uint64_t n, int capl, Stores4 st, PendRec *out) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int4 k0 = reinterpret_cast<const int4 *>(r + i)[0];
-    const int4 k1 = reinterpret_cast<const int4 *>(r + i)[1];
-    const double r0 = r[i].v[0], w = r[i].v[3];
-    const uint32_t sid = PSTF_META_SID((uint32_t)k1.w), sl = slot[i];
-    const KeyFields kf = st.s[sid].keyf[sl];
-    const bool bad = kf.level != k0.x || kf.c0 != k0.y || kf.c1 != k0.z || kf.c2 != k0.w ||
-                     kf.d0 != k1.x || kf.d1 != k1.y || dbits(w) != dbits(1.0);
-    if (bad && (atomicOr(flag, 1u) & 1u) == 0) flag[2] = (unsigned int)i; /* first seen */
     const int S = capl + 2;
-    const uint64_t sk = ((uint64_t)sid << capl) | sl;
-    key[i] = (sk << (64 - S)) | (dbits(r0) >> S);
-    idx[i] = (uint32_t)i;
+    const uint64_t sk = key[i] >> (64 - S);
+    const uint32_t sid = (uint32_t)(sk >> capl), slot = (uint32_t)(sk & ((1ull << capl) - 1ull));
+    const DevStore &s = st.s[sid];
+    const KeyFields kf = s.keyf[slot];
+    Key k;
+    k.level = kf.level;
+    k.cell[0] = kf.c0;
+    k.cell[1] = kf.c1;
+    k.cell[2] = kf.c2;
+    k.dir[0] = kf.d0;
+    k.dir[1] = kf.d1;
+    k.checksum = s.meta[slot].x;
+    const double4 v = val[i];
+    put_record(out + i, k, PSTF_META(sid, 0, 1), v.x, v.y, v.z, 1.0);
 }
 
 /* own position at each run head of the sorted keys (0 elsewhere): a max-scan gives every
@@ -3392,14 +3441,14 @@ __global__ void k_slot_heads(const uint64_t *key, uint64_t n, int S, uint32_t *h
 #define SLOT_FOLD_WARP 32 /* slots with more value calls than this are folded by a warp */
 
 /* the value calls' components in the sorted order, one array each (r, g, b) */
-__global__ void k_slot_terms(const PendRec *__restrict__ r, const uint32_t *__restrict__ idx,
+__global__ void k_slot_terms(const double4 *__restrict__ val, const uint32_t *__restrict__ idx,
                              uint64_t n, double *__restrict__ T) {
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (q >= n) return;
-    const PendRec &p = r[idx[q]];
-    T[q] = p.v[0];
-    T[n + q] = p.v[1];
-    T[2 * n + q] = p.v[2];
+    const double4 v = val[idx[q]];
+    T[q] = v.x;
+    T[n + q] = v.y;
+    T[2 * n + q] = v.z;
 }
 
 __device__ __forceinline__ double4 *slot_acc(const Stores4 &st, uint64_t key, int capl) {
@@ -3492,10 +3541,9 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         return PSTF_OK;
     }
     const int S = capl + 2;
-    const PendRec *rec = sc.pend2.as<PendRec>();
+    const double4 *val = sc.pend2_val.as<double4>();
     const Stores4 S4 = stores4(fs, nf);
     const uint64_t nw = (n + 31) / 32;
-    ENSURE(sc.o_key, n * 8);
     ENSURE(sc.o_key2, n * 8);
     ENSURE(sc.o_idx, n * 4);
     ENSURE(sc.o_idx2, n * 4);
@@ -3508,7 +3556,8 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     ENSURE(sc.fterms, n * 24);    /* the terms r | g | b in the sorted order */
     ENSURE(sc.fstart, (n + 1) * 4);
     ENSURE(sc.fnruns, 8);
-    uint64_t *key = sc.o_key.as<uint64_t>(), *key2 = sc.o_key2.as<uint64_t>();
+    const uint64_t *key = sc.pend2_key.as<uint64_t>();
+    uint64_t *key2 = sc.o_key2.as<uint64_t>();
     uint32_t *idx0 = sc.o_idx.as<uint32_t>(), *idx = sc.o_idx2.as<uint32_t>();
     unsigned int *flag = sc.o_flag.as<unsigned int>();
     uint32_t *hp = sc.head.as<uint32_t>(), *rstart = sc.uid.as<uint32_t>();
@@ -3517,8 +3566,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     double *T = sc.fterms.as<double>();
     CK(cudaMemsetAsync(sc.o_flag.p, 0, 32, st));
     CK(cudaMemsetAsync(sc.o_tgt.p, 0, nw * 8, st));
-    LAUNCH(k_slot_keys, grid_for(n, 256), 256, 0, st, rec, sc.pend2_slot.as<uint32_t>(), n, capl,
-           S4, key, idx0, flag);
+    LAUNCH(k_iota32, grid_for(n, 256), 256, 0, st, idx0, n);
     const auto cub_call = [&](const char *name, int nlaunch, auto &&fn) -> int {
         size_t bytes = 0;
         CK(fn((void *)nullptr, bytes));
@@ -3533,7 +3581,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx0, idx, (int64_t)n, 0, 64, st);
     });
     if (rc) return rc;
-    LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, rec, idx, n, T);
+    LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
     /* runs of equal sort keys holding an out-of-order pair, re-sorted in place by length class */
     LAUNCH(k_run_head_pos, grid_for(n, 256), 256, 0, st, key2, n, hp);
     rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
@@ -3560,10 +3608,6 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         fprintf(stderr, "[ordered] %llu value calls of existing slots, flag %u, marked runs %u "
                 "(thread) %u (block), %llu calls in longer marked runs\n",
                 (unsigned long long)n, fl, h[4], h[5], (unsigned long long)m);
-    if (fl & 1u) { /* a checksum alias or a weight other than 1 */
-        *fallback = true;
-        return PSTF_OK;
-    }
     if (m) { /* the runs too long for a block: b, g, then (run start, r) (stable, LSD) */
         ENSURE(sc.fisc, n);
         LAUNCH(k_run_marked, grid_for(n, 256), 256, 0, st, rstart, claim2, n, sc.fisc.as<uint8_t>());
@@ -3613,21 +3657,34 @@ static int resolve_ordered(Scratch &sc, pstf_field *const *fs, int nf, cudaStrea
     int rc = read_small(sc, sc.pend_count.p, 8, st);
     if (rc) return rc;
     uint64_t n1 = sc.h_small[0];
-    rc = read_small(sc, sc.pend2_count.p, 8, st);
+    rc = read_small(sc, sc.pend2_count.p, 16, st);
     if (rc) return rc;
-    const uint64_t n2 = std::min<uint64_t>(sc.h_small[0], sc.pend2.bytes / sizeof(PendRec));
+    const uint64_t n2 = std::min<uint64_t>(sc.h_small[0], sc.pend2_key.bytes / 8);
+    const bool alias = sc.h_small[1] != 0;
     if (n2) {
-        bool fallback = false;
+        bool fallback = alias;
         const bool force = getenv("PSTF_ORDERED_GENERAL") != nullptr; /* parity tests */
-        if (!force) {
+        if (!force && !alias) {
             rc = fold_slot_records(sc, fs, nf, n2, &fallback, st);
             if (rc) return rc;
         }
-        if (force || fallback) { /* append them to the general path's records */
-            if (n1 + n2 > sc.pend.bytes / sizeof(PendRec))
-                return set_err(PSTF_E_NOMEM, "pending-update buffer overflow");
-            CK(cudaMemcpyAsync(sc.pend.as<PendRec>() + n1, sc.pend2.p, n2 * sizeof(PendRec),
-                               cudaMemcpyDeviceToDevice, st));
+        if (force || fallback) { /* as full records, appended to the general path's */
+            if (n1 + n2 > sc.pend.bytes / sizeof(PendRec)) {
+                /* grow, keeping the n1 records already there */
+                DBuf nb;
+                CK(nb.ensure((n1 + n2) * sizeof(PendRec)));
+                CK(cudaMemcpyAsync(nb.p, sc.pend.p, n1 * sizeof(PendRec), cudaMemcpyDeviceToDevice,
+                                   st));
+                CK(cudaStreamSynchronize(st));
+                std::swap(nb.p, sc.pend.p);
+                std::swap(nb.bytes, sc.pend.bytes);
+            }
+            int capl = 0;
+            for (int i = 0; i < nf; ++i)
+                if (fs[i]) capl = std::max<int>(capl, (int)fs[i]->cfg.capacity_log2);
+            LAUNCH(k_slot_expand, grid_for(n2, 256), 256, 0, st, sc.pend2_key.as<uint64_t>(),
+                   sc.pend2_val.as<double4>(), n2, capl, stores4(fs, nf),
+                   sc.pend.as<PendRec>() + n1);
             n1 += n2;
             LAUNCH(k_set_u64, 1, 1, 0, st, sc.pend_count.as<unsigned long long>(),
                    (unsigned long long)n1);
@@ -3686,15 +3743,15 @@ static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t
     ENSURE(sc.pend_count, 8);
     if (with_seq) ENSURE(sc.pend_seq, cap * 8);
     CK(cudaMemsetAsync(sc.pend_count.p, 0, 8, st));
-    ENSURE(sc.pend2_count, 8);
-    CK(cudaMemsetAsync(sc.pend2_count.p, 0, 8, st));
+    ENSURE(sc.pend2_count, 16);
+    CK(cudaMemsetAsync(sc.pend2_count.p, 0, 16, st));
     return PSTF_OK;
 }
 
 /* ORDERED vertex passes: room for every value call of an existing slot (<= 7 per vertex) */
 static int ensure_pending2(Scratch &sc, uint64_t cap) {
-    ENSURE(sc.pend2, cap * sizeof(PendRec));
-    ENSURE(sc.pend2_slot, cap * 4);
+    ENSURE(sc.pend2_key, cap * 8);
+    ENSURE(sc.pend2_val, cap * 32);
     return PSTF_OK;
 }
 
@@ -4597,10 +4654,14 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
     a.pend_count = lo->sc.pend_count.as<unsigned long long>();
     a.pend_cap = lo->sc.pend.bytes / sizeof(PendRec);
     if (mode == PSTF_MODE_ORDERED) {
-        a.pend2 = lo->sc.pend2.as<PendRec>();
-        a.pend2_slot = lo->sc.pend2_slot.as<uint32_t>();
+        a.pend2_key = lo->sc.pend2_key.as<uint64_t>();
+        a.pend2_val = lo->sc.pend2_val.as<double4>();
         a.pend2_count = lo->sc.pend2_count.as<unsigned long long>();
-        a.pend2_cap = std::min(lo->sc.pend2.bytes / sizeof(PendRec), lo->sc.pend2_slot.bytes / 4);
+        a.pend2_cap = std::min(lo->sc.pend2_key.bytes / 8, lo->sc.pend2_val.bytes / 32);
+        int capl = 0;
+        for (int i = 0; i < 4; ++i)
+            if (fs[i]) capl = std::max<int>(capl, (int)fs[i]->cfg.capacity_log2);
+        a.pend2_capl = capl;
     }
     const bool shared_quant = a.same_lo_loe && a.same_fli_lo && a.same_li_fli;
     /* TMA path: every SoA segment must be 16 B aligned for cp.async.bulk */
