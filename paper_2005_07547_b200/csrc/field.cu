@@ -3231,10 +3231,10 @@ __global__ void k_set_u64(unsigned long long *p, unsigned long long v) { *p = v;
  *   2. the components gathered in that order (three arrays r | g | b);
  *   3. the only calls that can be out of (r, g, b) order are inside runs of equal sort keys
  *      (equal leading bits of r: r values an ulp apart, or equal r with different g, b): each
- *      run holding an out-of-order neighbour pair is re-sorted in place, by one thread
- *      (insertion, <= 32 calls), by one block (bitonic in shared memory, <= 4096 calls), or,
- *      longer, compacted with the other such runs and radix-sorted least significant word first
- *      (b, g, then run start with the low bits of r);
+ *      run holding an out-of-order neighbour pair is re-sorted in place, by one warp (rank sort
+ *      through shuffles, <= 32 calls; bitonic in shared memory, <= 256) or one block (the same,
+ *      <= 4096), or, longer, compacted with the other such runs and radix-sorted least
+ *      significant word first (b, g, then run start with the low bits of r);
  *   4. the terms folded sequentially per slot (a warp per long slot: three lanes carry the r, g
  *      and b sums).
  * A record whose key is not its slot's (a checksum alias sharing the slot: the queue would order
@@ -3268,11 +3268,14 @@ __global__ void k_slot_expand(const uint64_t *__restrict__ key, const double4 *_
     put_record(out + i, k, PSTF_META(sid, 0, 1), v.x, v.y, v.z, 1.0);
 }
 
-/* own position at each run head of the sorted keys (0 elsewhere): a max-scan gives every
- * position its run's start */
-__global__ void k_run_head_pos(const uint64_t *key, uint64_t n, uint32_t *hp) {
+/* own position at each run head of the sorted keys (0 elsewhere: a max-scan gives every position
+ * its run's start), and the heads of the slots' segments */
+__global__ void k_run_heads(const uint64_t *key, uint64_t n, int S, uint32_t *hp, uint32_t *sh) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j < n) hp[j] = (j == 0 || key[j] != key[j - 1]) ? (uint32_t)j : 0u;
+    if (j >= n) return;
+    const uint64_t k = key[j], kp = j ? key[j - 1] : ~k;
+    hp[j] = (j == 0 || k != kp) ? (uint32_t)j : 0u;
+    sh[j] = j == 0 || (k >> (64 - S)) != (kp >> (64 - S));
 }
 
 /* the canonical order of two value calls (weight 1 each): bits of r, then g, then b */
@@ -3299,50 +3302,131 @@ __global__ void k_run_check(const double *__restrict__ T, const uint64_t *__rest
     if (j == n - 1 || key[j + 1] != k) runlen[s0] = (uint32_t)(j + 1 - s0);
 }
 
-#define FIX_THREAD 32  /* marked runs up to this long: insertion sort by one thread */
-#define FIX_BLOCK 4096 /* up to this long: bitonic sort in shared memory by one block */
+#define FIX_THREAD 32  /* marked runs up to this long: rank sort by one warp */
+#define FIX_WARP 256   /* up to this long: bitonic sort in shared memory by one warp */
+#define FIX_BLOCK 4096 /* up to this long: the same by one block */
 
-/* the marked runs, by length: lists (start, length) for the thread and block sorters; longer
- * runs are marked again (claim2) for the radix path and counted (flag bit 2, cnt[3] records) */
-__global__ void k_run_lists(const uint32_t *__restrict__ hp, const uint32_t *__restrict__ claim,
-                            const uint32_t *__restrict__ runlen, uint64_t n, uint2 *lst_t,
-                            uint2 *lst_b, unsigned int *cnt, uint32_t *claim2) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= n || (j > 0 && hp[j] == 0)) return; /* run heads only */
-    if (!((claim[j >> 5] >> (j & 31u)) & 1u)) return;
-    const uint32_t len = runlen[j];
-    if (len <= FIX_THREAD) {
-        lst_t[atomicAdd(&cnt[4], 1u)] = make_uint2((uint32_t)j, len);
-    } else if (len <= FIX_BLOCK) {
-        lst_b[atomicAdd(&cnt[5], 1u)] = make_uint2((uint32_t)j, len);
-    } else {
-        atomicOr(&claim2[j >> 5], 1u << (j & 31u));
-        atomicOr(&cnt[0], 2u);
-        atomicAdd(&cnt[3], len);
+#define RL_PER_THREAD 8
+/* the marked runs, by length: (start, length) lists for the thread, warp and block sorters
+ * (sizes in cnt[4], cnt[7], cnt[5]; one global reservation per block and list); longer runs
+ * are marked again (claim2) for the radix path and counted (flag bit 2, cnt[3] calls) */
+__global__ void __launch_bounds__(256) k_run_lists(const uint32_t *__restrict__ hp,
+                                                   const uint32_t *__restrict__ claim,
+                                                   const uint32_t *__restrict__ runlen, uint64_t n,
+                                                   uint2 *lst_t, uint2 *lst_w, uint2 *lst_b,
+                                                   unsigned int *cnt, uint32_t *claim2) {
+    __shared__ unsigned bc[3], bb[3];
+    if (threadIdx.x < 3) bc[threadIdx.x] = 0;
+    __syncthreads();
+    uint2 item[RL_PER_THREAD];
+    unsigned cls[RL_PER_THREAD], off[RL_PER_THREAD];
+    const uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x * RL_PER_THREAD + threadIdx.x;
+#pragma unroll
+    for (int t = 0; t < RL_PER_THREAD; ++t) {
+        const uint64_t j = j0 + (uint64_t)t * blockDim.x;
+        cls[t] = 3;
+        if (j >= n || (j > 0 && hp[j] == 0) || !((claim[j >> 5] >> (j & 31u)) & 1u)) continue;
+        const uint32_t len = runlen[j];
+        item[t] = make_uint2((uint32_t)j, len);
+        if (len > FIX_BLOCK) {
+            atomicOr(&claim2[j >> 5], 1u << (j & 31u));
+            atomicOr(&cnt[0], 2u);
+            atomicAdd(&cnt[3], len);
+            continue;
+        }
+        cls[t] = len <= FIX_THREAD ? 0 : len <= FIX_WARP ? 1 : 2;
+        off[t] = atomicAdd(&bc[cls[t]], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && bc[threadIdx.x]) {
+        unsigned *g = threadIdx.x == 0 ? &cnt[4] : threadIdx.x == 1 ? &cnt[7] : &cnt[5];
+        bb[threadIdx.x] = atomicAdd(g, bc[threadIdx.x]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < RL_PER_THREAD; ++t) {
+        if (cls[t] == 3) continue;
+        uint2 *l = cls[t] == 0 ? lst_t : cls[t] == 1 ? lst_w : lst_b;
+        l[bb[cls[t]] + off[t]] = item[t];
     }
 }
 
-__global__ void k_fix_thread(double *T, uint64_t n, const uint2 *lst, const unsigned int *cnt) {
-    const uint32_t nl = cnt[4];
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nl;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j0 = lst[e].x, j1 = j0 + lst[e].y;
-        for (uint32_t p = j0 + 1; p < j1; ++p) {
-            const double r = T[p], g = T[n + p], b = T[2 * n + p];
-            uint32_t t = p;
-            while (t > j0) {
-                const uint64_t x[3] = {dbits(r), dbits(g), dbits(b)};
-                const uint64_t y[3] = {dbits(T[t - 1]), dbits(T[n + t - 1]), dbits(T[2 * n + t - 1])};
-                const bool lt = x[0] != y[0] ? x[0] < y[0] : x[1] != y[1] ? x[1] < y[1] : x[2] < y[2];
-                if (!lt) break;
-                T[t] = T[t - 1];
-                T[n + t] = T[n + t - 1];
-                T[2 * n + t] = T[2 * n + t - 1];
-                --t;
+/* bitonic sort of N (a power of two) (r, g, b) bit triples in shared memory by the threads
+ * [t0, t0 + nt); sync() between the steps */
+template <class Sync>
+__device__ __forceinline__ void bitonic3(uint64_t *kr, uint64_t *kg, uint64_t *kb, uint32_t N,
+                                         uint32_t t0, uint32_t nt, Sync sync) {
+    for (uint32_t k = 2; k <= N; k <<= 1)
+        for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+            for (uint32_t i = t0; i < N; i += nt) {
+                const uint32_t q = i ^ h;
+                if (q <= i) continue;
+                const bool gt = kr[i] != kr[q] ? kr[i] > kr[q]
+                                : kg[i] != kg[q] ? kg[i] > kg[q] : kb[i] > kb[q];
+                if (gt == ((i & k) == 0)) {
+                    uint64_t t = kr[i]; kr[i] = kr[q]; kr[q] = t;
+                    t = kg[i]; kg[i] = kg[q]; kg[q] = t;
+                    t = kb[i]; kb[i] = kb[q]; kb[q] = t;
+                }
             }
-            T[t] = r;
-            T[n + t] = g;
-            T[2 * n + t] = b;
+            sync();
+        }
+}
+
+/* one warp per marked run of up to FIX_WARP calls */
+__global__ void __launch_bounds__(256) k_fix_warp(double *T, uint64_t n, const uint2 *lst,
+                                                  const unsigned int *cnt) {
+    __shared__ uint64_t wsm[8][3][FIX_WARP];
+    const unsigned lane = lane_id(), w = threadIdx.x >> 5;
+    uint64_t *kr = wsm[w][0], *kg = wsm[w][1], *kb = wsm[w][2];
+    const uint32_t nl = cnt[7];
+    for (uint64_t e = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; e < nl;
+         e += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t j0 = lst[e].x, len = lst[e].y;
+        uint32_t N = 64;
+        while (N < len) N <<= 1;
+        for (uint32_t i = lane; i < N; i += 32) {
+            const bool in = i < len;
+            kr[i] = in ? dbits(T[j0 + i]) : ~0ull;
+            kg[i] = in ? dbits(T[n + j0 + i]) : ~0ull;
+            kb[i] = in ? dbits(T[2 * n + j0 + i]) : ~0ull;
+        }
+        __syncwarp();
+        bitonic3(kr, kg, kb, N, lane, 32, [] { __syncwarp(); });
+        for (uint32_t i = lane; i < len; i += 32) {
+            T[j0 + i] = __longlong_as_double((long long)kr[i]);
+            T[n + j0 + i] = __longlong_as_double((long long)kg[i]);
+            T[2 * n + j0 + i] = __longlong_as_double((long long)kb[i]);
+        }
+        __syncwarp();
+    }
+}
+
+/* one warp per marked run of up to 32 calls: each lane holds one call and counts the calls
+ * before it (rank sort through shuffles), then stores it at its rank */
+__global__ void __launch_bounds__(256) k_fix_small(double *T, uint64_t n, const uint2 *lst,
+                                                   const unsigned int *cnt) {
+    const unsigned lane = lane_id();
+    const uint32_t nl = cnt[4];
+    for (uint64_t e = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; e < nl;
+         e += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t j0 = lst[e].x, len = lst[e].y;
+        const bool in = lane < len;
+        const uint64_t r = in ? dbits(T[j0 + lane]) : ~0ull;
+        const uint64_t g = in ? dbits(T[n + j0 + lane]) : ~0ull;
+        const uint64_t b = in ? dbits(T[2 * n + j0 + lane]) : ~0ull;
+        uint32_t rank = 0;
+        for (uint32_t i = 0; i < len; ++i) {
+            const uint64_t ri = __shfl_sync(0xffffffffu, r, i);
+            const uint64_t gi = __shfl_sync(0xffffffffu, g, i);
+            const uint64_t bi = __shfl_sync(0xffffffffu, b, i);
+            const bool lt = ri != r ? ri < r : gi != g ? gi < g : bi != b ? bi < b : i < lane;
+            rank += lt;
+        }
+        if (in) {
+            T[j0 + rank] = __longlong_as_double((long long)r);
+            T[n + j0 + rank] = __longlong_as_double((long long)g);
+            T[2 * n + j0 + rank] = __longlong_as_double((long long)b);
         }
     }
 }
@@ -3356,7 +3440,7 @@ __global__ void __launch_bounds__(512) k_fix_block(double *T, uint64_t n, const 
     const uint32_t nl = cnt[5];
     for (uint32_t e = blockIdx.x; e < nl; e += gridDim.x) {
         const uint32_t j0 = lst[e].x, len = lst[e].y;
-        uint32_t N = 64;
+        uint32_t N = 512;
         while (N < len) N <<= 1;
         for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
             const bool in = i < len;
@@ -3365,21 +3449,7 @@ __global__ void __launch_bounds__(512) k_fix_block(double *T, uint64_t n, const 
             kb[i] = in ? dbits(T[2 * n + j0 + i]) : ~0ull;
         }
         __syncthreads();
-        for (uint32_t k = 2; k <= N; k <<= 1)
-            for (uint32_t h = k >> 1; h > 0; h >>= 1) {
-                for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
-                    const uint32_t q = i ^ h;
-                    if (q <= i) continue;
-                    const bool gt = kr[i] != kr[q] ? kr[i] > kr[q]
-                                    : kg[i] != kg[q] ? kg[i] > kg[q] : kb[i] > kb[q];
-                    if (gt == ((i & k) == 0)) {
-                        uint64_t t = kr[i]; kr[i] = kr[q]; kr[q] = t;
-                        t = kg[i]; kg[i] = kg[q]; kg[q] = t;
-                        t = kb[i]; kb[i] = kb[q]; kb[q] = t;
-                    }
-                }
-                __syncthreads();
-            }
+        bitonic3(kr, kg, kb, N, threadIdx.x, blockDim.x, [] { __syncthreads(); });
         for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
             T[j0 + i] = __longlong_as_double((long long)kr[i]);
             T[n + j0 + i] = __longlong_as_double((long long)kg[i]);
@@ -3430,12 +3500,6 @@ __global__ void k_fix_put(const double *__restrict__ tmp, const uint32_t *__rest
     T[j] = tmp[q];
     T[n + j] = tmp[m + q];
     T[2 * n + j] = tmp[2 * m + q];
-}
-
-/* heads of the slots' segments in the sorted order */
-__global__ void k_slot_heads(const uint64_t *key, uint64_t n, int S, uint32_t *head) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j < n) head[j] = j == 0 || (key[j] >> (64 - S)) != (key[j - 1] >> (64 - S));
 }
 
 #define SLOT_FOLD_WARP 32 /* slots with more value calls than this are folded by a warp */
@@ -3552,7 +3616,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     ENSURE(sc.uid, n * 4);
     ENSURE(sc.rank, n * 4);       /* run lengths (at run starts) */
     ENSURE(sc.o_tgt, nw * 8);     /* run-mark bitmaps: marked, over-long */
-    ENSURE(sc.o_fp, n * 8);       /* (start, length) lists of the marked runs */
+    ENSURE(sc.o_fp, (n / 2 + n / (FIX_THREAD + 1) + n / (FIX_WARP + 1) + 3) * 8); /* run lists */
     ENSURE(sc.fterms, n * 24);    /* the terms r | g | b in the sorted order */
     ENSURE(sc.fstart, (n + 1) * 4);
     ENSURE(sc.fnruns, 8);
@@ -3583,31 +3647,33 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     if (rc) return rc;
     LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
     /* runs of equal sort keys holding an out-of-order pair, re-sorted in place by length class */
-    LAUNCH(k_run_head_pos, grid_for(n, 256), 256, 0, st, key2, n, hp);
+    uint32_t *sh = idx0; /* slot-segment heads (the sort's input indices are spent) */
+    LAUNCH(k_run_heads, grid_for(n, 256), 256, 0, st, key2, n, S, hp, sh);
     rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
         return cub::DeviceScan::InclusiveScan(t, b, hp, rstart, cub::Max(), (int64_t)n, st);
     });
     if (rc) return rc;
     LAUNCH(k_run_check, grid_for(n, 256), 256, 0, st, T, key2, rstart, n, claim,
            sc.rank.as<uint32_t>());
-    /* at most n/2 marked runs in total (each holds two calls or more) */
-    uint2 *lst_b = lst_t + n / 2;
-    LAUNCH(k_run_lists, grid_for(n, 256), 256, 0, st, hp, claim, sc.rank.as<uint32_t>(), n, lst_t,
-           lst_b, flag, claim2);
+    /* at most n/2 marked runs (each holds two calls or more), n/33 longer than 32, ... */
+    uint2 *lst_w = lst_t + n / 2 + 1, *lst_b = lst_w + n / (FIX_THREAD + 1) + 1;
+    LAUNCH(k_run_lists, grid_for((n + RL_PER_THREAD - 1) / RL_PER_THREAD, 256), 256, 0, st, hp,
+           claim, sc.rank.as<uint32_t>(), n, lst_t, lst_w, lst_b, flag, claim2);
     const unsigned grid = (unsigned)sm_count() * 8;
-    LAUNCH(k_fix_thread, grid, 128, 0, st, T, n, lst_t, flag);
+    LAUNCH(k_fix_small, grid, 256, 0, st, T, n, lst_t, flag);
+    LAUNCH(k_fix_warp, grid, 256, 0, st, T, n, lst_w, flag);
     const size_t fsm = 3 * FIX_BLOCK * 8;
     CK(cudaFuncSetAttribute(k_fix_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
     LAUNCH(k_fix_block, (unsigned)sm_count() * 2, 512, fsm, st, T, n, lst_b, flag);
-    rc = read_small(sc, sc.o_flag.p, 24, st); /* the pass's one host read */
+    rc = read_small(sc, sc.o_flag.p, 32, st); /* the pass's one host read */
     if (rc) return rc;
     const uint32_t *h = (const uint32_t *)sc.h_small;
     const uint32_t fl = h[0];
     const uint64_t m = h[3];
     if (getenv("PSTF_ORDERED_DEBUG"))
         fprintf(stderr, "[ordered] %llu value calls of existing slots, flag %u, marked runs %u "
-                "(thread) %u (block), %llu calls in longer marked runs\n",
-                (unsigned long long)n, fl, h[4], h[5], (unsigned long long)m);
+                "(thread) %u (warp) %u (block), %llu calls in longer marked runs\n",
+                (unsigned long long)n, fl, h[4], h[7], h[5], (unsigned long long)m);
     if (m) { /* the runs too long for a block: b, g, then (run start, r) (stable, LSD) */
         ENSURE(sc.fisc, n);
         LAUNCH(k_run_marked, grid_for(n, 256), 256, 0, st, rstart, claim2, n, sc.fisc.as<uint8_t>());
@@ -3637,14 +3703,13 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         LAUNCH(k_fix_put, grid_for(m, 256), 256, 0, st, tmp, F, m, T, n);
     }
     /* one segment per slot, folded in that order */
-    LAUNCH(k_slot_heads, grid_for(n, 256), 256, 0, st, key2, n, S, hp);
     rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, hp, rstart, (int64_t)n, st);
+        return cub::DeviceScan::ExclusiveSum(t, b, sh, rstart, (int64_t)n, st);
     });
     if (rc) return rc;
     uint32_t *seg = sc.fstart.as<uint32_t>(); /* segment starts (+ the end sentinel) */
-    LAUNCH(k_fold_starts, grid_for(n, 256), 256, 0, st, hp, rstart, n, seg);
-    LAUNCH(k_fold_nruns, 1, 1, 0, st, hp, rstart, n, sc.fnruns.as<uint32_t>());
+    LAUNCH(k_fold_starts, grid_for(n, 256), 256, 0, st, sh, rstart, n, seg);
+    LAUNCH(k_fold_nruns, 1, 1, 0, st, sh, rstart, n, sc.fnruns.as<uint32_t>());
     LAUNCH(k_slot_fold, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl, S4);
     LAUNCH(k_slot_fold_long, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl,
            S4);
