@@ -177,6 +177,7 @@ struct Scratch {
     DBuf pend2_key, pend2_val, pend2_count; // ORDERED: value calls of existing slots
     DBuf o_key, o_key2, o_idx, o_idx2, o_tgt, o_flag; // their slot-grouped sort (o_tgt: run marks)
     DBuf o_fp, o_fk;                                  // its marked runs' re-sort
+    DBuf cn_cnt, cn_vals;                             // endFrame: Σc_new in slot order
     uint64_t live_bound = 0;
     long long *live_total_dev = nullptr;
     bool overflow_zeroed = false;
@@ -217,6 +218,8 @@ struct pstf_field {
      * C_F_CN (tiled ATOMIC vertex passes + their placement): endFrame may run in one pass
      * (k_ef_onepass + k_ef_tail).  Any other update path clears it until the next endFrame. */
     bool unit_frame = true;
+    /* pstf_field_apply with counter calls this frame: their weights may make Σc_new inexact */
+    bool counted_apply = false;
     ~pstf_field() {
         if (dp.ev) cudaEventDestroy(dp.ev);
         if (dp.h_count) cudaFreeHost(dp.h_count);
@@ -1437,9 +1440,11 @@ __global__ void k_apply_records(ApplyArgs a, const uint32_t *valid, const uint32
     rr.k[5] = k.dir_cell[1];
     rr.cs = k.checksum;
     rr.meta = PSTF_META(0, isc ? 1 : 0, 1);
-    rr.v[0] = (isc || !a.vr) ? 0.0 : a.vr[i];
-    rr.v[1] = (isc || !a.vg) ? 0.0 : a.vg[i];
-    rr.v[2] = (isc || !a.vb) ? 0.0 : a.vb[i];
+    /* a counter call keeps its value: the queue orders a key's calls by (isCounter, bits r, g,
+     * b, w) whatever they are (field.cpp:402-410); the fold ignores it (field.cpp:413-414) */
+    rr.v[0] = a.vr ? a.vr[i] : 0.0;
+    rr.v[1] = a.vg ? a.vg[i] : 0.0;
+    rr.v[2] = a.vb ? a.vb[i] : 0.0;
     rr.v[3] = a.w[i];
     uint32_t pos = scan[i];
     pend[pos] = rr;
@@ -2254,10 +2259,74 @@ __device__ __forceinline__ void ef_reduce_body(const Stores4 &st, int nst) {
             c += scnt[q][w];
         }
         if (c) {
-            atomicAdd(st.s[q].cn_sum, t);
+            /* an inexact frame's sum is already there, summed in slot order (k_cn_seq) */
+            if (!st.s[q].ctr[C_CN_INEXACT]) atomicAdd(st.s[q].cn_sum, t);
             atomicAdd(&st.s[q].ctr[C_CN_COUNT], c);
         }
     }
+}
+
+/* ---- Σc_new in the reference's order (field.cpp:201-213: slot order, left to right) ----
+ * A frame whose counter weights are whole numbers <= 2^20 (every vertex pass: weight 1) has an
+ * exact Σc_new, so the reduce pass sums it in any order.  Otherwise (C_CN_INEXACT, raised by
+ * pstf_field_apply) the touched slots' c_new values are compacted in slot order and summed by
+ * one thread, so the mean, and with it the c_old cap, is bitwise the reference's for any
+ * weights.  Every kernel here returns at once in exact frames. */
+__global__ void k_cn_flag(const double *w, const uint8_t *isc, uint64_t n,
+                          unsigned long long *ctr) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    bool bad = false;
+    if (i < n && isc[i]) {
+        const double x = w[i];
+        bad = x >= 0.0 && isfinite(x) && (x != floor(x) || x > 1048576.0); /* counted calls */
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31u) == 0) atomicOr(&ctr[C_CN_INEXACT], 1ull);
+}
+
+__global__ void k_cn_words(DevStore s, const unsigned long long *guard, uint32_t *cnt) {
+    if ((guard && *guard) || !s.ctr[C_CN_INEXACT]) return;
+    const uint64_t nw = ((uint64_t)s.mask + 32) / 32;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < nw) cnt[i] = __popc(s.tbits[i]);
+}
+
+__global__ void k_cn_scatter(DevStore s, const unsigned long long *guard, const uint32_t *pos,
+                             double *V) {
+    if ((guard && *guard) || !s.ctr[C_CN_INEXACT]) return;
+    const uint64_t nw = ((uint64_t)s.mask + 32) / 32;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= nw) return;
+    uint32_t w = s.tbits[i], p = pos[i];
+    while (w) {
+        const uint32_t slot = (uint32_t)(i * 32 + (uint64_t)(__ffs(w) - 1));
+        w &= w - 1;
+        /* live slots only (field.cpp:205-206); c_new <= 0 adds nothing to a sum that starts at
+         * +0.0 and only ever grows */
+        const double cn = s.meta[slot].x != 0u ? acc_ptr(s, slot)->w : 0.0;
+        V[p++] = cn > 0.0 ? cn : 0.0;
+    }
+}
+
+__global__ void k_cn_seq(DevStore s, const unsigned long long *guard, const uint32_t *pos,
+                         const uint32_t *cnt, const double *V) {
+    if ((guard && *guard) || !s.ctr[C_CN_INEXACT]) return;
+    const uint64_t nw = ((uint64_t)s.mask + 32) / 32;
+    const uint64_t n = (uint64_t)pos[nw - 1] + cnt[nw - 1];
+    double sum = 0.0, nx[16];
+    uint64_t i = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) nx[k] = (uint64_t)k < n ? V[k] : 0.0;
+    for (; i + 16 <= n; i += 16) {
+        double cur[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cur[k] = nx[k];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) nx[k] = i + 16 + k < n ? V[i + 16 + k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sum += cur[k];
+    }
+    for (int k = 0; i < n; ++i, ++k) sum += nx[k];
+    *s.cn_sum = sum;
 }
 
 /* the blend of one slot with c_new > 0 (field.cpp:218-241): candidate, alpha with the 1/T floor,
@@ -2353,6 +2422,7 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
         s.ctr[C_CN_COUNT] = 0;
         s.ctr[C_F_CN] = 0;
         s.ctr[C_F_DEFER] = 0;
+        s.ctr[C_CN_INEXACT] = 0;
         *s.cn_sum = 0.0;
     }
     for (int j = 0; j < nst; ++j) {
@@ -2507,6 +2577,7 @@ __device__ __forceinline__ void ef_roll(const DevStore &s) {
     s.ctr[C_CN_COUNT] = 0;
     s.ctr[C_F_CN] = 0;
     s.ctr[C_F_DEFER] = 0;
+    s.ctr[C_CN_INEXACT] = 0;
     *s.cn_sum = 0.0;
 }
 
@@ -2664,7 +2735,8 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_packed(Stores4 st, int nst,
             tc += stch[q][w];
         }
         if (c) {
-            atomicAdd(st.s[q].cn_sum, t);
+            /* an inexact frame's sum is already there, summed in slot order (k_cn_seq) */
+            if (!st.s[q].ctr[C_CN_INEXACT]) atomicAdd(st.s[q].cn_sum, t);
             atomicAdd(&st.s[q].ctr[C_CN_COUNT], c);
         }
         if (tc) atomicAdd(&st.s[q].ctr[C_TOUCHED_N], tc);
@@ -4014,6 +4086,10 @@ int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *v
     a.n = n;
     int rc = ensure_pending(sc, n, mode == PSTF_MODE_SEQUENTIAL, st);
     if (rc) return rc;
+    if (is_counter && !getenv("PSTF_CN_PARALLEL")) { /* the env: experiment / test switch */
+        LAUNCH(k_cn_flag, grid_for(n, 256), 256, 0, st, w, is_counter, n, f->d.ctr);
+        f->counted_apply = true;
+    }
     uint64_t known = (uint64_t)-1;
     if (mode == PSTF_MODE_ATOMIC) {
         LAUNCH(k_apply_atomic, grid_for(n, 256), 256, 0, st, a, sc.pend.as<PendRec>(),
@@ -4251,6 +4327,27 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
                    sc0.ef_done.as<unsigned int>());
             return PSTF_OK;
         }
+        for (int i = 0; i < n; ++i) { /* Σc_new in slot order, inexact frames only */
+            if (!fs[i]->counted_apply) continue; /* no counter weight but vertex passes' 1 */
+            Scratch &sc = fs[i]->sc;
+            const uint64_t nw = ((uint64_t)fs[i]->d.mask + 32) / 32;
+            ENSURE(sc.cn_cnt, nw * 8);
+            ENSURE(sc.cn_vals, ((uint64_t)fs[i]->d.mask + 1) * 8);
+            uint32_t *cnt = sc.cn_cnt.as<uint32_t>(), *pos = cnt + nw;
+            LAUNCH(k_cn_words, grid_for(nw, 256), 256, 0, st, fs[i]->d, gd, cnt);
+            size_t bytes = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, pos, (int64_t)nw, st));
+            ENSURE(sc.cub, bytes);
+            bytes = sc.cub.bytes;
+            {
+                ProfScope ps_("cub::DeviceScan", st);
+                CK(cub::DeviceScan::ExclusiveSum(sc.cub.p, bytes, cnt, pos, (int64_t)nw, st));
+                g_launches.fetch_add(2, std::memory_order_relaxed);
+            }
+            LAUNCH(k_cn_scatter, grid_for(nw, 256), 256, 0, st, fs[i]->d, gd, pos,
+                   sc.cn_vals.as<double>());
+            LAUNCH(k_cn_seq, 1, 1, 0, st, fs[i]->d, gd, pos, cnt, sc.cn_vals.as<double>());
+        }
         if (fused_blocks > 0) { /* one cooperative launch: reduce | blend | evict */
             unsigned gf = std::min<unsigned>(g, (unsigned)(sm_count() * fused_blocks));
             int nn = n;
@@ -4280,6 +4377,7 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     for (int i = 0; i < n; ++i) {
         fs[i]->frame += 1;
         fs[i]->unit_frame = true;
+        fs[i]->counted_apply = false;
     }
     return PSTF_OK;
 }

@@ -151,6 +151,51 @@ def _apply_gpu(g, u, mode):
     g.apply(keys, v, w, isc, mode)
 
 
+@pytest.mark.parametrize("mode", ["ordered", "sequential"])
+def test_inexact_counter_weights_bitwise(mode):
+    """Counter weights that are not whole numbers (uniform in (0, 3)) make the frame's Σc_new
+    depend on summation order; with t_max = 2 the c_old cap (T^2 - T) * mean c_new binds on most
+    slots, so the committed state is bitwise the reference's only if the mean is summed in
+    slot order (field.cpp:201-213)."""
+    cfg = po.Config.make(capacity_log2=12 if mode == "ordered" else 9, base_cell_size=0.5,
+                         probe_window=32, evict_age_frames=3, t_max=2.0)
+    o = po.OracleStore(cfg)
+    g = pb.FieldStore(_pcfg(cfg))
+    rng = np.random.default_rng(77)
+    if mode == "ordered":
+        n_keys = 3000
+        for f in range(5):
+            u = _random_updates(o, rng, 6 * n_keys, n_keys)
+            u["w"] = rng.uniform(0.0, 3.0, size=len(u))
+            o.queue_apply(u)
+            _apply_gpu(g, u[rng.permutation(len(u))], pb.MODE_ORDERED)
+            o.end_frame()
+            g.end_frame()
+            gu.assert_slots_bitwise(g.slots(), o.slots())
+        return
+    # SEQUENTIAL: the scalar calls (the facade flushes them in submission order)
+    n_keys = 400
+    pos = rng.uniform(-4, 4, size=(n_keys, 3))
+    dirs = inputs.random_dirs(rng, n_keys)
+    keys = [o.key_for(pos[i], dirs[i], 0) for i in range(n_keys)]
+    gkeys = [pb.SpatioDirectionalKey(k.level, tuple(k.cell), tuple(k.dir), k.checksum)
+             for k in keys]
+    for f in range(5):
+        for _ in range(3 * n_keys):
+            i = int(rng.integers(n_keys))
+            w = float(rng.uniform(0.0, 3.0))
+            if rng.random() < 0.5:
+                o.increment_counter(keys[i], w)
+                g.incrementCounter(gkeys[i], w)
+            else:
+                v = rng.uniform(0, 3, size=3)
+                o.accumulate(keys[i], v, w)
+                g.accumulate(gkeys[i], v, w)
+        o.end_frame()
+        g.end_frame()
+        gu.assert_slots_bitwise(g.slots(), o.slots())
+
+
 @pytest.mark.parametrize("cap,window", [(5, 8), (8, 32), (14, 32)])
 def test_queue_apply_ordered_bitwise(cap, window):
     """ORDERED mode == FieldUpdateQueue::apply (field.cpp:396-420), values bitwise."""
