@@ -785,6 +785,12 @@ struct VPArgs2 {
     uint64_t pend_cap;
     double *cv[3];     /* fused CV lookup outputs (estimators.cpp:453-462), CV instantiation only */
     uint8_t *cv_valid;
+    /* ORDERED instantiation: the slot-grouped value calls (as VPArgs) */
+    uint64_t *pend2_key;
+    double4 *pend2_val;
+    unsigned long long *pend2_count; /* [0] calls, [1] checksum alias seen */
+    uint64_t pend2_cap;
+    int pend2_capl;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -913,10 +919,51 @@ struct NoPipe {
     __device__ __forceinline__ void values_done() const {}
 };
 
-template <bool CV, class Src, class Pipe = NoPipe>
+/* ORDERED tiled kernel: each warp reserves the (sort key, value) pair buffer in chunks of
+ * PAIR_CHUNK entries (one atomic per chunk instead of one per contribution: the counter is a
+ * single hot address); a chunk's unused tail is filled with holes, key ~0 (above every real
+ * key: the slot-grouped sort moves them to the end), counted in pend2_count[2] */
+#define PAIR_CHUNK 256
+struct PairChunk {
+    unsigned long long base = 0;
+    uint32_t used = PAIR_CHUNK; /* full: the first need reserves */
+    uint64_t holes = 0;
+    bool any = false;
+};
+
+__device__ __forceinline__ void pair_close(const VPArgs2 &a, PairChunk &pc) {
+    if (pc.any) {
+        for (uint32_t i = pc.used + lane_id(); i < PAIR_CHUNK; i += 32)
+            if (pc.base + i < a.pend2_cap) a.pend2_key[pc.base + i] = ~0ull;
+        pc.holes += PAIR_CHUNK - pc.used;
+    }
+    pc.used = PAIR_CHUNK;
+}
+
+/* the warp's positions for `need` (<= 64) pairs; warp-uniform */
+__device__ __forceinline__ unsigned long long pair_reserve(const VPArgs2 &a, PairChunk &pc,
+                                                           uint32_t need) {
+    if (pc.used + need > PAIR_CHUNK) {
+        pair_close(a, pc);
+        unsigned long long b = 0;
+        if (lane_id() == 0) b = atomicAdd(a.pend2_count, (unsigned long long)PAIR_CHUNK);
+        pc.base = __shfl_sync(0xffffffffu, b, 0);
+        pc.used = 0;
+        pc.any = true;
+    }
+    const unsigned long long pos = pc.base + pc.used;
+    pc.used += need;
+    return pos;
+}
+
+/* ORD (ORDERED mode): every counter call of an existing key is added in place (the RED of
+ * {0, 0, 0, 1}), every value call becomes a (sort key, value) pair for the slot-grouped fold, a
+ * new key's (or a checksum alias's) calls become one full pending record each; see
+ * value_calls() for the per-thread kernel's version of the same rules */
+template <bool CV, bool ORD, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
                                             double4 *sm, uint32_t &nred, uint64_t &ef_cn,
-                                            const Pipe &pipe = Pipe()) {
+                                            PairChunk &pc, const Pipe &pipe = Pipe()) {
     const DevStore &sLo = a.st.s[0];
     const DevStore &sLoe = a.st.s[1];
     const DevStore &sFli = a.st.s[2];
@@ -1082,6 +1129,20 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
 #endif
     const int r4 = has4 ? resolve_probe(sLi, h4, kFc.checksum, m4, &k4) : -3;
     const PendSink ps{a.pend, a.pend_count, a.pend_cap};
+    /* ORD: a slot whose checksum matches but whose key fields do not (a checksum alias) */
+    uint32_t amask = 0;
+    if (ORD) {
+        const auto alias_of = [](const DevStore &s, int r, const Key &k) -> uint32_t {
+            if (r < 0) return 0u;
+            const KeyFields kf = s.keyf[r];
+            return (kf.level != k.level || kf.c0 != k.cell[0] || kf.c1 != k.cell[1] ||
+                    kf.c2 != k.cell[2] || kf.d0 != k.dir[0] || kf.d1 != k.dir[1]) ? 1u : 0u;
+        };
+        amask = alias_of(sLo, r0, kLo) | alias_of(sLoe, r1, kLo) << 1 |
+                alias_of(sFli, r2, kFc) << 2 | alias_of(sFli, r3, kFn) << 3 |
+                alias_of(sLi, r4, kFc) << 4;
+        if (amask) atomicOr(a.pend2_count + 1, 1ull);
+    }
 
     if (CV && live) {
         /* ---- fused CV lookup (estimators.cpp:453-462; k_cv_lookup semantics): the Lo\E query
@@ -1132,11 +1193,18 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const auto li = [&](int c, double lo_e) {
         return S.f(PS_NEMIS + c) * S.f(PS_NMIS) + lo_e;
     };
-    const auto add3 = [](double4 &v, uint32_t &nc, unsigned &rej, double x, double y, double z2) {
+    /* ORD: the contribution's individual value calls (at most two) */
+    double3 call0 = make_double3(0.0, 0.0, 0.0), call1 = call0;
+    const auto add3 = [&](double4 &v, uint32_t &nc, unsigned &rej, double x, double y, double z2) {
         if (finite3(x, y, z2)) {
-            v.x += x;
-            v.y += y;
-            v.z += z2;
+            if (ORD) {
+                if (nc == 1) call0 = make_double3(x, y, z2);
+                else call1 = make_double3(x, y, z2);
+            } else {
+                v.x += x;
+                v.y += y;
+                v.z += z2;
+            }
             ++nc;
         } else {
             ++rej;
@@ -1224,9 +1292,46 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
          * contribution with a slot; 16-bit fields per store */
         if (res >= 0) {
             touch_slot(s, (uint32_t)res, mark);
-            ef_cn += 1ull << (16 * sid);
+            if (!ORD) ef_cn += 1ull << (16 * sid);
         }
-        if (PendRec *p = warp_reserve(ps, res == -1)) { /* a new key (rare after warm-up) */
+        if (ORD) {
+            const bool al = (amask >> c) & 1u;
+            const uint32_t nv = nc - 1; /* value calls of this contribution */
+            const auto nz = [](double3 q) { return q.x != 0.0 || q.y != 0.0 || q.z != 0.0; };
+            const bool p0 = res >= 0 && !al && nv > 0 && nz(call0);
+            const bool p1 = res >= 0 && !al && nv > 1 && nz(call1);
+            const unsigned b0 = __ballot_sync(0xffffffffu, p0), b1 = __ballot_sync(0xffffffffu, p1);
+            const unsigned tot = __popc(b0) + __popc(b1);
+            if (tot) {
+                const unsigned long long base = pair_reserve(a, pc, tot);
+                const int capl = a.pend2_capl, S2 = capl + 2;
+                const uint64_t sk = ((uint64_t)sid << capl) | (uint32_t)(res >= 0 ? res : 0);
+                const unsigned lt = (1u << lane) - 1u;
+                if (p0) {
+                    const unsigned long long pos = base + __popc(b0 & lt);
+                    if (pos < a.pend2_cap) {
+                        a.pend2_key[pos] = (sk << (64 - S2)) | (dbits(call0.x) >> S2);
+                        a.pend2_val[pos] = make_double4(call0.x, call0.y, call0.z, 0.0);
+                    }
+                }
+                if (p1) {
+                    const unsigned long long pos = base + __popc(b0) + __popc(b1 & lt);
+                    if (pos < a.pend2_cap) {
+                        a.pend2_key[pos] = (sk << (64 - S2)) | (dbits(call1.x) >> S2);
+                        a.pend2_val[pos] = make_double4(call1.x, call1.y, call1.z, 0.0);
+                    }
+                }
+            }
+            const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
+            const bool full = res == -1 || al;
+            if (PendRec *p = warp_reserve(ps, res == -1)) /* a new key's counter call */
+                put_record(p, k, PSTF_META(sid, 1, 1) | ((uint32_t)s.rank << 3), 0.0, 0.0, 0.0,
+                           1.0);
+            if (PendRec *p = warp_reserve(ps, full && nv > 0))
+                put_record(p, k, PSTF_META(sid, 0, 1), call0.x, call0.y, call0.z, 1.0);
+            if (PendRec *p = warp_reserve(ps, full && nv > 1))
+                put_record(p, k, PSTF_META(sid, 0, 1), call1.x, call1.y, call1.z, 1.0);
+        } else if (PendRec *p = warp_reserve(ps, res == -1)) { /* a new key (rare after warm-up) */
             const Key k = c < 2 ? kLo : (c == 3 ? kFn : kFc);
             put_record(p, k, PSTF_META(sid, 0, nc) | ((uint32_t)s.rank << 3), v.x, v.y, v.z, v.w);
         }
@@ -1248,7 +1353,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     pipe.values_done();
 }
 
-template <int STAGES, int MINB, bool TMAP, bool CV = false>
+template <int STAGES, int MINB, bool TMAP, bool CV = false, bool ORD = false>
 __global__ void __launch_bounds__(VT, MINB)
     k_vertex_pass_tiled(VPArgs2 a, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1280,6 +1385,7 @@ __global__ void __launch_bounds__(VT, MINB)
         }
     uint32_t it = 0, nred = 0;
     uint64_t ef_cn = 0; /* per-store 16-bit counters, flushed every 1024 tiles */
+    PairChunk pc;       /* ORD only */
     const auto flush_ef = [&]() {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -1320,13 +1426,17 @@ __global__ void __launch_bounds__(VT, MINB)
         if (PSTF_VP_DBG_BUILD & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body<CV>(a, src, live, sm, nred, ef_cn);
+            vertex_body<CV, ORD>(a, src, live, sm, nred, ef_cn, pc);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
         if ((it & 1023u) == 1023u) flush_ef();
     }
     flush_ef();
+    if (ORD) {
+        pair_close(a, pc);
+        if ((tid & 31) == 0 && pc.holes) atomicAdd(a.pend2_count + 2, (unsigned long long)pc.holes);
+    }
     /* RED element updates issued (atomic-roofline accounting, one atomic per warp) */
     for (int o = 16; o; o >>= 1) nred += __shfl_xor_sync(0xffffffffu, nred, o);
     if ((tid & 31) == 0 && nred) atomicAdd(&a.st.s[0].ctr[C_REDS], (unsigned long long)nred);
@@ -3320,9 +3430,16 @@ __global__ void k_iota32(uint32_t *idx, uint64_t n) {
 /* the general path's full record of a slot-grouped call (the slot's key: no alias reached
  * this list), exactly as the vertex pass writes a new key's value call */
 __global__ void k_slot_expand(const uint64_t *__restrict__ key, const double4 *__restrict__ val,
-                              uint64_t n, int capl, Stores4 st, PendRec *out) {
+                              uint64_t n, int capl, Stores4 st, PendRec *out,
+                              unsigned long long *cnt) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const bool real = i < n && key[i] != ~0ull; /* holes: unused tails of the tiled kernel's chunks */
+    const unsigned m = __ballot_sync(0xffffffffu, real);
+    if (!m) return;
+    unsigned long long base = 0;
+    if (lane_id() == (unsigned)(__ffs(m) - 1)) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (!real) return;
     const int S = capl + 2;
     const uint64_t sk = key[i] >> (64 - S);
     const uint32_t sid = (uint32_t)(sk >> capl), slot = (uint32_t)(sk & ((1ull << capl) - 1ull));
@@ -3337,7 +3454,8 @@ __global__ void k_slot_expand(const uint64_t *__restrict__ key, const double4 *_
     k.dir[1] = kf.d1;
     k.checksum = s.meta[slot].x;
     const double4 v = val[i];
-    put_record(out + i, k, PSTF_META(sid, 0, 1), v.x, v.y, v.z, 1.0);
+    put_record(out + base + __popc(m & ((1u << lane_id()) - 1u)), k, PSTF_META(sid, 0, 1), v.x,
+               v.y, v.z, 1.0);
 }
 
 /* own position at each run head of the sorted keys (0 elsewhere: a max-scan gives every position
@@ -3666,23 +3784,24 @@ __global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict
 }
 
 /* returns through *fallback whether the records must take the general path instead */
-static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_t n,
-                             bool *fallback, cudaStream_t st) {
+static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_t nr,
+                             uint64_t n, bool *fallback, cudaStream_t st) {
     *fallback = false;
     int capl = 0;
     for (int i = 0; i < nf; ++i)
         if (fs[i]) capl = std::max<int>(capl, (int)fs[i]->cfg.capacity_log2);
-    if (capl > 30 || n >= (1ull << 31)) {
+    if (capl > 30 || nr >= (1ull << 31)) {
         *fallback = true;
         return PSTF_OK;
     }
+    /* nr entries, n real calls: the holes (key ~0) sort behind every call and are dropped */
     const int S = capl + 2;
     const double4 *val = sc.pend2_val.as<double4>();
     const Stores4 S4 = stores4(fs, nf);
     const uint64_t nw = (n + 31) / 32;
-    ENSURE(sc.o_key2, n * 8);
-    ENSURE(sc.o_idx, n * 4);
-    ENSURE(sc.o_idx2, n * 4);
+    ENSURE(sc.o_key2, nr * 8);
+    ENSURE(sc.o_idx, nr * 4);
+    ENSURE(sc.o_idx2, nr * 4);
     ENSURE(sc.o_flag, 32); /* [0] flags, [3] records in over-long runs, [4], [5] list sizes */
     ENSURE(sc.head, n * 4);
     ENSURE(sc.uid, n * 4);
@@ -3702,7 +3821,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     double *T = sc.fterms.as<double>();
     CK(cudaMemsetAsync(sc.o_flag.p, 0, 32, st));
     CK(cudaMemsetAsync(sc.o_tgt.p, 0, nw * 8, st));
-    LAUNCH(k_iota32, grid_for(n, 256), 256, 0, st, idx0, n);
+    LAUNCH(k_iota32, grid_for(nr, 256), 256, 0, st, idx0, nr);
     const auto cub_call = [&](const char *name, int nlaunch, auto &&fn) -> int {
         size_t bytes = 0;
         CK(fn((void *)nullptr, bytes));
@@ -3714,7 +3833,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         return PSTF_OK;
     };
     int rc = cub_call("cub::DeviceRadixSort", 4, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx0, idx, (int64_t)n, 0, 64, st);
+        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx0, idx, (int64_t)nr, 0, 64, st);
     });
     if (rc) return rc;
     LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
@@ -3794,15 +3913,17 @@ static int resolve_ordered(Scratch &sc, pstf_field *const *fs, int nf, cudaStrea
     int rc = read_small(sc, sc.pend_count.p, 8, st);
     if (rc) return rc;
     uint64_t n1 = sc.h_small[0];
-    rc = read_small(sc, sc.pend2_count.p, 16, st);
+    rc = read_small(sc, sc.pend2_count.p, 24, st);
     if (rc) return rc;
-    const uint64_t n2 = std::min<uint64_t>(sc.h_small[0], sc.pend2_key.bytes / 8);
+    if (sc.h_small[0] > sc.pend2_key.bytes / 8)
+        return set_err(PSTF_E_NOMEM, "slot-grouped call buffer overflow");
+    const uint64_t n2r = sc.h_small[0], n2 = n2r - sc.h_small[2]; /* reserved, real calls */
     const bool alias = sc.h_small[1] != 0;
     if (n2) {
         bool fallback = alias;
         const bool force = getenv("PSTF_ORDERED_GENERAL") != nullptr; /* parity tests */
         if (!force && !alias) {
-            rc = fold_slot_records(sc, fs, nf, n2, &fallback, st);
+            rc = fold_slot_records(sc, fs, nf, n2r, n2, &fallback, st);
             if (rc) return rc;
         }
         if (force || fallback) { /* as full records, appended to the general path's */
@@ -3819,9 +3940,11 @@ static int resolve_ordered(Scratch &sc, pstf_field *const *fs, int nf, cudaStrea
             int capl = 0;
             for (int i = 0; i < nf; ++i)
                 if (fs[i]) capl = std::max<int>(capl, (int)fs[i]->cfg.capacity_log2);
-            LAUNCH(k_slot_expand, grid_for(n2, 256), 256, 0, st, sc.pend2_key.as<uint64_t>(),
-                   sc.pend2_val.as<double4>(), n2, capl, stores4(fs, nf),
-                   sc.pend.as<PendRec>() + n1);
+            ENSURE(sc.o_flag, 32);
+            CK(cudaMemsetAsync(sc.o_flag.p, 0, 8, st));
+            LAUNCH(k_slot_expand, grid_for(n2r, 256), 256, 0, st, sc.pend2_key.as<uint64_t>(),
+                   sc.pend2_val.as<double4>(), n2r, capl, stores4(fs, nf),
+                   sc.pend.as<PendRec>() + n1, sc.o_flag.as<unsigned long long>());
             n1 += n2;
             LAUNCH(k_set_u64, 1, 1, 0, st, sc.pend_count.as<unsigned long long>(),
                    (unsigned long long)n1);
@@ -3880,8 +4003,8 @@ static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t
     ENSURE(sc.pend_count, 8);
     if (with_seq) ENSURE(sc.pend_seq, cap * 8);
     CK(cudaMemsetAsync(sc.pend_count.p, 0, 8, st));
-    ENSURE(sc.pend2_count, 16);
-    CK(cudaMemsetAsync(sc.pend2_count.p, 0, 16, st));
+    ENSURE(sc.pend2_count, 32); /* calls (incl. holes), alias flag, holes */
+    CK(cudaMemsetAsync(sc.pend2_count.p, 0, 32, st));
     return PSTF_OK;
 }
 
@@ -4838,7 +4961,9 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                             v->nee_loe.z, v->nee_fli.x, v->nee_fli.y, v->nee_fli.z, v->flags};
     bool aligned = true;
     for (int k = 0; k < 35; ++k) aligned = aligned && ((uintptr_t)ptrs[k] % 16 == 0);
-    if (mode == PSTF_MODE_ATOMIC && shared_quant && aligned && !getenv("PSTF_NO_TMA")) {
+    const bool ord_tiled = mode == PSTF_MODE_ORDERED && !cv && !getenv("PSTF_ORDERED_PERTHREAD");
+    if ((mode == PSTF_MODE_ATOMIC || ord_tiled) && shared_quant && aligned &&
+        !getenv("PSTF_NO_TMA")) {
         VPArgs2 b;
         memset(&b, 0, sizeof(b));
         b.st = a.st;
@@ -4885,6 +5010,26 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             }
         }
+        if (mode == PSTF_MODE_ORDERED) { /* the default tiled kernel, ORDERED instantiation */
+            if (!tmap || cfg != 1) goto per_thread;
+            b.pend2_key = a.pend2_key;
+            b.pend2_val = a.pend2_val;
+            b.pend2_count = a.pend2_count;
+            b.pend2_cap = a.pend2_cap;
+            b.pend2_capl = a.pend2_capl;
+            for (pstf_field *f : fs)
+                if (f) f->unit_frame = false; /* counters are not counted (k_ef_onepass) */
+            const size_t smem1 = sizeof(TileStage) + 64;
+            static bool attr_ord = false;
+            if (!attr_ord) {
+                CK(cudaFuncSetAttribute(k_vertex_pass_tiled<1, VT_MINB, true, false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+                attr_ord = true;
+            }
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
+            LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), grid, VT, smem1, st, b, tm);
+            return PSTF_OK;
+        }
         const int stages = cfg == 0 ? 2 : 1;
         const int minb = cfg == 0 ? 3 : cfg == 1 ? VT_MINB : cfg == 2 ? 5 : 3;
         const size_t smem = stages * sizeof(TileStage) + 64;
@@ -4912,6 +5057,9 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                                   (const void *)k_vertex_pass_tiled<1, 3, true>};
             CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
+            if (getenv("PSTF_CARVEOUT")) /* experiment: the L1 / shared-memory split */
+                CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        atoi(getenv("PSTF_CARVEOUT"))));
             attr[fi] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
@@ -4927,6 +5075,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         }
         return PSTF_OK;
     }
+per_thread:
     for (pstf_field *f : fs)
         if (f) f->unit_frame = false; /* the per-thread kernels do not count (k_ef_onepass) */
     if (cv)
