@@ -3731,22 +3731,49 @@ __global__ void k_slot_fold(const double *__restrict__ T, uint64_t n,
     }
 }
 
-/* long slots, one warp each: the warp loads the next 8 x 32 terms of each component (coalesced,
- * in flight while the current ones are summed) and lanes 0, 1, 2 add the r, g, b components in
- * order from shared memory */
+/* the slots folded by a warp (more than SLOT_FOLD_WARP calls), the longest first: the ones of
+ * at least SFL_HUGE calls go to list H, the rest to list M (sizes in cnt[0], cnt[1]) */
+#define SFL_HUGE 2048
+__global__ void k_seg_lists(const uint32_t *__restrict__ start, const uint32_t *__restrict__ nseg,
+                            uint32_t *lh, uint32_t *lm, unsigned int *cnt) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint32_t ns = *nseg;
+    const uint32_t len = g < ns ? start[g + 1] - start[g] : 0u;
+    const bool h = len >= SFL_HUGE, m = len > SLOT_FOLD_WARP && len < SFL_HUGE;
+    const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
+    const unsigned bh = __ballot_sync(0xffffffffu, h), bm = __ballot_sync(0xffffffffu, m);
+    unsigned baseh = 0, basem = 0;
+    if (lane == 0) {
+        if (bh) baseh = atomicAdd(&cnt[0], (unsigned)__popc(bh));
+        if (bm) basem = atomicAdd(&cnt[1], (unsigned)__popc(bm));
+    }
+    baseh = __shfl_sync(0xffffffffu, baseh, 0);
+    basem = __shfl_sync(0xffffffffu, basem, 0);
+    if (h) lh[baseh + __popc(bh & lt)] = (uint32_t)g;
+    if (m) lm[basem + __popc(bm & lt)] = (uint32_t)g;
+}
+
+/* long slots, one warp each, taken dynamically from H then M (the longest sequential chains
+ * start first); the warp loads the next 8 x 32 terms of each component (coalesced, in flight
+ * while the current ones are summed) and lanes 0, 1, 2 add the r, g, b components in order
+ * from shared memory */
 #define SFL_G 8
 __global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict__ T, uint64_t n,
                                                         const uint64_t *__restrict__ key,
                                                         const uint32_t *__restrict__ start,
-                                                        const uint32_t *__restrict__ nseg,
-                                                        int capl, Stores4 st) {
+                                                        const uint32_t *__restrict__ lh,
+                                                        const uint32_t *__restrict__ lm,
+                                                        unsigned int *cnt, int capl, Stores4 st) {
     __shared__ double sv[8][3][SFL_G * 32];
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    const uint32_t ns = *nseg;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; g < ns; g += nwarps) {
+    const uint32_t nh = cnt[0], nl = nh + cnt[1];
+    for (;;) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(&cnt[2], 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= nl) break;
+        const uint32_t g = item < nh ? lh[item] : lm[item - nh];
         const uint32_t q0 = start[g], q1 = start[g + 1];
-        if (q1 - q0 <= SLOT_FOLD_WARP) continue; /* warp-uniform */
         double4 *dst = slot_acc(st, key[q0], capl);
         const unsigned c = lane < 3 ? lane : 0;
         double acc = (&dst->x)[c];
@@ -3768,14 +3795,14 @@ __global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict
                 for (int cc = 0; cc < 3; ++cc) sv[w][cc][k * 32 + lane] = nx[cc][k];
             __syncwarp();
             if (q + SFL_G * 32 < q1) fetch(q + SFL_G * 32);
-            const uint32_t cnt = min((uint32_t)(SFL_G * 32), q1 - q);
+            const uint32_t cnt2 = min((uint32_t)(SFL_G * 32), q1 - q);
             if (lane < 3) {
                 const double *v = sv[w][c];
-                if (cnt == SFL_G * 32) {
+                if (cnt2 == SFL_G * 32) {
 #pragma unroll 32
                     for (int k = 0; k < SFL_G * 32; ++k) acc += v[k];
                 } else {
-                    for (uint32_t k = 0; k < cnt; ++k) acc += v[k];
+                    for (uint32_t k = 0; k < cnt2; ++k) acc += v[k];
                 }
             }
         }
@@ -3902,8 +3929,11 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     LAUNCH(k_fold_starts, grid_for(n, 256), 256, 0, st, sh, rstart, n, seg);
     LAUNCH(k_fold_nruns, 1, 1, 0, st, sh, rstart, n, sc.fnruns.as<uint32_t>());
     LAUNCH(k_slot_fold, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl, S4);
-    LAUNCH(k_slot_fold_long, grid, 256, 0, st, T, n, key2, seg, sc.fnruns.as<uint32_t>(), capl,
-           S4);
+    /* the warp-folded slots, longest first, taken dynamically (lists reuse the run-list space) */
+    uint32_t *lh = reinterpret_cast<uint32_t *>(lst_t), *lm = lh + n / SFL_HUGE + 1;
+    CK(cudaMemsetAsync(flag, 0, 12, st));
+    LAUNCH(k_seg_lists, grid_for(n, 256), 256, 0, st, seg, sc.fnruns.as<uint32_t>(), lh, lm, flag);
+    LAUNCH(k_slot_fold_long, grid, 256, 0, st, T, n, key2, seg, lh, lm, flag, capl, S4);
     return PSTF_OK;
 }
 
