@@ -993,7 +993,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             n2 = cell_try(nq.q[2], qz, l0, &nx);
     uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
     uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
-    uint32_t wl = look ? sLo.meta[ql].x : 0u, we = look ? sLoe.meta[qe].x : 0u;
+    uint32_t wl = look ? ld_meta(&sLo.meta[ql]).x : 0u, we = look ? ld_meta(&sLoe.meta[qe]).x : 0u;
     double4 sl = look ? ld4_ro(com_ptr(sLo, ql)) : z4, se = look ? ld4_ro(com_ptr(sLoe, qe)) : z4;
 
     /* ---- the update keys: one level, one cell triple, one packKeyFields prefix ---- */
@@ -1025,8 +1025,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
         ql = (uint32_t)qpk & sLo.mask;
         qe = (uint32_t)qpk & sLoe.mask;
-        wl = look ? sLo.meta[ql].x : 0u;
-        we = look ? sLoe.meta[qe].x : 0u;
+        wl = look ? ld_meta(&sLo.meta[ql]).x : 0u;
+        we = look ? ld_meta(&sLoe.meta[qe]).x : 0u;
         sl = look ? ld4_ro(com_ptr(sLo, ql)) : z4;
         se = look ? ld4_ro(com_ptr(sLoe, qe)) : z4;
     }
@@ -1041,13 +1041,13 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const uint32_t h0 = kLo.pack_lo & sLo.mask, h1s = kLo.pack_lo & sLoe.mask,
                    h2 = kFc.pack_lo & sFli.mask, h3 = kFn.pack_lo & sFli.mask,
                    h4 = kFc.pack_lo & sLi.mask;
-    const uint2 m0 = live ? sLo.meta[h0] : z, m1 = live ? sLoe.meta[h1s] : z,
-                m2 = has2 ? sFli.meta[h2] : z, m3 = has3 ? sFli.meta[h3] : z,
-                m4 = has4 ? sLi.meta[h4] : z;
+    const uint2 m0 = live ? ld_meta(&sLo.meta[h0]) : z, m1 = live ? ld_meta(&sLoe.meta[h1s]) : z,
+                m2 = has2 ? ld_meta(&sFli.meta[h2]) : z, m3 = has3 ? ld_meta(&sFli.meta[h3]) : z,
+                m4 = has4 ? ld_meta(&sLi.meta[h4]) : z;
 #if PSTF_FLI_NEXT_WORD
     /* the FLi store is the crowded one: its two probes also preload the word after home */
-    const uint2 m2b = has2 ? sFli.meta[(h2 + 1) & sFli.mask] : z,
-                m3b = has3 ? sFli.meta[(h3 + 1) & sFli.mask] : z;
+    const uint2 m2b = has2 ? ld_meta(&sFli.meta[(h2 + 1) & sFli.mask]) : z,
+                m3b = has3 ? ld_meta(&sFli.meta[(h3 + 1) & sFli.mask]) : z;
 #endif
     /* CV lookup at this vertex = Lo\E query of the Lo key: speculate its home record too */
     const double4 scv = CV && live ? ld4_ro(com_ptr(sLoe, h1s)) : z4;
@@ -1086,11 +1086,11 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 int il = -1, ie = -1;
                 if (!doneLo) {
                     if (l == l0 && homeLo) il = -1; /* home word: empty, or match not > 0 */
-                    else il = resolve_find(sLo, hl, ccs, l == l0 ? wl : sLo.meta[hl].x);
+                    else il = resolve_find(sLo, hl, ccs, l == l0 ? wl : ld_meta(&sLo.meta[hl]).x);
                 }
                 if (!doneLoe) {
                     if (l == l0 && homeLoe) ie = -1;
-                    else ie = resolve_find(sLoe, he, ccs, l == l0 ? we : sLoe.meta[he].x);
+                    else ie = resolve_find(sLoe, he, ccs, l == l0 ? we : ld_meta(&sLoe.meta[he]).x);
                 }
                 const double4 cl = il >= 0 ? ld4_ro(com_ptr(sLo, il)) : z4;
                 const double4 ce = ie >= 0 ? ld4_ro(com_ptr(sLoe, ie)) : z4;
