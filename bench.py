@@ -457,7 +457,8 @@ def run_b200(args):
     # capture); the value comes from the committed capture named in traffic_source
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_vertex_pass_traffic.json")
-    if os.path.exists(tpath):
+    # the capture is of the config-2 ATOMIC tiled kernel; other kernels have none
+    if os.path.exists(tpath) and args.mode == "atomic" and args.config == 2:
         try:
             with open(tpath) as f:
                 tj = json.load(f)

@@ -56,3 +56,40 @@ def test_ordered_fast_path_equals_general(W, H, B, frames, cap, mult, evict, sce
     for it in range(frames):
         for a, b in zip(fast[it], gen[it]):
             gu.assert_slots_bitwise(a, b)
+
+
+def _run_kernel(perthread, li, W=640, H=360, B=4, frames=4, cap=18):
+    if perthread:
+        os.environ["PSTF_ORDERED_PERTHREAD"] = "1"
+    try:
+        ks = [pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI] + ([pb.KIND_LI] if li else [])
+        gs = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=cap,
+                                                base_cell_size=inputs.BASE_CORNELL * 2.0,
+                                                evict_age_frames=2))
+              for k in ks]
+        out, kernels = [], set()
+        for it in range(frames):
+            buf, n = pb.synth_generate(W, H, B, iteration=it)
+            pb.profile_enable(True)
+            pb.vertex_pass(gs[0], gs[1], gs[2], gs[3] if li else None, buf, n,
+                           mode=pb.MODE_ORDERED)
+            pb.profile_enable(False)
+            kernels |= set(pb.profile_collect())
+            pb.end_frame_all(gs)
+            out.append([s.slots() for s in gs])
+        return out, kernels
+    finally:
+        os.environ.pop("PSTF_ORDERED_PERTHREAD", None)
+
+
+@pytest.mark.parametrize("li", [False, True])
+def test_ordered_tiled_kernel_equals_per_thread_kernel(li):
+    """The ORDERED instantiation of the TMA-tiled vertex kernel (chunk-reserved pairs, holes)
+    against the per-thread ORDERED kernel: every slot array bitwise, with and without Li."""
+    tiled, kt = _run_kernel(False, li)
+    per, kp = _run_kernel(True, li)
+    assert any("k_vertex_pass_tiled" in k for k in kt)
+    assert not any("k_vertex_pass_tiled" in k for k in kp)
+    for a_it, b_it in zip(tiled, per):
+        for a, b in zip(a_it, b_it):
+            gu.assert_slots_bitwise(a, b)
