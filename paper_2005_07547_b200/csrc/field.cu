@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #ifndef PSTF_PRED_RED
 #define PSTF_PRED_RED 1
 #endif
+#ifndef PSTF_MATCH_AGG
+#define PSTF_MATCH_AGG 0 /* experiment builds: warp aggregation of same-slot REDs */
+#endif
 #ifndef PSTF_FLI_NEXT_WORD
 #define PSTF_FLI_NEXT_WORD 1
 #endif
@@ -1260,8 +1263,39 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
          * cell hit one 32 B sector, so L1 sends 8 sector requests per instruction, not 32 */
         int *rsm = reinterpret_cast<int *>(sm + 32);
         const unsigned lane = lane_id();
+#if PSTF_MATCH_AGG
+        /* experiment (VERDICT N1): lanes whose contributions hit one slot are summed first and
+         * only the lowest of them issues the REDs (profiles/round2_match_any_ab.md); variant 2
+         * only when two neighbouring lanes share a slot (the cheap test for hot cells) */
+        const int rn = __shfl_down_sync(0xffffffffu, res, 1);
+        if (PSTF_MATCH_AGG == 1 || __any_sync(0xffffffffu, res >= 0 && lane < 31 && rn == res)) {
+            const unsigned peers =
+                __match_any_sync(0xffffffffu, res >= 0 ? (uint32_t)res : 0x80000000u | lane);
+            const int leader = __ffs(peers) - 1;
+            sm[lane] = v;
+            __syncwarp();
+            if (__popc(peers) > 1 && (int)lane == leader) {
+                unsigned m = peers & (peers - 1);
+                while (m) {
+                    const double4 o = sm[__ffs(m) - 1];
+                    m &= m - 1;
+                    v.x += o.x;
+                    v.y += o.y;
+                    v.z += o.z;
+                    v.w += o.w;
+                }
+            }
+            __syncwarp();
+            sm[lane] = v;
+            rsm[lane] = (PSTF_VP_DBG_BUILD & 2) || (int)lane != leader ? -3 : res;
+        } else {
+            sm[lane] = v;
+            rsm[lane] = (PSTF_VP_DBG_BUILD & 2) ? -3 : res;
+        }
+#else
         sm[lane] = v;
         rsm[lane] = (PSTF_VP_DBG_BUILD & 2) ? -3 : res;
+#endif
         __syncwarp();
         const double *flat = reinterpret_cast<const double *>(sm);
         const int comp = lane & 3;

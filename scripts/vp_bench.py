@@ -19,9 +19,10 @@ p.add_argument("--width", type=int, default=1920)
 p.add_argument("--height", type=int, default=1080)
 p.add_argument("--bounces", type=int, default=4)
 p.add_argument("--cap", type=int, default=22)
+p.add_argument("--base-mult", type=float, default=1.0, help="cell size multiplier (coarser cells: hotter slots)")
 args = p.parse_args()
 
-base = math.sqrt(12.0) / 256.0
+base = math.sqrt(12.0) / 256.0 * args.base_mult
 stores = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=args.cap, base_cell_size=base))
           for k in (0, 1, 3)]
 bufs = []
