@@ -228,7 +228,10 @@ int pstf_field_committed_host(pstf_field *f, uint32_t *checksum, double *com4);
  * Returns once phase 1 is enqueued on the stream: the placement of new keys (phase 2) is
  * completed by the next entry point that touches one of these stores, and pstf_fields_end_frame
  * on the same stream needs no host round trip when there are none (PSTF_NO_DEFER=1 places them
- * before returning).  Results are identical either way. */
+ * before returning).  Results are identical either way.  ORDERED passes finish before
+ * returning: the value calls of keys that already own a slot are put in the queue's order by
+ * the slot-grouped path (one radix sort, re-sorted runs, a sequential fold per slot) after one
+ * host read of the call counts; a checksum alias sends them through the general path. */
 int pstf_vertex_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li,
                      const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask, uint32_t fli_mask,
                      int mode, void *stream);

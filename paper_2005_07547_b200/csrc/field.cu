@@ -178,6 +178,8 @@ struct Scratch {
     DBuf o_key, o_key2, o_idx, o_idx2, o_tgt, o_flag; // their slot-grouped sort (o_tgt: run marks)
     DBuf o_fp, o_fk;                                  // its marked runs' re-sort
     DBuf cn_cnt, cn_vals;                             // endFrame: Σc_new in slot order
+    DBuf iota;                                        // 0, 1, 2, ... (iota_n entries written)
+    uint64_t iota_n = 0;
     uint64_t live_bound = 0;
     long long *live_total_dev = nullptr;
     bool overflow_zeroed = false;
@@ -3882,7 +3884,12 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     double *T = sc.fterms.as<double>();
     CK(cudaMemsetAsync(sc.o_flag.p, 0, 32, st));
     CK(cudaMemsetAsync(sc.o_tgt.p, 0, nw * 8, st));
-    LAUNCH(k_iota32, grid_for(nr, 256), 256, 0, st, idx0, nr);
+    if (sc.iota_n < nr) { /* the sort's input indices, written once per size */
+        ENSURE(sc.iota, nr * 4);
+        sc.iota_n = sc.iota.bytes / 4;
+        LAUNCH(k_iota32, grid_for(sc.iota_n, 256), 256, 0, st, sc.iota.as<uint32_t>(), sc.iota_n);
+    }
+    const uint32_t *iota = sc.iota.as<uint32_t>();
     const auto cub_call = [&](const char *name, int nlaunch, auto &&fn) -> int {
         size_t bytes = 0;
         CK(fn((void *)nullptr, bytes));
@@ -3894,12 +3901,12 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
         return PSTF_OK;
     };
     int rc = cub_call("cub::DeviceRadixSort", 4, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx0, idx, (int64_t)nr, 0, 64, st);
+        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, iota, idx, (int64_t)nr, 0, 64, st);
     });
     if (rc) return rc;
     LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
     /* runs of equal sort keys holding an out-of-order pair, re-sorted in place by length class */
-    uint32_t *sh = idx0; /* slot-segment heads (the sort's input indices are spent) */
+    uint32_t *sh = idx0; /* slot-segment heads */
     LAUNCH(k_run_heads, grid_for(n, 256), 256, 0, st, key2, n, S, hp, sh);
     rc = cub_call("cub::DeviceScan", 2, [&](void *t, size_t &b) {
         return cub::DeviceScan::InclusiveScan(t, b, hp, rstart, cub::Max(), (int64_t)n, st);
