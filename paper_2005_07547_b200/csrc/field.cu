@@ -222,9 +222,18 @@ struct pstf_field {
     bool unit_frame = true;
     /* pstf_field_apply with counter calls this frame: their weights may make Σc_new inexact */
     bool counted_apply = false;
+    /* hot-slot detection for the tiled vertex pass (this store as its Lo store): the last
+     * frame's REDs per touched slot, copied back asynchronously after endFrame */
+    DBuf rd_dev;
+    unsigned long long *rd_host = nullptr; /* pinned: {reds_total, touched slots} */
+    cudaEvent_t rd_ev = nullptr;
+    unsigned long long rd_last = 0;
+    bool rd_pending = false, rd_probe = false, agg = false;
     ~pstf_field() {
         if (dp.ev) cudaEventDestroy(dp.ev);
         if (dp.h_count) cudaFreeHost(dp.h_count);
+        if (rd_ev) cudaEventDestroy(rd_ev);
+        if (rd_host) cudaFreeHost(rd_host);
     }
 };
 
@@ -757,9 +766,6 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #ifndef PSTF_PRED_RED
 #define PSTF_PRED_RED 1
 #endif
-#ifndef PSTF_MATCH_AGG
-#define PSTF_MATCH_AGG 0 /* experiment builds: warp aggregation of same-slot REDs */
-#endif
 #ifndef PSTF_FLI_NEXT_WORD
 #define PSTF_FLI_NEXT_WORD 1
 #endif
@@ -965,7 +971,7 @@ __device__ __forceinline__ unsigned long long pair_reserve(const VPArgs2 &a, Pai
  * {0, 0, 0, 1}), every value call becomes a (sort key, value) pair for the slot-grouped fold, a
  * new key's (or a checksum alias's) calls become one full pending record each; see
  * value_calls() for the per-thread kernel's version of the same rules */
-template <bool CV, bool ORD, class Src, class Pipe = NoPipe>
+template <bool CV, bool ORD, bool AGG, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
                                             double4 *sm, uint32_t &nred, uint64_t &ef_cn,
                                             PairChunk &pc, const Pipe &pipe = Pipe()) {
@@ -1265,12 +1271,15 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
          * cell hit one 32 B sector, so L1 sends 8 sector requests per instruction, not 32 */
         int *rsm = reinterpret_cast<int *>(sm + 32);
         const unsigned lane = lane_id();
-#if PSTF_MATCH_AGG
-        /* experiment (VERDICT N1): lanes whose contributions hit one slot are summed first and
-         * only the lowest of them issues the REDs (profiles/round2_match_any_ab.md); variant 2
-         * only when two neighbouring lanes share a slot (the cheap test for hot cells) */
-        const int rn = __shfl_down_sync(0xffffffffu, res, 1);
-        if (PSTF_MATCH_AGG == 1 || __any_sync(0xffffffffu, res >= 0 && lane < 31 && rn == res)) {
+        /* the RED element updates of this lane's own contribution (before any aggregation:
+         * the hot-slot measure must not depend on the variant that measured it) */
+        const uint32_t own = AGG && res >= 0 ? (uint32_t)(v.x != 0.0) + (v.y != 0.0) +
+                                                   (v.z != 0.0) + (v.w != 0.0)
+                                             : 0u;
+        if (AGG) {
+            /* hot slots (chosen per launch from the last frame's RED density): lanes whose
+             * contributions hit one slot are summed first and only the lowest of them issues
+             * the REDs (profiles/round2_match_any_ab.md) */
             const unsigned peers =
                 __match_any_sync(0xffffffffu, res >= 0 ? (uint32_t)res : 0x80000000u | lane);
             const int leader = __ffs(peers) - 1;
@@ -1294,10 +1303,6 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             sm[lane] = v;
             rsm[lane] = (PSTF_VP_DBG_BUILD & 2) ? -3 : res;
         }
-#else
-        sm[lane] = v;
-        rsm[lane] = (PSTF_VP_DBG_BUILD & 2) ? -3 : res;
-#endif
         __syncwarp();
         const double *flat = reinterpret_cast<const double *>(sm);
         const int comp = lane & 3;
@@ -1322,7 +1327,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
 #endif
             cnt += on;
         }
-        nred += cnt;
+        nred += AGG ? own : cnt;
         __syncwarp();
         /* unit-weight frame accounting (k_ef_onepass): one counter call of weight 1 per
          * contribution with a slot; 16-bit fields per store */
@@ -1389,7 +1394,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     pipe.values_done();
 }
 
-template <int STAGES, int MINB, bool TMAP, bool CV = false, bool ORD = false>
+template <int STAGES, int MINB, bool TMAP, bool CV = false, bool ORD = false, bool AGG = false>
 __global__ void __launch_bounds__(VT, MINB)
     k_vertex_pass_tiled(VPArgs2 a, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1462,7 +1467,7 @@ __global__ void __launch_bounds__(VT, MINB)
         if (PSTF_VP_DBG_BUILD & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body<CV, ORD>(a, src, live, sm, nred, ef_cn, pc);
+            vertex_body<CV, ORD, AGG>(a, src, live, sm, nred, ef_cn, pc);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
@@ -2559,6 +2564,16 @@ __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
         if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
     }
 }
+/* {REDs issued so far by the tiled passes of store lo, touched slots of the frame just
+ * committed over the batch} (hot-slot detection, pstf_fields_end_frame) */
+__global__ void k_red_density(Stores4 st, int nst, int lo, unsigned long long *out) {
+    if (threadIdx.x) return;
+    unsigned long long t = 0;
+    for (int i = 0; i < nst; ++i) t += st.s[i].ctr[C_TOUCHED_LAST];
+    out[0] = st.s[lo].ctr[C_REDS];
+    out[1] = t;
+}
+
 __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int finish) {
     if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
         const DevStore &s = st.s[threadIdx.x];
@@ -4568,6 +4583,18 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
             SETTLE(owner); /* nothing pending: just retire the deferred pass */
         }
     }
+    for (int i = 0; i < n; ++i) /* the Lo store of a tiled pass: its RED density, async */
+        if (fs[i]->rd_probe) {
+            pstf_field *f = fs[i];
+            f->rd_probe = false;
+            ENSURE(f->rd_dev, 16);
+            if (!f->rd_host) CK(cudaMallocHost(&f->rd_host, 16));
+            if (!f->rd_ev) CK(cudaEventCreateWithFlags(&f->rd_ev, cudaEventDisableTiming));
+            LAUNCH(k_red_density, 1, 32, 0, st, S, n, i, f->rd_dev.as<unsigned long long>());
+            CK(cudaMemcpyAsync(f->rd_host, f->rd_dev.p, 16, cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(f->rd_ev, st));
+            f->rd_pending = true;
+        }
     for (int i = 0; i < n; ++i) {
         fs[i]->frame += 1;
         fs[i]->unit_frame = true;
@@ -5116,6 +5143,31 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         }
         const int fi = cfg == 0 ? 0 : cfg == 2 ? (tmap ? 6 : 1) : cfg == 3 ? 7
                      : (tmap ? 3 : 2) + (cvf ? 2 : 0);
+        if (fi == 3) { /* hot slots: the warp-aggregating instantiation (RED density > 1000) */
+            bool agg = lo->agg;
+            if (lo->rd_pending && cudaEventQuery(lo->rd_ev) == cudaSuccess) {
+                const unsigned long long reds = lo->rd_host[0], touched = lo->rd_host[1];
+                if (touched && reds >= lo->rd_last)
+                    agg = (double)(reds - lo->rd_last) / (double)touched > 1000.0;
+                lo->rd_last = reds;
+                lo->rd_pending = false;
+                lo->agg = agg;
+            }
+            if (const char *e = getenv("PSTF_RED_AGG")) agg = atoi(e) != 0; /* force on / off */
+            lo->rd_probe = true;
+            if (agg) {
+                static bool attr_agg = false;
+                if (!attr_agg) {
+                    CK(cudaFuncSetAttribute(k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    attr_agg = true;
+                }
+                const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
+                LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>), grid, VT, smem, st,
+                       b, tm);
+                return PSTF_OK;
+            }
+        }
         static bool attr[8] = {false, false, false, false, false, false, false, false};
         if (!attr[fi]) {
             const void *fns[8] = {(const void *)k_vertex_pass_tiled<2, 3, false>,

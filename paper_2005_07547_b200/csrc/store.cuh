@@ -96,7 +96,8 @@ enum Ctr : int {
     C_LIVE_SNAP,    // endFrame: live count before eviction (field.cpp:205-212)
     C_TOUCHED_LAST, // touched slots of the last committed frame
     C_TOUCHED_TOTAL, // touched slots summed over all committed frames
-    C_REDS,          // fp64 RED element updates issued by fused vertex passes (Lo store)
+    C_REDS,          // fp64 RED element updates of the fused vertex passes' contributions, before
+                     // any warp aggregation (Lo store)
     C_ROUNDS,        // deterministic-placement rounds of the last update pass
     C_F_CN,          // this frame: sum of counter weights into existing/placed slots (unit-
                      // weight frames: an exact integer, = field.cpp:205-212's sum of c_new)
