@@ -224,8 +224,7 @@ struct pstf_field {
     bool counted_apply = false;
     /* hot-slot detection for the tiled vertex pass (this store as its Lo store): the last
      * frame's REDs per touched slot, copied back asynchronously after endFrame */
-    DBuf rd_dev;
-    unsigned long long *rd_host = nullptr; /* pinned: {reds_total, touched slots} */
+    unsigned long long *rd_host = nullptr; /* mapped pinned: {reds_total, touched slots} */
     cudaEvent_t rd_ev = nullptr;
     unsigned long long rd_last = 0;
     bool rd_pending = false, rd_probe = false, agg = false;
@@ -2564,16 +2563,6 @@ __device__ __forceinline__ void ef_blend_body(const Stores4 &st, int nst) {
         if (lane_id() == 0 && t) atomicAdd(&st.s[q].ctr[C_INTERNAL], (unsigned long long)t);
     }
 }
-/* {REDs issued so far by the tiled passes of store lo, touched slots of the frame just
- * committed over the batch} (hot-slot detection, pstf_fields_end_frame) */
-__global__ void k_red_density(Stores4 st, int nst, int lo, unsigned long long *out) {
-    if (threadIdx.x) return;
-    unsigned long long t = 0;
-    for (int i = 0; i < nst; ++i) t += st.s[i].ctr[C_TOUCHED_LAST];
-    out[0] = st.s[lo].ctr[C_REDS];
-    out[1] = t;
-}
-
 __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int finish) {
     if (finish && blockIdx.x == 0 && threadIdx.x < nst) { /* roll the per-frame scratch */
         const DevStore &s = st.s[threadIdx.x];
@@ -2744,7 +2733,8 @@ __device__ __forceinline__ void ef_roll(const DevStore &s) {
 
 __global__ void __launch_bounds__(EF_BLOCK) k_ef_tail(Stores4 st, int nst,
                                                       const unsigned long long *guard,
-                                                      unsigned int *done) {
+                                                      unsigned int *done, int rd_lo,
+                                                      unsigned long long *rd_out) {
     if (guard && *guard) return;
     ef_tail_body(st, nst);
     /* last block: roll the per-frame counters */
@@ -2753,6 +2743,17 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_tail(Stores4 st, int nst,
     if (threadIdx.x == 0) {
         __threadfence();
         last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && rd_out && threadIdx.x == 0) {
+        /* hot-slot measure of the tiled vertex pass whose Lo store is rd_lo: its RED element
+         * updates so far and the frame's touched slots, straight into mapped host memory */
+        unsigned long long t = 0;
+        for (int i = 0; i < nst; ++i) t += st.s[i].ctr[C_TOUCHED_N];
+        volatile unsigned long long *o = rd_out;
+        o[0] = st.s[rd_lo].ctr[C_REDS];
+        o[1] = t;
+        __threadfence_system();
     }
     __syncthreads();
     if (last && threadIdx.x < (unsigned)nst) {
@@ -4095,7 +4096,10 @@ static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t
 }
 
 /* ORDERED vertex passes: room for every value call of an existing slot (<= 7 per vertex) */
-static int ensure_pending2(Scratch &sc, uint64_t cap) {
+static int ensure_pending2(Scratch &sc, uint64_t calls) {
+    /* every value call (<= 7 per vertex) plus the tiled kernel's unused chunk tails (at most
+     * one chunk per warp of its persistent grid) */
+    const uint64_t cap = calls + (uint64_t)sm_count() * VT_MINB * (VT / 32) * PAIR_CHUNK;
     ENSURE(sc.pend2_key, cap * 8);
     ENSURE(sc.pend2_val, cap * 32);
     return PSTF_OK;
@@ -4523,6 +4527,20 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
     static const bool no_onepass = getenv("PSTF_NO_ONEPASS_EF") != nullptr;
     bool unit = !no_onepass;
     for (int i = 0; i < n; ++i) unit = unit && fs[i]->unit_frame;
+    /* the Lo store of this frame's tiled vertex pass: the tail reports its RED density */
+    int rd_lo = -1;
+    unsigned long long *rd_dev = nullptr;
+    for (int i = 0; i < n && rd_lo < 0; ++i)
+        if (fs[i]->rd_probe && unit) {
+            pstf_field *f = fs[i];
+            if (!f->rd_host) {
+                CK(cudaHostAlloc(&f->rd_host, 16, cudaHostAllocMapped));
+                f->rd_host[0] = f->rd_host[1] = 0;
+            }
+            if (!f->rd_ev) CK(cudaEventCreateWithFlags(&f->rd_ev, cudaEventDisableTiming));
+            CK(cudaHostGetDevicePointer((void **)&rd_dev, f->rd_host, 0));
+            rd_lo = i;
+        }
     auto launch = [&](const unsigned long long *gd) -> int {
         if (unit) { /* counted frame: one pass over the touched slots, then the tail */
             Scratch &sc0 = fs[0]->sc;
@@ -4533,7 +4551,7 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
             LAUNCH(k_ef_onepass, g, EF_BLOCK, 0, st, S, n, gd);
             /* one block per SM: the deferred list is short, eviction rarely runs */
             LAUNCH(k_ef_tail, std::min<unsigned>(g, (unsigned)sm_count()), EF_BLOCK, 0, st, S, n, gd,
-                   sc0.ef_done.as<unsigned int>());
+                   sc0.ef_done.as<unsigned int>(), rd_lo, rd_dev);
             return PSTF_OK;
         }
         for (int i = 0; i < n; ++i) { /* Σc_new in slot order, inexact frames only */
@@ -4583,18 +4601,11 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
             SETTLE(owner); /* nothing pending: just retire the deferred pass */
         }
     }
-    for (int i = 0; i < n; ++i) /* the Lo store of a tiled pass: its RED density, async */
-        if (fs[i]->rd_probe) {
-            pstf_field *f = fs[i];
-            f->rd_probe = false;
-            ENSURE(f->rd_dev, 16);
-            if (!f->rd_host) CK(cudaMallocHost(&f->rd_host, 16));
-            if (!f->rd_ev) CK(cudaEventCreateWithFlags(&f->rd_ev, cudaEventDisableTiming));
-            LAUNCH(k_red_density, 1, 32, 0, st, S, n, i, f->rd_dev.as<unsigned long long>());
-            CK(cudaMemcpyAsync(f->rd_host, f->rd_dev.p, 16, cudaMemcpyDeviceToHost, st));
-            CK(cudaEventRecord(f->rd_ev, st));
-            f->rd_pending = true;
-        }
+    if (rd_lo >= 0) { /* the density is readable once this event completes */
+        CK(cudaEventRecord(fs[rd_lo]->rd_ev, st));
+        fs[rd_lo]->rd_pending = true;
+    }
+    for (int i = 0; i < n; ++i) fs[i]->rd_probe = false;
     for (int i = 0; i < n; ++i) {
         fs[i]->frame += 1;
         fs[i]->unit_frame = true;
@@ -5146,7 +5157,8 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         if (fi == 3) { /* hot slots: the warp-aggregating instantiation (RED density > 1000) */
             bool agg = lo->agg;
             if (lo->rd_pending && cudaEventQuery(lo->rd_ev) == cudaSuccess) {
-                const unsigned long long reds = lo->rd_host[0], touched = lo->rd_host[1];
+                const volatile unsigned long long *h = lo->rd_host;
+                const unsigned long long reds = h[0], touched = h[1];
                 if (touched && reds >= lo->rd_last)
                     agg = (double)(reds - lo->rd_last) / (double)touched > 1000.0;
                 lo->rd_last = reds;
@@ -5154,7 +5166,8 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                 lo->agg = agg;
             }
             if (const char *e = getenv("PSTF_RED_AGG")) agg = atoi(e) != 0; /* force on / off */
-            lo->rd_probe = true;
+            /* measured on the first frames (the first one inserts: few REDs), then every 4th */
+            lo->rd_probe = lo->frame < 4 || (lo->frame & 3) == 0;
             if (agg) {
                 static bool attr_agg = false;
                 if (!attr_agg) {

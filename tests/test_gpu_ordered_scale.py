@@ -93,3 +93,14 @@ def test_ordered_tiled_kernel_equals_per_thread_kernel(li):
     for a_it, b_it in zip(tiled, per):
         for a, b in zip(a_it, b_it):
             gu.assert_slots_bitwise(a, b)
+
+
+@pytest.mark.parametrize("W,H,B", [(10, 10, 2), (20, 10, 1), (33, 7, 3), (128, 72, 4)])
+def test_ordered_small_passes_equal_per_thread_kernel(W, H, B):
+    """Small ORDERED passes through the tiled kernel (a few tiles, most warps reserving a pair
+    chunk they barely use) equal the per-thread kernel, frame after frame."""
+    tiled, _ = _run_kernel(False, False, W=W, H=H, B=B, frames=3, cap=12)
+    per, _ = _run_kernel(True, False, W=W, H=H, B=B, frames=3, cap=12)
+    for a_it, b_it in zip(tiled, per):
+        for a, b in zip(a_it, b_it):
+            gu.assert_slots_bitwise(a, b)
