@@ -4096,10 +4096,11 @@ static int ensure_pending(Scratch &sc, uint64_t cap, bool with_seq, cudaStream_t
 }
 
 /* ORDERED vertex passes: room for every value call of an existing slot (<= 7 per vertex) */
-static int ensure_pending2(Scratch &sc, uint64_t calls) {
+static int ensure_pending2(Scratch &sc, uint64_t calls, uint64_t launches = 1) {
     /* every value call (<= 7 per vertex) plus the tiled kernel's unused chunk tails (at most
-     * one chunk per warp of its persistent grid) */
-    const uint64_t cap = calls + (uint64_t)sm_count() * VT_MINB * (VT / 32) * PAIR_CHUNK;
+     * one chunk per warp of its persistent grid, per launch) */
+    const uint64_t cap =
+        calls + launches * (uint64_t)sm_count() * VT_MINB * (VT / 32) * PAIR_CHUNK;
     ENSURE(sc.pend2_key, cap * 8);
     ENSURE(sc.pend2_val, cap * 32);
     return PSTF_OK;
@@ -5343,11 +5344,11 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
     cudaStream_t st = (cudaStream_t)stream;
     rc = ensure_pending(lo->sc, std::max<uint64_t>(1, n * records_per_vertex(mode, li)), false, st);
     if (rc) return rc;
-    if (mode == PSTF_MODE_ORDERED) {
-        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7));
+    const uint64_t chunk = std::min<uint64_t>(n, 1ull << 21);
+    if (mode == PSTF_MODE_ORDERED) { /* one phase-1 launch per chunk */
+        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7), (n + chunk - 1) / chunk);
         if (rc) return rc;
     }
-    const uint64_t chunk = std::min<uint64_t>(n, 1ull << 21);
     static thread_local cudaStream_t cs = nullptr;
     static thread_local cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     static thread_local DBuf stage[2];
