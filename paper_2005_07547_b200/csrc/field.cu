@@ -5346,7 +5346,8 @@ int pstf_vertex_pass_host(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf
     if (rc) return rc;
     const uint64_t chunk = std::min<uint64_t>(n, 1ull << 21);
     if (mode == PSTF_MODE_ORDERED) { /* one phase-1 launch per chunk */
-        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7), (n + chunk - 1) / chunk);
+        rc = ensure_pending2(lo->sc, std::max<uint64_t>(1, n * 7),
+                             chunk ? (n + chunk - 1) / chunk : 1);
         if (rc) return rc;
     }
     static thread_local cudaStream_t cs = nullptr;
