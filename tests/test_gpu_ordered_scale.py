@@ -104,3 +104,20 @@ def test_ordered_small_passes_equal_per_thread_kernel(W, H, B):
     for a_it, b_it in zip(tiled, per):
         for a, b in zip(a_it, b_it):
             gu.assert_slots_bitwise(a, b)
+
+
+@pytest.mark.parametrize("mode", ["atomic", "ordered"])
+def test_empty_passes(mode):
+    """n = 0 through the device and the host entry points: no error, nothing changes."""
+    gm = pb.MODE_ATOMIC if mode == "atomic" else pb.MODE_ORDERED
+    gs = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=12,
+                                            base_cell_size=inputs.BASE_CORNELL))
+          for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
+    buf, n = pb.synth_generate(16, 8, 2, iteration=0)
+    pb.vertex_pass(gs[0], gs[1], gs[2], None, buf, n, mode=gm)
+    pb.end_frame_all(gs)
+    before = [s.slots() for s in gs]
+    pb.vertex_pass(gs[0], gs[1], gs[2], None, buf, 0, mode=gm)
+    pb.vertex_pass_host(gs[0], gs[1], gs[2], None, buf.cpu(), 0, mode=gm)
+    for s, b in zip(gs, before):
+        gu.assert_slots_bitwise(s.slots(), b)
