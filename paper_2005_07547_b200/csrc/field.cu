@@ -773,7 +773,9 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #endif
 #define VT VT_THREADS
 #define VT_MINB (512 / VT) /* resident CTAs per SM of the default single-stage config */
+#ifndef PSTF_VT_EXPERIMENT
 static_assert(VT_MINB == 4, "the vertex-pass launch table names 4 CTAs/SM (VT = 128)");
+#endif
 
 struct TileStage {
     double f[PS_NUM_F64][VT];
@@ -5203,12 +5205,12 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         switch (fi) {
         case 0: LAUNCH((k_vertex_pass_tiled<2, 3, false>), grid, VT, smem, st, b, tm); break;
         case 1: LAUNCH((k_vertex_pass_tiled<1, 5, false>), grid, VT, smem, st, b, tm); break;
-        case 2: LAUNCH((k_vertex_pass_tiled<1, 4, false>), grid, VT, smem, st, b, tm); break;
-        case 3: LAUNCH((k_vertex_pass_tiled<1, 4, true>), grid, VT, smem, st, b, tm); break;
-        case 4: LAUNCH((k_vertex_pass_tiled<1, 4, false, true>), grid, VT, smem, st, b, tm); break;
+        case 2: LAUNCH((k_vertex_pass_tiled<1, VT_MINB, false>), grid, VT, smem, st, b, tm); break;
+        case 3: LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true>), grid, VT, smem, st, b, tm); break;
+        case 4: LAUNCH((k_vertex_pass_tiled<1, VT_MINB, false, true>), grid, VT, smem, st, b, tm); break;
         case 6: LAUNCH((k_vertex_pass_tiled<1, 5, true>), grid, VT, smem, st, b, tm); break;
         case 7: LAUNCH((k_vertex_pass_tiled<1, 3, true>), grid, VT, smem, st, b, tm); break;
-        default: LAUNCH((k_vertex_pass_tiled<1, 4, true, true>), grid, VT, smem, st, b, tm);
+        default: LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, true>), grid, VT, smem, st, b, tm);
         }
         return PSTF_OK;
     }
