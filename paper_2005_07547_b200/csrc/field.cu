@@ -1143,7 +1143,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const PendSink ps{a.pend, a.pend_count, a.pend_cap};
     /* ORD: a slot whose checksum matches but whose key fields do not (a checksum alias) */
     uint32_t amask = 0;
-    if (ORD) {
+    if (ORD) { /* 0.15 ms of the ORDERED tiled pass on config 2 */
         const auto alias_of = [](const DevStore &s, int r, const Key &k) -> uint32_t {
             if (r < 0) return 0u;
             const KeyFields kf = s.keyf[r];
