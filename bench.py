@@ -123,7 +123,9 @@ def bench_config(args, streams, world, multi=None):
                         if args.scaling == "weak" else
                         f"{world} ranks, one frame split into {world} image stripes (strong "
                         "scaling)") + ", one field cache: replicated stores, live-slot "
-                        "accumulators all-reduced over NCCL",
+                        "accumulators all-reduced over "
+                        + ("NCCL" if os.environ.get("PSTF_BENCH_BACKEND", "nccl") == "nccl"
+                           else os.environ["PSTF_BENCH_BACKEND"] + " (bench.py test mode)"),
     }
 
 
@@ -322,6 +324,11 @@ def run_b200(args):
     import paper_2005_07547_b200 as pb
 
     rank, world, local = dist_env()
+    # PSTF_BENCH_BACKEND=gloo: the multi-rank code path on fewer GPUs than ranks (a test of
+    # bench.py itself, collectives through the host; never a measurement)
+    backend = os.environ.get("PSTF_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1 or args.force_sharded:
@@ -331,7 +338,10 @@ def run_b200(args):
             os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     W, H, B = args.width, args.height, args.bounces
     base = DIAMETER / 256.0
     mode = pb.MODE_ATOMIC if args.mode == "atomic" else pb.MODE_ORDERED
