@@ -17,15 +17,16 @@ if not torch.cuda.is_available():  # pragma: no cover
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_two_ranks():
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_two_ranks(scaling):
     env = dict(os.environ, PSTF_BENCH_BACKEND="gloo")
     env.pop("WORLD_SIZE", None)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
                         "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
-                        "--width", "640", "--height", "360"],
+                        "--width", "640", "--height", "360", "--scaling", scaling],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
-    assert line["n_gpus"] == 2 and line["scaling"] == "weak"
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert "2 ranks" in line["config"]["parallelism"]
