@@ -29,9 +29,11 @@ namespace pstf_b200 {
  *   ld4_ro  read-only data of the running kernel (committed values in the vertex pass)
  *   ld4/st4 ordered with the thread's other memory accesses (endFrame read-modify-write) */
 /* L1 policy of the probe and committed-record loads: keeping them L1-resident over the other
- * traffic measured 0.5% faster on config 2 (0.808 vs 0.812 ms, 3 interleaved A/B rounds);
- * experiment builds: PSTF_L1_COM 0 plain volatile, 1 non-volatile, 2 + L1::evict_last, 3 +
- * L1::evict_first; PSTF_L1_META 0 plain, 1 L1::evict_last */
+ * traffic measured 0.5% faster on config 2 (0.808 vs 0.812 ms, 3 interleaved A/B rounds).
+ * The meta probes live off L1 (L1::no_allocate on them: 0.877 ms); the committed records do
+ * not (no_allocate on them: unchanged).  Experiment builds: PSTF_L1_COM 0 plain volatile,
+ * 1 non-volatile, 2 + L1::evict_last, 3 + L1::evict_first, 4 + L1::no_allocate; PSTF_L1_META
+ * 0 plain, 1 L1::evict_last, 2 L1::no_allocate */
 #ifndef PSTF_L1_COM
 #define PSTF_L1_COM 2
 #endif
@@ -49,6 +51,9 @@ __device__ __forceinline__ double4 ld4_ro(const double4 *p) {
 #elif PSTF_L1_COM == 3
     asm("ld.global.L1::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
         : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+#elif PSTF_L1_COM == 4
+    asm("ld.global.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
 #else
     asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
@@ -61,6 +66,10 @@ __device__ __forceinline__ uint2 ld_meta(const uint2 *p) {
 #if PSTF_L1_META == 1
     uint2 v;
     asm volatile("ld.global.L1::evict_last.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+#elif PSTF_L1_META == 2
+    uint2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 #else
     return *p;
