@@ -228,6 +228,14 @@ struct pstf_field {
     cudaEvent_t rd_ev = nullptr;
     unsigned long long rd_last = 0;
     bool rd_pending = false, rd_probe = false, agg = false;
+    /* Twin stores: a Lo and a Lo\E store created alike and, since creation, updated only by
+     * the same vertex passes and end-framed together receive the same keys, counters and
+     * touches (estimators.cpp:219,227: Lo\E's key is the Lo key), so their occupancy and
+     * touch marks are identical and the tiled kernel takes Lo\E's probes from Lo's (one probe
+     * and one lookup word fewer per vertex).  Any other update of either store, or a pass
+     * pairing it differently, ends the relation for good (twin_break). */
+    pstf_field *twin = nullptr;
+    bool pristine = true; /* nothing has touched the store since creation */
     ~pstf_field() {
         if (dp.ev) cudaEventDestroy(dp.ev);
         if (dp.h_count) cudaFreeHost(dp.h_count);
@@ -765,6 +773,7 @@ __global__ void __launch_bounds__(VP_BLOCK) k_vertex_pass(VPArgs a) {
 #ifndef PSTF_PRED_RED
 #define PSTF_PRED_RED 1
 #endif
+
 #ifndef PSTF_FLI_NEXT_WORD
 #define PSTF_FLI_NEXT_WORD 1
 #endif
@@ -972,7 +981,7 @@ __device__ __forceinline__ unsigned long long pair_reserve(const VPArgs2 &a, Pai
  * {0, 0, 0, 1}), every value call becomes a (sort key, value) pair for the slot-grouped fold, a
  * new key's (or a checksum alias's) calls become one full pending record each; see
  * value_calls() for the per-thread kernel's version of the same rules */
-template <bool CV, bool ORD, bool AGG, class Src, class Pipe = NoPipe>
+template <bool CV, bool ORD, bool AGG, bool TWIN, class Src, class Pipe = NoPipe>
 __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool live,
                                             double4 *sm, uint32_t &nred, uint64_t &ef_cn,
                                             PairChunk &pc, const Pipe &pipe = Pipe()) {
@@ -987,6 +996,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const bool nsurf = (fl & PSTF_VERTEX_NEXT_IS_SURFACE) != 0;
     const bool nee = (fl & PSTF_VERTEX_NEE_SAMPLED) != 0;
     const bool look = cont && nsurf && !(PSTF_VP_DBG_BUILD & 1);
+    /* Lo\E shares Lo's occupancy (twin stores, see pstf_field::twin): its probes are Lo's */
+    constexpr bool TWINQ = TWIN;
 
     /* ---- keys (estimators.cpp:195, 215, 226, 242, 248, 257): one level, one cell triple and
      * one packKeyFields prefix for all update keys of the vertex ---- */
@@ -1005,7 +1016,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
             n2 = cell_try(nq.q[2], qz, l0, &nx);
     uint64_t qpk = pack_key_fields(l0, n0, n1, n2, dir_cell_f8(fin.u, l0), dir_cell_f8(fin.v, l0));
     uint32_t ql = (uint32_t)qpk & sLo.mask, qe = (uint32_t)qpk & sLoe.mask;
-    uint32_t wl = look ? ld_meta(&sLo.meta[ql]).x : 0u, we = look ? ld_meta(&sLoe.meta[qe]).x : 0u;
+    uint32_t wl = look ? ld_meta(&sLo.meta[ql]).x : 0u;
+    uint32_t we = TWINQ ? wl : (look ? ld_meta(&sLoe.meta[qe]).x : 0u);
     double4 sl = look ? ld4_ro(com_ptr(sLo, ql)) : z4, se = look ? ld4_ro(com_ptr(sLoe, qe)) : z4;
 
     /* ---- the update keys: one level, one cell triple, one packKeyFields prefix ---- */
@@ -1053,7 +1065,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     const uint32_t h0 = kLo.pack_lo & sLo.mask, h1s = kLo.pack_lo & sLoe.mask,
                    h2 = kFc.pack_lo & sFli.mask, h3 = kFn.pack_lo & sFli.mask,
                    h4 = kFc.pack_lo & sLi.mask;
-    const uint2 m0 = live ? ld_meta(&sLo.meta[h0]) : z, m1 = live ? ld_meta(&sLoe.meta[h1s]) : z,
+    const uint2 m0 = live ? ld_meta(&sLo.meta[h0]) : z,
+                m1 = TWINQ ? m0 : (live ? ld_meta(&sLoe.meta[h1s]) : z),
                 m2 = has2 ? ld_meta(&sFli.meta[h2]) : z, m3 = has3 ? ld_meta(&sFli.meta[h3]) : z,
                 m4 = has4 ? ld_meta(&sLi.meta[h4]) : z;
 #if PSTF_FLI_NEXT_WORD
@@ -1102,6 +1115,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 }
                 if (!doneLoe) {
                     if (l == l0 && homeLoe) ie = -1;
+                    else if (TWINQ && !doneLo) ie = il;
                     else ie = resolve_find(sLoe, he, ccs, l == l0 ? we : ld_meta(&sLoe.meta[he]).x);
                 }
                 const double4 cl = il >= 0 ? ld4_ro(com_ptr(sLo, il)) : z4;
@@ -1131,7 +1145,13 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
      * words die before the values are built ---- */
     uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
     const int r0 = live ? resolve_probe(sLo, h0, kLo.checksum, m0, &k0) : -3;
-    const int r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
+    int r1 = -3;
+    if (TWINQ) {
+        r1 = r0;
+        k1 = k0;
+    } else {
+        r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
+    }
 #if PSTF_FLI_NEXT_WORD
     const int r2 = has2 ? resolve_probe2(sFli, h2, kFc.checksum, m2, m2b, &k2) : -3;
     const int r3 = has3 ? resolve_probe2(sFli, h3, kFn.checksum, m3, m3b, &k3) : -3;
@@ -1395,7 +1415,8 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     pipe.values_done();
 }
 
-template <int STAGES, int MINB, bool TMAP, bool CV = false, bool ORD = false, bool AGG = false>
+template <int STAGES, int MINB, bool TMAP, bool CV = false, bool ORD = false, bool AGG = false,
+          bool TWIN = false>
 __global__ void __launch_bounds__(VT, MINB)
     k_vertex_pass_tiled(VPArgs2 a, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1468,7 +1489,7 @@ __global__ void __launch_bounds__(VT, MINB)
         if (PSTF_VP_DBG_BUILD & 32) { /* experiment: stream only */
             if (src.f(PS_FP) == -12345.0) atomicAdd(&a.st.s[0].ctr[C_INTERNAL], 1ull);
         } else {
-            vertex_body<CV, ORD, AGG>(a, src, live, sm, nred, ef_cn, pc);
+            vertex_body<CV, ORD, AGG, TWIN>(a, src, live, sm, nred, ef_cn, pc);
         }
         __syncthreads(); /* every lane is done with stage s */
         if (tid == 0) issue_next();
@@ -4113,6 +4134,50 @@ static bool same_quant(const pstf_field_config &a, const pstf_field_config &b) {
            a.max_level == b.max_level;
 }
 
+static void twin_break(pstf_field *f) {
+    if (!f) return;
+    if (f->twin) f->twin->twin = nullptr;
+    f->twin = nullptr;
+    f->pristine = false;
+}
+
+/* a batch operation on stores fs[0..n): a store whose twin is not in the batch loses it */
+static void twin_batch(pstf_field *const *fs, int n) {
+    for (int i = 0; i < n; ++i) {
+        if (!fs[i]) continue;
+        bool in = false;
+        for (int j = 0; j < n; ++j) in = in || (fs[j] && fs[j] == fs[i]->twin);
+        if (fs[i]->twin && !in) twin_break(fs[i]);
+        fs[i]->pristine = false;
+    }
+}
+
+/* the twin relation of (lo, loe) for a vertex pass: kept, established (both fresh and alike),
+ * or ended; the other stores of the pass lose theirs */
+static bool twin_for_pass(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_field *li) {
+    bool twin = lo->twin == loe && loe->twin == lo;
+    if (!twin) {
+        const pstf_field_config &a = lo->cfg, &b = loe->cfg;
+        if (lo->pristine && loe->pristine && lo != loe && a.capacity_log2 == b.capacity_log2 &&
+            a.probe_window == b.probe_window && a.evict_age_frames == b.evict_age_frames &&
+            same_quant(a, b) && lo->frame == loe->frame && !getenv("PSTF_NO_TWIN")) {
+            twin_break(lo);
+            twin_break(loe);
+            lo->twin = loe;
+            loe->twin = lo;
+            twin = true;
+        } else {
+            twin_break(lo);
+            twin_break(loe);
+        }
+    }
+    if (fli != lo && fli != loe) twin_break(fli);
+    if (li && li != lo && li != loe) twin_break(li);
+    lo->pristine = loe->pristine = false;
+    return twin;
+}
+
+
 static int check_config(const pstf_field_config *c) {
     if (!c) return set_err(PSTF_E_INVALID, "config is NULL");
     if (c->capacity_log2 < 1 || c->capacity_log2 > 30)
@@ -4245,6 +4310,7 @@ int pstf_field_create(const pstf_field_config *config, int device, pstf_field **
 
 int pstf_field_destroy(pstf_field *f) {
     if (!f) return PSTF_OK;
+    twin_break(f); /* the partner must not keep a pointer to it */
     cudaSetDevice(f->device);
     settle(f); /* no dangling deferred pass may reference this store */
     cudaDeviceSynchronize();
@@ -4283,6 +4349,7 @@ int pstf_field_apply(pstf_field *f, const pstf_key *keys, const pstf_vec3_soa *v
                      const double *w, const uint8_t *is_counter, uint64_t n, int mode,
                      void *stream) {
     if (f) f->unit_frame = false; /* arbitrary weights: endFrame's reduce pass */
+    twin_break(f);                /* an update of this store alone */
     if (!f || (n && (!keys || !w))) return set_err(PSTF_E_INVALID, "NULL argument");
     if (mode < 0 || mode > 2) return set_err(PSTF_E_INVALID, "bad mode");
     if (!n) return PSTF_OK;
@@ -4507,6 +4574,7 @@ int pstf_fields_end_frame(pstf_field *const *fs, int n, void *stream) {
             if (fs[j] == fs[i]) return set_err(PSTF_E_INVALID, "store listed twice");
     }
     CK(cudaSetDevice(fs[0]->device));
+    twin_batch(fs, n); /* twins are end-framed together or not at all */
     cudaStream_t st = (cudaStream_t)stream;
     /* a deferred vertex pass of these stores on this stream: enqueue endFrame guarded by its
      * device-side pending count, then look at the count; other deferred passes settle first */
@@ -4624,6 +4692,7 @@ int pstf_field_end_frame(pstf_field *f, void *stream) {
 
 int pstf_field_invalidate(pstf_field *f, const double *aabb, void *stream) {
     if (!f) return set_err(PSTF_E_INVALID, "NULL argument");
+    twin_break(f);
     CK(cudaSetDevice(f->device));
     SETTLE(f);
     const uint64_t cap = (uint64_t)f->d.mask + 1;
@@ -4909,6 +4978,7 @@ static bool snap_key_less(const pstf_snapshot_record &a, const pstf_snapshot_rec
 
 extern "C" int pstf_field_restore(pstf_field *f, const pstf_snapshot_record *records, uint64_t n) {
     if (f) f->unit_frame = false; /* arbitrary weights: endFrame's reduce pass */
+    twin_break(f);
     if (!f || (n && !records)) return set_err(PSTF_E_INVALID, "NULL argument");
     if (n >= 0xffffffffULL) return set_err(PSTF_E_INVALID, "too many records");
     for (uint64_t i = 0; i < n; ++i) { /* keyFor's checksum (field.cpp:98-99) */
@@ -5036,6 +5106,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                          const pstf_vertex_soa *v, uint64_t n, uint32_t loe_mask,
                          uint32_t fli_mask, int mode, cudaStream_t st,
                          const CvOut *cv = nullptr) {
+    const bool twin = twin_for_pass(lo, loe, fli, li);
     VPArgs a;
     memset(&a, 0, sizeof(a));
     pstf_field *fs[4] = {lo, loe, fli, li};
@@ -5181,6 +5252,19 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                 const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
                 LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>), grid, VT, smem, st,
                        b, tm);
+                return PSTF_OK;
+            }
+            if (twin) { /* Lo\E's probes taken from Lo's (pstf_field::twin) */
+                static bool attr_twin = false;
+                if (!attr_twin) {
+                    CK(cudaFuncSetAttribute(
+                        k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>,
+                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    attr_twin = true;
+                }
+                const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
+                LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>), grid, VT,
+                       smem, st, b, tm);
                 return PSTF_OK;
             }
         }
@@ -5529,6 +5613,7 @@ int pstf_resolve_records(pstf_field *const *stores, int nst, const void *recs, u
                          void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
+    twin_batch(stores, nst);
     CK(cudaSetDevice(stores[0]->device));
     for (int i_ = 0; i_ < nst; ++i_) SETTLE(stores[i_]);
     cudaStream_t st = (cudaStream_t)stream;
@@ -5598,6 +5683,7 @@ int pstf_shard_live_unpack(pstf_field *const *stores, int nst, const double *pac
                            void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
+    twin_batch(stores, nst);
     Scratch &sc = stores[0]->sc;
     if (!sc.live_total_dev) return set_err(PSTF_E_INVALID, "pstf_shard_live_pack first");
     if (sc.live_bound && !packed) return set_err(PSTF_E_INVALID, "NULL packed");
@@ -5616,6 +5702,7 @@ int pstf_shard_end_frame(pstf_field *const *stores, int nst, const double *packe
                          void *stream) {
     int rc = shard_checks(stores, nst);
     if (rc) return rc;
+    twin_batch(stores, nst);
     for (int i = 0; i < nst; ++i)
         for (int j = 0; j < i; ++j)
             if (stores[j] == stores[i]) return set_err(PSTF_E_INVALID, "store listed twice");
