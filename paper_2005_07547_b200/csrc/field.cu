@@ -30,6 +30,7 @@
 #include <tuple>
 #include <mutex>
 #include <new>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -3158,6 +3159,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+/* the dynamic shared-memory limit is an attribute of a kernel on one device: set once per
+ * (kernel, device) pair */
+static int smem_attr(const void *fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({fn, dev})) return PSTF_OK;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({fn, dev});
+    return PSTF_OK;
+}
+#define SMEM_ATTR(fn, bytes)                                                                       \
+    do {                                                                                           \
+        int rc_ = smem_attr((const void *)(fn), (int)(bytes));                                   \
+        if (rc_) return rc_;                                                                       \
+    } while (0)
+
 static int read_small(Scratch &sc, const void *dev, size_t bytes, cudaStream_t st) {
     if (!sc.h_small) CK(cudaMallocHost(&sc.h_small, 4096));
     CK(cudaMemcpyAsync(sc.h_small, dev, bytes, cudaMemcpyDeviceToHost, st));
@@ -3973,7 +3993,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     LAUNCH(k_fix_small, grid, 256, 0, st, T, n, lst_t, flag);
     LAUNCH(k_fix_warp, grid, 256, 0, st, T, n, lst_w, flag);
     const size_t fsm = 3 * FIX_BLOCK * 8;
-    CK(cudaFuncSetAttribute(k_fix_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    SMEM_ATTR(k_fix_block, fsm);
     LAUNCH(k_fix_block, (unsigned)sm_count() * 2, 512, fsm, st, T, n, lst_b, flag);
     rc = read_small(sc, sc.o_flag.p, 32, st); /* the pass's one host read */
     if (rc) return rc;
@@ -5215,12 +5235,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             for (pstf_field *f : fs)
                 if (f) f->unit_frame = false; /* counters are not counted (k_ef_onepass) */
             const size_t smem1 = sizeof(TileStage) + 64;
-            static bool attr_ord = false;
-            if (!attr_ord) {
-                CK(cudaFuncSetAttribute(k_vertex_pass_tiled<1, VT_MINB, true, false, true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-                attr_ord = true;
-            }
+            SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), smem1);
             const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
             LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), grid, VT, smem1, st, b, tm);
             return PSTF_OK;
@@ -5255,33 +5270,21 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             /* measured on the first frames (the first one inserts: few REDs), then every 4th */
             lo->rd_probe = lo->frame < 4 || (lo->frame & 3) == 0;
             if (agg) {
-                static bool attr_agg = false;
-                if (!attr_agg) {
-                    CK(cudaFuncSetAttribute(k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    attr_agg = true;
-                }
+                SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>), smem);
                 const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
                 LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, true>), grid, VT, smem, st,
                        b, tm);
                 return PSTF_OK;
             }
             if (twin) { /* Lo\E's probes taken from Lo's (pstf_field::twin) */
-                static bool attr_twin = false;
-                if (!attr_twin) {
-                    CK(cudaFuncSetAttribute(
-                        k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>,
-                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    attr_twin = true;
-                }
+                SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>), smem);
                 const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
                 LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>), grid, VT,
                        smem, st, b, tm);
                 return PSTF_OK;
             }
         }
-        static bool attr[8] = {false, false, false, false, false, false, false, false};
-        if (!attr[fi]) {
+        {
             const void *fns[8] = {(const void *)k_vertex_pass_tiled<2, 3, false>,
                                   (const void *)k_vertex_pass_tiled<1, 5, false>,
                                   (const void *)k_vertex_pass_tiled<1, VT_MINB, false>,
@@ -5290,12 +5293,10 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                                   (const void *)k_vertex_pass_tiled<1, VT_MINB, true, true>,
                                   (const void *)k_vertex_pass_tiled<1, 5, true>,
                                   (const void *)k_vertex_pass_tiled<1, 3, true>};
-            CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+            SMEM_ATTR(fns[fi], smem);
             if (getenv("PSTF_CARVEOUT")) /* experiment: the L1 / shared-memory split */
                 CK(cudaFuncSetAttribute(fns[fi], cudaFuncAttributePreferredSharedMemoryCarveout,
                                         atoi(getenv("PSTF_CARVEOUT"))));
-            attr[fi] = true;
         }
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
         switch (fi) {
