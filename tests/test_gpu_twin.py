@@ -21,7 +21,25 @@ TWIN_NAME = "k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, tru"  # 
 EXACT = ("checksum", "level", "cell", "dir", "last_touched")
 
 
-def _run(no_twin, break_at=None, frames=5, evict=2, cap=16):
+def _break(gs, how):
+    """end the relation: an update, invalidation, restore or endFrame of Lo\\E alone"""
+    if how == "apply":
+        keys = gs[1].snapshot()[:50]
+        k = torch.from_numpy(np.stack([keys["level"], keys["cell"][:, 0], keys["cell"][:, 1],
+                                       keys["cell"][:, 2], keys["dir"][:, 0], keys["dir"][:, 1],
+                                       keys["checksum"].view(np.int32)], 1).astype(np.int32).copy())
+        n = len(keys)
+        gs[1].apply(k, torch.ones((3, n), dtype=torch.float64), torch.ones(n, dtype=torch.float64),
+                    torch.zeros(n, dtype=torch.uint8), pb.MODE_ATOMIC)
+    elif how == "invalidate":
+        gs[1].invalidate(((-0.5, 0.0, -0.5), (0.5, 1.0, 0.5)))
+    elif how == "restore":
+        gs[1].restore(gs[1].snapshot()[:100])
+    elif how == "end_frame":
+        gs[1].end_frame()
+
+
+def _run(no_twin, break_at=None, frames=5, evict=2, cap=16, how="apply"):
     if no_twin:
         os.environ["PSTF_NO_TWIN"] = "1"
     try:
@@ -31,16 +49,8 @@ def _run(no_twin, break_at=None, frames=5, evict=2, cap=16):
               for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
         used, out = [], []
         for it in range(frames):
-            if it == break_at:  # an update of Lo\E alone ends the relation
-                keys = gs[1].snapshot()[:50]
-                k = torch.from_numpy(np.stack([keys["level"], keys["cell"][:, 0], keys["cell"][:, 1],
-                                               keys["cell"][:, 2], keys["dir"][:, 0],
-                                               keys["dir"][:, 1], keys["checksum"].view(np.int32)],
-                                              1).astype(np.int32).copy())
-                n = len(keys)
-                gs[1].apply(k, torch.ones((3, n), dtype=torch.float64),
-                            torch.ones(n, dtype=torch.float64),
-                            torch.zeros(n, dtype=torch.uint8), pb.MODE_ATOMIC)
+            if it == break_at:
+                _break(gs, how)
             buf, n = pb.synth_generate(320, 180, 4, iteration=it)
             pb.profile_enable(True)
             pb.vertex_pass(gs[0], gs[1], gs[2], None, buf, n)
@@ -71,8 +81,9 @@ def test_twin_equals_separate_probes():
         gu.assert_slots_bitwise(fr[0], fr[1], EXACT)
 
 
-def test_twin_broken_by_a_single_store_update():
-    used_t, twin = _run(False, break_at=2)
-    used_s, sep = _run(True, break_at=2)
+@pytest.mark.parametrize("how", ["apply", "invalidate", "restore", "end_frame"])
+def test_twin_broken_by_a_single_store_update(how):
+    used_t, twin = _run(False, break_at=2, how=how)
+    used_s, sep = _run(True, break_at=2, how=how)
     assert used_t == [True, True, False, False, False] and not any(used_s)
     _same(twin, sep)
