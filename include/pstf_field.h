@@ -228,7 +228,12 @@ int pstf_field_committed_host(pstf_field *f, uint32_t *checksum, double *com4);
  * Returns once phase 1 is enqueued on the stream: the placement of new keys (phase 2) is
  * completed by the next entry point that touches one of these stores, and pstf_fields_end_frame
  * on the same stream needs no host round trip when there are none (PSTF_NO_DEFER=1 places them
- * before returning).  Results are identical either way.  ORDERED passes finish before
+ * before returning).  Results are identical either way.  Two behaviours are chosen inside:
+ * when lo and loe were created alike and have only ever been updated together (vertex passes,
+ * batched end-frames) they hold identical occupancy, and the kernel takes loe's probes from lo's
+ * (any other update of either ends that for good: PSTF_NO_TWIN=1 disables it); and when the
+ * previous frame issued more than 1000 RED updates per touched slot (hot slots: coarse cells),
+ * a warp-aggregating kernel variant runs (PSTF_RED_AGG=0|1 forces it).  ORDERED passes finish before
  * returning: the value calls of keys that already own a slot are put in the queue's order by
  * the slot-grouped path (one radix sort, re-sorted runs, a sequential fold per slot) after one
  * host read of the call counts; a checksum alias sends them through the general path. */
