@@ -227,7 +227,6 @@ struct pstf_field {
      * frame's REDs per touched slot, copied back asynchronously after endFrame */
     unsigned long long *rd_host = nullptr; /* mapped pinned: {reds_total, touched slots} */
     cudaEvent_t rd_ev = nullptr;
-    unsigned long long rd_last = 0;
     bool rd_pending = false, rd_probe = false, agg = false;
     /* Twin stores: a Lo and a Lo\E store created alike and, since creation, updated only by
      * the same vertex passes and end-framed together receive the same keys, counters and
@@ -2609,6 +2608,7 @@ __device__ __forceinline__ void ef_evict_body(const Stores4 &st, int nst, int fi
         s.ctr[C_F_CN] = 0;
         s.ctr[C_F_DEFER] = 0;
         s.ctr[C_CN_INEXACT] = 0;
+        s.ctr[C_REDS_MARK] = s.ctr[C_REDS];
         *s.cn_sum = 0.0;
     }
     for (int j = 0; j < nst; ++j) {
@@ -2764,6 +2764,7 @@ __device__ __forceinline__ void ef_roll(const DevStore &s) {
     s.ctr[C_F_CN] = 0;
     s.ctr[C_F_DEFER] = 0;
     s.ctr[C_CN_INEXACT] = 0;
+    s.ctr[C_REDS_MARK] = s.ctr[C_REDS];
     *s.cn_sum = 0.0;
 }
 
@@ -2787,7 +2788,7 @@ __global__ void __launch_bounds__(EF_BLOCK) k_ef_tail(Stores4 st, int nst,
         unsigned long long t = 0;
         for (int i = 0; i < nst; ++i) t += st.s[i].ctr[C_TOUCHED_N];
         volatile unsigned long long *o = rd_out;
-        o[0] = st.s[rd_lo].ctr[C_REDS];
+        o[0] = st.s[rd_lo].ctr[C_REDS] - st.s[rd_lo].ctr[C_REDS_MARK]; /* this frame's */
         o[1] = t;
         __threadfence_system();
     }
@@ -5259,10 +5260,8 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             bool agg = lo->agg;
             if (lo->rd_pending && cudaEventQuery(lo->rd_ev) == cudaSuccess) {
                 const volatile unsigned long long *h = lo->rd_host;
-                const unsigned long long reds = h[0], touched = h[1];
-                if (touched && reds >= lo->rd_last)
-                    agg = (double)(reds - lo->rd_last) / (double)touched > 1000.0;
-                lo->rd_last = reds;
+                const unsigned long long reds = h[0], touched = h[1]; /* of one frame */
+                if (touched) agg = (double)reds / (double)touched > 1000.0;
                 lo->rd_pending = false;
                 lo->agg = agg;
             }

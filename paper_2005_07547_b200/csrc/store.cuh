@@ -111,6 +111,7 @@ enum Ctr : int {
     C_F_CN,          // this frame: sum of counter weights into existing/placed slots (unit-
                      // weight frames: an exact integer, = field.cpp:205-212's sum of c_new)
     C_F_DEFER,       // one-pass endFrame: touched slots deferred to k_ef_tail (may be capped)
+    C_REDS_MARK,     // C_REDS at the start of the frame (the hot-slot measure's per-frame REDs)
     C_CN_INEXACT,    // this frame: a counter weight that is not a whole number <= 2^20 (then
                      // Σc_new is summed sequentially in slot order, field.cpp:201-213)
     C_NUM
