@@ -5256,6 +5256,13 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         }
         const int fi = cfg == 0 ? 0 : cfg == 2 ? (tmap ? 6 : 1) : cfg == 3 ? 7
                      : (tmap ? 3 : 2) + (cvf ? 2 : 0);
+        if (fi == 5 && twin) { /* the fused CV lookup with Lo\E's probes taken from Lo's */
+            SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, true, false, false, true>), smem);
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
+            LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, true, false, false, true>), grid, VT, smem,
+                   st, b, tm);
+            return PSTF_OK;
+        }
         if (fi == 3) { /* hot slots: the warp-aggregating instantiation (RED density > 1000) */
             bool agg = lo->agg;
             if (lo->rd_pending && cudaEventQuery(lo->rd_ev) == cudaSuccess) {
