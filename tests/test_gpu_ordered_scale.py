@@ -18,19 +18,21 @@ import inputs  # noqa: E402
 import paper_2005_07547_b200 as pb  # noqa: E402
 
 
-def _run(general, W, H, B, frames, cap, mult, evict, scene):
+def _run(general, W, H, B, frames, cap, mult, evict, scene, li=False):
     if general:
         os.environ["PSTF_ORDERED_GENERAL"] = "1"
     try:
+        kinds = [pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI] + ([pb.KIND_LI] if li else [])
         gs = [pb.FieldStore(pb.FieldStoreConfig(kind=k, capacity_log2=cap,
                                                 base_cell_size=inputs.BASE_CORNELL * mult,
                                                 evict_age_frames=evict))
-              for k in (pb.KIND_LO, pb.KIND_LO_MINUS_E, pb.KIND_FLI)]
+              for k in kinds]
         out, kernels = [], set()
         for it in range(frames):
             buf, n = pb.synth_generate(W, H, B, iteration=it, scene=scene)
             pb.profile_enable(True)
-            pb.vertex_pass(gs[0], gs[1], gs[2], None, buf, n, mode=pb.MODE_ORDERED)
+            pb.vertex_pass(gs[0], gs[1], gs[2], gs[3] if li else None, buf, n,
+                           mode=pb.MODE_ORDERED)
             pb.profile_enable(False)
             kernels |= set(pb.profile_collect())
             pb.end_frame_all(gs)
@@ -38,6 +40,16 @@ def _run(general, W, H, B, frames, cap, mult, evict, scene):
         return out, kernels
     finally:
         os.environ.pop("PSTF_ORDERED_GENERAL", None)
+
+
+def test_ordered_fast_path_equals_general_with_li():
+    """config-2 scale with the Li store (a fourth store in the sort key's store field)"""
+    fast, kf = _run(False, 1920, 1080, 4, 2, 22, 1.0, 64, 0, li=True)
+    gen, _ = _run(True, 1920, 1080, 4, 2, 22, 1.0, 64, 0, li=True)
+    assert "k_run_check" in kf
+    for it in range(2):
+        for a, b in zip(fast[it], gen[it]):
+            gu.assert_slots_bitwise(a, b)
 
 
 @pytest.mark.parametrize("W,H,B,frames,cap,mult,evict,scene,fast_runs", [
