@@ -35,6 +35,9 @@ def _run(mult, force=None, frames=6):
             pb.profile_enable(False)
             used.append(any(AGG_NAME in k for k in pb.profile_collect()))
             pb.end_frame_all(gs)
+            # the measure comes back asynchronously; a pass that finds it not yet written keeps
+            # the previous choice for one more frame, so let it land before the next pass
+            torch.cuda.synchronize()
             out.append([s.slots() for s in gs])
         return used, out
     finally:
