@@ -1259,7 +1259,9 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     int rr0 = r0, rr1 = r1, rr2 = r2, rr3 = r3, rr4 = r4;
     uint32_t kk0 = k0, kk1 = k1, kk2 = k2, kk3 = k3, kk4 = k4;
     uint32_t rejpack = 0; /* rejected calls per store, one byte each (at most 3 per vertex) */
-    const int ncontrib = a.has_li ? 5 : 4;
+    /* the TWIN instantiations run only without an Li store: its branch is compiled out (a
+     * smaller rolled loop, 1% on config 2) */
+    const int ncontrib = !TWIN && a.has_li ? 5 : 4;
 #pragma unroll 1
     for (int c = 0; c < ncontrib; ++c) {
         double4 v = make_double4(0.0, 0.0, 0.0, 1.0); /* the counter call */
@@ -1289,7 +1291,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
         } else if (c == 3) { /* FLi NEE (247-254) */
             if (nee && (a.fli_mask & PSTF_TECH_NEE))
                 add3(v, nc, rej, S.f(PS_NEEFLI), S.f(PS_NEEFLI + 1), S.f(PS_NEEFLI + 2));
-        } else { /* Li (256-261) */
+        } else if (!TWIN) { /* Li (256-261) */
             if (cont)
                 add3(v, nc, rej, li(0, loeNext.x) * 1.0, li(1, loeNext.y) * 1.0,
                      li(2, loeNext.z) * 1.0);
@@ -5264,7 +5266,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
         }
         const int fi = cfg == 0 ? 0 : cfg == 2 ? (tmap ? 6 : 1) : cfg == 3 ? 7
                      : (tmap ? 3 : 2) + (cvf ? 2 : 0);
-        if (fi == 5 && twin) { /* the fused CV lookup with Lo\E's probes taken from Lo's */
+        if (fi == 5 && twin && !li) { /* the fused CV lookup, Lo\E's probes taken from Lo's */
             SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, true, false, false, true>), smem);
             const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
             LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, true, false, false, true>), grid, VT, smem,
@@ -5290,7 +5292,7 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
                        b, tm);
                 return PSTF_OK;
             }
-            if (twin) { /* Lo\E's probes taken from Lo's (pstf_field::twin) */
+            if (twin && !li) { /* Lo\E's probes taken from Lo's (pstf_field::twin), no Li */
                 SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>), smem);
                 const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * minb);
                 LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, false, false, true>), grid, VT,
