@@ -177,7 +177,7 @@ struct Scratch {
     DBuf ef_done;                           // one-pass endFrame: blocks done (last rolls)
     DBuf pend2_key, pend2_val, pend2_count; // ORDERED: value calls of existing slots
     DBuf o_key, o_key2, o_idx, o_idx2, o_tgt, o_flag; // their slot-grouped sort (o_tgt: run marks)
-    DBuf o_fp, o_fk, o_ms;                            // its marked runs' re-sort
+    DBuf o_fp, o_fk;                                  // its marked runs' re-sort
     DBuf cn_cnt, cn_vals;                             // endFrame: Σc_new in slot order
     DBuf iota;                                        // 0, 1, 2, ... (iota_n entries written)
     uint64_t iota_n = 0;
@@ -3592,82 +3592,68 @@ __global__ void k_slot_terms(const double4 *__restrict__ val, const uint32_t *__
 }
 
 /* the run check on the sorted terms: a call that sorts before its neighbour inside a run of
- * equal keys marks the run (bit at its start; a newly marked run's start is appended to
- * mstart); each run's length is written at its start */
+ * equal keys marks the run (bit at its start); each run's length is written at its start */
 __global__ void k_run_check(const double *__restrict__ T, const uint64_t *__restrict__ key,
                             const uint32_t *__restrict__ rstart, uint64_t n, uint32_t *claim,
-                            uint32_t *runlen, uint32_t *mstart, unsigned int *mcount) {
+                            uint32_t *runlen) {
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const unsigned lane = lane_id();
-    bool mark = false;
-    uint32_t s0 = 0;
-    if (q < n) {
-        const uint64_t k = key[q];
-        s0 = rstart[q];
-        if (q > 0 && k == key[q - 1]) {
-            const uint64_t a0 = dbits(T[q]), b0 = dbits(T[q - 1]);
-            bool lt = a0 < b0;
-            if (a0 == b0) {
-                const uint64_t a1 = dbits(T[n + q]), b1 = dbits(T[n + q - 1]);
-                lt = a1 < b1 || (a1 == b1 && dbits(T[2 * n + q]) < dbits(T[2 * n + q - 1]));
-            }
-            if (lt) {
-                const uint32_t bit = 1u << (s0 & 31u);
-                mark = !(atomicOr(&claim[s0 >> 5], bit) & bit);
-            }
-        }
-        if (q == n - 1 || key[q + 1] != k) runlen[s0] = (uint32_t)(q + 1 - s0);
+    if (q >= n) return;
+    const uint64_t k = key[q];
+    const uint32_t s0 = rstart[q];
+    if (q > 0 && k == key[q - 1]) {
+        const uint64_t a0 = dbits(T[q]), b0 = dbits(T[q - 1]), a1 = dbits(T[n + q]),
+                       b1 = dbits(T[n + q - 1]), a2 = dbits(T[2 * n + q]),
+                       b2 = dbits(T[2 * n + q - 1]);
+        if (a0 != b0 ? a0 < b0 : a1 != b1 ? a1 < b1 : a2 < b2)
+            atomicOr(&claim[s0 >> 5], 1u << (s0 & 31u));
     }
-    const unsigned m = __ballot_sync(0xffffffffu, mark);
-    if (m) {
-        const int leader = __ffs(m) - 1;
-        unsigned base = 0;
-        if ((int)lane == leader) base = atomicAdd(mcount, (unsigned)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (mark) mstart[base + __popc(m & ((1u << lane) - 1u))] = s0;
-    }
+    if (q == n - 1 || key[q + 1] != k) runlen[s0] = (uint32_t)(q + 1 - s0);
 }
 
 #define FIX_THREAD 32  /* marked runs up to this long: rank sort by one warp */
 #define FIX_WARP 256   /* up to this long: bitonic sort in shared memory by one warp */
 #define FIX_BLOCK 4096 /* up to this long: the same by one block */
 
-/* the marked runs (their starts from k_run_check), by length: (start, length) lists for the
- * warp rank sort, the warp bitonic and the block bitonic sorters (cnt[4], cnt[7], cnt[5]);
- * longer runs are marked again (claim2) for the radix path and counted (flag bit 2, cnt[3]) */
-__global__ void k_marked_lists(const uint32_t *__restrict__ mstart, const unsigned int *mcount,
-                               const uint32_t *__restrict__ runlen, uint2 *lst_t, uint2 *lst_w,
-                               uint2 *lst_b, unsigned int *cnt, uint32_t *claim2) {
-    const uint32_t nm = *mcount;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t rounds = (nm + stride - 1) / stride; /* warp-uniform trip count */
-    const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
-    for (uint64_t r = 0; r < rounds; ++r) {
-        const uint64_t e = r * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-        const bool in = e < nm;
-        const uint32_t j = in ? mstart[e] : 0u, len = in ? runlen[j] : 0u;
-        const bool ct = in && len <= FIX_THREAD, cw = in && len > FIX_THREAD && len <= FIX_WARP,
-                   cb = in && len > FIX_WARP && len <= FIX_BLOCK;
-        const uint2 item = make_uint2(j, len);
-        const unsigned mt = __ballot_sync(0xffffffffu, ct), mw = __ballot_sync(0xffffffffu, cw),
-                       mb = __ballot_sync(0xffffffffu, cb);
-        unsigned bt = 0, bw = 0, bb = 0;
-        if (lane == 0) {
-            if (mt) bt = atomicAdd(&cnt[4], (unsigned)__popc(mt));
-            if (mw) bw = atomicAdd(&cnt[7], (unsigned)__popc(mw));
-            if (mb) bb = atomicAdd(&cnt[5], (unsigned)__popc(mb));
-        }
-        bt = __shfl_sync(0xffffffffu, bt, 0);
-        bw = __shfl_sync(0xffffffffu, bw, 0);
-        bb = __shfl_sync(0xffffffffu, bb, 0);
-        if (ct) lst_t[bt + __popc(mt & lt)] = item;
-        if (cw) lst_w[bw + __popc(mw & lt)] = item;
-        if (cb) lst_b[bb + __popc(mb & lt)] = item;
-        if (in && len > FIX_BLOCK) {
+/* the marked runs (the claim bitmap of k_run_check, a 32-position word per thread), by length:
+ * (start, length) lists for the warp rank sort, the warp bitonic and the block bitonic sorters
+ * (cnt[4], cnt[7], cnt[5]; one global reservation per block and list); longer runs are marked
+ * again (claim2) for the radix path and counted (flag bit 2, cnt[3]) */
+__global__ void __launch_bounds__(256) k_marked_lists(const uint32_t *__restrict__ claim, uint64_t nw,
+                                                      const uint32_t *__restrict__ runlen,
+                                                      uint2 *lst_t, uint2 *lst_w, uint2 *lst_b,
+                                                      unsigned int *cnt, uint32_t *claim2) {
+    __shared__ unsigned bc[3], bb[3];
+    if (threadIdx.x < 3) bc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint32_t bits = w < nw ? claim[w] : 0u;
+    unsigned mine[3] = {0u, 0u, 0u};
+    for (uint32_t m = bits; m; m &= m - 1) { /* count this word's runs per class */
+        const uint32_t j = (uint32_t)(w * 32 + (uint64_t)(__ffs(m) - 1)), len = runlen[j];
+        if (len <= FIX_THREAD) ++mine[0];
+        else if (len <= FIX_WARP) ++mine[1];
+        else if (len <= FIX_BLOCK) ++mine[2];
+        else {
             atomicOr(&claim2[j >> 5], 1u << (j & 31u));
             atomicOr(&cnt[0], 2u);
             atomicAdd(&cnt[3], len);
         }
+    }
+    unsigned off[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) off[c] = mine[c] ? atomicAdd(&bc[c], mine[c]) : 0u;
+    __syncthreads();
+    if (threadIdx.x < 3 && bc[threadIdx.x]) {
+        unsigned *g = threadIdx.x == 0 ? &cnt[4] : threadIdx.x == 1 ? &cnt[7] : &cnt[5];
+        bb[threadIdx.x] = atomicAdd(g, bc[threadIdx.x]);
+    }
+    __syncthreads();
+    for (uint32_t m = bits; m; m &= m - 1) {
+        const uint32_t j = (uint32_t)(w * 32 + (uint64_t)(__ffs(m) - 1)), len = runlen[j];
+        const uint2 item = make_uint2(j, len);
+        if (len <= FIX_THREAD) lst_t[bb[0] + off[0]++] = item;
+        else if (len <= FIX_WARP) lst_w[bb[1] + off[1]++] = item;
+        else if (len <= FIX_BLOCK) lst_b[bb[2] + off[2]++] = item;
     }
 }
 
@@ -3948,7 +3934,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     ENSURE(sc.o_key2, nr * 8);
     ENSURE(sc.o_idx, nr * 4);
     ENSURE(sc.o_idx2, nr * 4);
-    ENSURE(sc.o_flag, 32); /* [0] flags, [1] marked runs, [3] calls in over-long runs, [4] [5] [7] list sizes */
+    ENSURE(sc.o_flag, 32); /* [0] flags, [3] calls in over-long runs, [4] [5] [7] list sizes */
     ENSURE(sc.head, n * 4);
     ENSURE(sc.uid, n * 4);
     ENSURE(sc.rank, n * 4);       /* run lengths (at run starts) */
@@ -3995,13 +3981,12 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     });
     if (rc) return rc;
     LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
-    ENSURE(sc.o_ms, (n / 2 + 1) * 4); /* the marked runs' starts (each run holds >= 2 calls) */
     LAUNCH(k_run_check, grid_for(n, 256), 256, 0, st, T, key2, rstart, n, claim,
-           sc.rank.as<uint32_t>(), sc.o_ms.as<uint32_t>(), flag + 1);
+           sc.rank.as<uint32_t>());
     /* at most n/2 marked runs (each holds two calls or more), n/33 longer than 32, ... */
     uint2 *lst_w = lst_t + n / 2 + 1, *lst_b = lst_w + n / (FIX_THREAD + 1) + 1;
-    LAUNCH(k_marked_lists, (unsigned)sm_count() * 8, 256, 0, st, sc.o_ms.as<uint32_t>(), flag + 1,
-           sc.rank.as<uint32_t>(), lst_t, lst_w, lst_b, flag, claim2);
+    LAUNCH(k_marked_lists, grid_for(nw, 256), 256, 0, st, claim, nw, sc.rank.as<uint32_t>(), lst_t,
+           lst_w, lst_b, flag, claim2);
     const unsigned grid = (unsigned)sm_count() * 8;
     LAUNCH(k_fix_small, grid, 256, 0, st, T, n, lst_t, flag);
     LAUNCH(k_fix_warp, grid, 256, 0, st, T, n, lst_w, flag);
