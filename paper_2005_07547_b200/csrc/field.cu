@@ -3620,40 +3620,51 @@ __global__ void k_run_check(const double *__restrict__ T, const uint64_t *__rest
  * again (claim2) for the radix path and counted (flag bit 2, cnt[3]) */
 __global__ void __launch_bounds__(256) k_marked_lists(const uint32_t *__restrict__ claim, uint64_t nw,
                                                       const uint32_t *__restrict__ runlen,
-                                                      uint2 *lst_t, uint2 *lst_w, uint2 *lst_b,
+                                                      uint2 *lst8, uint2 *lst16, uint2 *lst_t,
+                                                      uint2 *lst_w, uint2 *lst_b,
                                                       unsigned int *cnt, uint32_t *claim2) {
-    __shared__ unsigned bc[3], bb[3];
-    if (threadIdx.x < 3) bc[threadIdx.x] = 0;
+    __shared__ unsigned bc[5], bb[5];
+    if (threadIdx.x < 5) bc[threadIdx.x] = 0;
     __syncthreads();
     const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint32_t bits = w < nw ? claim[w] : 0u;
-    unsigned mine[3] = {0u, 0u, 0u};
+    /* classes: <= 8, <= 16, <= 32 calls (the grouped rank sorts), <= FIX_WARP, <= FIX_BLOCK */
+    const auto cls = [](uint32_t len) {
+        return len <= 8 ? 0 : len <= 16 ? 1 : len <= FIX_THREAD ? 2 : len <= FIX_WARP ? 3
+                                                                   : len <= FIX_BLOCK ? 4 : 5;
+    };
+    unsigned mine[5] = {0u, 0u, 0u, 0u, 0u};
     for (uint32_t m = bits; m; m &= m - 1) { /* count this word's runs per class */
         const uint32_t j = (uint32_t)(w * 32 + (uint64_t)(__ffs(m) - 1)), len = runlen[j];
-        if (len <= FIX_THREAD) ++mine[0];
-        else if (len <= FIX_WARP) ++mine[1];
-        else if (len <= FIX_BLOCK) ++mine[2];
-        else {
+        const int c = cls(len);
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (q == c) ++mine[q];
+        if (c == 5) {
             atomicOr(&claim2[j >> 5], 1u << (j & 31u));
             atomicOr(&cnt[0], 2u);
             atomicAdd(&cnt[3], len);
         }
     }
-    unsigned off[3];
+    unsigned off[5];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) off[c] = mine[c] ? atomicAdd(&bc[c], mine[c]) : 0u;
+    for (int c = 0; c < 5; ++c) off[c] = mine[c] ? atomicAdd(&bc[c], mine[c]) : 0u;
     __syncthreads();
-    if (threadIdx.x < 3 && bc[threadIdx.x]) {
-        unsigned *g = threadIdx.x == 0 ? &cnt[4] : threadIdx.x == 1 ? &cnt[7] : &cnt[5];
-        bb[threadIdx.x] = atomicAdd(g, bc[threadIdx.x]);
+    if (threadIdx.x < 5 && bc[threadIdx.x]) {
+        const int cidx[5] = {1, 2, 4, 7, 5};
+        bb[threadIdx.x] = atomicAdd(&cnt[cidx[threadIdx.x]], bc[threadIdx.x]);
     }
     __syncthreads();
+    uint2 *const lists[5] = {lst8, lst16, lst_t, lst_w, lst_b};
     for (uint32_t m = bits; m; m &= m - 1) {
         const uint32_t j = (uint32_t)(w * 32 + (uint64_t)(__ffs(m) - 1)), len = runlen[j];
-        const uint2 item = make_uint2(j, len);
-        if (len <= FIX_THREAD) lst_t[bb[0] + off[0]++] = item;
-        else if (len <= FIX_WARP) lst_w[bb[1] + off[1]++] = item;
-        else if (len <= FIX_BLOCK) lst_b[bb[2] + off[2]++] = item;
+        const int c = cls(len);
+        if (c == 5) continue;
+        unsigned o = 0;
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (q == c) o = off[q]++;
+        lists[c][bb[c] + o] = make_uint2(j, len);
     }
 }
 
@@ -3708,25 +3719,31 @@ __global__ void __launch_bounds__(256) k_fix_warp(double *T, uint64_t n, const u
     }
 }
 
-/* one warp per marked run of up to 32 calls: each lane holds one call and counts the calls
- * before it (rank sort through shuffles), then stores it at its rank */
+/* marked runs of up to W calls (W = 8, 16, 32), 32 / W of them per warp: each lane of a W-lane
+ * group holds one call of its run and counts the calls before it (rank sort through shuffles
+ * within the group), then stores it at its rank */
+template <int W>
 __global__ void __launch_bounds__(256) k_fix_small(double *T, uint64_t n, const uint2 *lst,
-                                                   const unsigned int *cnt) {
-    const unsigned lane = lane_id();
-    const uint32_t nl = cnt[4];
-    for (uint64_t e = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; e < nl;
-         e += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t j0 = lst[e].x, len = lst[e].y;
-        const bool in = lane < len;
-        const uint64_t r = in ? dbits(T[j0 + lane]) : ~0ull;
-        const uint64_t g = in ? dbits(T[n + j0 + lane]) : ~0ull;
-        const uint64_t b = in ? dbits(T[2 * n + j0 + lane]) : ~0ull;
+                                                   const unsigned int *count) {
+    const unsigned lane = lane_id(), sub = lane % W, grp = lane / W;
+    const uint32_t nl = *count;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * (32 / W);
+         base < nl; base += nwarps * (32 / W)) {
+        const uint64_t e = base + grp;
+        const uint32_t j0 = e < nl ? lst[e].x : 0u, len = e < nl ? lst[e].y : 0u;
+        const bool in = sub < len;
+        const uint64_t r = in ? dbits(T[j0 + sub]) : ~0ull;
+        const uint64_t g = in ? dbits(T[n + j0 + sub]) : ~0ull;
+        const uint64_t b = in ? dbits(T[2 * n + j0 + sub]) : ~0ull;
         uint32_t rank = 0;
-        for (uint32_t i = 0; i < len; ++i) {
-            const uint64_t ri = __shfl_sync(0xffffffffu, r, i);
-            const uint64_t gi = __shfl_sync(0xffffffffu, g, i);
-            const uint64_t bi = __shfl_sync(0xffffffffu, b, i);
-            const bool lt = ri != r ? ri < r : gi != g ? gi < g : bi != b ? bi < b : i < lane;
+#pragma unroll 4
+        for (uint32_t i = 0; i < (uint32_t)W; ++i) {
+            const uint64_t ri = __shfl_sync(0xffffffffu, r, i, W);
+            const uint64_t gi = __shfl_sync(0xffffffffu, g, i, W);
+            const uint64_t bi = __shfl_sync(0xffffffffu, b, i, W);
+            const bool lt = i < len && (ri != r ? ri < r : gi != g ? gi < g : bi != b ? bi < b
+                                                                             : i < sub);
             rank += lt;
         }
         if (in) {
@@ -3934,12 +3951,12 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     ENSURE(sc.o_key2, nr * 8);
     ENSURE(sc.o_idx, nr * 4);
     ENSURE(sc.o_idx2, nr * 4);
-    ENSURE(sc.o_flag, 32); /* [0] flags, [3] calls in over-long runs, [4] [5] [7] list sizes */
+    ENSURE(sc.o_flag, 32); /* [0] flags, [3] calls in over-long runs, [1] [2] [4] [7] [5] lists */
     ENSURE(sc.head, n * 4);
     ENSURE(sc.uid, n * 4);
     ENSURE(sc.rank, n * 4);       /* run lengths (at run starts) */
     ENSURE(sc.o_tgt, nw * 8);     /* run-mark bitmaps: marked, over-long */
-    ENSURE(sc.o_fp, (n / 2 + n / (FIX_THREAD + 1) + n / (FIX_WARP + 1) + 3) * 8); /* run lists */
+    ENSURE(sc.o_fp, (n / 2 + n / 9 + n / 17 + n / (FIX_THREAD + 1) + n / (FIX_WARP + 1) + 5) * 8);
     ENSURE(sc.fterms, n * 24);    /* the terms r | g | b in the sorted order */
     ENSURE(sc.fstart, (n + 1) * 4);
     ENSURE(sc.fnruns, 8);
@@ -3983,12 +4000,15 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     LAUNCH(k_slot_terms, grid_for(n, 256), 256, 0, st, val, idx, n, T);
     LAUNCH(k_run_check, grid_for(n, 256), 256, 0, st, T, key2, rstart, n, claim,
            sc.rank.as<uint32_t>());
-    /* at most n/2 marked runs (each holds two calls or more), n/33 longer than 32, ... */
-    uint2 *lst_w = lst_t + n / 2 + 1, *lst_b = lst_w + n / (FIX_THREAD + 1) + 1;
-    LAUNCH(k_marked_lists, grid_for(nw, 256), 256, 0, st, claim, nw, sc.rank.as<uint32_t>(), lst_t,
-           lst_w, lst_b, flag, claim2);
+    /* at most n/2 marked runs (each holds two calls or more), n/9 longer than 8, ... */
+    uint2 *lst8 = lst_t, *lst16 = lst8 + n / 2 + 1, *lst32 = lst16 + n / 9 + 1,
+          *lst_w = lst32 + n / 17 + 1, *lst_b = lst_w + n / (FIX_THREAD + 1) + 1;
+    LAUNCH(k_marked_lists, grid_for(nw, 256), 256, 0, st, claim, nw, sc.rank.as<uint32_t>(), lst8,
+           lst16, lst32, lst_w, lst_b, flag, claim2);
     const unsigned grid = (unsigned)sm_count() * 8;
-    LAUNCH(k_fix_small, grid, 256, 0, st, T, n, lst_t, flag);
+    LAUNCH(k_fix_small<8>, grid, 256, 0, st, T, n, lst8, flag + 1);
+    LAUNCH(k_fix_small<16>, grid, 256, 0, st, T, n, lst16, flag + 2);
+    LAUNCH(k_fix_small<32>, grid, 256, 0, st, T, n, lst32, flag + 4);
     LAUNCH(k_fix_warp, grid, 256, 0, st, T, n, lst_w, flag);
     const size_t fsm = 3 * FIX_BLOCK * 8;
     SMEM_ATTR(k_fix_block, fsm);
@@ -4001,7 +4021,7 @@ static int fold_slot_records(Scratch &sc, pstf_field *const *fs, int nf, uint64_
     if (getenv("PSTF_ORDERED_DEBUG"))
         fprintf(stderr, "[ordered] %llu value calls of existing slots, flag %u, marked runs %u "
                 "(thread) %u (warp) %u (block), %llu calls in longer marked runs\n",
-                (unsigned long long)n, fl, h[4], h[7], h[5], (unsigned long long)m);
+                (unsigned long long)n, fl, h[1] + h[2] + h[4], h[7], h[5], (unsigned long long)m);
     if (m) { /* the runs too long for a block: b, g, then (run start, r) (stable, LSD) */
         ENSURE(sc.fisc, n);
         LAUNCH(k_run_marked, grid_for(n, 256), 256, 0, st, rstart, claim2, n, sc.fisc.as<uint8_t>());
