@@ -5253,8 +5253,15 @@ static int vertex_phase1(pstf_field *lo, pstf_field *loe, pstf_field *fli, pstf_
             for (pstf_field *f : fs)
                 if (f) f->unit_frame = false; /* counters are not counted (k_ef_onepass) */
             const size_t smem1 = sizeof(TileStage) + 64;
-            SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), smem1);
             const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm_count() * VT_MINB);
+            const uint32_t used = PSTF_TECH_CONTINUATION | PSTF_TECH_NEE;
+            if (twin && !li && (loe_mask & used) == used && (fli_mask & used) == used) {
+                SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, true, false, true>), smem1);
+                LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, true, false, true>), grid, VT,
+                       smem1, st, b, tm);
+                return PSTF_OK;
+            }
+            SMEM_ATTR((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), smem1);
             LAUNCH((k_vertex_pass_tiled<1, VT_MINB, true, false, true>), grid, VT, smem1, st, b, tm);
             return PSTF_OK;
         }
