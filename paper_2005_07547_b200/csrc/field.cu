@@ -3879,14 +3879,14 @@ __global__ void k_seg_lists(const uint32_t *__restrict__ start, const uint32_t *
  * start first); the warp loads the next 8 x 32 terms of each component (coalesced, in flight
  * while the current ones are summed) and lanes 0, 1, 2 add the r, g, b components in order
  * from shared memory */
-#define SFL_G 8
+#define SFL_G 7 /* 7 x 32 terms per component in flight (the padded rows fit 48 KB) */
 __global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict__ T, uint64_t n,
                                                         const uint64_t *__restrict__ key,
                                                         const uint32_t *__restrict__ start,
                                                         const uint32_t *__restrict__ lh,
                                                         const uint32_t *__restrict__ lm,
                                                         unsigned int *cnt, int capl, Stores4 st) {
-    __shared__ double sv[8][3][SFL_G * 32];
+    __shared__ double sv[8][3][SFL_G * 32 + 1]; /* +1: the three lanes' rows in different banks */
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const uint32_t nh = cnt[0], nl = nh + cnt[1];
     for (;;) {
