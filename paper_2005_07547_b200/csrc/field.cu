@@ -3921,8 +3921,16 @@ __global__ void __launch_bounds__(256) k_slot_fold_long(const double *__restrict
             if (lane < 3) {
                 const double *v = sv[w][c];
                 if (cnt2 == SFL_G * 32) {
-#pragma unroll 32
-                    for (int k = 0; k < SFL_G * 32; ++k) acc += v[k];
+                    /* 32 terms into registers first, then the dependent adds: the shared loads
+                     * stay off the add chain */
+#pragma unroll 1
+                    for (int ch = 0; ch < SFL_G; ++ch) {
+                        double t[32];
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) t[k] = v[ch * 32 + k];
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) acc += t[k];
+                    }
                 } else {
                     for (uint32_t k = 0; k < cnt2; ++k) acc += v[k];
                 }
