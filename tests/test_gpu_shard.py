@@ -24,7 +24,8 @@ def _stores(cap, base, evict):
 
 
 @pytest.mark.parametrize("world,cap,mult,evict", [(2, 12, 8.0, 2), (4, 14, 1.0, 64),
-                                                  (2, 10, 30.0, 2), (3, 12, 4.0, 3)])
+                                                  (2, 10, 30.0, 2), (3, 12, 4.0, 3),
+                                                  (2, 12, 8.0, 0)])
 def test_sharded_emulation_equals_single_gpu(world, cap, mult, evict):
     W, H, B, frames = 96, 54, 4, 5
     base = inputs.BASE_CORNELL * mult

@@ -67,7 +67,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,cap,evict", [(2, 9, 2), (2, 12, 64), (4, 10, 2)])
+@pytest.mark.parametrize("world,cap,evict", [(2, 9, 2), (2, 12, 64), (4, 10, 2), (2, 9, 0)])
 def test_sharded_protocol_matches_single_rank_semantics(tmp_path, world, cap, evict):
     mp.spawn(_worker, args=(world, _free_port(), cap, evict, str(tmp_path)), nprocs=world,
              join=True)
