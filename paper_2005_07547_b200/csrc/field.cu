@@ -1069,16 +1069,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
                 m1 = TWINQ ? m0 : (live ? ld_meta(&sLoe.meta[h1s]) : z),
                 m2 = has2 ? ld_meta(&sFli.meta[h2]) : z, m3 = has3 ? ld_meta(&sFli.meta[h3]) : z,
                 m4 = has4 ? ld_meta(&sLi.meta[h4]) : z;
-#if PSTF_FLI_NEXT_WORD >= 3
-    /* the FLi store is the crowded one (10% of its cells off home at config 2): its two probes
-     * preload the three words after home too, so a warp rarely waits on a second round trip */
-    const uint2 m2b = has2 ? ld_meta(&sFli.meta[(h2 + 1) & sFli.mask]) : z,
-                m2c = has2 ? ld_meta(&sFli.meta[(h2 + 2) & sFli.mask]) : z,
-                m2d = has2 ? ld_meta(&sFli.meta[(h2 + 3) & sFli.mask]) : z,
-                m3b = has3 ? ld_meta(&sFli.meta[(h3 + 1) & sFli.mask]) : z,
-                m3c = has3 ? ld_meta(&sFli.meta[(h3 + 2) & sFli.mask]) : z,
-                m3d = has3 ? ld_meta(&sFli.meta[(h3 + 3) & sFli.mask]) : z;
-#elif PSTF_FLI_NEXT_WORD
+#if PSTF_FLI_NEXT_WORD
     /* the FLi store is the crowded one: its two probes also preload the word after home */
     const uint2 m2b = has2 ? ld_meta(&sFli.meta[(h2 + 1) & sFli.mask]) : z,
                 m3b = has3 ? ld_meta(&sFli.meta[(h3 + 1) & sFli.mask]) : z;
@@ -1161,10 +1152,7 @@ __device__ __forceinline__ void vertex_body(const VPArgs2 &a, const Src &S, bool
     } else {
         r1 = live ? resolve_probe(sLoe, h1s, kLo.checksum, m1, &k1) : -3;
     }
-#if PSTF_FLI_NEXT_WORD >= 3
-    const int r2 = has2 ? resolve_probe4(sFli, h2, kFc.checksum, m2, m2b, m2c, m2d, &k2) : -3;
-    const int r3 = has3 ? resolve_probe4(sFli, h3, kFn.checksum, m3, m3b, m3c, m3d, &k3) : -3;
-#elif PSTF_FLI_NEXT_WORD
+#if PSTF_FLI_NEXT_WORD
     const int r2 = has2 ? resolve_probe2(sFli, h2, kFc.checksum, m2, m2b, &k2) : -3;
     const int r3 = has3 ? resolve_probe2(sFli, h3, kFn.checksum, m3, m3b, &k3) : -3;
 #else

@@ -261,34 +261,6 @@ __device__ __forceinline__ int resolve_probe2(const DevStore &s, uint32_t home, 
     return -2;
 }
 
-/* same with the three words after home preloaded (m0 .. m3 = home .. home + 3) */
-__device__ __forceinline__ int resolve_probe4(const DevStore &s, uint32_t home, uint32_t cs,
-                                              uint2 m0, uint2 m1, uint2 m2, uint2 m3,
-                                              uint32_t *mark) {
-    const uint32_t w = s.window;
-    if (m0.x == cs) { *mark = m0.y; return (int)home; }
-    if (m0.x == 0) return -1;
-    if (w < 2) return -2;
-    if (m1.x == cs) { *mark = m1.y; return (int)((home + 1) & s.mask); }
-    if (m1.x == 0) return -1;
-    if (w < 3) return -2;
-    if (m2.x == cs) { *mark = m2.y; return (int)((home + 2) & s.mask); }
-    if (m2.x == 0) return -1;
-    if (w < 4) return -2;
-    if (m3.x == cs) { *mark = m3.y; return (int)((home + 3) & s.mask); }
-    if (m3.x == 0) return -1;
-    for (uint32_t i = 4; i < w; ++i) {
-        uint32_t idx = (home + i) & s.mask;
-        uint2 m = ld_meta(&s.meta[idx]);
-        if (m.x == cs) {
-            *mark = m.y;
-            return (int)idx;
-        }
-        if (m.x == 0) return -1;
-    }
-    return -2;
-}
-
 /* finish a findSlot (lookup) whose home word was already loaded: slot or -1 */
 __device__ __forceinline__ int resolve_find(const DevStore &s, uint32_t home, uint32_t cs,
                                             uint32_t c0) {
